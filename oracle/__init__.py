@@ -1,0 +1,261 @@
+"""TEST INFRASTRUCTURE ONLY — numpy/ctypes front end of the CPU oracle.
+
+Two libraries live here, both checkers, never the product:
+
+* ``libsap_oracle.so`` — the plain-C restatement of the reference algorithm
+  (``oracle/sap_oracle.c``; each function cites the reference file:line it
+  follows).
+* ``_ref/libsapref.so`` — the unmodified reference headers compiled in place
+  (``oracle/ref_shim.cpp``, ``oracle/Makefile``). Present in the build
+  container and shipped prebuilt to the GPU box; ``has_ref()`` says whether it
+  is loadable.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+reference legs may import this package.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_ORACLE = os.path.join(HERE, "libsap_oracle.so")
+_REF = os.path.join(HERE, "_ref", "libsapref.so")
+
+_dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_ip = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int, msg: str = ""):
+        super().__init__(f"oracle error {code}: {msg}")
+        self.code = code
+
+
+def build() -> None:
+    """Compile the C restatement (and the reference shim where the sources exist)."""
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+class _Stats(C.Structure):
+    _fields_ = [("iterations", C.c_double), ("converged", C.c_int), ("final_relative_residual", C.c_double),
+                ("failure", C.c_int), ("hist_len", C.c_int)]
+
+
+_lib = None
+_ref = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_ORACLE):
+            build()
+        L = C.CDLL(_ORACLE)
+        L.sapo_random_banded.argtypes = [C.c_int, C.c_int, C.c_double, C.c_uint32, _dp, C.c_void_p]
+        L.sapo_uniform_stream.argtypes = [C.c_uint32, C.c_int, _dp]
+        L.sapo_partition_layout.argtypes = [C.c_int, C.c_int, C.c_int, _ip, _ip]
+        L.sapo_max_feasible_partitions.argtypes = [C.c_int, C.c_int]
+        L.sapo_band_matvec.argtypes = [C.c_int, C.c_int, _dp, _dp, _dp]
+        L.sapo_csr_matvec.argtypes = [C.c_int, _ip, _ip, _dp, _dp, _dp]
+        L.sapo_band_lu_inplace.argtypes = [C.c_int, C.c_int, _dp, C.c_double, C.c_double]
+        L.sapo_band_ul_inplace.argtypes = [C.c_int, C.c_int, _dp, C.c_double, C.c_double]
+        L.sapo_band_lu_solve.argtypes = [C.c_int, C.c_int, _dp, _dp]
+        L.sapo_band_ul_solve.argtypes = [C.c_int, C.c_int, _dp, _dp]
+        L.sapo_factor_blocks.argtypes = [C.c_int, C.c_int, _dp, C.c_int, C.c_int, C.c_double, _dp, C.c_void_p,
+                                         _ip, C.c_void_p, C.c_void_p]
+        L.sapo_dense_lu_nopivot_boosted.argtypes = [C.c_int, _dp, C.c_double]
+        L.sapo_dense_lu_solve.argtypes = [C.c_int, _dp, _dp]
+        L.sapo_extract_coupling.argtypes = [C.c_int, C.c_int, _dp, C.c_int, _ip, _dp, _dp]
+        L.sapo_spike_tips.argtypes = [C.c_int, C.c_int, _ip, _ip, _dp, _dp, _dp, _dp, C.c_double, _dp, _dp, _dp,
+                                      _ip]
+        L.sapo_apply.argtypes = [C.c_int, C.c_int, _dp, C.c_int, C.c_int, C.c_double, _dp, _dp]
+        L.sapo_solve_banded.argtypes = [C.c_int, C.c_int, _dp, _dp, C.c_int, C.c_int, C.c_double, C.c_int,
+                                        C.c_double, C.c_double, C.c_int, _dp, C.POINTER(_Stats), _dp, C.c_int]
+        L.sapo_krylov_csr_identity.argtypes = [C.c_int, _ip, _ip, _dp, _dp, C.c_int, C.c_double, C.c_int, _dp,
+                                               C.POINTER(_Stats), _dp, C.c_int]
+        _lib = L
+    return _lib
+
+
+def has_ref() -> bool:
+    try:
+        ref()
+        return True
+    except OSError:
+        return False
+
+
+def ref():
+    global _ref
+    if _ref is None:
+        R = C.CDLL(_REF)
+        R.sapref_last_error.restype = C.c_char_p
+        R.sapref_random_banded.argtypes = [C.c_int, C.c_int, C.c_double, C.c_uint, _dp, C.c_void_p]
+        R.sapref_partition_layout.argtypes = [C.c_int, C.c_int, C.c_int, _ip, _ip]
+        R.sapref_band_matvec.argtypes = [C.c_int, C.c_int, _dp, _dp, _dp]
+        R.sapref_factor_blocks.argtypes = [C.c_int, C.c_int, _dp, C.c_int, C.c_int, C.c_double, _dp, C.c_void_p,
+                                           _ip, C.c_void_p, C.c_void_p]
+        R.sapref_spikes.argtypes = [C.c_int, C.c_int, _dp, C.c_int, C.c_double, _dp, _dp, _dp, _dp, _dp, _ip]
+        R.sapref_apply.argtypes = [C.c_int, C.c_int, _dp, C.c_int, C.c_int, C.c_double, _dp, _dp]
+        R.sapref_solve_banded.argtypes = [C.c_int, C.c_int, _dp, _dp, C.c_int, C.c_int, C.c_double, C.c_int,
+                                          C.c_double, C.c_double, C.c_int, C.c_int, _dp,
+                                          C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_double),
+                                          C.POINTER(C.c_int), _dp, C.c_int, C.POINTER(C.c_int), _dp]
+        R.sapref_krylov_csr_identity.argtypes = [C.c_int, _ip, _ip, _dp, _dp, C.c_int, C.c_double, C.c_int, _dp,
+                                                 C.POINTER(C.c_double), C.POINTER(C.c_int),
+                                                 C.POINTER(C.c_double), C.POINTER(C.c_int), _dp, C.c_int,
+                                                 C.POINTER(C.c_int)]
+        R.sapref_solve_sparse.argtypes = [C.c_int, _ip, _ip, _dp, _dp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                          C.c_double, C.c_int, C.c_double, C.c_uint, C.c_int, C.c_double, C.c_int,
+                                          C.c_int, _dp, _dp, C.POINTER(C.c_double), C.POINTER(C.c_int),
+                                          C.POINTER(C.c_double), C.POINTER(C.c_int)]
+        _ref = R
+    return _ref
+
+
+def _ref_check(rc: int) -> None:
+    if rc:
+        raise OracleError(rc, ref().sapref_last_error().decode())
+
+
+# ---------------------------------------------------------------------------
+# C restatement (the checker)
+
+def random_banded(n: int, k: int, d: float, seed: int, with_rhs: bool = True):
+    band = np.zeros(n * (2 * k + 1))
+    rhs = np.zeros(n) if with_rhs else None
+    lib().sapo_random_banded(n, k, d, seed, band, rhs.ctypes.data if with_rhs else None)
+    return (band, rhs) if with_rhs else band
+
+
+def uniform_stream(seed: int, count: int) -> np.ndarray:
+    out = np.zeros(count)
+    lib().sapo_uniform_stream(seed, count, out)
+    return out
+
+
+def partition_layout(n: int, p: int, k: int):
+    sizes = np.zeros(max(p, 1), np.int32)
+    offs = np.zeros(max(p, 1) + 1, np.int32)
+    if lib().sapo_partition_layout(n, p, k, sizes, offs):
+        raise OracleError(1, "make_partition_layout: infeasible")
+    return sizes, offs
+
+
+def band_matvec(n, k, band, x):
+    y = np.zeros(n)
+    lib().sapo_band_matvec(n, k, band, np.ascontiguousarray(x, np.float64), y)
+    return y
+
+
+def csr_matvec(n, rp, ci, v, x):
+    y = np.zeros(n)
+    lib().sapo_csr_matvec(n, rp, ci, v, np.ascontiguousarray(x, np.float64), y)
+    return y
+
+
+def factor_blocks(n, k, band, p, lu_and_ul, boost_eps=1e-10):
+    lu = np.zeros(n * (2 * k + 1))
+    ul = np.zeros(n * (2 * k + 1)) if lu_and_ul else None
+    boosts = np.zeros(p, np.int32)
+    bul = np.zeros(p, np.int32)
+    norms = np.zeros(p)
+    rc = lib().sapo_factor_blocks(n, k, band, p, int(lu_and_ul), boost_eps, lu,
+                                  ul.ctypes.data if lu_and_ul else None, boosts, bul.ctypes.data,
+                                  norms.ctypes.data)
+    if rc:
+        raise OracleError(rc, "factor_blocks")
+    return dict(lu=lu, ul=ul, boosts=boosts, boosts_ul=bul, norms=norms)
+
+
+def spikes(n, k, band, p, boost_eps=1e-10):
+    """extract_coupling + compute_spike_tips (+ rbar) on the oracle's own factors."""
+    f = factor_blocks(n, k, band, p, True, boost_eps)
+    sizes, offs = partition_layout(n, p, k)
+    ww = max(p - 1, 0) * k * k
+    B, Cb, vb, wt, rb = (np.zeros(max(ww, 1)) for _ in range(5))
+    rbo = np.zeros(max(p - 1, 1), np.int32)
+    lib().sapo_extract_coupling(n, k, band, p, offs, B, Cb)
+    rc = lib().sapo_spike_tips(k, p, sizes, offs, f["lu"], f["ul"], B, Cb, boost_eps, vb, wt, rb, rbo)
+    if rc:
+        raise OracleError(rc, "spike tips not finite")
+    cut = slice(0, ww)
+    return dict(B=B[cut], C=Cb[cut], vb=vb[cut], wt=wt[cut], rbar=rb[cut], rbar_boosts=rbo[:max(p - 1, 0)],
+                **f)
+
+
+def apply(n, k, band, p, kind, x, boost_eps=1e-10):
+    out = np.zeros(n)
+    rc = lib().sapo_apply(n, k, band, p, kind, boost_eps, np.ascontiguousarray(x, np.float64), out)
+    if rc:
+        raise OracleError(rc, "apply")
+    return out
+
+
+def solve_banded(n, k, band, rhs, p, kind, boost_eps=1e-10, ell=2, rel_tol=1e-10, abs_tol=0.0, max_iterations=500):
+    x = np.zeros(n)
+    st = _Stats()
+    cap = 4 * 2 * max(max_iterations, 1) + 8
+    hist = np.zeros(cap)
+    rc = lib().sapo_solve_banded(n, k, band, rhs, p, kind, boost_eps, ell, rel_tol, abs_tol, max_iterations, x,
+                                 C.byref(st), hist, cap)
+    if rc:
+        raise OracleError(rc, "solve_banded")
+    return x, dict(iterations=st.iterations, converged=bool(st.converged),
+                   final_relative_residual=st.final_relative_residual, failure=st.failure,
+                   residual_history=hist[:min(st.hist_len, cap)].copy())
+
+
+# ---------------------------------------------------------------------------
+# The compiled reference (oracle/_ref)
+
+def ref_random_banded(n, k, d, seed):
+    band = np.zeros(n * (2 * k + 1))
+    rhs = np.zeros(n)
+    _ref_check(ref().sapref_random_banded(n, k, d, seed, band, rhs.ctypes.data))
+    return band, rhs
+
+
+def ref_factor_blocks(n, k, band, p, lu_and_ul, boost_eps=1e-10):
+    lu = np.zeros(n * (2 * k + 1))
+    ul = np.zeros(n * (2 * k + 1))
+    boosts = np.zeros(p, np.int32)
+    bul = np.zeros(p, np.int32)
+    norms = np.zeros(p)
+    _ref_check(ref().sapref_factor_blocks(n, k, band, p, int(lu_and_ul), boost_eps, lu, ul.ctypes.data, boosts,
+                                          bul.ctypes.data, norms.ctypes.data))
+    return dict(lu=lu, ul=ul if lu_and_ul else None, boosts=boosts, boosts_ul=bul, norms=norms)
+
+
+def ref_spikes(n, k, band, p, boost_eps=1e-10):
+    ww = max(p - 1, 0) * k * k
+    B, Cb, vb, wt, rb = (np.zeros(max(ww, 1)) for _ in range(5))
+    rbo = np.zeros(max(p - 1, 1), np.int32)
+    _ref_check(ref().sapref_spikes(n, k, band, p, boost_eps, B, Cb, vb, wt, rb, rbo))
+    cut = slice(0, ww)
+    return dict(B=B[cut], C=Cb[cut], vb=vb[cut], wt=wt[cut], rbar=rb[cut], rbar_boosts=rbo[:max(p - 1, 0)])
+
+
+def ref_apply(n, k, band, p, kind, x, boost_eps=1e-10):
+    out = np.zeros(n)
+    _ref_check(ref().sapref_apply(n, k, band, p, kind, boost_eps, np.ascontiguousarray(x, np.float64), out))
+    return out
+
+
+def ref_solve_banded(n, k, band, rhs, p, kind, boost_eps=1e-10, ell=2, rel_tol=1e-10, abs_tol=0.0,
+                     max_iterations=500, mixed_precision=False):
+    x = np.zeros(n)
+    it, conv, res, fail, hl = C.c_double(), C.c_int(), C.c_double(), C.c_int(), C.c_int()
+    cap = 4 * 2 * max(max_iterations, 1) + 8
+    hist = np.zeros(cap)
+    tim = np.zeros(5)
+    _ref_check(ref().sapref_solve_banded(n, k, band, rhs, p, kind, boost_eps, ell, rel_tol, abs_tol,
+                                         max_iterations, int(mixed_precision), x, C.byref(it), C.byref(conv),
+                                         C.byref(res), C.byref(fail), hist, cap, C.byref(hl), tim))
+    return x, dict(iterations=it.value, converged=bool(conv.value), final_relative_residual=res.value,
+                   failure=fail.value, residual_history=hist[:min(hl.value, cap)].copy(),
+                   t_lu=tim[0], t_bc=tim[1], t_spk=tim[2], t_lurdcd=tim[3], t_kry=tim[4])

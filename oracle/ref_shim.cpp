@@ -1,0 +1,281 @@
+// TEST INFRASTRUCTURE ONLY — never linked into the product.
+//
+// C-ABI shim over the UNMODIFIED reference headers (compiled in place from
+// /root/reference/proj/include by oracle/Makefile; no reference source is
+// copied into this repository). The product library (libsap_gpu.so) never
+// loads this; tests/, __graft_entry__.smoke() and bench.py's reference /
+// cpu_baseline legs do, as the checker and as the CPU baseline.
+//
+// Every entry point wires the reference's own public functions exactly as
+// the reference does:
+//   * sapref_random_banded  : testsup::random_banded (proj/tests/test_support.hpp:133-150)
+//                             followed by random_rhs (proj/tests/acceptance.cpp:48-53)
+//   * sapref_factor_blocks  : sap::factor_blocks (proj/include/sap/block_factors.hpp:138-206)
+//   * sapref_spikes         : extract_coupling + compute_spike_tips
+//                             (proj/include/sap/spike.hpp:95-116, :178-254)
+//   * sapref_apply          : apply_preconditioner (proj/include/sap/spike.hpp:304-351)
+//   * sapref_solve_banded   : detail::build_precond_op + run_krylov with the banded
+//                             operator (proj/include/sap/pipeline.hpp:140-202,
+//                             proj/include/sap/krylov.hpp:434-442), the dense wiring of
+//                             proj/tests/acceptance.cpp:114-132.
+//   * sapref_solve_sparse   : sap::solve_sparse (proj/include/sap/pipeline.hpp:213-369).
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "sap/sap.hpp"
+#include "test_support.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* what) {
+    g_err = what;
+    return code;
+}
+
+// 1 = std::invalid_argument, 2 = PreconditionerError, 3 = StructuralSingularityError, 9 = other
+#define SAPREF_TRY try {
+#define SAPREF_CATCH                                                           \
+    }                                                                          \
+    catch (const std::invalid_argument& e) { return fail(1, e.what()); }       \
+    catch (const sap::PreconditionerError& e) { return fail(2, e.what()); }    \
+    catch (const sap::StructuralSingularityError& e) { return fail(3, e.what()); } \
+    catch (const std::exception& e) { return fail(9, e.what()); }              \
+    return 0;
+
+sap::BandedMatrix<double> wrap_band(int n, int k, const double* band) {
+    sap::BandedMatrix<double> a(n, k);
+    std::memcpy(a.storage().data(), band, sizeof(double) * static_cast<std::size_t>(n) * (2 * k + 1));
+    return a;
+}
+
+double seconds_since(std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sapref_last_error() { return g_err.c_str(); }
+
+int sapref_random_banded(int n, int k, double d, unsigned seed, double* band_out, double* rhs_out) {
+    SAPREF_TRY
+    std::mt19937 rng(seed);
+    const sap::BandedMatrix<double> a = testsup::random_banded(n, k, d, rng);
+    std::memcpy(band_out, a.storage().data(), sizeof(double) * a.storage().size());
+    if (rhs_out) {
+        std::uniform_real_distribution<double> u(-1.0, 1.0);
+        for (int i = 0; i < n; ++i) rhs_out[i] = u(rng);
+    }
+    SAPREF_CATCH
+}
+
+int sapref_partition_layout(int n, int p, int k, int* sizes, int* offsets) {
+    SAPREF_TRY
+    const sap::PartitionLayout l = sap::make_partition_layout(n, p, k);
+    for (int i = 0; i < p; ++i) sizes[i] = l.sizes[static_cast<std::size_t>(i)];
+    for (int i = 0; i <= p; ++i) offsets[i] = l.offsets[static_cast<std::size_t>(i)];
+    SAPREF_CATCH
+}
+
+int sapref_band_matvec(int n, int k, const double* band, const double* x, double* y) {
+    SAPREF_TRY
+    const auto a = wrap_band(n, k, band);
+    a.matvec(std::span<const double>(x, static_cast<std::size_t>(n)), std::span<double>(y, static_cast<std::size_t>(n)));
+    SAPREF_CATCH
+}
+
+// lu_out / ul_out: per-block bands concatenated in partition order
+// (block b occupies sizes[b]*(2k+1) doubles). ul_out may be null for lu_only.
+int sapref_factor_blocks(int n, int k, const double* band, int p, int lu_and_ul, double boost_eps,
+                         double* lu_out, double* ul_out, int* boosts, int* boosts_ul, double* norms) {
+    SAPREF_TRY
+    const auto a = wrap_band(n, k, band);
+    const auto layout = sap::make_partition_layout(n, p, k);
+    const auto f = sap::factor_blocks<double>(
+        a, layout, lu_and_ul ? sap::FactorMode::lu_and_ul : sap::FactorMode::lu_only, boost_eps);
+    std::size_t off = 0;
+    for (int b = 0; b < p; ++b) {
+        const auto& lu = f.lu[static_cast<std::size_t>(b)];
+        std::memcpy(lu_out + off, lu.data(), sizeof(double) * lu.size());
+        if (lu_and_ul && ul_out) std::memcpy(ul_out + off, f.ul[static_cast<std::size_t>(b)].data(), sizeof(double) * lu.size());
+        off += lu.size();
+        boosts[b] = f.boost_count[static_cast<std::size_t>(b)];
+        if (boosts_ul) boosts_ul[b] = f.boost_count_ul[static_cast<std::size_t>(b)];
+        if (norms) norms[b] = f.block_norm[static_cast<std::size_t>(b)];
+    }
+    SAPREF_CATCH
+}
+
+// Coupling corners and spike tips for every interface (uniform width w = k).
+// Each output holds (p-1) row-major w x w blocks back to back.
+int sapref_spikes(int n, int k, const double* band, int p, double boost_eps, double* b_out, double* c_out,
+                  double* vb_out, double* wt_out, double* rbar_out, int* rbar_boosts) {
+    SAPREF_TRY
+    const auto a = wrap_band(n, k, band);
+    const auto layout = sap::make_partition_layout(n, p, k);
+    const auto f = sap::factor_blocks<double>(a, layout, sap::FactorMode::lu_and_ul, boost_eps);
+    const auto cb = sap::extract_coupling<double>(a, layout);
+    const auto s = sap::compute_spike_tips<double>(f, cb);
+    std::size_t off = 0;
+    for (int t = 0; t < s.interfaces(); ++t) {
+        const std::size_t ww = s.v_bottom[static_cast<std::size_t>(t)].size();
+        std::memcpy(b_out + off, cb.b_blocks[static_cast<std::size_t>(t)].data(), sizeof(double) * ww);
+        std::memcpy(c_out + off, cb.c_blocks[static_cast<std::size_t>(t)].data(), sizeof(double) * ww);
+        std::memcpy(vb_out + off, s.v_bottom[static_cast<std::size_t>(t)].data(), sizeof(double) * ww);
+        std::memcpy(wt_out + off, s.w_top[static_cast<std::size_t>(t)].data(), sizeof(double) * ww);
+        std::memcpy(rbar_out + off, s.rbar[static_cast<std::size_t>(t)].data(), sizeof(double) * ww);
+        rbar_boosts[t] = s.rbar_boosts[static_cast<std::size_t>(t)];
+        off += ww;
+    }
+    SAPREF_CATCH
+}
+
+// kind: 0 coupled, 1 decoupled (sap::PrecondKind order).
+int sapref_apply(int n, int k, const double* band, int p, int kind, double boost_eps, const double* in,
+                 double* out) {
+    SAPREF_TRY
+    const auto a = wrap_band(n, k, band);
+    const auto layout = sap::make_partition_layout(n, p, k);
+    const bool coupled = kind == 0 && p > 1;
+    const auto f = sap::factor_blocks<double>(
+        a, layout, coupled ? sap::FactorMode::lu_and_ul : sap::FactorMode::lu_only, boost_eps);
+    sap::SpikeSet<double> s;
+    if (coupled) s = sap::compute_spike_tips<double>(f, sap::extract_coupling<double>(a, layout));
+    const auto r = sap::apply_preconditioner<double>(static_cast<sap::PrecondKind>(kind), f, s,
+                                                     std::span<const double>(in, static_cast<std::size_t>(n)));
+    std::memcpy(out, r.data(), sizeof(double) * r.size());
+    SAPREF_CATCH
+}
+
+// Dense-banded SaP solve through the reference's own setup (build_precond_op)
+// and solve (run_krylov) entry points, A = BandedMatrix::matvec.
+// timings[0..4] = t_lu, t_bc, t_spk, t_lurdcd, t_kry (seconds).
+int sapref_solve_banded(int n, int k, const double* band, const double* rhs, int p, int kind,
+                        double boost_eps, int ell, double rel_tol, double abs_tol, int max_iterations,
+                        int mixed_precision, double* x_out, double* iterations, int* converged,
+                        double* final_res, int* failure, double* history, int hist_cap, int* hist_len,
+                        double* timings) {
+    SAPREF_TRY
+    const auto a = wrap_band(n, k, band);
+    const auto layout = sap::make_partition_layout(n, p, k);
+    sap::PipelineConfig cfg;
+    cfg.p = p;
+    cfg.precond = static_cast<sap::PrecondKind>(kind);
+    cfg.boost_eps = boost_eps;
+    cfg.krylov.ell = ell;
+    cfg.krylov.rel_tol = rel_tol;
+    cfg.krylov.abs_tol = abs_tol;
+    cfg.krylov.max_iterations = max_iterations;
+    cfg.krylov.mixed_precision = mixed_precision != 0;
+    sap::PipelineReport rep;
+    sap::LinearOp op_m;
+    try {
+        op_m = mixed_precision ? sap::detail::build_precond_op<float>(a, layout, cfg, false, nullptr, rep)
+                               : sap::detail::build_precond_op<double>(a, layout, cfg, false, nullptr, rep);
+    } catch (...) {
+        if (timings) {
+            timings[0] = rep.t_lu; timings[1] = rep.t_bc; timings[2] = rep.t_spk; timings[3] = rep.t_lurdcd; timings[4] = 0;
+        }
+        throw;
+    }
+    sap::LinearOp op_a = [&a](std::span<const double> in, std::span<double> out) { a.matvec(in, out); };
+    std::vector<double> x(static_cast<std::size_t>(n), 0.0);
+    const auto t0 = std::chrono::steady_clock::now();
+    const sap::SolveStats st = sap::run_krylov(op_a, op_m, std::span<const double>(rhs, static_cast<std::size_t>(n)), x, cfg.krylov);
+    const double t_kry = seconds_since(t0);
+    std::memcpy(x_out, x.data(), sizeof(double) * x.size());
+    *iterations = st.iterations;
+    *converged = st.converged ? 1 : 0;
+    *final_res = st.final_relative_residual;
+    *failure = static_cast<int>(st.failure);
+    const int hl = static_cast<int>(st.residual_history.size());
+    *hist_len = hl;
+    for (int i = 0; i < hl && i < hist_cap; ++i) history[i] = st.residual_history[static_cast<std::size_t>(i)];
+    if (timings) {
+        timings[0] = rep.t_lu; timings[1] = rep.t_bc; timings[2] = rep.t_spk; timings[3] = rep.t_lurdcd; timings[4] = t_kry;
+    }
+    SAPREF_CATCH
+}
+
+// Krylov on an explicit CSR operator with the identity preconditioner
+// (proj/tests/test_krylov.cpp style): exercises solve_krylov alone.
+int sapref_krylov_csr_identity(int n, const int* row_ptr, const int* col_idx, const double* vals,
+                               const double* rhs, int ell, double rel_tol, int max_iterations,
+                               double* x_out, double* iterations, int* converged, double* final_res,
+                               int* failure, double* history, int hist_cap, int* hist_len) {
+    SAPREF_TRY
+    sap::SparseMatrix m;
+    m.n = n;
+    m.row_ptr.assign(row_ptr, row_ptr + n + 1);
+    m.col_idx.assign(col_idx, col_idx + row_ptr[n]);
+    m.values.assign(vals, vals + row_ptr[n]);
+    sap::LinearOp op_a = [&m](std::span<const double> in, std::span<double> out) { m.matvec(in, out); };
+    sap::LinearOp op_m = [](std::span<const double> in, std::span<double> out) {
+        std::copy(in.begin(), in.end(), out.begin());
+    };
+    sap::KrylovOptions ko;
+    ko.ell = ell;
+    ko.rel_tol = rel_tol;
+    ko.max_iterations = max_iterations;
+    std::vector<double> x(static_cast<std::size_t>(n), 0.0);
+    const auto st = sap::solve_krylov(op_a, op_m, std::span<const double>(rhs, static_cast<std::size_t>(n)), x, ko);
+    std::memcpy(x_out, x.data(), sizeof(double) * x.size());
+    *iterations = st.iterations;
+    *converged = st.converged ? 1 : 0;
+    *final_res = st.final_relative_residual;
+    *failure = static_cast<int>(st.failure);
+    const int hl = static_cast<int>(st.residual_history.size());
+    *hist_len = hl;
+    for (int i = 0; i < hl && i < hist_cap; ++i) history[i] = st.residual_history[static_cast<std::size_t>(i)];
+    SAPREF_CATCH
+}
+
+// End-to-end sparse pipeline (config 4). report[0..9] = t_db, t_cm, t_drop,
+// t_asmbl, t_bc, t_lu, t_spk, t_lurdcd, t_kry, k_after; stats as above.
+int sapref_solve_sparse(int n, const int* row_ptr, const int* col_idx, const double* vals, const double* rhs,
+                        int use_db, int db_scaling, int use_cm, int third_stage, int p, double drop_tol,
+                        int kind, double boost_eps, unsigned seed, int ell, double rel_tol, int max_iterations,
+                        int mixed_precision, double* x_out, double* report, double* iterations,
+                        int* converged, double* final_res, int* failure) {
+    SAPREF_TRY
+    sap::SparseMatrix m;
+    m.n = n;
+    m.row_ptr.assign(row_ptr, row_ptr + n + 1);
+    m.col_idx.assign(col_idx, col_idx + row_ptr[n]);
+    m.values.assign(vals, vals + row_ptr[n]);
+    sap::PipelineConfig cfg;
+    cfg.use_db = use_db != 0;
+    cfg.db_scaling = db_scaling != 0;
+    cfg.use_cm = use_cm != 0;
+    cfg.third_stage = third_stage != 0;
+    cfg.p = p;
+    cfg.drop_tol = drop_tol;
+    cfg.precond = static_cast<sap::PrecondKind>(kind);
+    cfg.boost_eps = boost_eps;
+    cfg.seed = seed;
+    cfg.krylov.ell = ell;
+    cfg.krylov.rel_tol = rel_tol;
+    cfg.krylov.max_iterations = max_iterations;
+    cfg.krylov.mixed_precision = mixed_precision != 0;
+    sap::PipelineReport rep;
+    const auto x = sap::solve_sparse(m, std::span<const double>(rhs, static_cast<std::size_t>(n)), cfg, rep);
+    std::memcpy(x_out, x.data(), sizeof(double) * x.size());
+    report[0] = rep.t_db; report[1] = rep.t_cm; report[2] = rep.t_drop; report[3] = rep.t_asmbl;
+    report[4] = rep.t_bc; report[5] = rep.t_lu; report[6] = rep.t_spk; report[7] = rep.t_lurdcd;
+    report[8] = rep.t_kry; report[9] = rep.k;
+    *iterations = rep.stats.iterations;
+    *converged = rep.stats.converged ? 1 : 0;
+    *final_res = rep.stats.final_relative_residual;
+    *failure = static_cast<int>(rep.stats.failure);
+    if (!rep.success && !rep.failure_stage.empty()) g_err = rep.failure_stage + ": " + rep.failure_message;
+    SAPREF_CATCH
+}
+
+}  // extern "C"

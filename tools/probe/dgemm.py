@@ -1,0 +1,11 @@
+import torch, time
+a = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
+b = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
+for _ in range(2): torch.matmul(a, b)
+torch.cuda.synchronize()
+e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+best = 1e9
+for _ in range(5):
+    e0.record(); torch.matmul(a, b); e1.record(); torch.cuda.synchronize()
+    best = min(best, e0.elapsed_time(e1))
+print("cuBLAS DGEMM 8192^3: %.2f TFLOP/s" % (2 * 8192**3 / best / 1e9))
