@@ -1,0 +1,186 @@
+/*
+ * sap_gpu.h — C ABI of the B200-native SaP (split-and-parallelize) banded
+ * solver hot path (arXiv 1509.07919). Implemented by libsap_gpu.so
+ * (paper_1509_07919_b200/csrc/). Plain C types only: no CUDA, no torch and no
+ * C++ types cross this boundary; every call returns a sap_status and never
+ * throws.
+ *
+ * The reference (/root/reference/proj, header-only C++20) has no FFI; its
+ * hot-path boundary is the in-process C++ interface below, and each entry
+ * point names the reference function it replaces:
+ *
+ *   setup  ≙ sap::detail::build_precond_op<T>      proj/include/sap/pipeline.hpp:140-202
+ *            (factor_blocks block_factors.hpp:138-206, extract_coupling spike.hpp:95-116,
+ *             compute_spike_tips spike.hpp:178-254, finish_reduced_blocks spike.hpp:143-170)
+ *   M op   ≙ the returned LinearOp / apply_preconditioner   spike.hpp:304-351, krylov.hpp:14
+ *   A op   ≙ BandedMatrix::matvec banded_matrix.hpp:72-80 / SparseMatrix::matvec sparse_matrix.hpp:24-31
+ *   solve  ≙ sap::run_krylov (BiCGStab(l) solve_krylov)   krylov.hpp:434-442, :110-350
+ *
+ * Error mapping (status -> the reference's exception / failure channel):
+ *   SAP_ERR_INVALID_ARGUMENT  std::invalid_argument   (partition.hpp:52-63, block_factors.hpp:142-143,
+ *                                                      spike.hpp:180-184, :311-318, krylov.hpp:115)
+ *   SAP_ERR_PRECONDITIONER    sap::PreconditionerError (errors.hpp:17-20; spike.hpp:162-164, :217-219, :246-248)
+ *   Krylov numerical failures are NOT errors: sap_solve returns SAP_OK with
+ *   sap_solve_stats.failure set, exactly like SolveStats.failure (krylov.hpp:18, :35-41).
+ *   SAP_ERR_CUDA / SAP_ERR_COMM / SAP_ERR_STATE have no reference analogue
+ *   (device, communicator, call-order errors).
+ *
+ * Storage conventions (identical to the reference):
+ *   band   : "tall and thin" column-major, n*(2k+1) doubles, entry (i, j) at
+ *            j*(2k+1) + (i-j+k); out-of-matrix slots are zero (banded_matrix.hpp:22-51).
+ *   blocks : coupling corners, spike tips and reduced blocks are dense
+ *            row-major w x w (spike.hpp:80-138).
+ * Pointers flagged *_on_device are CUDA device pointers on the handle's
+ * device; otherwise host pointers (pageable or pinned).
+ *
+ * Threading: a handle is single-threaded and owns one CUDA stream; separate
+ * handles may run concurrently.
+ */
+#ifndef SAP_GPU_H
+#define SAP_GPU_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum sap_status {
+    SAP_OK = 0,
+    SAP_ERR_INVALID_ARGUMENT = 1,
+    SAP_ERR_PRECONDITIONER = 2,
+    SAP_ERR_CUDA = 3,
+    SAP_ERR_COMM = 4,
+    SAP_ERR_STATE = 5
+} sap_status;
+
+/* sap::PrecondKind, proj/include/sap/spike.hpp:14 (same order). */
+typedef enum sap_precond_kind {
+    SAP_PRECOND_COUPLED = 0,   /* SaP-C: truncated SPIKE */
+    SAP_PRECOND_DECOUPLED = 1, /* SaP-D: block Jacobi */
+    SAP_PRECOND_DIAGONAL = 2,
+    SAP_PRECOND_NONE = 3
+} sap_precond_kind;
+
+/* sap::KrylovMethod, proj/include/sap/krylov.hpp:16. */
+typedef enum sap_krylov_method {
+    SAP_KRYLOV_BICGSTAB_L = 0,
+    SAP_KRYLOV_CG = 1,
+    SAP_KRYLOV_AUTOMATIC = 2
+} sap_krylov_method;
+
+/* sap::KrylovFailure, proj/include/sap/krylov.hpp:18. */
+typedef enum sap_krylov_failure {
+    SAP_FAILURE_NONE = 0,
+    SAP_FAILURE_MAX_ITERATIONS = 1,
+    SAP_FAILURE_BREAKDOWN = 2,
+    SAP_FAILURE_NON_FINITE = 3,
+    SAP_FAILURE_INDEFINITE_OPERATOR = 4
+} sap_krylov_failure;
+
+/* PipelineConfig (pipeline.hpp:21-32) fields that reach the hot path, plus
+ * KrylovOptions (krylov.hpp:20-28). Defaults from sap_options_default() equal
+ * the reference's member initialisers. */
+typedef struct sap_options {
+    int p;                   /* partition count (PipelineConfig::p), default 1 */
+    int precond;             /* sap_precond_kind, default SAP_PRECOND_COUPLED */
+    double boost_eps;        /* pivot boosting threshold factor, default 1e-10 */
+    int method;              /* sap_krylov_method, default SAP_KRYLOV_BICGSTAB_L */
+    int ell;                 /* BiCGStab(l) degree, default 2 */
+    double rel_tol;          /* default 1e-10 */
+    double abs_tol;          /* default 0 */
+    int max_iterations;      /* default 500 */
+    int mixed_precision;     /* FP32 preconditioner (build_precond_op<float>), default 0 */
+    int caller_asserts_spd;  /* lets AUTOMATIC pick CG, default 0 */
+    int device;              /* CUDA device ordinal, default 0 */
+} sap_options;
+
+/* PipelineReport T_* stage timings (pipeline.hpp:37-52), in seconds,
+ * measured with CUDA events on the handle's stream. */
+typedef struct sap_report {
+    double t_lu;      /* factor_blocks: block norms, band copies, LU (+UL) */
+    double t_bc;      /* extract_coupling */
+    double t_spk;     /* spike tips */
+    double t_lurdcd;  /* reduced blocks: R = I - W V and its LU */
+    double t_kry;     /* last sap_solve (Krylov), device-resident */
+    double t_dtransf; /* host->device upload of the band in the last setup */
+    int n, k, partitions;
+    int total_boosts;     /* LU boosts summed over blocks */
+    int total_boosts_ul;  /* UL boosts summed over blocks */
+    int total_rbar_boosts;
+    long long kernel_launches; /* sm_100a kernels launched by this process so far */
+    double t_factor_kernel;    /* device time of the block LU/UL factorization launch alone */
+    double factor_flops;       /* algorithmic flops of that launch (band_lu_inplace op count) */
+} sap_report;
+
+/* SolveStats (krylov.hpp:35-41). history: caller-owned buffer of
+ * history_capacity doubles (may be NULL); history_len is the full count. */
+typedef struct sap_solve_stats {
+    double iterations;
+    int converged;
+    double final_relative_residual;
+    int failure; /* sap_krylov_failure */
+    int history_len;
+    double* history;
+    int history_capacity;
+} sap_solve_stats;
+
+typedef struct sap_handle sap_handle;
+
+/* ---- options / layout (host logic; no device work) ---- */
+void sap_options_default(sap_options* opts);
+/* max_feasible_partitions, partition.hpp:34-37 */
+int sap_max_feasible_partitions(int n, int k);
+/* make_partition_layout, partition.hpp:42-69: sizes[p], offsets[p+1].
+ * SAP_ERR_INVALID_ARGUMENT with the reference's message on infeasible input. */
+sap_status sap_partition_layout(int n, int p, int k, int* sizes, int* offsets);
+/* Message of the last failed call on this thread (handle-independent). */
+const char* sap_last_error(void);
+const char* sap_status_string(sap_status s);
+/* libsap_gpu version / build string. */
+const char* sap_version(void);
+
+/* ---- synthetic input: testsup::random_banded (proj/tests/test_support.hpp:133-150)
+ * followed, if rhs != NULL, by random_rhs (proj/tests/acceptance.cpp:48-53). ---- */
+sap_status sap_random_banded(int n, int k, double d, unsigned seed, double* band, double* rhs);
+
+/* ---- handle ---- */
+sap_status sap_create(const sap_options* opts, sap_handle** out);
+void sap_destroy(sap_handle* h);
+/* Use an external CUDA stream (cudaStream_t passed as void*); NULL = the handle's own. */
+sap_status sap_set_stream(sap_handle* h, void* stream);
+sap_status sap_synchronize(sap_handle* h);
+
+/* ---- setup ≙ build_precond_op<double|float> over make_partition_layout(n, opts.p, k).
+ * Installs the band as the Krylov A operator too (the dense wiring of
+ * proj/tests/acceptance.cpp:114-132). band_on_device: 0 = host pointer, copied;
+ * 1 = device pointer, copied; 2 = device pointer BORROWED for the A operator
+ * (no copy; it must stay valid while the handle applies A, like the
+ * reference's LinearOp capturing the BandedMatrix by reference). */
+sap_status sap_setup_banded(sap_handle* h, int n, int k, const double* band, int band_on_device);
+
+/* ---- A operator override: CSR matrix (solve_sparse's apply_a, pipeline.hpp:336-338).
+ * row_ptr[n+1], col_idx[nnz], values[nnz]; copied. */
+sap_status sap_set_operator_csr(sap_handle* h, int n, int nnz, const int* row_ptr, const int* col_idx,
+                                const double* values, int on_device);
+
+/* ---- the two LinearOps (krylov.hpp:14): out = M^{-1} in, out = A in. length n. ---- */
+sap_status sap_apply_preconditioner(sap_handle* h, const double* in, double* out, int on_device);
+sap_status sap_apply_operator(sap_handle* h, const double* in, double* out, int on_device);
+
+/* ---- solve ≙ run_krylov(A, M, b, x, KrylovOptions): x0 = 0, true-residual
+ * convergence ||b - A x|| <= rel_tol ||b|| + abs_tol, quarter-iteration accounting. */
+sap_status sap_solve(sap_handle* h, const double* b, double* x, int on_device, sap_solve_stats* stats);
+
+sap_status sap_get_report(const sap_handle* h, sap_report* rep);
+
+/* ---- parity accessors (BlockFactors / SpikeSet contents) ----
+ * which = 0: LU, 1: UL (SaP-C only). out: sizes[part]*(2k+1) doubles in the
+ * reference's per-block band layout. boosts / block_norm may be NULL. */
+sap_status sap_get_factor(sap_handle* h, int part, int which, double* out, int* boosts, double* block_norm);
+/* Interface t in [0, p-1): w = k. Any output pointer may be NULL. */
+sap_status sap_get_spike(sap_handle* h, int iface, double* b_block, double* c_block, double* v_bottom,
+                         double* w_top, double* rbar, int* rbar_boosts);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SAP_GPU_H */

@@ -1,0 +1,636 @@
+// C ABI (include/sap_gpu.h) over the SaP B200 kernels.
+//
+// The handle plays the role of the reference's PrecondState<T> +
+// LinearOp closures (proj/include/sap/pipeline.hpp:130-202): setup builds the
+// factors, coupling corners, spike tips and reduced blocks in HBM once;
+// every later apply / solve reuses them (the reference rebuilds per solve;
+// persisting factors across right-hand sides is the paper's stated use,
+// PAPER.md:408).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "../../include/sap_gpu.h"
+#include "common.cuh"
+#include "kernels.h"
+#include "krylov.h"
+
+using namespace sapgpu;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void alloc(size_t count) {
+        if (count == n && p) return;
+        release();
+        if (count == 0) return;
+        SAP_CUDA(cudaMalloc(&p, sizeof(T) * count));
+        n = count;
+    }
+    T* get() const { return p; }
+};
+
+struct Layout {
+    int n = 0, p = 0, k = 0;
+    std::vector<int> sizes, offsets;
+};
+
+// make_partition_layout (proj/include/sap/partition.hpp:42-69), same messages.
+Layout make_layout(int n, int p, int k) {
+    if (n <= 0) throw InvalidArgument("make_partition_layout: empty matrix");
+    if (p <= 0) throw InvalidArgument("make_partition_layout: partition count must be positive");
+    if (k < 0) throw InvalidArgument("make_partition_layout: negative bandwidth");
+    const int base = n / p, rem = n % p;
+    const int required = k == 0 ? 1 : 2 * k;
+    if (base < required)
+        throw InvalidArgument("make_partition_layout: " + std::to_string(p) + " partitions leave blocks under " +
+                              std::to_string(required) + " rows for half-bandwidth " + std::to_string(k) +
+                              "; largest feasible p is " + std::to_string(sap_max_feasible_partitions(n, k)));
+    Layout L;
+    L.n = n;
+    L.p = p;
+    L.k = k;
+    L.sizes.resize(p);
+    L.offsets.resize(p + 1);
+    L.offsets[0] = 0;
+    for (int i = 0; i < p; ++i) {
+        L.sizes[i] = base + (i < rem ? 1 : 0);
+        L.offsets[i + 1] = L.offsets[i] + L.sizes[i];
+    }
+    return L;
+}
+
+}  // namespace
+
+struct sap_handle {
+    sap_options opt{};
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    cudaEvent_t ev[12] = {};
+    // problem
+    bool ready = false;
+    int n = 0, k = 0;
+    Layout layout;
+    int kind = SAP_PRECOND_COUPLED;
+    bool coupled = false;  // coupled && p > 1
+    DevBuf<int> d_offsets;
+    const double* band_ptr = nullptr;  // A operator band (owned copy or borrowed)
+    DevBuf<double> band, lu, ul, norms, bblk, cblk, vb, wt, rbar, rbar_norms, diag, scratch_g, scratch_in,
+        scratch_out, dscal;
+    DevBuf<int> boosts, rbar_boosts, nonfinite;
+    DevBuf<FactorJob> jobs, rjobs;
+    // CSR operator
+    bool csr = false;
+    int csr_n = 0;
+    DevBuf<int> rp, ci;
+    DevBuf<double> vals;
+    // Krylov
+    KrylovSolver krylov;
+    DevBuf<double> kb, kx;
+    sap_report rep{};
+};
+
+namespace {
+
+template <class F>
+sap_status guard(F&& f) {
+    try {
+        f();
+        return SAP_OK;
+    } catch (const InvalidArgument& e) {
+        g_last_error = e.what();
+        return SAP_ERR_INVALID_ARGUMENT;
+    } catch (const PreconditionerFailure& e) {
+        g_last_error = e.what();
+        return SAP_ERR_PRECONDITIONER;
+    } catch (const CudaFailure& e) {
+        g_last_error = e.what();
+        return SAP_ERR_CUDA;
+    } catch (const StateError& e) {
+        g_last_error = e.what();
+        return SAP_ERR_STATE;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return SAP_ERR_CUDA;
+    }
+}
+
+void require(bool c, const char* msg) {
+    if (!c) throw InvalidArgument(msg);
+}
+
+float ev_ms(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.f;
+    SAP_CUDA(cudaEventElapsedTime(&ms, a, b));
+    return ms;
+}
+
+// M^{-1}: the reference's apply_preconditioner (spike.hpp:304-351) over the
+// handle's device factors. in/out are device pointers; they may alias.
+void apply_m(sap_handle* h, const double* in, double* out) {
+    const cudaStream_t s = h->stream;
+    const int n = h->n;
+    const size_t bytes = sizeof(double) * (size_t)n;
+    switch (h->kind) {
+        case SAP_PRECOND_NONE:
+            if (out != in) SAP_CUDA(cudaMemcpyAsync(out, in, bytes, cudaMemcpyDeviceToDevice, s));
+            return;
+        case SAP_PRECOND_DIAGONAL:
+            launch_diag_apply(in, h->diag.get(), out, n, s);
+            return;
+        default:
+            break;
+    }
+    const int p = h->layout.p, k = h->k;
+    if (!h->coupled) {
+        if (out != in) SAP_CUDA(cudaMemcpyAsync(out, in, bytes, cudaMemcpyDeviceToDevice, s));
+        launch_block_solve<double>(h->lu.get(), h->d_offsets.get(), p, k, out, s);
+        return;
+    }
+    double* g = h->scratch_g.get();
+    SAP_CUDA(cudaMemcpyAsync(g, in, bytes, cudaMemcpyDeviceToDevice, s));
+    if (out != in) SAP_CUDA(cudaMemcpyAsync(out, in, bytes, cudaMemcpyDeviceToDevice, s));
+    launch_block_solve<double>(h->lu.get(), h->d_offsets.get(), p, k, g, s);
+    launch_interfaces<double>(g, h->d_offsets.get(), p, k, h->wt.get(), h->vb.get(), h->rbar.get(), h->bblk.get(),
+                              h->cblk.get(), out, s);
+    launch_block_solve<double>(h->lu.get(), h->d_offsets.get(), p, k, out, s);
+}
+
+void apply_a(sap_handle* h, const double* in, double* out) {
+    if (h->csr)
+        launch_csr_spmv(h->rp.get(), h->ci.get(), h->vals.get(), h->csr_n, in, out, nullptr, h->stream);
+    else
+        launch_band_spmv(h->band_ptr, h->n, h->k, in, out, nullptr, h->stream);
+}
+
+int op_n(const sap_handle* h) { return h->csr ? h->csr_n : h->n; }
+
+void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device) {
+    require(n >= 0 && k >= 0, "BandedMatrix: negative dimension");
+    require(band != nullptr || n == 0, "sap_setup_banded: null band");
+    if (h->opt.mixed_precision)
+        throw InvalidArgument("sap_setup_banded: mixed_precision is not supported by this build");
+    const cudaStream_t s = h->stream;
+    h->ready = false;
+    h->kind = h->opt.precond;
+    require(h->kind >= 0 && h->kind <= 3, "sap_setup_banded: unknown preconditioner kind");
+    const bool blocks = h->kind == SAP_PRECOND_COUPLED || h->kind == SAP_PRECOND_DECOUPLED;
+    Layout L;
+    if (blocks) L = make_layout(n, h->opt.p, k);
+    h->n = n;
+    h->k = k;
+    h->layout = L;
+    const int p = L.p;
+    h->coupled = h->kind == SAP_PRECOND_COUPLED && p > 1;
+    h->rep = sap_report{};
+    h->rep.n = n;
+    h->rep.k = k;
+    h->rep.partitions = p;
+
+    const size_t total = (size_t)n * (2 * (size_t)k + 1);
+    SAP_CUDA(cudaEventRecord(h->ev[0], s));
+    if (on_device == 2) {
+        h->band.release();
+        h->band_ptr = band;
+    } else {
+        h->band.alloc(total);
+        if (n > 0)
+            SAP_CUDA(cudaMemcpyAsync(h->band.get(), band, sizeof(double) * total,
+                                     on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+        h->band_ptr = h->band.get();
+    }
+    SAP_CUDA(cudaEventRecord(h->ev[1], s));
+    h->scratch_in.alloc(std::max(n, 1));
+    h->scratch_out.alloc(std::max(n, 1));
+    h->dscal.alloc(4);
+
+    if (h->kind == SAP_PRECOND_NONE || n == 0) {
+        SAP_CUDA(cudaStreamSynchronize(s));
+        h->rep.t_dtransf = ev_ms(h->ev[0], h->ev[1]) * 1e-3;
+        h->ready = true;
+        return;
+    }
+    if (h->kind == SAP_PRECOND_DIAGONAL) {
+        // scale = banded.inf_norm() (pipeline.hpp:153) = the 1-block norm over all rows
+        DevBuf<int> offs1;
+        offs1.alloc(2);
+        const int ho[2] = {0, n};
+        SAP_CUDA(cudaMemcpyAsync(offs1.get(), ho, sizeof(ho), cudaMemcpyHostToDevice, s));
+        h->diag.alloc(n);
+        launch_block_norms(h->band_ptr, n, k, offs1.get(), 1, h->dscal.get(), s);
+        launch_boosted_diag(h->band_ptr, n, k, h->dscal.get(), h->opt.boost_eps, h->diag.get(), s);
+        SAP_CUDA(cudaEventRecord(h->ev[2], s));
+        SAP_CUDA(cudaStreamSynchronize(s));
+        h->rep.t_dtransf = ev_ms(h->ev[0], h->ev[1]) * 1e-3;
+        h->rep.t_lu = ev_ms(h->ev[1], h->ev[2]) * 1e-3;
+        h->ready = true;
+        return;
+    }
+
+    // ---- factor_blocks: norms, block band copies, LU (+ UL) ----
+    h->d_offsets.alloc(p + 1);
+    SAP_CUDA(cudaMemcpyAsync(h->d_offsets.get(), L.offsets.data(), sizeof(int) * (p + 1), cudaMemcpyHostToDevice, s));
+    h->norms.alloc(p);
+    h->boosts.alloc(2 * (size_t)p);
+    SAP_CUDA(cudaMemsetAsync(h->boosts.get(), 0, sizeof(int) * 2 * p, s));
+    h->lu.alloc(total);
+    if (h->coupled)
+        h->ul.alloc(total);
+    else
+        h->ul.release();
+    const int njobs = h->coupled ? 2 * p : p;
+    std::vector<FactorJob> jobs(njobs);
+    for (int b = 0; b < p; ++b) {
+        const int off = L.offsets[b], m = L.sizes[b];
+        double* f = h->lu.get() + (size_t)off * (2 * k + 1);
+        jobs[b] = FactorJob{f + k, 1, 2LL * k, m, k, h->norms.get() + b, h->boosts.get() + b};
+        if (h->coupled) {
+            double* g = h->ul.get() + (size_t)off * (2 * k + 1);
+            jobs[p + b] = FactorJob{g + (size_t)(m - 1) * (2 * k + 1) + k, -1, -2LL * k, m, k, h->norms.get() + b,
+                                    h->boosts.get() + p + b};
+        }
+    }
+    h->jobs.alloc(njobs);
+    SAP_CUDA(cudaMemcpyAsync(h->jobs.get(), jobs.data(), sizeof(FactorJob) * njobs, cudaMemcpyHostToDevice, s));
+    launch_block_norms(h->band_ptr, n, k, h->d_offsets.get(), p, h->norms.get(), s);
+    launch_copy_blocks(h->band_ptr, n, k, p, h->lu.get(), h->coupled ? h->ul.get() : nullptr, s);
+    SAP_CUDA(cudaEventRecord(h->ev[8], s));
+    launch_band_lu(h->jobs.get(), njobs, k, h->opt.boost_eps, s);
+    SAP_CUDA(cudaEventRecord(h->ev[9], s));
+    SAP_CUDA(cudaEventRecord(h->ev[2], s));
+    for (int b = 0; b < p; ++b) {
+        // band_lu_inplace op count: sum over columns of d + 2 d^2, d = min(k, m-1-j)
+        const double m = L.sizes[b], kk = std::min<double>(k, m - 1 > 0 ? m - 1 : 0);
+        const double f = (m - kk) * (2 * kk * kk + kk) + (kk - 1) * kk * (4 * kk + 1) / 6.0;
+        h->rep.factor_flops += (h->coupled ? 2.0 : 1.0) * f;
+    }
+
+    int ni = 0;
+    if (h->coupled) {
+        ni = p - 1;
+        const size_t ww = (size_t)k * k * ni;
+        h->bblk.alloc(std::max<size_t>(ww, 1));
+        h->cblk.alloc(std::max<size_t>(ww, 1));
+        h->vb.alloc(std::max<size_t>(ww, 1));
+        h->wt.alloc(std::max<size_t>(ww, 1));
+        h->rbar.alloc(std::max<size_t>(ww, 1));
+        h->rbar_norms.alloc(ni);
+        h->rbar_boosts.alloc(ni);
+        h->nonfinite.alloc(3 * (size_t)ni);
+        h->scratch_g.alloc(n);
+        SAP_CUDA(cudaMemsetAsync(h->nonfinite.get(), 0, sizeof(int) * 3 * ni, s));
+        SAP_CUDA(cudaMemsetAsync(h->rbar_boosts.get(), 0, sizeof(int) * ni, s));
+        // ---- T_BC: extract_coupling ----
+        launch_extract_coupling(h->band_ptr, n, k, h->d_offsets.get(), p, h->bblk.get(), h->cblk.get(), s);
+        SAP_CUDA(cudaEventRecord(h->ev[3], s));
+        // ---- T_SPK: spike tips ----
+        launch_spike_tips(h->lu.get(), h->ul.get(), h->d_offsets.get(), p, k, h->bblk.get(), h->cblk.get(),
+                          h->vb.get(), h->wt.get(), h->nonfinite.get(), s);
+        SAP_CUDA(cudaEventRecord(h->ev[4], s));
+        // ---- T_LUrdcd: rbar = I - W V and its boosted no-pivot LU ----
+        launch_rbar(h->wt.get(), h->vb.get(), k, ni, h->rbar.get(), s);
+        launch_dense_norms(h->rbar.get(), k, ni, h->rbar_norms.get(), h->nonfinite.get() + 2 * ni, s);
+        std::vector<FactorJob> rj(ni);
+        for (int t = 0; t < ni; ++t)
+            rj[t] = FactorJob{h->rbar.get() + (size_t)t * k * k, (long long)k, 1, k, k - 1, h->rbar_norms.get() + t,
+                              h->rbar_boosts.get() + t};
+        h->rjobs.alloc(ni);
+        SAP_CUDA(cudaMemcpyAsync(h->rjobs.get(), rj.data(), sizeof(FactorJob) * ni, cudaMemcpyHostToDevice, s));
+        launch_band_lu(h->rjobs.get(), ni, k - 1, h->opt.boost_eps, s);
+        SAP_CUDA(cudaEventRecord(h->ev[5], s));
+    }
+    SAP_CUDA(cudaStreamSynchronize(s));
+    h->rep.t_dtransf = ev_ms(h->ev[0], h->ev[1]) * 1e-3;
+    h->rep.t_lu = ev_ms(h->ev[1], h->ev[2]) * 1e-3;
+    h->rep.t_factor_kernel = ev_ms(h->ev[8], h->ev[9]) * 1e-3;
+    std::vector<int> hb(2 * p);
+    SAP_CUDA(cudaMemcpy(hb.data(), h->boosts.get(), sizeof(int) * 2 * p, cudaMemcpyDeviceToHost));
+    for (int b = 0; b < p; ++b) {
+        h->rep.total_boosts += hb[b];
+        h->rep.total_boosts_ul += hb[p + b];
+    }
+    if (h->coupled) {
+        h->rep.t_bc = ev_ms(h->ev[2], h->ev[3]) * 1e-3;
+        h->rep.t_spk = ev_ms(h->ev[3], h->ev[4]) * 1e-3;
+        h->rep.t_lurdcd = ev_ms(h->ev[4], h->ev[5]) * 1e-3;
+        std::vector<int> nf(3 * ni), rb(ni);
+        SAP_CUDA(cudaMemcpy(nf.data(), h->nonfinite.get(), sizeof(int) * 3 * ni, cudaMemcpyDeviceToHost));
+        SAP_CUDA(cudaMemcpy(rb.data(), h->rbar_boosts.get(), sizeof(int) * ni, cudaMemcpyDeviceToHost));
+        for (int t = 0; t < ni; ++t) h->rep.total_rbar_boosts += rb[t];
+        // the reference throws at the first failure in interface order (spike.hpp:217-219, :246-248),
+        // then at the first non-finite reduced block (:162-164)
+        for (int t = 0; t < ni; ++t) {
+            if (nf[2 * t]) throw PreconditionerFailure("right spike tip at interface " + std::to_string(t) + " is not finite");
+            if (nf[2 * t + 1]) throw PreconditionerFailure("left spike tip at interface " + std::to_string(t) + " is not finite");
+        }
+        for (int t = 0; t < ni; ++t)
+            if (nf[2 * ni + t]) throw PreconditionerFailure("reduced interface block " + std::to_string(t) + " is not finite");
+    }
+    h->ready = true;
+}
+
+}  // namespace
+
+extern "C" {
+
+void sap_options_default(sap_options* o) {
+    if (!o) return;
+    o->p = 1;
+    o->precond = SAP_PRECOND_COUPLED;
+    o->boost_eps = 1e-10;
+    o->method = SAP_KRYLOV_BICGSTAB_L;
+    o->ell = 2;
+    o->rel_tol = 1e-10;
+    o->abs_tol = 0.0;
+    o->max_iterations = 500;
+    o->mixed_precision = 0;
+    o->caller_asserts_spd = 0;
+    o->device = 0;
+}
+
+int sap_max_feasible_partitions(int n, int k) {
+    if (n <= 0) return 0;
+    return k == 0 ? n : n / (2 * k);
+}
+
+sap_status sap_partition_layout(int n, int p, int k, int* sizes, int* offsets) {
+    return guard([&] {
+        const Layout L = make_layout(n, p, k);
+        if (sizes) std::copy(L.sizes.begin(), L.sizes.end(), sizes);
+        if (offsets) std::copy(L.offsets.begin(), L.offsets.end(), offsets);
+    });
+}
+
+const char* sap_last_error(void) { return g_last_error.c_str(); }
+
+const char* sap_status_string(sap_status s) {
+    switch (s) {
+        case SAP_OK: return "ok";
+        case SAP_ERR_INVALID_ARGUMENT: return "invalid argument";
+        case SAP_ERR_PRECONDITIONER: return "preconditioner error";
+        case SAP_ERR_CUDA: return "cuda error";
+        case SAP_ERR_COMM: return "communication error";
+        case SAP_ERR_STATE: return "invalid call order";
+    }
+    return "unknown";
+}
+
+const char* sap_version(void) { return "sap_gpu 0.1 (sm_100a)"; }
+
+sap_status sap_random_banded(int n, int k, double d, unsigned seed, double* band, double* rhs) {
+    return guard([&] {
+        require(n >= 0 && k >= 0, "BandedMatrix: negative dimension");
+        require(band != nullptr || n == 0, "sap_random_banded: null band");
+        // testsup::random_banded (proj/tests/test_support.hpp:133-150), same generator stream
+        std::mt19937 rng(seed);
+        std::uniform_real_distribution<double> u(-1.0, 1.0);
+        const size_t w = 2 * (size_t)k + 1;
+        std::memset(band, 0, sizeof(double) * (size_t)n * w);
+        for (int i = 0; i < n; ++i) {
+            double off = 0.0;
+            const int lo = i - k > 0 ? i - k : 0;
+            const int hi = i + k < n - 1 ? i + k : n - 1;
+            for (int j = lo; j <= hi; ++j) {
+                if (j == i) continue;
+                double v = u(rng);
+                if (v == 0.0) v = 0.5;
+                band[(size_t)j * w + (size_t)(i - j + k)] = v;
+                off += std::abs(v);
+            }
+            band[(size_t)i * w + (size_t)k] = off > 0.0 ? d * off : d;
+        }
+        if (rhs)
+            for (int i = 0; i < n; ++i) rhs[i] = u(rng);
+    });
+}
+
+sap_status sap_create(const sap_options* opts, sap_handle** out) {
+    return guard([&] {
+        require(out != nullptr, "sap_create: null output");
+        *out = nullptr;
+        auto* h = new sap_handle();
+        if (opts)
+            h->opt = *opts;
+        else
+            sap_options_default(&h->opt);
+        try {
+            SAP_CUDA(cudaSetDevice(h->opt.device));
+            SAP_CUDA(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
+            h->stream = h->own_stream;
+            for (auto& e : h->ev) SAP_CUDA(cudaEventCreate(&e));
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+void sap_destroy(sap_handle* h) {
+    if (!h) return;
+    cudaSetDevice(h->opt.device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    for (auto& e : h->ev)
+        if (e) cudaEventDestroy(e);
+    if (h->own_stream) cudaStreamDestroy(h->own_stream);
+    delete h;
+}
+
+sap_status sap_set_stream(sap_handle* h, void* stream) {
+    return guard([&] {
+        require(h != nullptr, "null handle");
+        h->stream = stream ? static_cast<cudaStream_t>(stream) : h->own_stream;
+    });
+}
+
+sap_status sap_synchronize(sap_handle* h) {
+    return guard([&] {
+        require(h != nullptr, "null handle");
+        SAP_CUDA(cudaStreamSynchronize(h->stream));
+    });
+}
+
+sap_status sap_setup_banded(sap_handle* h, int n, int k, const double* band, int band_on_device) {
+    return guard([&] {
+        require(h != nullptr, "null handle");
+        SAP_CUDA(cudaSetDevice(h->opt.device));
+        setup_banded(h, n, k, band, band_on_device);
+    });
+}
+
+sap_status sap_set_operator_csr(sap_handle* h, int n, int nnz, const int* row_ptr, const int* col_idx,
+                                const double* values, int on_device) {
+    return guard([&] {
+        require(h != nullptr, "null handle");
+        require(n >= 0 && nnz >= 0, "sap_set_operator_csr: negative size");
+        SAP_CUDA(cudaSetDevice(h->opt.device));
+        const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+        h->rp.alloc(n + 1);
+        h->ci.alloc(std::max(nnz, 1));
+        h->vals.alloc(std::max(nnz, 1));
+        SAP_CUDA(cudaMemcpyAsync(h->rp.get(), row_ptr, sizeof(int) * (n + 1), kind, h->stream));
+        if (nnz > 0) {
+            SAP_CUDA(cudaMemcpyAsync(h->ci.get(), col_idx, sizeof(int) * nnz, kind, h->stream));
+            SAP_CUDA(cudaMemcpyAsync(h->vals.get(), values, sizeof(double) * nnz, kind, h->stream));
+        }
+        SAP_CUDA(cudaStreamSynchronize(h->stream));
+        h->csr = true;
+        h->csr_n = n;
+    });
+}
+
+static void io_apply(sap_handle* h, const double* in, double* out, int on_device, bool precond) {
+    require(h != nullptr, "null handle");
+    SAP_CUDA(cudaSetDevice(h->opt.device));
+    if (precond && !h->ready) throw StateError("preconditioner applied before setup");
+    if (!precond && !h->csr && !h->ready) throw StateError("operator applied before setup");
+    const int n = precond ? h->n : op_n(h);
+    if (n == 0) return;
+    const size_t bytes = sizeof(double) * (size_t)n;
+    const double* din = in;
+    double* dout = out;
+    if (!on_device) {
+        h->scratch_in.alloc(n);
+        h->scratch_out.alloc(n);
+        SAP_CUDA(cudaMemcpyAsync(h->scratch_in.get(), in, bytes, cudaMemcpyHostToDevice, h->stream));
+        din = h->scratch_in.get();
+        dout = h->scratch_out.get();
+    }
+    if (precond)
+        apply_m(h, din, dout);
+    else
+        apply_a(h, din, dout);
+    if (!on_device) SAP_CUDA(cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDeviceToHost, h->stream));
+    SAP_CUDA(cudaStreamSynchronize(h->stream));
+}
+
+sap_status sap_apply_preconditioner(sap_handle* h, const double* in, double* out, int on_device) {
+    return guard([&] { io_apply(h, in, out, on_device, true); });
+}
+
+sap_status sap_apply_operator(sap_handle* h, const double* in, double* out, int on_device) {
+    return guard([&] { io_apply(h, in, out, on_device, false); });
+}
+
+sap_status sap_solve(sap_handle* h, const double* b, double* x, int on_device, sap_solve_stats* stats) {
+    return guard([&] {
+        require(h != nullptr, "null handle");
+        SAP_CUDA(cudaSetDevice(h->opt.device));
+        const bool m_ok = h->ready;
+        const bool a_ok = h->csr || h->ready;
+        if (!a_ok) throw StateError("sap_solve before setup");
+        const int n = op_n(h);
+        if (!m_ok && h->opt.precond != SAP_PRECOND_NONE) throw StateError("sap_solve before preconditioner setup");
+        if (m_ok && h->n != n) throw InvalidArgument("sap_solve: operator and preconditioner sizes differ");
+        const cudaStream_t s = h->stream;
+        const size_t bytes = sizeof(double) * (size_t)n;
+        const double* db = b;
+        double* dx = x;
+        if (!on_device) {
+            h->kb.alloc(std::max(n, 1));
+            h->kx.alloc(std::max(n, 1));
+            if (n) SAP_CUDA(cudaMemcpyAsync(h->kb.get(), b, bytes, cudaMemcpyHostToDevice, s));
+            db = h->kb.get();
+            dx = h->kx.get();
+        }
+        KrylovConfig kc;
+        kc.method = h->opt.method;
+        kc.ell = h->opt.ell;
+        kc.rel_tol = h->opt.rel_tol;
+        kc.abs_tol = h->opt.abs_tol;
+        kc.max_iterations = h->opt.max_iterations;
+        kc.caller_asserts_spd = h->opt.caller_asserts_spd != 0;
+        DeviceOp A = [h](const double* in, double* out) { apply_a(h, in, out); };
+        DeviceOp M = [h](const double* in, double* out) {
+            if (h->ready)
+                apply_m(h, in, out);
+            else
+                SAP_CUDA(cudaMemcpyAsync(out, in, sizeof(double) * (size_t)op_n(h), cudaMemcpyDeviceToDevice,
+                                         h->stream));
+        };
+        SAP_CUDA(cudaEventRecord(h->ev[6], s));
+        const KrylovResult r = h->krylov.run(A, M, db, dx, n, kc, s);
+        SAP_CUDA(cudaEventRecord(h->ev[7], s));
+        if (!on_device && n) SAP_CUDA(cudaMemcpyAsync(x, dx, bytes, cudaMemcpyDeviceToHost, s));
+        SAP_CUDA(cudaStreamSynchronize(s));
+        h->rep.t_kry = ev_ms(h->ev[6], h->ev[7]) * 1e-3;
+        if (stats) {
+            stats->iterations = r.iterations;
+            stats->converged = r.converged ? 1 : 0;
+            stats->final_relative_residual = r.final_relative_residual;
+            stats->failure = r.failure;
+            stats->history_len = (int)r.residual_history.size();
+            if (stats->history && stats->history_capacity > 0) {
+                const int c = std::min(stats->history_capacity, stats->history_len);
+                std::copy(r.residual_history.begin(), r.residual_history.begin() + c, stats->history);
+            }
+        }
+    });
+}
+
+sap_status sap_get_report(const sap_handle* h, sap_report* rep) {
+    return guard([&] {
+        require(h != nullptr && rep != nullptr, "null argument");
+        *rep = h->rep;
+        rep->kernel_launches = g_launch_count;
+    });
+}
+
+sap_status sap_get_factor(sap_handle* h, int part, int which, double* out, int* boosts, double* block_norm) {
+    return guard([&] {
+        require(h != nullptr, "null handle");
+        if (!h->ready) throw StateError("sap_get_factor before setup");
+        require(h->kind == SAP_PRECOND_COUPLED || h->kind == SAP_PRECOND_DECOUPLED,
+                "sap_get_factor: no block factors for this preconditioner kind");
+        require(part >= 0 && part < h->layout.p, "sap_get_factor: partition out of range");
+        require(which == 0 || which == 1, "sap_get_factor: which must be 0 (LU) or 1 (UL)");
+        if (which == 1 && !h->coupled) throw InvalidArgument("block_solve: UL factors not available");
+        SAP_CUDA(cudaSetDevice(h->opt.device));
+        const size_t w = 2 * (size_t)h->k + 1;
+        const double* src = (which == 0 ? h->lu.get() : h->ul.get()) + (size_t)h->layout.offsets[part] * w;
+        if (out)
+            SAP_CUDA(cudaMemcpy(out, src, sizeof(double) * (size_t)h->layout.sizes[part] * w, cudaMemcpyDeviceToHost));
+        if (boosts)
+            SAP_CUDA(cudaMemcpy(boosts, h->boosts.get() + (which == 0 ? 0 : h->layout.p) + part, sizeof(int),
+                                cudaMemcpyDeviceToHost));
+        if (block_norm) SAP_CUDA(cudaMemcpy(block_norm, h->norms.get() + part, sizeof(double), cudaMemcpyDeviceToHost));
+    });
+}
+
+sap_status sap_get_spike(sap_handle* h, int iface, double* b_block, double* c_block, double* v_bottom, double* w_top,
+                         double* rbar, int* rbar_boosts) {
+    return guard([&] {
+        require(h != nullptr, "null handle");
+        if (!h->ready) throw StateError("sap_get_spike before setup");
+        require(h->coupled, "sap_get_spike: no spikes (not a coupled preconditioner with p > 1)");
+        require(iface >= 0 && iface < h->layout.p - 1, "sap_get_spike: interface out of range");
+        SAP_CUDA(cudaSetDevice(h->opt.device));
+        const size_t ww = (size_t)h->k * h->k, off = ww * iface, bytes = sizeof(double) * ww;
+        if (b_block) SAP_CUDA(cudaMemcpy(b_block, h->bblk.get() + off, bytes, cudaMemcpyDeviceToHost));
+        if (c_block) SAP_CUDA(cudaMemcpy(c_block, h->cblk.get() + off, bytes, cudaMemcpyDeviceToHost));
+        if (v_bottom) SAP_CUDA(cudaMemcpy(v_bottom, h->vb.get() + off, bytes, cudaMemcpyDeviceToHost));
+        if (w_top) SAP_CUDA(cudaMemcpy(w_top, h->wt.get() + off, bytes, cudaMemcpyDeviceToHost));
+        if (rbar) SAP_CUDA(cudaMemcpy(rbar, h->rbar.get() + off, bytes, cudaMemcpyDeviceToHost));
+        if (rbar_boosts)
+            SAP_CUDA(cudaMemcpy(rbar_boosts, h->rbar_boosts.get() + iface, sizeof(int), cudaMemcpyDeviceToHost));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,72 @@
+// Shared definitions for the SaP B200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace sapgpu {
+
+// ---------------------------------------------------------------------------
+// Errors crossing from kernels/host helpers to the C ABI.
+
+struct InvalidArgument : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct PreconditionerFailure : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct CudaFailure : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct StateError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaFailure(std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define SAP_CUDA(call) ::sapgpu::cuda_check((call), #call)
+
+// Launch counter (read back through sap_report.kernel_launches).
+extern long long g_launch_count;
+inline void count_launch(int n = 1) { g_launch_count += n; }
+#define SAP_LAUNCHED() do { ::sapgpu::count_launch(); SAP_CUDA(cudaGetLastError()); } while (0)
+
+// ---------------------------------------------------------------------------
+// Strided matrix view: element (i, c) lives at base[i*rs + c*cs].
+//   band LU  : base = f + k,                     rs = 1,  cs = 2k
+//   band UL  : base = f + (m-1)(2k+1) + k,       rs = -1, cs = -2k   (flipped system J A J)
+//   dense row-major w x w : base = a,            rs = w,  cs = 1
+// With slot(i, j) = j*(2k+1) + (i-j+k) = j*2k + i + k the tall-thin band is a
+// column-major matrix of leading dimension 2k, which is what makes one
+// factorization kernel serve all three.
+struct FactorJob {
+    double* base;
+    long long rs;
+    long long cs;
+    int m;            // order of the block
+    int k;            // half-bandwidth (dense: w-1)
+    const double* scale;  // boost scale (block infinity norm), device pointer
+    int* boosts;      // device counter (written, not accumulated)
+};
+
+constexpr int kWarp = 32;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ void dmma_m8n8k4(double& d0, double& d1, double a, double b, double c0, double c1) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};\n"
+                 : "=d"(d0), "=d"(d1)
+                 : "d"(a), "d"(b), "d"(c0), "d"(c1));
+}
+
+inline int ceil_div(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
+
+}  // namespace sapgpu

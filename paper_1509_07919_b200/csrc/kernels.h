@@ -1,0 +1,62 @@
+// Host-side launchers of the SaP sm_100a kernels. All launch on `s` and are
+// asynchronous; none synchronizes.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace sapgpu {
+
+// ---- factorization (factor.cu) ----
+// Infinity norm of every diagonal block, restricted to in-block columns
+// (factor_blocks' boost scale, block_factors.hpp:187-195). p blocks, offsets on device.
+void launch_block_norms(const double* band, int n, int k, const int* d_offsets, int p, double* norms, cudaStream_t s);
+// LU (and UL) buffers = the band with every entry outside its diagonal block zeroed.
+void launch_copy_blocks(const double* band, int n, int k, int p, double* lu, double* ul, cudaStream_t s);
+// Blocked no-pivot LU with pivot boosting of every job (one CTA per job).
+void launch_band_lu(const FactorJob* d_jobs, int njobs, int max_k, double boost_eps, cudaStream_t s);
+// Row-sum infinity norms of ni dense row-major w x w blocks and a non-finite flag per block.
+void launch_dense_norms(const double* a, int w, int ni, double* norms, int* nonfinite, cudaStream_t s);
+
+// ---- spikes (spike.cu) ----
+void launch_extract_coupling(const double* band, int n, int k, const int* d_offsets, int p, double* bblk,
+                             double* cblk, cudaStream_t s);
+// v_bottom / w_top tips from the LU / UL corners; nonfinite[2t] (V) / [2t+1] (W).
+void launch_spike_tips(const double* lu, const double* ul, const int* d_offsets, int p, int k, const double* bblk,
+                       const double* cblk, double* vb, double* wt, int* nonfinite, cudaStream_t s);
+// rbar[t] = I - wt[t] * vb[t] (row-major w x w).
+void launch_rbar(const double* wt, const double* vb, int w, int ni, double* rbar, cudaStream_t s);
+
+// ---- preconditioner apply (apply.cu) ----
+// x <- D^{-1} x per partition with the LU factors (band_lu_solve, block_factors.hpp:74-90).
+template <class T>
+void launch_block_solve(const T* lu, const int* d_offsets, int p, int k, T* x, cudaStream_t s);
+// SaP-C interface step (apply_preconditioner, spike.hpp:323-347): from g (= D^{-1} b) form
+// x^t, x^b per interface and subtract the coupling terms from b2 (which holds b).
+template <class T>
+void launch_interfaces(const T* g, const int* d_offsets, int p, int k, const T* wt, const T* vb, const T* rbar,
+                       const T* bblk, const T* cblk, T* b2, cudaStream_t s);
+void launch_diag_apply(const double* in, const double* diag, double* out, int n, cudaStream_t s);
+void launch_boosted_diag(const double* band, int n, int k, const double* scale, double boost_eps, double* diag,
+                         cudaStream_t s);
+
+// ---- operators (spmv.cu) ----
+// y = A x on the band; if b != nullptr also y = b - A x.
+void launch_band_spmv(const double* band, int n, int k, const double* x, double* y, const double* b, cudaStream_t s);
+void launch_csr_spmv(const int* rp, const int* ci, const double* v, int n, const double* x, double* y,
+                     const double* b, cudaStream_t s);
+
+// ---- vector kernels (vec.cu) ----
+// Deterministic reductions: fixed partition of [0, n) into blocks, fixed tree.
+int reduce_blocks(int n);
+// *counter must be 0 on entry (the kernel leaves it 0).
+void launch_dot(const double* a, const double* b, int n, double* partials, unsigned* counter, double* out,
+                cudaStream_t s);
+void launch_nonfinite(const double* a, int n, int* flag, cudaStream_t s);
+void launch_cast_d2f(const double* in, float* out, int n, cudaStream_t s);
+void launch_cast_f2d(const float* in, double* out, int n, cudaStream_t s);
+template <class T>
+void launch_cast_band(const double* in, T* out, size_t count, cudaStream_t s);
+
+}  // namespace sapgpu

@@ -1,0 +1,65 @@
+// Device-resident BiCGStab(l) and CG (the reference's solve_krylov / solve_cg /
+// run_krylov, proj/include/sap/krylov.hpp:110-442). Vectors live in HBM; the
+// scalar recurrences run on the host exactly as the reference writes them,
+// fed by deterministic device reductions.
+#pragma once
+
+#include <functional>
+#include <vector>
+
+#include "common.cuh"
+
+namespace sapgpu {
+
+// Device LinearOp: out = Op(in), both device pointers of length n.
+using DeviceOp = std::function<void(const double* in, double* out)>;
+
+struct KrylovResult {
+    double iterations = 0.0;
+    std::vector<double> residual_history;
+    bool converged = false;
+    double final_relative_residual = 0.0;
+    int failure = 0;  // sap_krylov_failure
+};
+
+struct KrylovConfig {
+    int method = 0;  // 0 bicgstab_l, 1 cg, 2 automatic
+    int ell = 2;
+    double rel_tol = 1e-10;
+    double abs_tol = 0.0;
+    int max_iterations = 500;
+    bool caller_asserts_spd = false;
+};
+
+class KrylovSolver {
+public:
+    KrylovSolver() = default;
+    ~KrylovSolver();
+    KrylovSolver(const KrylovSolver&) = delete;
+    KrylovSolver& operator=(const KrylovSolver&) = delete;
+
+    // run_krylov: b, x device pointers; x is overwritten (x0 = 0).
+    KrylovResult run(const DeviceOp& A, const DeviceOp& M, const double* b, double* x, int n,
+                     const KrylovConfig& cfg, cudaStream_t s);
+
+private:
+    void ensure(int n, int ell);
+    double dot(const double* a, const double* b);
+    bool nonfinite(const double* v);
+    KrylovResult bicgstab(const DeviceOp& A, const DeviceOp& M, const double* b, double* x, const KrylovConfig& cfg);
+    KrylovResult cg(const DeviceOp& A, const DeviceOp& M, const double* b, double* x, const KrylovConfig& cfg);
+
+    int n_ = 0, ell_ = 0;
+    cudaStream_t s_ = nullptr;
+    double* buf_ = nullptr;       // all vectors
+    double* partials_ = nullptr;  // reduction partials
+    double* dscal_ = nullptr;     // device scalar outputs
+    unsigned* counter_ = nullptr;
+    int* dflag_ = nullptr;
+    double* hpinned_ = nullptr;   // pinned host scalar
+    int* hflag_ = nullptr;
+    std::vector<double*> r_, u_;
+    double *tmp_ = nullptr, *rtilde_ = nullptr, *scratch_ = nullptr, *xc_ = nullptr, *noise_ = nullptr;
+};
+
+}  // namespace sapgpu

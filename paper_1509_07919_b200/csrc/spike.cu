@@ -1,0 +1,192 @@
+// Truncated-SPIKE coupling: corners, spike tips and reduced-block products.
+//
+// Reference: extract_coupling proj/include/sap/spike.hpp:95-116,
+// compute_spike_tips :178-254, finish_reduced_blocks :143-170.
+//
+// Tips. V^b_t = U_BB^{-1} L_BB^{-1} B_t uses the trailing w x w corner of
+// LU_t; W^t_t = L_TT^{-1} U_TT^{-1} C_t the leading corner of UL_{t+1}. Each
+// CTA owns one tip and a chunk of right-hand-side columns held in smem and
+// runs the triangular solves right-looking: at step j every (row, column)
+// element below (above) j is updated in parallel. For the forward solves this
+// applies each element's updates in the reference's ascending-j order; the
+// backward solves apply them in descending j (within tolerance).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace sapgpu {
+
+__global__ void k_extract_coupling(const double* __restrict__ a, int n, int k, const int* __restrict__ offs,
+                                   double* __restrict__ bblk, double* __restrict__ cblk) {
+    const int t = blockIdx.y;
+    const int w = k;
+    const int e = offs[t + 1];
+    const long long ld = 2LL * k;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < w * w; idx += gridDim.x * blockDim.x) {
+        const int r = idx / w, j = idx - r * w;
+        // B_t[r][j] = A(e-w+r, e+j); C_t[r][j] = A(e+r, e-w+j)  (zero outside the band)
+        const int bi = e - w + r, bj = e + j, ci = e + r, cj = e - w + j;
+        const bool bin = bi >= 0 && bi < n && bj >= 0 && bj < n && bi - bj <= k && bj - bi <= k;
+        const bool cin = ci >= 0 && ci < n && cj >= 0 && cj < n && ci - cj <= k && cj - ci <= k;
+        bblk[(long long)t * w * w + idx] = bin ? a[(long long)bj * ld + bi + k] : 0.0;
+        cblk[(long long)t * w * w + idx] = cin ? a[(long long)cj * ld + ci + k] : 0.0;
+    }
+}
+
+void launch_extract_coupling(const double* band, int n, int k, const int* d_offsets, int p, double* bblk,
+                             double* cblk, cudaStream_t s) {
+    if (p < 2 || k == 0) return;
+    dim3 grid(ceil_div((long long)k * k, 256), p - 1);
+    k_extract_coupling<<<grid, 256, 0, s>>>(band, n, k, d_offsets, bblk, cblk);
+    SAP_LAUNCHED();
+}
+
+// ---------------------------------------------------------------------------
+constexpr int kTipCols = 32;
+constexpr int kTipThreads = 256;
+
+// grid: (column chunks, 2 tips, p-1 interfaces). X is w x kTipCols row-major in smem.
+__global__ void __launch_bounds__(kTipThreads)
+    k_spike_tips(const double* __restrict__ lu, const double* __restrict__ ul, const int* __restrict__ offs, int k,
+                 const double* __restrict__ bblk, const double* __restrict__ cblk, double* __restrict__ vb,
+                 double* __restrict__ wt, int* __restrict__ nonfinite) {
+    extern __shared__ double sm[];
+    const int w = k;
+    const int t = blockIdx.z, which = blockIdx.y, c0 = blockIdx.x * kTipCols;
+    const int nc = min(kTipCols, w - c0);
+    double* X = sm;                    // [w][kTipCols]
+    double* colv = sm + w * kTipCols;  // factor column j, [w]
+    const long long ld = 2LL * k;      // band: (i, j) at j*2k + i + k
+    const double* f;
+    int corner;  // first global row/col of the corner inside the block band
+    if (which == 0) {
+        const int off = offs[t], m = offs[t + 1] - off;
+        f = lu + (long long)off * (2 * k + 1);
+        corner = m - w;
+    } else {
+        f = ul + (long long)offs[t + 1] * (2 * k + 1);
+        corner = 0;
+    }
+    const double* rhs = (which == 0 ? bblk : cblk) + (long long)t * w * w;
+    for (int idx = threadIdx.x; idx < w * kTipCols; idx += blockDim.x) {
+        const int r = idx / kTipCols, c = idx - r * kTipCols;
+        X[idx] = c < nc ? rhs[(long long)r * w + c0 + c] : 0.0;
+    }
+    auto F = [&](int i, int j) -> double {  // corner entry (i, j); all |i-j| < w <= k are in band
+        return f[(long long)(corner + j) * ld + (corner + i) + k];
+    };
+    if (which == 0) {
+        // forward, unit lower L: X[i] -= L(i,j) X[j], j ascending
+        for (int j = 0; j < w - 1; ++j) {
+            __syncthreads();
+            for (int i = j + 1 + threadIdx.x; i < w; i += blockDim.x) colv[i] = F(i, j);
+            __syncthreads();
+            const int rows = w - 1 - j;
+            for (int idx = threadIdx.x; idx < rows * kTipCols; idx += blockDim.x) {
+                const int i = j + 1 + idx / kTipCols, c = idx % kTipCols;
+                X[i * kTipCols + c] = fma(-colv[i], X[j * kTipCols + c], X[i * kTipCols + c]);
+            }
+        }
+        // backward, upper U with diagonal
+        for (int j = w - 1; j >= 0; --j) {
+            __syncthreads();
+            for (int i = threadIdx.x; i <= j; i += blockDim.x) colv[i] = F(i, j);
+            __syncthreads();
+            if (threadIdx.x < kTipCols) X[j * kTipCols + threadIdx.x] = X[j * kTipCols + threadIdx.x] / colv[j];
+            __syncthreads();
+            for (int idx = threadIdx.x; idx < j * kTipCols; idx += blockDim.x) {
+                const int i = idx / kTipCols, c = idx % kTipCols;
+                X[i * kTipCols + c] = fma(-colv[i], X[j * kTipCols + c], X[i * kTipCols + c]);
+            }
+        }
+    } else {
+        // backward, unit upper U (UL's U): X[i] -= U(i,j) X[j] for i < j, j descending
+        for (int j = w - 1; j >= 1; --j) {
+            __syncthreads();
+            for (int i = threadIdx.x; i < j; i += blockDim.x) colv[i] = F(i, j);
+            __syncthreads();
+            for (int idx = threadIdx.x; idx < j * kTipCols; idx += blockDim.x) {
+                const int i = idx / kTipCols, c = idx % kTipCols;
+                X[i * kTipCols + c] = fma(-colv[i], X[j * kTipCols + c], X[i * kTipCols + c]);
+            }
+        }
+        // forward, lower L with diagonal, j ascending
+        for (int j = 0; j < w; ++j) {
+            __syncthreads();
+            for (int i = j + threadIdx.x; i < w; i += blockDim.x) colv[i] = F(i, j);
+            __syncthreads();
+            if (threadIdx.x < kTipCols) X[j * kTipCols + threadIdx.x] = X[j * kTipCols + threadIdx.x] / colv[j];
+            __syncthreads();
+            const int rows = w - 1 - j;
+            for (int idx = threadIdx.x; idx < rows * kTipCols; idx += blockDim.x) {
+                const int i = j + 1 + idx / kTipCols, c = idx % kTipCols;
+                X[i * kTipCols + c] = fma(-colv[i], X[j * kTipCols + c], X[i * kTipCols + c]);
+            }
+        }
+    }
+    __syncthreads();
+    double* out = (which == 0 ? vb : wt) + (long long)t * w * w;
+    int bad = 0;
+    for (int idx = threadIdx.x; idx < w * kTipCols; idx += blockDim.x) {
+        const int r = idx / kTipCols, c = idx - r * kTipCols;
+        if (c < nc) {
+            const double v = X[idx];
+            if (!isfinite(v)) bad = 1;
+            out[(long long)r * w + c0 + c] = v;
+        }
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite + 2 * t + which, 1);
+}
+
+void launch_spike_tips(const double* lu, const double* ul, const int* d_offsets, int p, int k, const double* bblk,
+                       const double* cblk, double* vb, double* wt, int* nonfinite, cudaStream_t s) {
+    if (p < 2 || k == 0) return;
+    const size_t bytes = sizeof(double) * ((size_t)k * kTipCols + k);
+    if (bytes > 227 * 1024) throw InvalidArgument("spike tips: half-bandwidth too large");
+    SAP_CUDA(cudaFuncSetAttribute(k_spike_tips, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    dim3 grid(ceil_div(k, kTipCols), 2, p - 1);
+    k_spike_tips<<<grid, kTipThreads, bytes, s>>>(lu, ul, d_offsets, k, bblk, cblk, vb, wt, nonfinite);
+    SAP_LAUNCHED();
+}
+
+// ---------------------------------------------------------------------------
+// rbar[t] = I - wt[t] vb[t]; each element accumulates l ascending (FMA) as
+// finish_reduced_blocks does (spike.hpp:154-160). 32x32 output tile per CTA.
+__global__ void k_rbar(const double* __restrict__ wt, const double* __restrict__ vb, int w,
+                       double* __restrict__ rbar) {
+    __shared__ double As[32][33];
+    __shared__ double Bs[32][33];
+    const int t = blockIdx.z;
+    const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads, 4 rows each
+    const double* A = wt + (long long)t * w * w;
+    const double* Bm = vb + (long long)t * w * w;
+    double acc[4] = {0, 0, 0, 0};
+    for (int l0 = 0; l0 < w; l0 += 32) {
+        for (int q = 0; q < 4; ++q) {
+            const int r = ty + 8 * q;
+            As[r][tx] = (i0 + r < w && l0 + tx < w) ? A[(long long)(i0 + r) * w + l0 + tx] : 0.0;
+            Bs[r][tx] = (l0 + r < w && j0 + tx < w) ? Bm[(long long)(l0 + r) * w + j0 + tx] : 0.0;
+        }
+        __syncthreads();
+        const int lmax = min(32, w - l0);
+        for (int l = 0; l < lmax; ++l) {
+            const double b = Bs[l][tx];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q] = fma(As[ty + 8 * q][l], b, acc[q]);
+        }
+        __syncthreads();
+    }
+    for (int q = 0; q < 4; ++q) {
+        const int i = i0 + ty + 8 * q, j = j0 + tx;
+        if (i < w && j < w) rbar[(long long)t * w * w + (long long)i * w + j] = (i == j ? 1.0 : 0.0) - acc[q];
+    }
+}
+
+void launch_rbar(const double* wt, const double* vb, int w, int ni, double* rbar, cudaStream_t s) {
+    if (ni <= 0 || w == 0) return;
+    dim3 grid(ceil_div(w, 32), ceil_div(w, 32), ni);
+    k_rbar<<<grid, 256, 0, s>>>(wt, vb, w, rbar);
+    SAP_LAUNCHED();
+}
+
+}  // namespace sapgpu

@@ -1,0 +1,61 @@
+// Krylov A operators: banded and CSR SpMV (optionally fused with b - A x).
+//
+// Reference: BandedMatrix::matvec proj/include/sap/banded_matrix.hpp:72-80 and
+// SparseMatrix::matvec proj/include/sap/sparse_matrix.hpp:24-31. Each row
+// accumulates its products in ascending column order from zero (FMA), as the
+// reference does.
+//
+// Banded: a warp owns 32 consecutive rows and walks the union of their
+// column windows; for each column the 32 lanes read 32 consecutive slots
+// (slot = j*2k + i + k), i.e. one fully used 256-byte run of the tall-thin
+// band, and x[j] is a warp-wide broadcast.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace sapgpu {
+
+__global__ void __launch_bounds__(256)
+    k_band_spmv(const double* __restrict__ a, int n, int k, const double* __restrict__ x, double* __restrict__ y,
+                const double* __restrict__ b) {
+    const int lane = threadIdx.x & 31;
+    const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const long long ld = 2LL * k;
+    for (int r0 = warp_global * 32; r0 < n; r0 += nwarps * 32) {
+        const int i = r0 + lane;
+        const int clo = max(r0 - k, 0), chi = min(r0 + 31 + k, n - 1);
+        double acc = 0.0;
+        const double* col = a + (long long)clo * ld + i + k;
+#pragma unroll 8
+        for (int j = clo; j <= chi; ++j, col += ld) {
+            const double xv = __ldg(x + j);
+            if (i < n && i - j <= k && j - i <= k) acc = fma(*col, xv, acc);
+        }
+        if (i < n) y[i] = b ? b[i] - acc : acc;
+    }
+}
+
+void launch_band_spmv(const double* band, int n, int k, const double* x, double* y, const double* b, cudaStream_t s) {
+    const int warps = ceil_div(n, 32);
+    const int grid = std::min(ceil_div(warps, 8), 148 * 64);
+    k_band_spmv<<<grid, 256, 0, s>>>(band, n, k, x, y, b);
+    SAP_LAUNCHED();
+}
+
+__global__ void k_csr_spmv(const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ v,
+                           int n, const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ b) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        const int e = rp[i + 1];
+        for (int s = rp[i]; s < e; ++s) acc = fma(v[s], __ldg(x + ci[s]), acc);
+        y[i] = b ? b[i] - acc : acc;
+    }
+}
+
+void launch_csr_spmv(const int* rp, const int* ci, const double* v, int n, const double* x, double* y,
+                     const double* b, cudaStream_t s) {
+    k_csr_spmv<<<std::min(ceil_div(n, 256), 148 * 32), 256, 0, s>>>(rp, ci, v, n, x, y, b);
+    SAP_LAUNCHED();
+}
+
+}  // namespace sapgpu

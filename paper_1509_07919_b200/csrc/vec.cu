@@ -1,0 +1,104 @@
+// Deterministic reductions and small vector kernels.
+//
+// Dot products (krylov.hpp:45-49 sums sequentially) are formed over a fixed
+// partition of [0, n) into kRedChunk-element chunks, each reduced by a fixed
+// tree; the chunk partials are summed in index order by the last CTA to
+// finish. The result therefore depends only on n and the data - never on
+// scheduling - which keeps solves bitwise repeatable (acceptance criterion
+// 10, proj/tests/acceptance.cpp:592-606).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace sapgpu {
+
+constexpr int kRedThreads = 256;
+constexpr int kRedChunk = 4096;
+
+int reduce_blocks(int n) { return std::max(1, ceil_div(n, kRedChunk)); }
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    v = warp_sum(v);
+    if (lane == 0) sh[warp] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+    return t;  // valid on thread 0
+}
+
+__global__ void __launch_bounds__(kRedThreads)
+    k_dot(const double* __restrict__ a, const double* __restrict__ b, int n, double* __restrict__ partials,
+          unsigned* __restrict__ counter, double* __restrict__ out) {
+    __shared__ double sh[32];
+    __shared__ bool last;
+    const int base = blockIdx.x * kRedChunk;
+    const int end = min(base + kRedChunk, n);
+    double s = 0.0;
+    for (int i = base + threadIdx.x; i < end; i += kRedThreads) s = fma(a[i], b[i], s);
+    const double t = block_sum(s, sh);
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = t;
+        __threadfence();
+        const unsigned prev = atomicAdd(counter, 1u);
+        last = (prev == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        if (threadIdx.x == 0) {
+            double tot = 0.0;
+            for (int q = 0; q < (int)gridDim.x; ++q) tot += __ldcg(partials + q);
+            *out = tot;
+            *counter = 0u;
+        }
+    }
+}
+
+void launch_dot(const double* a, const double* b, int n, double* partials, unsigned* counter, double* out,
+                cudaStream_t s) {
+    k_dot<<<reduce_blocks(n), kRedThreads, 0, s>>>(a, b, n, partials, counter, out);
+    SAP_LAUNCHED();
+}
+
+__global__ void k_nonfinite(const double* __restrict__ a, int n, int* flag) {
+    int bad = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        if (!isfinite(a[i])) bad = 1;
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+void launch_nonfinite(const double* a, int n, int* flag, cudaStream_t s) {
+    k_nonfinite<<<std::min(ceil_div(n, 256), 148 * 8), 256, 0, s>>>(a, n, flag);
+    SAP_LAUNCHED();
+}
+
+__global__ void k_cast_d2f(const double* __restrict__ in, float* __restrict__ out, int n) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = (float)in[i];
+}
+__global__ void k_cast_f2d(const float* __restrict__ in, double* __restrict__ out, int n) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = (double)in[i];
+}
+void launch_cast_d2f(const double* in, float* out, int n, cudaStream_t s) {
+    k_cast_d2f<<<std::min(ceil_div(n, 256), 148 * 8), 256, 0, s>>>(in, out, n);
+    SAP_LAUNCHED();
+}
+void launch_cast_f2d(const float* in, double* out, int n, cudaStream_t s) {
+    k_cast_f2d<<<std::min(ceil_div(n, 256), 148 * 8), 256, 0, s>>>(in, out, n);
+    SAP_LAUNCHED();
+}
+
+template <class T>
+__global__ void k_cast_band(const double* __restrict__ in, T* __restrict__ out, size_t count) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x)
+        out[i] = static_cast<T>(in[i]);
+}
+template <class T>
+void launch_cast_band(const double* in, T* out, size_t count, cudaStream_t s) {
+    k_cast_band<T><<<(int)std::min<size_t>((count + 255) / 256, 148 * 16), 256, 0, s>>>(in, out, count);
+    SAP_LAUNCHED();
+}
+template void launch_cast_band<float>(const double*, float*, size_t, cudaStream_t);
+template void launch_cast_band<double>(const double*, double*, size_t, cudaStream_t);
+
+}  // namespace sapgpu

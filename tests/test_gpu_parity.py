@@ -1,0 +1,303 @@
+"""GPU parity: the CUDA path (through the C ABI) against the pinned CPU oracle.
+
+Tolerances (growth-aware; the reference multiplies then subtracts,
+the GPU contracts to FMA / DMMA):
+  factors      max|F_gpu - F_ref| / max|F_ref| <= 1e-13 (d >= 0.5), <= 1e-6 (d < 0.5); boosts equal
+  tips, rbar   normwise <= 1e-12 (d >= 0.5), <= 1e-9 (d < 0.5)
+  M r          relative 2-norm <= 1e-12 (d >= 0.5)
+  solve        converged to rel_tol; iterations within +-1 of the oracle
+Integer/copy outputs (coupling corners, block norms, boost counts) are bit-exact.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def nrel(a, b):
+    den = np.max(np.abs(b))
+    return np.max(np.abs(a - b)) / (den if den > 0 else 1.0)
+
+
+def rel2(a, b):
+    den = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (den if den > 0 else 1.0)
+
+
+def make(sap, n, k, band, p, kind, **kw):
+    kr = sap.KrylovOptions(**kw)
+    s = sap.Solver(p=p, precond=kind, krylov=kr)
+    s.setup(band, n, k)
+    return s
+
+
+FACTOR_CASES = [
+    # n, k, d, seed, p
+    (200, 5, 1.0, 1, 4),
+    (300, 7, 0.1, 2, 3),
+    (64, 1, 0.5, 3, 4),
+    (50, 0, 1.3, 4, 5),
+    (403, 9, 0.7, 5, 5),
+    (1000, 31, 1.0, 11, 3),
+    (2000, 50, 1.0, 12, 8),
+    (2000, 50, 0.1, 13, 8),
+    (1500, 64, 1.2, 14, 4),
+    (3000, 200, 1.0, 15, 3),
+    (3000, 200, 0.06, 16, 2),
+    (2400, 500, 1.0, 17, 2),
+    (997, 33, 0.5, 18, 7),
+]
+
+
+@pytest.mark.parametrize("n,k,d,seed,p", FACTOR_CASES)
+def test_factor_and_spike_parity(sap, oracle, n, k, d, seed, p):
+    band, rhs = oracle.random_banded(n, k, d, seed)
+    want = oracle.factor_blocks(n, k, band, p, True)
+    s = make(sap, n, k, band, p, sap.PrecondKind.coupled if p > 1 else sap.PrecondKind.decoupled)
+    lu, boosts, norms = s.factors(0)
+    tol = 1e-13 if d >= 0.5 else 1e-6
+    assert np.array_equal(norms, want["norms"])
+    assert np.array_equal(boosts, want["boosts"])
+    assert nrel(lu, want["lu"]) <= tol
+    if p > 1:
+        ul, bul, _ = s.factors(1)
+        assert np.array_equal(bul, want["boosts_ul"])
+        assert nrel(ul, want["ul"]) <= tol
+        sp = oracle.spikes(n, k, band, p)
+        ttol = 1e-12 if d >= 0.5 else 1e-9
+        w2 = k * k
+        for t in range(p - 1):
+            g = s.spike(t)
+            sl = slice(t * w2, (t + 1) * w2)
+            assert np.array_equal(g["B"], sp["B"][sl]) and np.array_equal(g["C"], sp["C"][sl])
+            if k:
+                assert nrel(g["vb"], sp["vb"][sl]) <= ttol
+                assert nrel(g["wt"], sp["wt"][sl]) <= ttol
+                assert nrel(g["rbar"], sp["rbar"][sl]) <= ttol
+            assert g["rbar_boosts"] == sp["rbar_boosts"][t]
+    for kind in (0, 1):
+        s2 = make(sap, n, k, band, p, kind)
+        got = s2.apply_preconditioner(rhs)
+        ref = oracle.apply(n, k, band, p, kind, rhs)
+        assert rel2(got, ref) <= (1e-12 if d >= 0.5 else 1e-6)
+    s.close()
+
+
+def test_known_answer_zero_pivot_boost(sap):
+    """proj/tests/test_banded_core.cpp:257-277 on the GPU: exact values."""
+    band = np.zeros(6)
+    band[3] = 1.0  # a(0,1)
+    band[2] = 1.0  # a(1,0)
+    s = sap.Solver(p=1, precond=sap.PrecondKind.decoupled, boost_eps=1e-6)
+    s.setup(band, 2, 1)
+    lu, b, nrm = s.factor(0, 0)
+    assert b == 1 and nrm == 1.0
+    assert lu[1] == 1e-6 and lu[3] == 1.0 and lu[2] == 1e6 and lu[4] == -1e6
+    x = s.apply_preconditioner(np.array([1.0, 0.0]))
+    assert x[0] == 0.0 and x[1] == 1.0
+
+
+def test_identity_factors_exact(sap):
+    n, k = 40, 3
+    band = np.zeros(n * (2 * k + 1))
+    band[np.arange(n) * (2 * k + 1) + k] = 1.0
+    s = sap.Solver(p=4, precond=sap.PrecondKind.coupled)
+    s.setup(band, n, k)
+    lu, b, _ = s.factors(0)
+    ul, bu, _ = s.factors(1)
+    assert np.array_equal(lu, band) and np.array_equal(ul, band) and b.sum() == 0 and bu.sum() == 0
+
+
+def test_identity_blocks_tips_equal_couplings_bitwise(sap, oracle):
+    """proj/tests/test_spike.cpp:94-134."""
+    n, k = 8, 2
+    w = 2 * k + 1
+    band = np.zeros(n * w)
+
+    def put(i, j, v):
+        band[j * w + (i - j + k)] = v
+
+    for i in range(n):
+        put(i, i, 1.0)
+    put(2, 4, 0.5); put(3, 4, 0.25); put(3, 5, 0.5); put(4, 2, 0.3); put(4, 3, 0.1); put(5, 3, 0.3)
+    s = sap.Solver(p=2, precond=sap.PrecondKind.coupled)
+    s.setup(band, n, k)
+    g = s.spike(0)
+    assert np.array_equal(g["vb"], g["B"]) and np.array_equal(g["wt"], g["C"])
+    ref = oracle.spikes(n, k, band, 2)
+    assert np.array_equal(g["rbar"], ref["rbar"])
+
+
+def test_zero_coupling_both_exact(sap, oracle):
+    """Acceptance criterion 3 (proj/tests/acceptance.cpp:156-188)."""
+    n, k, p = 512, 4, 4
+    band, rhs = oracle.random_banded(n, k, 1.5, 33)
+    w = 2 * k + 1
+    _, offs = oracle.partition_layout(n, p, k)
+    for t in range(1, p):
+        cut = int(offs[t])
+        for i in range(cut - k, cut):
+            for j in range(cut, min(i + k, n - 1) + 1):
+                band[j * w + (i - j + k)] = 0.0
+        for i in range(cut, min(cut + k, n)):
+            for j in range(i - k, cut):
+                band[j * w + (i - j + k)] = 0.0
+    dense = np.zeros((n, n))
+    for j in range(n):
+        for i in range(max(0, j - k), min(n, j + k + 1)):
+            dense[i, j] = band[j * w + (i - j + k)]
+    exact = np.linalg.solve(dense, rhs)
+    for kind in (0, 1):
+        s = make(sap, n, k, band, p, kind)
+        assert rel2(s.apply_preconditioner(rhs), exact) <= 1e-12
+
+
+def test_single_partition_coupled_equals_decoupled_bitwise(sap, oracle):
+    """proj/tests/test_spike.cpp:277-292."""
+    band, rhs = oracle.random_banded(500, 6, 0.8, 71)
+    a = make(sap, 500, 6, band, 1, 0).apply_preconditioner(rhs)
+    b = make(sap, 500, 6, band, 1, 1).apply_preconditioner(rhs)
+    assert np.array_equal(a, b)
+
+
+def test_preconditioner_is_linear(sap, oracle):
+    """proj/tests/test_spike.cpp:294-315."""
+    band, r1 = oracle.random_banded(800, 10, 1.0, 72)
+    r2 = oracle.uniform_stream(73, 800)
+    s = make(sap, 800, 10, band, 4, 0)
+    lhs = s.apply_preconditioner(2.0 * r1 - 3.0 * r2)
+    rhs = 2.0 * s.apply_preconditioner(r1) - 3.0 * s.apply_preconditioner(r2)
+    assert rel2(lhs, rhs) <= 1e-12
+
+
+@pytest.mark.parametrize("n,k", [(1000, 5), (3001, 50), (5000, 200), (70, 0)])
+def test_banded_matvec(sap, oracle, n, k):
+    band, x = oracle.random_banded(n, k, 1.0, 90 + k)
+    s = make(sap, n, k, band, 1, 3)
+    y = s.matvec(x)
+    ref = oracle.band_matvec(n, k, band, x)
+    assert rel2(y, ref) <= 1e-14
+
+
+def test_csr_matvec(sap, oracle):
+    rng = np.random.default_rng(5)
+    n = 3000
+    rows = [np.unique(np.clip(i + rng.integers(-40, 41, size=7), 0, n - 1)) for i in range(n)]
+    rp = np.zeros(n + 1, np.int32)
+    rp[1:] = np.cumsum([len(r) for r in rows])
+    ci = np.concatenate(rows).astype(np.int32)
+    v = rng.uniform(-1, 1, size=len(ci))
+    x = rng.uniform(-1, 1, size=n)
+    s = sap.Solver(p=1, precond=sap.PrecondKind.none)
+    s.set_operator_csr(rp, ci, v)
+    assert rel2(s.matvec(x), oracle.csr_matvec(n, rp, ci, v, x)) <= 1e-14
+
+
+@pytest.mark.parametrize("name", ["small_d1", "small_d01", "k1", "k0", "ragged"])
+def test_solve_matches_reference_goldens(sap, name):
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", name + ".npz"))
+    n, k, p = int(g["n"]), int(g["k"]), int(g["p"])
+    for kind, tag in ((0, "c"), (1, "d")):
+        s = make(sap, n, k, g["band"], p, kind, max_iterations=100)
+        x, st = s.solve(g["rhs"])
+        want_it = float(g["it_" + tag])
+        assert abs(st.iterations - want_it) <= 1.0, (tag, st.iterations, want_it)
+        assert st.converged == (int(g["fail_" + tag]) == 0)
+        if st.converged:
+            assert st.final_relative_residual <= 1e-10
+            assert len(st.residual_history) == int(round(4 * st.iterations)) + 1
+            assert rel2(x, g["x_" + tag]) <= 1e-8
+
+
+def test_acceptance_criterion2_iterations(sap):
+    """proj/tests/acceptance.cpp:103-154 (N=10000, K=50, P=8, SaP-C): iterations within +-1 of the reference."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "criterion2.npz"))
+    for d, seed, it, res, fail in g["rows"]:
+        band, rhs = sap.random_banded(10000, 50, float(d), int(seed))
+        s = make(sap, 10000, 50, band, 8, 0, max_iterations=50)
+        _, st = s.solve(rhs)
+        assert abs(st.iterations - it) <= 1.0
+        if fail == 0:
+            assert st.converged and st.final_relative_residual <= 1e-10
+        s.close()
+    band, rhs = sap.random_banded(10000, 10, 1.0, 1)
+    _, st = make(sap, 10000, 10, band, 4, 1).solve(rhs)
+    assert abs(st.iterations - g["config1"][0]) <= 1.0 and st.final_relative_residual <= 1e-10
+
+
+def test_krylov_identity_quarter(sap, oracle):
+    """proj/tests/test_krylov.cpp:62-76: identity system, 0.25 iterations, history {1, 0}."""
+    n = 10
+    b = oracle.uniform_stream(101, n)
+    s = make(sap, n, 0, np.ones(n), 1, 3)
+    x, st = s.solve(b)
+    assert st.converged and st.iterations == 0.25 and st.residual_history == [1.0, 0.0]
+    assert np.array_equal(x, b)
+
+
+def test_krylov_budget_and_failure_flags(sap, oracle):
+    band, rhs = oracle.random_banded(2000, 8, 0.05, 44)
+    s = make(sap, 2000, 8, band, 1, 3, max_iterations=2)
+    _, st = s.solve(rhs)
+    _, so = oracle.solve_banded(2000, 8, band, rhs, 1, 3, max_iterations=2)
+    assert not st.converged and st.failure == sap.KrylovFailure.max_iterations == so["failure"]
+    assert st.iterations == 2.0
+
+
+def test_preconditioner_error_on_nonfinite(sap, oracle):
+    band, rhs = oracle.random_banded(400, 4, 1.0, 3)
+    band[150 * 9 + 4] = np.nan  # diagonal of row 150 (partition 1 of 4)
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.apply(400, 4, band, 4, 0, rhs)
+    assert e.value.code == 2
+    with pytest.raises(sap.PreconditionerError, match="is not finite"):
+        make(sap, 400, 4, band, 4, 0)
+
+
+def test_solve_bitwise_repeatable(sap, oracle):
+    """Acceptance criterion 10 (proj/tests/acceptance.cpp:592-606)."""
+    band, rhs = oracle.random_banded(20000, 30, 0.5, 8)
+    s = make(sap, 20000, 30, band, 8, 1)
+    x1, s1 = s.solve(rhs)
+    x2, s2 = s.solve(rhs)
+    assert np.array_equal(x1, x2) and s1.residual_history == s2.residual_history
+
+
+def test_device_pointer_path(sap, oracle):
+    torch = pytest.importorskip("torch")
+    band, rhs = oracle.random_banded(5000, 20, 1.0, 9)
+    s = sap.Solver(p=5, precond=sap.PrecondKind.coupled)
+    s.setup(torch.from_numpy(band).cuda(), 5000, 20)
+    xb = torch.from_numpy(rhs).cuda()
+    out = s.apply_preconditioner(xb)
+    assert rel2(out.cpu().numpy(), oracle.apply(5000, 20, band, 5, 0, rhs)) <= 1e-12
+    x, st = s.solve(xb)
+    assert st.converged and x.is_cuda
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("kind,want_it", [(0, 0.25), (1, 1.75)])
+def test_config2_full_size(sap, oracle, kind, want_it):
+    """BASELINE config 2 (N=200000, K=200, d=1, P=50): reference iterations 0.25 (SaP-C) / 1.75
+    (SaP-D) with seed 1; two partitions' factors against the oracle."""
+    n, k, p = 200000, 200, 50
+    band, rhs = sap.random_banded(n, k, 1.0, 1)
+    s = make(sap, n, k, band, p, kind)
+    x, st = s.solve(rhs)
+    assert st.converged and st.final_relative_residual <= 1e-10
+    assert abs(st.iterations - want_it) <= 1.0
+    lay = s.layout
+    w = 2 * k + 1
+    for part in (0, p - 1):
+        off, m = lay.offsets[part], lay.sizes[part]
+        blk = band[off * w:(off + m) * w].copy()
+        # zero entries reaching outside the block (factor_blocks copies only in-block entries)
+        cols = np.repeat(np.arange(m), w)
+        rows = cols - k + np.tile(np.arange(w), m)
+        blk[(rows < 0) | (rows >= m)] = 0.0
+        f = oracle.factor_blocks(m, k, blk, 1, False)
+        lu, b, _ = s.factor(part, 0)
+        assert b == f["boosts"][0] and nrel(lu, f["lu"]) <= 1e-13
+    s.close()
