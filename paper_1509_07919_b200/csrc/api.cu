@@ -90,12 +90,15 @@ struct sap_handle {
     Layout layout;
     int kind = SAP_PRECOND_COUPLED;
     bool coupled = false;  // coupled && p > 1
-    DevBuf<int> d_offsets;
+    DevBuf<int> d_offsets, d_roffsets;
     const double* band_ptr = nullptr;  // A operator band (owned copy or borrowed)
     DevBuf<double> band, lu, ul, norms, bblk, cblk, vb, wt, rbar, rbar_norms, diag, scratch_g, scratch_in,
-        scratch_out, dscal;
+        scratch_out, dscal, xt, xb;
     DevBuf<int> boosts, rbar_boosts, nonfinite;
     DevBuf<FactorJob> jobs, rjobs;
+    BandStore fst, rst;                  // LU/UL and reduced-block stores
+    DevBuf<double> dinv, rdinv;          // chunk inverses for the sweeps
+    SweepPlan<double> lplan, rplan;      // block sweeps over LU and over the reduced blocks
     // CSR operator
     bool csr = false;
     int csr_n = 0;
@@ -161,16 +164,16 @@ void apply_m(sap_handle* h, const double* in, double* out) {
     const int p = h->layout.p, k = h->k;
     if (!h->coupled) {
         if (out != in) SAP_CUDA(cudaMemcpyAsync(out, in, bytes, cudaMemcpyDeviceToDevice, s));
-        launch_block_solve<double>(h->lu.get(), h->d_offsets.get(), p, k, out, s);
+        launch_block_solve<double>(h->lplan, out, s);
         return;
     }
     double* g = h->scratch_g.get();
     SAP_CUDA(cudaMemcpyAsync(g, in, bytes, cudaMemcpyDeviceToDevice, s));
     if (out != in) SAP_CUDA(cudaMemcpyAsync(out, in, bytes, cudaMemcpyDeviceToDevice, s));
-    launch_block_solve<double>(h->lu.get(), h->d_offsets.get(), p, k, g, s);
-    launch_interfaces<double>(g, h->d_offsets.get(), p, k, h->wt.get(), h->vb.get(), h->rbar.get(), h->bblk.get(),
-                              h->cblk.get(), out, s);
-    launch_block_solve<double>(h->lu.get(), h->d_offsets.get(), p, k, out, s);
+    launch_block_solve<double>(h->lplan, g, s);
+    launch_interfaces<double>(g, h->d_offsets.get(), h->rplan, p, k, h->wt.get(), h->vb.get(), h->bblk.get(),
+                              h->cblk.get(), h->xt.get(), h->xb.get(), out, s);
+    launch_block_solve<double>(h->lplan, out, s);
 }
 
 void apply_a(sap_handle* h, const double* in, double* out) {
@@ -234,7 +237,7 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
         const int ho[2] = {0, n};
         SAP_CUDA(cudaMemcpyAsync(offs1.get(), ho, sizeof(ho), cudaMemcpyHostToDevice, s));
         h->diag.alloc(n);
-        launch_block_norms(h->band_ptr, n, k, offs1.get(), 1, h->dscal.get(), s);
+        launch_block_norms(h->band_ptr, n, k, offs1.get(), 1, nullptr, h->dscal.get(), s);
         launch_boosted_diag(h->band_ptr, n, k, h->dscal.get(), h->opt.boost_eps, h->diag.get(), s);
         SAP_CUDA(cudaEventRecord(h->ev[2], s));
         SAP_CUDA(cudaStreamSynchronize(s));
@@ -250,30 +253,45 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
     h->norms.alloc(p);
     h->boosts.alloc(2 * (size_t)p);
     SAP_CUDA(cudaMemsetAsync(h->boosts.get(), 0, sizeof(int) * 2 * p, s));
-    h->lu.alloc(total);
+    const int m_max = L.sizes[0];
+    h->fst = BandStore::make(m_max, k);
+    h->lu.alloc(h->fst.total(p));
     if (h->coupled)
-        h->ul.alloc(total);
+        h->ul.alloc(h->fst.total(p));
     else
         h->ul.release();
     const int njobs = h->coupled ? 2 * p : p;
     std::vector<FactorJob> jobs(njobs);
     for (int b = 0; b < p; ++b) {
-        const int off = L.offsets[b], m = L.sizes[b];
-        double* f = h->lu.get() + (size_t)off * (2 * k + 1);
+        const int m = L.sizes[b];
+        double* f = h->lu.get() + h->fst.block(b);
         jobs[b] = FactorJob{f + k, 1, 2LL * k, m, k, h->norms.get() + b, h->boosts.get() + b};
         if (h->coupled) {
-            double* g = h->ul.get() + (size_t)off * (2 * k + 1);
+            double* g = h->ul.get() + h->fst.block(b);
             jobs[p + b] = FactorJob{g + (size_t)(m - 1) * (2 * k + 1) + k, -1, -2LL * k, m, k, h->norms.get() + b,
                                     h->boosts.get() + p + b};
         }
     }
     h->jobs.alloc(njobs);
     SAP_CUDA(cudaMemcpyAsync(h->jobs.get(), jobs.data(), sizeof(FactorJob) * njobs, cudaMemcpyHostToDevice, s));
-    launch_block_norms(h->band_ptr, n, k, h->d_offsets.get(), p, h->norms.get(), s);
-    launch_copy_blocks(h->band_ptr, n, k, p, h->lu.get(), h->coupled ? h->ul.get() : nullptr, s);
+    launch_block_norms(h->band_ptr, m_max, k, h->d_offsets.get(), p, nullptr, h->norms.get(), s);
+    launch_copy_blocks(h->band_ptr, k, h->d_offsets.get(), p, h->fst, h->lu.get(), h->coupled ? h->ul.get() : nullptr,
+                       s);
     SAP_CUDA(cudaEventRecord(h->ev[8], s));
     launch_band_lu(h->jobs.get(), njobs, k, h->opt.boost_eps, s);
     SAP_CUDA(cudaEventRecord(h->ev[9], s));
+    {
+        SweepPlan<double>& lp = h->lplan;
+        lp = SweepPlan<double>{};
+        lp.f = h->lu.get();
+        lp.st = h->fst;
+        lp.offs = h->d_offsets.get();
+        lp.p = p;
+        lp.k = k;
+        h->dinv.alloc(std::max<size_t>(sweep_dinv_elems(lp), 1));
+        plan_sweeps(lp, h->dinv.get());
+        launch_chunk_inverses(lp, s);
+    }
     SAP_CUDA(cudaEventRecord(h->ev[2], s));
     for (int b = 0; b < p; ++b) {
         // band_lu_inplace op count: sum over columns of d + 2 d^2, d = min(k, m-1-j)
@@ -286,34 +304,54 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
     if (h->coupled) {
         ni = p - 1;
         const size_t ww = (size_t)k * k * ni;
+        h->rst = BandStore::make(k, k > 0 ? k - 1 : 0);  // reduced blocks in band layout, k' = w-1
         h->bblk.alloc(std::max<size_t>(ww, 1));
         h->cblk.alloc(std::max<size_t>(ww, 1));
         h->vb.alloc(std::max<size_t>(ww, 1));
         h->wt.alloc(std::max<size_t>(ww, 1));
-        h->rbar.alloc(std::max<size_t>(ww, 1));
+        h->rbar.alloc(std::max<size_t>(h->rst.total(ni), 1));
+        SAP_CUDA(cudaMemsetAsync(h->rbar.get(), 0, sizeof(double) * h->rst.total(ni), s));
         h->rbar_norms.alloc(ni);
         h->rbar_boosts.alloc(ni);
         h->nonfinite.alloc(3 * (size_t)ni);
         h->scratch_g.alloc(n);
+        h->xt.alloc(std::max<size_t>((size_t)ni * k, 1));
+        h->xb.alloc(std::max<size_t>((size_t)ni * k, 1));
+        std::vector<int> roffs(ni + 1);
+        for (int t = 0; t <= ni; ++t) roffs[t] = t * k;
+        h->d_roffsets.alloc(ni + 1);
+        SAP_CUDA(cudaMemcpyAsync(h->d_roffsets.get(), roffs.data(), sizeof(int) * (ni + 1), cudaMemcpyHostToDevice, s));
         SAP_CUDA(cudaMemsetAsync(h->nonfinite.get(), 0, sizeof(int) * 3 * ni, s));
         SAP_CUDA(cudaMemsetAsync(h->rbar_boosts.get(), 0, sizeof(int) * ni, s));
         // ---- T_BC: extract_coupling ----
         launch_extract_coupling(h->band_ptr, n, k, h->d_offsets.get(), p, h->bblk.get(), h->cblk.get(), s);
         SAP_CUDA(cudaEventRecord(h->ev[3], s));
         // ---- T_SPK: spike tips ----
-        launch_spike_tips(h->lu.get(), h->ul.get(), h->d_offsets.get(), p, k, h->bblk.get(), h->cblk.get(),
+        launch_spike_tips(h->lu.get(), h->ul.get(), h->fst, h->d_offsets.get(), p, k, h->bblk.get(), h->cblk.get(),
                           h->vb.get(), h->wt.get(), h->nonfinite.get(), s);
         SAP_CUDA(cudaEventRecord(h->ev[4], s));
-        // ---- T_LUrdcd: rbar = I - W V and its boosted no-pivot LU ----
-        launch_rbar(h->wt.get(), h->vb.get(), k, ni, h->rbar.get(), s);
-        launch_dense_norms(h->rbar.get(), k, ni, h->rbar_norms.get(), h->nonfinite.get() + 2 * ni, s);
-        std::vector<FactorJob> rj(ni);
-        for (int t = 0; t < ni; ++t)
-            rj[t] = FactorJob{h->rbar.get() + (size_t)t * k * k, (long long)k, 1, k, k - 1, h->rbar_norms.get() + t,
-                              h->rbar_boosts.get() + t};
-        h->rjobs.alloc(ni);
-        SAP_CUDA(cudaMemcpyAsync(h->rjobs.get(), rj.data(), sizeof(FactorJob) * ni, cudaMemcpyHostToDevice, s));
-        launch_band_lu(h->rjobs.get(), ni, k - 1, h->opt.boost_eps, s);
+        // ---- T_LUrdcd: rbar = I - W V (band layout, k' = w-1) and its boosted no-pivot LU ----
+        if (k > 0) {
+            launch_rbar(h->wt.get(), h->vb.get(), k, ni, h->rbar.get(), h->rst, h->nonfinite.get() + 2 * ni, s);
+            launch_block_norms(h->rbar.get(), k, k - 1, h->d_roffsets.get(), ni, &h->rst, h->rbar_norms.get(), s);
+            std::vector<FactorJob> rj(ni);
+            for (int t = 0; t < ni; ++t)
+                rj[t] = FactorJob{h->rbar.get() + h->rst.block(t) + (k - 1), 1, 2LL * (k - 1), k, k - 1,
+                                  h->rbar_norms.get() + t, h->rbar_boosts.get() + t};
+            h->rjobs.alloc(ni);
+            SAP_CUDA(cudaMemcpyAsync(h->rjobs.get(), rj.data(), sizeof(FactorJob) * ni, cudaMemcpyHostToDevice, s));
+            launch_band_lu(h->rjobs.get(), ni, k - 1, h->opt.boost_eps, s);
+            SweepPlan<double>& rp = h->rplan;
+            rp = SweepPlan<double>{};
+            rp.f = h->rbar.get();
+            rp.st = h->rst;
+            rp.offs = h->d_roffsets.get();
+            rp.p = ni;
+            rp.k = k - 1;
+            h->rdinv.alloc(std::max<size_t>(sweep_dinv_elems(rp), 1));
+            plan_sweeps(rp, h->rdinv.get());
+            launch_chunk_inverses(rp, s);
+        }
         SAP_CUDA(cudaEventRecord(h->ev[5], s));
     }
     SAP_CUDA(cudaStreamSynchronize(s));
@@ -604,7 +642,7 @@ sap_status sap_get_factor(sap_handle* h, int part, int which, double* out, int* 
         if (which == 1 && !h->coupled) throw InvalidArgument("block_solve: UL factors not available");
         SAP_CUDA(cudaSetDevice(h->opt.device));
         const size_t w = 2 * (size_t)h->k + 1;
-        const double* src = (which == 0 ? h->lu.get() : h->ul.get()) + (size_t)h->layout.offsets[part] * w;
+        const double* src = (which == 0 ? h->lu.get() : h->ul.get()) + h->fst.block(part);
         if (out)
             SAP_CUDA(cudaMemcpy(out, src, sizeof(double) * (size_t)h->layout.sizes[part] * w, cudaMemcpyDeviceToHost));
         if (boosts)
@@ -627,7 +665,15 @@ sap_status sap_get_spike(sap_handle* h, int iface, double* b_block, double* c_bl
         if (c_block) SAP_CUDA(cudaMemcpy(c_block, h->cblk.get() + off, bytes, cudaMemcpyDeviceToHost));
         if (v_bottom) SAP_CUDA(cudaMemcpy(v_bottom, h->vb.get() + off, bytes, cudaMemcpyDeviceToHost));
         if (w_top) SAP_CUDA(cudaMemcpy(w_top, h->wt.get() + off, bytes, cudaMemcpyDeviceToHost));
-        if (rbar) SAP_CUDA(cudaMemcpy(rbar, h->rbar.get() + off, bytes, cudaMemcpyDeviceToHost));
+        if (rbar && h->k > 0) {
+            const int w = h->k;
+            const size_t rb = (size_t)w * (2 * (size_t)w - 1);
+            std::vector<double> band(rb);
+            SAP_CUDA(cudaMemcpy(band.data(), h->rbar.get() + h->rst.block(iface), sizeof(double) * rb,
+                                cudaMemcpyDeviceToHost));
+            for (int i = 0; i < w; ++i)
+                for (int j = 0; j < w; ++j) rbar[(size_t)i * w + j] = band[(size_t)j * (2 * w - 1) + (i - j + w - 1)];
+        }
         if (rbar_boosts)
             SAP_CUDA(cudaMemcpy(rbar_boosts, h->rbar_boosts.get() + iface, sizeof(int), cudaMemcpyDeviceToHost));
     });

@@ -3,169 +3,617 @@
 // Reference: block_solve / band_lu_solve proj/include/sap/block_factors.hpp:74-90,
 // :210-236 and apply_preconditioner proj/include/sap/spike.hpp:304-351.
 //
-// Block solve: one CTA per partition walks its rows in 32-row chunks. For a
-// chunk, the 16 warps form the off-chunk part of every row's dot product
-// (each warp a strided subset of the previous K columns, lane = row, so every
-// load is a contiguous 256-byte run of the column-major band), the partials
-// are summed in fixed order, and warp 0 finishes the 32x32 triangle with
-// shuffles. The backward (U) sweep mirrors it from the bottom chunk up.
+// Band sweeps, TMA path (k_sweep_tma). One CTA per block walks the rows in
+// TR-row chunks. The factor slab a chunk needs -- rows [i0, i0+TR) of the K
+// columns left of it (forward, L) or right of it (backward, U) -- is ONE 2-D
+// TMA box of an overlapping tensor view of the tall-thin band (element (i, c)
+// at c*2k + i + k: dim0 = row, stride1 = 2k doubles), streamed S chunks ahead
+// into a shared-memory ring under an mbarrier, with deeper L2 prefetches.
+// The chunk's diagonal TRxTR triangle is not walked serially: its inverse
+// (unit-lower L^{-1} / upper U^{-1}, precomputed once at setup by
+// k_chunk_inverses) arrives with the slab, so finishing a chunk is a TRxTR
+// mat-vec on warp 0 instead of a TR-step shuffle chain. Per chunk:
+//   phase 1: warp 0 finishes chunk ch-1 (x = D^{-1} z) while warps 1..15 form
+//            the part of chunk ch's row sums that only needs older x;
+//   phase 2: all warps add the TR columns that need chunk ch-1's x.
+// x lives in a circular shared-memory window of the last K+2TR rows.
+// Padding/out-of-band slab entries are masked in registers; entries beyond the
+// block are zero in the BandStore or zero-filled by TMA.
+//
+// k == 0 (or a band too wide for the TMA ring) uses k_sweep_ldgsts: the same
+// chunking with cp.async slabs and a shuffle triangle solve.
+#include <cuda.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
 namespace sapgpu {
 
-constexpr int kSolveThreads = 512;
-constexpr int kSolveWarps = kSolveThreads / 32;
-
-template <class T>
-__global__ void __launch_bounds__(kSolveThreads)
-    k_block_solve(const T* __restrict__ lu, const int* __restrict__ offs, int k, T* __restrict__ x) {
-    const int b = blockIdx.x;
-    const int off = offs[b], m = offs[b + 1] - off;
-    const T* f = lu + (long long)off * (2 * k + 1);
-    const long long ld = 2LL * k;
-    T* xb = x + off;
-    __shared__ T part[kSolveWarps][33];
-    __shared__ T tri[32][33];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int nchunks = (m + 31) / 32;
-
-    // forward: L unit lower, x_i -= sum_{j<i} L(i,j) x_j
-    for (int ch = 0; ch < nchunks; ++ch) {
-        const int i0 = ch * 32, rows = min(32, m - i0);
-        const int i = i0 + lane;
-        T s = T(0);
-        const int jlo = max(i0 - k, 0);
-#pragma unroll 4
-        for (int j = jlo + warp; j < i0; j += kSolveWarps)
-            if (lane < rows && i - j <= k) s = fma(f[(long long)j * ld + i + k], xb[j], s);
-        part[warp][lane] = s;
-        for (int jj = warp; jj < rows; jj += kSolveWarps)
-            tri[lane][jj] = (lane > jj && lane < rows && lane - jj <= k) ? f[(long long)(i0 + jj) * ld + i + k] : T(0);
-        __syncthreads();
-        if (warp == 0) {
-            T tot = T(0);
-#pragma unroll
-            for (int q = 0; q < kSolveWarps; ++q) tot += part[q][lane];
-            T y = lane < rows ? xb[i] - tot : T(0);
-            for (int jj = 0; jj < rows; ++jj) {
-                const T xj = __shfl_sync(0xffffffffu, y, jj);
-                if (lane > jj) y = fma(-tri[lane][jj], xj, y);
-            }
-            if (lane < rows) xb[i] = y;
-        }
-        __syncthreads();
-    }
-    // backward: U with diagonal, x_i = (x_i - sum_{j>i} U(i,j) x_j) / U(i,i)
-    for (int ch = nchunks - 1; ch >= 0; --ch) {
-        const int i0 = ch * 32, rows = min(32, m - i0);
-        const int i = i0 + lane;
-        T s = T(0);
-        const int jhi = min(i0 + 31 + k, m - 1);
-#pragma unroll 4
-        for (int j = i0 + rows + warp; j <= jhi; j += kSolveWarps)
-            if (lane < rows && j - i <= k) s = fma(f[(long long)j * ld + i + k], xb[j], s);
-        part[warp][lane] = s;
-        for (int jj = warp; jj < rows; jj += kSolveWarps)
-            tri[lane][jj] = (lane <= jj && lane < rows && jj - lane <= k) ? f[(long long)(i0 + jj) * ld + i + k] : T(0);
-        __syncthreads();
-        if (warp == 0) {
-            T tot = T(0);
-#pragma unroll
-            for (int q = 0; q < kSolveWarps; ++q) tot += part[q][lane];
-            T y = lane < rows ? xb[i] - tot : T(0);
-            for (int jj = rows - 1; jj >= 0; --jj) {
-                if (lane == jj) y = y / tri[lane][lane];
-                const T xj = __shfl_sync(0xffffffffu, y, jj);
-                if (lane < jj) y = fma(-tri[lane][jj], xj, y);
-            }
-            if (lane < rows) xb[i] = y;
-        }
-        __syncthreads();
-    }
-}
-
-template <class T>
-void launch_block_solve(const T* lu, const int* d_offsets, int p, int k, T* x, cudaStream_t s) {
-    k_block_solve<T><<<p, kSolveThreads, 0, s>>>(lu, d_offsets, k, x);
-    SAP_LAUNCHED();
-}
-template void launch_block_solve<double>(const double*, const int*, int, int, double*, cudaStream_t);
-template void launch_block_solve<float>(const float*, const int*, int, int, float*, cudaStream_t);
+constexpr int kSwThreads = 512;
+constexpr int kSwWarps = kSwThreads / 32;
 
 // ---------------------------------------------------------------------------
-// SaP-C interface step, one CTA per interface t (spike.hpp:323-347):
-//   rhs = g[e:e+w] - W^t g[e-w:e];  R xt = rhs;  xb = g[e-w:e] - V^b xt;
-//   b2[e-w:e] -= B xt;  b2[e:e+w] -= C xb.
-// Interfaces write disjoint rows of b2 (every block has >= 2K rows).
+// PTX helpers: mbarrier, TMA, bulk copies, cp.async.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    const unsigned a = smem_u32(bar);
+    unsigned done = 0;
+    while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done)
+                     : "r"(a), "r"(parity)
+                     : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x0, int x1, int x2,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(x0), "r"(x1), "r"(x2), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int x0, int x1, int x2) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(map), "r"(x0), "r"(x1),
+                 "r"(x2)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
 template <class T>
-__device__ void gemv_sub_warps(const T* __restrict__ a, int w, const T* xv, T* y) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int i = warp; i < w; i += nw) {
-        T acc = T(0);
-        for (int j = lane; j < w; j += 32) acc = fma(a[(long long)i * w + j], xv[j], acc);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) y[i] -= acc;
+__device__ __forceinline__ void cp_async_elem(T* smem, const T* gmem) {
+    if constexpr (sizeof(T) == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(smem)), "l"(gmem));
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(smem)), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// ---------------------------------------------------------------------------
+// Diagonal-chunk inverses: dinv[((b*nch_max + q)*2 + dir)*TR*TR + j*TR + i] =
+// (L_qq^{-1})(i, j) for dir 0 (unit lower), (U_qq^{-1})(i, j) for dir 1.
+// Rows beyond the block are padded with the identity. One warp per inverse,
+// lane j builds column j by substitution on e_j.
+template <class T, int TR>
+__global__ void k_chunk_inverses(const T* __restrict__ f0, long long pstride, int pad, const int* __restrict__ offs,
+                                 int k, T* __restrict__ dinv, int nch_max) {
+    __shared__ T blk[TR][TR + 1];       // blk[j][i] = F(i0+i, i0+j)
+    __shared__ T X[2][TR][TR + 1];      // X[dir][j][i]
+    const int b = blockIdx.y, q = blockIdx.x;
+    const int m = offs[b + 1] - offs[b];
+    const int i0 = q * TR;
+    if (i0 >= m) return;
+    const int rows = min(TR, m - i0);
+    const T* f = f0 + (long long)b * pstride + pad;
+    const long long ld = 2LL * k;
+    for (int idx = threadIdx.x; idx < TR * TR; idx += blockDim.x) {
+        const int j = idx / TR, i = idx % TR;
+        T v;
+        if (i < rows && j < rows)
+            v = (i - j <= k && j - i <= k) ? f[(long long)(i0 + j) * ld + i0 + i + k] : T(0);
+        else
+            v = (i == j) ? T(1) : T(0);
+        blk[j][i] = v;
+    }
+    __syncthreads();
+    const int dir = threadIdx.x >> 5, j = threadIdx.x & 31;
+    if (j < TR) {
+        if (dir == 0) {  // unit lower
+            for (int i = 0; i < TR; ++i) X[0][j][i] = (i == j) ? T(1) : T(0);
+            for (int i = j + 1; i < TR; ++i) {
+                T acc = T(0);
+                for (int l = j; l < i; ++l) acc = fma(blk[l][i], X[0][j][l], acc);
+                X[0][j][i] = -acc;
+            }
+        } else {  // upper with diagonal
+            for (int i = 0; i < TR; ++i) X[1][j][i] = T(0);
+            X[1][j][j] = T(1) / blk[j][j];
+            for (int i = j - 1; i >= 0; --i) {
+                T acc = T(0);
+                for (int l = i + 1; l <= j; ++l) acc = fma(blk[l][i], X[1][j][l], acc);
+                X[1][j][i] = -acc / blk[i][i];
+            }
+        }
+    }
+    __syncthreads();
+    T* out = dinv + ((long long)b * nch_max + q) * 2 * TR * TR;
+    for (int idx = threadIdx.x; idx < 2 * TR * TR; idx += blockDim.x) {
+        const int d = idx / (TR * TR), r = idx % (TR * TR);
+        out[idx] = X[d][r / TR][r % TR];
     }
 }
 
-template <class T>
-__global__ void __launch_bounds__(256)
-    k_interfaces(const T* __restrict__ g, const int* __restrict__ offs, int k, const T* __restrict__ wt,
-                 const T* __restrict__ vb, const T* __restrict__ rbar, const T* __restrict__ bblk,
-                 const T* __restrict__ cblk, T* __restrict__ b2) {
+// ---------------------------------------------------------------------------
+template <class T, int TR, int S>
+struct SweepSmem {
+    static constexpr int SD = S + 1;  // inverse ring outlives the slab by one chunk
+};
+
+template <class T, int TR, int S>
+__global__ void __launch_bounds__(kSwThreads, 1)
+    k_sweep_tma(const __grid_constant__ CUtensorMap map, const T* __restrict__ dinv, int nch_max,
+                const int* __restrict__ offs, int k, T* __restrict__ xbase, int xw, int slab_cols, int box_c,
+                int nbox) {
+    constexpr int SD = SweepSmem<T, TR, S>::SD;
+    constexpr int CG = 32 / TR;  // column groups per warp
+    constexpr int PF = 6;        // L2 prefetch distance (chunks)
+    extern __shared__ __align__(128) unsigned char smraw[];
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(smraw);  // S barriers (128 B reserved)
+    T* slab = reinterpret_cast<T*>(smraw + 128);
+    const size_t slab_elems = (size_t)TR * slab_cols;
+    T* dv = slab + S * slab_elems;                 // SD x TR*TR
+    T* xs = dv + SD * TR * TR;                     // xw
+    T* part = xs + xw;                             // kSwWarps x TR
+
+    const int b = blockIdx.x;
+    const int off = offs[b], m = offs[b + 1] - off;
+    T* x = xbase + off;
+    const int xm = xw - 1;
+    const int nch = (m + TR - 1) / TR;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int r = lane % TR, cg = lane / TR;
+    const T* dvb = dinv + (long long)b * nch_max * 2 * TR * TR;
+    const unsigned slab_bytes = (unsigned)(slab_elems * sizeof(T));
+    const unsigned dv_bytes = (unsigned)(TR * TR * sizeof(T));
+    const bool producer = (warp == 1 && lane == 0);
+
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(bar + s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int i = tid; i < xw; i += kSwThreads) xs[i] = T(0);
+    __syncthreads();
+
+    // g = global chunk sequence number (forward 0..nch-1, backward nch..2nch-1)
+    auto issue = [&](int g) {
+        const bool fwd = g < nch;
+        const int ch = fwd ? g : 2 * nch - 1 - g;
+        const int i0 = ch * TR;
+        const int c0 = fwd ? i0 - k : i0 + TR;
+        const int st = g % S;
+        mbar_expect_tx(bar + st, slab_bytes + dv_bytes);
+        T* dst = slab + st * slab_elems;
+        for (int q = 0; q < nbox; ++q) tma_load_3d(dst + (size_t)q * TR * box_c, &map, i0, c0 + q * box_c, b, bar + st);
+        bulk_load(dv + (g % SD) * TR * TR, dvb + ((long long)ch * 2 + (fwd ? 0 : 1)) * TR * TR, dv_bytes, bar + st);
+    };
+    auto prefetch = [&](int g) {
+        const bool fwd = g < nch;
+        const int ch = fwd ? g : 2 * nch - 1 - g;
+        const int i0 = ch * TR;
+        const int c0 = fwd ? i0 - k : i0 + TR;
+        for (int q = 0; q < nbox; ++q) tma_prefetch_3d(&map, i0, c0 + q * box_c, b);
+    };
+
+    for (int dir = 0; dir < 2; ++dir) {
+        const bool fwd = dir == 0;
+        const int gbase = fwd ? 0 : nch;
+        if (producer) {
+            for (int q = 0; q < S - 1 && q < nch; ++q) issue(gbase + q);
+            for (int q = S - 1; q < S - 1 + PF && q < nch; ++q) prefetch(gbase + q);
+        }
+        T yprev = T(0);  // y of the chunk warp 0 finishes next (warp 0 only)
+        if (warp == 0) {
+            const int ch0 = fwd ? 0 : nch - 1;
+            const int in = ch0 * TR + lane;
+            yprev = (lane < TR && in < m) ? x[in] : T(0);
+        }
+        int prev_rows = 0;
+        for (int t = 0; t <= nch; ++t) {
+            const int g = gbase + t;
+            const int ch = fwd ? t : nch - 1 - t;   // chunk whose row sums are formed now
+            const int pch = fwd ? t - 1 : nch - t;  // chunk finished now by warp 0
+            if (t < nch) mbar_wait(bar + g % S, (unsigned)((g / S) & 1));
+            __syncthreads();  // A
+            if (producer && t + S - 1 < nch) {
+                issue(g + S - 1);
+                if (t + S - 1 + PF < nch) prefetch(g + S - 1 + PF);
+            }
+            const T* L = slab + (g % S) * slab_elems;
+            const int i0 = ch * TR;
+            // ---- phase 1 ----
+            T sA = T(0);
+            if (warp == 0) {
+                if (t >= 1) {
+                    const int p0 = pch * TR;
+                    T z = T(0);
+                    if (lane < TR) {
+                        T tot = T(0);
+#pragma unroll
+                        for (int q = 0; q < kSwWarps; ++q) tot += part[q * TR + lane];
+                        z = yprev - tot;
+                    }
+                    const T* D = dv + ((g - 1) % SD) * TR * TR;
+                    T a0 = T(0), a1 = T(0);
+#pragma unroll
+                    for (int jj = 0; jj < TR; jj += 2) {
+                        const T z0 = __shfl_sync(0xffffffffu, z, jj);
+                        const T z1 = __shfl_sync(0xffffffffu, z, jj + 1);
+                        if (lane < TR) {
+                            a0 = fma(D[jj * TR + lane], z0, a0);
+                            a1 = fma(D[(jj + 1) * TR + lane], z1, a1);
+                        }
+                    }
+                    const T xv = a0 + a1;
+                    if (lane < prev_rows) {
+                        xs[(p0 + lane) & xm] = xv;
+                        x[p0 + lane] = xv;
+                    }
+                }
+                if (t < nch) {  // y of chunk ch, finished in the next iteration
+                    const int in = i0 + lane;
+                    yprev = (lane < TR && in < m) ? x[in] : T(0);
+                    prev_rows = min(TR, m - i0);
+                }
+            } else if (t < nch) {
+                // columns needing only x older than chunk pch
+                const int ca = fwd ? 0 : TR, cb = fwd ? k - TR : k;
+                const int cbase = fwd ? i0 - k : i0 + TR;
+                for (int cc = ca + (warp - 1) * CG + cg; cc < cb; cc += (kSwWarps - 1) * CG) {
+                    const int c = cbase + cc;
+                    T l = L[cc * TR + r];
+                    if (fwd) {
+                        if (cc < TR && r > cc) l = T(0);
+                    } else {
+                        if (TR + cc - r > k) l = T(0);
+                    }
+                    sA = fma(l, xs[c & xm], sA);
+                }
+            }
+            __syncthreads();  // B
+            // ---- phase 2: the TR columns of chunk pch ----
+            if (t < nch) {
+                T sB = T(0);
+                const int ca = fwd ? max(k - TR, 0) : 0, cb = fwd ? k : min(TR, k);
+                const int cbase = fwd ? i0 - k : i0 + TR;
+                for (int cc = ca + warp * CG + cg; cc < cb; cc += kSwWarps * CG) {
+                    const int c = cbase + cc;
+                    T l = L[cc * TR + r];
+                    if (fwd) {
+                        if (cc < TR && r > cc) l = T(0);
+                    } else {
+                        if (TR + cc - r > k) l = T(0);
+                    }
+                    sB = fma(l, xs[c & xm], sB);
+                }
+                T s = sA + sB;
+                if constexpr (CG > 1) {
+#pragma unroll
+                    for (int o = TR; o < 32; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                }
+                if (cg == 0) part[warp * TR + r] = s;
+            }
+        }
+        __syncthreads();
+        for (int i = tid; i < xw; i += kSwThreads) xs[i] = T(0);
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Fallback sweep (k == 0, or bands too wide for the TMA ring): cp.async slabs,
+// shuffle triangle solves. TR = 32.
+template <class T, int S>
+__global__ void __launch_bounds__(kSwThreads, 1)
+    k_sweep_ldgsts(const T* __restrict__ f0, long long pstride, int pad, const int* __restrict__ offs, int k,
+                   T* __restrict__ xbase, int xw) {
+    constexpr int TR = 32;
     extern __shared__ __align__(16) unsigned char smraw[];
-    T* gb = reinterpret_cast<T*>(smraw);
-    T* rhs = gb + k;
-    const int t = blockIdx.x, w = k;
-    const int e = offs[t + 1];
-    const long long ww = (long long)w * w;
-    for (int i = threadIdx.x; i < w; i += blockDim.x) {
-        gb[i] = g[e - w + i];
-        rhs[i] = g[e + i];
-    }
-    __syncthreads();
-    gemv_sub_warps(wt + t * ww, w, gb, rhs);
-    __syncthreads();
-    const T* R = rbar + t * ww;
-    const int lane = threadIdx.x & 31;
-    if (threadIdx.x < 32) {
-        for (int i = 0; i < w; ++i) {  // unit lower
-            T acc = T(0);
-            for (int j = lane; j < i; j += 32) acc = fma(R[(long long)i * w + j], rhs[j], acc);
+    const int ncol = k + TR;
+    T* ring = reinterpret_cast<T*>(smraw);
+    T* xs = ring + (size_t)S * ncol * TR;
+    T* part = xs + xw;
+    const int b = blockIdx.x;
+    const int off = offs[b], m = offs[b + 1] - off;
+    const T* f = f0 + (long long)b * pstride + pad;
+    T* x = xbase + off;
+    const long long ld = 2LL * k;
+    const int xm = xw - 1;
+    const int nch = (m + TR - 1) / TR;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < xw; i += kSwThreads) xs[i] = T(0);
+    for (int dir = 0; dir < 2; ++dir) {
+        const bool fwd = dir == 0;
+        auto issue = [&](int t) {
+            const int ch = fwd ? t : nch - 1 - t;
+            T* dst = ring + (size_t)(t % S) * ncol * TR;
+            const int i0 = ch * TR, c0 = fwd ? i0 - k : i0;
+            for (int idx = tid; idx < ncol * TR; idx += kSwThreads) {
+                const int cc = idx >> 5, rr = idx & 31;
+                const int c = c0 + cc, i = i0 + rr;
+                const bool ok = fwd ? (c >= 0 && i < m && c < i && i - c <= k) : (i < m && c < m && c >= i && c - i <= k);
+                if (ok)
+                    cp_async_elem(dst + idx, f + (long long)c * ld + i + k);
+                else
+                    dst[idx] = T(0);
+            }
+        };
+        __syncthreads();
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (lane == 0) rhs[i] -= acc;
-            __syncwarp();
+        for (int s = 0; s < S - 1; ++s) {
+            if (s < nch) issue(s);
+            cp_async_commit();
         }
-        for (int i = w - 1; i >= 0; --i) {  // upper with diagonal
-            T acc = T(0);
-            for (int j = i + 1 + lane; j < w; j += 32) acc = fma(R[(long long)i * w + j], rhs[j], acc);
+        for (int t = 0; t < nch; ++t) {
+            const int ch = fwd ? t : nch - 1 - t;
+            cp_async_wait<S - 2>();
+            __syncthreads();
+            if (t + S - 1 < nch) issue(t + S - 1);
+            cp_async_commit();
+            const T* Lc = ring + (size_t)(t % S) * ncol * TR;
+            const int i0 = ch * TR;
+            T s = T(0);
+            if (fwd) {
+                for (int cc = warp; cc < k; cc += kSwWarps) s = fma(Lc[cc * TR + lane], xs[(i0 - k + cc) & xm], s);
+            } else {
+                for (int cc = TR + warp; cc < ncol; cc += kSwWarps) s = fma(Lc[cc * TR + lane], xs[(i0 + cc) & xm], s);
+            }
+            part[warp * 33 + lane] = s;
+            __syncthreads();
+            if (warp == 0) {
+                T tot = T(0);
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (lane == 0) rhs[i] = (rhs[i] - acc) / R[(long long)i * w + i];
-            __syncwarp();
+                for (int q = 0; q < kSwWarps; ++q) tot += part[q * 33 + lane];
+                const int rows = min(TR, m - i0);
+                T y = lane < rows ? x[i0 + lane] - tot : T(0);
+                if (fwd) {
+                    const T* tri = Lc + (size_t)k * TR;
+                    for (int jj = 0; jj < rows; ++jj) {
+                        const T xj = __shfl_sync(0xffffffffu, y, jj);
+                        if (lane > jj) y = fma(-tri[jj * TR + lane], xj, y);
+                    }
+                } else {
+                    for (int jj = rows - 1; jj >= 0; --jj) {
+                        if (lane == jj) y = y / Lc[jj * TR + jj];
+                        const T xj = __shfl_sync(0xffffffffu, y, jj);
+                        if (lane < jj) y = fma(-Lc[jj * TR + lane], xj, y);
+                    }
+                }
+                if (lane < rows) {
+                    xs[(i0 + lane) & xm] = y;
+                    x[i0 + lane] = y;
+                }
+            }
         }
+        cp_async_wait<0>();
+        __syncthreads();
+        for (int i = tid; i < xw; i += kSwThreads) xs[i] = T(0);
     }
-    __syncthreads();
-    gemv_sub_warps(vb + t * ww, w, rhs, gb);  // gb becomes xb
-    __syncthreads();
-    gemv_sub_warps(bblk + t * ww, w, rhs, b2 + e - w);
-    gemv_sub_warps(cblk + t * ww, w, gb, b2 + e);
+}
+
+// ---------------------------------------------------------------------------
+static int pow2_at_least(int v) {
+    int p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        SAP_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (!p || q != cudaDriverEntryPointSuccess) throw CudaFailure("cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+template <class T, int TR, int S>
+static size_t tma_smem_bytes(int slab_cols, int xw) {
+    return 128 + sizeof(T) * ((size_t)S * TR * slab_cols + (size_t)(S + 1) * TR * TR + xw + kSwWarps * TR);
 }
 
 template <class T>
-void launch_interfaces(const T* g, const int* d_offsets, int p, int k, const T* wt, const T* vb, const T* rbar,
-                       const T* bblk, const T* cblk, T* b2, cudaStream_t s) {
-    if (p < 2 || k == 0) return;
-    k_interfaces<T><<<p - 1, 256, 2 * k * sizeof(T), s>>>(g, d_offsets, k, wt, vb, rbar, bblk, cblk, b2);
+static void choose_tma(SweepPlan<T>& pl) {
+    pl.tma = false;
+    const int k = pl.k;
+    if (k < 1) return;
+    const int xw = pow2_at_least(k + 96);
+    pl.xw = xw;
+    for (int tr : {32, 16}) {
+        const int nbox = (k + 255) / 256;
+        const int box_c = ((k + nbox - 1) / nbox + 7) / 8 * 8;
+        const int cols = box_c * nbox;
+        for (int s : {3, 2}) {
+            size_t bytes = 0;
+            if (tr == 32)
+                bytes = s == 3 ? tma_smem_bytes<T, 32, 3>(cols, xw) : tma_smem_bytes<T, 32, 2>(cols, xw);
+            else
+                bytes = s == 3 ? tma_smem_bytes<T, 16, 3>(cols, xw) : tma_smem_bytes<T, 16, 2>(cols, xw);
+            if (bytes <= 225 * 1024) {
+                pl.tma = true;
+                pl.tr = tr;
+                pl.stages = s;
+                pl.nbox = nbox;
+                pl.box_c = box_c;
+                pl.smem = bytes;
+                return;
+            }
+        }
+    }
+}
+
+template <class T>
+void plan_sweeps(SweepPlan<T>& pl, T* dinv_storage) {
+    choose_tma(pl);
+    if (!pl.tma) return;
+    const int tr = pl.tr;
+    pl.nch_max = (pl.st.m_max + tr - 1) / tr;
+    pl.dinv = dinv_storage;
+    // overlapping 3-D view: (row i, column c, block b) -> base + b*pstride + pad + k + c*2k + i
+    cuuint64_t dims[3] = {(cuuint64_t)pl.st.m_max, (cuuint64_t)pl.st.m_max, (cuuint64_t)pl.p};
+    cuuint64_t strides[2] = {(cuuint64_t)2 * pl.k * sizeof(T), (cuuint64_t)pl.st.pstride * sizeof(T)};
+    cuuint32_t box[3] = {(cuuint32_t)tr, (cuuint32_t)pl.box_c, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    void* base = const_cast<T*>(pl.f) + pl.st.pad + pl.k;
+    const CUresult rc = encode_fn()(&pl.map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                    3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (rc != CUDA_SUCCESS) {
+        pl.tma = false;
+        return;
+    }
+}
+template void plan_sweeps<double>(SweepPlan<double>&, double*);
+template void plan_sweeps<float>(SweepPlan<float>&, float*);
+
+template <class T>
+size_t sweep_dinv_elems(const SweepPlan<T>& pl) {
+    SweepPlan<T> tmp = pl;
+    choose_tma(tmp);
+    if (!tmp.tma) return 0;
+    const int nch_max = (pl.st.m_max + tmp.tr - 1) / tmp.tr;
+    return (size_t)pl.p * nch_max * 2 * tmp.tr * tmp.tr;
+}
+template size_t sweep_dinv_elems<double>(const SweepPlan<double>&);
+template size_t sweep_dinv_elems<float>(const SweepPlan<float>&);
+
+template <class T>
+void launch_chunk_inverses(const SweepPlan<T>& pl, cudaStream_t s) {
+    if (!pl.tma) return;
+    dim3 grid(pl.nch_max, pl.p);
+    if (pl.tr == 32)
+        k_chunk_inverses<T, 32><<<grid, 64, 0, s>>>(pl.f, pl.st.pstride, pl.st.pad, pl.offs, pl.k, pl.dinv, pl.nch_max);
+    else
+        k_chunk_inverses<T, 16><<<grid, 64, 0, s>>>(pl.f, pl.st.pstride, pl.st.pad, pl.offs, pl.k, pl.dinv, pl.nch_max);
     SAP_LAUNCHED();
 }
-template void launch_interfaces<double>(const double*, const int*, int, int, const double*, const double*,
-                                        const double*, const double*, const double*, double*, cudaStream_t);
-template void launch_interfaces<float>(const float*, const int*, int, int, const float*, const float*,
-                                       const float*, const float*, const float*, float*, cudaStream_t);
+template void launch_chunk_inverses<double>(const SweepPlan<double>&, cudaStream_t);
+template void launch_chunk_inverses<float>(const SweepPlan<float>&, cudaStream_t);
+
+template <class T, int TR, int S>
+static void run_tma(const SweepPlan<T>& pl, T* x, cudaStream_t s) {
+    auto kern = k_sweep_tma<T, TR, S>;
+    SAP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+    kern<<<pl.p, kSwThreads, pl.smem, s>>>(pl.map, pl.dinv, pl.nch_max, pl.offs, pl.k, x, pl.xw, pl.box_c * pl.nbox,
+                                           pl.box_c, pl.nbox);
+    SAP_LAUNCHED();
+}
+
+template <class T, int S>
+static bool try_ldgsts(const SweepPlan<T>& pl, T* x, cudaStream_t s) {
+    const int xw = pow2_at_least(pl.k + 64);
+    const size_t bytes = sizeof(T) * ((size_t)S * (pl.k + 32) * 32 + xw + kSwWarps * 33);
+    if (bytes > 200 * 1024) return false;
+    SAP_CUDA(cudaFuncSetAttribute(k_sweep_ldgsts<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    k_sweep_ldgsts<T, S><<<pl.p, kSwThreads, bytes, s>>>(pl.f, pl.st.pstride, pl.st.pad, pl.offs, pl.k, x, xw);
+    SAP_LAUNCHED();
+    return true;
+}
+
+template <class T>
+void launch_block_solve(const SweepPlan<T>& pl, T* x, cudaStream_t s) {
+    if (pl.p <= 0) return;
+    if (pl.tma) {
+        if (pl.tr == 32)
+            pl.stages == 3 ? run_tma<T, 32, 3>(pl, x, s) : run_tma<T, 32, 2>(pl, x, s);
+        else
+            pl.stages == 3 ? run_tma<T, 16, 3>(pl, x, s) : run_tma<T, 16, 2>(pl, x, s);
+        return;
+    }
+    if (try_ldgsts<T, 4>(pl, x, s)) return;
+    if (try_ldgsts<T, 3>(pl, x, s)) return;
+    if (try_ldgsts<T, 2>(pl, x, s)) return;
+    throw InvalidArgument("band solve: half-bandwidth too large for the shared-memory chunk ring");
+}
+template void launch_block_solve<double>(const SweepPlan<double>&, double*, cudaStream_t);
+template void launch_block_solve<float>(const SweepPlan<float>&, float*, cudaStream_t);
+
+// ---------------------------------------------------------------------------
+// SaP-C interface step (spike.hpp:323-347), split into wide GEMV kernels:
+//   pre   : XT[t] = g[e:e+w] - W^t_t g[e-w:e]
+//   solve : rbar_t XT[t] = ... (band sweep over the reduced blocks)
+//   post1 : XB[t] = g[e-w:e] - V^b_t XT[t];  b2[e-w:e] -= B_t XT[t]
+//   post2 : b2[e:e+w] -= C_t XB[t]
+// A warp owns one output row (lanes stride the row, fixed-order shuffle tree).
+template <class T>
+__device__ __forceinline__ T row_dot(const T* __restrict__ a, const T* __restrict__ v, int w, int lane) {
+    T acc = T(0);
+    for (int j = lane; j < w; j += 32) acc = fma(a[j], v[j], acc);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    return acc;
+}
+
+template <class T>
+__global__ void k_iface_pre(const T* __restrict__ g, const int* __restrict__ offs, int w, const T* __restrict__ wt,
+                            T* __restrict__ xt) {
+    const int t = blockIdx.y, lane = threadIdx.x & 31;
+    const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (i >= w) return;
+    const int e = offs[t + 1];
+    const T acc = row_dot(wt + ((size_t)t * w + i) * w, g + e - w, w, lane);
+    if (lane == 0) xt[(size_t)t * w + i] = g[e + i] - acc;
+}
+
+template <class T>
+__global__ void k_iface_post1(const T* __restrict__ g, const int* __restrict__ offs, int w, const T* __restrict__ vb,
+                              const T* __restrict__ bblk, const T* __restrict__ xt, T* __restrict__ xb,
+                              T* __restrict__ b2) {
+    const int t = blockIdx.y, lane = threadIdx.x & 31;
+    const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (i >= w) return;
+    const int e = offs[t + 1];
+    const T* v = xt + (size_t)t * w;
+    if (blockIdx.z == 0) {
+        const T acc = row_dot(vb + ((size_t)t * w + i) * w, v, w, lane);
+        if (lane == 0) xb[(size_t)t * w + i] = g[e - w + i] - acc;
+    } else {
+        const T acc = row_dot(bblk + ((size_t)t * w + i) * w, v, w, lane);
+        if (lane == 0) b2[e - w + i] -= acc;
+    }
+}
+
+template <class T>
+__global__ void k_iface_post2(const int* __restrict__ offs, int w, const T* __restrict__ cblk,
+                              const T* __restrict__ xb, T* __restrict__ b2) {
+    const int t = blockIdx.y, lane = threadIdx.x & 31;
+    const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (i >= w) return;
+    const int e = offs[t + 1];
+    const T acc = row_dot(cblk + ((size_t)t * w + i) * w, xb + (size_t)t * w, w, lane);
+    if (lane == 0) b2[e + i] -= acc;
+}
+
+template <class T>
+void launch_interfaces(const T* g, const int* d_offsets, const SweepPlan<T>& rplan, int p, int k, const T* wt,
+                       const T* vb, const T* bblk, const T* cblk, T* xt, T* xb, T* b2, cudaStream_t s) {
+    if (p < 2 || k == 0) return;
+    const int ni = p - 1, w = k;
+    dim3 grid(ceil_div(w, 8), ni);
+    k_iface_pre<T><<<grid, 256, 0, s>>>(g, d_offsets, w, wt, xt);
+    SAP_LAUNCHED();
+    launch_block_solve<T>(rplan, xt, s);
+    k_iface_post1<T><<<dim3(grid.x, ni, 2), 256, 0, s>>>(g, d_offsets, w, vb, bblk, xt, xb, b2);
+    SAP_LAUNCHED();
+    k_iface_post2<T><<<grid, 256, 0, s>>>(d_offsets, w, cblk, xb, b2);
+    SAP_LAUNCHED();
+}
+template void launch_interfaces<double>(const double*, const int*, const SweepPlan<double>&, int, int, const double*,
+                                        const double*, const double*, const double*, double*, double*, double*,
+                                        cudaStream_t);
+template void launch_interfaces<float>(const float*, const int*, const SweepPlan<float>&, int, int, const float*,
+                                       const float*, const float*, const float*, float*, float*, float*,
+                                       cudaStream_t);
 
 // ---------------------------------------------------------------------------
 // Diagonal preconditioner (build_precond_op's `diagonal` branch, pipeline.hpp:151-161).

@@ -53,6 +53,29 @@ struct FactorJob {
     int* boosts;      // device counter (written, not accumulated)
 };
 
+// Per-block strided band store used for every factor buffer (LU, UL, reduced
+// blocks): block b's tall-thin band (m_b*(2k+1) doubles in the reference's slot
+// layout) starts at base + b*pstride + pad. pad = k & 1 makes (block start + k)
+// 16-byte aligned, so every 32-row column segment (slot c*2k + i0 + k, i0 % 32 == 0)
+// is 16-byte aligned for TMA. Padding slots are zero.
+struct BandStore {
+    long long pstride = 0;
+    int pad = 0;
+    int m_max = 0;
+    int k = 0;
+    static BandStore make(int m_max, int k) {
+        BandStore b;
+        b.m_max = m_max;
+        b.k = k;
+        b.pad = k & 1;
+        long long need = (long long)m_max * (2LL * k + 1) + 64 + 2;
+        b.pstride = (need + 15) & ~15LL;
+        return b;
+    }
+    size_t total(int blocks) const { return (size_t)pstride * blocks; }
+    long long block(int b) const { return (long long)b * pstride + pad; }
+};
+
 constexpr int kWarp = 32;
 
 __device__ __forceinline__ double warp_sum(double v) {

@@ -33,75 +33,75 @@ long long g_launch_count = 0;
 
 // ---------------------------------------------------------------------------
 // Block infinity norms: row r of block b sums |A(off+r, off+c)| over in-block
-// columns c in ascending order (bitwise the reference's row loop). A warp
-// owns 32 consecutive rows and walks the union of their column ranges so
-// that for each column the 32 loads are contiguous (slot = c*2k + r + k).
-__global__ void k_block_norms(const double* __restrict__ a, int n, int k, const int* __restrict__ offs,
-                              double* __restrict__ norms) {
-    const int b = blockIdx.x;
+// columns c in ascending order (bitwise the reference's row loop,
+// block_factors.hpp:196-203). A warp owns 32 consecutive rows of one block and
+// walks the union of their column ranges so that, for each column, the 32
+// loads are one contiguous run (slot = c*2k + r + k). The per-block max is
+// order-independent: non-negative doubles compare like their bit patterns,
+// so atomicMax on the bits is exact; NaN rows are skipped like the
+// reference's `row > norm` test.
+__global__ void __launch_bounds__(256)
+    k_block_norms(const double* __restrict__ a, int k, const int* __restrict__ offs, long long pstride, int pad,
+                  unsigned long long* __restrict__ norms_bits) {
+    const int lane = threadIdx.x & 31;
+    const int b = blockIdx.y;
     const int off = offs[b], m = offs[b + 1] - off;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int r0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
+    if (r0 >= m) return;
     const long long ld = 2LL * k;
-    double best = 0.0;
-    for (int r0 = warp * 32; r0 < m; r0 += nw * 32) {
-        const int r = r0 + lane;
-        const int clo = max(r0 - k, 0), chi = min(r0 + 31 + k, m - 1);
-        double row = 0.0;
-        for (int c = clo; c <= chi; ++c) {
-            if (r < m && r - c <= k && c - r <= k) row += fabs(a[(long long)(off + c) * ld + (off + r) + k]);
-        }
-        if (r < m) best = fmax(best, row);
-    }
+    const double* base = a + (pstride > 0 ? (long long)b * pstride + pad : (long long)off * (2LL * k + 1));
+    const int r = r0 + lane;
+    const int clo = max(r0 - k, 0), chi = min(r0 + 31 + k, m - 1);
+    double row = 0.0;
+    const double* col = base + (long long)clo * ld + r + k;
+#pragma unroll 8
+    for (int c = clo; c <= chi; ++c, col += ld)
+        if (r < m && r - c <= k && c - r <= k) row += fabs(*col);
+    double best = (r < m && row > 0.0) ? row : 0.0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
-    __shared__ double red[32];
-    if (lane == 0) red[warp] = best;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double v = 0.0;
-        for (int w = 0; w < nw; ++w) v = fmax(v, red[w]);
-        norms[b] = v;
-    }
+    if (lane == 0 && best > 0.0) atomicMax(norms_bits + b, (unsigned long long)__double_as_longlong(best));
 }
 
-void launch_block_norms(const double* band, int n, int k, const int* d_offsets, int p, double* norms, cudaStream_t s) {
-    k_block_norms<<<p, 512, 0, s>>>(band, n, k, d_offsets, norms);
+void launch_block_norms(const double* band, int max_m, int k, const int* d_offsets, int p, const BandStore* store,
+                        double* norms, cudaStream_t s) {
+    SAP_CUDA(cudaMemsetAsync(norms, 0, sizeof(double) * p, s));
+    dim3 grid(ceil_div(ceil_div(max_m, 32), 8), p);
+    k_block_norms<<<grid, 256, 0, s>>>(band, k, d_offsets, store ? store->pstride : 0, store ? store->pad : 0,
+                                        reinterpret_cast<unsigned long long*>(norms));
     SAP_LAUNCHED();
 }
 
 // ---------------------------------------------------------------------------
-// Per-block band copies. Block b's band, stored at offsets[b]*(2k+1), has the
-// same slot index as the global band for every in-block entry, so the copy is
-// an elementwise masked copy of the whole array.
-__global__ void k_copy_blocks(const double* __restrict__ a, long long total, int k, int base, int rem,
-                              double* __restrict__ lu, double* __restrict__ ul) {
+// Block band copies into a BandStore: slot o of block b (o < m_b*(2k+1)) is
+// local column c = o / (2k+1), local row r = c - k + o % (2k+1); it takes the
+// global band's value when r lies inside the block and zero otherwise;
+// padding slots are zeroed.
+__global__ void k_copy_blocks(const double* __restrict__ a, int k, const int* __restrict__ offs, long long pstride,
+                              int pad, long long total, double* __restrict__ lu, double* __restrict__ ul) {
     const long long w = 2LL * k + 1;
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        const long long c = idx / w;
-        const long long row = c - k + (idx - c * w);
-        const long long big = (long long)rem * (base + 1);
-        long long b, lo, hi;
-        if (c < big) {
-            b = c / (base + 1);
-            lo = b * (base + 1);
-            hi = lo + base + 1;
-        } else {
-            b = rem + (c - big) / base;
-            lo = big + (b - rem) * base;
-            hi = lo + base;
+    for (long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x; d < total;
+         d += (long long)gridDim.x * blockDim.x) {
+        const int b = (int)(d / pstride);
+        const long long o = d - (long long)b * pstride - pad;
+        const int off = offs[b], m = offs[b + 1] - off;
+        double v = 0.0;
+        if (o >= 0 && o < (long long)m * w) {
+            const long long c = o / w;
+            const long long slot = o - c * w;
+            const long long r = c - k + slot;
+            if (r >= 0 && r < m) v = a[(off + c) * w + slot];
         }
-        const double v = (row >= lo && row < hi) ? a[idx] : 0.0;
-        lu[idx] = v;
-        if (ul) ul[idx] = v;
+        lu[d] = v;
+        if (ul) ul[d] = v;
     }
 }
 
-void launch_copy_blocks(const double* band, int n, int k, int p, double* lu, double* ul, cudaStream_t s) {
-    const long long total = (long long)n * (2LL * k + 1);
-    const int base = n / p, rem = n % p;
+void launch_copy_blocks(const double* band, int k, const int* d_offsets, int p, const BandStore& st, double* lu,
+                             double* ul, cudaStream_t s) {
+    const long long total = st.pstride * (long long)p;
     const int grid = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
-    k_copy_blocks<<<grid, 256, 0, s>>>(band, total, k, base, rem, lu, ul);
+    k_copy_blocks<<<grid, 256, 0, s>>>(band, k, d_offsets, st.pstride, st.pad, total, lu, ul);
     SAP_LAUNCHED();
 }
 

@@ -2,6 +2,7 @@
 // asynchronous; none synchronizes.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -11,9 +12,13 @@ namespace sapgpu {
 // ---- factorization (factor.cu) ----
 // Infinity norm of every diagonal block, restricted to in-block columns
 // (factor_blocks' boost scale, block_factors.hpp:187-195). p blocks, offsets on device.
-void launch_block_norms(const double* band, int n, int k, const int* d_offsets, int p, double* norms, cudaStream_t s);
-// LU (and UL) buffers = the band with every entry outside its diagonal block zeroed.
-void launch_copy_blocks(const double* band, int n, int k, int p, double* lu, double* ul, cudaStream_t s);
+// store == nullptr: `band` is one contiguous band (the A operator); otherwise the
+// blocks live in a BandStore.
+void launch_block_norms(const double* band, int max_m, int k, const int* d_offsets, int p, const BandStore* store,
+                        double* norms, cudaStream_t s);
+// LU (and UL) BandStores = each diagonal block's band, entries outside the block zeroed.
+void launch_copy_blocks(const double* band, int k, const int* d_offsets, int p, const BandStore& st, double* lu,
+                        double* ul, cudaStream_t s);
 // Blocked no-pivot LU with pivot boosting of every job (one CTA per job).
 void launch_band_lu(const FactorJob* d_jobs, int njobs, int max_k, double boost_eps, cudaStream_t s);
 // Row-sum infinity norms of ni dense row-major w x w blocks and a non-finite flag per block.
@@ -23,20 +28,45 @@ void launch_dense_norms(const double* a, int w, int ni, double* norms, int* nonf
 void launch_extract_coupling(const double* band, int n, int k, const int* d_offsets, int p, double* bblk,
                              double* cblk, cudaStream_t s);
 // v_bottom / w_top tips from the LU / UL corners; nonfinite[2t] (V) / [2t+1] (W).
-void launch_spike_tips(const double* lu, const double* ul, const int* d_offsets, int p, int k, const double* bblk,
-                       const double* cblk, double* vb, double* wt, int* nonfinite, cudaStream_t s);
-// rbar[t] = I - wt[t] * vb[t] (row-major w x w).
-void launch_rbar(const double* wt, const double* vb, int w, int ni, double* rbar, cudaStream_t s);
+void launch_spike_tips(const double* lu, const double* ul, const BandStore& st, const int* d_offsets, int p, int k,
+                       const double* bblk, const double* cblk, double* vb, double* wt, int* nonfinite, cudaStream_t s);
+// rbar[t] = I - wt[t] * vb[t], written in band layout (k = w-1) of the block-diagonal
+// matrix diag(rbar_0, ..., rbar_{ni-1}); nonfinite[t] flags a non-finite block.
+void launch_rbar(const double* wt, const double* vb, int w, int ni, double* rbar_band, const BandStore& rst,
+                 int* nonfinite, cudaStream_t s);
 
 // ---- preconditioner apply (apply.cu) ----
-// x <- D^{-1} x per partition with the LU factors (band_lu_solve, block_factors.hpp:74-90).
+// Everything a block sweep needs, built once at setup: the factor BandStore,
+// its overlapping 3-D TMA view and the per-chunk diagonal inverses.
 template <class T>
-void launch_block_solve(const T* lu, const int* d_offsets, int p, int k, T* x, cudaStream_t s);
+struct SweepPlan {
+    const T* f = nullptr;       // BandStore base (LU factors)
+    BandStore st;
+    const int* offs = nullptr;  // device block offsets (p+1)
+    int p = 0, k = 0;
+    bool tma = false;
+    int tr = 32, stages = 3, nbox = 1, box_c = 0, xw = 0, nch_max = 0;
+    size_t smem = 0;
+    T* dinv = nullptr;          // [p][nch_max][2][tr*tr] chunk inverses
+    CUtensorMap map;
+};
+// Elements of chunk-inverse storage the plan needs (0 when the TMA path is not used).
+template <class T>
+size_t sweep_dinv_elems(const SweepPlan<T>& pl);
+// Chooses the sweep kernel and encodes the tensor map (pl.f/st/offs/p/k set by the caller).
+template <class T>
+void plan_sweeps(SweepPlan<T>& pl, T* dinv_storage);
+template <class T>
+void launch_chunk_inverses(const SweepPlan<T>& pl, cudaStream_t s);
+// x <- D^{-1} x per block with the LU factors (band_lu_solve, block_factors.hpp:74-90).
+template <class T>
+void launch_block_solve(const SweepPlan<T>& pl, T* x, cudaStream_t s);
 // SaP-C interface step (apply_preconditioner, spike.hpp:323-347): from g (= D^{-1} b) form
-// x^t, x^b per interface and subtract the coupling terms from b2 (which holds b).
+// x^t (xt), x^b (xb) per interface and subtract the coupling terms from b2 (which holds b).
+// rbar_band: the reduced blocks' LU in band layout (k = w-1), blocks at d_roffsets (t*w).
 template <class T>
-void launch_interfaces(const T* g, const int* d_offsets, int p, int k, const T* wt, const T* vb, const T* rbar,
-                       const T* bblk, const T* cblk, T* b2, cudaStream_t s);
+void launch_interfaces(const T* g, const int* d_offsets, const SweepPlan<T>& rplan, int p, int k, const T* wt,
+                       const T* vb, const T* bblk, const T* cblk, T* xt, T* xb, T* b2, cudaStream_t s);
 void launch_diag_apply(const double* in, const double* diag, double* out, int n, cudaStream_t s);
 void launch_boosted_diag(const double* band, int n, int k, const double* scale, double boost_eps, double* diag,
                          cudaStream_t s);

@@ -46,7 +46,8 @@ constexpr int kTipThreads = 256;
 
 // grid: (column chunks, 2 tips, p-1 interfaces). X is w x kTipCols row-major in smem.
 __global__ void __launch_bounds__(kTipThreads)
-    k_spike_tips(const double* __restrict__ lu, const double* __restrict__ ul, const int* __restrict__ offs, int k,
+    k_spike_tips(const double* __restrict__ lu, const double* __restrict__ ul, long long pstride, int pad,
+                 const int* __restrict__ offs, int k,
                  const double* __restrict__ bblk, const double* __restrict__ cblk, double* __restrict__ vb,
                  double* __restrict__ wt, int* __restrict__ nonfinite) {
     extern __shared__ double sm[];
@@ -59,11 +60,11 @@ __global__ void __launch_bounds__(kTipThreads)
     const double* f;
     int corner;  // first global row/col of the corner inside the block band
     if (which == 0) {
-        const int off = offs[t], m = offs[t + 1] - off;
-        f = lu + (long long)off * (2 * k + 1);
+        const int m = offs[t + 1] - offs[t];
+        f = lu + (long long)t * pstride + pad;
         corner = m - w;
     } else {
-        f = ul + (long long)offs[t + 1] * (2 * k + 1);
+        f = ul + (long long)(t + 1) * pstride + pad;
         corner = 0;
     }
     const double* rhs = (which == 0 ? bblk : cblk) + (long long)t * w * w;
@@ -137,14 +138,15 @@ __global__ void __launch_bounds__(kTipThreads)
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite + 2 * t + which, 1);
 }
 
-void launch_spike_tips(const double* lu, const double* ul, const int* d_offsets, int p, int k, const double* bblk,
-                       const double* cblk, double* vb, double* wt, int* nonfinite, cudaStream_t s) {
+void launch_spike_tips(const double* lu, const double* ul, const BandStore& st, const int* d_offsets, int p, int k,
+                       const double* bblk, const double* cblk, double* vb, double* wt, int* nonfinite, cudaStream_t s) {
     if (p < 2 || k == 0) return;
     const size_t bytes = sizeof(double) * ((size_t)k * kTipCols + k);
     if (bytes > 227 * 1024) throw InvalidArgument("spike tips: half-bandwidth too large");
     SAP_CUDA(cudaFuncSetAttribute(k_spike_tips, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     dim3 grid(ceil_div(k, kTipCols), 2, p - 1);
-    k_spike_tips<<<grid, kTipThreads, bytes, s>>>(lu, ul, d_offsets, k, bblk, cblk, vb, wt, nonfinite);
+    k_spike_tips<<<grid, kTipThreads, bytes, s>>>(lu, ul, st.pstride, st.pad, d_offsets, k, bblk, cblk, vb, wt,
+                                                   nonfinite);
     SAP_LAUNCHED();
 }
 
@@ -152,7 +154,7 @@ void launch_spike_tips(const double* lu, const double* ul, const int* d_offsets,
 // rbar[t] = I - wt[t] vb[t]; each element accumulates l ascending (FMA) as
 // finish_reduced_blocks does (spike.hpp:154-160). 32x32 output tile per CTA.
 __global__ void k_rbar(const double* __restrict__ wt, const double* __restrict__ vb, int w,
-                       double* __restrict__ rbar) {
+                       double* __restrict__ rbar, long long rpstride, int rpad, int* __restrict__ nonfinite) {
     __shared__ double As[32][33];
     __shared__ double Bs[32][33];
     const int t = blockIdx.z;
@@ -176,16 +178,24 @@ __global__ void k_rbar(const double* __restrict__ wt, const double* __restrict__
         }
         __syncthreads();
     }
+    int bad = 0;
+    const long long bw = 2LL * w - 1;  // band width of the k = w-1 layout
     for (int q = 0; q < 4; ++q) {
         const int i = i0 + ty + 8 * q, j = j0 + tx;
-        if (i < w && j < w) rbar[(long long)t * w * w + (long long)i * w + j] = (i == j ? 1.0 : 0.0) - acc[q];
+        if (i < w && j < w) {
+            const double v = (i == j ? 1.0 : 0.0) - acc[q];
+            if (!isfinite(v)) bad = 1;
+            rbar[(long long)t * rpstride + rpad + (long long)j * bw + (i - j + w - 1)] = v;
+        }
     }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite + t, 1);
 }
 
-void launch_rbar(const double* wt, const double* vb, int w, int ni, double* rbar, cudaStream_t s) {
+void launch_rbar(const double* wt, const double* vb, int w, int ni, double* rbar, const BandStore& rst,
+                 int* nonfinite, cudaStream_t s) {
     if (ni <= 0 || w == 0) return;
     dim3 grid(ceil_div(w, 32), ceil_div(w, 32), ni);
-    k_rbar<<<grid, 256, 0, s>>>(wt, vb, w, rbar);
+    k_rbar<<<grid, 256, 0, s>>>(wt, vb, w, rbar, rst.pstride, rst.pad, nonfinite);
     SAP_LAUNCHED();
 }
 
