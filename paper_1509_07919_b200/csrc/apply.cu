@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
     k_sweep_ldgsts(const T* __restrict__ f0, long long pstride, int pad, const int* __restrict__ offs, int k,
                    T* __restrict__ xbase, int xw) {
     constexpr int TR = 32;
-    extern __shared__ __align__(16) unsigned char smraw[];
+    extern __shared__ __align__(128) unsigned char smraw[];
     const int ncol = k + TR;
     T* ring = reinterpret_cast<T*>(smraw);
     T* xs = ring + (size_t)S * ncol * TR;

@@ -23,6 +23,7 @@
 // 320 KB at K = 200, so 100 concurrent factorizations keep ~32 MB hot in the
 // 126 MB L2 while the band itself is read from and written to HBM once.
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -266,6 +267,8 @@ static void launch_lu_b(const FactorJob* jobs, int njobs, int max_k, double eps,
 
 void launch_band_lu(const FactorJob* d_jobs, int njobs, int max_k, double boost_eps, cudaStream_t s) {
     if (njobs <= 0) return;
+    static const bool simple = getenv("SAP_LU_SIMPLE") != nullptr;
+    if (!simple && launch_band_lu_ws(d_jobs, njobs, max_k, boost_eps, s)) return;
     if (max_k >= 48 && max_k <= 360)
         launch_lu_b<32>(d_jobs, njobs, max_k, boost_eps, s);
     else if (max_k > 360 && max_k <= 820)

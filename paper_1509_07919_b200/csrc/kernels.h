@@ -21,6 +21,8 @@ void launch_copy_blocks(const double* band, int k, const int* d_offsets, int p, 
                         double* ul, cudaStream_t s);
 // Blocked no-pivot LU with pivot boosting of every job (one CTA per job).
 void launch_band_lu(const FactorJob* d_jobs, int njobs, int max_k, double boost_eps, cudaStream_t s);
+// The warp-specialized look-ahead variant (lu.cu); false if the smem budget does not fit.
+bool launch_band_lu_ws(const FactorJob* d_jobs, int njobs, int max_k, double boost_eps, cudaStream_t s);
 // Row-sum infinity norms of ni dense row-major w x w blocks and a non-finite flag per block.
 void launch_dense_norms(const double* a, int w, int ni, double* norms, int* nonfinite, cudaStream_t s);
 

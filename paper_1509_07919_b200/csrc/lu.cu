@@ -1,0 +1,515 @@
+// Warp-specialized, look-ahead blocked band LU (the hot loop of factor_blocks).
+//
+// Reference: band_lu_inplace / band_ul_inplace, proj/include/sap/block_factors.hpp:22-71;
+// dense_lu_nopivot_boosted, proj/include/sap/spike.hpp:20-45 (same strided job
+// views as factor.cu: LU, UL on the flipped system, and the reduced blocks).
+//
+// Panel width B (<= 32, from the smem budget). Step s owns panel columns
+// [jb, jb+nb); A22 = the R x R trailing window at (jb+nb, jb+nb), R = min(K, m-jb-nb).
+// The CTA's 16 warps split into
+//   PG, warps 0-3  : factor panel s+1 (one named barrier per column) and form
+//                    U12(s+1) = L11^{-1} A12 (right-looking, reference order);
+//   UG, warps 4-15 : the bulk of step s's trailing update A22 -= L21 U12 on
+//                    FP64 tensor cores (mma.sync m8n8k4 -> DMMA.8x8x4), A22
+//                    streamed through L2, the top rows (U12(s+1)'s) first.
+// Look-ahead: before the split, all 16 warps apply step s's update to the
+// next panel's columns straight into the next panel's smem buffer, so panel
+// s+1's factorization overlaps step s's bulk update. Panel and U12 buffers are
+// double-buffered. Every element still receives its rank-1 updates in the
+// reference's column order (DMMA / DFMA contract mul+sub).
+#include <cstdint>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace sapgpu {
+
+namespace {
+
+constexpr int kLuThreads = 512;
+constexpr int kPgWarps = 8;
+constexpr int kUgWarps = 8;
+constexpr int kPgThreads = kPgWarps * 32;
+constexpr int kBarPg = 1;   // named barrier: panel group (256 threads)
+constexpr int kBarTop = 2;  // named barrier: UG top rows done -> PG (512 threads)
+
+__device__ __forceinline__ void named_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(a), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+struct Lu {
+    double* base;
+    long long rs, cs;
+    int m, K, B, pld, uld;
+    double bv;
+    __device__ __forceinline__ double* at(int i, int c) const { return base + (long long)i * rs + (long long)c * cs; }
+    __device__ __forceinline__ bool inband(int i, int c) const { return i - c <= K && c - i <= K; }
+};
+
+// C -= L21 * U12 over A22 tiles rows [r_lo, r_hi) x cols [c_lo, c_hi) (A22 coordinates, origin (ja, ja)).
+// Warp tiles are 16 x 32, enumerated row-major; this warp takes every nw-th from widx.
+// The MMA computes the transposed tile C^T -= U12^T L21^T (m8n8k4 row.col:
+// A' = U12^T fragment, B' = -L21^T fragment) so that each thread's two
+// accumulator elements are rows (i, i+1) of one column: adjacent in the
+// tall-thin band (|rs| == 1), moved with one 16-byte access when aligned.
+// Tiles are software-pipelined: the next tile's accumulators load while the
+// current tile computes. Pn != nullptr: results go to the next panel buffer.
+struct TileCtx {
+    int r_lo, r_hi, c_lo, c_hi, tcols, ja;
+};
+constexpr int kTileR = 16, kTileC = 32;  // warp tile: 2 x 4 DMMA tiles
+constexpr int kTQ = kTileC / 8;
+
+__device__ __forceinline__ void tile_load(const Lu& L, const TileCtx& T, int t, double (&acc)[2][kTQ][2]) {
+    const int lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
+    const int row0 = T.r_lo + (t / T.tcols) * kTileR, col0 = T.c_lo + (t % T.tcols) * kTileC;
+    const int ib = row0 + 2 * lc, cb = col0 + lr;
+    const long long rs = L.rs, ra8 = 8 * rs, cq8 = 8 * L.cs;
+    const double* p00 = L.at(T.ja + ib, T.ja + cb);
+    const double* lo00 = rs > 0 ? p00 : p00 - 1;
+    const bool full = row0 + kTileR <= T.r_hi && col0 + kTileC <= T.c_hi;
+    if (full && (rs == 1 || rs == -1) && ((reinterpret_cast<uintptr_t>(lo00) & 15) == 0)) {
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int q = 0; q < kTQ; ++q) {
+                const double2 v = __ldcg(reinterpret_cast<const double2*>(lo00 + a * ra8 + q * cq8));
+                acc[a][q][0] = rs > 0 ? v.x : v.y;
+                acc[a][q][1] = rs > 0 ? v.y : v.x;
+            }
+    } else {
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int q = 0; q < kTQ; ++q)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int i = ib + a * 8 + e, c = cb + q * 8;
+                    acc[a][q][e] = (i < T.r_hi && c < T.c_hi) ? __ldcg(p00 + a * ra8 + e * rs + q * cq8) : 0.0;
+                }
+    }
+}
+
+__device__ __forceinline__ void tile_compute_store(const Lu& L, const TileCtx& T, int t, double (&acc)[2][kTQ][2],
+                                                   const double* __restrict__ P, const double* __restrict__ U, int nb,
+                                                   double* Pn) {
+    const int lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
+    const int row0 = T.r_lo + (t / T.tcols) * kTileR, col0 = T.c_lo + (t % T.tcols) * kTileC;
+    const int ib = row0 + 2 * lc, cb = col0 + lr;
+    const int pld = L.pld, uld = L.uld;
+    const int ksteps = (nb + 3) >> 2;
+    const bool a1 = row0 + 8 < T.r_hi;
+    bool qv[kTQ];
+#pragma unroll
+    for (int q = 0; q < kTQ; ++q) qv[q] = col0 + q * 8 < T.c_hi;
+    const double* pk = P + nb + row0 + lr;
+    const double* uk = U + col0 + lr;
+    for (int ks = 0; ks < ksteps; ++ks) {
+        const int kk = ks * 4 + lc;
+        const double b0 = -pk[kk * pld];
+        const double b1 = -pk[kk * pld + 8];
+#pragma unroll
+        for (int q = 0; q < kTQ; ++q) {
+            if (qv[q]) {
+                const double aq = uk[kk * uld + q * 8];
+                dmma_m8n8k4(acc[0][q][0], acc[0][q][1], aq, b0, acc[0][q][0], acc[0][q][1]);
+                if (a1) dmma_m8n8k4(acc[1][q][0], acc[1][q][1], aq, b1, acc[1][q][0], acc[1][q][1]);
+            }
+        }
+    }
+    if (Pn) {
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int q = 0; q < kTQ; ++q)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int i = ib + a * 8 + e, c = cb + q * 8;
+                    if (i < T.r_hi && c < T.c_hi) Pn[c * pld + i] = acc[a][q][e];
+                }
+        return;
+    }
+    const long long rs = L.rs, ra8 = 8 * rs, cq8 = 8 * L.cs;
+    double* p00 = L.at(T.ja + ib, T.ja + cb);
+    double* lo00 = rs > 0 ? p00 : p00 - 1;
+    const bool full = row0 + kTileR <= T.r_hi && col0 + kTileC <= T.c_hi;
+    if (full && (rs == 1 || rs == -1) && ((reinterpret_cast<uintptr_t>(lo00) & 15) == 0)) {
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int q = 0; q < kTQ; ++q) {
+                double2 v;
+                v.x = rs > 0 ? acc[a][q][0] : acc[a][q][1];
+                v.y = rs > 0 ? acc[a][q][1] : acc[a][q][0];
+                __stcg(reinterpret_cast<double2*>(lo00 + a * ra8 + q * cq8), v);
+            }
+    } else {
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int q = 0; q < kTQ; ++q)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int i = ib + a * 8 + e, c = cb + q * 8;
+                    if (i < T.r_hi && c < T.c_hi) __stcg(p00 + a * ra8 + e * rs + q * cq8, acc[a][q][e]);
+                }
+    }
+}
+
+__device__ __noinline__ void dmma_region(const Lu& L, const double* __restrict__ P, const double* __restrict__ U,
+                                         int nb, int ja, int r_lo, int r_hi, int c_lo, int c_hi, int widx, int nw,
+                                         double* Pn) {
+    if (r_lo >= r_hi || c_lo >= c_hi) return;
+    TileCtx T{r_lo, r_hi, c_lo, c_hi, (c_hi - c_lo + kTileC - 1) / kTileC, ja};
+    const int ntiles = ((r_hi - r_lo + kTileR - 1) / kTileR) * T.tcols;
+    double A[2][kTQ][2];
+    for (int t = widx; t < ntiles; t += nw) {
+        tile_load(L, T, t, A);
+        tile_compute_store(L, T, t, A, P, U, nb, Pn);
+    }
+}
+
+// Panel group: stage the parts of panel (jp, np) that phase (a) did not
+// produce (rows >= ra or columns >= ca), zero everything outside the band.
+__device__ __forceinline__ void pg_stage_panel(const Lu& L, double* Pn, int jp, int np, int ph, int ra, int ca,
+                                               int ptid) {
+    const int pld = L.pld;
+    for (int r = ptid; r < pld; r += kPgThreads)
+        for (int c = 0; c < L.B; ++c) {
+            if (c < np && r < ph && r < ra && c < ca) continue;  // written by phase (a)
+            if (c < np && r < ph && L.inband(r, c))
+                cp_async8(Pn + c * pld + r, L.at(jp + r, jp + c));
+            else
+                Pn[c * pld + r] = 0.0;
+        }
+    cp_async_wait_all();
+}
+
+// Panel group: unblocked factorization of the staged panel. Thread ptid owns
+// panel row ptid (ph <= kPgThreads) in registers; per column the pivot row's
+// owner publishes it (double-buffered) and one named barrier follows.
+// Panel group: unblocked factorization of the staged panel. Thread ptid owns
+// panel row ptid (ph <= kPgThreads; its entries Pn[c*pld + ptid] are private
+// to it, conflict-free). Per column the pivot row's owner publishes it with
+// the reciprocal of the (boosted) pivot, double buffered, then one named
+// barrier; multipliers are l = a * (1/p).
+// Panel group: unblocked factorization of the staged panel. Thread ptid owns
+// panel row ptid (ph <= kPgThreads) in REGISTERS (compile-time column
+// indices). Per column the owner of the pivot row boosts the pivot
+// (block_factors.hpp:26-34) and publishes 1/p and the row's remaining entries
+// (double-buffered smem), right after updating that row so the division
+// overlaps the other rows' work; one named barrier per column; l = a * (1/p).
+template <int B, int C>
+__device__ __forceinline__ double pg_recip(const Lu& L, double (&row)[B], int* boost_ctr) {
+    double p = row[C];
+    if (fabs(p) < L.bv) {
+        p = p < 0.0 ? -L.bv : L.bv;
+        row[C] = p;
+        atomicAdd(boost_ctr, 1);
+    }
+    return 1.0 / p;
+}
+
+template <int B, int C>
+__device__ __forceinline__ void pg_pub(const double (&row)[B], double rcp, double* __restrict__ prow) {
+    double* __restrict__ pr = prow + (C & 1) * (B + 1);
+    pr[C] = rcp;
+#pragma unroll
+    for (int cc = C + 1; cc < B; ++cc) pr[cc] = row[cc];
+}
+
+template <int B, int C>
+__device__ __forceinline__ void pg_col(const Lu& L, double (&row)[B], double* __restrict__ prow, int* boost_ctr,
+                                       int np, int ph, int ptid) {
+    if constexpr (C < B) {
+        if (C < np) {
+            named_sync(kBarPg, kPgThreads);
+            const double* __restrict__ pr = prow + (C & 1) * (B + 1);
+            if (ptid > C && ptid < ph) {
+                const double l = row[C] * pr[C];
+                row[C] = l;
+                if constexpr (C + 1 < B) {
+                    row[C + 1] = fma(-l, pr[C + 1], row[C + 1]);
+                    // the next pivot's owner starts its division now; its row is published
+                    // only after the whole update of this column
+                    const bool owner = ptid == C + 1 && C + 1 < np;
+                    double rcp = 0.0;
+                    if (owner) rcp = pg_recip<B, C + 1>(L, row, boost_ctr);
+#pragma unroll
+                    for (int cc = C + 2; cc < B; ++cc) row[cc] = fma(-l, pr[cc], row[cc]);
+                    if (owner) pg_pub<B, C + 1>(row, rcp, prow);
+                }
+            }
+            pg_col<B, C + 1>(L, row, prow, boost_ctr, np, ph, ptid);
+        }
+    }
+}
+
+template <int B>
+__device__ __noinline__ void pg_factor_panel(const Lu& L, double* __restrict__ Pn, double* __restrict__ prow,
+                                             int* boost_ctr, int np, int ph, int ptid) {
+    const int pld = L.pld;
+    double row[B];
+#pragma unroll
+    for (int c = 0; c < B; ++c) row[c] = ptid < ph ? Pn[c * pld + ptid] : 0.0;
+    if (ptid == 0 && np > 0) pg_pub<B, 0>(row, pg_recip<B, 0>(L, row, boost_ctr), prow);
+    pg_col<B, 0>(L, row, prow, boost_ctr, np, ph, ptid);
+    if (ptid < ph) {
+#pragma unroll
+        for (int c = 0; c < B; ++c) Pn[c * pld + ptid] = row[c];
+    }
+    named_sync(kBarPg, kPgThreads);
+}
+
+__device__ __forceinline__ void pg_store_panel(const Lu& L, const double* Pn, int jp, int np, int ph, int ptid) {
+    const int pld = L.pld;
+    for (int r = ptid; r < ph; r += kPgThreads)
+        for (int c = 0; c < np; ++c)
+            if (L.inband(r, c)) __stcg(L.at(jp + r, jp + c), Pn[c * pld + r]);
+}
+
+// Panel group: U12 of panel (jp, np): rows [0, np) x cols [0, Rn) at (jp, jp+np),
+// staged from global, solved with the panel's unit-lower L11 (thread = column,
+// register accumulators; element (r, c) receives j = 0..r-1 in order as in
+// block_factors.hpp:246-250), written back.
+template <int B>
+__device__ __noinline__ void pg_u12(const Lu& L, const double* __restrict__ Pn, double* __restrict__ Un, int jp, int np,
+                                    int Rn, int ptid) {
+    constexpr int H = 8;
+    static_assert(B % H == 0, "B must be a multiple of 8");
+    const int pld = L.pld, uld = L.uld;
+    for (int idx = ptid; idx < 32 * uld; idx += kPgThreads) {
+        const int r = idx & 31, c = idx >> 5;  // lanes walk a column: contiguous in the band
+        if (r >= B) continue;
+        if (r < np && c < Rn && np + c - r <= L.K)
+            cp_async8(Un + r * uld + c, L.at(jp + r, jp + np + c));
+        else
+            Un[r * uld + c] = 0.0;
+    }
+    cp_async_wait_all();
+    named_sync(kBarPg, kPgThreads);
+    // element (r, c) receives j = 0..r-1 in ascending order (block_factors.hpp:246-250);
+    // rows in blocks of H: contributions of the solved rows above, then the block's own triangle
+    for (int c = ptid; c < Rn; c += kPgThreads) {
+#pragma unroll 1
+        for (int b0 = 0; b0 < B; b0 += H) {
+            double x[H];
+#pragma unroll
+            for (int r = 0; r < H; ++r) x[r] = Un[(b0 + r) * uld + c];
+#pragma unroll 4
+            for (int j = 0; j < b0; ++j) {
+                const double uj = Un[j * uld + c];
+                const double* __restrict__ lj = Pn + j * pld + b0;
+#pragma unroll
+                for (int r = 0; r < H; ++r) x[r] = fma(-lj[r], uj, x[r]);
+            }
+#pragma unroll
+            for (int j = 0; j + 1 < H; ++j) {
+                const double* __restrict__ lj = Pn + (b0 + j) * pld + b0;
+#pragma unroll
+                for (int r = j + 1; r < H; ++r) x[r] = fma(-lj[r], x[j], x[r]);
+            }
+#pragma unroll
+            for (int r = 0; r < H; ++r) Un[(b0 + r) * uld + c] = x[r];
+        }
+    }
+    named_sync(kBarPg, kPgThreads);
+    for (int idx = ptid; idx < 32 * Rn; idx += kPgThreads) {
+        const int r = idx & 31, c = idx >> 5;
+        if (r < np && np + c - r <= L.K) __stcg(L.at(jp + r, jp + np + c), Un[r * uld + c]);
+    }
+}
+
+}  // namespace
+
+// Optional phase trace (build with -DSAP_LU_TRACE): CTA 0 records clock64 at
+// phase boundaries for the first kTraceSteps steps (PG thread 0, UG warp 4 lane 0).
+constexpr int kTraceSteps = 16;
+constexpr int kTraceSlots = 12;
+__device__ long long g_lu_trace[kTraceSteps * kTraceSlots];
+#ifdef SAP_LU_TRACE
+#define LU_TRACE(step, slot, cond)                                                        \
+    do {                                                                                  \
+        if (blockIdx.x == 0 && (cond) && (step) < kTraceSteps) g_lu_trace[(step)*kTraceSlots + (slot)] = clock64(); \
+    } while (0)
+#else
+#define LU_TRACE(step, slot, cond) do { } while (0)
+#endif
+
+template <int B>
+__global__ void __launch_bounds__(kLuThreads, 1)
+    k_band_lu_ws(const FactorJob* __restrict__ jobs, double eps, int pld, int uld) {
+    extern __shared__ __align__(16) double smem[];
+    __shared__ int s_boosts;
+    __shared__ double s_prow[2 * (B + 1)];
+    const FactorJob J = jobs[blockIdx.x];
+    const double scale = *J.scale;
+    Lu L{J.base, J.rs, J.cs, J.m, J.k, B, pld, uld, eps * (scale > 0 ? scale : 1.0)};
+    const int psz = B * pld, usz = B * uld;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const bool pg = warp < kPgWarps;
+    const int ptid = tid;  // valid for PG threads (0..127)
+    const int m = L.m, K = L.K;
+    if (tid == 0) s_boosts = 0;
+    __syncthreads();
+
+    // ---- prologue: panel 0 and U12(0) ----
+    {
+        const int nb = min(B, m), ph = min(nb + K, m), R = min(K, m - nb);
+        if (pg) {
+            pg_stage_panel(L, smem, 0, nb, ph, 0, 0, ptid);
+            named_sync(kBarPg, kPgThreads);
+            pg_factor_panel<B>(L, smem, s_prow, &s_boosts, nb, ph, ptid);
+            pg_store_panel(L, smem, 0, nb, ph, ptid);
+            pg_u12<B>(L, smem, smem + 2 * psz, 0, nb, R, ptid);
+        }
+    }
+    int cur = 0;
+    int step = 0;
+    for (int jb = 0; jb < m; jb += B, ++step) {
+        __syncthreads();  // S0: panel s and U12(s) complete (smem and global)
+        LU_TRACE(step, 0, tid == 0);
+        const int nb = min(B, m - jb);
+        const int ja = jb + nb;               // A22 origin
+        const int R = min(K, m - ja);         // A22 order
+        const bool has_next = ja < m;
+        const int nbn = has_next ? min(B, m - ja) : 0;
+        const int phn = has_next ? min(nbn + K, m - ja) : 0;
+        const int Rn = has_next ? min(K, m - ja - nbn) : 0;
+        const int ca = min(nbn, R);           // next-panel columns inside A22
+        const double* P = smem + cur * psz;
+        const double* U = smem + 2 * psz + cur * usz;
+        double* Pn = smem + (cur ^ 1) * psz;
+        double* Un = smem + 2 * psz + (cur ^ 1) * usz;
+        // ---- phase (a): all warps update the next panel's columns into Pn ----
+        if (has_next) dmma_region(L, P, U, nb, ja, 0, R, 0, ca, warp, kLuThreads / 32, Pn);
+        __syncthreads();  // S1
+        LU_TRACE(step, 1, tid == 0);
+        if (pg) {
+            if (has_next) {
+                pg_stage_panel(L, Pn, ja, nbn, phn, R, ca, ptid);
+                named_sync(kBarPg, kPgThreads);
+                LU_TRACE(step, 2, tid == 0);
+                pg_factor_panel<B>(L, Pn, s_prow, &s_boosts, nbn, phn, ptid);
+                LU_TRACE(step, 3, tid == 0);
+                pg_store_panel(L, Pn, ja, nbn, phn, ptid);
+                LU_TRACE(step, 4, tid == 0);
+                named_sync(kBarTop, kLuThreads);  // UG has written A22's top rows (U12(s+1) sources)
+                LU_TRACE(step, 5, tid == 0);
+                pg_u12<B>(L, Pn, Un, ja, nbn, Rn, ptid);
+                LU_TRACE(step, 6, tid == 0);
+            }
+        } else {
+            const int uw = warp - kPgWarps;
+            const int top = has_next ? min(R, ((nbn + 15) >> 4) << 4) : 0;
+            dmma_region(L, P, U, nb, ja, 0, top, ca, R, uw, kUgWarps, nullptr);
+            LU_TRACE(step, 7, tid == kPgThreads);
+            if (has_next) {
+                __threadfence_block();
+                named_arrive(kBarTop, kLuThreads);
+            }
+            dmma_region(L, P, U, nb, ja, top, R, ca, R, uw, kUgWarps, nullptr);
+            LU_TRACE(step, 8, tid == kPgThreads);
+            LU_TRACE(step, 9, tid == kLuThreads - 32);
+        }
+        cur ^= 1;
+    }
+    __syncthreads();
+    if (tid == 0) *J.boosts = s_boosts;
+}
+
+// All warps in every phase (no specialization): stage -> factor panel ->
+// U12 -> DMMA trailing update, one panel at a time. Panel rows are owned by
+// threads 0..kPgThreads-1; the DMMA update uses all 16 warps.
+template <int B>
+__global__ void __launch_bounds__(kLuThreads, 1)
+    k_band_lu_seq(const FactorJob* __restrict__ jobs, double eps, int pld, int uld) {
+    extern __shared__ __align__(16) double smem[];
+    __shared__ int s_boosts;
+    __shared__ double s_prow[2 * (B + 1)];
+    const FactorJob J = jobs[blockIdx.x];
+    const double scale = *J.scale;
+    Lu L{J.base, J.rs, J.cs, J.m, J.k, B, pld, uld, eps * (scale > 0 ? scale : 1.0)};
+    double* P = smem;
+    double* U = smem + B * pld;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const bool pg = tid < kPgThreads;
+    const int m = L.m, K = L.K;
+    if (tid == 0) s_boosts = 0;
+    __syncthreads();
+    int step = 0;
+    for (int jb = 0; jb < m; jb += B, ++step) {
+        const int nb = min(B, m - jb);
+        const int ph = min(nb + K, m - jb);
+        const int ja = jb + nb;
+        const int R = min(K, m - ja);
+        LU_TRACE(step, 0, tid == 0);
+        if (pg) {
+            pg_stage_panel(L, P, jb, nb, ph, 0, 0, tid);
+            named_sync(kBarPg, kPgThreads);
+            LU_TRACE(step, 2, tid == 0);
+            pg_factor_panel<B>(L, P, s_prow, &s_boosts, nb, ph, tid);
+            LU_TRACE(step, 3, tid == 0);
+            pg_store_panel(L, P, jb, nb, ph, tid);
+            LU_TRACE(step, 4, tid == 0);
+            pg_u12<B>(L, P, U, jb, nb, R, tid);
+            LU_TRACE(step, 6, tid == 0);
+        }
+        __syncthreads();
+        LU_TRACE(step, 1, tid == 0);
+        dmma_region(L, P, U, nb, ja, 0, R, 0, R, warp, kLuThreads / 32, nullptr);
+        LU_TRACE(step, 8, tid == 0);
+        LU_TRACE(step, 9, tid == kLuThreads - 32);
+        __syncthreads();
+    }
+    if (tid == 0) *J.boosts = s_boosts;
+}
+
+static int pad_ld(int x) {
+    // leading dimensions == 4 or 12 (mod 16) keep the DMMA fragment loads conflict-free
+    while ((x % 16) != 4 && (x % 16) != 12) ++x;
+    return x;
+}
+
+void read_lu_trace(long long* out) {
+    SAP_CUDA(cudaMemcpyFromSymbol(out, g_lu_trace, sizeof(long long) * kTraceSteps * kTraceSlots));
+}
+
+bool launch_band_lu_ws(const FactorJob* d_jobs, int njobs, int max_k, double eps, cudaStream_t s) {
+    constexpr int B = 32;
+    // panel rows (<= B + K) must fit one per panel-group thread
+    if (max_k < 1 || B + max_k > kPgThreads) return false;
+    const int k8 = ((max_k + 7) / 8) * 8;
+    const int pld = pad_ld(B + 16 * ((max_k + 15) / 16) + 8);
+    const int uld = pad_ld(k8 + 32);
+    static const bool ws = getenv("SAP_LU_WS") != nullptr;
+    if (ws) {
+        constexpr int BW = 24;
+        const int pldw = pad_ld(BW + 16 * ((max_k + 15) / 16) + 8);
+        const int uldw = pad_ld(k8 + 8);
+        const size_t bytes = sizeof(double) * (size_t)(2 * BW * pldw + 2 * BW * uldw);
+        if (bytes > 222 * 1024) return false;
+        SAP_CUDA(cudaFuncSetAttribute(k_band_lu_ws<BW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        k_band_lu_ws<BW><<<njobs, kLuThreads, bytes, s>>>(d_jobs, eps, pldw, uldw);
+        SAP_LAUNCHED();
+        return true;
+    }
+    const size_t bytes = sizeof(double) * (size_t)(B * pld + B * uld);
+    if (bytes > 222 * 1024) return false;
+    SAP_CUDA(cudaFuncSetAttribute(k_band_lu_seq<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    k_band_lu_seq<B><<<njobs, kLuThreads, bytes, s>>>(d_jobs, eps, pld, uld);
+    SAP_LAUNCHED();
+    return true;
+}
+
+}  // namespace sapgpu

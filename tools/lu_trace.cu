@@ -1,0 +1,26 @@
+// Standalone driver: factor config-2 blocks once with the traced LU and print the per-phase timeline.
+#include <cstdio>
+#include <vector>
+#include "../include/sap_gpu.h"
+namespace sapgpu { void read_lu_trace(long long* out); }
+int main(int argc, char** argv) {
+    const int n = 200000, k = 200, p = 50;
+    std::vector<double> band((size_t)n * (2 * k + 1)), rhs(n);
+    sap_random_banded(n, k, 1.0, 1, band.data(), rhs.data());
+    sap_options o; sap_options_default(&o); o.p = p; o.precond = argc > 1 ? SAP_PRECOND_DECOUPLED : SAP_PRECOND_COUPLED;
+    sap_handle* h; sap_create(&o, &h);
+    sap_setup_banded(h, n, k, band.data(), 0);
+    sap_setup_banded(h, n, k, band.data(), 0);
+    sap_report r; sap_get_report(h, &r);
+    printf("t_factor_kernel %.3f ms\n", r.t_factor_kernel * 1e3);
+    long long t[16 * 12];
+    sapgpu::read_lu_trace(t);
+    const char* names[] = {"S0", "S1", "staged", "factored", "stored", "TOP", "u12", "UGtop", "UGbulk", "UGlast"};
+    for (int s = 0; s < 15; ++s) {
+        long long b = t[s * 12];
+        printf("step %2d:", s);
+        for (int q = 1; q < 10; ++q) printf(" %s=%6lld", names[q], t[s * 12 + q] ? t[s * 12 + q] - b : -1);
+        printf(" | next S0 %6lld\n", t[(s + 1) * 12] - b);
+    }
+    sap_destroy(h);
+}
