@@ -209,6 +209,20 @@ __device__ __forceinline__ void pg_stage_panel(const Lu& L, double* Pn, int jp, 
 // (block_factors.hpp:26-34) and publishes 1/p and the row's remaining entries
 // (double-buffered smem), right after updating that row so the division
 // overlaps the other rows' work; one named barrier per column; l = a * (1/p).
+// 1/p without the IEEE division routine: MUFU.RCP64H seed + three Newton steps
+// (~2^-23 -> full double precision; the multipliers l = a * (1/p) already
+// differ from the reference's a / p by rounding only).
+__device__ __forceinline__ double fast_rcp(double p) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(p));
+    double e = fma(-p, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-p, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-p, r, 1.0);
+    return fma(r, e, r);
+}
+
 template <int B, int C>
 __device__ __forceinline__ double pg_recip(const Lu& L, double (&row)[B], int* boost_ctr) {
     double p = row[C];
@@ -217,15 +231,27 @@ __device__ __forceinline__ double pg_recip(const Lu& L, double (&row)[B], int* b
         row[C] = p;
         atomicAdd(boost_ctr, 1);
     }
-    return 1.0 / p;
+    return fast_rcp(p);
 }
+
+// prow layout per buffer (B + 2 doubles, 16-byte aligned): [0] = 1/p, [2 + cc] = row entry cc
+template <int B>
+struct Prow {
+    static constexpr int kStride = B + 2;
+};
 
 template <int B, int C>
 __device__ __forceinline__ void pg_pub(const double (&row)[B], double rcp, double* __restrict__ prow) {
-    double* __restrict__ pr = prow + (C & 1) * (B + 1);
-    pr[C] = rcp;
+    double* __restrict__ pr = prow + (C & 1) * Prow<B>::kStride;
+    pr[0] = rcp;
+    constexpr int c0 = (C + 1) & ~1;  // publish pairs from an even column
 #pragma unroll
-    for (int cc = C + 1; cc < B; ++cc) pr[cc] = row[cc];
+    for (int cc = c0; cc < B; cc += 2) {
+        double2 v;
+        v.x = row[cc];
+        v.y = cc + 1 < B ? row[cc + 1] : 0.0;
+        *reinterpret_cast<double2*>(pr + 2 + cc) = v;
+    }
 }
 
 template <int B, int C>
@@ -234,19 +260,27 @@ __device__ __forceinline__ void pg_col(const Lu& L, double (&row)[B], double* __
     if constexpr (C < B) {
         if (C < np) {
             named_sync(kBarPg, kPgThreads);
-            const double* __restrict__ pr = prow + (C & 1) * (B + 1);
+            const double* __restrict__ pr = prow + (C & 1) * Prow<B>::kStride;
             if (ptid > C && ptid < ph) {
-                const double l = row[C] * pr[C];
+                double u[B];
+                constexpr int c0 = (C + 1) & ~1;
+#pragma unroll
+                for (int cc = c0; cc < B; cc += 2) {
+                    const double2 v = *reinterpret_cast<const double2*>(pr + 2 + cc);
+                    u[cc] = v.x;
+                    if (cc + 1 < B) u[cc + 1] = v.y;
+                }
+                const double l = row[C] * pr[0];
                 row[C] = l;
                 if constexpr (C + 1 < B) {
-                    row[C + 1] = fma(-l, pr[C + 1], row[C + 1]);
-                    // the next pivot's owner starts its division now; its row is published
+                    row[C + 1] = fma(-l, u[C + 1], row[C + 1]);
+                    // the next pivot's owner starts its reciprocal now; its row is published
                     // only after the whole update of this column
                     const bool owner = ptid == C + 1 && C + 1 < np;
                     double rcp = 0.0;
                     if (owner) rcp = pg_recip<B, C + 1>(L, row, boost_ctr);
 #pragma unroll
-                    for (int cc = C + 2; cc < B; ++cc) row[cc] = fma(-l, pr[cc], row[cc]);
+                    for (int cc = C + 2; cc < B; ++cc) row[cc] = fma(-l, u[cc], row[cc]);
                     if (owner) pg_pub<B, C + 1>(row, rcp, prow);
                 }
             }
@@ -351,7 +385,7 @@ __global__ void __launch_bounds__(kLuThreads, 1)
     k_band_lu_ws(const FactorJob* __restrict__ jobs, double eps, int pld, int uld) {
     extern __shared__ __align__(16) double smem[];
     __shared__ int s_boosts;
-    __shared__ double s_prow[2 * (B + 1)];
+    __shared__ __align__(16) double s_prow[2 * (B + 2)];
     const FactorJob J = jobs[blockIdx.x];
     const double scale = *J.scale;
     Lu L{J.base, J.rs, J.cs, J.m, J.k, B, pld, uld, eps * (scale > 0 ? scale : 1.0)};
@@ -436,7 +470,7 @@ __global__ void __launch_bounds__(kLuThreads, 1)
     k_band_lu_seq(const FactorJob* __restrict__ jobs, double eps, int pld, int uld) {
     extern __shared__ __align__(16) double smem[];
     __shared__ int s_boosts;
-    __shared__ double s_prow[2 * (B + 1)];
+    __shared__ __align__(16) double s_prow[2 * (B + 2)];
     const FactorJob J = jobs[blockIdx.x];
     const double scale = *J.scale;
     Lu L{J.base, J.rs, J.cs, J.m, J.k, B, pld, uld, eps * (scale > 0 ? scale : 1.0)};
