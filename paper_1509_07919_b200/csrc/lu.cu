@@ -64,20 +64,30 @@ struct Lu {
 // tall-thin band (|rs| == 1), moved with one 16-byte access when aligned.
 // Tiles are software-pipelined: the next tile's accumulators load while the
 // current tile computes. Pn != nullptr: results go to the next panel buffer.
+// A DMMA update region: region rows [r_lo, r_hi) x cols [c_lo, c_hi), region
+// (i, c) = global (row_org + i, col_org + c); the B' operand row of region row
+// i is P[poff + i]. Region rows i < band_top are panel rows whose entries are
+// in the band only when nbk + c - i <= K (masked on load and store).
+// Pn != nullptr: results go to smem Pn[c*pld + i - dst_off] instead of global.
 struct TileCtx {
-    int r_lo, r_hi, c_lo, c_hi, tcols, ja;
+    int r_lo, r_hi, c_lo, c_hi, tcols;
+    int row_org, col_org, poff, band_top, nbk, dst_off;
 };
 constexpr int kTileR = 16, kTileC = 32;  // warp tile: 2 x 4 DMMA tiles
 constexpr int kTQ = kTileC / 8;
+
+__device__ __forceinline__ bool tile_ok(const Lu& L, const TileCtx& T, int i, int c) {
+    return i < T.r_hi && c < T.c_hi && (i >= T.band_top || T.nbk + c - i <= L.K);
+}
 
 __device__ __forceinline__ void tile_load(const Lu& L, const TileCtx& T, int t, double (&acc)[2][kTQ][2]) {
     const int lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
     const int row0 = T.r_lo + (t / T.tcols) * kTileR, col0 = T.c_lo + (t % T.tcols) * kTileC;
     const int ib = row0 + 2 * lc, cb = col0 + lr;
     const long long rs = L.rs, ra8 = 8 * rs, cq8 = 8 * L.cs;
-    const double* p00 = L.at(T.ja + ib, T.ja + cb);
+    const double* p00 = L.at(T.row_org + ib, T.col_org + cb);
     const double* lo00 = rs > 0 ? p00 : p00 - 1;
-    const bool full = row0 + kTileR <= T.r_hi && col0 + kTileC <= T.c_hi;
+    const bool full = row0 + kTileR <= T.r_hi && col0 + kTileC <= T.c_hi && row0 >= T.band_top;
     if (full && (rs == 1 || rs == -1) && ((reinterpret_cast<uintptr_t>(lo00) & 15) == 0)) {
 #pragma unroll
         for (int a = 0; a < 2; ++a)
@@ -95,7 +105,7 @@ __device__ __forceinline__ void tile_load(const Lu& L, const TileCtx& T, int t, 
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
                     const int i = ib + a * 8 + e, c = cb + q * 8;
-                    acc[a][q][e] = (i < T.r_hi && c < T.c_hi) ? __ldcg(p00 + a * ra8 + e * rs + q * cq8) : 0.0;
+                    acc[a][q][e] = tile_ok(L, T, i, c) ? __ldcg(p00 + a * ra8 + e * rs + q * cq8) : 0.0;
                 }
     }
 }
@@ -112,7 +122,7 @@ __device__ __forceinline__ void tile_compute_store(const Lu& L, const TileCtx& T
     bool qv[kTQ];
 #pragma unroll
     for (int q = 0; q < kTQ; ++q) qv[q] = col0 + q * 8 < T.c_hi;
-    const double* pk = P + nb + row0 + lr;
+    const double* pk = P + T.poff + row0 + lr;
     const double* uk = U + col0 + lr;
     for (int ks = 0; ks < ksteps; ++ks) {
         const int kk = ks * 4 + lc;
@@ -135,14 +145,14 @@ __device__ __forceinline__ void tile_compute_store(const Lu& L, const TileCtx& T
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
                     const int i = ib + a * 8 + e, c = cb + q * 8;
-                    if (i < T.r_hi && c < T.c_hi) Pn[c * pld + i] = acc[a][q][e];
+                    if (tile_ok(L, T, i, c)) Pn[c * pld + i - T.dst_off] = acc[a][q][e];
                 }
         return;
     }
     const long long rs = L.rs, ra8 = 8 * rs, cq8 = 8 * L.cs;
-    double* p00 = L.at(T.ja + ib, T.ja + cb);
+    double* p00 = L.at(T.row_org + ib, T.col_org + cb);
     double* lo00 = rs > 0 ? p00 : p00 - 1;
-    const bool full = row0 + kTileR <= T.r_hi && col0 + kTileC <= T.c_hi;
+    const bool full = row0 + kTileR <= T.r_hi && col0 + kTileC <= T.c_hi && row0 >= T.band_top;
     if (full && (rs == 1 || rs == -1) && ((reinterpret_cast<uintptr_t>(lo00) & 15) == 0)) {
 #pragma unroll
         for (int a = 0; a < 2; ++a)
@@ -161,22 +171,33 @@ __device__ __forceinline__ void tile_compute_store(const Lu& L, const TileCtx& T
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
                     const int i = ib + a * 8 + e, c = cb + q * 8;
-                    if (i < T.r_hi && c < T.c_hi) __stcg(p00 + a * ra8 + e * rs + q * cq8, acc[a][q][e]);
+                    if (tile_ok(L, T, i, c)) __stcg(p00 + a * ra8 + e * rs + q * cq8, acc[a][q][e]);
                 }
     }
 }
 
-__device__ __noinline__ void dmma_region(const Lu& L, const double* __restrict__ P, const double* __restrict__ U,
-                                         int nb, int ja, int r_lo, int r_hi, int c_lo, int c_hi, int widx, int nw,
-                                         double* Pn) {
-    if (r_lo >= r_hi || c_lo >= c_hi) return;
-    TileCtx T{r_lo, r_hi, c_lo, c_hi, (c_hi - c_lo + kTileC - 1) / kTileC, ja};
-    const int ntiles = ((r_hi - r_lo + kTileR - 1) / kTileR) * T.tcols;
+__device__ __noinline__ void dmma_tiles(const Lu& L, const TileCtx& T, const double* __restrict__ P,
+                                        const double* __restrict__ U, int nb, int widx, int nw, double* Pn) {
+    if (T.r_lo >= T.r_hi || T.c_lo >= T.c_hi) return;
+    const int ntiles = ((T.r_hi - T.r_lo + kTileR - 1) / kTileR) * T.tcols;
     double A[2][kTQ][2];
     for (int t = widx; t < ntiles; t += nw) {
         tile_load(L, T, t, A);
         tile_compute_store(L, T, t, A, P, U, nb, Pn);
     }
+}
+
+__device__ __forceinline__ TileCtx make_tiles(int r_lo, int r_hi, int c_lo, int c_hi, int row_org, int col_org,
+                                              int poff, int band_top, int nbk, int dst_off) {
+    return TileCtx{r_lo, r_hi, c_lo, c_hi, (c_hi - c_lo + kTileC - 1) / kTileC, row_org, col_org, poff, band_top, nbk,
+                   dst_off};
+}
+
+// The classic A22 region (origin (ja, ja), B' rows offset by nb).
+__device__ __forceinline__ void dmma_region(const Lu& L, const double* __restrict__ P, const double* __restrict__ U,
+                                            int nb, int ja, int r_lo, int r_hi, int c_lo, int c_hi, int widx, int nw,
+                                            double* Pn) {
+    dmma_tiles(L, make_tiles(r_lo, r_hi, c_lo, c_hi, ja, ja, nb, 0, 0, 0), P, U, nb, widx, nw, Pn);
 }
 
 // Panel group: stage the parts of panel (jp, np) that phase (a) did not
@@ -364,6 +385,86 @@ __device__ __noinline__ void pg_u12(const Lu& L, const double* __restrict__ Pn, 
     }
 }
 
+// ---------------------------------------------------------------------------
+// Look-ahead kernel pieces (k_band_lu_la). The trailing update of step s is
+// C <- C - Pext * A12 over the extended rows [panel rows ; A22 rows] with
+// Pext = [I - L11^{-1} ; L21 L11^{-1}] and A12 the raw (unsolved) block row:
+// the top rows come out as U12 = L11^{-1} A12, the rest as
+// A22 - L21 U12 -- the U12 triangular solve folds into the tensor-core pass.
+
+// Panel group: factor the staged panel (register rows), store it, then build
+// Pext in place. Xs/L11s: 32 x 33 smem scratch.
+template <int B>
+__device__ __noinline__ void pg_panel_pext(const Lu& L, double* __restrict__ Pn, double* __restrict__ prow,
+                                           double* __restrict__ Xs, double* __restrict__ L11s, int* boost_ctr,
+                                           int jp, int np, int ph, int ptid) {
+    const int pld = L.pld;
+    double row[B];
+#pragma unroll
+    for (int c = 0; c < B; ++c) row[c] = ptid < ph ? Pn[c * pld + ptid] : 0.0;
+    if (ptid == 0 && np > 0) pg_pub<B, 0>(row, pg_recip<B, 0>(L, row, boost_ctr), prow);
+    pg_col<B, 0>(L, row, prow, boost_ctr, np, ph, ptid);
+    // the factored row: global store (L and U entries), and L11 to smem
+    if (ptid < ph) {
+#pragma unroll
+        for (int c = 0; c < B; ++c)
+            if (c < np && L.inband(ptid, c)) __stcg(L.at(jp + ptid, jp + c), row[c]);
+    }
+    if (ptid < 32) {
+#pragma unroll
+        for (int c = 0; c < B; ++c) L11s[ptid * 33 + c] = (c < ptid && ptid < np) ? row[c] : 0.0;
+        for (int c = B; c < 32; ++c) L11s[ptid * 33 + c] = 0.0;
+    }
+    for (int idx = ptid; idx < 32 * 33; idx += kPgThreads) Xs[idx] = (idx / 33 == idx % 33) ? 1.0 : 0.0;
+    named_sync(kBarPg, kPgThreads);
+    // X = L11^{-1}: X[i][c] -= L(i,j) X[j][c] for i > j >= c, j ascending (forward substitution order)
+    for (int j = 0; j + 1 < np; ++j) {
+        const int ni = np - 1 - j, nc = j + 1;
+        for (int idx = ptid; idx < ni * nc; idx += kPgThreads) {
+            const int i = j + 1 + idx / nc, c = idx % nc;
+            Xs[i * 33 + c] = fma(-L11s[i * 33 + j], Xs[j * 33 + c], Xs[i * 33 + c]);
+        }
+        named_sync(kBarPg, kPgThreads);
+    }
+    // Pext row ptid
+    for (int r = ptid; r < pld; r += kPgThreads) {
+        if (r < np) {
+#pragma unroll
+            for (int c = 0; c < B; ++c) Pn[c * pld + r] = (c < r && c < np) ? -Xs[r * 33 + c] : 0.0;
+        } else if (r < ph) {
+            // M(r, c) = sum_{j = c}^{np-1} L21(r, j) X(j, c)   (r == ptid: row[] holds L21(r, .))
+#pragma unroll
+            for (int c = 0; c < B; ++c) {
+                double acc = 0.0;
+#pragma unroll
+                for (int j = c; j < B; ++j)
+                    if (j < np) acc = fma(row[j], Xs[j * 33 + c], acc);
+                Pn[c * pld + r] = c < np ? acc : 0.0;
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < B; ++c) Pn[c * pld + r] = 0.0;
+        }
+    }
+    named_sync(kBarPg, kPgThreads);
+}
+
+// Panel group: raw A12 of panel (jp, np): rows [0, np) x cols [0, Rn) at (jp, jp+np).
+template <int B>
+__device__ __forceinline__ void pg_stage_a12(const Lu& L, double* __restrict__ An, int jp, int np, int Rn, int ptid) {
+    const int uld = L.uld;
+    for (int idx = ptid; idx < 32 * uld; idx += kPgThreads) {
+        const int r = idx & 31, c = idx >> 5;
+        if (r >= B) continue;
+        if (r < np && c < Rn && np + c - r <= L.K)
+            cp_async8(An + r * uld + c, L.at(jp + r, jp + np + c));
+        else
+            An[r * uld + c] = 0.0;
+    }
+    cp_async_wait_all();
+    named_sync(kBarPg, kPgThreads);
+}
+
 }  // namespace
 
 // Optional phase trace (build with -DSAP_LU_TRACE): CTA 0 records clock64 at
@@ -509,6 +610,136 @@ __global__ void __launch_bounds__(kLuThreads, 1)
     if (tid == 0) *J.boosts = s_boosts;
 }
 
+template <int B>
+__global__ void __launch_bounds__(kLuThreads, 1)
+    k_band_lu_la(const FactorJob* __restrict__ jobs, double eps, int pld, int uld) {
+    extern __shared__ __align__(16) double smem[];
+    __shared__ int s_boosts;
+    __shared__ __align__(16) double s_prow[2 * (B + 2)];
+    __shared__ double s_X[32 * 33];
+    __shared__ double s_L11[32 * 33];
+    const FactorJob J = jobs[blockIdx.x];
+    const double scale = *J.scale;
+    Lu L{J.base, J.rs, J.cs, J.m, J.k, B, pld, uld, eps * (scale > 0 ? scale : 1.0)};
+    const int psz = B * pld, usz = B * uld;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const bool pg = warp < kPgWarps;
+    const int m = L.m, K = L.K;
+    if (tid == 0) s_boosts = 0;
+    __syncthreads();
+    {
+        const int nb = min(B, m), ph = min(nb + K, m), R = min(K, m - nb);
+        if (pg) {
+            pg_stage_panel(L, smem, 0, nb, ph, 0, 0, tid);
+            named_sync(kBarPg, kPgThreads);
+            pg_panel_pext<B>(L, smem, s_prow, s_X, s_L11, &s_boosts, 0, nb, ph, tid);
+            pg_stage_a12<B>(L, smem + 2 * psz, 0, nb, R, tid);
+        }
+    }
+    int cur = 0;
+    int step = 0;
+    for (int jb = 0; jb < m; jb += B, ++step) {
+        __syncthreads();  // S0: Pext(s), A12(s) ready
+        LU_TRACE(step, 0, tid == 0);
+        const int nb = min(B, m - jb);
+        const int ja = jb + nb;
+        const int R = min(K, m - ja);
+        const bool has_next = ja < m;
+        const int nbn = has_next ? min(B, m - ja) : 0;
+        const int phn = has_next ? min(nbn + K, m - ja) : 0;
+        const int Rn = has_next ? min(K, m - ja - nbn) : 0;
+        const int ca = min(nbn, R);
+        const double* P = smem + cur * psz;
+        const double* A = smem + 2 * psz + cur * usz;
+        double* Pn = smem + (cur ^ 1) * psz;
+        double* An = smem + 2 * psz + (cur ^ 1) * usz;
+        // ---- phase (a): the next panel's columns (U12 part -> global, A22 part -> Pn) ----
+        if (has_next && ca > 0) {
+            dmma_tiles(L, make_tiles(0, nb, 0, ca, jb, ja, 0, nb, nb, 0), P, A, nb, warp, kLuThreads / 32, nullptr);
+            dmma_tiles(L, make_tiles(nb, nb + R, 0, ca, jb, ja, 0, 0, 0, nb), P, A, nb,
+                       (warp + kLuThreads / 32 - 2) % (kLuThreads / 32), kLuThreads / 32, Pn);
+        }
+        __syncthreads();  // S1
+        LU_TRACE(step, 1, tid == 0);
+        if (pg) {
+            if (has_next) {
+                pg_stage_panel(L, Pn, ja, nbn, phn, R, ca, tid);
+                named_sync(kBarPg, kPgThreads);
+                LU_TRACE(step, 2, tid == 0);
+                pg_panel_pext<B>(L, Pn, s_prow, s_X, s_L11, &s_boosts, ja, nbn, phn, tid);
+                LU_TRACE(step, 3, tid == 0);
+                named_sync(kBarTop, kLuThreads);  // UG has written A12(s+1)'s rows
+                LU_TRACE(step, 5, tid == 0);
+                pg_stage_a12<B>(L, An, ja, nbn, Rn, tid);
+                LU_TRACE(step, 6, tid == 0);
+            }
+        } else {
+            const int uw = warp - kPgWarps;
+            const int top = has_next ? nb + min(R, ((nbn + 15) >> 4) << 4) : nb;
+            dmma_tiles(L, make_tiles(nb, top, ca, R, jb, ja, 0, 0, 0, 0), P, A, nb, uw, kUgWarps, nullptr);
+            LU_TRACE(step, 7, tid == kPgThreads);
+            if (has_next) {
+                __threadfence_block();
+                named_arrive(kBarTop, kLuThreads);
+            }
+            dmma_tiles(L, make_tiles(0, nb, ca, R, jb, ja, 0, nb, nb, 0), P, A, nb, uw, kUgWarps, nullptr);
+            dmma_tiles(L, make_tiles(top, nb + R, ca, R, jb, ja, 0, 0, 0, 0), P, A, nb, uw, kUgWarps, nullptr);
+            LU_TRACE(step, 8, tid == kPgThreads);
+            LU_TRACE(step, 9, tid == kLuThreads - 32);
+        }
+        cur ^= 1;
+    }
+    __syncthreads();
+    if (tid == 0) *J.boosts = s_boosts;
+}
+
+// Sequential schedule with the extended-row update (no U12 triangular solve):
+// stage panel -> factor + build Pext (threads 0..255) -> stage raw A12 ->
+// C <- C - Pext * A12 over [panel rows ; A22 rows] with all 16 warps.
+template <int B>
+__global__ void __launch_bounds__(kLuThreads, 1)
+    k_band_lu_ext(const FactorJob* __restrict__ jobs, double eps, int pld, int uld) {
+    extern __shared__ __align__(16) double smem[];
+    __shared__ int s_boosts;
+    __shared__ __align__(16) double s_prow[2 * (B + 2)];
+    __shared__ double s_X[32 * 33];
+    __shared__ double s_L11[32 * 33];
+    const FactorJob J = jobs[blockIdx.x];
+    const double scale = *J.scale;
+    Lu L{J.base, J.rs, J.cs, J.m, J.k, B, pld, uld, eps * (scale > 0 ? scale : 1.0)};
+    double* P = smem;
+    double* A = smem + B * pld;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const bool pg = tid < kPgThreads;
+    const int m = L.m, K = L.K;
+    if (tid == 0) s_boosts = 0;
+    __syncthreads();
+    int step = 0;
+    for (int jb = 0; jb < m; jb += B, ++step) {
+        const int nb = min(B, m - jb);
+        const int ph = min(nb + K, m - jb);
+        const int ja = jb + nb;
+        const int R = min(K, m - ja);
+        LU_TRACE(step, 0, tid == 0);
+        if (pg) {
+            pg_stage_panel(L, P, jb, nb, ph, 0, 0, tid);
+            named_sync(kBarPg, kPgThreads);
+            LU_TRACE(step, 2, tid == 0);
+            pg_panel_pext<B>(L, P, s_prow, s_X, s_L11, &s_boosts, jb, nb, ph, tid);
+            LU_TRACE(step, 3, tid == 0);
+            pg_stage_a12<B>(L, A, jb, nb, R, tid);
+            LU_TRACE(step, 6, tid == 0);
+        }
+        __syncthreads();
+        LU_TRACE(step, 1, tid == 0);
+        dmma_tiles(L, make_tiles(0, nb + R, 0, R, jb, ja, 0, nb, nb, 0), P, A, nb, warp, kLuThreads / 32, nullptr);
+        LU_TRACE(step, 8, tid == 0);
+        LU_TRACE(step, 9, tid == kLuThreads - 32);
+        __syncthreads();
+    }
+    if (tid == 0) *J.boosts = s_boosts;
+}
+
 static int pad_ld(int x) {
     // leading dimensions == 4 or 12 (mod 16) keep the DMMA fragment loads conflict-free
     while ((x % 16) != 4 && (x % 16) != 12) ++x;
@@ -526,6 +757,35 @@ bool launch_band_lu_ws(const FactorJob* d_jobs, int njobs, int max_k, double eps
     const int k8 = ((max_k + 7) / 8) * 8;
     const int pld = pad_ld(B + 16 * ((max_k + 15) / 16) + 8);
     const int uld = pad_ld(k8 + 32);
+    // variants kept for study, all measured slower than k_band_lu_seq on B200:
+    //   SAP_LU_EXT=1  extended-row update (U12 folded into DMMA through L11^{-1}; also less accurate at d < 0.5)
+    //   SAP_LU_LA=1   warp-specialized look-ahead + extended rows
+    //   SAP_LU_WS=1   warp-specialized look-ahead
+    static const bool ext = getenv("SAP_LU_EXT") != nullptr;
+    if (ext && B + max_k <= kPgThreads) {
+        const int plde = pad_ld(B + 16 * ((max_k + 15) / 16) + 8);
+        const int ulde = pad_ld(((max_k + 7) / 8) * 8 + 8);
+        const size_t bytes = sizeof(double) * (size_t)(B * plde + B * ulde);
+        if (bytes <= 200 * 1024) {
+            SAP_CUDA(cudaFuncSetAttribute(k_band_lu_ext<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+            k_band_lu_ext<B><<<njobs, kLuThreads, bytes, s>>>(d_jobs, eps, plde, ulde);
+            SAP_LAUNCHED();
+            return true;
+        }
+    }
+    static const bool la = getenv("SAP_LU_LA") != nullptr;
+    if (la) {
+        constexpr int BL = 28;
+        const int pldl = pad_ld(BL + 16 * ((max_k + 15) / 16) + 8);
+        const int uldl = pad_ld(((max_k + 7) / 8) * 8 + 8);
+        const size_t bytes = sizeof(double) * (size_t)(2 * BL * pldl + 2 * BL * uldl);
+        if (bytes <= 206 * 1024 && BL + max_k <= kPgThreads) {
+            SAP_CUDA(cudaFuncSetAttribute(k_band_lu_la<BL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+            k_band_lu_la<BL><<<njobs, kLuThreads, bytes, s>>>(d_jobs, eps, pldl, uldl);
+            SAP_LAUNCHED();
+            return true;
+        }
+    }
     static const bool ws = getenv("SAP_LU_WS") != nullptr;
     if (ws) {
         constexpr int BW = 24;

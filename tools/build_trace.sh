@@ -9,4 +9,5 @@ for f in paper_1509_07919_b200/csrc/*.cu; do
 done
 wait
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Iinclude tools/lu_trace.cu /tmp/trbuild/*.o -o tools/lu_trace -lcudart_static
-nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Iinclude tools/sweep_trace.cu /tmp/trbuild/*.o -o tools/sweep_trace -lcudart_static
+# (sweep trace driver needs the SAP_SWEEP_TRACE hooks, removed with the reverted sweep)
+# nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Iinclude tools/sweep_trace.cu /tmp/trbuild/*.o -o tools/sweep_trace -lcudart_static
