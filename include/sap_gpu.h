@@ -180,6 +180,40 @@ sap_status sap_get_factor(sap_handle* h, int part, int which, double* out, int* 
 sap_status sap_get_spike(sap_handle* h, int iface, double* b_block, double* c_block, double* v_bottom,
                          double* w_top, double* rbar, int* rbar_boosts);
 
+/* ---- multi-GPU (one process per GPU) ----
+ * Communication is supplied by the caller (NCCL through torch.distributed on a
+ * node, or any other transport). Each rank owns a contiguous range of whole
+ * partitions, [offsets[pb], offsets[pe]) of make_partition_layout(n, opts.p, k).
+ * Factorization is rank-local. At setup the neighbours swap the one spike tip
+ * of each rank-crossing interface they cannot compute (V^b of the left rank's
+ * last block, W^t of the right rank's first block; w*w doubles each way), and
+ * both ranks build and factor that interface's reduced block. Every
+ * preconditioner apply then makes ONE neighbour exchange of w = k rows of
+ * D^{-1} r each way, every operator apply one exchange of the k-row x halo, and
+ * every Krylov reduction is a host allreduce. Callbacks are invoked with the
+ * handle's stream synchronized and must complete the transfer before returning.
+ * The preconditioner kinds distributed are coupled, decoupled and none. */
+typedef struct sap_comm {
+    void* ctx;
+    int rank, world;
+    /* in-place sum over all ranks of `count` doubles in HOST memory; 0 = ok */
+    int (*allreduce_sum)(void* ctx, double* host, int count);
+    /* neighbour exchange of DEVICE buffers: send_left[n_sl] -> rank-1, send_right[n_sr] -> rank+1,
+     * recv_left[n_rl] <- rank-1, recv_right[n_rr] <- rank+1 (any count may be 0); 0 = ok */
+    int (*exchange)(void* ctx, const double* send_left, int n_sl, const double* send_right, int n_sr,
+                    double* recv_left, int n_rl, double* recv_right, int n_rr);
+} sap_comm;
+
+/* Rank r's row range under the SURVEY §8e assignment: partitions
+ * [r*p/world, (r+1)*p/world) of make_partition_layout(n, p, k). */
+sap_status sap_rank_rows(int n, int p, int k, int rank, int world, int* row_lo, int* row_hi);
+sap_status sap_create_distributed(const sap_options* opts, const sap_comm* comm, sap_handle** out);
+/* band_slice: the GLOBAL band's columns [max(0, row_lo-k), min(n, row_hi+k)) (tall-thin layout,
+ * (2k+1) doubles per column). Afterwards apply / operator / solve take the rank's local vectors
+ * (length row_hi - row_lo). Collective: every rank must call it. */
+sap_status sap_setup_banded_dist(sap_handle* h, int n, int k, int row_lo, int row_hi, const double* band_slice,
+                                 int on_device);
+
 #ifdef __cplusplus
 }
 #endif

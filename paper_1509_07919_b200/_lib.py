@@ -32,6 +32,16 @@ class sap_solve_stats(C.Structure):
                 ("history_capacity", C.c_int)]
 
 
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int)
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int,
+                          C.c_void_p, C.c_int)
+
+
+class sap_comm(C.Structure):
+    _fields_ = [("ctx", C.c_void_p), ("rank", C.c_int), ("world", C.c_int), ("allreduce_sum", ALLREDUCE_FN),
+                ("exchange", EXCHANGE_FN)]
+
+
 # Every symbol include/sap_gpu.h declares, with its ctypes signature.
 _vp = C.c_void_p
 _dp = C.POINTER(C.c_double)
@@ -56,6 +66,9 @@ SIGNATURES = {
     "sap_get_report": (C.c_int, [_vp, C.POINTER(sap_report)]),
     "sap_get_factor": (C.c_int, [_vp, C.c_int, C.c_int, _vp, _ip, _dp]),
     "sap_get_spike": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, _vp, _vp, _ip]),
+    "sap_rank_rows": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _ip, _ip]),
+    "sap_create_distributed": (C.c_int, [C.POINTER(sap_options), C.POINTER(sap_comm), C.POINTER(_vp)]),
+    "sap_setup_banded_dist": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp, C.c_int]),
 }
 
 _lib = None

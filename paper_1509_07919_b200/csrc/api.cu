@@ -104,6 +104,17 @@ struct sap_handle {
     int csr_n = 0;
     DevBuf<int> rp, ci;
     DevBuf<double> vals;
+    DevBuf<TipJob> tipjobs;
+    // multi-GPU (sap_create_distributed): this rank owns global rows [row_lo, row_hi) = partitions
+    // [pb, pe); the band slice holds global columns [c_lo, c_hi). Interface slots are ordered
+    // [left cross?, local 0..p_loc-2, right cross?]; cross interfaces are solved on both ranks.
+    bool dist = false;
+    sap_comm comm{};
+    Layout glayout;
+    int n_glob = 0, row_lo = 0, row_hi = 0, c_lo = 0, c_hi = 0, pb = 0, pe = 0, ni_tot = 0;
+    bool has_left = false, has_right = false;
+    DevBuf<int> d_ioffs, d_boffs;
+    DevBuf<double> xext;
     // Krylov
     KrylovSolver krylov;
     DevBuf<double> kb, kx;
@@ -129,6 +140,9 @@ sap_status guard(F&& f) {
     } catch (const StateError& e) {
         g_last_error = e.what();
         return SAP_ERR_STATE;
+    } catch (const CommFailure& e) {
+        g_last_error = e.what();
+        return SAP_ERR_COMM;
     } catch (const std::exception& e) {
         g_last_error = e.what();
         return SAP_ERR_CUDA;
@@ -147,7 +161,11 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
 
 // M^{-1}: the reference's apply_preconditioner (spike.hpp:304-351) over the
 // handle's device factors. in/out are device pointers; they may alias.
+void apply_m_dist(sap_handle* h, const double* in, double* out);
+void apply_a_dist(sap_handle* h, const double* in, double* out);
+
 void apply_m(sap_handle* h, const double* in, double* out) {
+    if (h->dist) return apply_m_dist(h, in, out);
     const cudaStream_t s = h->stream;
     const int n = h->n;
     const size_t bytes = sizeof(double) * (size_t)n;
@@ -171,13 +189,15 @@ void apply_m(sap_handle* h, const double* in, double* out) {
     SAP_CUDA(cudaMemcpyAsync(g, in, bytes, cudaMemcpyDeviceToDevice, s));
     if (out != in) SAP_CUDA(cudaMemcpyAsync(out, in, bytes, cudaMemcpyDeviceToDevice, s));
     launch_block_solve<double>(h->lplan, g, s);
-    launch_interfaces<double>(g, h->d_offsets.get(), h->rplan, p, k, h->wt.get(), h->vb.get(), h->bblk.get(),
-                              h->cblk.get(), h->xt.get(), h->xb.get(), out, s);
+    launch_interfaces<double>(g, h->d_offsets.get(), h->rplan, p - 1, k, h->wt.get(), h->vb.get(), h->bblk.get(),
+                              h->cblk.get(), h->xt.get(), h->xb.get(), out, false, false, s);
     launch_block_solve<double>(h->lplan, out, s);
 }
 
 void apply_a(sap_handle* h, const double* in, double* out) {
-    if (h->csr)
+    if (h->dist)
+        apply_a_dist(h, in, out);
+    else if (h->csr)
         launch_csr_spmv(h->rp.get(), h->ci.get(), h->vals.get(), h->csr_n, in, out, nullptr, h->stream);
     else
         launch_band_spmv(h->band_ptr, h->n, h->k, in, out, nullptr, h->stream);
@@ -327,8 +347,19 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
         launch_extract_coupling(h->band_ptr, n, k, h->d_offsets.get(), p, h->bblk.get(), h->cblk.get(), s);
         SAP_CUDA(cudaEventRecord(h->ev[3], s));
         // ---- T_SPK: spike tips ----
-        launch_spike_tips(h->lu.get(), h->ul.get(), h->fst, h->d_offsets.get(), p, k, h->bblk.get(), h->cblk.get(),
-                          h->vb.get(), h->wt.get(), h->nonfinite.get(), s);
+        {
+            std::vector<TipJob> tj;
+            for (int t = 0; t < ni; ++t) {
+                const size_t o = (size_t)t * k * k;
+                tj.push_back(TipJob{h->lu.get() + h->fst.block(t), L.sizes[t] - k, 0, h->bblk.get() + o,
+                                    h->vb.get() + o, 2 * t});
+                tj.push_back(TipJob{h->ul.get() + h->fst.block(t + 1), 0, 1, h->cblk.get() + o,
+                                    h->wt.get() + o, 2 * t + 1});
+            }
+            h->tipjobs.alloc(std::max<size_t>(tj.size(), 1));
+            SAP_CUDA(cudaMemcpyAsync(h->tipjobs.get(), tj.data(), sizeof(TipJob) * tj.size(), cudaMemcpyHostToDevice, s));
+            launch_spike_tips(h->tipjobs.get(), (int)tj.size(), k, h->nonfinite.get(), s);
+        }
         SAP_CUDA(cudaEventRecord(h->ev[4], s));
         // ---- T_LUrdcd: rbar = I - W V (band layout, k' = w-1) and its boosted no-pivot LU ----
         if (k > 0) {
@@ -381,6 +412,327 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
         for (int t = 0; t < ni; ++t)
             if (nf[2 * ni + t]) throw PreconditionerFailure("reduced interface block " + std::to_string(t) + " is not finite");
     }
+    h->ready = true;
+}
+
+// ---------------------------------------------------------------------------
+// Multi-GPU: the partitions are sharded across ranks in order (rank r owns a contiguous run of
+// whole partitions). A rank factors its own blocks and the spike tips it can compute from them;
+// the neighbours swap the one tip each needs (V^b of the left rank's last block, W^t of the right
+// rank's first block) once at setup. Each cross interface's reduced block R̄ is then built and
+// factored on BOTH ranks (bitwise identical), so an apply needs one neighbour exchange of w rows of
+// g = D^{-1} in each way and no second round. The operator exchanges a k-row halo each way;
+// Krylov dots are summed over ranks.
+
+void comm_exchange(sap_handle* h, const double* sl, const double* sr, double* rl, double* rr, int count) {
+    if (count == 0 || h->comm.world <= 1) return;
+    SAP_CUDA(cudaStreamSynchronize(h->stream));
+    const int rc = h->comm.exchange(h->comm.ctx, h->has_left ? sl : nullptr, h->has_left ? count : 0,
+                                    h->has_right ? sr : nullptr, h->has_right ? count : 0,
+                                    h->has_left ? rl : nullptr, h->has_left ? count : 0,
+                                    h->has_right ? rr : nullptr, h->has_right ? count : 0);
+    if (rc != 0) throw CommFailure("sap: neighbour exchange failed (" + std::to_string(rc) + ")");
+}
+
+void comm_allreduce(sap_handle* h, double* v, int count) {
+    if (h->comm.world <= 1 || count == 0) return;
+    const int rc = h->comm.allreduce_sum(h->comm.ctx, v, count);
+    if (rc != 0) throw CommFailure("sap: allreduce failed (" + std::to_string(rc) + ")");
+}
+
+void apply_m_dist(sap_handle* h, const double* in, double* out) {
+    const cudaStream_t s = h->stream;
+    const int n = h->n, k = h->k;
+    const size_t bytes = sizeof(double) * (size_t)n;
+    if (h->kind == SAP_PRECOND_NONE) {
+        if (out != in) SAP_CUDA(cudaMemcpyAsync(out, in, bytes, cudaMemcpyDeviceToDevice, s));
+        return;
+    }
+    if (!h->coupled) {
+        if (out != in) SAP_CUDA(cudaMemcpyAsync(out, in, bytes, cudaMemcpyDeviceToDevice, s));
+        launch_block_solve<double>(h->lplan, out, s);
+        return;
+    }
+    double* g = h->scratch_g.get() + k;  // [left halo w | own n | right halo w]
+    SAP_CUDA(cudaMemcpyAsync(g, in, bytes, cudaMemcpyDeviceToDevice, s));
+    if (out != in) SAP_CUDA(cudaMemcpyAsync(out, in, bytes, cudaMemcpyDeviceToDevice, s));
+    launch_block_solve<double>(h->lplan, g, s);
+    comm_exchange(h, g, g + n - k, g - k, g + n, k);
+    launch_interfaces<double>(g, h->d_ioffs.get(), h->rplan, h->ni_tot, k, h->wt.get(), h->vb.get(), h->bblk.get(),
+                              h->cblk.get(), h->xt.get(), h->xb.get(), out, h->has_left, h->has_right, s);
+    launch_block_solve<double>(h->lplan, out, s);
+}
+
+void apply_a_dist(sap_handle* h, const double* in, double* out) {
+    const cudaStream_t s = h->stream;
+    const int n = h->n, k = h->k;
+    const int band_n = h->c_hi - h->c_lo, own = h->row_lo - h->c_lo;
+    double* x = h->xext.get();
+    SAP_CUDA(cudaMemcpyAsync(x + own, in, sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, s));
+    comm_exchange(h, in, in + n - k, x, x + own + n, k);
+    launch_band_spmv_rows(h->band_ptr, band_n, k, own, own + n, x, out, s);
+}
+
+void setup_banded_dist(sap_handle* h, int n, int k, int row_lo, int row_hi, const double* slice, int on_device) {
+    require(n >= 0 && k >= 0, "BandedMatrix: negative dimension");
+    if (h->opt.mixed_precision)
+        throw InvalidArgument("sap_setup_banded_dist: mixed_precision is not supported by this build");
+    const cudaStream_t s = h->stream;
+    h->ready = false;
+    h->kind = h->opt.precond;
+    require(h->kind == SAP_PRECOND_COUPLED || h->kind == SAP_PRECOND_DECOUPLED || h->kind == SAP_PRECOND_NONE,
+            "sap_setup_banded_dist: only the coupled, decoupled and none preconditioners are distributed");
+    const Layout G = make_layout(n, h->opt.p, k);
+    require(G.p >= h->comm.world, "sap_setup_banded_dist: fewer partitions than ranks");
+    int pb = -1, pe = -1;
+    for (int b = 0; b <= G.p; ++b) {
+        if (G.offsets[b] == row_lo) pb = b;
+        if (G.offsets[b] == row_hi) pe = b;
+    }
+    require(pb >= 0 && pe > pb, "sap_setup_banded_dist: row range does not align with partition boundaries");
+    require(slice != nullptr, "sap_setup_banded_dist: null band slice");
+    const int pl = pe - pb, nl = row_hi - row_lo;
+    Layout L;
+    L.n = nl;
+    L.p = pl;
+    L.k = k;
+    L.sizes.assign(G.sizes.begin() + pb, G.sizes.begin() + pe);
+    L.offsets.resize(pl + 1);
+    for (int b = 0; b <= pl; ++b) L.offsets[b] = G.offsets[pb + b] - row_lo;
+    h->glayout = G;
+    h->layout = L;
+    h->n_glob = n;
+    h->n = nl;
+    h->k = k;
+    h->row_lo = row_lo;
+    h->row_hi = row_hi;
+    h->pb = pb;
+    h->pe = pe;
+    h->c_lo = std::max(0, row_lo - k);
+    h->c_hi = std::min(n, row_hi + k);
+    h->has_left = row_lo > 0;
+    h->has_right = row_hi < n;
+    h->coupled = h->kind == SAP_PRECOND_COUPLED && G.p > 1 && k > 0;
+    const int band_n = h->c_hi - h->c_lo, own = row_lo - h->c_lo;
+    h->rep = sap_report{};
+    h->rep.n = n;
+    h->rep.k = k;
+    h->rep.partitions = G.p;
+
+    const size_t total = (size_t)band_n * (2 * (size_t)k + 1);
+    SAP_CUDA(cudaEventRecord(h->ev[0], s));
+    if (on_device == 2) {
+        h->band.release();
+        h->band_ptr = slice;
+    } else {
+        h->band.alloc(total);
+        SAP_CUDA(cudaMemcpyAsync(h->band.get(), slice, sizeof(double) * total,
+                                 on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+        h->band_ptr = h->band.get();
+    }
+    SAP_CUDA(cudaEventRecord(h->ev[1], s));
+    h->scratch_in.alloc(nl);
+    h->scratch_out.alloc(nl);
+    h->xext.alloc(band_n);
+    SAP_CUDA(cudaMemsetAsync(h->xext.get(), 0, sizeof(double) * band_n, s));
+    if (h->kind == SAP_PRECOND_NONE) {
+        SAP_CUDA(cudaStreamSynchronize(s));
+        h->rep.t_dtransf = ev_ms(h->ev[0], h->ev[1]) * 1e-3;
+        h->ready = true;
+        return;
+    }
+
+    // ---- factor the local blocks (as setup_banded) ----
+    std::vector<int> boffs(pl + 1);
+    for (int b = 0; b <= pl; ++b) boffs[b] = L.offsets[b] + own;
+    h->d_offsets.alloc(pl + 1);
+    h->d_boffs.alloc(pl + 1);
+    SAP_CUDA(cudaMemcpyAsync(h->d_offsets.get(), L.offsets.data(), sizeof(int) * (pl + 1), cudaMemcpyHostToDevice, s));
+    SAP_CUDA(cudaMemcpyAsync(h->d_boffs.get(), boffs.data(), sizeof(int) * (pl + 1), cudaMemcpyHostToDevice, s));
+    h->norms.alloc(pl);
+    h->boosts.alloc(2 * (size_t)pl);
+    SAP_CUDA(cudaMemsetAsync(h->boosts.get(), 0, sizeof(int) * 2 * pl, s));
+    const int m_max = *std::max_element(L.sizes.begin(), L.sizes.end());
+    h->fst = BandStore::make(m_max, k);
+    h->lu.alloc(h->fst.total(pl));
+    if (h->coupled)
+        h->ul.alloc(h->fst.total(pl));
+    else
+        h->ul.release();
+    const int njobs = h->coupled ? 2 * pl : pl;
+    std::vector<FactorJob> jobs(njobs);
+    for (int b = 0; b < pl; ++b) {
+        const int m = L.sizes[b];
+        jobs[b] = FactorJob{h->lu.get() + h->fst.block(b) + k, 1, 2LL * k, m, k, h->norms.get() + b,
+                            h->boosts.get() + b};
+        if (h->coupled)
+            jobs[pl + b] = FactorJob{h->ul.get() + h->fst.block(b) + (size_t)(m - 1) * (2 * k + 1) + k, -1, -2LL * k, m,
+                                     k, h->norms.get() + b, h->boosts.get() + pl + b};
+    }
+    h->jobs.alloc(njobs);
+    SAP_CUDA(cudaMemcpyAsync(h->jobs.get(), jobs.data(), sizeof(FactorJob) * njobs, cudaMemcpyHostToDevice, s));
+    launch_block_norms(h->band_ptr, m_max, k, h->d_boffs.get(), pl, nullptr, h->norms.get(), s);
+    launch_copy_blocks(h->band_ptr, k, h->d_boffs.get(), pl, h->fst, h->lu.get(), h->coupled ? h->ul.get() : nullptr,
+                       s);
+    SAP_CUDA(cudaEventRecord(h->ev[8], s));
+    launch_band_lu(h->jobs.get(), njobs, k, h->opt.boost_eps, s);
+    SAP_CUDA(cudaEventRecord(h->ev[9], s));
+    {
+        SweepPlan<double>& lp = h->lplan;
+        lp = SweepPlan<double>{};
+        lp.f = h->lu.get();
+        lp.st = h->fst;
+        lp.offs = h->d_offsets.get();
+        lp.p = pl;
+        lp.k = k;
+        h->dinv.alloc(std::max<size_t>(sweep_dinv_elems(lp), 1));
+        plan_sweeps(lp, h->dinv.get());
+        launch_chunk_inverses(lp, s);
+    }
+    SAP_CUDA(cudaEventRecord(h->ev[2], s));
+    for (int b = 0; b < pl; ++b) {
+        const double m = L.sizes[b], kk = std::min<double>(k, m - 1 > 0 ? m - 1 : 0);
+        const double f = (m - kk) * (2 * kk * kk + kk) + (kk - 1) * kk * (4 * kk + 1) / 6.0;
+        h->rep.factor_flops += (h->coupled ? 2.0 : 1.0) * f;
+    }
+
+    // ---- interfaces: [left cross?] [local 0..pl-2] [right cross?] ----
+    const int lc = h->coupled && h->has_left ? 1 : 0, rc = h->coupled && h->has_right ? 1 : 0;
+    const int ni = h->coupled ? lc + (pl - 1) + rc : 0;
+    h->ni_tot = ni;
+    const int gi0 = pb - lc;  // global index of interface slot 0
+    const int P = G.p;
+    if (ni > 0) {
+        const int w = k;
+        const size_t ww = (size_t)w * w;
+        std::vector<int> ioffs(ni + 1, 0);
+        for (int t = 0; t < ni; ++t) {
+            const int li = t - lc;  // local interface index (-1: left cross, pl-1: right cross)
+            ioffs[t + 1] = li < 0 ? 0 : (li >= pl - 1 ? nl : L.offsets[li + 1]);
+        }
+        h->d_ioffs.alloc(ni + 1);
+        SAP_CUDA(cudaMemcpyAsync(h->d_ioffs.get(), ioffs.data(), sizeof(int) * (ni + 1), cudaMemcpyHostToDevice, s));
+        h->rst = BandStore::make(w, w - 1);
+        for (auto* b : {&h->bblk, &h->cblk, &h->vb, &h->wt}) b->alloc(ww * ni);
+        h->rbar.alloc(h->rst.total(ni));
+        SAP_CUDA(cudaMemsetAsync(h->rbar.get(), 0, sizeof(double) * h->rst.total(ni), s));
+        h->rbar_norms.alloc(ni);
+        h->rbar_boosts.alloc(ni);
+        h->nonfinite.alloc(3 * (size_t)ni);
+        SAP_CUDA(cudaMemsetAsync(h->nonfinite.get(), 0, sizeof(int) * 3 * ni, s));
+        SAP_CUDA(cudaMemsetAsync(h->rbar_boosts.get(), 0, sizeof(int) * ni, s));
+        h->scratch_g.alloc((size_t)nl + 2 * w);
+        SAP_CUDA(cudaMemsetAsync(h->scratch_g.get(), 0, sizeof(double) * ((size_t)nl + 2 * w), s));
+        h->xt.alloc((size_t)ni * w);
+        h->xb.alloc((size_t)ni * w);
+        std::vector<int> roffs(ni + 1);
+        for (int t = 0; t <= ni; ++t) roffs[t] = t * w;
+        h->d_roffsets.alloc(ni + 1);
+        SAP_CUDA(cudaMemcpyAsync(h->d_roffsets.get(), roffs.data(), sizeof(int) * (ni + 1), cudaMemcpyHostToDevice, s));
+        // T_BC: every corner lies in this rank's column slice
+        if (pl > 1)
+            launch_extract_coupling(h->band_ptr, band_n, k, h->d_boffs.get(), pl, h->bblk.get() + lc * ww,
+                                    h->cblk.get() + lc * ww, s);
+        if (lc) {
+            launch_extract_one(h->band_ptr, band_n, k, own, 0, h->bblk.get(), s);
+            launch_extract_one(h->band_ptr, band_n, k, own, 1, h->cblk.get(), s);
+        }
+        if (rc) {
+            launch_extract_one(h->band_ptr, band_n, k, own + nl, 0, h->bblk.get() + (ni - 1) * ww, s);
+            launch_extract_one(h->band_ptr, band_n, k, own + nl, 1, h->cblk.get() + (ni - 1) * ww, s);
+        }
+        SAP_CUDA(cudaEventRecord(h->ev[3], s));
+        // T_SPK: the tips this rank's factors give; V of the left cross / W of the right cross come
+        // from the neighbours
+        std::vector<TipJob> tj;
+        for (int t = 0; t < ni; ++t) {
+            const int li = t - lc;
+            const size_t o = (size_t)t * ww;
+            if (li >= 0)  // V^b from this rank's block li
+                tj.push_back(TipJob{h->lu.get() + h->fst.block(li), L.sizes[li] - w, 0, h->bblk.get() + o,
+                                    h->vb.get() + o, 2 * t});
+            if (li + 1 < pl)  // W^t from this rank's block li+1
+                tj.push_back(TipJob{h->ul.get() + h->fst.block(li + 1), 0, 1, h->cblk.get() + o, h->wt.get() + o,
+                                    2 * t + 1});
+        }
+        h->tipjobs.alloc(tj.size());
+        SAP_CUDA(cudaMemcpyAsync(h->tipjobs.get(), tj.data(), sizeof(TipJob) * tj.size(), cudaMemcpyHostToDevice, s));
+        launch_spike_tips(h->tipjobs.get(), (int)tj.size(), k, h->nonfinite.get(), s);
+        if (h->comm.world > 1) {
+            const size_t cnt = ww;
+            SAP_CUDA(cudaStreamSynchronize(s));
+            const int rcode = h->comm.exchange(
+                h->comm.ctx, lc ? h->wt.get() : nullptr, lc ? (int)cnt : 0,
+                rc ? h->vb.get() + (ni - 1) * ww : nullptr, rc ? (int)cnt : 0, lc ? h->vb.get() : nullptr,
+                lc ? (int)cnt : 0, rc ? h->wt.get() + (ni - 1) * ww : nullptr, rc ? (int)cnt : 0);
+            if (rcode != 0) throw CommFailure("sap: spike tip exchange failed (" + std::to_string(rcode) + ")");
+        }
+        SAP_CUDA(cudaEventRecord(h->ev[4], s));
+        // T_LUrdcd: every slot's R̄ (cross ones on both ranks)
+        launch_rbar(h->wt.get(), h->vb.get(), w, ni, h->rbar.get(), h->rst, h->nonfinite.get() + 2 * ni, s);
+        launch_block_norms(h->rbar.get(), w, w - 1, h->d_roffsets.get(), ni, &h->rst, h->rbar_norms.get(), s);
+        std::vector<FactorJob> rj(ni);
+        for (int t = 0; t < ni; ++t)
+            rj[t] = FactorJob{h->rbar.get() + h->rst.block(t) + (w - 1), 1, 2LL * (w - 1), w, w - 1,
+                              h->rbar_norms.get() + t, h->rbar_boosts.get() + t};
+        h->rjobs.alloc(ni);
+        SAP_CUDA(cudaMemcpyAsync(h->rjobs.get(), rj.data(), sizeof(FactorJob) * ni, cudaMemcpyHostToDevice, s));
+        launch_band_lu(h->rjobs.get(), ni, w - 1, h->opt.boost_eps, s);
+        SweepPlan<double>& rp = h->rplan;
+        rp = SweepPlan<double>{};
+        rp.f = h->rbar.get();
+        rp.st = h->rst;
+        rp.offs = h->d_roffsets.get();
+        rp.p = ni;
+        rp.k = w - 1;
+        h->rdinv.alloc(std::max<size_t>(sweep_dinv_elems(rp), 1));
+        plan_sweeps(rp, h->rdinv.get());
+        launch_chunk_inverses(rp, s);
+        SAP_CUDA(cudaEventRecord(h->ev[5], s));
+    }
+    SAP_CUDA(cudaStreamSynchronize(s));
+    h->rep.t_dtransf = ev_ms(h->ev[0], h->ev[1]) * 1e-3;
+    h->rep.t_lu = ev_ms(h->ev[1], h->ev[2]) * 1e-3;
+    h->rep.t_factor_kernel = ev_ms(h->ev[8], h->ev[9]) * 1e-3;
+    if (ni > 0) {
+        h->rep.t_bc = ev_ms(h->ev[2], h->ev[3]) * 1e-3;
+        h->rep.t_spk = ev_ms(h->ev[3], h->ev[4]) * 1e-3;
+        h->rep.t_lurdcd = ev_ms(h->ev[4], h->ev[5]) * 1e-3;
+    }
+    // global failure flags and boost counts, summed over ranks so every rank raises the same error
+    const int nig = P - 1;
+    std::vector<double> gl(3 * (size_t)nig + 3, 0.0);
+    std::vector<int> hb(2 * pl);
+    SAP_CUDA(cudaMemcpy(hb.data(), h->boosts.get(), sizeof(int) * 2 * pl, cudaMemcpyDeviceToHost));
+    for (int b = 0; b < pl; ++b) {
+        gl[3 * nig] += hb[b];
+        gl[3 * nig + 1] += hb[pl + b];
+    }
+    if (ni > 0) {
+        std::vector<int> nf(3 * ni), rb(ni);
+        SAP_CUDA(cudaMemcpy(nf.data(), h->nonfinite.get(), sizeof(int) * 3 * ni, cudaMemcpyDeviceToHost));
+        SAP_CUDA(cudaMemcpy(rb.data(), h->rbar_boosts.get(), sizeof(int) * ni, cudaMemcpyDeviceToHost));
+        for (int t = 0; t < ni; ++t) {
+            const int gi = gi0 + t;
+            gl[2 * gi] += nf[2 * t];
+            gl[2 * gi + 1] += nf[2 * t + 1];
+            if (t >= lc) {  // a cross R̄ is counted by the rank on its left
+                gl[2 * nig + gi] += nf[2 * ni + t];
+                gl[3 * nig + 2] += rb[t];
+            }
+        }
+    }
+    comm_allreduce(h, gl.data(), (int)gl.size());
+    h->rep.total_boosts = (int)gl[3 * nig];
+    h->rep.total_boosts_ul = (int)gl[3 * nig + 1];
+    h->rep.total_rbar_boosts = (int)gl[3 * nig + 2];
+    for (int t = 0; t < nig; ++t) {
+        if (gl[2 * t] != 0.0) throw PreconditionerFailure("right spike tip at interface " + std::to_string(t) + " is not finite");
+        if (gl[2 * t + 1] != 0.0) throw PreconditionerFailure("left spike tip at interface " + std::to_string(t) + " is not finite");
+    }
+    for (int t = 0; t < nig; ++t)
+        if (gl[2 * nig + t] != 0.0)
+            throw PreconditionerFailure("reduced interface block " + std::to_string(t) + " is not finite");
     h->ready = true;
 }
 
@@ -508,8 +860,44 @@ sap_status sap_synchronize(sap_handle* h) {
 sap_status sap_setup_banded(sap_handle* h, int n, int k, const double* band, int band_on_device) {
     return guard([&] {
         require(h != nullptr, "null handle");
+        require(!h->dist, "sap_setup_banded: use sap_setup_banded_dist on a distributed handle");
         SAP_CUDA(cudaSetDevice(h->opt.device));
         setup_banded(h, n, k, band, band_on_device);
+    });
+}
+
+sap_status sap_rank_rows(int n, int p, int k, int rank, int world, int* row_lo, int* row_hi) {
+    return guard([&] {
+        require(world >= 1 && rank >= 0 && rank < world, "sap_rank_rows: rank out of range");
+        const Layout L = make_layout(n, p, k);
+        require(p >= world, "sap_rank_rows: fewer partitions than ranks");
+        const int b0 = (int)((long long)rank * p / world), b1 = (int)((long long)(rank + 1) * p / world);
+        if (row_lo) *row_lo = L.offsets[b0];
+        if (row_hi) *row_hi = L.offsets[b1];
+    });
+}
+
+sap_status sap_create_distributed(const sap_options* opts, const sap_comm* comm, sap_handle** out) {
+    return guard([&] {
+        require(comm != nullptr && out != nullptr, "sap_create_distributed: null argument");
+        require(comm->world >= 1 && comm->rank >= 0 && comm->rank < comm->world,
+                "sap_create_distributed: rank out of range");
+        require(comm->world == 1 || (comm->allreduce_sum && comm->exchange),
+                "sap_create_distributed: missing communication callbacks");
+        const sap_status st = sap_create(opts, out);
+        if (st != SAP_OK) throw InvalidArgument(g_last_error);
+        (*out)->dist = true;
+        (*out)->comm = *comm;
+    });
+}
+
+sap_status sap_setup_banded_dist(sap_handle* h, int n, int k, int row_lo, int row_hi, const double* band_slice,
+                                 int on_device) {
+    return guard([&] {
+        require(h != nullptr, "null handle");
+        require(h->dist, "sap_setup_banded_dist: handle was not created by sap_create_distributed");
+        SAP_CUDA(cudaSetDevice(h->opt.device));
+        setup_banded_dist(h, n, k, row_lo, row_hi, band_slice, on_device);
     });
 }
 
@@ -518,6 +906,7 @@ sap_status sap_set_operator_csr(sap_handle* h, int n, int nnz, const int* row_pt
     return guard([&] {
         require(h != nullptr, "null handle");
         require(n >= 0 && nnz >= 0, "sap_set_operator_csr: negative size");
+        require(!h->dist, "sap_set_operator_csr: not available on a distributed handle");
         SAP_CUDA(cudaSetDevice(h->opt.device));
         const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
         h->rp.alloc(n + 1);
@@ -595,6 +984,10 @@ sap_status sap_solve(sap_handle* h, const double* b, double* x, int on_device, s
         kc.abs_tol = h->opt.abs_tol;
         kc.max_iterations = h->opt.max_iterations;
         kc.caller_asserts_spd = h->opt.caller_asserts_spd != 0;
+        if (h->dist && h->comm.world > 1) {
+            kc.reduce = [h](double* v, int c) { comm_allreduce(h, v, c); };
+            kc.row_offset = h->row_lo;
+        }
         DeviceOp A = [h](const double* in, double* out) { apply_a(h, in, out); };
         DeviceOp M = [h](const double* in, double* out) {
             if (h->ready)
@@ -637,6 +1030,10 @@ sap_status sap_get_factor(sap_handle* h, int part, int which, double* out, int* 
         if (!h->ready) throw StateError("sap_get_factor before setup");
         require(h->kind == SAP_PRECOND_COUPLED || h->kind == SAP_PRECOND_DECOUPLED,
                 "sap_get_factor: no block factors for this preconditioner kind");
+        if (h->dist) {
+            require(part >= h->pb && part < h->pe, "sap_get_factor: partition not on this rank");
+            part -= h->pb;
+        }
         require(part >= 0 && part < h->layout.p, "sap_get_factor: partition out of range");
         require(which == 0 || which == 1, "sap_get_factor: which must be 0 (LU) or 1 (UL)");
         if (which == 1 && !h->coupled) throw InvalidArgument("block_solve: UL factors not available");
@@ -658,7 +1055,13 @@ sap_status sap_get_spike(sap_handle* h, int iface, double* b_block, double* c_bl
         require(h != nullptr, "null handle");
         if (!h->ready) throw StateError("sap_get_spike before setup");
         require(h->coupled, "sap_get_spike: no spikes (not a coupled preconditioner with p > 1)");
-        require(iface >= 0 && iface < h->layout.p - 1, "sap_get_spike: interface out of range");
+        if (h->dist) {
+            const int slot = iface - (h->pb - (h->has_left ? 1 : 0));
+            require(slot >= 0 && slot < h->ni_tot, "sap_get_spike: interface not on this rank");
+            iface = slot;
+        } else {
+            require(iface >= 0 && iface < h->layout.p - 1, "sap_get_spike: interface out of range");
+        }
         SAP_CUDA(cudaSetDevice(h->opt.device));
         const size_t ww = (size_t)h->k * h->k, off = ww * iface, bytes = sizeof(double) * ww;
         if (b_block) SAP_CUDA(cudaMemcpy(b_block, h->bblk.get() + off, bytes, cudaMemcpyDeviceToHost));

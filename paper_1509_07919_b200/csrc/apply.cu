@@ -742,10 +742,11 @@ __global__ void k_iface_pre(const T* __restrict__ g, const int* __restrict__ off
 template <class T>
 __global__ void k_iface_post1(const T* __restrict__ g, const int* __restrict__ offs, int w, const T* __restrict__ vb,
                               const T* __restrict__ bblk, const T* __restrict__ xt, T* __restrict__ xb,
-                              T* __restrict__ b2) {
+                              T* __restrict__ b2, int skip_first_b) {
     const int t = blockIdx.y, lane = threadIdx.x & 31;
     const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (i >= w) return;
+    if (blockIdx.z == 1 && t == 0 && skip_first_b) return;  // left rank's rows (multi-GPU cross interface)
     const int e = offs[t + 1];
     const T* v = xt + (size_t)t * w;
     if (blockIdx.z == 0) {
@@ -759,34 +760,36 @@ __global__ void k_iface_post1(const T* __restrict__ g, const int* __restrict__ o
 
 template <class T>
 __global__ void k_iface_post2(const int* __restrict__ offs, int w, const T* __restrict__ cblk,
-                              const T* __restrict__ xb, T* __restrict__ b2) {
+                              const T* __restrict__ xb, T* __restrict__ b2, int skip_last) {
     const int t = blockIdx.y, lane = threadIdx.x & 31;
     const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (i >= w) return;
+    if (t == (int)gridDim.y - 1 && skip_last) return;  // right rank's rows (multi-GPU cross interface)
     const int e = offs[t + 1];
     const T acc = row_dot(cblk + ((size_t)t * w + i) * w, xb + (size_t)t * w, w, lane);
     if (lane == 0) b2[e + i] -= acc;
 }
 
 template <class T>
-void launch_interfaces(const T* g, const int* d_offsets, const SweepPlan<T>& rplan, int p, int k, const T* wt,
-                       const T* vb, const T* bblk, const T* cblk, T* xt, T* xb, T* b2, cudaStream_t s) {
-    if (p < 2 || k == 0) return;
-    const int ni = p - 1, w = k;
+void launch_interfaces(const T* g, const int* d_ioffs, const SweepPlan<T>& rplan, int ni, int k, const T* wt,
+                       const T* vb, const T* bblk, const T* cblk, T* xt, T* xb, T* b2, bool skip_first_b,
+                       bool skip_last_c, cudaStream_t s) {
+    if (ni < 1 || k == 0) return;
+    const int w = k;
     dim3 grid(ceil_div(w, 8), ni);
-    k_iface_pre<T><<<grid, 256, 0, s>>>(g, d_offsets, w, wt, xt);
+    k_iface_pre<T><<<grid, 256, 0, s>>>(g, d_ioffs, w, wt, xt);
     SAP_LAUNCHED();
     launch_block_solve<T>(rplan, xt, s);
-    k_iface_post1<T><<<dim3(grid.x, ni, 2), 256, 0, s>>>(g, d_offsets, w, vb, bblk, xt, xb, b2);
+    k_iface_post1<T><<<dim3(grid.x, ni, 2), 256, 0, s>>>(g, d_ioffs, w, vb, bblk, xt, xb, b2, skip_first_b);
     SAP_LAUNCHED();
-    k_iface_post2<T><<<grid, 256, 0, s>>>(d_offsets, w, cblk, xb, b2);
+    k_iface_post2<T><<<grid, 256, 0, s>>>(d_ioffs, w, cblk, xb, b2, skip_last_c);
     SAP_LAUNCHED();
 }
 template void launch_interfaces<double>(const double*, const int*, const SweepPlan<double>&, int, int, const double*,
-                                        const double*, const double*, const double*, double*, double*, double*,
-                                        cudaStream_t);
+                                        const double*, const double*, const double*, double*, double*, double*, bool,
+                                        bool, cudaStream_t);
 template void launch_interfaces<float>(const float*, const int*, const SweepPlan<float>&, int, int, const float*,
-                                       const float*, const float*, const float*, float*, float*, float*,
+                                       const float*, const float*, const float*, float*, float*, float*, bool, bool,
                                        cudaStream_t);
 
 // ---------------------------------------------------------------------------

@@ -24,6 +24,9 @@ struct CudaFailure : std::runtime_error {
 struct StateError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
+struct CommFailure : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
 
 inline void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw CudaFailure(std::string(what) + ": " + cudaGetErrorString(e));

@@ -29,9 +29,19 @@ void launch_dense_norms(const double* a, int w, int ni, double* norms, int* nonf
 // ---- spikes (spike.cu) ----
 void launch_extract_coupling(const double* band, int n, int k, const int* d_offsets, int p, double* bblk,
                              double* cblk, cudaStream_t s);
-// v_bottom / w_top tips from the LU / UL corners; nonfinite[2t] (V) / [2t+1] (W).
-void launch_spike_tips(const double* lu, const double* ul, const BandStore& st, const int* d_offsets, int p, int k,
-                       const double* bblk, const double* cblk, double* vb, double* wt, int* nonfinite, cudaStream_t s);
+// One spike tip (compute_spike_tips, spike.hpp:190-250): which 0 -> V^b = U^{-1} L^{-1} rhs on the
+// trailing corner of an LU block; which 1 -> W^t = L^{-1} U^{-1} rhs on the leading corner of a UL block.
+struct TipJob {
+    const double* f;    // the block's band (BandStore block base)
+    int corner;         // first row/col of the w x w corner inside the block
+    int which;
+    const double* rhs;  // B or C corner, row-major w x w
+    double* out;        // row-major w x w
+    int flag;           // nonfinite[flag] set on a non-finite tip
+};
+void launch_spike_tips(const TipJob* d_jobs, int njobs, int k, int* nonfinite, cudaStream_t s);
+// One coupling corner (which 0: B at boundary e, 1: C) of a band with n columns.
+void launch_extract_one(const double* band, int n, int k, int e, int which, double* out, cudaStream_t s);
 // rbar[t] = I - wt[t] * vb[t], written in band layout (k = w-1) of the block-diagonal
 // matrix diag(rbar_0, ..., rbar_{ni-1}); nonfinite[t] flags a non-finite block.
 void launch_rbar(const double* wt, const double* vb, int w, int ni, double* rbar_band, const BandStore& rst,
@@ -67,8 +77,12 @@ void launch_block_solve(const SweepPlan<T>& pl, T* x, cudaStream_t s);
 // x^t (xt), x^b (xb) per interface and subtract the coupling terms from b2 (which holds b).
 // rbar_band: the reduced blocks' LU in band layout (k = w-1), blocks at d_roffsets (t*w).
 template <class T>
-void launch_interfaces(const T* g, const int* d_offsets, const SweepPlan<T>& rplan, int p, int k, const T* wt,
-                       const T* vb, const T* bblk, const T* cblk, T* xt, T* xb, T* b2, cudaStream_t s);
+// Interface t sits at row d_ioffs[t + 1] of g / b2 (t < ni). On a multi-GPU rank the first / last
+// interface may cross to a neighbour: skip_first_b / skip_last_c drop the update of the rows the
+// neighbour owns (g then carries the neighbour's w rows as a halo on that side).
+void launch_interfaces(const T* g, const int* d_ioffs, const SweepPlan<T>& rplan, int ni, int k, const T* wt,
+                       const T* vb, const T* bblk, const T* cblk, T* xt, T* xb, T* b2, bool skip_first_b,
+                       bool skip_last_c, cudaStream_t s);
 void launch_diag_apply(const double* in, const double* diag, double* out, int n, cudaStream_t s);
 void launch_boosted_diag(const double* band, int n, int k, const double* scale, double boost_eps, double* diag,
                          cudaStream_t s);
@@ -76,6 +90,10 @@ void launch_boosted_diag(const double* band, int n, int k, const double* scale, 
 // ---- operators (spmv.cu) ----
 // y = A x on the band; if b != nullptr also y = b - A x.
 void launch_band_spmv(const double* band, int n, int k, const double* x, double* y, const double* b, cudaStream_t s);
+// y[i - r0] = sum_j A(i, j) x[j], rows [r0, r1) of a band with n columns (x indexed like the band's columns).
+void launch_band_spmv_rows(const double* band, int n, int k, int r0, int r1, const double* x, double* y, cudaStream_t s);
+// w x w row-major GEMV: mode 0: y = u - A v;  mode 1: y -= A v.
+void launch_gemv_w(const double* A, int w, const double* v, const double* u, double* y, int mode, cudaStream_t s);
 void launch_csr_spmv(const int* rp, const int* ci, const double* v, int n, const double* x, double* y,
                      const double* b, cudaStream_t s);
 

@@ -129,7 +129,15 @@ double KrylovSolver::dot(const double* a, const double* b) {
     launch_dot(a, b, n_, partials_, counter_, dscal_, s_);
     SAP_CUDA(cudaMemcpyAsync(hpinned_, dscal_, sizeof(double), cudaMemcpyDeviceToHost, s_));
     SAP_CUDA(cudaStreamSynchronize(s_));
+    if (reduce_) reduce_(hpinned_, 1);
     return hpinned_[0];
+}
+
+bool KrylovSolver::any_flag(int local) {
+    if (!reduce_) return local != 0;
+    double v = local ? 1.0 : 0.0;
+    reduce_(&v, 1);
+    return v > 0.0;
 }
 
 bool KrylovSolver::nonfinite(const double* v) {
@@ -143,6 +151,7 @@ bool KrylovSolver::nonfinite(const double* v) {
 KrylovResult KrylovSolver::run(const DeviceOp& A, const DeviceOp& M, const double* b, double* x, int n,
                                const KrylovConfig& cfg, cudaStream_t s) {
     s_ = s;
+    reduce_ = cfg.reduce;
     int method = cfg.method;
     if (method == 2) method = cfg.caller_asserts_spd ? 1 : 0;  // run_krylov dispatch (krylov.hpp:437-441)
     if (method == 0) {
@@ -209,6 +218,7 @@ KrylovResult KrylovSolver::bicgstab(const DeviceOp& A, const DeviceOp& M, const 
             std::uniform_real_distribution<double> dist(-1.0, 1.0);
             const double scale = 1e-8 * std::sqrt(dot(r_[0], r_[0]));
             std::vector<double> h(static_cast<size_t>(n));
+            for (long long i = 0; i < cfg.row_offset; ++i) (void)dist(gen);  // this rank's slice of the stream
             for (int i = 0; i < n; ++i) h[static_cast<size_t>(i)] = dist(gen);
             SAP_CUDA(cudaMemcpyAsync(noise_, h.data(), sizeof(double) * (size_t)n, cudaMemcpyHostToDevice, s_));
             k_axpy_check<<<G, 256, 0, s_>>>(rtilde_, scale, noise_, n, nullptr);
@@ -248,7 +258,7 @@ KrylovResult KrylovSolver::bicgstab(const DeviceOp& A, const DeviceOp& M, const 
             SAP_LAUNCHED();
             SAP_CUDA(cudaMemcpyAsync(hflag_, dflag_, sizeof(int), cudaMemcpyDeviceToHost, s_));
             tr = tres(x);  // synchronizes (dot), so hflag_ is valid below
-            if (*hflag_) { st.failure = 3; return st; }
+            if (any_flag(*hflag_)) { st.failure = 3; return st; }
             if (!std::isfinite(tr)) { st.failure = 3; return st; }
             record(sweep, j + 1, tr);
             if (tr <= thr) { st.converged = true; return st; }
@@ -344,7 +354,7 @@ KrylovResult KrylovSolver::bicgstab(const DeviceOp& A, const DeviceOp& M, const 
             SAP_LAUNCHED();
             SAP_CUDA(cudaMemcpyAsync(hflag_, dflag_, sizeof(int), cudaMemcpyDeviceToHost, s_));
             tr = tres(x);
-            if (*hflag_) { st.failure = 3; return st; }
+            if (any_flag(*hflag_)) { st.failure = 3; return st; }
             if (!std::isfinite(tr)) { st.failure = 3; return st; }
             record(sweep, 2 * ell, tr);
             if (tr <= thr) { st.converged = true; return st; }

@@ -29,6 +29,10 @@ struct KrylovConfig {
     double abs_tol = 0.0;
     int max_iterations = 500;
     bool caller_asserts_spd = false;
+    // multi-GPU: in-place sum over ranks of host doubles (null = single rank), and the
+    // global index of this rank's first row (for the restart perturbation stream)
+    std::function<void(double*, int)> reduce;
+    long long row_offset = 0;
 };
 
 class KrylovSolver {
@@ -45,11 +49,13 @@ public:
 private:
     void ensure(int n, int ell);
     double dot(const double* a, const double* b);
+    bool any_flag(int local);
     bool nonfinite(const double* v);
     KrylovResult bicgstab(const DeviceOp& A, const DeviceOp& M, const double* b, double* x, const KrylovConfig& cfg);
     KrylovResult cg(const DeviceOp& A, const DeviceOp& M, const double* b, double* x, const KrylovConfig& cfg);
 
     int n_ = 0, ell_ = 0;
+    std::function<void(double*, int)> reduce_;
     cudaStream_t s_ = nullptr;
     double* buf_ = nullptr;       // all vectors
     double* partials_ = nullptr;  // reduction partials

@@ -44,30 +44,20 @@ void launch_extract_coupling(const double* band, int n, int k, const int* d_offs
 constexpr int kTipCols = 32;
 constexpr int kTipThreads = 256;
 
-// grid: (column chunks, 2 tips, p-1 interfaces). X is w x kTipCols row-major in smem.
+// grid: (column chunks, jobs). X is w x kTipCols row-major in smem.
 __global__ void __launch_bounds__(kTipThreads)
-    k_spike_tips(const double* __restrict__ lu, const double* __restrict__ ul, long long pstride, int pad,
-                 const int* __restrict__ offs, int k,
-                 const double* __restrict__ bblk, const double* __restrict__ cblk, double* __restrict__ vb,
-                 double* __restrict__ wt, int* __restrict__ nonfinite) {
+    k_spike_tips(const TipJob* __restrict__ jobs, int k, int* __restrict__ nonfinite) {
     extern __shared__ double sm[];
     const int w = k;
-    const int t = blockIdx.z, which = blockIdx.y, c0 = blockIdx.x * kTipCols;
+    const TipJob J = jobs[blockIdx.y];
+    const int which = J.which, c0 = blockIdx.x * kTipCols;
     const int nc = min(kTipCols, w - c0);
     double* X = sm;                    // [w][kTipCols]
     double* colv = sm + w * kTipCols;  // factor column j, [w]
     const long long ld = 2LL * k;      // band: (i, j) at j*2k + i + k
-    const double* f;
-    int corner;  // first global row/col of the corner inside the block band
-    if (which == 0) {
-        const int m = offs[t + 1] - offs[t];
-        f = lu + (long long)t * pstride + pad;
-        corner = m - w;
-    } else {
-        f = ul + (long long)(t + 1) * pstride + pad;
-        corner = 0;
-    }
-    const double* rhs = (which == 0 ? bblk : cblk) + (long long)t * w * w;
+    const double* f = J.f;
+    const int corner = J.corner;       // first row/col of the corner inside the block band
+    const double* rhs = J.rhs;
     for (int idx = threadIdx.x; idx < w * kTipCols; idx += blockDim.x) {
         const int r = idx / kTipCols, c = idx - r * kTipCols;
         X[idx] = c < nc ? rhs[(long long)r * w + c0 + c] : 0.0;
@@ -125,7 +115,7 @@ __global__ void __launch_bounds__(kTipThreads)
         }
     }
     __syncthreads();
-    double* out = (which == 0 ? vb : wt) + (long long)t * w * w;
+    double* out = J.out;
     int bad = 0;
     for (int idx = threadIdx.x; idx < w * kTipCols; idx += blockDim.x) {
         const int r = idx / kTipCols, c = idx - r * kTipCols;
@@ -135,18 +125,36 @@ __global__ void __launch_bounds__(kTipThreads)
             out[(long long)r * w + c0 + c] = v;
         }
     }
-    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite + 2 * t + which, 1);
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite + J.flag, 1);
 }
 
-void launch_spike_tips(const double* lu, const double* ul, const BandStore& st, const int* d_offsets, int p, int k,
-                       const double* bblk, const double* cblk, double* vb, double* wt, int* nonfinite, cudaStream_t s) {
-    if (p < 2 || k == 0) return;
+void launch_spike_tips(const TipJob* d_jobs, int njobs, int k, int* nonfinite, cudaStream_t s) {
+    if (njobs <= 0 || k == 0) return;
     const size_t bytes = sizeof(double) * ((size_t)k * kTipCols + k);
     if (bytes > 227 * 1024) throw InvalidArgument("spike tips: half-bandwidth too large");
     SAP_CUDA(cudaFuncSetAttribute(k_spike_tips, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    dim3 grid(ceil_div(k, kTipCols), 2, p - 1);
-    k_spike_tips<<<grid, kTipThreads, bytes, s>>>(lu, ul, st.pstride, st.pad, d_offsets, k, bblk, cblk, vb, wt,
-                                                   nonfinite);
+    dim3 grid(ceil_div(k, kTipCols), njobs);
+    k_spike_tips<<<grid, kTipThreads, bytes, s>>>(d_jobs, k, nonfinite);
+    SAP_LAUNCHED();
+}
+
+// One coupling corner at block boundary e (band coordinates): which 0 -> B[r][j] = A(e-w+r, e+j),
+// which 1 -> C[r][j] = A(e+r, e-w+j) (extract_coupling, spike.hpp:107-111).
+__global__ void k_extract_one(const double* __restrict__ a, int n, int k, int e, int which, double* __restrict__ out) {
+    const int w = k;
+    const long long ld = 2LL * k;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < w * w; idx += gridDim.x * blockDim.x) {
+        const int r = idx / w, j = idx - r * w;
+        const int i = which == 0 ? e - w + r : e + r;
+        const int c = which == 0 ? e + j : e - w + j;
+        const bool in = i >= 0 && i < n && c >= 0 && c < n && i - c <= k && c - i <= k;
+        out[idx] = in ? a[(long long)c * ld + i + k] : 0.0;
+    }
+}
+
+void launch_extract_one(const double* band, int n, int k, int e, int which, double* out, cudaStream_t s) {
+    if (k == 0) return;
+    k_extract_one<<<ceil_div((long long)k * k, 256), 256, 0, s>>>(band, n, k, e, which, out);
     SAP_LAUNCHED();
 }
 

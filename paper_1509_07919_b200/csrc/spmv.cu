@@ -42,6 +42,52 @@ void launch_band_spmv(const double* band, int n, int k, const double* x, double*
     SAP_LAUNCHED();
 }
 
+__global__ void __launch_bounds__(256)
+    k_band_spmv_rows(const double* __restrict__ a, int n, int k, int rbeg, int rend, const double* __restrict__ x,
+                     double* __restrict__ y) {
+    const int lane = threadIdx.x & 31;
+    const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const long long ld = 2LL * k;
+    for (int r0 = rbeg + warp_global * 32; r0 < rend; r0 += nwarps * 32) {
+        const int i = r0 + lane;
+        const int clo = max(r0 - k, 0), chi = min(r0 + 31 + k, n - 1);
+        double acc = 0.0;
+        const double* col = a + (long long)clo * ld + i + k;
+#pragma unroll 8
+        for (int j = clo; j <= chi; ++j, col += ld) {
+            const double xv = __ldg(x + j);
+            if (i < rend && i - j <= k && j - i <= k) acc = fma(*col, xv, acc);
+        }
+        if (i < rend) y[i - rbeg] = acc;
+    }
+}
+
+void launch_band_spmv_rows(const double* band, int n, int k, int r0, int r1, const double* x, double* y, cudaStream_t s) {
+    if (r1 <= r0) return;
+    const int warps = ceil_div(r1 - r0, 32);
+    k_band_spmv_rows<<<std::min(ceil_div(warps, 8), 148 * 64), 256, 0, s>>>(band, n, k, r0, r1, x, y);
+    SAP_LAUNCHED();
+}
+
+__global__ void k_gemv_w(const double* __restrict__ A, int w, const double* __restrict__ v,
+                         const double* __restrict__ u, double* __restrict__ y, int mode) {
+    const int lane = threadIdx.x & 31;
+    const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (i >= w) return;
+    double acc = 0.0;
+    for (int j = lane; j < w; j += 32) acc = fma(A[(long long)i * w + j], v[j], acc);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) y[i] = (mode == 0 ? u[i] : y[i]) - acc;
+}
+
+void launch_gemv_w(const double* A, int w, const double* v, const double* u, double* y, int mode, cudaStream_t s) {
+    if (w <= 0) return;
+    k_gemv_w<<<ceil_div(w, 8), 256, 0, s>>>(A, w, v, u, y, mode);
+    SAP_LAUNCHED();
+}
+
 __global__ void k_csr_spmv(const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ v,
                            int n, const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ b) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {

@@ -141,11 +141,14 @@ class Solver:
         o.caller_asserts_spd, o.device = int(kr.caller_asserts_spd), int(device)
         self.options = o
         self._h = C.c_void_p()
-        _check(L.load().sap_create(C.byref(o), C.byref(self._h)))
+        self._create()
         self.n = 0
         self.k = 0
         self.p = int(p)
         self.layout: PartitionLayout | None = None
+
+    def _create(self) -> None:
+        _check(L.load().sap_create(C.byref(self.options), C.byref(self._h)))
 
     def close(self) -> None:
         if self._h:
