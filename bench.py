@@ -9,7 +9,9 @@ needed between steps.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--precond C|D] [--impl ours|reference]
 
-Prints one JSON line on rank 0. `--impl reference` times the reference's own
+Prints one JSON line on rank 0. Under torchrun (N>1) the same config-2 system is
+solved with its partitions sharded over the ranks (strong scaling):
+NCCL neighbour exchanges for the interfaces and halos, allreduce for the dots. `--impl reference` times the reference's own
 CPU implementation (oracle/_ref, compiled from the unmodified reference
 headers; single-threaded, as the reference is) on the same workload.
 """
@@ -47,7 +49,7 @@ def config(pre: str, world: int) -> dict:
                         f"setup + BiCGStab(2) to rel_tol 1e-10, band resident in HBM",
             "n": N, "k": K, "d": D, "p": P, "precond": "coupled" if pre == "C" else "decoupled",
             "seed": SEED, "l2": "inputs larger than L2 (641.6 MB band), no flush",
-            "parallelism": f"replicas x{world}" if world > 1 else "single GPU"}
+            "parallelism": "single GPU"}
 
 
 class Clocks:
@@ -120,7 +122,7 @@ def run_reference(args) -> None:
     v = statistics.mean(times)
     line = {"metric": metric_name(pre), "value": v, "unit": "s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": v / PAPER_K20X_S[pre], "dtype": "f64",
+            "scaling": "strong", "vs_baseline": v / PAPER_K20X_S[pre], "dtype": "f64",
             "data": f"synthetic (testsup::random_banded, seed {SEED})", "config": config(pre, 1), "impl": "reference",
             "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "reference",
                              "sample": f"full config-2 SaP-{pre} solves (build_precond_op + run_krylov), "
@@ -149,36 +151,59 @@ def cpu_baseline(pre: str) -> dict:
 
 
 def run_ours(args) -> None:
+    import ctypes as C
     import numpy as np
     import torch
     world, rank, local = dist_env()
+    # SAP_BENCH_BACKEND=gloo lets several ranks share one GPU (a functional check of this script only)
+    backend = os.environ.get("SAP_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     import paper_1509_07919_b200 as S
+    from paper_1509_07919_b200 import _lib as L
     pre = args.precond
     kind = S.PrecondKind.coupled if pre == "C" else S.PrecondKind.decoupled
     band_h, rhs_h = S.random_banded(N, K, D, SEED)
-    band = torch.from_numpy(band_h).cuda()
-    rhs = torch.from_numpy(rhs_h).cuda()
     stream = torch.cuda.Stream()
-    solver = S.Solver(p=P, precond=kind, device=local)
+    lib = L.load()
+
+    def chk(rc):
+        if rc:
+            raise RuntimeError(lib.sap_last_error().decode())
+
+    if world == 1:
+        lo, hi, c0, c1 = 0, N, 0, N
+        solver = S.Solver(p=P, precond=kind, device=local)
+    else:
+        # strong scaling: the same config-2 system, partitions sharded over the ranks
+        from paper_1509_07919_b200.distributed import DistributedSolver, TorchComm, band_slice_columns
+        comm = TorchComm()
+        solver = DistributedSolver(comm, p=P, precond=kind, device=local)
+        lo, hi = solver.rows(N, K)
+        c0, c1 = band_slice_columns(N, K, lo, hi)
+    w = 2 * K + 1
+    band_loc = np.ascontiguousarray(band_h[c0 * w:c1 * w])
+    rhs_loc = np.ascontiguousarray(rhs_h[lo:hi])
+    band = torch.from_numpy(band_loc).cuda()
+    rhs = torch.from_numpy(rhs_loc).cuda()
     solver.set_stream(stream)
 
-    # device band is passed through the public API; borrow it (no copy) like the reference's LinearOp
-    import ctypes as C
-    from paper_1509_07919_b200 import _lib as L
-
-    def setup_borrowed():
-        rc = L.load().sap_setup_banded(solver._h, N, K, C.c_void_p(band.data_ptr()), 2)
-        if rc:
-            raise RuntimeError(L.load().sap_last_error().decode())
-        solver.n, solver.k = N, K
-        solver.layout = S.make_partition_layout(N, P, K)
+    def setup(ptr, on_device):
+        # device band passed through the public API and borrowed (no copy), like the reference's LinearOp
+        if world == 1:
+            chk(lib.sap_setup_banded(solver._h, N, K, C.c_void_p(ptr), on_device))
+        else:
+            chk(lib.sap_setup_banded_dist(solver._h, N, K, lo, hi, C.c_void_p(ptr), on_device))
 
     def step_dev():
-        setup_borrowed()
+        setup(band.data_ptr(), 2)
         return solver.solve(rhs)
 
     with torch.cuda.stream(stream):
@@ -202,47 +227,58 @@ def run_ours(args) -> None:
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
     launches = reps[-1]["kernel_launches"] - launches0
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
+
+    rdev = "cuda" if backend == "nccl" else "cpu"
+
+    def allmax(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], device=rdev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+        return float(t.item())
+
+    def allsum(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], device=rdev, dtype=torch.float64)
+        torch.distributed.all_reduce(t)
+        return float(t.item())
+
+    ms = allmax(ms)
     value = ms * 1e-3
     assert st.converged and st.final_relative_residual <= 1e-10, st
 
-    # dominant kernel: the block LU/UL factorization launch
-    t_fk = statistics.median(r["t_factor_kernel"] for r in reps)
-    flops = reps[-1]["factor_flops"]
+    # dominant kernel: the block LU/UL factorization launch (max over ranks; flops summed)
+    t_fk = allmax(statistics.median(r["t_factor_kernel"] for r in reps))
+    flops = allsum(reps[-1]["factor_flops"])
+    launches = int(allsum(launches))
     achieved = flops / t_fk / 1e12
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_lu_traffic.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and world == 1:
         try:
             traffic = json.load(open(prof)).get(f"SaP-{pre}")
         except Exception:
             traffic = None
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
-                "kernel": "k_band_lu (block LU+UL, DMMA f64)",
-                "peak_source": "FP64 DMMA measured on this pool (profiles/fp64_peaks_r01.json); "
+    peak = FP64_PEAK_TFLOPS * world
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "kernel": "k_band_lu_seq (block LU+UL, DMMA f64)",
+                "peak_source": f"FP64 DMMA measured on this pool (profiles/fp64_peaks_r01.json) x {world} GPU; "
                                "MEASURED_PEAKS.json carries no FP64 figure",
-                "algorithmic_flops_per_launch": flops, "launch_ms": t_fk * 1e3,
-                "time_to_solution_roofline_s": None}
+                "algorithmic_flops_per_launch": flops, "launch_ms": t_fk * 1e3}
 
     # end to end through the public API with host buffers (pinned), H2D/D2H inside the timed region
-    band_pin = torch.from_numpy(band_h).pin_memory()
-    rhs_pin = torch.from_numpy(rhs_h).pin_memory()
-    x_pin = torch.empty(N, dtype=torch.float64).pin_memory()
+    band_pin = torch.from_numpy(band_loc).pin_memory()
+    rhs_pin = torch.from_numpy(rhs_loc).pin_memory()
+    x_pin = torch.empty(hi - lo, dtype=torch.float64).pin_memory()
     esteps = max(1, min(args.steps, 3))
 
     def step_e2e():
-        rc = L.load().sap_setup_banded(solver._h, N, K, C.c_void_p(band_pin.data_ptr()), 0)
-        if rc:
-            raise RuntimeError(L.load().sap_last_error().decode())
+        setup(band_pin.data_ptr(), 0)
         st_ = L.sap_solve_stats()
-        rc = L.load().sap_solve(solver._h, C.c_void_p(rhs_pin.data_ptr()), C.c_void_p(x_pin.data_ptr()), 0,
-                                C.byref(st_))
-        if rc:
-            raise RuntimeError(L.load().sap_last_error().decode())
+        chk(lib.sap_solve(solver._h, C.c_void_p(rhs_pin.data_ptr()), C.c_void_p(x_pin.data_ptr()), 0,
+                          C.byref(st_)))
         return st_
 
     with torch.cuda.stream(stream):
@@ -255,25 +291,24 @@ def run_ours(args) -> None:
             ste = step_e2e()
         f1.record(stream)
     torch.cuda.synchronize()
-    e2e = f0.elapsed_time(f1) / esteps * 1e-3
+    e2e = allmax(f0.elapsed_time(f1) / esteps * 1e-3)
     assert ste.converged
-    xr = x_pin.numpy()
-    if world > 1:
-        t = torch.tensor([e2e], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e = float(t.item())
+    h2d = allsum(band_loc.nbytes + rhs_loc.nbytes)
+    d2h = allsum(x_pin.numpy().nbytes)
 
     if rank == 0:
         r = reps[-1]
+        par = "single GPU" if world == 1 else f"partitions sharded over {world} GPUs (NCCL neighbour exchange)"
+        cfg = config(pre, world)
+        cfg["parallelism"] = par
         line = {"metric": metric_name(pre), "value": value, "unit": "s", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
                 "vs_baseline": value / PAPER_K20X_S[pre], "dtype": "f64",
                 "data": f"synthetic (testsup::random_banded N={N} K={K} d={D}, seed {SEED}; b = random_rhs)",
-                "config": config(pre, world), "roofline": roofline,
-                "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": band_h.nbytes + rhs_h.nbytes,
-                        "d2h_bytes_per_step": xr.nbytes,
-                        "path": "sap_setup_banded(host band) + sap_solve(host b, host x), pinned buffers"},
-                "gpu_launches": int(launches),
+                "config": cfg, "roofline": roofline,
+                "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                        "path": "sap_setup_banded[_dist](host band) + sap_solve(host b, host x), pinned buffers"},
+                "gpu_launches": launches,
                 "clocks": clk.summary(),
                 "breakdown": {"t_lu": r["t_lu"], "t_factor_kernel": r["t_factor_kernel"], "t_bc": r["t_bc"],
                               "t_spk": r["t_spk"], "t_lurdcd": r["t_lurdcd"], "t_kry": r["t_kry"],
