@@ -472,6 +472,7 @@ __device__ __forceinline__ void pg_stage_a12(const Lu& L, double* __restrict__ A
 constexpr int kTraceSteps = 16;
 constexpr int kTraceSlots = 12;
 __device__ long long g_lu_trace[kTraceSteps * kTraceSlots];
+__device__ long long g_lu_wtrace[64];  // per-warp timestamps of one step (SAP_LU_TRACE builds)
 #ifdef SAP_LU_TRACE
 #define LU_TRACE(step, slot, cond)                                                        \
     do {                                                                                  \
@@ -740,12 +741,459 @@ __global__ void __launch_bounds__(kLuThreads, 1)
     if (tid == 0) *J.boosts = s_boosts;
 }
 
+// ---------------------------------------------------------------------------
+// k_band_lu_res: panel and A12 resident in shared memory.
+//
+// Per step s (panel columns [jb, jb+nb), A22 = the R x R window at (ja, ja), ja = jb+nb):
+//   1. warp 0 factors the nb x nb diagonal block in registers (lane = row; the pivot
+//      row's entries and 1/p travel by shuffle: no CTA barrier on the pivot chain);
+//      warps 8-15 meanwhile prefetch the band's NEW rows of panel s+1 and NEW columns
+//      of A12(s+1) (never touched by an update, so they can load this early);
+//   2. threads 0-255 finish L21 row by row (x_c = (a_c - sum_{j<c} x_j u_jc) * (1/p_c)),
+//      threads 256-511 solve U12 = L11^{-1} A12 column by column;
+//   3. the panel and U12 go to global (fire and forget);
+//   4. all 16 warps run A22 -= L21 U12 on DMMA; the tiles that form panel s+1 (A22's
+//      first nb columns) and A12(s+1) (its first rows) are written straight into the
+//      other smem buffers instead of global, so the next step starts without staging.
+// Every element receives its updates in the reference's column order with the same
+// operations as k_band_lu_seq (bitwise identical factors).
+// 8 x 8 diagonal block at (q0, q0) of the panel, factored by ONE thread in registers: the pivot chain
+// (boost -> 1/p -> multiplier -> next pivot) involves no communication at all. Left-looking by column
+// (only the multipliers stay live), with per element the same FMAs in the same ascending-column order
+// as the right-looking loop of block_factors.hpp:22-44.
+template <bool FULL>
+__device__ __noinline__ void res_diag8(double* __restrict__ P, int pld, double bv, int q0, int nq_rt,
+                                       double* __restrict__ s_rcp, int* boost_ctr) {
+    const int nq = FULL ? 8 : nq_rt;  // compile-time in the common case: no branches on the pivot chain
+    double l[8][8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        if (c < nq) {
+            double a[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) a[r] = P[(q0 + c) * pld + q0 + r];
+#pragma unroll
+            for (int r = 1; r < 8; ++r)
+#pragma unroll
+                for (int j = 0; j < (r < c ? r : c); ++j) a[r] = fma(-l[r][j], a[j], a[r]);
+            double p = a[c];
+            if (fabs(p) < bv) {
+                p = p < 0.0 ? -bv : bv;
+                a[c] = p;
+                atomicAdd(boost_ctr, 1);
+            }
+            const double rc = fast_rcp(p);
+            s_rcp[q0 + c] = rc;
+#pragma unroll
+            for (int r = c + 1; r < 8; ++r) {
+                l[r][c] = a[r] * rc;
+                a[r] = l[r][c];
+            }
+#pragma unroll
+            for (int r = 0; r < 8; ++r) P[(q0 + c) * pld + q0 + r] = a[r];
+        }
+    }
+}
+
+// The rest of sub-panel [q0, q0+8) once its diagonal block is factored (all 512 threads):
+//   rows:    threads 0-255 own panel rows r >= q0+8: x_c = (a_c - sum x_j u_jc) * (1/p_c) over the
+//            sub-panel's columns, then (after the barrier) the rank-8 update of their panel columns >= q0+8;
+//   columns: threads 256-511 own the sub-panel's U rows in panel columns >= q0+8 and in A12: the unit-lower
+//            solve, then (A12 columns) the rank-8 update of A12 rows [q0+8, nb).
+// Per element the updates arrive in ascending column order with the same FMAs as pg_col / pg_u12.
+template <bool FULL>
+__device__ __noinline__ void res_sub(double* __restrict__ P, double* __restrict__ A, int pld, int uld, int q0, int nq_rt,
+                                     int nb, int ph, int R, const double* __restrict__ s_rcp, int step) {
+    const int nq = FULL ? 8 : nq_rt;
+    const int tid = threadIdx.x;
+    const int q1 = q0 + 8;
+    double x[8];
+    const bool rowt = tid < 256;
+    const int r = q1 + tid;  // row threads
+    const int t = tid - 256, npc = max(nb - q1, 0);
+    const bool is_p = t < npc;
+    const int c = is_p ? q1 + t : t - npc;  // column threads: panel column or A12 column
+    const bool act = rowt ? r < ph : (is_p || c < R);
+    if (act) {
+        if (rowt) {
+#pragma unroll
+            for (int cc = 0; cc < 8; ++cc) x[cc] = P[(q0 + cc) * pld + r];
+#pragma unroll
+            for (int cc = 0; cc < 8; ++cc) {
+                if (cc < nq) {
+                    const double l = x[cc] * s_rcp[q0 + cc];
+                    x[cc] = l;
+#pragma unroll
+                    for (int c2 = cc + 1; c2 < 8; ++c2) x[c2] = fma(-l, P[(q0 + c2) * pld + q0 + cc], x[c2]);
+                }
+            }
+#pragma unroll
+            for (int cc = 0; cc < 8; ++cc) P[(q0 + cc) * pld + r] = x[cc];
+        } else {
+            double* col = is_p ? P + c * pld + q0 : A + q0 * uld + c;
+            const int st = is_p ? 1 : uld;
+#pragma unroll
+            for (int rr = 0; rr < 8; ++rr) x[rr] = col[rr * st];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (j < nq) {
+#pragma unroll
+                    for (int rr = j + 1; rr < 8; ++rr) x[rr] = fma(-P[(q0 + j) * pld + q0 + rr], x[j], x[rr]);
+                }
+            }
+#pragma unroll
+            for (int rr = 0; rr < 8; ++rr) col[rr * st] = x[rr];
+        }
+    }
+    if (q0 == 0) LU_TRACE(step, 9, threadIdx.x == 0);
+#ifdef SAP_LU_TRACE
+    if (q0 == 0 && step == 8 && blockIdx.x == 0 && (threadIdx.x & 31) == 0) g_lu_wtrace[threadIdx.x >> 5] = clock64();
+#endif
+    __syncthreads();
+    if (q0 == 0) LU_TRACE(step, 7, threadIdx.x == 0);
+    if constexpr (FULL) {
+        // rank-8 updates on DMMA (8 x 8 tiles, two k4 steps): the panel's rows [q1, ph) x columns [q1, nb)
+        // and A12's rows [q1, nb) x columns [0, R). Transposed product as in tile_compute_store:
+        // D^T = C^T - U^T L^T, so each thread's accumulator pair is two adjacent rows of one column.
+        const int lane = tid & 31, warp = tid >> 5, lr = lane >> 2, lc = lane & 3;
+        const int pct = (nb - q1 + 7) >> 3, np_t = ((ph - q1 + 7) >> 3) * pct;
+        const int act8 = (R + 7) >> 3, na_t = ((nb - q1 + 7) >> 3) * act8;
+        for (int t = warp; t < np_t + na_t; t += blockDim.x >> 5) {
+            const bool pan = t < np_t;
+            const int t2 = pan ? t : t - np_t, tc = pan ? pct : act8;
+            const int i0 = q1 + (t2 / tc) * 8, j0 = (pan ? q1 : 0) + (t2 % tc) * 8;
+            const int rmax = pan ? ph : nb, cmax = pan ? nb : R;
+            const int j = j0 + lr;
+            double* cp = pan ? P + j * pld : A + j;      // C(i, j) = cp[i * cs]
+            const int cs = pan ? 1 : uld;
+            const double* up = pan ? P + j * pld + q0 : A + q0 * uld + j;  // U(k, j) = up[k * us]
+            const int us = pan ? 1 : uld;
+            const int ib = i0 + 2 * lc;
+            double c0 = (ib < rmax && j < cmax) ? cp[ib * cs] : 0.0;
+            double c1 = (ib + 1 < rmax && j < cmax) ? cp[(ib + 1) * cs] : 0.0;
+            const int il = i0 + lr;
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) {
+                const int k = ks * 4 + lc;
+                const double av = j < cmax ? up[k * us] : 0.0;
+                const double bv = il < rmax ? -P[(q0 + k) * pld + il] : 0.0;
+                dmma_m8n8k4(c0, c1, av, bv, c0, c1);
+            }
+            if (j < cmax) {
+                if (ib < rmax) cp[ib * cs] = c0;
+                if (ib + 1 < rmax) cp[(ib + 1) * cs] = c1;
+            }
+        }
+        return;
+    }
+    if (!act) return;
+    if (rowt) {
+        // panel row r, columns [q1, nb) (nb - q1 is a multiple of 8 whenever nb == B): four independent
+        // accumulators per pass, the sub-panel's U rows read as 16-byte pairs
+        for (int cc0 = q1; cc0 < nb; cc0 += 4) {
+            double acc[4];
+            double u[4][8];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int cc = min(cc0 + k, nb - 1);
+                acc[k] = P[cc * pld + r];
+                const double2* up = reinterpret_cast<const double2*>(P + cc * pld + q0);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const double2 v = up[j];
+                    u[k][2 * j] = v.x;
+                    u[k][2 * j + 1] = v.y;
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (j < nq) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) acc[k] = fma(-x[j], u[k][j], acc[k]);
+                }
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (cc0 + k < nb) P[(cc0 + k) * pld + r] = acc[k];
+        }
+    } else if (!is_p) {
+        // A12 column c, rows [q1, nb): the L21 entries of four rows as 16-byte pairs
+        for (int rr0 = q1; rr0 < nb; rr0 += 4) {
+            double acc[4];
+            double lv[8][4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) acc[k] = A[min(rr0 + k, nb - 1) * uld + c];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const double2* lp = reinterpret_cast<const double2*>(P + (q0 + j) * pld + rr0);
+                const double2 v0 = lp[0], v1 = lp[1];
+                lv[j][0] = v0.x;
+                lv[j][1] = v0.y;
+                lv[j][2] = v1.x;
+                lv[j][3] = v1.y;
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (j < nq) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) acc[k] = fma(-lv[j][k], x[j], acc[k]);
+                }
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (rr0 + k < nb) A[(rr0 + k) * uld + c] = acc[k];
+        }
+    }
+}
+
+// cp.async the entries of panel (jp, np) (rows [0, ph)) and of its A12 block (rows [0, np) x cols [0, Rn) at
+// (jp, jp+np)) that the previous step's trailing update does not produce: that update covers the window
+// [0, cov) x [0, cov) of panel coordinates (cov = 0 in the prologue). In-band entries only; the rest of
+// the buffers stays zero.
+__device__ __forceinline__ void res_fetch(const Lu& L, double* __restrict__ Pb, double* __restrict__ Ab, int jp, int np,
+                                          int cov, int ph, int Rn, int t0, int nt) {
+    const int pld = L.pld, uld = L.uld;
+    for (int idx = threadIdx.x - t0; idx < ph * np; idx += nt) {
+        const int c = idx / ph, r = idx - c * ph;
+        if (r < cov && c < cov) continue;
+        if (L.inband(r, c)) cp_async8(Pb + c * pld + r, L.at(jp + r, jp + c));
+    }
+    for (int idx = threadIdx.x - t0; idx < Rn * 32; idx += nt) {
+        const int r = idx & 31, c = idx >> 5;
+        if (r >= np || (r < cov && np + c < cov)) continue;
+        if (np + c - r <= L.K) cp_async8(Ab + r * uld + c, L.at(jp + r, jp + np + c));
+    }
+}
+
+// A22 -= L21 U12 over 16 x 32 warp tiles; panel-(s+1) columns -> Pn, A12(s+1) rows -> An, rest -> global.
+// Also brings in step s+1's NEW band entries (panel rows [R, phn), A12 columns [R-nbn, Rn); never touched by
+// an update): loaded into registers before the tile loop, stored to smem after it, so the load latency
+// hides under the DMMA work (in-flight cp.async would stall the next step's shared loads).
+__device__ __noinline__ void res_bulk(const Lu& L, const double* __restrict__ P, const double* __restrict__ U, int nb,
+                                      int ja, int R, int nbn, int phn, int Rn, double* __restrict__ Pn,
+                                      double* __restrict__ An) {
+    const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
+    const int pld = L.pld, uld = L.uld;
+    constexpr int kPf = 4;  // fetch columns per warp: 64 = 32 panel + 32 A12 columns over 16 warps
+    double pf[kPf];
+    const bool fast = nbn > 0 && R >= nbn && nw * kPf >= 64;
+    if (nbn > 0 && !fast) res_fetch(L, Pn, An, ja, nbn, R, phn, Rn, 0, nw * 32);
+    if (fast) {
+#pragma unroll
+        for (int i = 0; i < kPf; ++i) {
+            const int f = warp + nw * i;
+            pf[i] = 0.0;
+            if (f < 32) {  // panel column f, row R + lane
+                const int r = R + lane;
+                if (f < nbn && r < phn && r - f <= L.K) pf[i] = __ldcg(L.at(ja + r, ja + f));
+            } else if (f < 64) {  // A12 column R - nbn + (f - 32), row lane
+                const int c = R - nbn + (f - 32);
+                if (c < Rn && lane < nbn && nbn + c - lane <= L.K) pf[i] = __ldcg(L.at(ja + lane, ja + nbn + c));
+            }
+        }
+    }
+    if (R > 0) {
+        const TileCtx T = make_tiles(0, R, 0, R, ja, ja, nb, 0, 0, 0);
+        const int ntiles = ((R + kTileR - 1) / kTileR) * T.tcols;
+        const int ksteps = (nb + 3) >> 2;
+        double acc[2][kTQ][2];
+        for (int t = warp; t < ntiles; t += nw) {
+            tile_load(L, T, t, acc);
+            const int row0 = (t / T.tcols) * kTileR, col0 = (t % T.tcols) * kTileC;
+            const bool a1 = row0 + 8 < R;
+            bool qv[kTQ];
+#pragma unroll
+            for (int q = 0; q < kTQ; ++q) qv[q] = col0 + q * 8 < R;
+            const double* pk = P + nb + row0 + lr;
+            const double* uk = U + col0 + lr;
+            if (ksteps == 8 && a1 && qv[kTQ - 1]) {
+                // full tile, full panel: operands of k-step ks+1 load while ks's DMMAs issue
+                double b0 = -pk[lc * pld], b1 = -pk[lc * pld + 8], aq[kTQ];
+#pragma unroll
+                for (int q = 0; q < kTQ; ++q) aq[q] = uk[lc * uld + q * 8];
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks) {
+                    double nb0 = 0.0, nb1 = 0.0, naq[kTQ];
+                    if (ks + 1 < 8) {
+                        const int kn = (ks + 1) * 4 + lc;
+                        nb0 = -pk[kn * pld];
+                        nb1 = -pk[kn * pld + 8];
+#pragma unroll
+                        for (int q = 0; q < kTQ; ++q) naq[q] = uk[kn * uld + q * 8];
+                    }
+#pragma unroll
+                    for (int q = 0; q < kTQ; ++q) {
+                        dmma_m8n8k4(acc[0][q][0], acc[0][q][1], aq[q], b0, acc[0][q][0], acc[0][q][1]);
+                        dmma_m8n8k4(acc[1][q][0], acc[1][q][1], aq[q], b1, acc[1][q][0], acc[1][q][1]);
+                    }
+                    if (ks + 1 < 8) {
+                        b0 = nb0;
+                        b1 = nb1;
+#pragma unroll
+                        for (int q = 0; q < kTQ; ++q) aq[q] = naq[q];
+                    }
+                }
+            } else {
+                for (int ks = 0; ks < ksteps; ++ks) {
+                    const int kk = ks * 4 + lc;
+                    const double b0 = -pk[kk * pld];
+                    const double b1 = -pk[kk * pld + 8];
+#pragma unroll
+                    for (int q = 0; q < kTQ; ++q) {
+                        if (qv[q]) {
+                            const double aq = uk[kk * uld + q * 8];
+                            dmma_m8n8k4(acc[0][q][0], acc[0][q][1], aq, b0, acc[0][q][0], acc[0][q][1]);
+                            if (a1) dmma_m8n8k4(acc[1][q][0], acc[1][q][1], aq, b1, acc[1][q][0], acc[1][q][1]);
+                        }
+                    }
+                }
+            }
+            const int ib = row0 + 2 * lc, cb = col0 + lr;
+            const bool to_p = col0 < nbn, to_a = !to_p && row0 < nbn;
+            if (!to_p && !to_a) {
+                // global: one 16-byte store per row pair when aligned (tall-thin band, |rs| == 1)
+                const long long rs = L.rs, ra8 = 8 * rs, cq8 = 8 * L.cs;
+                double* p00 = L.at(ja + ib, ja + cb);
+                double* lo00 = rs > 0 ? p00 : p00 - 1;
+                const bool full = row0 + kTileR <= R && col0 + kTileC <= R;
+                if (full && ((reinterpret_cast<uintptr_t>(lo00) & 15) == 0)) {
+#pragma unroll
+                    for (int a = 0; a < 2; ++a)
+#pragma unroll
+                        for (int q = 0; q < kTQ; ++q) {
+                            double2 v;
+                            v.x = rs > 0 ? acc[a][q][0] : acc[a][q][1];
+                            v.y = rs > 0 ? acc[a][q][1] : acc[a][q][0];
+                            __stcg(reinterpret_cast<double2*>(lo00 + a * ra8 + q * cq8), v);
+                        }
+                } else {
+#pragma unroll
+                    for (int a = 0; a < 2; ++a)
+#pragma unroll
+                        for (int q = 0; q < kTQ; ++q)
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) {
+                                const int i = ib + a * 8 + e, c = cb + q * 8;
+                                if (i < R && c < R) __stcg(p00 + a * ra8 + e * rs + q * cq8, acc[a][q][e]);
+                            }
+                }
+            } else {
+#pragma unroll
+                for (int a = 0; a < 2; ++a)
+#pragma unroll
+                    for (int q = 0; q < kTQ; ++q)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int i = ib + a * 8 + e, c = cb + q * 8;
+                            if (i >= R || c >= R) continue;
+                            if (c < nbn)
+                                Pn[c * pld + i] = acc[a][q][e];
+                            else if (i < nbn)
+                                An[i * uld + (c - nbn)] = acc[a][q][e];
+                            else
+                                __stcg(L.at(ja + i, ja + c), acc[a][q][e]);
+                        }
+            }
+        }
+    }
+    if (fast) {
+#pragma unroll
+        for (int i = 0; i < kPf; ++i) {
+            const int f = warp + nw * i;
+            if (f < 32) {
+                const int r = R + lane;
+                if (f < nbn && r < phn) Pn[f * pld + r] = pf[i];
+            } else if (f < 64) {
+                const int c = R - nbn + (f - 32);
+                if (c < Rn && lane < nbn) An[lane * uld + c] = pf[i];
+            }
+        }
+    }
+}
+
+template <int B>
+__global__ void __launch_bounds__(kLuThreads, 1)
+    k_band_lu_res(const FactorJob* __restrict__ jobs, double eps, int pld, int uld) {
+    extern __shared__ __align__(16) double smem[];
+    __shared__ int s_boosts;
+    __shared__ double s_rcp[B];
+    const FactorJob J = jobs[blockIdx.x];
+    const double scale = *J.scale;
+    Lu L{J.base, J.rs, J.cs, J.m, J.k, B, pld, uld, eps * (scale > 0 ? scale : 1.0)};
+    const int psz = B * pld, usz = B * uld;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int m = L.m, K = L.K;
+    for (int i = tid; i < 2 * (psz + usz); i += kLuThreads) smem[i] = 0.0;
+    if (tid == 0) s_boosts = 0;
+    __syncthreads();
+    {
+        const int nb = min(B, m), ph = min(nb + K, m), R = min(K, m - nb);
+        res_fetch(L, smem, smem + 2 * psz, 0, nb, 0, ph, R, 0, kLuThreads);
+        cp_async_wait_all();
+    }
+    __syncthreads();
+    int cur = 0, step = 0;
+    for (int jb = 0; jb < m; jb += B, ++step) {
+        const int nb = min(B, m - jb);
+        const int ph = min(nb + K, m - jb);
+        const int ja = jb + nb;
+        const int R = min(K, m - ja);
+        const bool has_next = ja < m;
+        const int nbn = has_next ? min(B, m - ja) : 0;
+        const int phn = has_next ? min(nbn + K, m - ja) : 0;
+        const int Rn = has_next ? min(K, m - ja - nbn) : 0;
+        double* P = smem + cur * psz;
+        double* A = smem + 2 * psz + cur * usz;
+        double* Pn = smem + (cur ^ 1) * psz;
+        double* An = smem + 2 * psz + (cur ^ 1) * usz;
+        LU_TRACE(step, 0, tid == 0);
+        // 1-2. blocked panel + U12: per 8-column sub-panel, the diagonal block (one thread) then the L rows,
+        //      U rows and rank-8 updates (all threads); warps 8-15 prefetch step s+1's new band entries meanwhile
+        for (int q0 = 0; q0 < nb; q0 += 8) {
+            const int nq = min(8, nb - q0);
+            const bool full = nb == B;
+            if (tid == 0) {
+                if (full)
+                    res_diag8<true>(P, pld, L.bv, q0, nq, s_rcp, &s_boosts);
+                else
+                    res_diag8<false>(P, pld, L.bv, q0, nq, s_rcp, &s_boosts);
+            }
+            __syncthreads();
+            if (q0 == 0) LU_TRACE(step, 5, tid == 0);
+            if (full)
+                res_sub<true>(P, A, pld, uld, q0, nq, nb, ph, R, s_rcp, step);
+            else
+                res_sub<false>(P, A, pld, uld, q0, nq, nb, ph, R, s_rcp, step);
+            __syncthreads();
+            if (q0 == 0) LU_TRACE(step, 6, tid == 0);
+        }
+        LU_TRACE(step, 3, tid == 0);
+        // 3. panel (L11\U11, L21) and U12 to global: a warp per column, lanes down the rows
+        {
+            const int lane = tid & 31;
+            for (int c = warp; c < nb; c += kLuThreads / 32)
+                for (int r = lane; r < ph; r += 32)
+                    if (L.inband(r, c)) __stcg(L.at(jb + r, jb + c), P[c * pld + r]);
+            for (int c = warp; c < R; c += kLuThreads / 32)
+                if (lane < nb && nb + c - lane <= K) __stcg(L.at(jb + lane, ja + c), A[lane * uld + c]);
+        }
+        LU_TRACE(step, 4, tid == 0);
+        // 4. trailing update (next panel / A12 land in smem) + step s+1's new band entries
+        res_bulk(L, P, A, nb, ja, R, nbn, phn, Rn, Pn, An);
+        cp_async_wait_all();
+        LU_TRACE(step, 8, tid == 0);
+        __syncthreads();
+        cur ^= 1;
+    }
+    if (tid == 0) *J.boosts = s_boosts;
+}
+
 static int pad_ld(int x) {
     // leading dimensions == 4 or 12 (mod 16) keep the DMMA fragment loads conflict-free
     while ((x % 16) != 4 && (x % 16) != 12) ++x;
     return x;
 }
 
+void read_lu_wtrace(long long* out) { SAP_CUDA(cudaMemcpyFromSymbol(out, g_lu_wtrace, sizeof(long long) * 64)); }
 void read_lu_trace(long long* out) {
     SAP_CUDA(cudaMemcpyFromSymbol(out, g_lu_trace, sizeof(long long) * kTraceSteps * kTraceSlots));
 }
@@ -797,6 +1245,19 @@ bool launch_band_lu_ws(const FactorJob* d_jobs, int njobs, int max_k, double eps
         k_band_lu_ws<BW><<<njobs, kLuThreads, bytes, s>>>(d_jobs, eps, pldw, uldw);
         SAP_LAUNCHED();
         return true;
+    }
+    static const bool seq = getenv("SAP_LU_SEQ") != nullptr;
+    if (!seq && max_k <= 256 - B) {
+        // panel rows: L21 by threads 0-255, U12 columns by threads 256-511
+        const int pldr = pad_ld(B + max_k);
+        const int uldr = pad_ld(max_k);
+        const size_t rbytes = sizeof(double) * (size_t)(2 * B * pldr + 2 * B * uldr);
+        if (rbytes <= 226 * 1024) {
+            SAP_CUDA(cudaFuncSetAttribute(k_band_lu_res<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rbytes));
+            k_band_lu_res<B><<<njobs, kLuThreads, rbytes, s>>>(d_jobs, eps, pldr, uldr);
+            SAP_LAUNCHED();
+            return true;
+        }
     }
     const size_t bytes = sizeof(double) * (size_t)(B * pld + B * uld);
     if (bytes > 222 * 1024) return false;

@@ -2,7 +2,7 @@
 #include <cstdio>
 #include <vector>
 #include "../include/sap_gpu.h"
-namespace sapgpu { void read_lu_trace(long long* out); }
+namespace sapgpu { void read_lu_trace(long long* out); void read_lu_wtrace(long long* out); }
 int main(int argc, char** argv) {
     const int n = 200000, k = 200, p = 50;
     std::vector<double> band((size_t)n * (2 * k + 1)), rhs(n);
@@ -15,12 +15,17 @@ int main(int argc, char** argv) {
     printf("t_factor_kernel %.3f ms\n", r.t_factor_kernel * 1e3);
     long long t[16 * 12];
     sapgpu::read_lu_trace(t);
-    const char* names[] = {"S0", "S1", "staged", "factored", "stored", "TOP", "u12", "UGtop", "UGbulk", "UGlast"};
+    const char* names[] = {"S0", "S1", "staged", "factored", "stored", "q0diag", "q0sub", "q0A2bar", "UGbulk", "q0A2"};
     for (int s = 0; s < 15; ++s) {
         long long b = t[s * 12];
         printf("step %2d:", s);
         for (int q = 1; q < 10; ++q) printf(" %s=%6lld", names[q], t[s * 12 + q] ? t[s * 12 + q] - b : -1);
         printf(" | next S0 %6lld\n", t[(s + 1) * 12] - b);
     }
+    long long wt[64];
+    sapgpu::read_lu_wtrace(wt);
+    printf("step 8 per-warp end of A2 (q0=0), relative to q0diag:");
+    for (int w = 0; w < 16; ++w) printf(" %lld", wt[w] - t[8 * 12 + 5]);
+    printf("\n");
     sap_destroy(h);
 }
