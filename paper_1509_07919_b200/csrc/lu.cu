@@ -1170,17 +1170,389 @@ __global__ void __launch_bounds__(kLuThreads, 1)
         // 3. panel (L11\U11, L21) and U12 to global: a warp per column, lanes down the rows
         {
             const int lane = tid & 31;
-            for (int c = warp; c < nb; c += kLuThreads / 32)
-                for (int r = lane; r < ph; r += 32)
-                    if (L.inband(r, c)) __stcg(L.at(jb + r, jb + c), P[c * pld + r]);
-            for (int c = warp; c < R; c += kLuThreads / 32)
-                if (lane < nb && nb + c - lane <= K) __stcg(L.at(jb + lane, ja + c), A[lane * uld + c]);
+            const long long rs = L.rs;
+            for (int c = warp; c < nb; c += kLuThreads / 32) {
+                double* g = L.at(jb, jb + c);
+                const int r1 = min(ph, c + K + 1);
+#pragma unroll 4
+                for (int r = max(c - K, 0) + lane; r < r1; r += 32) __stcg(g + r * rs, P[c * pld + r]);
+            }
+            if (lane < nb) {
+                double* g = L.at(jb + lane, ja);
+                const long long cs = L.cs;
+#pragma unroll 4
+                for (int c = warp; c < R; c += kLuThreads / 32)
+                    if (nb + c - lane <= K) __stcg(g + c * cs, A[lane * uld + c]);
+            }
         }
         LU_TRACE(step, 4, tid == 0);
         // 4. trailing update (next panel / A12 land in smem) + step s+1's new band entries
         res_bulk(L, P, A, nb, ja, R, nbn, phn, Rn, Pn, An);
         cp_async_wait_all();
         LU_TRACE(step, 8, tid == 0);
+        __syncthreads();
+        cur ^= 1;
+    }
+    if (tid == 0) *J.boosts = s_boosts;
+}
+
+// ---------------------------------------------------------------------------
+// k_band_lu_la2: k_band_lu_res with look-ahead. Warps 0-7 (PG) factor panel s+1 and its U12 while warps
+// 8-15 (UG) finish step s's trailing update. UG first computes the tiles that form panel s+1 (A22's first
+// column tile) and A12(s+1) (its first two row tiles) into smem plus step s+1's new band entries, then
+// releases PG through a named barrier and streams the remaining tiles through L2.
+
+// Sub-panel [q0, q0+8) after its diagonal block, by a group of nthr threads (ptid = index in the group):
+// each thread takes one L row and one U column, then the rank-8 updates (DMMA when FULL).
+template <bool FULL>
+__device__ __noinline__ void grp_sub(double* __restrict__ P, double* __restrict__ A, int pld, int uld, int q0, int nq_rt,
+                                     int nb, int ph, int R, const double* __restrict__ s_rcp, int ptid, int nthr,
+                                     int bar) {
+    const int nq = FULL ? 8 : nq_rt;
+    const int q1 = q0 + 8;
+    const int npc = max(nb - q1, 0);
+    double xr[8], xc[8];
+    const int r = q1 + ptid;
+    const bool rowa = r < ph;
+    const bool is_p = ptid < npc;
+    const int c = is_p ? q1 + ptid : ptid - npc;
+    const bool cola = is_p || c < R;
+    if (rowa) {
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) xr[cc] = P[(q0 + cc) * pld + r];
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) {
+            if (cc < nq) {
+                const double l = xr[cc] * s_rcp[q0 + cc];
+                xr[cc] = l;
+#pragma unroll
+                for (int c2 = cc + 1; c2 < 8; ++c2) xr[c2] = fma(-l, P[(q0 + c2) * pld + q0 + cc], xr[c2]);
+            }
+        }
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) P[(q0 + cc) * pld + r] = xr[cc];
+    }
+    if (cola) {
+        double* col = is_p ? P + c * pld + q0 : A + q0 * uld + c;
+        const int st = is_p ? 1 : uld;
+#pragma unroll
+        for (int rr = 0; rr < 8; ++rr) xc[rr] = col[rr * st];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (j < nq) {
+#pragma unroll
+                for (int rr = j + 1; rr < 8; ++rr) xc[rr] = fma(-P[(q0 + j) * pld + q0 + rr], xc[j], xc[rr]);
+            }
+        }
+#pragma unroll
+        for (int rr = 0; rr < 8; ++rr) col[rr * st] = xc[rr];
+    }
+    named_sync(bar, nthr);
+    if constexpr (FULL) {
+        const int lane = ptid & 31, w = ptid >> 5, nw = nthr >> 5, lr = lane >> 2, lc = lane & 3;
+        const int pct = (nb - q1 + 7) >> 3, np_t = ((ph - q1 + 7) >> 3) * pct;
+        const int act8 = (R + 7) >> 3, na_t = ((nb - q1 + 7) >> 3) * act8;
+        for (int t = w; t < np_t + na_t; t += nw) {
+            const bool pan = t < np_t;
+            const int t2 = pan ? t : t - np_t, tc = pan ? pct : act8;
+            const int i0 = q1 + (t2 / tc) * 8, j0 = (pan ? q1 : 0) + (t2 % tc) * 8;
+            const int rmax = pan ? ph : nb, cmax = pan ? nb : R;
+            const int j = j0 + lr;
+            double* cp = pan ? P + j * pld : A + j;
+            const int cs = pan ? 1 : uld;
+            const double* up = pan ? P + j * pld + q0 : A + q0 * uld + j;
+            const int us = pan ? 1 : uld;
+            const int ib = i0 + 2 * lc;
+            double c0 = (ib < rmax && j < cmax) ? cp[ib * cs] : 0.0;
+            double c1 = (ib + 1 < rmax && j < cmax) ? cp[(ib + 1) * cs] : 0.0;
+            const int il = i0 + lr;
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) {
+                const int k = ks * 4 + lc;
+                const double av = j < cmax ? up[k * us] : 0.0;
+                const double bv = il < rmax ? -P[(q0 + k) * pld + il] : 0.0;
+                dmma_m8n8k4(c0, c1, av, bv, c0, c1);
+            }
+            if (j < cmax) {
+                if (ib < rmax) cp[ib * cs] = c0;
+                if (ib + 1 < rmax) cp[(ib + 1) * cs] = c1;
+            }
+        }
+    } else {
+        if (rowa)
+            for (int cc = q1; cc < nb; ++cc) {
+                double acc = P[cc * pld + r];
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (j < nq) acc = fma(-xr[j], P[cc * pld + q0 + j], acc);
+                P[cc * pld + r] = acc;
+            }
+        if (cola && !is_p)
+            for (int rr = q1; rr < nb; ++rr) {
+                double acc = A[rr * uld + c];
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (j < nq) acc = fma(-P[(q0 + j) * pld + rr], xc[j], acc);
+                A[rr * uld + c] = acc;
+            }
+    }
+    named_sync(bar, nthr);
+}
+
+// Factor panel (jp, np) and its U12 (rows [0, np) x cols [0, R)) in smem with a thread group, then store
+// both to global.
+__device__ __noinline__ void grp_panel(const Lu& L, double* __restrict__ P, double* __restrict__ A, int jp, int np,
+                                       int ph, int R, double* __restrict__ s_rcp, int* boost_ctr, int ptid, int nthr,
+                                       int bar) {
+    const int pld = L.pld, uld = L.uld, K = L.K;
+    const bool full = np == 32;
+    for (int q0 = 0; q0 < np; q0 += 8) {
+        const int nq = min(8, np - q0);
+        if (ptid == 0) {
+            if (full)
+                res_diag8<true>(P, pld, L.bv, q0, nq, s_rcp, boost_ctr);
+            else
+                res_diag8<false>(P, pld, L.bv, q0, nq, s_rcp, boost_ctr);
+        }
+        named_sync(bar, nthr);
+        if (full)
+            grp_sub<true>(P, A, pld, uld, q0, nq, np, ph, R, s_rcp, ptid, nthr, bar);
+        else
+            grp_sub<false>(P, A, pld, uld, q0, nq, np, ph, R, s_rcp, ptid, nthr, bar);
+    }
+    // panel (L11\U11, L21) and U12 to global: a warp per column, lanes down the rows
+    const int lane = ptid & 31, w = ptid >> 5, nw = nthr >> 5;
+    const long long rs = L.rs;
+    for (int c = w; c < np; c += nw) {
+        double* g = L.at(jp, jp + c);
+        const int r0 = max(c - K, 0), r1 = min(ph, c + K + 1);
+        for (int r = r0 + lane; r < r1; r += 32) __stcg(g + r * rs, P[c * pld + r]);
+    }
+    for (int c = w; c < R; c += nw)
+        if (lane < np && np + c - lane <= K) __stcg(L.at(jp + lane, jp + np + c), A[lane * uld + c]);
+}
+
+// Trailing update tiles [t0, t1) of step (nb, ja, R) in priority order: the first column tile (panel s+1's
+// columns -> Pn), the first two row tiles (A12(s+1) -> An), then the rest (-> global).
+__device__ __noinline__ void ug_tiles(const Lu& L, const double* __restrict__ P, const double* __restrict__ U, int nb,
+                                      int ja, int R, int nbn, double* __restrict__ Pn, double* __restrict__ An, int t0,
+                                      int t1, int uw, int nuw) {
+    const int lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
+    const int pld = L.pld, uld = L.uld;
+    const TileCtx T = make_tiles(0, R, 0, R, ja, ja, nb, 0, 0, 0);
+    const int nrt = (R + kTileR - 1) / kTileR, tcols = T.tcols;
+    const int pr = min(2, nrt);  // priority row tiles (rows < 32)
+    const int ksteps = (nb + 3) >> 2;
+    double acc[2][kTQ][2];
+    for (int t = t0 + uw; t < t1; t += nuw) {
+        int ri, ci;
+        if (t < nrt) {
+            ri = t;
+            ci = 0;
+        } else if (t < nrt + pr * (tcols - 1)) {
+            const int u = t - nrt;
+            ri = u % pr;
+            ci = 1 + u / pr;
+        } else {
+            const int u = t - nrt - pr * (tcols - 1);
+            ri = pr + u / (tcols - 1);
+            ci = 1 + u % (tcols - 1);
+        }
+        const int tt = ri * tcols + ci;  // tile index in make_tiles order
+        const int row0 = ri * kTileR, col0 = ci * kTileC;
+        tile_load(L, T, tt, acc);
+        const bool a1 = row0 + 8 < R;
+        bool qv[kTQ];
+#pragma unroll
+        for (int q = 0; q < kTQ; ++q) qv[q] = col0 + q * 8 < R;
+        const double* pk = P + nb + row0 + lr;
+        const double* uk = U + col0 + lr;
+        if (ksteps == 8 && a1 && qv[kTQ - 1]) {
+            double b0 = -pk[lc * pld], b1 = -pk[lc * pld + 8], aq[kTQ];
+#pragma unroll
+            for (int q = 0; q < kTQ; ++q) aq[q] = uk[lc * uld + q * 8];
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                double nb0 = 0.0, nb1 = 0.0, naq[kTQ];
+                if (ks + 1 < 8) {
+                    const int kn = (ks + 1) * 4 + lc;
+                    nb0 = -pk[kn * pld];
+                    nb1 = -pk[kn * pld + 8];
+#pragma unroll
+                    for (int q = 0; q < kTQ; ++q) naq[q] = uk[kn * uld + q * 8];
+                }
+#pragma unroll
+                for (int q = 0; q < kTQ; ++q) {
+                    dmma_m8n8k4(acc[0][q][0], acc[0][q][1], aq[q], b0, acc[0][q][0], acc[0][q][1]);
+                    dmma_m8n8k4(acc[1][q][0], acc[1][q][1], aq[q], b1, acc[1][q][0], acc[1][q][1]);
+                }
+                if (ks + 1 < 8) {
+                    b0 = nb0;
+                    b1 = nb1;
+#pragma unroll
+                    for (int q = 0; q < kTQ; ++q) aq[q] = naq[q];
+                }
+            }
+        } else {
+            for (int ks = 0; ks < ksteps; ++ks) {
+                const int kk = ks * 4 + lc;
+                const double b0 = -pk[kk * pld];
+                const double b1 = -pk[kk * pld + 8];
+#pragma unroll
+                for (int q = 0; q < kTQ; ++q) {
+                    if (qv[q]) {
+                        const double aq = uk[kk * uld + q * 8];
+                        dmma_m8n8k4(acc[0][q][0], acc[0][q][1], aq, b0, acc[0][q][0], acc[0][q][1]);
+                        if (a1) dmma_m8n8k4(acc[1][q][0], acc[1][q][1], aq, b1, acc[1][q][0], acc[1][q][1]);
+                    }
+                }
+            }
+        }
+        const int ib = row0 + 2 * lc, cb = col0 + lr;
+        const bool to_p = col0 < nbn, to_a = !to_p && row0 < nbn;
+        if (!to_p && !to_a) {
+            const long long rs = L.rs, ra8 = 8 * rs, cq8 = 8 * L.cs;
+            double* p00 = L.at(ja + ib, ja + cb);
+            double* lo00 = rs > 0 ? p00 : p00 - 1;
+            const bool fullt = row0 + kTileR <= R && col0 + kTileC <= R;
+            if (fullt && ((reinterpret_cast<uintptr_t>(lo00) & 15) == 0)) {
+#pragma unroll
+                for (int a = 0; a < 2; ++a)
+#pragma unroll
+                    for (int q = 0; q < kTQ; ++q) {
+                        double2 v;
+                        v.x = rs > 0 ? acc[a][q][0] : acc[a][q][1];
+                        v.y = rs > 0 ? acc[a][q][1] : acc[a][q][0];
+                        __stcg(reinterpret_cast<double2*>(lo00 + a * ra8 + q * cq8), v);
+                    }
+            } else {
+#pragma unroll
+                for (int a = 0; a < 2; ++a)
+#pragma unroll
+                    for (int q = 0; q < kTQ; ++q)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int i = ib + a * 8 + e, c = cb + q * 8;
+                            if (i < R && c < R) __stcg(p00 + a * ra8 + e * rs + q * cq8, acc[a][q][e]);
+                        }
+            }
+        } else {
+#pragma unroll
+            for (int a = 0; a < 2; ++a)
+#pragma unroll
+                for (int q = 0; q < kTQ; ++q)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int i = ib + a * 8 + e, c = cb + q * 8;
+                        if (i >= R || c >= R) continue;
+                        if (c < nbn)
+                            Pn[c * pld + i] = acc[a][q][e];
+                        else if (i < nbn)
+                            An[i * uld + (c - nbn)] = acc[a][q][e];
+                        else
+                            __stcg(L.at(ja + i, ja + c), acc[a][q][e]);
+                    }
+        }
+    }
+}
+
+// Step s+1's new band entries (panel rows [R, phn), A12 columns [R-nbn, Rn)) into smem, by a thread group.
+__device__ __noinline__ void ug_new_entries(const Lu& L, double* __restrict__ Pn, double* __restrict__ An, int ja, int R,
+                                            int nbn, int phn, int Rn, int uw, int nuw) {
+    const int lane = threadIdx.x & 31, pld = L.pld, uld = L.uld;
+    if (R < nbn) {  // tail: the generic fetch (rare)
+        res_fetch(L, Pn, An, ja, nbn, R, phn, Rn, threadIdx.x - lane - uw * 32, nuw * 32);
+        cp_async_wait_all();
+        return;
+    }
+    double v[8];
+    int n = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int f = uw + nuw * i;
+        v[i] = 0.0;
+        if (f < 32) {
+            const int r = R + lane;
+            if (f < nbn && r < phn && r - f <= L.K) v[i] = __ldcg(L.at(ja + r, ja + f));
+        } else if (f < 64) {
+            const int c = R - nbn + (f - 32);
+            if (c < Rn && lane < nbn && nbn + c - lane <= L.K) v[i] = __ldcg(L.at(ja + lane, ja + nbn + c));
+        }
+        n = i + 1;
+        if (uw + nuw * (i + 1) >= 64) break;
+    }
+    for (int i = 0; i < n; ++i) {
+        const int f = uw + nuw * i;
+        if (f < 32) {
+            const int r = R + lane;
+            if (f < nbn && r < phn) Pn[f * pld + r] = v[i];
+        } else if (f < 64) {
+            const int c = R - nbn + (f - 32);
+            if (c < Rn && lane < nbn) An[lane * uld + c] = v[i];
+        }
+    }
+}
+
+template <int B>
+__global__ void __launch_bounds__(kLuThreads, 1)
+    k_band_lu_la2(const FactorJob* __restrict__ jobs, double eps, int pld, int uld) {
+    extern __shared__ __align__(16) double smem[];
+    __shared__ int s_boosts;
+    __shared__ double s_rcp[B];
+    constexpr int kPg = 256;          // PG: threads 0-255
+    constexpr int kBarPgL = 3;        // PG internal
+    constexpr int kBarNext = 4;       // UG -> PG: panel s+1 / A12(s+1) complete in smem
+    const FactorJob J = jobs[blockIdx.x];
+    const double scale = *J.scale;
+    Lu L{J.base, J.rs, J.cs, J.m, J.k, B, pld, uld, eps * (scale > 0 ? scale : 1.0)};
+    const int psz = B * pld, usz = B * uld;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const bool pg = tid < kPg;
+    const int m = L.m, K = L.K;
+    for (int i = tid; i < 2 * (psz + usz); i += kLuThreads) smem[i] = 0.0;
+    if (tid == 0) s_boosts = 0;
+    __syncthreads();
+    {
+        const int nb = min(B, m), ph = min(nb + K, m), R = min(K, m - nb);
+        res_fetch(L, smem, smem + 2 * psz, 0, nb, 0, ph, R, 0, kLuThreads);
+        cp_async_wait_all();
+        __syncthreads();
+        if (pg) grp_panel(L, smem, smem + 2 * psz, 0, nb, ph, R, s_rcp, &s_boosts, tid, kPg, kBarPgL);
+    }
+    __syncthreads();
+    int cur = 0, step = 0;
+    for (int jb = 0; jb < m; jb += B, ++step) {
+        const int nb = min(B, m - jb);
+        const int ja = jb + nb;
+        const int R = min(K, m - ja);
+        const bool has_next = ja < m;
+        const int nbn = has_next ? min(B, m - ja) : 0;
+        const int phn = has_next ? min(nbn + K, m - ja) : 0;
+        const int Rn = has_next ? min(K, m - ja - nbn) : 0;
+        double* P = smem + cur * psz;
+        double* A = smem + 2 * psz + cur * usz;
+        double* Pn = smem + (cur ^ 1) * psz;
+        double* An = smem + 2 * psz + (cur ^ 1) * usz;
+        LU_TRACE(step, 0, tid == 0);
+        const int nrt = R > 0 ? (R + kTileR - 1) / kTileR : 0;
+        const int tcols = R > 0 ? (R + kTileC - 1) / kTileC : 0;
+        const int ntiles = nrt * tcols;
+        const int nprio = (has_next && nbn == B && tcols > 1) ? nrt + min(2, nrt) * (tcols - 1) : ntiles;
+        if (!pg) {
+            const int uw = warp - kPg / 32, nuw = (kLuThreads - kPg) / 32;
+            ug_tiles(L, P, A, nb, ja, R, nbn, Pn, An, 0, nprio, uw, nuw);
+            if (has_next) ug_new_entries(L, Pn, An, ja, R, nbn, phn, Rn, uw, nuw);
+            __threadfence_block();
+            named_arrive(kBarNext, kLuThreads);
+            LU_TRACE(step, 7, tid == kPg);
+            ug_tiles(L, P, A, nb, ja, R, nbn, Pn, An, nprio, ntiles, uw, nuw);
+            LU_TRACE(step, 8, tid == kPg);
+        } else {
+            named_sync(kBarNext, kLuThreads);
+            LU_TRACE(step, 2, tid == 0);
+            if (has_next) grp_panel(L, Pn, An, ja, nbn, phn, Rn, s_rcp, &s_boosts, tid, kPg, kBarPgL);
+            LU_TRACE(step, 3, tid == 0);
+        }
         __syncthreads();
         cur ^= 1;
     }
@@ -1247,6 +1619,18 @@ bool launch_band_lu_ws(const FactorJob* d_jobs, int njobs, int max_k, double eps
         return true;
     }
     static const bool seq = getenv("SAP_LU_SEQ") != nullptr;
+    static const bool la2 = getenv("SAP_LU_LA2") != nullptr;
+    if (!seq && la2 && max_k <= 256 - B) {
+        const int pldr = pad_ld(B + max_k);
+        const int uldr = pad_ld(max_k);
+        const size_t rbytes = sizeof(double) * (size_t)(2 * B * pldr + 2 * B * uldr);
+        if (rbytes <= 226 * 1024) {
+            SAP_CUDA(cudaFuncSetAttribute(k_band_lu_la2<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rbytes));
+            k_band_lu_la2<B><<<njobs, kLuThreads, rbytes, s>>>(d_jobs, eps, pldr, uldr);
+            SAP_LAUNCHED();
+            return true;
+        }
+    }
     if (!seq && max_k <= 256 - B) {
         // panel rows: L21 by threads 0-255, U12 columns by threads 256-511
         const int pldr = pad_ld(B + max_k);
