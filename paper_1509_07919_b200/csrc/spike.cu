@@ -10,6 +10,8 @@
 // element below (above) j is updated in parallel. For the forward solves this
 // applies each element's updates in the reference's ascending-j order; the
 // backward solves apply them in descending j (within tolerance).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -128,8 +130,191 @@ __global__ void __launch_bounds__(kTipThreads)
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite + J.flag, 1);
 }
 
+// ---------------------------------------------------------------------------
+// Blocked tips: X (w x 32 columns of the right-hand side, row-major in smem) is solved in 32-row blocks.
+// For block rb the already-solved blocks contribute X_rb -= F_rb,cb X_cb on DMMA (m8n8k4, factor block
+// staged in smem, accumulators in registers over all cb), then one warp finishes the diagonal block with
+// a lane per column (substitution in the reference's order within the block). Phases:
+//   which 0 (V^b = U^{-1} L^{-1} B): lower unit (forward), then upper with diagonal (backward);
+//   which 1 (W^t = L^{-1} U^{-1} C): upper unit (backward), then lower with diagonal (forward).
+constexpr int kTB = 32;        // row block
+constexpr int kTC = 32;        // right-hand-side columns per CTA
+constexpr int kTXld = kTC + 4;  // X row stride (doubles): conflict-free DMMA B fragments
+constexpr int kTSld = kTB + 4;  // staged factor block stride: conflict-free A fragments
+
+struct TipCorner {
+    const double* f;
+    int corner;
+    long long ld;
+    int k;
+    __device__ __forceinline__ const double* col(int j) const { return f + (long long)(corner + j) * ld + corner + k; }
+};
+
+// stage F[i0:i0+ni, j0:j0+nj] into S[i][j] (zero-padded to 32 x 32)
+__device__ __forceinline__ void tip_stage(const TipCorner& F, double* __restrict__ S, int i0, int ni, int j0, int nj) {
+    for (int idx = threadIdx.x; idx < kTB * kTB; idx += blockDim.x) {
+        const int j = idx >> 5, i = idx & 31;  // lanes walk a factor column (contiguous rows)
+        S[i * kTSld + j] = (i < ni && j < nj) ? F.col(j0 + j)[i0 + i] : 0.0;
+    }
+}
+
+// acc (this warp's two 8 x 8 tiles of X_rb) -= S (32 x 32) * X[j0:j0+32, :]
+__device__ __forceinline__ void tip_mma(double (&acc)[2][2], const double* __restrict__ S,
+                                        const double* __restrict__ X, int j0, int nj, int tm, int tn0) {
+    const int lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
+#pragma unroll
+    for (int ks = 0; ks < kTB / 4; ++ks) {
+        const int kk = ks * 4 + lc;
+        const double a = -S[(tm * 8 + lr) * kTSld + kk];
+        const double bx0 = kk < nj ? X[(j0 + kk) * kTXld + tn0 * 8 + lr] : 0.0;
+        const double bx1 = kk < nj ? X[(j0 + kk) * kTXld + (tn0 + 1) * 8 + lr] : 0.0;
+        dmma_m8n8k4(acc[0][0], acc[0][1], a, bx0, acc[0][0], acc[0][1]);
+        dmma_m8n8k4(acc[1][0], acc[1][1], a, bx1, acc[1][0], acc[1][1]);
+    }
+}
+
+// One triangular phase over all row blocks. LOWER: blocks top-down, else bottom-up. UNIT: no division.
+template <bool LOWER, bool UNIT>
+__device__ __forceinline__ void tip_phase(const TipCorner& F, double* __restrict__ X, double* __restrict__ S, int w) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
+    const int nrb = (w + kTB - 1) / kTB;
+    // 16 DMMA tiles (8 x 8) of a 32 x 32 block: warp -> row tile tm, column tiles tn0, tn0+1
+    const int tm = warp >> 1, tn0 = (warp & 1) * 2;
+    for (int bi = 0; bi < nrb; ++bi) {
+        const int rb = LOWER ? bi : nrb - 1 - bi;
+        const int r0 = rb * kTB, nr = min(kTB, w - r0);
+        double acc[2][2];
+        const int ri = r0 + tm * 8 + lr;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            const int c = (tn0 + t) * 8 + 2 * lc;
+            acc[t][0] = ri < w ? X[ri * kTXld + c] : 0.0;
+            acc[t][1] = ri < w ? X[ri * kTXld + c + 1] : 0.0;
+        }
+        // acc layout: D[m = lr][n = 2 lc + e] = X(r0 + tm*8 + lr, (tn0+t)*8 + 2lc + e)
+        // off-diagonal blocks: the next factor block loads into registers while this one multiplies
+        double pre[kTB * kTB / 256];
+        auto fetch = [&](int bj) {
+            const int cb = LOWER ? bj : nrb - 1 - bj;
+            const int c0 = cb * kTB, nc = min(kTB, w - c0);
+#pragma unroll
+            for (int u = 0; u < kTB * kTB / 256; ++u) {
+                const int idx = threadIdx.x + 256 * u, j = idx >> 5, i = idx & 31;
+                pre[u] = (i < nr && j < nc) ? F.col(c0 + j)[r0 + i] : 0.0;
+            }
+        };
+        auto put = [&](double* Sb) {
+#pragma unroll
+            for (int u = 0; u < kTB * kTB / 256; ++u) {
+                const int idx = threadIdx.x + 256 * u, j = idx >> 5, i = idx & 31;
+                Sb[i * kTSld + j] = pre[u];
+            }
+        };
+        if (bi > 0) {
+            fetch(0);
+            __syncthreads();
+            put(S);
+        }
+        for (int bj = 0; bj < bi; ++bj) {
+            const int cb = LOWER ? bj : nrb - 1 - bj;
+            const int c0 = cb * kTB, nc = min(kTB, w - c0);
+            if (bj + 1 < bi) fetch(bj + 1);
+            __syncthreads();
+            tip_mma(acc, S, X, c0, nc, tm, tn0);
+            if (bj + 1 < bi) {
+                __syncthreads();
+                put(S);
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            const int c = (tn0 + t) * 8 + 2 * lc;
+            if (ri < w) {
+                X[ri * kTXld + c] = acc[t][0];
+                X[ri * kTXld + c + 1] = acc[t][1];
+            }
+        }
+        tip_stage(F, S, r0, nr, r0, nr);
+        __syncthreads();
+        if (warp == 0) {
+            // lane = column: substitution inside the diagonal block. 1/diag comes from one IEEE division per
+            // lane up front (shuffled), so the chain carries a multiply instead of a division.
+            double rd = 1.0;
+            if (!UNIT) rd = lane < nr ? 1.0 / S[lane * kTSld + lane] : 1.0;
+            double x[kTB];
+#pragma unroll
+            for (int i = 0; i < kTB; ++i) x[i] = i < nr ? X[(r0 + i) * kTXld + lane] : 0.0;
+            if (LOWER) {
+#pragma unroll
+                for (int j = 0; j < kTB; ++j) {
+                    if (!UNIT) x[j] *= __shfl_sync(0xffffffffu, rd, j);
+#pragma unroll
+                    for (int i = j + 1; i < kTB; ++i) x[i] = fma(-S[i * kTSld + j], x[j], x[i]);
+                }
+            } else {
+#pragma unroll
+                for (int jj = 0; jj < kTB; ++jj) {
+                    const int j = kTB - 1 - jj;
+                    if (!UNIT) x[j] *= __shfl_sync(0xffffffffu, rd, j);
+#pragma unroll
+                    for (int i = 0; i < j; ++i) x[i] = fma(-S[i * kTSld + j], x[j], x[i]);
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < kTB; ++i)
+                if (i < nr) X[(r0 + i) * kTXld + lane] = x[i];
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(256, 3)
+    k_spike_tips_blk(const TipJob* __restrict__ jobs, int k, int* __restrict__ nonfinite) {
+    extern __shared__ __align__(16) double sm[];
+    const int w = k;
+    const TipJob J = jobs[blockIdx.y];
+    const int c0 = blockIdx.x * kTC, nc = min(kTC, w - c0);
+    double* X = sm;                  // [w][kTXld]
+    double* S = sm + (size_t)w * kTXld;  // [32][kTSld]
+    const TipCorner F{J.f, J.corner, 2LL * k, k};
+    for (int idx = threadIdx.x; idx < w * kTC; idx += blockDim.x) {
+        const int r = idx / kTC, c = idx - r * kTC;
+        X[r * kTXld + c] = c < nc ? J.rhs[(long long)r * w + c0 + c] : 0.0;
+    }
+    __syncthreads();
+    if (J.which == 0) {
+        tip_phase<true, true>(F, X, S, w);
+        tip_phase<false, false>(F, X, S, w);
+    } else {
+        tip_phase<false, true>(F, X, S, w);
+        tip_phase<true, false>(F, X, S, w);
+    }
+    int bad = 0;
+    for (int idx = threadIdx.x; idx < w * kTC; idx += blockDim.x) {
+        const int r = idx / kTC, c = idx - r * kTC;
+        if (c < nc) {
+            const double v = X[r * kTXld + c];
+            if (!isfinite(v)) bad = 1;
+            J.out[(long long)r * w + c0 + c] = v;
+        }
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite + J.flag, 1);
+}
+
 void launch_spike_tips(const TipJob* d_jobs, int njobs, int k, int* nonfinite, cudaStream_t s) {
     if (njobs <= 0 || k == 0) return;
+    static const bool old = getenv("SAP_TIPS_OLD") != nullptr;
+    if (!old) {
+        const size_t bytes = sizeof(double) * ((size_t)k * kTXld + kTB * kTSld);
+        if (bytes <= 200 * 1024) {
+            SAP_CUDA(cudaFuncSetAttribute(k_spike_tips_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+            SAP_CUDA(cudaFuncSetAttribute(k_spike_tips_blk, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+            k_spike_tips_blk<<<dim3(ceil_div(k, kTC), njobs), 256, bytes, s>>>(d_jobs, k, nonfinite);
+            SAP_LAUNCHED();
+            return;
+        }
+    }
     const size_t bytes = sizeof(double) * ((size_t)k * kTipCols + k);
     if (bytes > 227 * 1024) throw InvalidArgument("spike tips: half-bandwidth too large");
     SAP_CUDA(cudaFuncSetAttribute(k_spike_tips, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
