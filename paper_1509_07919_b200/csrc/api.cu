@@ -282,21 +282,29 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
         h->ul.release();
     const int njobs = h->coupled ? 2 * p : p;
     std::vector<FactorJob> jobs(njobs);
+    // the default LU kernel reads the unfactored blocks straight from the band (no block copies)
+    const bool from_src = band_lu_reads_source(k);
+    const size_t w = 2 * (size_t)k + 1;
     for (int b = 0; b < p; ++b) {
         const int m = L.sizes[b];
         double* f = h->lu.get() + h->fst.block(b);
-        jobs[b] = FactorJob{f + k, 1, 2LL * k, m, k, h->norms.get() + b, h->boosts.get() + b};
+        const double* a = h->band_ptr + (size_t)L.offsets[b] * w;
+        jobs[b] = FactorJob{f + k, 1, 2LL * k, m, k, h->norms.get() + b, h->boosts.get() + b, from_src ? a + k : nullptr};
         if (h->coupled) {
             double* g = h->ul.get() + h->fst.block(b);
-            jobs[p + b] = FactorJob{g + (size_t)(m - 1) * (2 * k + 1) + k, -1, -2LL * k, m, k, h->norms.get() + b,
-                                    h->boosts.get() + p + b};
+            const size_t last = (size_t)(m - 1) * w + k;
+            jobs[p + b] = FactorJob{g + last, -1, -2LL * k, m, k, h->norms.get() + b, h->boosts.get() + p + b,
+                                    from_src ? a + last : nullptr};
         }
     }
     h->jobs.alloc(njobs);
     SAP_CUDA(cudaMemcpyAsync(h->jobs.get(), jobs.data(), sizeof(FactorJob) * njobs, cudaMemcpyHostToDevice, s));
     launch_block_norms(h->band_ptr, m_max, k, h->d_offsets.get(), p, nullptr, h->norms.get(), s);
-    launch_copy_blocks(h->band_ptr, k, h->d_offsets.get(), p, h->fst, h->lu.get(), h->coupled ? h->ul.get() : nullptr,
-                       s);
+    if (from_src)
+        launch_zero_pad(k, h->d_offsets.get(), p, h->fst, h->lu.get(), h->coupled ? h->ul.get() : nullptr, s);
+    else
+        launch_copy_blocks(h->band_ptr, k, h->d_offsets.get(), p, h->fst, h->lu.get(),
+                           h->coupled ? h->ul.get() : nullptr, s);
     SAP_CUDA(cudaEventRecord(h->ev[8], s));
     launch_band_lu(h->jobs.get(), njobs, k, h->opt.boost_eps, s);
     SAP_CUDA(cudaEventRecord(h->ev[9], s));
@@ -561,19 +569,27 @@ void setup_banded_dist(sap_handle* h, int n, int k, int row_lo, int row_hi, cons
         h->ul.release();
     const int njobs = h->coupled ? 2 * pl : pl;
     std::vector<FactorJob> jobs(njobs);
+    const bool from_src = band_lu_reads_source(k);
+    const size_t w = 2 * (size_t)k + 1;
     for (int b = 0; b < pl; ++b) {
         const int m = L.sizes[b];
+        const double* a = h->band_ptr + (size_t)boffs[b] * w;
         jobs[b] = FactorJob{h->lu.get() + h->fst.block(b) + k, 1, 2LL * k, m, k, h->norms.get() + b,
-                            h->boosts.get() + b};
-        if (h->coupled)
-            jobs[pl + b] = FactorJob{h->ul.get() + h->fst.block(b) + (size_t)(m - 1) * (2 * k + 1) + k, -1, -2LL * k, m,
-                                     k, h->norms.get() + b, h->boosts.get() + pl + b};
+                            h->boosts.get() + b, from_src ? a + k : nullptr};
+        if (h->coupled) {
+            const size_t last = (size_t)(m - 1) * w + k;
+            jobs[pl + b] = FactorJob{h->ul.get() + h->fst.block(b) + last, -1, -2LL * k, m, k, h->norms.get() + b,
+                                     h->boosts.get() + pl + b, from_src ? a + last : nullptr};
+        }
     }
     h->jobs.alloc(njobs);
     SAP_CUDA(cudaMemcpyAsync(h->jobs.get(), jobs.data(), sizeof(FactorJob) * njobs, cudaMemcpyHostToDevice, s));
     launch_block_norms(h->band_ptr, m_max, k, h->d_boffs.get(), pl, nullptr, h->norms.get(), s);
-    launch_copy_blocks(h->band_ptr, k, h->d_boffs.get(), pl, h->fst, h->lu.get(), h->coupled ? h->ul.get() : nullptr,
-                       s);
+    if (from_src)
+        launch_zero_pad(k, h->d_boffs.get(), pl, h->fst, h->lu.get(), h->coupled ? h->ul.get() : nullptr, s);
+    else
+        launch_copy_blocks(h->band_ptr, k, h->d_boffs.get(), pl, h->fst, h->lu.get(),
+                           h->coupled ? h->ul.get() : nullptr, s);
     SAP_CUDA(cudaEventRecord(h->ev[8], s));
     launch_band_lu(h->jobs.get(), njobs, k, h->opt.boost_eps, s);
     SAP_CUDA(cudaEventRecord(h->ev[9], s));

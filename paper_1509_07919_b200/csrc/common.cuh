@@ -54,6 +54,7 @@ struct FactorJob {
     int k;            // half-bandwidth (dense: w-1)
     const double* scale;  // boost scale (block infinity norm), device pointer
     int* boosts;      // device counter (written, not accumulated)
+    const double* src = nullptr;  // unfactored block in the same strided view (nullptr: in place, base)
 };
 
 // Per-block strided band store used for every factor buffer (LU, UL, reduced
@@ -88,7 +89,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 __device__ __forceinline__ void dmma_m8n8k4(double& d0, double& d1, double a, double b, double c0, double c1) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};\n"
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};\n"
                  : "=d"(d0), "=d"(d1)
                  : "d"(a), "d"(b), "d"(c0), "d"(c1));
 }

@@ -106,6 +106,46 @@ void launch_copy_blocks(const double* band, int k, const int* d_offsets, int p, 
     SAP_LAUNCHED();
 }
 
+// The slots of a BandStore block that lie outside the block's matrix (the top-left and bottom-right
+// corner triangles of its band, the leading pad and the trailing slack) zeroed: what k_copy_blocks
+// leaves in them, for the LU kernels that read the unfactored band from its source instead.
+__global__ void k_zero_pad(int k, const int* __restrict__ offs, long long pstride, int pad, double* __restrict__ lu,
+                           double* __restrict__ ul) {
+    const int b = blockIdx.y;
+    const long long w = 2LL * k + 1;
+    const int m = offs[b + 1] - offs[b];
+    double* f0 = lu + (long long)b * pstride;
+    double* f1 = ul ? ul + (long long)b * pstride : nullptr;
+    const long long corner = (long long)k * w;
+    const long long tail0 = pad + (long long)m * w;
+    const long long n_items = 2 * corner + pad + (pstride - tail0);
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n_items;
+         q += (long long)gridDim.x * blockDim.x) {
+        long long d = -1;
+        if (q < 2 * corner) {
+            const long long qq = q < corner ? q : q - corner;
+            const long long c0 = qq / w, slot = qq - c0 * w;
+            const long long c = q < corner ? c0 : m - 1 - c0;
+            if (c < 0 || c >= m) continue;
+            const long long r = c - k + slot;
+            if (r >= 0 && r < m) continue;
+            d = pad + c * w + slot;
+        } else {
+            const long long t = q - 2 * corner;
+            d = t < pad ? t : tail0 + (t - pad);
+        }
+        f0[d] = 0.0;
+        if (f1) f1[d] = 0.0;
+    }
+}
+
+void launch_zero_pad(int k, const int* d_offsets, int p, const BandStore& st, double* lu, double* ul, cudaStream_t s) {
+    const long long items = 2LL * k * (2LL * k + 1) + st.pstride;
+    dim3 grid((unsigned)std::min<long long>((items + 255) / 256, 64), (unsigned)p);
+    k_zero_pad<<<grid, 256, 0, s>>>(k, d_offsets, st.pstride, st.pad, lu, ul);
+    SAP_LAUNCHED();
+}
+
 // ---------------------------------------------------------------------------
 // Blocked LU.
 

@@ -52,7 +52,11 @@ struct Lu {
     long long rs, cs;
     int m, K, B, pld, uld;
     double bv;
+    const double* src;  // unfactored entries (k_band_lu_res reads every never-updated entry from here)
     __device__ __forceinline__ double* at(int i, int c) const { return base + (long long)i * rs + (long long)c * cs; }
+    __device__ __forceinline__ const double* src_at(int i, int c) const {
+        return src + (long long)i * rs + (long long)c * cs;
+    }
     __device__ __forceinline__ bool inband(int i, int c) const { return i - c <= K && c - i <= K; }
 };
 
@@ -954,13 +958,57 @@ __device__ __forceinline__ void res_fetch(const Lu& L, double* __restrict__ Pb, 
     for (int idx = threadIdx.x - t0; idx < ph * np; idx += nt) {
         const int c = idx / ph, r = idx - c * ph;
         if (r < cov && c < cov) continue;
-        if (L.inband(r, c)) cp_async8(Pb + c * pld + r, L.at(jp + r, jp + c));
+        if (L.inband(r, c)) cp_async8(Pb + c * pld + r, L.src_at(jp + r, jp + c));
     }
     for (int idx = threadIdx.x - t0; idx < Rn * 32; idx += nt) {
         const int r = idx & 31, c = idx >> 5;
         if (r >= np || (r < cov && np + c < cov)) continue;
-        if (np + c - r <= L.K) cp_async8(Ab + r * uld + c, L.at(jp + r, jp + np + c));
+        if (np + c - r <= L.K) cp_async8(Ab + r * uld + c, L.src_at(jp + r, jp + np + c));
     }
+}
+
+// tile_load for k_band_lu_res: A22 entries at window coordinates (i, c) with i >= fr or c >= fr have never
+// been updated (they entered the window this step) and come from the unfactored source view; the rest
+// come from the factor store, where the previous step's update left them.
+__device__ __forceinline__ void tile_load_fr(const Lu& L, const TileCtx& T, int t, double (&acc)[2][kTQ][2], int fr) {
+    const int row0 = T.r_lo + (t / T.tcols) * kTileR, col0 = T.c_lo + (t % T.tcols) * kTileC;
+    if (row0 + kTileR <= fr && col0 + kTileC <= fr) {
+        tile_load(L, T, t, acc);
+        return;
+    }
+    const int lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
+    const int ib = row0 + 2 * lc, cb = col0 + lr;
+    const long long rs = L.rs, ra8 = 8 * rs, cq8 = 8 * L.cs;
+    const int gi = T.row_org + ib, gc = T.col_org + cb;
+    const double* d00 = L.at(gi, gc);
+    const double* s00 = L.src_at(gi, gc);
+    const double* dlo = rs > 0 ? d00 : d00 - 1;
+    const double* slo = rs > 0 ? s00 : s00 - 1;
+    const bool full = row0 + kTileR <= T.r_hi && col0 + kTileC <= T.c_hi && row0 >= T.band_top;
+    if (full && (rs == 1 || rs == -1) && (fr & 1) == 0 &&
+        (((reinterpret_cast<uintptr_t>(dlo) | reinterpret_cast<uintptr_t>(slo)) & 15) == 0)) {
+        // row pairs (ib + 8a, ib + 8a + 1) never straddle an even fr: one 16-byte load per pair from its side
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int q = 0; q < kTQ; ++q) {
+                const bool fresh = ib + a * 8 >= fr || cb + q * 8 >= fr;
+                const double2 v = __ldcg(reinterpret_cast<const double2*>((fresh ? slo : dlo) + a * ra8 + q * cq8));
+                acc[a][q][0] = rs > 0 ? v.x : v.y;
+                acc[a][q][1] = rs > 0 ? v.y : v.x;
+            }
+        return;
+    }
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int q = 0; q < kTQ; ++q)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int i = ib + a * 8 + e, c = cb + q * 8;
+                const long long o = a * ra8 + e * rs + q * cq8;
+                acc[a][q][e] = tile_ok(L, T, i, c) ? __ldcg((i >= fr || c >= fr ? s00 : d00) + o) : 0.0;
+            }
 }
 
 // A22 -= L21 U12 over 16 x 32 warp tiles; panel-(s+1) columns -> Pn, A12(s+1) rows -> An, rest -> global.
@@ -969,7 +1017,7 @@ __device__ __forceinline__ void res_fetch(const Lu& L, double* __restrict__ Pb, 
 // hides under the DMMA work (in-flight cp.async would stall the next step's shared loads).
 __device__ __noinline__ void res_bulk(const Lu& L, const double* __restrict__ P, const double* __restrict__ U, int nb,
                                       int ja, int R, int nbn, int phn, int Rn, double* __restrict__ Pn,
-                                      double* __restrict__ An) {
+                                      double* __restrict__ An, int fr) {
     const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
     const int pld = L.pld, uld = L.uld;
@@ -984,10 +1032,10 @@ __device__ __noinline__ void res_bulk(const Lu& L, const double* __restrict__ P,
             pf[i] = 0.0;
             if (f < 32) {  // panel column f, row R + lane
                 const int r = R + lane;
-                if (f < nbn && r < phn && r - f <= L.K) pf[i] = __ldcg(L.at(ja + r, ja + f));
+                if (f < nbn && r < phn && r - f <= L.K) pf[i] = __ldcg(L.src_at(ja + r, ja + f));
             } else if (f < 64) {  // A12 column R - nbn + (f - 32), row lane
                 const int c = R - nbn + (f - 32);
-                if (c < Rn && lane < nbn && nbn + c - lane <= L.K) pf[i] = __ldcg(L.at(ja + lane, ja + nbn + c));
+                if (c < Rn && lane < nbn && nbn + c - lane <= L.K) pf[i] = __ldcg(L.src_at(ja + lane, ja + nbn + c));
             }
         }
     }
@@ -997,7 +1045,7 @@ __device__ __noinline__ void res_bulk(const Lu& L, const double* __restrict__ P,
         const int ksteps = (nb + 3) >> 2;
         double acc[2][kTQ][2];
         for (int t = warp; t < ntiles; t += nw) {
-            tile_load(L, T, t, acc);
+            tile_load_fr(L, T, t, acc, fr);
             const int row0 = (t / T.tcols) * kTileR, col0 = (t % T.tcols) * kTileC;
             const bool a1 = row0 + 8 < R;
             bool qv[kTQ];
@@ -1118,7 +1166,7 @@ __global__ void __launch_bounds__(kLuThreads, 1)
     __shared__ double s_rcp[B];
     const FactorJob J = jobs[blockIdx.x];
     const double scale = *J.scale;
-    Lu L{J.base, J.rs, J.cs, J.m, J.k, B, pld, uld, eps * (scale > 0 ? scale : 1.0)};
+    Lu L{J.base, J.rs, J.cs, J.m, J.k, B, pld, uld, eps * (scale > 0 ? scale : 1.0), J.src ? J.src : J.base};
     const int psz = B * pld, usz = B * uld;
     const int tid = threadIdx.x, warp = tid >> 5;
     const int m = L.m, K = L.K;
@@ -1187,7 +1235,8 @@ __global__ void __launch_bounds__(kLuThreads, 1)
         }
         LU_TRACE(step, 4, tid == 0);
         // 4. trailing update (next panel / A12 land in smem) + step s+1's new band entries
-        res_bulk(L, P, A, nb, ja, R, nbn, phn, Rn, Pn, An);
+        // window entries at or beyond the previous step's window edge (jb + min(K, m - jb)) are fresh
+        res_bulk(L, P, A, nb, ja, R, nbn, phn, Rn, Pn, An, jb == 0 ? 0 : min(K, m - jb) - nb);
         cp_async_wait_all();
         LU_TRACE(step, 8, tid == 0);
         __syncthreads();
@@ -1649,6 +1698,19 @@ bool launch_band_lu_ws(const FactorJob* d_jobs, int njobs, int max_k, double eps
     k_band_lu_seq<B><<<njobs, kLuThreads, bytes, s>>>(d_jobs, eps, pld, uld);
     SAP_LAUNCHED();
     return true;
+}
+
+// True when launch_band_lu_ws will run k_band_lu_res for this bandwidth: that kernel reads every
+// never-updated entry from FactorJob::src, so the factor stores need no initial copy of the band
+// (only their out-of-matrix slots zeroed, launch_zero_pad).
+bool band_lu_reads_source(int max_k) {
+    if (getenv("SAP_LU_SIMPLE") || getenv("SAP_LU_EXT") || getenv("SAP_LU_LA") || getenv("SAP_LU_WS") ||
+        getenv("SAP_LU_SEQ") || getenv("SAP_LU_LA2"))
+        return false;
+    constexpr int B = 32;
+    if (max_k < 1 || max_k > 256 - B) return false;
+    const int pldr = pad_ld(B + max_k), uldr = pad_ld(max_k);
+    return sizeof(double) * (size_t)(2 * B * pldr + 2 * B * uldr) <= 226 * 1024;
 }
 
 }  // namespace sapgpu
