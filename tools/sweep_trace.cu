@@ -1,4 +1,5 @@
-// Driver: config-2 SaP-D setup + one preconditioner apply with the traced sweep; prints the per-chunk timeline.
+// Driver: config-2 SaP-D setup + one preconditioner apply with the traced pair sweep (forward chunks 8..39 of
+// block 0); prints per-chunk clock64 deltas, finisher CTA and helper CTA separately (different SMs).
 #include <cstdio>
 #include <vector>
 #include "../include/sap_gpu.h"
@@ -12,12 +13,14 @@ int main() {
     sap_setup_banded(h, n, k, band.data(), 0);
     sap_apply_preconditioner(h, rhs.data(), out.data(), 0);
     sap_apply_preconditioner(h, rhs.data(), out.data(), 0);
-    long long t[24 * 8];
+    long long t[32 * 12];
     sapgpu::read_sweep_trace(t);
-    printf("chunk: wait_done barA phase1(w0) phase1(w1) phase1(w15) barB | next\n");
-    for (int c = 1; c < 23; ++c) {
-        long long b = t[c * 8];
-        printf("%2d: %6lld %6lld %6lld %6lld %6lld %6lld | %6lld\n", c, t[c*8+1]-b, t[c*8+2]-b, t[c*8+3]-b, t[c*8+4]-b, t[c*8+5]-b, t[c*8+6]-b, t[(c+1)*8]-b);
+    printf("F (relative to w0 X-sync of the chunk): w0 Y-arrive | w1: start slab bar5 hpart wbuf || H (rel. to start): slab+sync sent | H period\n");
+    for (int c = 0; c < 31; ++c) {
+        const long long* r = t + c * 12;
+        long long b = r[0];
+        printf("%2d: %6lld | %6lld %6lld %6lld %6lld %6lld | F period %6lld || %6lld %6lld | %6lld\n", c + 8, r[1] - b, r[2] - b, r[3] - b,
+               r[4] - b, r[5] - b, r[6] - b, r[12] - b, r[8] - r[7], r[9] - r[7], r[12 + 7] - r[7]);
     }
     sap_destroy(h);
 }
