@@ -807,7 +807,8 @@ __device__ __noinline__ void res_diag8(double* __restrict__ P, int pld, double b
 // Per element the updates arrive in ascending column order with the same FMAs as pg_col / pg_u12.
 template <bool FULL>
 __device__ __noinline__ void res_sub(double* __restrict__ P, double* __restrict__ A, int pld, int uld, int q0, int nq_rt,
-                                     int nb, int ph, int R, const double* __restrict__ s_rcp, int step) {
+                                     int nb, int ph, int R, double* __restrict__ s_rcp, int step, double bv,
+                                     int* boost_ctr) {
     const int nq = FULL ? 8 : nq_rt;
     const int tid = threadIdx.x;
     const int q1 = q0 + 8;
@@ -859,34 +860,79 @@ __device__ __noinline__ void res_sub(double* __restrict__ P, double* __restrict_
         // rank-8 updates on DMMA (8 x 8 tiles, two k4 steps): the panel's rows [q1, ph) x columns [q1, nb)
         // and A12's rows [q1, nb) x columns [0, R). Transposed product as in tile_compute_store:
         // D^T = C^T - U^T L^T, so each thread's accumulator pair is two adjacent rows of one column.
+        // Work unit = a strip of up to three independent 8 x 8 tiles sharing one operand per k4 step:
+        // a panel row tile across the sub-panel's remaining columns (shared L fragment), or an A12
+        // column tile down its remaining rows (shared U fragment). Warp 0 takes only strip 0 (rows
+        // [q1, q1+8): it holds the next sub-panel's diagonal block) and then factors that block
+        // (res_diag8 by its lane 0) while warps 1..15 finish the other strips.
         const int lane = tid & 31, warp = tid >> 5, lr = lane >> 2, lc = lane & 3;
-        const int pct = (nb - q1 + 7) >> 3, np_t = ((ph - q1 + 7) >> 3) * pct;
-        const int act8 = (R + 7) >> 3, na_t = ((nb - q1 + 7) >> 3) * act8;
-        for (int t = warp; t < np_t + na_t; t += blockDim.x >> 5) {
-            const bool pan = t < np_t;
-            const int t2 = pan ? t : t - np_t, tc = pan ? pct : act8;
-            const int i0 = q1 + (t2 / tc) * 8, j0 = (pan ? q1 : 0) + (t2 % tc) * 8;
-            const int rmax = pan ? ph : nb, cmax = pan ? nb : R;
-            const int j = j0 + lr;
-            double* cp = pan ? P + j * pld : A + j;      // C(i, j) = cp[i * cs]
-            const int cs = pan ? 1 : uld;
-            const double* up = pan ? P + j * pld + q0 : A + q0 * uld + j;  // U(k, j) = up[k * us]
-            const int us = pan ? 1 : uld;
-            const int ib = i0 + 2 * lc;
-            double c0 = (ib < rmax && j < cmax) ? cp[ib * cs] : 0.0;
-            double c1 = (ib + 1 < rmax && j < cmax) ? cp[(ib + 1) * cs] : 0.0;
-            const int il = i0 + lr;
+        const int nq8 = (nb - q1) >> 3;  // remaining sub-panel columns / U rows, in tiles (nb == B: exact)
+        const int prt = (ph - q1 + 7) >> 3, act8 = (R + 7) >> 3;
+        const int nw = blockDim.x >> 5;
+        for (int sidx = warp == 0 ? 0 : warp; sidx < prt + act8; sidx += warp == 0 ? prt + act8 : nw - 1) {
+            double c[3][2];
+            if (sidx < prt) {
+                const int i0 = q1 + sidx * 8, il = i0 + lr, ib = i0 + 2 * lc;
 #pragma unroll
-            for (int ks = 0; ks < 2; ++ks) {
-                const int k = ks * 4 + lc;
-                const double av = j < cmax ? up[k * us] : 0.0;
-                const double bv = il < rmax ? -P[(q0 + k) * pld + il] : 0.0;
-                dmma_m8n8k4(c0, c1, av, bv, c0, c1);
+                for (int jt = 0; jt < 3; ++jt)
+                    if (jt < nq8) {
+                        const double* cp = P + (q1 + jt * 8 + lr) * pld;
+                        c[jt][0] = ib < ph ? cp[ib] : 0.0;
+                        c[jt][1] = ib + 1 < ph ? cp[ib + 1] : 0.0;
+                    }
+#pragma unroll
+                for (int ks = 0; ks < 2; ++ks) {
+                    const int k = ks * 4 + lc;
+                    const double bv8 = il < ph ? -P[(q0 + k) * pld + il] : 0.0;
+#pragma unroll
+                    for (int jt = 0; jt < 3; ++jt)
+                        if (jt < nq8) {
+                            const double av = P[(q1 + jt * 8 + lr) * pld + q0 + k];
+                            dmma_m8n8k4(c[jt][0], c[jt][1], av, bv8, c[jt][0], c[jt][1]);
+                        }
+                }
+#pragma unroll
+                for (int jt = 0; jt < 3; ++jt)
+                    if (jt < nq8) {
+                        double* cp = P + (q1 + jt * 8 + lr) * pld;
+                        if (ib < ph) cp[ib] = c[jt][0];
+                        if (ib + 1 < ph) cp[ib + 1] = c[jt][1];
+                    }
+            } else {
+                const int j = (sidx - prt) * 8 + lr;
+                const bool jok = j < R;
+#pragma unroll
+                for (int it = 0; it < 3; ++it)
+                    if (it < nq8) {
+                        const int ib = q1 + it * 8 + 2 * lc;
+                        c[it][0] = jok ? A[ib * uld + j] : 0.0;
+                        c[it][1] = jok ? A[(ib + 1) * uld + j] : 0.0;
+                    }
+#pragma unroll
+                for (int ks = 0; ks < 2; ++ks) {
+                    const int k = ks * 4 + lc;
+                    const double av = jok ? A[(q0 + k) * uld + j] : 0.0;
+#pragma unroll
+                    for (int it = 0; it < 3; ++it)
+                        if (it < nq8) {
+                            const double bv8 = -P[(q0 + k) * pld + q1 + it * 8 + lr];
+                            dmma_m8n8k4(c[it][0], c[it][1], av, bv8, c[it][0], c[it][1]);
+                        }
+                }
+                if (jok) {
+#pragma unroll
+                    for (int it = 0; it < 3; ++it)
+                        if (it < nq8) {
+                            const int ib = q1 + it * 8 + 2 * lc;
+                            A[ib * uld + j] = c[it][0];
+                            A[(ib + 1) * uld + j] = c[it][1];
+                        }
+                }
             }
-            if (j < cmax) {
-                if (ib < rmax) cp[ib * cs] = c0;
-                if (ib + 1 < rmax) cp[(ib + 1) * cs] = c1;
-            }
+        }
+        if (warp == 0 && nq8 > 0) {
+            __syncwarp();
+            if (lane == 0) res_diag8<true>(P, pld, bv, q1, 8, s_rcp, boost_ctr);
         }
         return;
     }
@@ -965,6 +1011,28 @@ __device__ __forceinline__ void res_fetch(const Lu& L, double* __restrict__ Pb, 
         if (r >= np || (r < cov && np + c < cov)) continue;
         if (np + c - r <= L.K) cp_async8(Ab + r * uld + c, L.src_at(jp + r, jp + np + c));
     }
+}
+
+// L2 prefetch of the unfactored entries that step s+1 reads for the first time (HBM -> L2 one step
+// ahead): band rows [ja+R, ja+R+nb) of every column they meet, and columns [ja+R, ja+R+nb) of the rows
+// above them. One contiguous run (|rs| == 1) per column and bulk prefetch instruction.
+__device__ __forceinline__ void prefetch_run(const Lu& L, int c, int r0, int r1) {
+    r0 = max(r0, c - L.K);
+    r1 = min(r1, min(c + L.K + 1, L.m));
+    if (r0 >= r1) return;
+    const double* a = L.rs > 0 ? L.src_at(r0, c) : L.src_at(r1 - 1, c);
+    uintptr_t lo = reinterpret_cast<uintptr_t>(a) & ~uintptr_t(15);
+    uintptr_t hi = (reinterpret_cast<uintptr_t>(a) + 8 * (r1 - r0) + 15) & ~uintptr_t(15);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"((unsigned)(hi - lo)) : "memory");
+}
+__device__ __forceinline__ void prefetch_fresh(const Lu& L, int ja, int R, int nb) {
+    const int e = ja + R;  // first row/column the next step sees fresh
+    if (e >= L.m) return;
+    const int t = threadIdx.x;
+    const int ncol = min(e + nb, L.m) - ja;  // columns [ja, e+nb): their rows [e, e+nb)
+    if (t < ncol) prefetch_run(L, ja + t, e, e + nb);
+    const int t2 = t - ncol;                 // columns [e, e+nb): rows [ja+nb, e)
+    if (t2 >= 0 && t2 < min(nb, L.m - e)) prefetch_run(L, e + t2, ja + nb, e);
 }
 
 // tile_load for k_band_lu_res: A22 entries at window coordinates (i, c) with i >= fr or c >= fr have never
@@ -1196,25 +1264,27 @@ __global__ void __launch_bounds__(kLuThreads, 1)
         LU_TRACE(step, 0, tid == 0);
         // 1-2. blocked panel + U12: per 8-column sub-panel, the diagonal block (one thread) then the L rows,
         //      U rows and rank-8 updates (all threads); warps 8-15 prefetch step s+1's new band entries meanwhile
-        for (int q0 = 0; q0 < nb; q0 += 8) {
-            const int nq = min(8, nb - q0);
-            const bool full = nb == B;
-            if (tid == 0) {
-                if (full)
-                    res_diag8<true>(P, pld, L.bv, q0, nq, s_rcp, &s_boosts);
-                else
-                    res_diag8<false>(P, pld, L.bv, q0, nq, s_rcp, &s_boosts);
+        if (nb == B) {
+            // full panel: diagonal block 0 here, every later one inside the previous res_sub (overlapped)
+            if (tid == 0) res_diag8<true>(P, pld, L.bv, 0, 8, s_rcp, &s_boosts);
+            __syncthreads();
+            LU_TRACE(step, 5, tid == 0);
+            for (int q0 = 0; q0 < nb; q0 += 8) {
+                res_sub<true>(P, A, pld, uld, q0, 8, nb, ph, R, s_rcp, step, L.bv, &s_boosts);
+                __syncthreads();
+                if (q0 == 0) LU_TRACE(step, 6, tid == 0);
             }
-            __syncthreads();
-            if (q0 == 0) LU_TRACE(step, 5, tid == 0);
-            if (full)
-                res_sub<true>(P, A, pld, uld, q0, nq, nb, ph, R, s_rcp, step);
-            else
-                res_sub<false>(P, A, pld, uld, q0, nq, nb, ph, R, s_rcp, step);
-            __syncthreads();
-            if (q0 == 0) LU_TRACE(step, 6, tid == 0);
+        } else {
+            for (int q0 = 0; q0 < nb; q0 += 8) {
+                const int nq = min(8, nb - q0);
+                if (tid == 0) res_diag8<false>(P, pld, L.bv, q0, nq, s_rcp, &s_boosts);
+                __syncthreads();
+                res_sub<false>(P, A, pld, uld, q0, nq, nb, ph, R, s_rcp, step, L.bv, &s_boosts);
+                __syncthreads();
+            }
         }
         LU_TRACE(step, 3, tid == 0);
+        if (ja < m) prefetch_fresh(L, ja, R, nb);
         // 3. panel (L11\U11, L21) and U12 to global: a warp per column, lanes down the rows
         {
             const int lane = tid & 31;
