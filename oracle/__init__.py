@@ -23,7 +23,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 _ORACLE = os.path.join(HERE, "libsap_oracle.so")
-_REF = os.path.join(HERE, "_ref", "libsapref.so")
+_REF = os.path.join(HERE, "_ref", os.environ.get("SAP_REF_LIB", "libsapref.so"))  # tools may pick libsapref_fma.so
 
 _dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
 _ip = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")

@@ -97,7 +97,8 @@ struct sap_handle {
     DevBuf<int> boosts, rbar_boosts, nonfinite;
     DevBuf<FactorJob> jobs, rjobs;
     BandStore fst, rst;                  // LU/UL and reduced-block stores
-    DevBuf<double> dinv, rdinv;          // chunk inverses for the sweeps
+    DevBuf<double> dinv, rdinv;          // chunk inverses (+ triangles) for the sweeps
+    DevBuf<unsigned long long> kappa;    // [0] LU plan, [1] reduced plan: chunk-triangle condition estimates
     SweepPlan<double> lplan, rplan;      // block sweeps over LU and over the reduced blocks
     // CSR operator
     bool csr = false;
@@ -161,6 +162,23 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
 
 // M^{-1}: the reference's apply_preconditioner (spike.hpp:304-351) over the
 // handle's device factors. in/out are device pointers; they may alias.
+// Sweeps on ill-conditioned chunk triangles (max ||T|| ||T^-1|| over chunks above kSubstKappa: element
+// growth at low diagonal dominance) solve them by substitution (k_sweep_tma<SUBST>); well conditioned
+// factors keep the chunk-inverse product. SAP_SWEEP_TRI=subst/inverse forces the choice.
+constexpr double kSubstKappa = 1e2;
+void choose_triangle_solve(sap_handle* h) {
+    unsigned long long kb[2] = {0, 0};
+    if (h->kappa.get()) SAP_CUDA(cudaMemcpy(kb, h->kappa.get(), sizeof(kb), cudaMemcpyDeviceToHost));
+    double kap[2];
+    std::memcpy(kap, kb, sizeof(kap));
+    const char* force = getenv("SAP_SWEEP_TRI");
+    h->lplan.subst = force ? force[0] == 's' : kap[0] > kSubstKappa;
+    h->rplan.subst = force ? force[0] == 's' : kap[1] > kSubstKappa;
+    if (getenv("SAP_DEBUG_KAPPA"))
+        fprintf(stderr, "sap: chunk-triangle condition estimates LU %.3e reduced %.3e -> substitution %d %d\n", kap[0],
+                kap[1], (int)h->lplan.subst, (int)h->rplan.subst);
+}
+
 void apply_m_dist(sap_handle* h, const double* in, double* out);
 void apply_a_dist(sap_handle* h, const double* in, double* out);
 
@@ -299,6 +317,8 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
     }
     h->jobs.alloc(njobs);
     SAP_CUDA(cudaMemcpyAsync(h->jobs.get(), jobs.data(), sizeof(FactorJob) * njobs, cudaMemcpyHostToDevice, s));
+    h->kappa.alloc(2);
+    SAP_CUDA(cudaMemsetAsync(h->kappa.get(), 0, 2 * sizeof(unsigned long long), s));
     launch_block_norms(h->band_ptr, m_max, k, h->d_offsets.get(), p, nullptr, h->norms.get(), s);
     if (from_src)
         launch_zero_pad(k, h->d_offsets.get(), p, h->fst, h->lu.get(), h->coupled ? h->ul.get() : nullptr, s);
@@ -318,6 +338,7 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
         lp.k = k;
         h->dinv.alloc(std::max<size_t>(sweep_dinv_elems(lp), 1));
         plan_sweeps(lp, h->dinv.get());
+        lp.kappa = h->kappa.get();
         launch_chunk_inverses(lp, s);
     }
     SAP_CUDA(cudaEventRecord(h->ev[2], s));
@@ -389,11 +410,14 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
             rp.k = k - 1;
             h->rdinv.alloc(std::max<size_t>(sweep_dinv_elems(rp), 1));
             plan_sweeps(rp, h->rdinv.get());
-            launch_chunk_inverses(rp, s);
+            rp.kappa = h->kappa.get() + 1;
+            rp.kappa = h->kappa.get() + 1;
+        launch_chunk_inverses(rp, s);
         }
         SAP_CUDA(cudaEventRecord(h->ev[5], s));
     }
     SAP_CUDA(cudaStreamSynchronize(s));
+    choose_triangle_solve(h);
     h->rep.t_dtransf = ev_ms(h->ev[0], h->ev[1]) * 1e-3;
     h->rep.t_lu = ev_ms(h->ev[1], h->ev[2]) * 1e-3;
     h->rep.t_factor_kernel = ev_ms(h->ev[8], h->ev[9]) * 1e-3;
@@ -584,6 +608,8 @@ void setup_banded_dist(sap_handle* h, int n, int k, int row_lo, int row_hi, cons
     }
     h->jobs.alloc(njobs);
     SAP_CUDA(cudaMemcpyAsync(h->jobs.get(), jobs.data(), sizeof(FactorJob) * njobs, cudaMemcpyHostToDevice, s));
+    h->kappa.alloc(2);
+    SAP_CUDA(cudaMemsetAsync(h->kappa.get(), 0, 2 * sizeof(unsigned long long), s));
     launch_block_norms(h->band_ptr, m_max, k, h->d_boffs.get(), pl, nullptr, h->norms.get(), s);
     if (from_src)
         launch_zero_pad(k, h->d_boffs.get(), pl, h->fst, h->lu.get(), h->coupled ? h->ul.get() : nullptr, s);
@@ -603,6 +629,7 @@ void setup_banded_dist(sap_handle* h, int n, int k, int row_lo, int row_hi, cons
         lp.k = k;
         h->dinv.alloc(std::max<size_t>(sweep_dinv_elems(lp), 1));
         plan_sweeps(lp, h->dinv.get());
+        lp.kappa = h->kappa.get();
         launch_chunk_inverses(lp, s);
     }
     SAP_CUDA(cudaEventRecord(h->ev[2], s));
@@ -703,10 +730,12 @@ void setup_banded_dist(sap_handle* h, int n, int k, int row_lo, int row_hi, cons
         rp.k = w - 1;
         h->rdinv.alloc(std::max<size_t>(sweep_dinv_elems(rp), 1));
         plan_sweeps(rp, h->rdinv.get());
+        rp.kappa = h->kappa.get() + 1;
         launch_chunk_inverses(rp, s);
         SAP_CUDA(cudaEventRecord(h->ev[5], s));
     }
     SAP_CUDA(cudaStreamSynchronize(s));
+    choose_triangle_solve(h);
     h->rep.t_dtransf = ev_ms(h->ev[0], h->ev[1]) * 1e-3;
     h->rep.t_lu = ev_ms(h->ev[1], h->ev[2]) * 1e-3;
     h->rep.t_factor_kernel = ev_ms(h->ev[8], h->ev[9]) * 1e-3;

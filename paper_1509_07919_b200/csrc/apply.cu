@@ -91,7 +91,8 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // lane j builds column j by substitution on e_j.
 template <class T, int TR>
 __global__ void k_chunk_inverses(const T* __restrict__ f0, long long pstride, int pad, const int* __restrict__ offs,
-                                 int k, T* __restrict__ dinv, int nch_max) {
+                                 int k, T* __restrict__ dinv, int nch_max, T* __restrict__ tri,
+                                 unsigned long long* __restrict__ kappa_bits) {
     __shared__ T blk[TR][TR + 1];       // blk[j][i] = F(i0+i, i0+j)
     __shared__ T X[2][TR][TR + 1];      // X[dir][j][i]
     const int b = blockIdx.y, q = blockIdx.x;
@@ -132,9 +133,36 @@ __global__ void k_chunk_inverses(const T* __restrict__ f0, long long pstride, in
     }
     __syncthreads();
     T* out = dinv + ((long long)b * nch_max + q) * 2 * TR * TR;
+    T* tout = tri + ((long long)b * nch_max + q) * 2 * TR * TR;
     for (int idx = threadIdx.x; idx < 2 * TR * TR; idx += blockDim.x) {
-        const int d = idx / (TR * TR), r = idx % (TR * TR);
-        out[idx] = X[d][r / TR][r % TR];
+        const int d = idx / (TR * TR), r = idx % (TR * TR), jj = r / TR, ii = r % TR;
+        out[idx] = X[d][jj][ii];
+        // the triangle itself (unit lower / upper with diagonal), for the substitution sweeps; the upper
+        // triangle's unused strictly-lower slots carry 1/d_ii (tri_rcp_slot) for the quotient
+        T v = d == 0 ? (jj < ii ? blk[jj][ii] : (jj == ii ? T(1) : T(0))) : (jj >= ii ? blk[jj][ii] : T(0));
+        if (d == 1) {
+            const int r = jj == 0 ? ii : -1;  // column 0 rows 1..TR-1 hold 1/d for rows 1..TR-1
+            if (r >= 1) v = X[1][r][r];
+            if (jj == TR - 2 && ii == TR - 1) v = X[1][0][0];  // 1/d_00
+        }
+        tout[idx] = v;
+    }
+    // infinity-norm condition estimate ||T|| ||T^{-1}|| of both triangles (max over chunks, as double bits)
+    {
+        const int d = threadIdx.x >> 5, i = threadIdx.x & 31;
+        double rt = 0.0, ri = 0.0;
+        if (i < TR)
+            for (int jj = 0; jj < TR; ++jj) {
+                const T tv = d == 0 ? (jj < i ? blk[jj][i] : (jj == i ? T(1) : T(0))) : (jj >= i ? blk[jj][i] : T(0));
+                rt += fabs((double)tv);
+                ri += fabs((double)X[d][jj][i]);
+            }
+        for (int o = 16; o > 0; o >>= 1) {
+            rt = fmax(rt, __shfl_xor_sync(0xffffffffu, rt, o));
+            ri = fmax(ri, __shfl_xor_sync(0xffffffffu, ri, o));
+        }
+        const double kap = rt * ri;
+        if (i == 0 && isfinite(kap)) atomicMax(kappa_bits, (unsigned long long)__double_as_longlong(kap));
     }
 }
 
@@ -144,11 +172,17 @@ struct SweepSmem {
     static constexpr int SD = S + 1;  // inverse ring outlives the slab by one chunk
 };
 
-template <class T, int TR, int S>
+// SUBST: the chunk's triangle T (bulk-loaded in place of D^{-1}) is solved by substitution on warp 0
+// (32 broadcast steps; the reference's band_lu_solve order within the chunk, a / p as IEEE division).
+// Chosen at setup when the chunk triangles are ill conditioned (element growth at low diagonal
+// dominance, max ||T|| ||T^-1|| > 1e2): a product with an explicit inverse is not backward stable there
+// and moves the Krylov iteration counts (measured: config 3 at d = 0.06, 20.25 vs the reference's 1.5);
+// well-conditioned factors keep the 32x32 inverse mat-vec (one dependent step instead of 32).
+template <class T, int TR, int S, bool SUBST>
 __global__ void __launch_bounds__(kSwThreads, 1)
     k_sweep_tma(const __grid_constant__ CUtensorMap map, const T* __restrict__ dinv, int nch_max,
                 const int* __restrict__ offs, int k, T* __restrict__ xbase, int xw, int slab_cols, int box_c,
-                int nbox) {
+                int nbox, const T* __restrict__ tri) {
     constexpr int SD = SweepSmem<T, TR, S>::SD;
     constexpr int CG = 32 / TR;  // column groups per warp
     constexpr int PF = 6;        // L2 prefetch distance (chunks)
@@ -189,7 +223,9 @@ __global__ void __launch_bounds__(kSwThreads, 1)
         mbar_expect_tx(bar + st, slab_bytes + dv_bytes);
         T* dst = slab + st * slab_elems;
         for (int q = 0; q < nbox; ++q) tma_load_3d(dst + (size_t)q * TR * box_c, &map, i0, c0 + q * box_c, b, bar + st);
-        bulk_load(dv + (g % SD) * TR * TR, dvb + ((long long)ch * 2 + (fwd ? 0 : 1)) * TR * TR, dv_bytes, bar + st);
+        const long long o = ((long long)ch * 2 + (fwd ? 0 : 1)) * TR * TR;
+        bulk_load(dv + (g % SD) * TR * TR, (SUBST ? tri : dinv) + (long long)b * nch_max * 2 * TR * TR + o, dv_bytes,
+                  bar + st);
     };
     auto prefetch = [&](int g) {
         const bool fwd = g < nch;
@@ -238,17 +274,46 @@ __global__ void __launch_bounds__(kSwThreads, 1)
                         z = yprev - tot;
                     }
                     const T* D = dv + ((g - 1) % SD) * TR * TR;
-                    T a0 = T(0), a1 = T(0);
-#pragma unroll
-                    for (int jj = 0; jj < TR; jj += 2) {
-                        const T z0 = __shfl_sync(0xffffffffu, z, jj);
-                        const T z1 = __shfl_sync(0xffffffffu, z, jj + 1);
-                        if (lane < TR) {
-                            a0 = fma(D[jj * TR + lane], z0, a0);
-                            a1 = fma(D[(jj + 1) * TR + lane], z1, a1);
+                    T xv;
+                    if constexpr (SUBST) {
+                        // D holds the triangle itself: forward unit lower (column j after x_j), backward upper
+                        T zz = z;
+                        if (fwd) {
+#pragma unroll 4
+                            for (int jj = 0; jj < TR; ++jj) {
+                                const T xj = __shfl_sync(0xffffffffu, zz, jj);
+                                if (lane > jj && lane < TR) zz = fma(-D[jj * TR + lane], xj, zz);
+                            }
+                        } else {
+                            // 1/d of this lane's row (precomputed, see k_chunk_inverses), quotient corrected
+                            // once: the correctly rounded z / d of band_lu_solve without a 140-cycle
+                            // division on each of the 32 dependent steps
+                            const T dl = lane < TR ? D[lane * TR + lane] : T(1);
+                            const T rl = lane < TR ? (lane == 0 ? D[(TR - 2) * TR + TR - 1] : D[lane]) : T(1);
+#pragma unroll 4
+                            for (int jj = TR - 1; jj >= 0; --jj) {
+                                if (lane == jj) {
+                                    const T q = zz * rl;
+                                    zz = fma(fma(-q, dl, zz), rl, q);
+                                }
+                                const T xj = __shfl_sync(0xffffffffu, zz, jj);
+                                if (lane < jj) zz = fma(-D[jj * TR + lane], xj, zz);
+                            }
                         }
+                        xv = zz;
+                    } else {
+                        T a0 = T(0), a1 = T(0);
+#pragma unroll
+                        for (int jj = 0; jj < TR; jj += 2) {
+                            const T z0 = __shfl_sync(0xffffffffu, z, jj);
+                            const T z1 = __shfl_sync(0xffffffffu, z, jj + 1);
+                            if (lane < TR) {
+                                a0 = fma(D[jj * TR + lane], z0, a0);
+                                a1 = fma(D[(jj + 1) * TR + lane], z1, a1);
+                            }
+                        }
+                        xv = a0 + a1;
                     }
-                    const T xv = a0 + a1;
                     if (lane < prev_rows) {
                         xs[(p0 + lane) & xm] = xv;
                         x[p0 + lane] = xv;
@@ -629,6 +694,7 @@ void plan_sweeps(SweepPlan<T>& pl, T* dinv_storage) {
     const int tr = pl.tr;
     pl.nch_max = (pl.st.m_max + tr - 1) / tr;
     pl.dinv = dinv_storage;
+    pl.tri = dinv_storage + (size_t)pl.p * pl.nch_max * 2 * tr * tr;
     // overlapping 3-D view: (row i, column c, block b) -> base + b*pstride + pad + k + c*2k + i
     cuuint64_t dims[3] = {(cuuint64_t)pl.st.m_max, (cuuint64_t)pl.st.m_max, (cuuint64_t)pl.p};
     cuuint64_t strides[2] = {(cuuint64_t)2 * pl.k * sizeof(T), (cuuint64_t)pl.st.pstride * sizeof(T)};
@@ -653,7 +719,7 @@ size_t sweep_dinv_elems(const SweepPlan<T>& pl) {
     choose_tma(tmp);
     if (!tmp.tma) return 0;
     const int nch_max = (pl.st.m_max + tmp.tr - 1) / tmp.tr;
-    return (size_t)pl.p * nch_max * 2 * tmp.tr * tmp.tr;
+    return 2 * (size_t)pl.p * nch_max * 2 * tmp.tr * tmp.tr;  // inverses, then the triangles (substitution)
 }
 template size_t sweep_dinv_elems<double>(const SweepPlan<double>&);
 template size_t sweep_dinv_elems<float>(const SweepPlan<float>&);
@@ -663,9 +729,11 @@ void launch_chunk_inverses(const SweepPlan<T>& pl, cudaStream_t s) {
     if (!pl.tma) return;
     dim3 grid(pl.nch_max, pl.p);
     if (pl.tr == 32)
-        k_chunk_inverses<T, 32><<<grid, 64, 0, s>>>(pl.f, pl.st.pstride, pl.st.pad, pl.offs, pl.k, pl.dinv, pl.nch_max);
+        k_chunk_inverses<T, 32><<<grid, 64, 0, s>>>(pl.f, pl.st.pstride, pl.st.pad, pl.offs, pl.k, pl.dinv, pl.nch_max,
+                                                    pl.tri, pl.kappa);
     else
-        k_chunk_inverses<T, 16><<<grid, 64, 0, s>>>(pl.f, pl.st.pstride, pl.st.pad, pl.offs, pl.k, pl.dinv, pl.nch_max);
+        k_chunk_inverses<T, 16><<<grid, 64, 0, s>>>(pl.f, pl.st.pstride, pl.st.pad, pl.offs, pl.k, pl.dinv, pl.nch_max,
+                                                    pl.tri, pl.kappa);
     SAP_LAUNCHED();
 }
 template void launch_chunk_inverses<double>(const SweepPlan<double>&, cudaStream_t);
@@ -673,10 +741,11 @@ template void launch_chunk_inverses<float>(const SweepPlan<float>&, cudaStream_t
 
 template <class T, int TR, int S>
 static void run_tma(const SweepPlan<T>& pl, T* x, cudaStream_t s) {
-    auto kern = k_sweep_tma<T, TR, S>;
+    const int cols = pl.box_c * pl.nbox;
+    auto kern = pl.subst ? k_sweep_tma<T, TR, S, true> : k_sweep_tma<T, TR, S, false>;
     SAP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
-    kern<<<pl.p, kSwThreads, pl.smem, s>>>(pl.map, pl.dinv, pl.nch_max, pl.offs, pl.k, x, pl.xw, pl.box_c * pl.nbox,
-                                           pl.box_c, pl.nbox);
+    kern<<<pl.p, kSwThreads, pl.smem, s>>>(pl.map, pl.dinv, pl.nch_max, pl.offs, pl.k, x, pl.xw, cols, pl.box_c,
+                                           pl.nbox, pl.tri);
     SAP_LAUNCHED();
 }
 
@@ -697,7 +766,10 @@ void launch_block_solve(const SweepPlan<T>& pl, T* x, cudaStream_t s) {
     // register-streamed variant: opt-in (SAP_SWEEP_LDG=1); measured 2x slower than the TMA ring at K = 200
     static const bool ldg = getenv("SAP_SWEEP_LDG") != nullptr;
     if (ldg && try_ldg<T>(pl, x, s)) return;
-    if (pl.tma) {
+    // SAP_SWEEP_SUBST=1: the cp.async chunk ring with a substitution (shuffle) triangle solve instead of the
+    // precomputed chunk inverses (numerics study: substitution is backward stable under element growth)
+    static const bool subst = getenv("SAP_SWEEP_SUBST") != nullptr;
+    if (pl.tma && !subst) {
         if (pl.tr == 32)
             pl.stages == 3 ? run_tma<T, 32, 3>(pl, x, s) : run_tma<T, 32, 2>(pl, x, s);
         else

@@ -62,6 +62,9 @@ struct SweepPlan {
     int tr = 32, stages = 3, nbox = 1, box_c = 0, xw = 0, nch_max = 0;
     size_t smem = 0;
     T* dinv = nullptr;          // [p][nch_max][2][tr*tr] chunk inverses
+    T* tri = nullptr;           // [p][nch_max][2][tr*tr] the chunk triangles themselves (substitution)
+    unsigned long long* kappa = nullptr;  // device: max chunk-triangle condition estimate (double bits)
+    bool subst = false;         // sweeps solve chunk triangles by substitution (ill-conditioned triangles)
     CUtensorMap map;
 };
 // Elements of chunk-inverse storage the plan needs (0 when the TMA path is not used).

@@ -248,6 +248,14 @@ __device__ __forceinline__ double fast_rcp(double p) {
     return fma(r, e, r);
 }
 
+// a / p from a precomputed 1/p: q = a * (1/p) plus one residual correction (e = a - q p exactly by FMA,
+// q += e * (1/p)) -- the correctly rounded quotient in all but rare ties, i.e. the reference's l = a / p
+// (block_factors.hpp:36), not a * (1/p) with its second rounding (growth at low d amplifies the difference).
+__device__ __forceinline__ double div_rcp(double a, double p, double rc) {
+    const double q = a * rc;
+    return fma(fma(-q, p, a), rc, q);
+}
+
 template <int B, int C>
 __device__ __forceinline__ double pg_recip(const Lu& L, double (&row)[B], int* boost_ctr) {
     double p = row[C];
@@ -788,9 +796,10 @@ __device__ __noinline__ void res_diag8(double* __restrict__ P, int pld, double b
             }
             const double rc = fast_rcp(p);
             s_rcp[q0 + c] = rc;
+            s_rcp[32 + q0 + c] = p;  // the (boosted) pivot, for the quotient correction of the L rows
 #pragma unroll
             for (int r = c + 1; r < 8; ++r) {
-                l[r][c] = a[r] * rc;
+                l[r][c] = div_rcp(a[r], p, rc);
                 a[r] = l[r][c];
             }
 #pragma unroll
@@ -826,7 +835,7 @@ __device__ __noinline__ void res_sub(double* __restrict__ P, double* __restrict_
 #pragma unroll
             for (int cc = 0; cc < 8; ++cc) {
                 if (cc < nq) {
-                    const double l = x[cc] * s_rcp[q0 + cc];
+                    const double l = div_rcp(x[cc], s_rcp[32 + q0 + cc], s_rcp[q0 + cc]);
                     x[cc] = l;
 #pragma unroll
                     for (int c2 = cc + 1; c2 < 8; ++c2) x[c2] = fma(-l, P[(q0 + c2) * pld + q0 + cc], x[c2]);
@@ -1231,7 +1240,7 @@ __global__ void __launch_bounds__(kLuThreads, 1)
     k_band_lu_res(const FactorJob* __restrict__ jobs, double eps, int pld, int uld) {
     extern __shared__ __align__(16) double smem[];
     __shared__ int s_boosts;
-    __shared__ double s_rcp[B];
+    __shared__ double s_rcp[2 * B];  // [0, B): 1/p, [B, 2B): p
     const FactorJob J = jobs[blockIdx.x];
     const double scale = *J.scale;
     Lu L{J.base, J.rs, J.cs, J.m, J.k, B, pld, uld, eps * (scale > 0 ? scale : 1.0), J.src ? J.src : J.base};
@@ -1342,7 +1351,7 @@ __device__ __noinline__ void grp_sub(double* __restrict__ P, double* __restrict_
 #pragma unroll
         for (int cc = 0; cc < 8; ++cc) {
             if (cc < nq) {
-                const double l = xr[cc] * s_rcp[q0 + cc];
+                const double l = div_rcp(xr[cc], s_rcp[32 + q0 + cc], s_rcp[q0 + cc]);
                 xr[cc] = l;
 #pragma unroll
                 for (int c2 = cc + 1; c2 < 8; ++c2) xr[c2] = fma(-l, P[(q0 + c2) * pld + q0 + cc], xr[c2]);
@@ -1617,7 +1626,7 @@ __global__ void __launch_bounds__(kLuThreads, 1)
     k_band_lu_la2(const FactorJob* __restrict__ jobs, double eps, int pld, int uld) {
     extern __shared__ __align__(16) double smem[];
     __shared__ int s_boosts;
-    __shared__ double s_rcp[B];
+    __shared__ double s_rcp[2 * B];  // [0, B): 1/p, [B, 2B): p
     constexpr int kPg = 256;          // PG: threads 0-255
     constexpr int kBarPgL = 3;        // PG internal
     constexpr int kBarNext = 4;       // UG -> PG: panel s+1 / A12(s+1) complete in smem
