@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsap_gpu.so")
+LIB_PATH = os.environ.get("SAP_GPU_LIB", os.path.join(_HERE, "libsap_gpu.so"))  # tools: A/B builds
 
 
 class sap_options(C.Structure):

@@ -99,6 +99,8 @@ struct sap_handle {
     BandStore fst, rst;                  // LU/UL and reduced-block stores
     DevBuf<double> dinv, rdinv;          // chunk inverses (+ triangles) for the sweeps
     DevBuf<unsigned long long> kappa;    // [0] LU plan, [1] reduced plan: chunk-triangle condition estimates
+    DevBuf<int> op_nonfinite;            // any non-finite entry in the banded operator (single-GPU setup)
+    bool op_finite = false;              // checked: the zero-guess shortcut of the Krylov solver applies
     SweepPlan<double> lplan, rplan;      // block sweeps over LU and over the reduced blocks
     // CSR operator
     bool csr = false;
@@ -167,6 +169,10 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
 // factors keep the chunk-inverse product. SAP_SWEEP_TRI=subst/inverse forces the choice.
 constexpr double kSubstKappa = 1e2;
 void choose_triangle_solve(sap_handle* h) {
+    int nf = 1;
+    if (!h->dist && h->op_nonfinite.get())
+        SAP_CUDA(cudaMemcpy(&nf, h->op_nonfinite.get(), sizeof(int), cudaMemcpyDeviceToHost));
+    h->op_finite = nf == 0;
     unsigned long long kb[2] = {0, 0};
     if (h->kappa.get()) SAP_CUDA(cudaMemcpy(kb, h->kappa.get(), sizeof(kb), cudaMemcpyDeviceToHost));
     double kap[2];
@@ -224,6 +230,7 @@ void apply_a(sap_handle* h, const double* in, double* out) {
 int op_n(const sap_handle* h) { return h->csr ? h->csr_n : h->n; }
 
 void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device) {
+    h->op_finite = false;
     require(n >= 0 && k >= 0, "BandedMatrix: negative dimension");
     require(band != nullptr || n == 0, "sap_setup_banded: null band");
     if (h->opt.mixed_precision)
@@ -319,7 +326,10 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
     SAP_CUDA(cudaMemcpyAsync(h->jobs.get(), jobs.data(), sizeof(FactorJob) * njobs, cudaMemcpyHostToDevice, s));
     h->kappa.alloc(2);
     SAP_CUDA(cudaMemsetAsync(h->kappa.get(), 0, 2 * sizeof(unsigned long long), s));
-    launch_block_norms(h->band_ptr, m_max, k, h->d_offsets.get(), p, nullptr, h->norms.get(), s);
+    h->op_nonfinite.alloc(1);
+    SAP_CUDA(cudaMemsetAsync(h->op_nonfinite.get(), 0, sizeof(int), s));
+    launch_block_norms(h->band_ptr, m_max, k, h->d_offsets.get(), p, nullptr, h->norms.get(), s,
+                       h->op_nonfinite.get());
     if (from_src)
         launch_zero_pad(k, h->d_offsets.get(), p, h->fst, h->lu.get(), h->coupled ? h->ul.get() : nullptr, s);
     else
@@ -506,6 +516,7 @@ void apply_a_dist(sap_handle* h, const double* in, double* out) {
 }
 
 void setup_banded_dist(sap_handle* h, int n, int k, int row_lo, int row_hi, const double* slice, int on_device) {
+    h->op_finite = false;
     require(n >= 0 && k >= 0, "BandedMatrix: negative dimension");
     if (h->opt.mixed_precision)
         throw InvalidArgument("sap_setup_banded_dist: mixed_precision is not supported by this build");
@@ -1029,6 +1040,7 @@ sap_status sap_solve(sap_handle* h, const double* b, double* x, int on_device, s
         kc.abs_tol = h->opt.abs_tol;
         kc.max_iterations = h->opt.max_iterations;
         kc.caller_asserts_spd = h->opt.caller_asserts_spd != 0;
+        kc.zero_guess_exact = h->op_finite && !h->csr && !h->dist;
         if (h->dist && h->comm.world > 1) {
             kc.reduce = [h](double* v, int c) { comm_allreduce(h, v, c); };
             kc.row_offset = h->row_lo;

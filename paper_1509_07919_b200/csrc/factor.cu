@@ -43,7 +43,7 @@ long long g_launch_count = 0;
 // reference's `row > norm` test.
 __global__ void __launch_bounds__(256)
     k_block_norms(const double* __restrict__ a, int k, const int* __restrict__ offs, long long pstride, int pad,
-                  unsigned long long* __restrict__ norms_bits) {
+                  unsigned long long* __restrict__ norms_bits, int* __restrict__ nonfinite, int p) {
     const int lane = threadIdx.x & 31;
     const int b = blockIdx.y;
     const int off = offs[b], m = offs[b + 1] - off;
@@ -58,6 +58,16 @@ __global__ void __launch_bounds__(256)
 #pragma unroll 8
     for (int c = clo; c <= chi; ++c, col += ld)
         if (r < m && r - c <= k && c - r <= k) row += fabs(*col);
+    if (nonfinite && r < m) {
+        // finiteness of every stored entry of global row off + r (the Krylov solver may then take
+        // b - A*0 = b exactly for the zero initial guess): the in-block entries through the row sum
+        // (a non-finite |a| makes it inf/NaN), the coupling columns outside the block here
+        bool bad = !isfinite(row);
+        const int n = offs[p];
+        for (int c = max(r - k, -off); c < 0; ++c) bad |= !isfinite(base[(long long)c * ld + r + k]);
+        for (int c = m; c <= min(r + k, n - 1 - off); ++c) bad |= !isfinite(base[(long long)c * ld + r + k]);
+        if (bad) atomicOr(nonfinite, 1);
+    }
     double best = (r < m && row > 0.0) ? row : 0.0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
@@ -65,11 +75,11 @@ __global__ void __launch_bounds__(256)
 }
 
 void launch_block_norms(const double* band, int max_m, int k, const int* d_offsets, int p, const BandStore* store,
-                        double* norms, cudaStream_t s) {
+                        double* norms, cudaStream_t s, int* nonfinite) {
     SAP_CUDA(cudaMemsetAsync(norms, 0, sizeof(double) * p, s));
     dim3 grid(ceil_div(ceil_div(max_m, 32), 8), p);
     k_block_norms<<<grid, 256, 0, s>>>(band, k, d_offsets, store ? store->pstride : 0, store ? store->pad : 0,
-                                        reinterpret_cast<unsigned long long*>(norms));
+                                        reinterpret_cast<unsigned long long*>(norms), store ? nullptr : nonfinite, p);
     SAP_LAUNCHED();
 }
 

@@ -15,7 +15,8 @@ namespace sapgpu {
 // store == nullptr: `band` is one contiguous band (the A operator); otherwise the
 // blocks live in a BandStore.
 void launch_block_norms(const double* band, int max_m, int k, const int* d_offsets, int p, const BandStore* store,
-                        double* norms, cudaStream_t s);
+                        double* norms, cudaStream_t s,
+                        int* nonfinite = nullptr);
 // LU (and UL) BandStores = each diagonal block's band, entries outside the block zeroed.
 void launch_copy_blocks(const double* band, int k, const int* d_offsets, int p, const BandStore& st, double* lu,
                         double* ul, cudaStream_t s);

@@ -206,10 +206,15 @@ KrylovResult KrylovSolver::bicgstab(const DeviceOp& A, const DeviceOp& M, const 
         SAP_LAUNCHED();
         return std::sqrt(dot(scratch_, scratch_));
     };
+    bool x_is_zero = true;  // x was just zeroed (krylov.hpp:117); false once any update is applied
     auto reset_iteration_state = [&](bool perturb) {
-        A(x, tmp_);
-        k_xpay<<<G, 256, 0, s_>>>(tmp_, -1.0, b, n);
-        SAP_LAUNCHED();
+        if (x_is_zero && cfg.zero_guess_exact) {
+            SAP_CUDA(cudaMemcpyAsync(tmp_, b, sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, s_));
+        } else {
+            A(x, tmp_);
+            k_xpay<<<G, 256, 0, s_>>>(tmp_, -1.0, b, n);
+            SAP_LAUNCHED();
+        }
         M(tmp_, r_[0]);
         SAP_CUDA(cudaMemcpyAsync(rtilde_, r_[0], sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, s_));
         if (perturb) {
@@ -229,6 +234,7 @@ KrylovResult KrylovSolver::bicgstab(const DeviceOp& A, const DeviceOp& M, const 
     };
 
     reset_iteration_state(false);
+    x_is_zero = false;  // the restart (reset_iteration_state(true)) always applies A to the current x
     double rho0 = 1.0, alpha = 0.0, omega = 1.0;
     bool restarted = false, breakdown = false;
     std::vector<double> gamma(ell + 1), gamma_p(ell + 1), gamma_pp(ell + 1), sigma(ell + 1);

@@ -33,6 +33,9 @@ struct KrylovConfig {
     // global index of this rank's first row (for the restart perturbation stream)
     std::function<void(double*, int)> reduce;
     long long row_offset = 0;
+    // the operator has only finite entries (checked at setup): with the zero initial guess the first
+    // residual b - A*0 is b exactly (every row sum of a*(+0) terms is +0), so the first A apply is skipped
+    bool zero_guess_exact = false;
 };
 
 class KrylovSolver {

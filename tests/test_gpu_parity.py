@@ -336,3 +336,21 @@ def test_low_dominance_preconditioner_parity(sap, oracle):
     _, so = oracle.solve_banded(n, k, band, rhs, p, 0)
     assert st.converged and abs(st.iterations - so["iterations"]) <= 1.0
     s.close()
+
+
+def test_nonfinite_coupling_entry_fails_like_reference(sap, oracle):
+    """A NaN outside every diagonal block (a coupling entry, SaP-D never reads it while factoring) reaches
+    the Krylov solver through the first A*x0 (krylov.hpp:152): the solve must fail non_finite exactly like
+    the reference, i.e. the zero-guess shortcut (b - A*0 = b) must not apply to such an operator."""
+    n, k, p = 2000, 10, 4
+    band, rhs = sap.random_banded(n, k, 1.0, 7)
+    lay = sap.make_partition_layout(n, p, k)
+    e = lay.offsets[1]
+    row, col = e - 1, e  # row in block 0, column in block 1: inside the band, outside every block
+    band[col * (2 * k + 1) + (row - col + k)] = np.nan
+    s = make(sap, n, k, band, p, sap.PrecondKind.decoupled)
+    _, st = s.solve(rhs)
+    _, so = oracle.solve_banded(n, k, band, rhs, p, 1)
+    assert not st.converged and st.failure == sap.KrylovFailure.non_finite
+    assert so["failure"] == int(sap.KrylovFailure.non_finite)
+    s.close()
