@@ -167,6 +167,44 @@ __global__ void k_chunk_inverses(const T* __restrict__ f0, long long pstride, in
 }
 
 // ---------------------------------------------------------------------------
+#ifdef SAP_SWEEP_TRACE
+__device__ long long g_sw_trace[16];
+void read_sweep_trace(long long* out) { SAP_CUDA(cudaMemcpyFromSymbol(out, g_sw_trace, sizeof(long long) * 16)); }
+#define SWT(var) long long var = clock64()
+#else
+#define SWT(var) do { } while (0)
+#endif
+// Row r's sum over the slab's CONTIGUOUS columns [c_lo, c_hi) against x (ring xs). The common case (no
+// band-edge masking, no ring wrap) is two FMA chains over constant-offset shared loads: ~3 instructions
+// per column. The sweep's per-chunk time is instruction-issue bound (ncu: helper loop stalls are
+// not_selected / selected / wait), and warp 0's finishing step shares its SMSP with three helpers.
+template <class T, int TR>
+__device__ __forceinline__ T slab_range(const T* __restrict__ L, const T* __restrict__ xs, int xm, int cbase, int c_lo,
+                                        int c_hi, int r, int k, bool fwd) {
+    if (c_lo >= c_hi) return T(0);
+    const bool masked = fwd ? (c_lo < TR) : (c_hi - 1 > k - TR + r || c_hi - 1 > k - TR);
+    const int xb = (cbase + c_lo) & xm;
+    if (!masked && xb + (c_hi - c_lo) <= xm + 1) {
+        const T* __restrict__ xp = xs + xb - c_lo;  // xp[c] = x(cbase + c)
+        const T* __restrict__ lp = L + r;           // lp[c * TR] = slab(r, c)
+        T s0 = T(0), s1 = T(0);
+        int c = c_lo;
+#pragma unroll 4
+        for (; c + 1 < c_hi; c += 2) {
+            s0 = fma(lp[c * TR], xp[c], s0);
+            s1 = fma(lp[(c + 1) * TR], xp[c + 1], s1);
+        }
+        if (c < c_hi) s0 = fma(lp[c * TR], xp[c], s0);
+        return s0 + s1;
+    }
+    T s0 = T(0);
+    for (int c = c_lo; c < c_hi; ++c) {
+        const bool mk = fwd ? (c < TR && r > c) : (TR + c - r > k);
+        s0 = fma(mk ? T(0) : L[c * TR + r], xs[(cbase + c) & xm], s0);
+    }
+    return s0;
+}
+
 template <class T, int TR, int S>
 struct SweepSmem {
     static constexpr int SD = S + 1;  // inverse ring outlives the slab by one chunk
@@ -193,6 +231,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
     T* dv = slab + S * slab_elems;                 // SD x TR*TR
     T* xs = dv + SD * TR * TR;                     // xw
     T* part = xs + xw;                             // kSwWarps x TR
+    T* zb = part + kSwWarps * TR;                  // TR: warp 0's z broadcast
 
     const int b = blockIdx.x;
     const int off = offs[b], m = offs[b + 1] - off;
@@ -204,7 +243,9 @@ __global__ void __launch_bounds__(kSwThreads, 1)
     const T* dvb = dinv + (long long)b * nch_max * 2 * TR * TR;
     const unsigned slab_bytes = (unsigned)(slab_elems * sizeof(T));
     const unsigned dv_bytes = (unsigned)(TR * TR * sizeof(T));
-    const bool producer = (warp == 1 && lane == 0);
+    // TMA producer: lane 0 of the last warp, which forms no phase-1 sums (issuing a slab's TMA takes ~500
+    // cycles, measured; on a helper warp that delayed every chunk's phase 1)
+    const bool producer = (warp == kSwWarps - 1 && lane == 0);
 
     if (tid == 0) {
         for (int s = 0; s < S; ++s) mbar_init(bar + s, 1);
@@ -249,12 +290,22 @@ __global__ void __launch_bounds__(kSwThreads, 1)
             yprev = (lane < TR && in < m) ? x[in] : T(0);
         }
         int prev_rows = 0;
+#ifdef SAP_SWEEP_TRACE
+        long long acc_wait = 0, acc_p1 = 0, acc_p2 = 0, acc_a = 0, t_loop0 = clock64();
+#endif
         for (int t = 0; t <= nch; ++t) {
             const int g = gbase + t;
             const int ch = fwd ? t : nch - 1 - t;   // chunk whose row sums are formed now
             const int pch = fwd ? t - 1 : nch - t;  // chunk finished now by warp 0
+            SWT(tw0);
             if (t < nch) mbar_wait(bar + g % S, (unsigned)((g / S) & 1));
+            SWT(tw1);
             __syncthreads();  // A
+            SWT(tw2);
+#ifdef SAP_SWEEP_TRACE
+            acc_wait += tw1 - tw0;
+            acc_a += tw2 - tw1;
+#endif
             if (producer && t + S - 1 < nch) {
                 issue(g + S - 1);
                 if (t + S - 1 + PF < nch) prefetch(g + S - 1 + PF);
@@ -268,10 +319,15 @@ __global__ void __launch_bounds__(kSwThreads, 1)
                     const int p0 = pch * TR;
                     T z = T(0);
                     if (lane < TR) {
-                        T tot = T(0);
+                        T t0 = T(0), t1 = T(0), t2 = T(0), t3 = T(0);
 #pragma unroll
-                        for (int q = 0; q < kSwWarps; ++q) tot += part[q * TR + lane];
-                        z = yprev - tot;
+                        for (int q = 0; q < kSwWarps; q += 4) {
+                            t0 += part[q * TR + lane];
+                            t1 += part[(q + 1) * TR + lane];
+                            t2 += part[(q + 2) * TR + lane];
+                            t3 += part[(q + 3) * TR + lane];
+                        }
+                        z = yprev - ((t0 + t1) + (t2 + t3));
                     }
                     const T* D = dv + ((g - 1) % SD) * TR * TR;
                     T xv;
@@ -302,17 +358,22 @@ __global__ void __launch_bounds__(kSwThreads, 1)
                         }
                         xv = zz;
                     } else {
-                        T a0 = T(0), a1 = T(0);
+                        // z broadcast through shared memory (measured: the SHFL version of this mat-vec
+                        // was ~1.4K cycles of the ~2.1K-cycle chunk)
+                        if (lane < TR) zb[lane] = z;
+                        __syncwarp();
+                        T a0 = T(0), a1 = T(0), a2 = T(0), a3 = T(0);
+                        if (lane < TR) {
 #pragma unroll
-                        for (int jj = 0; jj < TR; jj += 2) {
-                            const T z0 = __shfl_sync(0xffffffffu, z, jj);
-                            const T z1 = __shfl_sync(0xffffffffu, z, jj + 1);
-                            if (lane < TR) {
-                                a0 = fma(D[jj * TR + lane], z0, a0);
-                                a1 = fma(D[(jj + 1) * TR + lane], z1, a1);
+                            for (int jj = 0; jj < TR; jj += 4) {
+                                a0 = fma(D[jj * TR + lane], zb[jj], a0);
+                                a1 = fma(D[(jj + 1) * TR + lane], zb[jj + 1], a1);
+                                a2 = fma(D[(jj + 2) * TR + lane], zb[jj + 2], a2);
+                                a3 = fma(D[(jj + 3) * TR + lane], zb[jj + 3], a3);
                             }
                         }
-                        xv = a0 + a1;
+                        xv = (a0 + a1) + (a2 + a3);
+                        __syncwarp();
                     }
                     if (lane < prev_rows) {
                         xs[(p0 + lane) & xm] = xv;
@@ -324,37 +385,30 @@ __global__ void __launch_bounds__(kSwThreads, 1)
                     yprev = (lane < TR && in < m) ? x[in] : T(0);
                     prev_rows = min(TR, m - i0);
                 }
-            } else if (t < nch) {
+            } else if (t < nch && warp < kSwWarps - 1) {
                 // columns needing only x older than chunk pch
                 const int ca = fwd ? 0 : TR, cb = fwd ? k - TR : k;
                 const int cbase = fwd ? i0 - k : i0 + TR;
-                for (int cc = ca + (warp - 1) * CG + cg; cc < cb; cc += (kSwWarps - 1) * CG) {
-                    const int c = cbase + cc;
-                    T l = L[cc * TR + r];
-                    if (fwd) {
-                        if (cc < TR && r > cc) l = T(0);
-                    } else {
-                        if (TR + cc - r > k) l = T(0);
-                    }
-                    sA = fma(l, xs[c & xm], sA);
-                }
+                // contiguous column ranges: helper warp (warp-1) of 14, column group cg of CG
+                const int nparts = (kSwWarps - 2) * CG, part_id = (warp - 1) * CG + cg;
+                const int len = (cb - ca + nparts - 1) / nparts;
+                const int lo = ca + part_id * len, hi = min(lo + len, cb);
+                sA = slab_range<T, TR>(L, xs, xm, cbase, lo, hi, r, k, fwd);
             }
+            SWT(tw3);
             __syncthreads();  // B
+            SWT(tw4);
+#ifdef SAP_SWEEP_TRACE
+            acc_p1 += tw3 - tw2;
+#endif
             // ---- phase 2: the TR columns of chunk pch ----
             if (t < nch) {
-                T sB = T(0);
                 const int ca = fwd ? max(k - TR, 0) : 0, cb = fwd ? k : min(TR, k);
                 const int cbase = fwd ? i0 - k : i0 + TR;
-                for (int cc = ca + warp * CG + cg; cc < cb; cc += kSwWarps * CG) {
-                    const int c = cbase + cc;
-                    T l = L[cc * TR + r];
-                    if (fwd) {
-                        if (cc < TR && r > cc) l = T(0);
-                    } else {
-                        if (TR + cc - r > k) l = T(0);
-                    }
-                    sB = fma(l, xs[c & xm], sB);
-                }
+                const int nparts = kSwWarps * CG, part_id = warp * CG + cg;
+                const int len = (cb - ca + nparts - 1) / nparts;
+                const int lo = ca + part_id * len, hi = min(lo + len, cb);
+                const T sB = slab_range<T, TR>(L, xs, xm, cbase, lo, hi, r, k, fwd);
                 T s = sA + sB;
                 if constexpr (CG > 1) {
 #pragma unroll
@@ -362,7 +416,21 @@ __global__ void __launch_bounds__(kSwThreads, 1)
                 }
                 if (cg == 0) part[warp * TR + r] = s;
             }
+#ifdef SAP_SWEEP_TRACE
+            acc_p2 += clock64() - tw4;
+#endif
         }
+#ifdef SAP_SWEEP_TRACE
+        if (blockIdx.x == 0 && fwd && (tid == 0 || tid == 32)) {
+            const int o = tid == 0 ? 0 : 6;
+            g_sw_trace[o + 0] = clock64() - t_loop0;
+            g_sw_trace[o + 1] = acc_wait;
+            g_sw_trace[o + 2] = acc_a;
+            g_sw_trace[o + 3] = acc_p1;
+            g_sw_trace[o + 4] = acc_p2;
+            g_sw_trace[o + 5] = nch;
+        }
+#endif
         __syncthreads();
         for (int i = tid; i < xw; i += kSwThreads) xs[i] = T(0);
         __syncthreads();
@@ -654,7 +722,7 @@ static EncodeTiledFn encode_fn() {
 
 template <class T, int TR, int S>
 static size_t tma_smem_bytes(int slab_cols, int xw) {
-    return 128 + sizeof(T) * ((size_t)S * TR * slab_cols + (size_t)(S + 1) * TR * TR + xw + kSwWarps * TR);
+    return 128 + sizeof(T) * ((size_t)S * TR * slab_cols + (size_t)(S + 1) * TR * TR + xw + (kSwWarps + 1) * TR);
 }
 
 template <class T>

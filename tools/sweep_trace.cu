@@ -1,5 +1,6 @@
-// Driver: config-2 SaP-D setup + one preconditioner apply with the traced pair sweep (forward chunks 8..39 of
-// block 0); prints per-chunk clock64 deltas, finisher CTA and helper CTA separately (different SMs).
+// Driver: config-2 SaP-D setup + preconditioner applies with the traced k_sweep_tma; prints, for block 0's
+// forward sweep, cycles per chunk spent waiting on the slab mbarrier, at barrier A, in phase 1 and phase 2
+// (thread 0 = warp 0, thread 32 = warp 1).
 #include <cstdio>
 #include <vector>
 #include "../include/sap_gpu.h"
@@ -13,14 +14,13 @@ int main() {
     sap_setup_banded(h, n, k, band.data(), 0);
     sap_apply_preconditioner(h, rhs.data(), out.data(), 0);
     sap_apply_preconditioner(h, rhs.data(), out.data(), 0);
-    long long t[32 * 12];
+    long long t[16];
     sapgpu::read_sweep_trace(t);
-    printf("F (relative to w0 X-sync of the chunk): w0 Y-arrive | w1: start slab bar5 hpart wbuf || H (rel. to start): slab+sync sent | H period\n");
-    for (int c = 0; c < 31; ++c) {
-        const long long* r = t + c * 12;
-        long long b = r[0];
-        printf("%2d: %6lld | %6lld %6lld %6lld %6lld %6lld | F period %6lld || %6lld %6lld | %6lld\n", c + 8, r[1] - b, r[2] - b, r[3] - b,
-               r[4] - b, r[5] - b, r[6] - b, r[12] - b, r[8] - r[7], r[9] - r[7], r[12 + 7] - r[7]);
+    for (int w = 0; w < 2; ++w) {
+        const long long* r = t + 6 * w;
+        const double c = (double)r[5];
+        printf("warp %d: %lld chunks, per chunk: total %.0f | mbar wait %.0f | barrier A %.0f | phase 1 %.0f | "
+               "phase 2 (+B) %.0f cycles\n", w, r[5], r[0] / c, r[1] / c, r[2] / c, r[3] / c, r[4] / c);
     }
     sap_destroy(h);
 }
