@@ -205,6 +205,54 @@ __device__ __forceinline__ T slab_range(const T* __restrict__ L, const T* __rest
     return s0;
 }
 
+// TR = 32 paired form: lane = (half h, row pair rp) -- rows rp, rp+1 of the slab in one 16-byte load, the
+// half-warps h = 0/1 take the two halves of [c_lo, c_hi); sums of the two halves are combined by the
+// caller. ~2 instructions per FMA instead of ~8 (the sweep is instruction-issue bound).
+template <class T>
+struct Vec2;
+template <>
+struct Vec2<double> {
+    using type = double2;
+};
+template <>
+struct Vec2<float> {
+    using type = float2;
+};
+template <class T>
+__device__ __forceinline__ void slab_range_pair(const T* __restrict__ L, const T* __restrict__ xs, int xm, int cbase,
+                                                int c_lo, int c_hi, int lane, int k, bool fwd, T& s0, T& s1) {
+    constexpr int TR = 32;
+    const int h = lane >> 4, rp = (lane & 15) * 2;
+    const int mid = c_lo + ((c_hi - c_lo + 1) >> 1);
+    const int a = h ? mid : c_lo, b = h ? c_hi : mid;
+    if (a >= b) return;
+    const bool masked = fwd ? (a < TR) : (b - 1 > k - TR);
+    const int xb = (cbase + a) & xm;
+    if (!masked && xb + (b - a) <= xm + 1) {
+        using V = typename Vec2<T>::type;
+        const V* __restrict__ lp = reinterpret_cast<const V*>(L + rp);  // lp[c * 16] = rows rp, rp+1 of column c
+        const T* __restrict__ xp = xs + xb - a;
+        T t0 = T(0), t1 = T(0);
+#pragma unroll 4
+        for (int c = a; c < b; ++c) {
+            const V v = lp[c * (TR / 2)];
+            const T xv = xp[c];
+            s0 = fma(v.x, xv, s0);
+            s1 = fma(v.y, xv, s1);
+        }
+        (void)t0;
+        (void)t1;
+        return;
+    }
+    for (int c = a; c < b; ++c) {
+        const T xv = xs[(cbase + c) & xm];
+        const bool m0 = fwd ? (c < TR && rp > c) : (TR + c - rp > k);
+        const bool m1 = fwd ? (c < TR && rp + 1 > c) : (TR + c - rp - 1 > k);
+        s0 = fma(m0 ? T(0) : L[c * TR + rp], xv, s0);
+        s1 = fma(m1 ? T(0) : L[c * TR + rp + 1], xv, s1);
+    }
+}
+
 template <class T, int TR, int S>
 struct SweepSmem {
     static constexpr int SD = S + 1;  // inverse ring outlives the slab by one chunk
@@ -313,7 +361,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
             const T* L = slab + (g % S) * slab_elems;
             const int i0 = ch * TR;
             // ---- phase 1 ----
-            T sA = T(0);
+            T sA = T(0), sA2 = T(0);  // TR = 32: rows 2*(lane&15), +1 (paired form); else row r
             if (warp == 0) {
                 if (t >= 1) {
                     const int p0 = pch * TR;
@@ -390,10 +438,17 @@ __global__ void __launch_bounds__(kSwThreads, 1)
                 const int ca = fwd ? 0 : TR, cb = fwd ? k - TR : k;
                 const int cbase = fwd ? i0 - k : i0 + TR;
                 // contiguous column ranges: helper warp (warp-1) of 14, column group cg of CG
-                const int nparts = (kSwWarps - 2) * CG, part_id = (warp - 1) * CG + cg;
-                const int len = (cb - ca + nparts - 1) / nparts;
-                const int lo = ca + part_id * len, hi = min(lo + len, cb);
-                sA = slab_range<T, TR>(L, xs, xm, cbase, lo, hi, r, k, fwd);
+                if constexpr (TR == 32) {
+                    const int nparts = kSwWarps - 2, part_id = warp - 1;
+                    const int len = (cb - ca + nparts - 1) / nparts;
+                    const int lo = ca + part_id * len, hi = min(lo + len, cb);
+                    slab_range_pair<T>(L, xs, xm, cbase, lo, hi, lane, k, fwd, sA, sA2);
+                } else {
+                    const int nparts = (kSwWarps - 2) * CG, part_id = (warp - 1) * CG + cg;
+                    const int len = (cb - ca + nparts - 1) / nparts;
+                    const int lo = ca + part_id * len, hi = min(lo + len, cb);
+                    sA = slab_range<T, TR>(L, xs, xm, cbase, lo, hi, r, k, fwd);
+                }
             }
             SWT(tw3);
             __syncthreads();  // B
@@ -405,16 +460,28 @@ __global__ void __launch_bounds__(kSwThreads, 1)
             if (t < nch) {
                 const int ca = fwd ? max(k - TR, 0) : 0, cb = fwd ? k : min(TR, k);
                 const int cbase = fwd ? i0 - k : i0 + TR;
-                const int nparts = kSwWarps * CG, part_id = warp * CG + cg;
-                const int len = (cb - ca + nparts - 1) / nparts;
-                const int lo = ca + part_id * len, hi = min(lo + len, cb);
-                const T sB = slab_range<T, TR>(L, xs, xm, cbase, lo, hi, r, k, fwd);
-                T s = sA + sB;
-                if constexpr (CG > 1) {
+                if constexpr (TR == 32) {
+                    const int len = (cb - ca + kSwWarps - 1) / kSwWarps;
+                    const int lo = ca + warp * len, hi = min(lo + len, cb);
+                    slab_range_pair<T>(L, xs, xm, cbase, lo, hi, lane, k, fwd, sA, sA2);
+                    sA += __shfl_xor_sync(0xffffffffu, sA, 16);
+                    sA2 += __shfl_xor_sync(0xffffffffu, sA2, 16);
+                    if (lane < 16) {
+                        part[warp * TR + 2 * lane] = sA;
+                        part[warp * TR + 2 * lane + 1] = sA2;
+                    }
+                } else {
+                    const int nparts = kSwWarps * CG, part_id = warp * CG + cg;
+                    const int len = (cb - ca + nparts - 1) / nparts;
+                    const int lo = ca + part_id * len, hi = min(lo + len, cb);
+                    const T sB = slab_range<T, TR>(L, xs, xm, cbase, lo, hi, r, k, fwd);
+                    T s = sA + sB;
+                    if constexpr (CG > 1) {
 #pragma unroll
-                    for (int o = TR; o < 32; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                        for (int o = TR; o < 32; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                    }
+                    if (cg == 0) part[warp * TR + r] = s;
                 }
-                if (cg == 0) part[warp * TR + r] = s;
             }
 #ifdef SAP_SWEEP_TRACE
             acc_p2 += clock64() - tw4;
