@@ -84,6 +84,9 @@ struct sap_handle {
     cudaStream_t stream = nullptr;
     cudaStream_t own_stream = nullptr;
     cudaEvent_t ev[12] = {};
+    // SaP-C setup: the sweep chunk inverses run on `side` while extract/tips/rbar continue on `stream`
+    cudaStream_t side = nullptr;
+    cudaEvent_t sev[2] = {};
     // problem
     bool ready = false;
     int n = 0, k = 0;
@@ -349,7 +352,14 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
         h->dinv.alloc(std::max<size_t>(sweep_dinv_elems(lp), 1));
         plan_sweeps(lp, h->dinv.get());
         lp.kappa = h->kappa.get();
-        launch_chunk_inverses(lp, s);
+        if (h->coupled) {  // only the solve needs them: overlap with coupling / tips / reduced blocks
+            SAP_CUDA(cudaEventRecord(h->sev[0], s));
+            SAP_CUDA(cudaStreamWaitEvent(h->side, h->sev[0], 0));
+            launch_chunk_inverses(lp, h->side);
+            SAP_CUDA(cudaEventRecord(h->sev[1], h->side));
+        } else {
+            launch_chunk_inverses(lp, s);
+        }
     }
     SAP_CUDA(cudaEventRecord(h->ev[2], s));
     for (int b = 0; b < p; ++b) {
@@ -425,6 +435,7 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
         launch_chunk_inverses(rp, s);
         }
         SAP_CUDA(cudaEventRecord(h->ev[5], s));
+        SAP_CUDA(cudaStreamWaitEvent(s, h->sev[1], 0));  // the LU chunk inverses (side stream)
     }
     SAP_CUDA(cudaStreamSynchronize(s));
     choose_triangle_solve(h);
@@ -881,6 +892,8 @@ sap_status sap_create(const sap_options* opts, sap_handle** out) {
             SAP_CUDA(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
             h->stream = h->own_stream;
             for (auto& e : h->ev) SAP_CUDA(cudaEventCreate(&e));
+            SAP_CUDA(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+            for (auto& e : h->sev) SAP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         } catch (...) {
             delete h;
             throw;
@@ -895,6 +908,9 @@ void sap_destroy(sap_handle* h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     for (auto& e : h->ev)
         if (e) cudaEventDestroy(e);
+    for (auto& e : h->sev)
+        if (e) cudaEventDestroy(e);
+    if (h->side) cudaStreamDestroy(h->side);
     if (h->own_stream) cudaStreamDestroy(h->own_stream);
     delete h;
 }
