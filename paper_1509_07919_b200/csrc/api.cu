@@ -170,7 +170,7 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
 // Sweeps on ill-conditioned chunk triangles (max ||T|| ||T^-1|| over chunks above kSubstKappa: element
 // growth at low diagonal dominance) solve them by substitution (k_sweep_tma<SUBST>); well conditioned
 // factors keep the chunk-inverse product. SAP_SWEEP_TRI=subst/inverse forces the choice.
-constexpr double kSubstKappa = 1e2;
+constexpr double kSubstKappa = 1e4;
 void choose_triangle_solve(sap_handle* h) {
     int nf = 1;
     if (!h->dist && h->op_nonfinite.get())

@@ -261,7 +261,7 @@ struct SweepSmem {
 // SUBST: the chunk's triangle T (bulk-loaded in place of D^{-1}) is solved by substitution on warp 0
 // (32 broadcast steps; the reference's band_lu_solve order within the chunk, a / p as IEEE division).
 // Chosen at setup when the chunk triangles are ill conditioned (element growth at low diagonal
-// dominance, max ||T|| ||T^-1|| > 1e2): a product with an explicit inverse is not backward stable there
+// dominance, max ||T|| ||T^-1|| > 1e4): a product with an explicit inverse is not backward stable there
 // and moves the Krylov iteration counts (measured: config 3 at d = 0.06, 20.25 vs the reference's 1.5);
 // well-conditioned factors keep the 32x32 inverse mat-vec (one dependent step instead of 32).
 template <class T, int TR, int S, bool SUBST>
