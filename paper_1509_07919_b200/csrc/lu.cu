@@ -23,6 +23,10 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#ifndef SAP_LA2_PG
+#define SAP_LA2_PG 128  // k_band_lu_la2 panel-group threads (tools: -DSAP_LA2_PG=256 for the 8+8 split)
+#endif
+
 namespace sapgpu {
 
 namespace {
@@ -502,7 +506,7 @@ __global__ void __launch_bounds__(kLuThreads, 1)
     __shared__ __align__(16) double s_prow[2 * (B + 2)];
     const FactorJob J = jobs[blockIdx.x];
     const double scale = *J.scale;
-    Lu L{J.base, J.rs, J.cs, J.m, J.k, B, pld, uld, eps * (scale > 0 ? scale : 1.0)};
+    Lu L{J.base, J.rs, J.cs, J.m, J.k, B, pld, uld, eps * (scale > 0 ? scale : 1.0), J.src ? J.src : J.base};
     const int psz = B * pld, usz = B * uld;
     const int tid = threadIdx.x, warp = tid >> 5;
     const bool pg = warp < kPgWarps;
@@ -587,7 +591,7 @@ __global__ void __launch_bounds__(kLuThreads, 1)
     __shared__ __align__(16) double s_prow[2 * (B + 2)];
     const FactorJob J = jobs[blockIdx.x];
     const double scale = *J.scale;
-    Lu L{J.base, J.rs, J.cs, J.m, J.k, B, pld, uld, eps * (scale > 0 ? scale : 1.0)};
+    Lu L{J.base, J.rs, J.cs, J.m, J.k, B, pld, uld, eps * (scale > 0 ? scale : 1.0), J.src ? J.src : J.base};
     double* P = smem;
     double* U = smem + B * pld;
     const int tid = threadIdx.x, warp = tid >> 5;
@@ -633,7 +637,7 @@ __global__ void __launch_bounds__(kLuThreads, 1)
     __shared__ double s_L11[32 * 33];
     const FactorJob J = jobs[blockIdx.x];
     const double scale = *J.scale;
-    Lu L{J.base, J.rs, J.cs, J.m, J.k, B, pld, uld, eps * (scale > 0 ? scale : 1.0)};
+    Lu L{J.base, J.rs, J.cs, J.m, J.k, B, pld, uld, eps * (scale > 0 ? scale : 1.0), J.src ? J.src : J.base};
     const int psz = B * pld, usz = B * uld;
     const int tid = threadIdx.x, warp = tid >> 5;
     const bool pg = warp < kPgWarps;
@@ -719,7 +723,7 @@ __global__ void __launch_bounds__(kLuThreads, 1)
     __shared__ double s_L11[32 * 33];
     const FactorJob J = jobs[blockIdx.x];
     const double scale = *J.scale;
-    Lu L{J.base, J.rs, J.cs, J.m, J.k, B, pld, uld, eps * (scale > 0 ? scale : 1.0)};
+    Lu L{J.base, J.rs, J.cs, J.m, J.k, B, pld, uld, eps * (scale > 0 ? scale : 1.0), J.src ? J.src : J.base};
     double* P = smem;
     double* A = smem + B * pld;
     const int tid = threadIdx.x, warp = tid >> 5;
@@ -1336,16 +1340,13 @@ template <bool FULL>
 __device__ __noinline__ void grp_sub(double* __restrict__ P, double* __restrict__ A, int pld, int uld, int q0, int nq_rt,
                                      int nb, int ph, int R, const double* __restrict__ s_rcp, int ptid, int nthr,
                                      int bar) {
+    // rows [q1, ph) and columns (panel [q1, nb), then A12 [0, R)) are dealt round-robin over the group's nthr
+    // threads (one each when nthr covers them)
     const int nq = FULL ? 8 : nq_rt;
     const int q1 = q0 + 8;
     const int npc = max(nb - q1, 0);
-    double xr[8], xc[8];
-    const int r = q1 + ptid;
-    const bool rowa = r < ph;
-    const bool is_p = ptid < npc;
-    const int c = is_p ? q1 + ptid : ptid - npc;
-    const bool cola = is_p || c < R;
-    if (rowa) {
+    for (int r = q1 + ptid; r < ph; r += nthr) {
+        double xr[8];
 #pragma unroll
         for (int cc = 0; cc < 8; ++cc) xr[cc] = P[(q0 + cc) * pld + r];
 #pragma unroll
@@ -1360,7 +1361,10 @@ __device__ __noinline__ void grp_sub(double* __restrict__ P, double* __restrict_
 #pragma unroll
         for (int cc = 0; cc < 8; ++cc) P[(q0 + cc) * pld + r] = xr[cc];
     }
-    if (cola) {
+    for (int ct = ptid; ct < npc + R; ct += nthr) {
+        const bool is_p = ct < npc;
+        const int c = is_p ? q1 + ct : ct - npc;
+        double xc[8];
         double* col = is_p ? P + c * pld + q0 : A + q0 * uld + c;
         const int st = is_p ? 1 : uld;
 #pragma unroll
@@ -1407,20 +1411,20 @@ __device__ __noinline__ void grp_sub(double* __restrict__ P, double* __restrict_
             }
         }
     } else {
-        if (rowa)
+        for (int r = q1 + ptid; r < ph; r += nthr)
             for (int cc = q1; cc < nb; ++cc) {
                 double acc = P[cc * pld + r];
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
-                    if (j < nq) acc = fma(-xr[j], P[cc * pld + q0 + j], acc);
+                    if (j < nq) acc = fma(-P[(q0 + j) * pld + r], P[cc * pld + q0 + j], acc);
                 P[cc * pld + r] = acc;
             }
-        if (cola && !is_p)
+        for (int c = ptid; c < R; c += nthr)
             for (int rr = q1; rr < nb; ++rr) {
                 double acc = A[rr * uld + c];
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
-                    if (j < nq) acc = fma(-P[(q0 + j) * pld + rr], xc[j], acc);
+                    if (j < nq) acc = fma(-P[(q0 + j) * pld + rr], A[(q0 + j) * uld + c], acc);
                 A[rr * uld + c] = acc;
             }
     }
@@ -1627,12 +1631,12 @@ __global__ void __launch_bounds__(kLuThreads, 1)
     extern __shared__ __align__(16) double smem[];
     __shared__ int s_boosts;
     __shared__ double s_rcp[2 * B];  // [0, B): 1/p, [B, 2B): p
-    constexpr int kPg = 256;          // PG: threads 0-255
+    constexpr int kPg = SAP_LA2_PG;   // PG: threads [0, kPg); UG: the rest
     constexpr int kBarPgL = 3;        // PG internal
     constexpr int kBarNext = 4;       // UG -> PG: panel s+1 / A12(s+1) complete in smem
     const FactorJob J = jobs[blockIdx.x];
     const double scale = *J.scale;
-    Lu L{J.base, J.rs, J.cs, J.m, J.k, B, pld, uld, eps * (scale > 0 ? scale : 1.0)};
+    Lu L{J.base, J.rs, J.cs, J.m, J.k, B, pld, uld, eps * (scale > 0 ? scale : 1.0), J.src ? J.src : J.base};
     const int psz = B * pld, usz = B * uld;
     const int tid = threadIdx.x, warp = tid >> 5;
     const bool pg = tid < kPg;

@@ -18,7 +18,7 @@ if __name__ == "__main__":
             ts.append(s.report()["t_factor_kernel"])
         print(f"{os.environ.get('VARIANT', 'default'):12s} t_factor_kernel ms: " + " ".join(f"{t * 1e3:.3f}" for t in ts))
         sys.exit(0)
-    for v in ["default", "SAP_LU_SEQ"] + sys.argv[1:]:
+    for v in ["default", "SAP_LU_SEQ", "SAP_LU_LA2"] + sys.argv[1:]:
         env = dict(os.environ)
         env["VARIANT"] = v
         if v != "default":
