@@ -1098,13 +1098,16 @@ __device__ __forceinline__ void tile_load_fr(const Lu& L, const TileCtx& T, int 
 // hides under the DMMA work (in-flight cp.async would stall the next step's shared loads).
 __device__ __noinline__ void res_bulk(const Lu& L, const double* __restrict__ P, const double* __restrict__ U, int nb,
                                       int ja, int R, int nbn, int phn, int Rn, double* __restrict__ Pn,
-                                      double* __restrict__ An, int fr) {
+                                      double* __restrict__ An, int fr, int step) {
     const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
     const int pld = L.pld, uld = L.uld;
     constexpr int kPf = 4;  // fetch columns per warp: 64 = 32 panel + 32 A12 columns over 16 warps
     double pf[kPf];
     const bool fast = nbn > 0 && R >= nbn && nw * kPf >= 64;
+#ifdef SAP_LU_TRACE
+    if (step == 8 && blockIdx.x == 0 && lane == 0) g_lu_wtrace[warp] = clock64();
+#endif
     if (nbn > 0 && !fast) res_fetch(L, Pn, An, ja, nbn, R, phn, Rn, 0, nw * 32);
     if (fast) {
 #pragma unroll
@@ -1205,6 +1208,26 @@ __device__ __noinline__ void res_bulk(const Lu& L, const double* __restrict__ P,
                                 if (i < R && c < R) __stcg(p00 + a * ra8 + e * rs + q * cq8, acc[a][q][e]);
                             }
                 }
+            } else if (nbn == kTileC && row0 + kTileR <= R && col0 + kTileC <= R &&
+                       (to_p || row0 + kTileR <= nbn)) {
+                // whole tile inside the next panel (16-byte pairs: rows i, i+1 adjacent in Pn) or inside
+                // the next U12 rows (An row-major)
+                if (to_p) {
+#pragma unroll
+                    for (int a = 0; a < 2; ++a)
+#pragma unroll
+                        for (int q = 0; q < kTQ; ++q)
+                            *reinterpret_cast<double2*>(Pn + (cb + q * 8) * pld + ib + a * 8) =
+                                make_double2(acc[a][q][0], acc[a][q][1]);
+                } else {
+#pragma unroll
+                    for (int a = 0; a < 2; ++a)
+#pragma unroll
+                        for (int q = 0; q < kTQ; ++q) {
+                            An[(ib + a * 8) * uld + (cb + q * 8 - nbn)] = acc[a][q][0];
+                            An[(ib + a * 8 + 1) * uld + (cb + q * 8 - nbn)] = acc[a][q][1];
+                        }
+                }
             } else {
 #pragma unroll
                 for (int a = 0; a < 2; ++a)
@@ -1224,6 +1247,9 @@ __device__ __noinline__ void res_bulk(const Lu& L, const double* __restrict__ P,
             }
         }
     }
+#ifdef SAP_LU_TRACE
+    if (step == 8 && blockIdx.x == 0 && lane == 0) g_lu_wtrace[16 + warp] = clock64();
+#endif
     if (fast) {
 #pragma unroll
         for (int i = 0; i < kPf; ++i) {
@@ -1319,7 +1345,7 @@ __global__ void __launch_bounds__(kLuThreads, 1)
         LU_TRACE(step, 4, tid == 0);
         // 4. trailing update (next panel / A12 land in smem) + step s+1's new band entries
         // window entries at or beyond the previous step's window edge (jb + min(K, m - jb)) are fresh
-        res_bulk(L, P, A, nb, ja, R, nbn, phn, Rn, Pn, An, jb == 0 ? 0 : min(K, m - jb) - nb);
+        res_bulk(L, P, A, nb, ja, R, nbn, phn, Rn, Pn, An, jb == 0 ? 0 : min(K, m - jb) - nb, step);
         cp_async_wait_all();
         LU_TRACE(step, 8, tid == 0);
         __syncthreads();

@@ -24,8 +24,10 @@ int main(int argc, char** argv) {
     }
     long long wt[64];
     sapgpu::read_lu_wtrace(wt);
-    printf("step 8 per-warp end of A2 (q0=0), relative to q0diag:");
-    for (int w = 0; w < 16; ++w) printf(" %lld", wt[w] - t[8 * 12 + 5]);
+    printf("step 8 per-warp trailing-update time (tile loop, cycles):");
+    for (int w = 0; w < 16; ++w) printf(" %lld", wt[16 + w] - wt[w]);
+    printf("\nstep 8 per-warp start offset (vs warp 0):");
+    for (int w = 0; w < 16; ++w) printf(" %lld", wt[w] - wt[0]);
     printf("\n");
     sap_destroy(h);
 }
