@@ -109,6 +109,10 @@ typedef struct sap_report {
     long long kernel_launches; /* sm_100a kernels launched by this process so far */
     double t_factor_kernel;    /* device time of the block LU/UL factorization launch alone */
     double factor_flops;       /* algorithmic flops of that launch (band_lu_inplace op count) */
+    /* sweeps: max over 32-row chunks of ||T|| ||T^-1|| of the LU chunk triangles (T^-1 explicit); above 1e4
+     * the block solves use substitution instead of the inverse products (1 = substitution) */
+    double chunk_condition;
+    int sweep_substitution;
 } sap_report;
 
 /* SolveStats (krylov.hpp:35-41). history: caller-owned buffer of

@@ -23,7 +23,8 @@ class sap_report(C.Structure):
                 ("t_kry", C.c_double), ("t_dtransf", C.c_double), ("n", C.c_int), ("k", C.c_int),
                 ("partitions", C.c_int), ("total_boosts", C.c_int), ("total_boosts_ul", C.c_int),
                 ("total_rbar_boosts", C.c_int), ("kernel_launches", C.c_longlong),
-                ("t_factor_kernel", C.c_double), ("factor_flops", C.c_double)]
+                ("t_factor_kernel", C.c_double), ("factor_flops", C.c_double), ("chunk_condition", C.c_double),
+                ("sweep_substitution", C.c_int)]
 
 
 class sap_solve_stats(C.Structure):

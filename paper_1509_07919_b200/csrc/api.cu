@@ -183,6 +183,8 @@ void choose_triangle_solve(sap_handle* h) {
     const char* force = getenv("SAP_SWEEP_TRI");
     h->lplan.subst = force ? force[0] == 's' : kap[0] > kSubstKappa;
     h->rplan.subst = force ? force[0] == 's' : kap[1] > kSubstKappa;
+    h->rep.chunk_condition = kap[0];
+    h->rep.sweep_substitution = h->lplan.subst ? 1 : 0;
     if (getenv("SAP_DEBUG_KAPPA"))
         fprintf(stderr, "sap: chunk-triangle condition estimates LU %.3e reduced %.3e -> substitution %d %d\n", kap[0],
                 kap[1], (int)h->lplan.subst, (int)h->rplan.subst);

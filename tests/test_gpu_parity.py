@@ -294,6 +294,7 @@ def test_config2_full_size(sap, oracle, kind, want_it):
     x, st = s.solve(rhs)
     assert st.converged and st.final_relative_residual <= 1e-10
     assert abs(st.iterations - want_it) <= 1.0
+    assert s.report()["sweep_substitution"] == 0  # d = 1: well-conditioned chunk triangles, inverse products
     lay = s.layout
     w = 2 * k + 1
     for part in (0, p - 1):
@@ -322,6 +323,8 @@ def test_config3_low_dominance_iterations(sap, oracle):
     x, st = s.solve(rhs)
     assert st.converged and st.final_relative_residual <= 1e-10
     assert abs(st.iterations - 1.5) <= 1.0
+    rep = s.report()
+    assert rep["sweep_substitution"] == 1 and rep["chunk_condition"] > 1e4
     s.close()
 
 
