@@ -309,6 +309,12 @@ __global__ void __launch_bounds__(kSwThreads, 1)
         const int i0 = ch * TR;
         const int c0 = fwd ? i0 - k : i0 + TR;
         const int st = g % S;
+#ifdef SAP_ABL_NOTMA
+        if (g >= S) {  // timing study only: no slab traffic after the first ring pass (results invalid)
+            mbar_expect_tx(bar + st, 0);
+            return;
+        }
+#endif
         mbar_expect_tx(bar + st, slab_bytes + dv_bytes);
         T* dst = slab + st * slab_elems;
         for (int q = 0; q < nbox; ++q) tma_load_3d(dst + (size_t)q * TR * box_c, &map, i0, c0 + q * box_c, b, bar + st);
