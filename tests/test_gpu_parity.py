@@ -46,6 +46,7 @@ FACTOR_CASES = [
     (3000, 200, 0.06, 16, 2),
     (2400, 500, 1.0, 17, 2),
     (997, 33, 0.5, 18, 7),
+    (2400, 300, 0.7, 19, 2),  # K > 224: the B = 32 fallback LU kernel
 ]
 
 
@@ -357,3 +358,16 @@ def test_nonfinite_coupling_entry_fails_like_reference(sap, oracle):
     assert not st.converged and st.failure == sap.KrylovFailure.non_finite
     assert so["failure"] == int(sap.KrylovFailure.non_finite)
     s.close()
+
+
+def test_zero_rhs_converges_immediately(sap, oracle):
+    """krylov.hpp:117-123: b = 0 -> converged with x = 0, zero iterations, history [0]."""
+    n, k, p = 3000, 20, 3
+    band, _ = sap.random_banded(n, k, 1.0, 4)
+    for kind in (sap.PrecondKind.coupled, sap.PrecondKind.decoupled):
+        s = make(sap, n, k, band, p, kind)
+        x, st = s.solve(np.zeros(n))
+        _, so = oracle.solve_banded(n, k, band, np.zeros(n), p, int(kind))
+        assert st.converged and so["converged"] and st.iterations == so["iterations"] == 0.0
+        assert list(st.residual_history) == [0.0] and not np.any(x)
+        s.close()
