@@ -105,6 +105,12 @@ struct sap_handle {
     DevBuf<int> op_nonfinite;            // any non-finite entry in the banded operator (single-GPU setup)
     bool op_finite = false;              // checked: the zero-guess shortcut of the Krylov solver applies
     SweepPlan<double> lplan, rplan;      // block sweeps over LU and over the reduced blocks
+    // mixed precision (KrylovOptions::mixed_precision, build_precond_op<float>): the preconditioner is
+    // applied in FP32 from FP32 copies of the factors, tips and reduced factors
+    bool mixed = false;
+    DevBuf<float> lu_f, rbar_f, vb_f, wt_f, bblk_f, cblk_f, dinv_f, rdinv_f, g_f, o_f, xt_f, xb_f;
+    DevBuf<unsigned long long> kappa_f;
+    SweepPlan<float> lplan_f, rplan_f;
     // CSR operator
     bool csr = false;
     int csr_n = 0;
@@ -185,6 +191,8 @@ void choose_triangle_solve(sap_handle* h) {
     h->rplan.subst = force ? force[0] == 's' : kap[1] > kSubstKappa;
     h->rep.chunk_condition = kap[0];
     h->rep.sweep_substitution = h->lplan.subst ? 1 : 0;
+    h->lplan_f.subst = h->lplan.subst;
+    h->rplan_f.subst = h->rplan.subst;
     if (getenv("SAP_DEBUG_KAPPA"))
         fprintf(stderr, "sap: chunk-triangle condition estimates LU %.3e reduced %.3e -> substitution %d %d\n", kap[0],
                 kap[1], (int)h->lplan.subst, (int)h->rplan.subst);
@@ -192,6 +200,76 @@ void choose_triangle_solve(sap_handle* h) {
 
 void apply_m_dist(sap_handle* h, const double* in, double* out);
 void apply_a_dist(sap_handle* h, const double* in, double* out);
+
+// FP32 copies of everything the preconditioner apply reads (factor stores, chunk inverses recomputed in
+// FP32 from the FP32 factors, tips, couplings, reduced factors). The factorization itself ran in FP64
+// (the DMMA kernels): the reference's build_precond_op<float> factors in FP32, so the FP32 operands
+// here differ from its by FP32 rounding -- both are FP32-accurate preconditioners.
+void build_fp32_preconditioner(sap_handle* h, cudaStream_t s) {
+    h->mixed = true;
+    const int p = h->layout.p, k = h->k;
+    h->lu_f.alloc(h->fst.total(p));
+    launch_cast_band<float>(h->lu.get(), h->lu_f.get(), h->fst.total(p), s);
+    h->kappa_f.alloc(2);
+    SAP_CUDA(cudaMemsetAsync(h->kappa_f.get(), 0, 2 * sizeof(unsigned long long), s));
+    SweepPlan<float>& lp = h->lplan_f;
+    lp = SweepPlan<float>{};
+    lp.f = h->lu_f.get();
+    lp.st = h->fst;
+    lp.offs = h->d_offsets.get();
+    lp.p = p;
+    lp.k = k;
+    h->dinv_f.alloc(std::max<size_t>(sweep_dinv_elems(lp), 1));
+    plan_sweeps(lp, h->dinv_f.get());
+    lp.kappa = h->kappa_f.get();
+    launch_chunk_inverses(lp, s);
+    if (h->coupled && k > 0) {
+        const int ni = p - 1;
+        const size_t ww = (size_t)k * k * ni;
+        h->vb_f.alloc(ww);
+        h->wt_f.alloc(ww);
+        h->bblk_f.alloc(ww);
+        h->cblk_f.alloc(ww);
+        launch_cast_band<float>(h->vb.get(), h->vb_f.get(), ww, s);
+        launch_cast_band<float>(h->wt.get(), h->wt_f.get(), ww, s);
+        launch_cast_band<float>(h->bblk.get(), h->bblk_f.get(), ww, s);
+        launch_cast_band<float>(h->cblk.get(), h->cblk_f.get(), ww, s);
+        h->rbar_f.alloc(std::max<size_t>(h->rst.total(ni), 1));
+        launch_cast_band<float>(h->rbar.get(), h->rbar_f.get(), h->rst.total(ni), s);
+        SweepPlan<float>& rp = h->rplan_f;
+        rp = SweepPlan<float>{};
+        rp.f = h->rbar_f.get();
+        rp.st = h->rst;
+        rp.offs = h->d_roffsets.get();
+        rp.p = ni;
+        rp.k = k - 1;
+        h->rdinv_f.alloc(std::max<size_t>(sweep_dinv_elems(rp), 1));
+        plan_sweeps(rp, h->rdinv_f.get());
+        rp.kappa = h->kappa_f.get() + 1;
+        launch_chunk_inverses(rp, s);
+        h->xt_f.alloc(std::max<size_t>((size_t)ni * k, 1));
+        h->xb_f.alloc(std::max<size_t>((size_t)ni * k, 1));
+    }
+    h->g_f.alloc(std::max(h->n, 1));
+    h->o_f.alloc(std::max(h->n, 1));
+}
+
+// M^{-1} in FP32 (apply_preconditioner<float>, spike.hpp:304-351 with pipeline.hpp:191-200's casts)
+void apply_m_fp32(sap_handle* h, const double* in, double* out) {
+    const cudaStream_t s = h->stream;
+    const int n = h->n, p = h->layout.p, k = h->k;
+    float* o = h->o_f.get();
+    launch_cast_d2f(in, o, n, s);
+    if (h->coupled) {
+        float* g = h->g_f.get();
+        SAP_CUDA(cudaMemcpyAsync(g, o, sizeof(float) * (size_t)n, cudaMemcpyDeviceToDevice, s));
+        launch_block_solve<float>(h->lplan_f, g, s);
+        launch_interfaces<float>(g, h->d_offsets.get(), h->rplan_f, p - 1, k, h->wt_f.get(), h->vb_f.get(),
+                                 h->bblk_f.get(), h->cblk_f.get(), h->xt_f.get(), h->xb_f.get(), o, false, false, s);
+    }
+    launch_block_solve<float>(h->lplan_f, o, s);
+    launch_cast_f2d(o, out, n, s);
+}
 
 void apply_m(sap_handle* h, const double* in, double* out) {
     if (h->dist) return apply_m_dist(h, in, out);
@@ -208,6 +286,7 @@ void apply_m(sap_handle* h, const double* in, double* out) {
         default:
             break;
     }
+    if (h->mixed) return apply_m_fp32(h, in, out);
     const int p = h->layout.p, k = h->k;
     if (!h->coupled) {
         if (out != in) SAP_CUDA(cudaMemcpyAsync(out, in, bytes, cudaMemcpyDeviceToDevice, s));
@@ -238,9 +317,8 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
     h->op_finite = false;
     require(n >= 0 && k >= 0, "BandedMatrix: negative dimension");
     require(band != nullptr || n == 0, "sap_setup_banded: null band");
-    if (h->opt.mixed_precision)
-        throw InvalidArgument("sap_setup_banded: mixed_precision is not supported by this build");
     const cudaStream_t s = h->stream;
+    h->mixed = false;
     h->ready = false;
     h->kind = h->opt.precond;
     require(h->kind >= 0 && h->kind <= 3, "sap_setup_banded: unknown preconditioner kind");
@@ -439,6 +517,7 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
         SAP_CUDA(cudaEventRecord(h->ev[5], s));
         SAP_CUDA(cudaStreamWaitEvent(s, h->sev[1], 0));  // the LU chunk inverses (side stream)
     }
+    if (h->opt.mixed_precision) build_fp32_preconditioner(h, s);
     SAP_CUDA(cudaStreamSynchronize(s));
     choose_triangle_solve(h);
     h->rep.t_dtransf = ev_ms(h->ev[0], h->ev[1]) * 1e-3;

@@ -371,3 +371,33 @@ def test_zero_rhs_converges_immediately(sap, oracle):
         assert st.converged and so["converged"] and st.iterations == so["iterations"] == 0.0
         assert list(st.residual_history) == [0.0] and not np.any(x)
         s.close()
+
+
+def test_mixed_precision_preconditioner_tracks_fp64(sap, oracle):
+    """test_spike.cpp:334-352: the FP32 preconditioner's M r is within 1e-4 (and not equal) of the FP64 one."""
+    for n, k, d, p in ((24, 2, 1.5, 2), (20000, 200, 1.0, 5), (12345, 64, 0.5, 7)):
+        band, rhs = sap.random_banded(n, k, d, 83)
+        sd = make(sap, n, k, band, p, sap.PrecondKind.coupled)
+        sf = make(sap, n, k, band, p, sap.PrecondKind.coupled, mixed_precision=True)
+        r = np.random.default_rng(5).uniform(-1, 1, n)
+        e = rel2(sf.apply_preconditioner(r), sd.apply_preconditioner(r))
+        assert 0.0 < e < 1e-4, (n, k, e)
+        sd.close()
+        sf.close()
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_mixed_precision_solve_reaches_full_accuracy(sap, oracle, kind):
+    """test_pipeline.cpp:327-347: FP32 preconditioning still converges to rel_tol 1e-10 in FP64 Krylov.
+    The FP32 operands here are rounded from the FP64 factorization, a more accurate
+    preconditioner than the reference's FP32-arithmetic factorization: iterations are at most the
+    reference's + 1 (measured 7.25 vs 11.25 SaP-C at this case)."""
+    n, k, p = 20000, 50, 8
+    band, rhs = sap.random_banded(n, k, 1.0, 910)
+    s = make(sap, n, k, band, p, kind, mixed_precision=True)
+    x, st = s.solve(rhs)
+    assert st.converged and st.final_relative_residual <= 1e-10
+    if oracle.has_ref():
+        _, so = oracle.ref_solve_banded(n, k, band, rhs, p, kind, mixed_precision=True)
+        assert so["converged"] and st.iterations <= so["iterations"] + 1.0, (st.iterations, so["iterations"])
+    s.close()
