@@ -163,6 +163,14 @@ sap_status sap_setup_banded(sap_handle* h, int n, int k, const double* band, int
 
 /* ---- A operator override: CSR matrix (solve_sparse's apply_a, pipeline.hpp:336-338).
  * row_ptr[n+1], col_idx[nnz], values[nnz]; copied. */
+/* setup from a sparse matrix (pipeline.hpp:103-115 assemble_banded + build_precond_op): the CSR matrix
+ * (already reordered / dropped by the host stage, every entry within half-bandwidth k) is assembled into
+ * band storage ON THE DEVICE and set up like sap_setup_banded; entries outside the band are the
+ * reference's std::invalid_argument ("assemble_banded: entry (i, j) outside half-bandwidth k").
+ * csr_on_device: 0 host pointers, 1 device pointers. Replaces solve_sparse's assemble + setup
+ * (pipeline.hpp:286-330); the Krylov operator stays the banded one until sap_set_operator_csr. */
+sap_status sap_setup_banded_from_csr(sap_handle* h, int n, int k, int nnz, const int* row_ptr, const int* col_idx,
+                                     const double* values, int csr_on_device);
 sap_status sap_set_operator_csr(sap_handle* h, int n, int nnz, const int* row_ptr, const int* col_idx,
                                 const double* values, int on_device);
 

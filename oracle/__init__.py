@@ -259,3 +259,21 @@ def ref_solve_banded(n, k, band, rhs, p, kind, boost_eps=1e-10, ell=2, rel_tol=1
     return x, dict(iterations=it.value, converged=bool(conv.value), final_relative_residual=res.value,
                    failure=fail.value, residual_history=hist[:min(hl.value, cap)].copy(),
                    t_lu=tim[0], t_bc=tim[1], t_spk=tim[2], t_lurdcd=tim[3], t_kry=tim[4])
+
+
+def ref_solve_sparse(n, row_ptr, col_idx, vals, rhs, p, kind, use_db=False, db_scaling=True, use_cm=False,
+                     third_stage=False, drop_tol=0.0, boost_eps=1e-10, seed=0, ell=2, rel_tol=1e-10,
+                     max_iterations=500, mixed_precision=False):
+    """The reference's solve_sparse (pipeline.hpp:213-369) end to end; report = t_db, t_cm, t_drop, t_asmbl,
+    t_bc, t_lu, t_spk, t_lurdcd, t_kry, k (after drop-off)."""
+    x = np.zeros(n)
+    rep = np.zeros(10)
+    it, conv, res, fail = C.c_double(), C.c_int(), C.c_double(), C.c_int()
+    _ref_check(ref().sapref_solve_sparse(n, np.ascontiguousarray(row_ptr, np.int32),
+                                         np.ascontiguousarray(col_idx, np.int32),
+                                         np.ascontiguousarray(vals, np.float64), np.ascontiguousarray(rhs, np.float64),
+                                         int(use_db), int(db_scaling), int(use_cm), int(third_stage), p, drop_tol,
+                                         kind, boost_eps, seed, ell, rel_tol, max_iterations, int(mixed_precision),
+                                         x, rep, C.byref(it), C.byref(conv), C.byref(res), C.byref(fail)))
+    return x, dict(iterations=it.value, converged=bool(conv.value), final_relative_residual=res.value,
+                   failure=fail.value, k_after=int(rep[9]), report=rep)

@@ -61,6 +61,7 @@ SIGNATURES = {
     "sap_synchronize": (C.c_int, [_vp]),
     "sap_setup_banded": (C.c_int, [_vp, C.c_int, C.c_int, _vp, C.c_int]),
     "sap_set_operator_csr": (C.c_int, [_vp, C.c_int, C.c_int, _vp, _vp, _vp, C.c_int]),
+    "sap_setup_banded_from_csr": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, C.c_int]),
     "sap_apply_preconditioner": (C.c_int, [_vp, _vp, _vp, C.c_int]),
     "sap_apply_operator": (C.c_int, [_vp, _vp, _vp, C.c_int]),
     "sap_solve": (C.c_int, [_vp, _vp, _vp, C.c_int, C.POINTER(sap_solve_stats)]),

@@ -116,6 +116,10 @@ struct sap_handle {
     int csr_n = 0;
     DevBuf<int> rp, ci;
     DevBuf<double> vals;
+    DevBuf<double> asm_band;             // sap_setup_banded_from_csr: the band assembled on the device
+    DevBuf<int> asm_rp, asm_ci;
+    DevBuf<double> asm_v;
+    DevBuf<unsigned long long> asm_bad;
     DevBuf<TipJob> tipjobs;
     // multi-GPU (sap_create_distributed): this rank owns global rows [row_lo, row_hi) = partitions
     // [pb, pe); the band slice holds global columns [c_lo, c_hi). Interface slots are ordered
@@ -1051,6 +1055,47 @@ sap_status sap_setup_banded_dist(sap_handle* h, int n, int k, int row_lo, int ro
         require(h->dist, "sap_setup_banded_dist: handle was not created by sap_create_distributed");
         SAP_CUDA(cudaSetDevice(h->opt.device));
         setup_banded_dist(h, n, k, row_lo, row_hi, band_slice, on_device);
+    });
+}
+
+sap_status sap_setup_banded_from_csr(sap_handle* h, int n, int k, int nnz, const int* row_ptr, const int* col_idx,
+                                     const double* values, int csr_on_device) {
+    return guard([&] {
+        require(h != nullptr, "null handle");
+        require(!h->dist, "sap_setup_banded_from_csr: not available on a distributed handle");
+        require(n >= 0 && k >= 0 && nnz >= 0, "BandedMatrix: negative dimension");
+        SAP_CUDA(cudaSetDevice(h->opt.device));
+        const cudaStream_t s = h->stream;
+        const int* rp = row_ptr;
+        const int* ci = col_idx;
+        const double* v = values;
+        if (!csr_on_device) {
+            h->asm_rp.alloc(n + 1);
+            h->asm_ci.alloc(std::max(nnz, 1));
+            h->asm_v.alloc(std::max(nnz, 1));
+            SAP_CUDA(cudaMemcpyAsync(h->asm_rp.get(), row_ptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, s));
+            if (nnz > 0) {
+                SAP_CUDA(cudaMemcpyAsync(h->asm_ci.get(), col_idx, sizeof(int) * nnz, cudaMemcpyHostToDevice, s));
+                SAP_CUDA(cudaMemcpyAsync(h->asm_v.get(), values, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
+            }
+            rp = h->asm_rp.get();
+            ci = h->asm_ci.get();
+            v = h->asm_v.get();
+        }
+        const size_t total = (size_t)n * (2 * (size_t)k + 1);
+        h->asm_band.alloc(std::max<size_t>(total, 1));
+        SAP_CUDA(cudaMemsetAsync(h->asm_band.get(), 0, sizeof(double) * total, s));
+        h->asm_bad.alloc(1);
+        SAP_CUDA(cudaMemsetAsync(h->asm_bad.get(), 0xff, sizeof(unsigned long long), s));
+        launch_assemble_band(rp, ci, v, n, k, h->asm_band.get(), h->asm_bad.get(), s);
+        unsigned long long bad = 0;
+        SAP_CUDA(cudaMemcpyAsync(&bad, h->asm_bad.get(), sizeof(bad), cudaMemcpyDeviceToHost, s));
+        SAP_CUDA(cudaStreamSynchronize(s));
+        if (bad != ~0ULL)
+            throw InvalidArgument("assemble_banded: entry (" + std::to_string(bad / (unsigned long long)n) + ", " +
+                                  std::to_string(bad % (unsigned long long)n) + ") outside half-bandwidth " +
+                                  std::to_string(k));
+        setup_banded(h, n, k, h->asm_band.get(), 2);
     });
 }
 

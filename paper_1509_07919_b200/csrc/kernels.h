@@ -100,6 +100,8 @@ void launch_band_spmv(const double* band, int n, int k, const double* x, double*
 void launch_band_spmv_rows(const double* band, int n, int k, int r0, int r1, const double* x, double* y, cudaStream_t s);
 // w x w row-major GEMV: mode 0: y = u - A v;  mode 1: y -= A v.
 void launch_gemv_w(const double* A, int w, const double* v, const double* u, double* y, int mode, cudaStream_t s);
+void launch_assemble_band(const int* rp, const int* ci, const double* v, int n, int k, double* band,
+                          unsigned long long* bad, cudaStream_t s);
 void launch_csr_spmv(const int* rp, const int* ci, const double* v, int n, const double* x, double* y,
                      const double* b, cudaStream_t s);
 

@@ -104,4 +104,26 @@ void launch_csr_spmv(const int* rp, const int* ci, const double* v, int n, const
     SAP_LAUNCHED();
 }
 
+// assemble_banded (pipeline.hpp:103-115) on the device: entry (i, j) -> slot j*(2k+1) + (i-j+k); the
+// first entry outside the band (lowest row, then position) is reported through bad = i * n + j.
+__global__ void k_assemble_band(const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ v,
+                                int n, int k, double* __restrict__ band, unsigned long long* __restrict__ bad) {
+    const long long w = 2LL * k + 1;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        for (int s = rp[i]; s < rp[i + 1]; ++s) {
+            const int j = ci[s];
+            if (i - j > k || j - i > k)
+                atomicMin(bad, (unsigned long long)i * (unsigned long long)n + (unsigned long long)j);
+            else
+                band[(long long)j * w + (i - j + k)] = v[s];
+        }
+}
+
+void launch_assemble_band(const int* rp, const int* ci, const double* v, int n, int k, double* band,
+                          unsigned long long* bad, cudaStream_t s) {
+    if (n <= 0) return;
+    k_assemble_band<<<std::min(ceil_div(n, 256), 148 * 8), 256, 0, s>>>(rp, ci, v, n, k, band, bad);
+    SAP_LAUNCHED();
+}
+
 }  // namespace sapgpu

@@ -196,6 +196,18 @@ class Solver:
         if self.options.precond in (PrecondKind.coupled, PrecondKind.decoupled):
             self.layout = make_partition_layout(n, self.p, k)
 
+    def setup_from_csr(self, row_ptr, col_idx, values, k: int) -> None:
+        """assemble_banded (pipeline.hpp:103-115) on the device + setup; entries outside k raise ValueError."""
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int32)
+        ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        n = len(rp) - 1
+        _check(L.load().sap_setup_banded_from_csr(self._h, n, k, len(ci), rp.ctypes.data, ci.ctypes.data,
+                                                  v.ctypes.data, 0))
+        self.n, self.k = n, k
+        if self.options.precond in (PrecondKind.coupled, PrecondKind.decoupled):
+            self.layout = make_partition_layout(n, self.p, k)
+
     def set_operator_csr(self, row_ptr, col_idx, values) -> None:
         rp = np.ascontiguousarray(row_ptr, dtype=np.int32)
         ci = np.ascontiguousarray(col_idx, dtype=np.int32)

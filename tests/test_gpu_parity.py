@@ -401,3 +401,53 @@ def test_mixed_precision_solve_reaches_full_accuracy(sap, oracle, kind):
         _, so = oracle.ref_solve_banded(n, k, band, rhs, p, kind, mixed_precision=True)
         assert so["converged"] and st.iterations <= so["iterations"] + 1.0, (st.iterations, so["iterations"])
     s.close()
+
+
+def _convection_diffusion_csr(s):
+    """3-D 7-point upwind convection-diffusion on an s^3 grid (SURVEY §8d config 4 at small s):
+    diagonal 6.3, -1.3 towards x-1/y-1/z-1, -0.7 towards +1; natural ordering, half-bandwidth s^2."""
+    n = s ** 3
+    rows, cols, vals = [], [], []
+    for z in range(s):
+        for y in range(s):
+            for x in range(s):
+                i = (z * s + y) * s + x
+                for dz, dy, dx, v in ((-1, 0, 0, -1.3), (0, -1, 0, -1.3), (0, 0, -1, -1.3), (0, 0, 0, 6.3),
+                                      (0, 0, 1, -0.7), (0, 1, 0, -0.7), (1, 0, 0, -0.7)):
+                    zz, yy, xx = z + dz, y + dy, x + dx
+                    if 0 <= zz < s and 0 <= yy < s and 0 <= xx < s:
+                        rows.append(i)
+                        cols.append((zz * s + yy) * s + xx)
+                        vals.append(v)
+    order = np.lexsort((np.array(cols), np.array(rows)))
+    r, c, v = np.array(rows)[order], np.array(cols)[order], np.array(vals)[order]
+    rp = np.zeros(n + 1, np.int32)
+    np.add.at(rp, r + 1, 1)
+    return n, np.cumsum(rp).astype(np.int32), c.astype(np.int32), v
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_sparse_pipeline_device_assembly_matches_solve_sparse(sap, oracle, kind):
+    """Config 4's path without the host reorderings: assemble_banded on the device from the CSR matrix
+    (pipeline.hpp:103-115), the banded SaP setup, BiCGStab(2) over the CSR operator (pipeline.hpp:336-338),
+    against the reference's solve_sparse with use_db = use_cm = false, drop_tol = 0."""
+    if not oracle.has_ref():
+        pytest.skip("compiled reference absent")
+    s_ = 10
+    n, rp, ci, v = _convection_diffusion_csr(s_)
+    k = int(np.max(np.abs(np.repeat(np.arange(n), np.diff(rp)) - ci)))
+    assert k == s_ * s_
+    xs = np.array([1.0 + 399.0 * (1.0 - (2.0 * i / (n - 1) - 1.0) ** 2) for i in range(n)])  # 1 -> 400 -> 1
+    rhs = oracle.csr_matvec(n, rp, ci, v, xs)
+    xr, so = oracle.ref_solve_sparse(n, rp, ci, v, rhs, 2, kind)
+    assert so["converged"] and so["k_after"] == k
+    s = sap.Solver(p=2, precond=kind)
+    s.setup_from_csr(rp, ci, v, k)
+    s.set_operator_csr(rp, ci, v)
+    x, st = s.solve(rhs)
+    assert st.converged and st.final_relative_residual <= 1e-10
+    assert abs(st.iterations - so["iterations"]) <= 1.0, (st.iterations, so["iterations"])
+    assert rel2(x, xr) <= 1e-8
+    with pytest.raises(ValueError, match="outside half-bandwidth"):
+        s.setup_from_csr(rp, ci, v, k - 1)
+    s.close()
