@@ -188,9 +188,28 @@ sap_status sap_get_report(const sap_handle* h, sap_report* rep);
  * which = 0: LU, 1: UL (SaP-C only). out: sizes[part]*(2k+1) doubles in the
  * reference's per-block band layout. boosts / block_norm may be NULL. */
 sap_status sap_get_factor(sap_handle* h, int part, int which, double* out, int* boosts, double* block_norm);
-/* Interface t in [0, p-1): w = k. Any output pointer may be NULL. */
+/* Interface t in [0, p-1): w = k (third stage: w_t). Any output pointer may be NULL. */
 sap_status sap_get_spike(sap_handle* h, int iface, double* b_block, double* c_block, double* v_bottom,
                          double* w_top, double* rbar, int* rbar_boosts);
+
+/* ---- third stage: per-block reordering (PipelineConfig::third_stage, pipeline.hpp:312-319) ----
+ * Arms every following sap_setup_banded / sap_setup_banded_from_csr of a coupled or decoupled
+ * preconditioner with sap::third_stage's result (ThirdStageResult, reorder_cm.hpp:227-231), computed
+ * on the host by the caller: block_k[p] the per-partition half-bandwidths (each in [0, k]; p must equal
+ * the setup's partition count), has_perm[p] (NULL = no permutations) and perm[n]: for a block b with
+ * has_perm[b], perm[offsets[b] + r] is the position of block row r in the reordered block. The setup
+ * then factors P_b A_b P_b^T at K_b (LU only; block_factors.hpp:138-206), extracts the couplings at
+ * w_t = max(K_t, K_{t+1}) (spike.hpp:95-116) and solves full spikes (compute_full_spikes,
+ * spike.hpp:258-296); every block solve permutes (block_solve, block_factors.hpp:210-236).
+ * Errors: a nonzero entry pushed outside K_b -> SAP_ERR_INVALID_ARGUMENT ("factor_blocks: block
+ * permutation exceeds bandwidth K_b"); a non-finite spike -> SAP_ERR_PRECONDITIONER.
+ * block_k == NULL disarms. Single-GPU handles only. sap_get_factor then returns block b at its own
+ * bandwidth (m_b*(2K_b+1) doubles) and sap_get_spike w_t x w_t blocks. */
+sap_status sap_set_third_stage(sap_handle* h, int p, const int* block_k, const int* has_perm, const int* perm, int n);
+/* SpikeSet::v_full / w_full of interface t (third stage, coupled): V_t (sizes[t] x w_t) and W_t
+ * (sizes[t+1] x w_t), column-major in the original row order, as compute_full_spikes stores them.
+ * Either pointer may be NULL. */
+sap_status sap_get_full_spike(sap_handle* h, int iface, double* v_full, double* w_full);
 
 /* ---- multi-GPU (one process per GPU) ----
  * Communication is supplied by the caller (NCCL through torch.distributed on a

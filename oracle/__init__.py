@@ -277,3 +277,119 @@ def ref_solve_sparse(n, row_ptr, col_idx, vals, rhs, p, kind, use_db=False, db_s
                                          x, rep, C.byref(it), C.byref(conv), C.byref(res), C.byref(fail)))
     return x, dict(iterations=it.value, converged=bool(conv.value), final_relative_residual=res.value,
                    failure=fail.value, k_after=int(rep[9]), report=rep)
+
+
+# ---------------------------------------------------------------------------
+# Third stage (per-block reordering) through the compiled reference. The C restatement does not
+# cover it: these wrappers ARE the checker for the third-stage path (the reference's own
+# third_stage / factor_blocks(perms) / compute_full_spikes / apply / build_precond_op code).
+
+def _ts_args(p, block_k, has_perm, perm, n):
+    kb = np.ascontiguousarray(block_k, np.int32)
+    hp = np.ascontiguousarray(has_perm if has_perm is not None else np.zeros(p), np.int32)
+    pm = np.ascontiguousarray(perm if perm is not None else np.zeros(max(n, 1)), np.int32)
+    return kb, hp, pm
+
+
+def ref_third_stage(n, k, band, p, seed=0):
+    """sap::third_stage (reorder_cm.hpp:233-274): (block_k[p], has_perm[p], perm[n])."""
+    kb = np.zeros(p, np.int32)
+    hp = np.zeros(p, np.int32)
+    pm = np.zeros(max(n, 1), np.int32)
+    R = ref()
+    R.sapref_third_stage.argtypes = [C.c_int, C.c_int, _dp, C.c_int, C.c_uint, _ip, _ip, _ip]
+    _ref_check(R.sapref_third_stage(n, k, band, p, seed, kb, hp, pm))
+    return kb, hp, pm[:n]
+
+
+def ref_third_setup(n, k, band, p, block_k, has_perm, perm, coupled=True, boost_eps=1e-10):
+    """factor_blocks(perms, K_b) + extract_coupling + compute_full_spikes; per-block / per-interface lists."""
+    kb, hp, pm = _ts_args(p, block_k, has_perm, perm, n)
+    sizes, offsets = partition_layout(n, p, k)
+    lu = np.zeros(sum(int(sizes[b]) * (2 * int(kb[b]) + 1) for b in range(p)))
+    boosts = np.zeros(p, np.int32)
+    norms = np.zeros(p)
+    wid = [int(max(kb[t], kb[t + 1])) for t in range(p - 1)]
+    ww = max(sum(w * w for w in wid), 1)
+    B, Cb, vb, wt, rb = (np.zeros(ww) for _ in range(5))
+    rbo = np.zeros(max(p - 1, 1), np.int32)
+    vf = np.zeros(max(sum(int(sizes[t]) * wid[t] for t in range(p - 1)), 1))
+    wf = np.zeros(max(sum(int(sizes[t + 1]) * wid[t] for t in range(p - 1)), 1))
+    R = ref()
+    R.sapref_third_setup.argtypes = [C.c_int, C.c_int, _dp, C.c_int, _ip, _ip, _ip, C.c_double, C.c_int, _dp, _ip,
+                                     _dp, _dp, _dp, _dp, _dp, _dp, _ip, _dp, _dp]
+    _ref_check(R.sapref_third_setup(n, k, band, p, kb, hp, pm, boost_eps, int(coupled), lu, boosts, norms, B, Cb, vb,
+                                    wt, rb, rbo, vf, wf))
+    out = dict(lu=[], boosts=boosts, norms=norms, B=[], C=[], vb=[], wt=[], rbar=[], rbar_boosts=rbo[:p - 1],
+               v_full=[], w_full=[], widths=wid)
+    o = 0
+    for b in range(p):
+        ln = int(sizes[b]) * (2 * int(kb[b]) + 1)
+        out["lu"].append(lu[o:o + ln])
+        o += ln
+    o = ov = ow = 0
+    for t, w in enumerate(wid):
+        for key, arr in (("B", B), ("C", Cb), ("vb", vb), ("wt", wt), ("rbar", rb)):
+            out[key].append(arr[o:o + w * w].reshape(w, w))
+        o += w * w
+        mt, mn = int(sizes[t]), int(sizes[t + 1])
+        out["v_full"].append(vf[ov:ov + mt * w].reshape(w, mt).T)
+        out["w_full"].append(wf[ow:ow + mn * w].reshape(w, mn).T)
+        ov += mt * w
+        ow += mn * w
+    return out
+
+
+def ref_third_apply(n, k, band, p, block_k, has_perm, perm, kind, x, boost_eps=1e-10):
+    kb, hp, pm = _ts_args(p, block_k, has_perm, perm, n)
+    out = np.zeros(n)
+    R = ref()
+    R.sapref_third_apply.argtypes = [C.c_int, C.c_int, _dp, C.c_int, _ip, _ip, _ip, C.c_int, C.c_double, _dp, _dp]
+    _ref_check(R.sapref_third_apply(n, k, band, p, kb, hp, pm, kind, boost_eps, np.ascontiguousarray(x, np.float64),
+                                    out))
+    return out
+
+
+def ref_third_solve_banded(n, k, band, rhs, p, block_k, has_perm, perm, kind, boost_eps=1e-10, ell=2,
+                           rel_tol=1e-10, max_iterations=500, mixed_precision=False):
+    kb, hp, pm = _ts_args(p, block_k, has_perm, perm, n)
+    x = np.zeros(n)
+    it, conv, res, fail = C.c_double(), C.c_int(), C.c_double(), C.c_int()
+    R = ref()
+    R.sapref_third_solve_banded.argtypes = [C.c_int, C.c_int, _dp, _dp, C.c_int, _ip, _ip, _ip, C.c_int, C.c_double,
+                                            C.c_int, C.c_double, C.c_int, C.c_int, _dp, C.POINTER(C.c_double),
+                                            C.POINTER(C.c_int), C.POINTER(C.c_double), C.POINTER(C.c_int)]
+    _ref_check(R.sapref_third_solve_banded(n, k, band, np.ascontiguousarray(rhs, np.float64), p, kb, hp, pm, kind,
+                                           boost_eps, ell, rel_tol, max_iterations, int(mixed_precision), x,
+                                           C.byref(it), C.byref(conv), C.byref(res), C.byref(fail)))
+    return x, dict(iterations=it.value, converged=bool(conv.value), final_relative_residual=res.value,
+                   failure=fail.value)
+
+
+def scrambled_banded(n, kn, window, k, d, seed):
+    """Test input for the third stage: a random diagonally dominant band of half-bandwidth kn,
+    symmetrically permuted by reversing every `window` consecutive indices (bandwidth grows to at most
+    2*window - 1 + kn <= k), stored at half-bandwidth k. Cuthill-McKee recovers a narrow band per block."""
+    rng = np.random.default_rng(seed)
+    pos = np.arange(n)
+    w0 = (pos // window) * window
+    perm = np.minimum(w0 + window - 1, n - 1) - (pos - w0)  # new index of old index i
+    if n % window:  # tail window reversed within its own length
+        t0 = (n // window) * window
+        perm[t0:] = n - 1 - (pos[t0:] - t0)
+    band = np.zeros(n * (2 * k + 1))
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        off = 0.0
+        for j in range(max(0, i - kn), min(n, i + kn + 1)):
+            if j == i:
+                continue
+            v = rng.uniform(-1, 1) or 0.5
+            rows.append(i); cols.append(j); vals.append(v)
+            off += abs(v)
+        rows.append(i); cols.append(i); vals.append(d * off)
+    for i, j, v in zip(rows, cols, vals):
+        pi, pj = int(perm[i]), int(perm[j])
+        assert abs(pi - pj) <= k
+        band[pj * (2 * k + 1) + (pi - pj + k)] = v
+    return band

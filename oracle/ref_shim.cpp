@@ -19,6 +19,10 @@
 //                             proj/include/sap/krylov.hpp:434-442), the dense wiring of
 //                             proj/tests/acceptance.cpp:114-132.
 //   * sapref_solve_sparse   : sap::solve_sparse (proj/include/sap/pipeline.hpp:213-369).
+//   * sapref_third_*        : the third stage - sap::third_stage (proj/include/sap/reorder_cm.hpp:233-274),
+//                             factor_blocks with block permutations and per-partition bandwidths,
+//                             compute_full_spikes (spike.hpp:258-296), apply_preconditioner and
+//                             build_precond_op(third_active = true) + run_krylov.
 #include <chrono>
 #include <cstdio>
 #include <cstring>
@@ -56,6 +60,20 @@ sap::BandedMatrix<double> wrap_band(int n, int k, const double* band) {
 
 double seconds_since(std::chrono::steady_clock::time_point t0) {
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+sap::PartitionLayout ts_layout(int n, int p, int k, const int* block_k) {
+    sap::PartitionLayout l = sap::make_partition_layout(n, p, k);
+    l.per_partition_k.assign(block_k, block_k + p);
+    return l;
+}
+
+// block_perms as sap::third_stage returns them: empty vector = identity
+std::vector<std::vector<int>> ts_perms(const sap::PartitionLayout& l, const int* has_perm, const int* perm) {
+    std::vector<std::vector<int>> out(static_cast<std::size_t>(l.p));
+    for (int b = 0; b < l.p; ++b)
+        if (has_perm && has_perm[b]) out[static_cast<std::size_t>(b)].assign(perm + l.offset(b), perm + l.offset(b) + l.size(b));
+    return out;
 }
 
 }  // namespace
@@ -275,6 +293,113 @@ int sapref_solve_sparse(int n, const int* row_ptr, const int* col_idx, const dou
     *final_res = rep.stats.final_relative_residual;
     *failure = static_cast<int>(rep.stats.failure);
     if (!rep.success && !rep.failure_stage.empty()) g_err = rep.failure_stage + ": " + rep.failure_message;
+    SAPREF_CATCH
+}
+
+// sap::third_stage: block_k[p], has_perm[p], perm[n] (perm[offset(b) + r] = new position of block row r).
+int sapref_third_stage(int n, int k, const double* band, int p, unsigned seed, int* block_k, int* has_perm,
+                       int* perm) {
+    SAPREF_TRY
+    const auto a = wrap_band(n, k, band);
+    const auto layout = sap::make_partition_layout(n, p, k);
+    const sap::ThirdStageResult ts = sap::third_stage(a, layout, seed);
+    for (int b = 0; b < p; ++b) {
+        block_k[b] = ts.block_k[static_cast<std::size_t>(b)];
+        const auto& pm = ts.block_perms[static_cast<std::size_t>(b)];
+        has_perm[b] = pm.empty() ? 0 : 1;
+        for (int r = 0; r < layout.size(b); ++r) perm[layout.offset(b) + r] = pm.empty() ? r : pm[static_cast<std::size_t>(r)];
+    }
+    SAPREF_CATCH
+}
+
+// Third-stage setup: factor_blocks (LU only, perms, K_b) + extract_coupling + compute_full_spikes.
+// lu_out: blocks at their own bandwidth back to back (m_b*(2K_b+1)); b/c/vb/wt/rbar: w_t x w_t per
+// interface back to back; vfull/wfull: m_t x w_t and m_{t+1} x w_t column-major back to back. Any
+// spike output may be null (coupled = 0 skips the spikes).
+int sapref_third_setup(int n, int k, const double* band, int p, const int* block_k, const int* has_perm,
+                       const int* perm, double boost_eps, int coupled, double* lu_out, int* boosts, double* norms,
+                       double* b_out, double* c_out, double* vb_out, double* wt_out, double* rbar_out,
+                       int* rbar_boosts, double* vfull_out, double* wfull_out) {
+    SAPREF_TRY
+    const auto a = wrap_band(n, k, band);
+    const auto layout = ts_layout(n, p, k, block_k);
+    const auto perms = ts_perms(layout, has_perm, perm);
+    const auto f = sap::factor_blocks<double>(a, layout, sap::FactorMode::lu_only, boost_eps, &perms);
+    std::size_t off = 0;
+    for (int b = 0; b < p; ++b) {
+        const auto& lu = f.lu[static_cast<std::size_t>(b)];
+        if (lu_out) std::memcpy(lu_out + off, lu.data(), sizeof(double) * lu.size());
+        off += lu.size();
+        if (boosts) boosts[b] = f.boost_count[static_cast<std::size_t>(b)];
+        if (norms) norms[b] = f.block_norm[static_cast<std::size_t>(b)];
+    }
+    if (!coupled || p < 2) return 0;
+    const auto cb = sap::extract_coupling<double>(a, layout);
+    const auto s = sap::compute_full_spikes<double>(f, cb);
+    std::size_t o2 = 0, ov = 0, ow = 0;
+    for (int t = 0; t < s.interfaces(); ++t) {
+        const auto T = static_cast<std::size_t>(t);
+        const std::size_t ww = s.v_bottom[T].size();
+        if (b_out) std::memcpy(b_out + o2, cb.b_blocks[T].data(), sizeof(double) * ww);
+        if (c_out) std::memcpy(c_out + o2, cb.c_blocks[T].data(), sizeof(double) * ww);
+        if (vb_out) std::memcpy(vb_out + o2, s.v_bottom[T].data(), sizeof(double) * ww);
+        if (wt_out) std::memcpy(wt_out + o2, s.w_top[T].data(), sizeof(double) * ww);
+        if (rbar_out) std::memcpy(rbar_out + o2, s.rbar[T].data(), sizeof(double) * ww);
+        if (rbar_boosts) rbar_boosts[t] = s.rbar_boosts[T];
+        if (vfull_out) std::memcpy(vfull_out + ov, s.v_full[T].data(), sizeof(double) * s.v_full[T].size());
+        if (wfull_out) std::memcpy(wfull_out + ow, s.w_full[T].data(), sizeof(double) * s.w_full[T].size());
+        o2 += ww;
+        ov += s.v_full[T].size();
+        ow += s.w_full[T].size();
+    }
+    SAPREF_CATCH
+}
+
+// apply_preconditioner over third-stage factors; kind 0 coupled, 1 decoupled.
+int sapref_third_apply(int n, int k, const double* band, int p, const int* block_k, const int* has_perm,
+                       const int* perm, int kind, double boost_eps, const double* in, double* out) {
+    SAPREF_TRY
+    const auto a = wrap_band(n, k, band);
+    const auto layout = ts_layout(n, p, k, block_k);
+    const auto perms = ts_perms(layout, has_perm, perm);
+    const auto f = sap::factor_blocks<double>(a, layout, sap::FactorMode::lu_only, boost_eps, &perms);
+    sap::SpikeSet<double> s;
+    if (kind == 0 && p > 1) s = sap::compute_full_spikes<double>(f, sap::extract_coupling<double>(a, layout));
+    const auto r = sap::apply_preconditioner<double>(static_cast<sap::PrecondKind>(kind), f, s,
+                                                     std::span<const double>(in, static_cast<std::size_t>(n)));
+    std::memcpy(out, r.data(), sizeof(double) * r.size());
+    SAPREF_CATCH
+}
+
+// build_precond_op(third_active = true, block_perms) + run_krylov, A = BandedMatrix::matvec.
+int sapref_third_solve_banded(int n, int k, const double* band, const double* rhs, int p, const int* block_k,
+                              const int* has_perm, const int* perm, int kind, double boost_eps, int ell,
+                              double rel_tol, int max_iterations, int mixed_precision, double* x_out,
+                              double* iterations, int* converged, double* final_res, int* failure) {
+    SAPREF_TRY
+    const auto a = wrap_band(n, k, band);
+    const auto layout = ts_layout(n, p, k, block_k);
+    const auto perms = ts_perms(layout, has_perm, perm);
+    sap::PipelineConfig cfg;
+    cfg.p = p;
+    cfg.precond = static_cast<sap::PrecondKind>(kind);
+    cfg.boost_eps = boost_eps;
+    cfg.krylov.ell = ell;
+    cfg.krylov.rel_tol = rel_tol;
+    cfg.krylov.max_iterations = max_iterations;
+    cfg.krylov.mixed_precision = mixed_precision != 0;
+    sap::PipelineReport rep;
+    const sap::LinearOp op_m = mixed_precision
+                                   ? sap::detail::build_precond_op<float>(a, layout, cfg, true, &perms, rep)
+                                   : sap::detail::build_precond_op<double>(a, layout, cfg, true, &perms, rep);
+    sap::LinearOp op_a = [&a](std::span<const double> in, std::span<double> out) { a.matvec(in, out); };
+    std::vector<double> x(static_cast<std::size_t>(n), 0.0);
+    const sap::SolveStats st = sap::run_krylov(op_a, op_m, std::span<const double>(rhs, static_cast<std::size_t>(n)), x, cfg.krylov);
+    std::memcpy(x_out, x.data(), sizeof(double) * x.size());
+    *iterations = st.iterations;
+    *converged = st.converged ? 1 : 0;
+    *final_res = st.final_relative_residual;
+    *failure = static_cast<int>(st.failure);
     SAPREF_CATCH
 }
 

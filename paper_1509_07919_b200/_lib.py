@@ -68,6 +68,8 @@ SIGNATURES = {
     "sap_get_report": (C.c_int, [_vp, C.POINTER(sap_report)]),
     "sap_get_factor": (C.c_int, [_vp, C.c_int, C.c_int, _vp, _ip, _dp]),
     "sap_get_spike": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, _vp, _vp, _ip]),
+    "sap_set_third_stage": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, C.c_int]),
+    "sap_get_full_spike": (C.c_int, [_vp, C.c_int, _vp, _vp]),
     "sap_rank_rows": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _ip, _ip]),
     "sap_create_distributed": (C.c_int, [C.POINTER(sap_options), C.POINTER(sap_comm), C.POINTER(_vp)]),
     "sap_setup_banded_dist": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp, C.c_int]),

@@ -121,6 +121,14 @@ struct sap_handle {
     DevBuf<double> asm_v;
     DevBuf<unsigned long long> asm_bad;
     DevBuf<TipJob> tipjobs;
+    // third stage (sap_set_third_stage): ThirdStageResult (reorder_cm.hpp:227-231) applied at setup
+    bool ts_armed = false;  // set by the caller; consumed by every following block setup
+    bool ts = false;        // the current setup runs the third-stage path
+    std::vector<int> ts_k, ts_has, ts_perm, widths;
+    DevBuf<int> d_gperm, d_has, d_kb, d_wid, d_bad;
+    DevBuf<double> vfull, wfull, norms_op, scratch_p;
+    DevBuf<float> scratch_pf;
+    DevBuf<FullSpikeJob> fsjobs;
     // multi-GPU (sap_create_distributed): this rank owns global rows [row_lo, row_hi) = partitions
     // [pb, pe); the band slice holds global columns [c_lo, c_hi). Interface slots are ordered
     // [left cross?, local 0..p_loc-2, right cross?]; cross interfaces are solved on both ranks.
@@ -264,14 +272,22 @@ void apply_m_fp32(sap_handle* h, const double* in, double* out) {
     const int n = h->n, p = h->layout.p, k = h->k;
     float* o = h->o_f.get();
     launch_cast_d2f(in, o, n, s);
+    // block_solve with block permutations (block_factors.hpp:222-229): gather, sweep, scatter back
+    auto solve = [&](float* v) {
+        if (!h->ts) return launch_block_solve<float>(h->lplan_f, v, s);
+        float* t = h->scratch_pf.get();
+        launch_permute<float>(h->d_gperm.get(), v, t, n, true, s);
+        launch_block_solve<float>(h->lplan_f, t, s);
+        launch_permute<float>(h->d_gperm.get(), t, v, n, false, s);
+    };
     if (h->coupled) {
         float* g = h->g_f.get();
         SAP_CUDA(cudaMemcpyAsync(g, o, sizeof(float) * (size_t)n, cudaMemcpyDeviceToDevice, s));
-        launch_block_solve<float>(h->lplan_f, g, s);
+        solve(g);
         launch_interfaces<float>(g, h->d_offsets.get(), h->rplan_f, p - 1, k, h->wt_f.get(), h->vb_f.get(),
                                  h->bblk_f.get(), h->cblk_f.get(), h->xt_f.get(), h->xb_f.get(), o, false, false, s);
     }
-    launch_block_solve<float>(h->lplan_f, o, s);
+    solve(o);
     launch_cast_f2d(o, out, n, s);
 }
 
@@ -292,6 +308,22 @@ void apply_m(sap_handle* h, const double* in, double* out) {
     }
     if (h->mixed) return apply_m_fp32(h, in, out);
     const int p = h->layout.p, k = h->k;
+    if (h->ts) {
+        // block_solve with block permutations (block_factors.hpp:222-229): gather, sweep, scatter back
+        double* t = h->scratch_p.get();
+        launch_permute<double>(h->d_gperm.get(), in, t, n, true, s);
+        launch_block_solve<double>(h->lplan, t, s);
+        if (!h->coupled) return launch_permute<double>(h->d_gperm.get(), t, out, n, false, s);
+        double* g = h->scratch_g.get();
+        launch_permute<double>(h->d_gperm.get(), t, g, n, false, s);
+        if (out != in) SAP_CUDA(cudaMemcpyAsync(out, in, bytes, cudaMemcpyDeviceToDevice, s));
+        launch_interfaces<double>(g, h->d_offsets.get(), h->rplan, p - 1, k, h->wt.get(), h->vb.get(),
+                                  h->bblk.get(), h->cblk.get(), h->xt.get(), h->xb.get(), out, false, false, s);
+        launch_permute<double>(h->d_gperm.get(), out, t, n, true, s);
+        launch_block_solve<double>(h->lplan, t, s);
+        launch_permute<double>(h->d_gperm.get(), t, out, n, false, s);
+        return;
+    }
     if (!h->coupled) {
         if (out != in) SAP_CUDA(cudaMemcpyAsync(out, in, bytes, cudaMemcpyDeviceToDevice, s));
         launch_block_solve<double>(h->lplan, out, s);
@@ -334,6 +366,23 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
     h->layout = L;
     const int p = L.p;
     h->coupled = h->kind == SAP_PRECOND_COUPLED && p > 1;
+    // third stage (pipeline.hpp:312-319): only for the block preconditioners
+    h->ts = h->ts_armed && blocks && n > 0;
+    if (h->ts) {
+        require((int)h->ts_k.size() == p, "third stage: block count does not match the partition layout");
+        for (int b = 0; b < p; ++b) {
+            require(h->ts_k[b] >= 0 && h->ts_k[b] <= k,
+                    "third stage: per-partition half-bandwidth outside [0, k]");
+            if (!h->ts_has[b]) continue;
+            std::vector<char> seen(L.sizes[b], 0);
+            for (int r = 0; r < L.sizes[b]; ++r) {
+                const int v = h->ts_perm[L.offsets[b] + r];
+                require(v >= 0 && v < L.sizes[b] && !seen[v], "third stage: block permutation is not a permutation");
+                seen[v] = 1;
+            }
+        }
+    }
+    const bool want_ul = h->coupled && !h->ts;  // build_precond_op: UL only without the third stage (:163-164)
     h->rep = sap_report{};
     h->rep.n = n;
     h->rep.k = k;
@@ -388,21 +437,22 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
     const int m_max = L.sizes[0];
     h->fst = BandStore::make(m_max, k);
     h->lu.alloc(h->fst.total(p));
-    if (h->coupled)
+    if (want_ul)
         h->ul.alloc(h->fst.total(p));
     else
         h->ul.release();
-    const int njobs = h->coupled ? 2 * p : p;
+    const int njobs = want_ul ? 2 * p : p;
     std::vector<FactorJob> jobs(njobs);
-    // the default LU kernel reads the unfactored blocks straight from the band (no block copies)
-    const bool from_src = band_lu_reads_source(k);
+    // the default LU kernel reads the unfactored blocks straight from the band (no block copies);
+    // the third stage factors the permuted blocks assembled in the store
+    const bool from_src = band_lu_reads_source(k) && !h->ts;
     const size_t w = 2 * (size_t)k + 1;
     for (int b = 0; b < p; ++b) {
         const int m = L.sizes[b];
         double* f = h->lu.get() + h->fst.block(b);
         const double* a = h->band_ptr + (size_t)L.offsets[b] * w;
         jobs[b] = FactorJob{f + k, 1, 2LL * k, m, k, h->norms.get() + b, h->boosts.get() + b, from_src ? a + k : nullptr};
-        if (h->coupled) {
+        if (want_ul) {
             double* g = h->ul.get() + h->fst.block(b);
             const size_t last = (size_t)(m - 1) * w + k;
             jobs[p + b] = FactorJob{g + last, -1, -2LL * k, m, k, h->norms.get() + b, h->boosts.get() + p + b,
@@ -415,13 +465,38 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
     SAP_CUDA(cudaMemsetAsync(h->kappa.get(), 0, 2 * sizeof(unsigned long long), s));
     h->op_nonfinite.alloc(1);
     SAP_CUDA(cudaMemsetAsync(h->op_nonfinite.get(), 0, sizeof(int), s));
-    launch_block_norms(h->band_ptr, m_max, k, h->d_offsets.get(), p, nullptr, h->norms.get(), s,
-                       h->op_nonfinite.get());
-    if (from_src)
-        launch_zero_pad(k, h->d_offsets.get(), p, h->fst, h->lu.get(), h->coupled ? h->ul.get() : nullptr, s);
-    else
-        launch_copy_blocks(h->band_ptr, k, h->d_offsets.get(), p, h->fst, h->lu.get(),
-                           h->coupled ? h->ul.get() : nullptr, s);
+    if (h->ts) {
+        // P_b A_b P_b^T at K_b into the zeroed store (block_factors.hpp:155-180), norms over it (:187-195)
+        std::vector<int> gperm(n);
+        for (int b = 0; b < p; ++b)
+            for (int r = 0; r < L.sizes[b]; ++r)
+                gperm[L.offsets[b] + r] = L.offsets[b] + (h->ts_has[b] ? h->ts_perm[L.offsets[b] + r] : r);
+        h->d_gperm.alloc(n);
+        h->d_has.alloc(p);
+        h->d_kb.alloc(p);
+        h->d_bad.alloc(1);
+        SAP_CUDA(cudaMemcpyAsync(h->d_gperm.get(), gperm.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
+        SAP_CUDA(cudaMemcpyAsync(h->d_has.get(), h->ts_has.data(), sizeof(int) * p, cudaMemcpyHostToDevice, s));
+        SAP_CUDA(cudaMemcpyAsync(h->d_kb.get(), h->ts_k.data(), sizeof(int) * p, cudaMemcpyHostToDevice, s));
+        static const int big = 0x7fffffff;
+        SAP_CUDA(cudaMemcpyAsync(h->d_bad.get(), &big, sizeof(int), cudaMemcpyHostToDevice, s));
+        h->norms_op.alloc(p);
+        launch_block_norms(h->band_ptr, m_max, k, h->d_offsets.get(), p, nullptr, h->norms_op.get(), s,
+                           h->op_nonfinite.get());
+        SAP_CUDA(cudaMemsetAsync(h->lu.get(), 0, sizeof(double) * h->fst.total(p), s));
+        launch_assemble_blocks(h->band_ptr, n, k, h->d_offsets.get(), p, h->d_gperm.get(), h->d_has.get(),
+                               h->d_kb.get(), h->fst, h->lu.get(), h->d_bad.get(), s);
+        launch_block_norms(h->lu.get(), m_max, k, h->d_offsets.get(), p, &h->fst, h->norms.get(), s);
+        h->scratch_p.alloc(n);
+    } else {
+        launch_block_norms(h->band_ptr, m_max, k, h->d_offsets.get(), p, nullptr, h->norms.get(), s,
+                           h->op_nonfinite.get());
+        if (from_src)
+            launch_zero_pad(k, h->d_offsets.get(), p, h->fst, h->lu.get(), want_ul ? h->ul.get() : nullptr, s);
+        else
+            launch_copy_blocks(h->band_ptr, k, h->d_offsets.get(), p, h->fst, h->lu.get(),
+                               want_ul ? h->ul.get() : nullptr, s);
+    }
     SAP_CUDA(cudaEventRecord(h->ev[8], s));
     launch_band_lu(h->jobs.get(), njobs, k, h->opt.boost_eps, s);
     SAP_CUDA(cudaEventRecord(h->ev[9], s));
@@ -436,7 +511,7 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
         h->dinv.alloc(std::max<size_t>(sweep_dinv_elems(lp), 1));
         plan_sweeps(lp, h->dinv.get());
         lp.kappa = h->kappa.get();
-        if (h->coupled) {  // only the solve needs them: overlap with coupling / tips / reduced blocks
+        if (want_ul) {  // only the solve needs them: overlap with coupling / tips / reduced blocks
             SAP_CUDA(cudaEventRecord(h->sev[0], s));
             SAP_CUDA(cudaStreamWaitEvent(h->side, h->sev[0], 0));
             launch_chunk_inverses(lp, h->side);
@@ -450,7 +525,7 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
         // band_lu_inplace op count: sum over columns of d + 2 d^2, d = min(k, m-1-j)
         const double m = L.sizes[b], kk = std::min<double>(k, m - 1 > 0 ? m - 1 : 0);
         const double f = (m - kk) * (2 * kk * kk + kk) + (kk - 1) * kk * (4 * kk + 1) / 6.0;
-        h->rep.factor_flops += (h->coupled ? 2.0 : 1.0) * f;
+        h->rep.factor_flops += (want_ul ? 2.0 : 1.0) * f;
     }
 
     int ni = 0;
@@ -477,10 +552,46 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
         SAP_CUDA(cudaMemsetAsync(h->nonfinite.get(), 0, sizeof(int) * 3 * ni, s));
         SAP_CUDA(cudaMemsetAsync(h->rbar_boosts.get(), 0, sizeof(int) * ni, s));
         // ---- T_BC: extract_coupling ----
-        launch_extract_coupling(h->band_ptr, n, k, h->d_offsets.get(), p, h->bblk.get(), h->cblk.get(), s);
+        if (h->ts) {
+            h->widths.assign(ni, 0);
+            for (int t = 0; t < ni; ++t) h->widths[t] = std::max(h->ts_k[t], h->ts_k[t + 1]);  // spike.hpp:102
+            h->d_wid.alloc(ni);
+            SAP_CUDA(cudaMemcpyAsync(h->d_wid.get(), h->widths.data(), sizeof(int) * ni, cudaMemcpyHostToDevice, s));
+        }
+        launch_extract_coupling(h->band_ptr, n, k, h->d_offsets.get(), p, h->bblk.get(), h->cblk.get(), s,
+                                h->ts ? h->d_wid.get() : nullptr);
         SAP_CUDA(cudaEventRecord(h->ev[3], s));
-        // ---- T_SPK: spike tips ----
-        {
+        // ---- T_SPK: spike tips (third stage: full spikes, spike.hpp:258-296) ----
+        if (h->ts) {
+            const size_t nk = (size_t)n * k;
+            h->vfull.alloc(std::max<size_t>(nk, 1));
+            h->wfull.alloc(std::max<size_t>(nk, 1));
+            SAP_CUDA(cudaMemsetAsync(h->vfull.get(), 0, sizeof(double) * nk, s));
+            SAP_CUDA(cudaMemsetAsync(h->wfull.get(), 0, sizeof(double) * nk, s));
+            launch_full_rhs(h->bblk.get(), h->cblk.get(), k, h->d_offsets.get(), ni, h->d_gperm.get(),
+                            h->vfull.get(), h->wfull.get(), s);
+            std::vector<FullSpikeJob> fj;
+            for (int t = 0; t < ni; ++t) {
+                // forward sweeps start at the first permuted row carrying a right-hand side
+                const int e = L.offsets[t + 1];
+                int fv = L.sizes[t], fw = L.sizes[t + 1];
+                for (int r = 0; r < k; ++r) {
+                    const int ov = e - k + r - L.offsets[t], ow = r;
+                    fv = std::min(fv, h->ts_has[t] ? h->ts_perm[L.offsets[t] + ov] : ov);
+                    fw = std::min(fw, h->ts_has[t + 1] ? h->ts_perm[e + ow] : ow);
+                }
+                fj.push_back(FullSpikeJob{h->lu.get() + h->fst.block(t) + k, h->vfull.get() + (size_t)L.offsets[t] * k,
+                                          L.sizes[t], fv, 2 * t});
+                fj.push_back(FullSpikeJob{h->lu.get() + h->fst.block(t + 1) + k, h->wfull.get() + (size_t)e * k,
+                                          L.sizes[t + 1], fw, 2 * t + 1});
+            }
+            h->fsjobs.alloc(fj.size());
+            SAP_CUDA(cudaMemcpyAsync(h->fsjobs.get(), fj.data(), sizeof(FullSpikeJob) * fj.size(),
+                                     cudaMemcpyHostToDevice, s));
+            launch_full_spikes(h->fsjobs.get(), (int)fj.size(), k, h->nonfinite.get(), s);
+            launch_full_tips(h->vfull.get(), h->wfull.get(), k, h->d_offsets.get(), ni, h->d_gperm.get(),
+                             h->d_wid.get(), h->vb.get(), h->wt.get(), s);
+        } else {
             std::vector<TipJob> tj;
             for (int t = 0; t < ni; ++t) {
                 const size_t o = (size_t)t * k * k;
@@ -497,7 +608,9 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
         // ---- T_LUrdcd: rbar = I - W V (band layout, k' = w-1) and its boosted no-pivot LU ----
         if (k > 0) {
             launch_rbar(h->wt.get(), h->vb.get(), k, ni, h->rbar.get(), h->rst, h->nonfinite.get() + 2 * ni, s);
-            launch_block_norms(h->rbar.get(), k, k - 1, h->d_roffsets.get(), ni, &h->rst, h->rbar_norms.get(), s);
+            // third stage: R' = diag(R_t, I); the boost scale is R_t's norm (rows < w_t)
+            launch_block_norms(h->rbar.get(), k, k - 1, h->d_roffsets.get(), ni, &h->rst, h->rbar_norms.get(), s,
+                               nullptr, h->ts ? h->d_wid.get() : nullptr);
             std::vector<FactorJob> rj(ni);
             for (int t = 0; t < ni; ++t)
                 rj[t] = FactorJob{h->rbar.get() + h->rst.block(t) + (k - 1), 1, 2LL * (k - 1), k, k - 1,
@@ -519,10 +632,19 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
         launch_chunk_inverses(rp, s);
         }
         SAP_CUDA(cudaEventRecord(h->ev[5], s));
-        SAP_CUDA(cudaStreamWaitEvent(s, h->sev[1], 0));  // the LU chunk inverses (side stream)
+        if (want_ul) SAP_CUDA(cudaStreamWaitEvent(s, h->sev[1], 0));  // the LU chunk inverses (side stream)
     }
-    if (h->opt.mixed_precision) build_fp32_preconditioner(h, s);
+    if (h->opt.mixed_precision) {
+        build_fp32_preconditioner(h, s);
+        if (h->ts) h->scratch_pf.alloc(n);
+    }
     SAP_CUDA(cudaStreamSynchronize(s));
+    if (h->ts) {
+        int bad = 0;
+        SAP_CUDA(cudaMemcpy(&bad, h->d_bad.get(), sizeof(int), cudaMemcpyDeviceToHost));
+        if (bad != 0x7fffffff)
+            throw InvalidArgument("factor_blocks: block permutation exceeds bandwidth " + std::to_string(h->ts_k[bad]));
+    }
     choose_triangle_solve(h);
     h->rep.t_dtransf = ev_ms(h->ev[0], h->ev[1]) * 1e-3;
     h->rep.t_lu = ev_ms(h->ev[1], h->ev[2]) * 1e-3;
@@ -543,6 +665,9 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
         for (int t = 0; t < ni; ++t) h->rep.total_rbar_boosts += rb[t];
         // the reference throws at the first failure in interface order (spike.hpp:217-219, :246-248),
         // then at the first non-finite reduced block (:162-164)
+        for (int t = 0; t < ni && h->ts; ++t)  // compute_full_spikes, spike.hpp:279-280
+            if (nf[2 * t] || nf[2 * t + 1])
+                throw PreconditionerFailure("spike at interface " + std::to_string(t) + " is not finite");
         for (int t = 0; t < ni; ++t) {
             if (nf[2 * t]) throw PreconditionerFailure("right spike tip at interface " + std::to_string(t) + " is not finite");
             if (nf[2 * t + 1]) throw PreconditionerFailure("left spike tip at interface " + std::to_string(t) + " is not finite");
@@ -1053,6 +1178,7 @@ sap_status sap_setup_banded_dist(sap_handle* h, int n, int k, int row_lo, int ro
     return guard([&] {
         require(h != nullptr, "null handle");
         require(h->dist, "sap_setup_banded_dist: handle was not created by sap_create_distributed");
+        require(!h->ts_armed, "sap_setup_banded_dist: the third stage is not distributed");
         SAP_CUDA(cudaSetDevice(h->opt.device));
         setup_banded_dist(h, n, k, row_lo, row_hi, band_slice, on_device);
     });
@@ -1239,12 +1365,65 @@ sap_status sap_get_factor(sap_handle* h, int part, int which, double* out, int* 
         SAP_CUDA(cudaSetDevice(h->opt.device));
         const size_t w = 2 * (size_t)h->k + 1;
         const double* src = (which == 0 ? h->lu.get() : h->ul.get()) + h->fst.block(part);
-        if (out)
-            SAP_CUDA(cudaMemcpy(out, src, sizeof(double) * (size_t)h->layout.sizes[part] * w, cudaMemcpyDeviceToHost));
+        const int m = h->layout.sizes[part];
+        if (out && h->ts && h->ts_k[part] != h->k) {
+            // third stage: the reference stores block b at its own bandwidth K_b (block_factors.hpp:158-160)
+            std::vector<double> band((size_t)m * w);
+            SAP_CUDA(cudaMemcpy(band.data(), src, sizeof(double) * band.size(), cudaMemcpyDeviceToHost));
+            const int k = h->k, kb = h->ts_k[part];
+            const size_t wb = 2 * (size_t)kb + 1;
+            for (int j = 0; j < m; ++j)
+                for (int d = -kb; d <= kb; ++d) out[(size_t)j * wb + d + kb] = band[(size_t)j * w + d + k];
+        } else if (out) {
+            SAP_CUDA(cudaMemcpy(out, src, sizeof(double) * (size_t)m * w, cudaMemcpyDeviceToHost));
+        }
         if (boosts)
             SAP_CUDA(cudaMemcpy(boosts, h->boosts.get() + (which == 0 ? 0 : h->layout.p) + part, sizeof(int),
                                 cudaMemcpyDeviceToHost));
         if (block_norm) SAP_CUDA(cudaMemcpy(block_norm, h->norms.get() + part, sizeof(double), cudaMemcpyDeviceToHost));
+    });
+}
+
+sap_status sap_set_third_stage(sap_handle* h, int p, const int* block_k, const int* has_perm, const int* perm,
+                               int n) {
+    return guard([&] {
+        require(h != nullptr, "null handle");
+        if (!block_k) {
+            h->ts_armed = false;
+            return;
+        }
+        require(p >= 1 && n >= 0, "sap_set_third_stage: bad sizes");
+        require(perm != nullptr || has_perm == nullptr, "sap_set_third_stage: has_perm without perm");
+        h->ts_k.assign(block_k, block_k + p);
+        h->ts_has.assign(p, 0);
+        if (has_perm) h->ts_has.assign(has_perm, has_perm + p);
+        h->ts_perm.assign(n, 0);
+        if (perm) h->ts_perm.assign(perm, perm + n);
+        h->ts_armed = true;
+    });
+}
+
+sap_status sap_get_full_spike(sap_handle* h, int iface, double* v_full, double* w_full) {
+    return guard([&] {
+        require(h != nullptr, "null handle");
+        if (!h->ready) throw StateError("sap_get_full_spike before setup");
+        require(h->ts && h->coupled, "sap_get_full_spike: full spikes exist only for the coupled third stage");
+        require(iface >= 0 && iface < h->layout.p - 1, "sap_get_full_spike: interface out of range");
+        SAP_CUDA(cudaSetDevice(h->opt.device));
+        const int k = h->k, w = h->widths[iface], o = k - w;
+        for (int side = 0; side < 2; ++side) {
+            double* out = side == 0 ? v_full : w_full;
+            if (!out) continue;
+            const int b = iface + side, off = h->layout.offsets[b], m = h->layout.sizes[b];
+            std::vector<double> X((size_t)m * k);
+            SAP_CUDA(cudaMemcpy(X.data(), (side == 0 ? h->vfull.get() : h->wfull.get()) + (size_t)off * k,
+                                sizeof(double) * X.size(), cudaMemcpyDeviceToHost));
+            // reference layout: m x w column-major in original row order (spike.hpp:266-276)
+            for (int r = 0; r < m; ++r) {
+                const int pr = h->ts_has[b] ? h->ts_perm[off + r] : r;
+                for (int c = 0; c < w; ++c) out[(size_t)c * m + r] = X[(size_t)pr * k + (side == 0 ? c : o + c)];
+            }
+        }
     });
 }
 
@@ -1263,6 +1442,31 @@ sap_status sap_get_spike(sap_handle* h, int iface, double* b_block, double* c_bl
         }
         SAP_CUDA(cudaSetDevice(h->opt.device));
         const size_t ww = (size_t)h->k * h->k, off = ww * iface, bytes = sizeof(double) * ww;
+        if (h->ts) {
+            // third stage: interface width w_t <= k, embedded in the k x k corners (third.cu header)
+            const int k = h->k, w = h->widths[iface], o = k - w;
+            std::vector<double> B(ww), Cc(ww), V(ww), W(ww);
+            SAP_CUDA(cudaMemcpy(B.data(), h->bblk.get() + off, bytes, cudaMemcpyDeviceToHost));
+            SAP_CUDA(cudaMemcpy(Cc.data(), h->cblk.get() + off, bytes, cudaMemcpyDeviceToHost));
+            SAP_CUDA(cudaMemcpy(V.data(), h->vb.get() + off, bytes, cudaMemcpyDeviceToHost));
+            SAP_CUDA(cudaMemcpy(W.data(), h->wt.get() + off, bytes, cudaMemcpyDeviceToHost));
+            std::vector<double> band((size_t)k * (2 * (size_t)k - 1));
+            if (rbar && k > 0)
+                SAP_CUDA(cudaMemcpy(band.data(), h->rbar.get() + h->rst.block(iface), sizeof(double) * band.size(),
+                                    cudaMemcpyDeviceToHost));
+            for (int i = 0; i < w; ++i)
+                for (int j = 0; j < w; ++j) {
+                    const size_t d = (size_t)i * w + j;
+                    if (b_block) b_block[d] = B[(size_t)(o + i) * k + j];
+                    if (c_block) c_block[d] = Cc[(size_t)i * k + o + j];
+                    if (v_bottom) v_bottom[d] = V[(size_t)(o + i) * k + j];
+                    if (w_top) w_top[d] = W[(size_t)i * k + o + j];
+                    if (rbar) rbar[d] = band[(size_t)j * (2 * k - 1) + (i - j + k - 1)];
+                }
+            if (rbar_boosts)
+                SAP_CUDA(cudaMemcpy(rbar_boosts, h->rbar_boosts.get() + iface, sizeof(int), cudaMemcpyDeviceToHost));
+            return;
+        }
         if (b_block) SAP_CUDA(cudaMemcpy(b_block, h->bblk.get() + off, bytes, cudaMemcpyDeviceToHost));
         if (c_block) SAP_CUDA(cudaMemcpy(c_block, h->cblk.get() + off, bytes, cudaMemcpyDeviceToHost));
         if (v_bottom) SAP_CUDA(cudaMemcpy(v_bottom, h->vb.get() + off, bytes, cudaMemcpyDeviceToHost));

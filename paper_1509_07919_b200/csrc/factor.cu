@@ -43,7 +43,8 @@ long long g_launch_count = 0;
 // reference's `row > norm` test.
 __global__ void __launch_bounds__(256)
     k_block_norms(const double* __restrict__ a, int k, const int* __restrict__ offs, long long pstride, int pad,
-                  unsigned long long* __restrict__ norms_bits, int* __restrict__ nonfinite, int p) {
+                  unsigned long long* __restrict__ norms_bits, int* __restrict__ nonfinite, int p,
+                  const int* __restrict__ nrows) {
     const int lane = threadIdx.x & 31;
     const int b = blockIdx.y;
     const int off = offs[b], m = offs[b + 1] - off;
@@ -68,18 +69,19 @@ __global__ void __launch_bounds__(256)
         for (int c = m; c <= min(r + k, n - 1 - off); ++c) bad |= !isfinite(base[(long long)c * ld + r + k]);
         if (bad) atomicOr(nonfinite, 1);
     }
-    double best = (r < m && row > 0.0) ? row : 0.0;
+    double best = (r < m && row > 0.0 && (!nrows || r < nrows[b])) ? row : 0.0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
     if (lane == 0 && best > 0.0) atomicMax(norms_bits + b, (unsigned long long)__double_as_longlong(best));
 }
 
 void launch_block_norms(const double* band, int max_m, int k, const int* d_offsets, int p, const BandStore* store,
-                        double* norms, cudaStream_t s, int* nonfinite) {
+                        double* norms, cudaStream_t s, int* nonfinite, const int* d_nrows) {
     SAP_CUDA(cudaMemsetAsync(norms, 0, sizeof(double) * p, s));
     dim3 grid(ceil_div(ceil_div(max_m, 32), 8), p);
     k_block_norms<<<grid, 256, 0, s>>>(band, k, d_offsets, store ? store->pstride : 0, store ? store->pad : 0,
-                                        reinterpret_cast<unsigned long long*>(norms), store ? nullptr : nonfinite, p);
+                                        reinterpret_cast<unsigned long long*>(norms), store ? nullptr : nonfinite, p,
+                                        d_nrows);
     SAP_LAUNCHED();
 }
 

@@ -14,9 +14,10 @@ namespace sapgpu {
 // (factor_blocks' boost scale, block_factors.hpp:187-195). p blocks, offsets on device.
 // store == nullptr: `band` is one contiguous band (the A operator); otherwise the
 // blocks live in a BandStore.
+// d_nrows (optional): only rows r < d_nrows[b] of block b count (third-stage reduced blocks diag(R_t, I)).
 void launch_block_norms(const double* band, int max_m, int k, const int* d_offsets, int p, const BandStore* store,
                         double* norms, cudaStream_t s,
-                        int* nonfinite = nullptr);
+                        int* nonfinite = nullptr, const int* d_nrows = nullptr);
 // LU (and UL) BandStores = each diagonal block's band, entries outside the block zeroed.
 void launch_copy_blocks(const double* band, int k, const int* d_offsets, int p, const BandStore& st, double* lu,
                         double* ul, cudaStream_t s);
@@ -30,8 +31,9 @@ bool launch_band_lu_ws(const FactorJob* d_jobs, int njobs, int max_k, double boo
 void launch_dense_norms(const double* a, int w, int ni, double* norms, int* nonfinite, cudaStream_t s);
 
 // ---- spikes (spike.cu) ----
+// d_wid (optional, third stage): interface widths w_t <= k embedded in the k x k corners (third.cu).
 void launch_extract_coupling(const double* band, int n, int k, const int* d_offsets, int p, double* bblk,
-                             double* cblk, cudaStream_t s);
+                             double* cblk, cudaStream_t s, const int* d_wid = nullptr);
 // One spike tip (compute_spike_tips, spike.hpp:190-250): which 0 -> V^b = U^{-1} L^{-1} rhs on the
 // trailing corner of an LU block; which 1 -> W^t = L^{-1} U^{-1} rhs on the leading corner of a UL block.
 struct TipJob {
@@ -49,6 +51,27 @@ void launch_extract_one(const double* band, int n, int k, int e, int which, doub
 // matrix diag(rbar_0, ..., rbar_{ni-1}); nonfinite[t] flags a non-finite block.
 void launch_rbar(const double* wt, const double* vb, int w, int ni, double* rbar_band, const BandStore& rst,
                  int* nonfinite, cudaStream_t s);
+
+// ---- third stage: per-block reordering (third.cu) ----
+// P_b A_b P_b^T at bandwidth kb[b] into the (zeroed) LU store; *bad = min block with an entry outside.
+void launch_assemble_blocks(const double* band, int n, int k, const int* d_offsets, int p, const int* d_gperm,
+                            const int* d_has_perm, const int* d_kb, const BandStore& st, double* lu, int* bad,
+                            cudaStream_t s);
+struct FullSpikeJob {
+    const double* f;  // block LU: (i, j) at f[j * 2k + i]
+    double* x;        // m x k row-major: the right-hand sides in, the spike out
+    int m;
+    int first_row;    // right-hand-side rows above it are zero
+    int flag;         // nonfinite[flag] set on a non-finite spike entry
+};
+void launch_full_rhs(const double* bblk, const double* cblk, int k, const int* d_offsets, int ni,
+                     const int* d_gperm, double* vfull, double* wfull, cudaStream_t s);
+void launch_full_spikes(const FullSpikeJob* d_jobs, int njobs, int k, int* nonfinite, cudaStream_t s);
+size_t full_spike_smem(int k);
+void launch_full_tips(const double* vfull, const double* wfull, int k, const int* d_offsets, int ni,
+                      const int* d_gperm, const int* d_wid, double* vb, double* wt, cudaStream_t s);
+template <class T>
+void launch_permute(const int* d_gperm, const T* in, T* out, int n, bool scatter, cudaStream_t s);
 
 // ---- preconditioner apply (apply.cu) ----
 // Everything a block sweep needs, built once at setup: the factor BandStore,

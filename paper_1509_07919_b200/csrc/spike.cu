@@ -18,9 +18,11 @@
 namespace sapgpu {
 
 __global__ void k_extract_coupling(const double* __restrict__ a, int n, int k, const int* __restrict__ offs,
-                                   double* __restrict__ bblk, double* __restrict__ cblk) {
+                                   double* __restrict__ bblk, double* __restrict__ cblk,
+                                   const int* __restrict__ wid) {
     const int t = blockIdx.y;
     const int w = k;
+    const int wt = wid ? wid[t] : k;  // third stage: the reference's width, embedded (third.cu)
     const int e = offs[t + 1];
     const long long ld = 2LL * k;
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < w * w; idx += gridDim.x * blockDim.x) {
@@ -29,16 +31,17 @@ __global__ void k_extract_coupling(const double* __restrict__ a, int n, int k, c
         const int bi = e - w + r, bj = e + j, ci = e + r, cj = e - w + j;
         const bool bin = bi >= 0 && bi < n && bj >= 0 && bj < n && bi - bj <= k && bj - bi <= k;
         const bool cin = ci >= 0 && ci < n && cj >= 0 && cj < n && ci - cj <= k && cj - ci <= k;
-        bblk[(long long)t * w * w + idx] = bin ? a[(long long)bj * ld + bi + k] : 0.0;
-        cblk[(long long)t * w * w + idx] = cin ? a[(long long)cj * ld + ci + k] : 0.0;
+        const bool bw = r >= w - wt && j < wt, cw = r < wt && j >= w - wt;
+        bblk[(long long)t * w * w + idx] = bin && bw ? a[(long long)bj * ld + bi + k] : 0.0;
+        cblk[(long long)t * w * w + idx] = cin && cw ? a[(long long)cj * ld + ci + k] : 0.0;
     }
 }
 
 void launch_extract_coupling(const double* band, int n, int k, const int* d_offsets, int p, double* bblk,
-                             double* cblk, cudaStream_t s) {
+                             double* cblk, cudaStream_t s, const int* d_wid) {
     if (p < 2 || k == 0) return;
     dim3 grid(ceil_div((long long)k * k, 256), p - 1);
-    k_extract_coupling<<<grid, 256, 0, s>>>(band, n, k, d_offsets, bblk, cblk);
+    k_extract_coupling<<<grid, 256, 0, s>>>(band, n, k, d_offsets, bblk, cblk, d_wid);
     SAP_LAUNCHED();
 }
 

@@ -191,6 +191,7 @@ class Solver:
         if int(band.numel() if _is_cuda_tensor(band) else band.size) != n * (2 * k + 1):
             raise ValueError("setup: band must hold n*(2k+1) entries")
         ptr, dev = self._ptr(band)
+        self._arm_third_stage(n, k)
         _check(L.load().sap_setup_banded(self._h, n, k, ptr, dev))
         self.n, self.k = n, k
         if self.options.precond in (PrecondKind.coupled, PrecondKind.decoupled):
@@ -202,11 +203,55 @@ class Solver:
         ci = np.ascontiguousarray(col_idx, dtype=np.int32)
         v = np.ascontiguousarray(values, dtype=np.float64)
         n = len(rp) - 1
+        self._arm_third_stage(n, k)
         _check(L.load().sap_setup_banded_from_csr(self._h, n, k, len(ci), rp.ctypes.data, ci.ctypes.data,
                                                   v.ctypes.data, 0))
         self.n, self.k = n, k
         if self.options.precond in (PrecondKind.coupled, PrecondKind.decoupled):
             self.layout = make_partition_layout(n, self.p, k)
+
+    def set_third_stage(self, block_k, block_perms=None) -> None:
+        """Arm the third stage (PipelineConfig::third_stage, pipeline.hpp:312-319) with
+        sap::third_stage's result (ThirdStageResult, reorder_cm.hpp:227-231): block_k[p] per-partition
+        half-bandwidths and block_perms[p] (an int array per block, or None / empty for identity).
+        Applies to every following setup; ``set_third_stage(None)`` disarms."""
+        if block_k is None:
+            self._ts = None
+            _check(L.load().sap_set_third_stage(self._h, 0, None, None, None, 0))
+            return
+        kb = np.ascontiguousarray(block_k, dtype=np.int32)
+        perms = list(block_perms) if block_perms is not None else [None] * len(kb)
+        if len(perms) != len(kb):
+            raise ValueError("set_third_stage: one permutation (or None) per block")
+        self._ts = (kb, perms)
+
+    def _arm_third_stage(self, n: int, k: int) -> None:
+        """Hand the armed third stage to the library; perm[n] is indexed by global row, so it is
+        expanded over the partition layout the coming setup uses."""
+        if not getattr(self, "_ts", None):
+            return
+        kb, perms = self._ts
+        has = np.array([0 if q is None or len(q) == 0 else 1 for q in perms], np.int32)
+        full = np.zeros(max(n, 1), np.int32)
+        if has.any():
+            lay = make_partition_layout(n, self.p, k)
+            if lay.p != len(kb):
+                raise ValueError("third stage: block count does not match the partition layout")
+            for b, (q, h) in enumerate(zip(perms, has)):
+                if h:
+                    full[lay.offsets[b]:lay.offsets[b] + lay.sizes[b]] = np.asarray(q, np.int32)
+        _check(L.load().sap_set_third_stage(self._h, len(kb), kb.ctypes.data, has.ctypes.data, full.ctypes.data, n))
+
+    def full_spike(self, t: int):
+        """(V_t, W_t) of the third stage (SpikeSet::v_full / w_full, spike.hpp:258-296): column-major
+        sizes[t] x w_t and sizes[t+1] x w_t, returned as (m, w) numpy arrays."""
+        kb = self._ts[0]
+        w = int(max(kb[t], kb[t + 1]))
+        mt, mn = self.layout.sizes[t], self.layout.sizes[t + 1]
+        v = np.zeros(mt * w)
+        wv = np.zeros(mn * w)
+        _check(L.load().sap_get_full_spike(self._h, t, v.ctypes.data, wv.ctypes.data))
+        return v.reshape(w, mt).T, wv.reshape(w, mn).T
 
     def set_operator_csr(self, row_ptr, col_idx, values) -> None:
         rp = np.ascontiguousarray(row_ptr, dtype=np.int32)
@@ -264,7 +309,8 @@ class Solver:
     def factor(self, part: int, which: int = 0):
         """(band, boosts, block_norm) of block `part`; which 0 = LU, 1 = UL."""
         m = self.layout.sizes[part]
-        out = np.zeros(m * (2 * self.k + 1))
+        ts = getattr(self, "_ts", None)
+        out = np.zeros(m * (2 * (int(ts[0][part]) if ts else self.k) + 1))
         b = C.c_int()
         nrm = C.c_double()
         _check(L.load().sap_get_factor(self._h, part, which, out.ctypes.data, C.byref(b), C.byref(nrm)))
@@ -277,7 +323,8 @@ class Solver:
                 np.array([q[2] for q in parts]))
 
     def spike(self, t: int) -> dict:
-        w = self.k
+        ts = getattr(self, "_ts", None)
+        w = int(max(ts[0][t], ts[0][t + 1])) if ts else self.k
         arrs = {q: np.zeros(w * w) for q in ("B", "C", "vb", "wt", "rbar")}
         rb = C.c_int()
         _check(L.load().sap_get_spike(self._h, t, arrs["B"].ctypes.data, arrs["C"].ctypes.data,

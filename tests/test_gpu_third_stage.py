@@ -1,0 +1,185 @@
+"""GPU parity of the third stage (per-block reordering; PipelineConfig::third_stage,
+proj/include/sap/pipeline.hpp:312-319) against the compiled reference (oracle/_ref):
+sap::third_stage (reorder_cm.hpp:233-274) supplies the block permutations and per-partition
+bandwidths, then factor_blocks with permutations (block_factors.hpp:138-206), compute_full_spikes
+(spike.hpp:258-296), apply_preconditioner and build_precond_op(third_active) + run_krylov.
+
+Tolerances as tests/test_gpu_parity.py (d >= 0.5): factors normwise <= 1e-13 with equal
+boost counts and bit-equal block norms; coupling corners bit-exact; tips, R, full spikes normwise
+<= 1e-12; M r relative <= 1e-12; solves converge with iterations within +-1 of the reference.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def nrel(a, b):
+    den = np.max(np.abs(b)) if np.size(b) else 0.0
+    return np.max(np.abs(a - b)) / (den if den > 0 else 1.0) if np.size(b) else 0.0
+
+
+def rel2(a, b):
+    den = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (den if den > 0 else 1.0)
+
+
+@pytest.fixture(scope="module")
+def ref(oracle):
+    if not oracle.has_ref():
+        pytest.skip("compiled reference absent")
+    return oracle
+
+
+def _perms(n, k, p, kb, hp, pm, oracle):
+    sizes, offsets = oracle.partition_layout(n, p, k)
+    return [pm[offsets[b]:offsets[b] + sizes[b]] if hp[b] else None for b in range(p)]
+
+
+def _check_setup(sap, ref, n, k, band, p, kb, hp, pm):
+    want = ref.ref_third_setup(n, k, band, p, kb, hp, pm)
+    s = sap.Solver(p=p, precond=sap.PrecondKind.coupled)
+    s.set_third_stage(kb, _perms(n, k, p, kb, hp, pm, ref))
+    s.setup(band, n, k)
+    for b in range(p):
+        lu, boosts, norm = s.factor(b)
+        assert lu.shape == want["lu"][b].shape
+        assert nrel(lu, want["lu"][b]) <= 1e-13, b
+        assert boosts == want["boosts"][b] and norm == want["norms"][b]
+    for t in range(p - 1):
+        g = s.spike(t)
+        w = want["widths"][t]
+        assert np.array_equal(g["B"].reshape(w, w), want["B"][t]) and np.array_equal(g["C"].reshape(w, w), want["C"][t])
+        for key in ("vb", "wt", "rbar"):
+            assert nrel(g[key].reshape(w, w), want[key][t]) <= 1e-12, (t, key)
+        assert g["rbar_boosts"] == want["rbar_boosts"][t]
+        v, wv = s.full_spike(t)
+        assert nrel(v, want["v_full"][t]) <= 1e-12 and nrel(wv, want["w_full"][t]) <= 1e-12, t
+    r = np.random.default_rng(5).uniform(-1, 1, n)
+    for kind in (0, 1):
+        s2 = sap.Solver(p=p, precond=kind)
+        s2.set_third_stage(kb, _perms(n, k, p, kb, hp, pm, ref))
+        s2.setup(band, n, k)
+        assert rel2(s2.apply_preconditioner(r), ref.ref_third_apply(n, k, band, p, kb, hp, pm, kind, r)) <= 1e-12
+        s2.close()
+    return s
+
+
+@pytest.mark.parametrize("n,kn,window,k,p,seed", [
+    (4000, 2, 8, 20, 4, 1),
+    (6000, 6, 24, 60, 3, 2),
+    (8003, 10, 40, 100, 5, 3),
+])
+def test_third_stage_reordered_blocks(sap, ref, n, kn, window, k, p, seed):
+    """Blocks whose band Cuthill-McKee shrinks: permutations adopted, K_b < k, w_t < k."""
+    band = ref.scrambled_banded(n, kn, window, k, 1.0, seed)
+    kb, hp, pm = ref.ref_third_stage(n, k, band, p, 0)
+    assert hp.all() and (kb < k).all()
+    s = _check_setup(sap, ref, n, k, band, p, kb, hp, pm)
+    rhs = np.random.default_rng(seed).uniform(-1, 1, n)
+    x, st = s.solve(rhs)
+    xr, so = ref.ref_third_solve_banded(n, k, band, rhs, p, kb, hp, pm, 0)
+    assert st.converged and so["converged"] and st.final_relative_residual <= 1e-10
+    assert abs(st.iterations - so["iterations"]) <= 1.0, (st.iterations, so["iterations"])
+    assert rel2(x, xr) <= 1e-8
+    s.close()
+
+
+def test_third_stage_truncated_bandwidths_without_permutations(sap, ref):
+    """Identity blocks at K_b < k: the block bands and the couplings are truncated (w_t = max(K_t, K_{t+1}),
+    spike.hpp:102); several 32-column groups and off-chunk tiles in the full-spike solve."""
+    n, k, p = 3000, 70, 4
+    band, _ = ref.random_banded(n, k, 1.0, 21)
+    kb = np.array([70, 50, 61, 40], np.int32)
+    hp = np.zeros(p, np.int32)
+    pm = np.tile(np.arange(n // p, dtype=np.int32), p)
+    _check_setup(sap, ref, n, k, band, p, kb, hp, pm).close()
+
+
+def test_third_stage_mixed_identity_and_permuted_blocks(sap, ref):
+    n, k, p = 4000, 40, 4
+    band = ref.scrambled_banded(n, 3, 12, k, 1.0, 7)
+    kb, hp, pm = ref.ref_third_stage(n, k, band, p, 0)
+    assert hp.all()
+    sizes, offsets = ref.partition_layout(n, p, k)
+    hp = hp.copy()
+    kb = kb.copy()
+    hp[1] = 0
+    kb[1] = k  # identity block 1 at the full bandwidth
+    pm = pm.copy()
+    pm[offsets[1]:offsets[2]] = np.arange(sizes[1])
+    _check_setup(sap, ref, n, k, band, p, kb, hp, pm).close()
+
+
+def test_third_stage_permutation_outside_bandwidth_is_invalid_argument(sap, ref):
+    n, k, p = 2000, 20, 2
+    band = ref.scrambled_banded(n, 2, 8, k, 1.0, 3)
+    kb, hp, pm = ref.ref_third_stage(n, k, band, p, 0)
+    kb = np.maximum(kb - 1, 0).astype(np.int32)
+    with pytest.raises(ref.OracleError, match="exceeds bandwidth"):
+        ref.ref_third_setup(n, k, band, p, kb, hp, pm)
+    s = sap.Solver(p=p, precond=sap.PrecondKind.coupled)
+    s.set_third_stage(kb, _perms(n, k, p, kb, hp, pm, ref))
+    with pytest.raises(ValueError, match="block permutation exceeds bandwidth"):
+        s.setup(band, n, k)
+    s.set_third_stage(None)  # disarmed: the plain setup works again
+    s.setup(band, n, k)
+    s.close()
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_third_stage_mixed_precision_solve(sap, ref, kind):
+    n, k, p = 6000, 60, 3
+    band = ref.scrambled_banded(n, 6, 24, k, 1.0, 2)
+    kb, hp, pm = ref.ref_third_stage(n, k, band, p, 0)
+    rhs = np.random.default_rng(9).uniform(-1, 1, n)
+    s = sap.Solver(p=p, precond=kind, krylov=sap.KrylovOptions(mixed_precision=True))
+    s.set_third_stage(kb, _perms(n, k, p, kb, hp, pm, ref))
+    s.setup(band, n, k)
+    x, st = s.solve(rhs)
+    _, so = ref.ref_third_solve_banded(n, k, band, rhs, p, kb, hp, pm, kind, mixed_precision=True)
+    assert st.converged and st.final_relative_residual <= 1e-10
+    assert so["converged"] and st.iterations <= so["iterations"] + 1.0, (st.iterations, so["iterations"])
+    s.close()
+
+
+def _natural_grid_csr(s_):
+    """2-D 5-point convection-diffusion on an s x s grid in natural order (half-bandwidth s)."""
+    n = s_ * s_
+    rows, cols, vals = [], [], []
+    for y in range(s_):
+        for x in range(s_):
+            i = y * s_ + x
+            for dy, dx, v in ((-1, 0, -1.3), (0, -1, -1.3), (0, 0, 4.3), (0, 1, -0.7), (1, 0, -0.7)):
+                yy, xx = y + dy, x + dx
+                if 0 <= yy < s_ and 0 <= xx < s_:
+                    rows.append(i); cols.append(yy * s_ + xx); vals.append(v)
+    rp = np.zeros(n + 1, np.int32)
+    np.add.at(rp, np.array(rows) + 1, 1)
+    return n, np.cumsum(rp).astype(np.int32), np.array(cols, np.int32), np.array(vals)
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_third_stage_sparse_pipeline_matches_solve_sparse(sap, ref, kind):
+    """solve_sparse with third_stage on (no DB / CM / drop-off): the reference runs sap::third_stage
+    itself; the device path gets the same ThirdStageResult and assembles the CSR matrix on the device."""
+    s_ = 40
+    n, rp, ci, v = _natural_grid_csr(s_)
+    k = s_
+    rhs = ref.csr_matvec(n, rp, ci, v, np.linspace(1.0, 2.0, n))
+    xr, so = ref.ref_solve_sparse(n, rp, ci, v, rhs, 4, kind, third_stage=True)
+    assert so["converged"]
+    dense = np.zeros(n * (2 * k + 1))
+    for i in range(n):
+        for q in range(rp[i], rp[i + 1]):
+            dense[ci[q] * (2 * k + 1) + (i - ci[q] + k)] = v[q]
+    kb, hp, pm = ref.ref_third_stage(n, k, dense, 4, 0)
+    s = sap.Solver(p=4, precond=kind)
+    s.set_third_stage(kb, _perms(n, k, 4, kb, hp, pm, ref))
+    s.setup_from_csr(rp, ci, v, k)
+    s.set_operator_csr(rp, ci, v)
+    x, st = s.solve(rhs)
+    assert st.converged and st.final_relative_residual <= 1e-10
+    assert abs(st.iterations - so["iterations"]) <= 1.0, (st.iterations, so["iterations"])
+    assert rel2(x, xr) <= 1e-8
+    s.close()
