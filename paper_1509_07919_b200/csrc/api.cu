@@ -580,15 +580,19 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
                     fv = std::min(fv, h->ts_has[t] ? h->ts_perm[L.offsets[t] + ov] : ov);
                     fw = std::min(fw, h->ts_has[t + 1] ? h->ts_perm[e + ow] : ow);
                 }
+                // V' lives in columns [0, w_t), W' in [k - w_t, k) (third.cu header)
+                const int w = h->widths[t];
                 fj.push_back(FullSpikeJob{h->lu.get() + h->fst.block(t) + k, h->vfull.get() + (size_t)L.offsets[t] * k,
-                                          L.sizes[t], fv, 2 * t});
+                                          L.sizes[t], fv, 2 * t, 0, w, h->ts_k[t], t});
                 fj.push_back(FullSpikeJob{h->lu.get() + h->fst.block(t + 1) + k, h->wfull.get() + (size_t)e * k,
-                                          L.sizes[t + 1], fw, 2 * t + 1});
+                                          L.sizes[t + 1], fw, 2 * t + 1, k - w, k, h->ts_k[t + 1], t + 1});
             }
             h->fsjobs.alloc(fj.size());
             SAP_CUDA(cudaMemcpyAsync(h->fsjobs.get(), fj.data(), sizeof(FullSpikeJob) * fj.size(),
                                      cudaMemcpyHostToDevice, s));
-            launch_full_spikes(h->fsjobs.get(), (int)fj.size(), k, h->nonfinite.get(), s);
+            const bool inv = h->lplan.tma && h->lplan.tr == 32 && !getenv("SAP_FULL_SPIKE_SUBST");
+            launch_full_spikes(h->fsjobs.get(), (int)fj.size(), k, h->nonfinite.get(), inv ? h->lplan.dinv : nullptr,
+                               h->lplan.nch_max, h->kappa.get(), kSubstKappa, s);
             launch_full_tips(h->vfull.get(), h->wfull.get(), k, h->d_offsets.get(), ni, h->d_gperm.get(),
                              h->d_wid.get(), h->vb.get(), h->wt.get(), s);
         } else {

@@ -63,10 +63,15 @@ struct FullSpikeJob {
     int m;
     int first_row;    // right-hand-side rows above it are zero
     int flag;         // nonfinite[flag] set on a non-finite spike entry
+    int col_lo, col_hi;  // columns outside [col_lo, col_hi) have zero right-hand sides (and stay zero)
+    int kb;              // the block's bandwidth K_b <= k: factor entries beyond it are zero
+    int blk;             // block index (its chunk inverses)
 };
 void launch_full_rhs(const double* bblk, const double* cblk, int k, const int* d_offsets, int ni,
                      const int* d_gperm, double* vfull, double* wfull, cudaStream_t s);
-void launch_full_spikes(const FullSpikeJob* d_jobs, int njobs, int k, int* nonfinite, cudaStream_t s);
+// dinv (nullable): the LU plan's 32-row chunk inverses, used when *kappa <= kappa_max; else substitution
+void launch_full_spikes(const FullSpikeJob* d_jobs, int njobs, int k, int* nonfinite, const double* dinv, int nch_max,
+                        const unsigned long long* kappa, double kappa_max, cudaStream_t s);
 size_t full_spike_smem(int k);
 void launch_full_tips(const double* vfull, const double* wfull, int k, const int* d_offsets, int ni,
                       const int* d_gperm, const int* d_wid, double* vb, double* wt, cudaStream_t s);

@@ -129,7 +129,13 @@ constexpr int kFS = 32;
 constexpr int kFSThreads = 256;
 
 __device__ __forceinline__ void fs_tile_load(const FullSpikeJob& J, long long ld, int k, int r0, int j0, bool fwd,
-                                             double (&pf)[4]) {
+                                             double (&pf)[4], const double* dinv_b = nullptr) {
+    if (dinv_b && j0 == r0) {  // diagonal tile: the chunk triangle's inverse (column-major, like the tiles)
+        const double* src = dinv_b + ((long long)(r0 / kFS) * 2 + (fwd ? 0 : 1)) * kFS * kFS;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) pf[q] = __ldg(src + threadIdx.x + kFSThreads * q);
+        return;
+    }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const int idx = threadIdx.x + kFSThreads * q;
@@ -145,11 +151,14 @@ __device__ __forceinline__ void fs_tile_store(double* Lt, const double (&pf)[4])
 }
 
 __global__ void __launch_bounds__(kFSThreads, 2)
-    k_full_spike_solve(const FullSpikeJob* __restrict__ jobs, int k, int* __restrict__ nonfinite) {
+    k_full_spike_solve(const FullSpikeJob* __restrict__ jobs, int k, int* __restrict__ nonfinite,
+                       const double* __restrict__ dinv, int nch_max, const unsigned long long* __restrict__ kappa,
+                       double kappa_max) {
     extern __shared__ __align__(16) double sm[];
     const FullSpikeJob J = jobs[blockIdx.y];
-    const int T = (k + kFS - 1) / kFS;  // off-chunk tiles per chunk
-    const int RB = T + 1;               // ring chunks
+    if (blockIdx.x * kFS >= J.col_hi || (blockIdx.x + 1) * kFS <= J.col_lo) return;  // all-zero columns
+    const int RB = (k + kFS - 1) / kFS + 1;  // ring chunks
+    const int T = (J.kb + kFS - 1) / kFS;    // off-chunk tiles per chunk: the block's own bandwidth
     double* Lt = sm;                    // [2][32 cols j][32 rows i]
     double* Xr = sm + 2 * kFS * kFS;    // [RB * 32 rows][32 columns]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -160,36 +169,48 @@ __global__ void __launch_bounds__(kFSThreads, 2)
     auto slot = [&](int row) { return ((row / kFS) % RB) * kFS + (row % kFS); };
     double pf[4];
     int bad = 0;
+    // the chunk triangles through their precomputed inverses (the sweeps' k_chunk_inverses, same 32-row
+    // chunks) unless they are ill-conditioned: then warp 0 substitutes (as the substitution sweeps)
+    const bool use_inv = dinv != nullptr && __longlong_as_double((long long)*kappa) <= kappa_max;
+    const double* dinv_b = use_inv ? dinv + (long long)J.blk * nch_max * 2 * kFS * kFS : nullptr;
     for (int pass = 0; pass < 2; ++pass) {
         const bool fwd = pass == 0;
         for (int i = threadIdx.x; i < RB * kFS * kFS; i += kFSThreads) Xr[i] = 0.0;
-        __syncthreads();
-        const int ch_first = fwd ? J.first_row / kFS : nch - 1;
-        for (int ch = ch_first; fwd ? ch < nch : ch >= 0; ch += fwd ? 1 : -1) {
-            const int r0 = ch * kFS;
-            double acc[4];
+        // tile t < T: off-chunk columns (forward: j0 = r0 - 32 (T - t), ascending; backward:
+        // j0 = r0 + 32 (t + 1)); tile T: the diagonal tile j0 = r0
+        auto tile_j0 = [&](int r0, int t) {
+            return t == T ? r0 : (fwd ? r0 - kFS * (T - t) : r0 + kFS * (t + 1));
+        };
+        auto first_tile = [&](int r0) {
+            int t = 0;
+            while (t < T && (fwd ? tile_j0(r0, t) + kFS <= 0 : tile_j0(r0, t) >= m)) ++t;
+            return t;
+        };
+        auto load_rhs = [&](int r0, double (&a)[4]) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int row = r0 + warp * 4 + q;
-                acc[q] = (row < m && colok) ? J.x[(long long)row * k + col] : 0.0;
+                a[q] = (row < m && colok) ? J.x[(long long)row * k + col] : 0.0;
             }
-            // tile t < T: off-chunk columns (forward: j0 = r0 - 32 (T - t), ascending; backward:
-            // j0 = r0 + 32 (t + 1)); tile T: the diagonal tile j0 = r0
-            auto tile_j0 = [&](int t) { return t == T ? r0 : (fwd ? r0 - kFS * (T - t) : r0 + kFS * (t + 1)); };
-            auto tile_live = [&](int t) {
-                const int j0 = tile_j0(t);
-                return t == T || (fwd ? j0 + kFS > 0 : j0 < m);
-            };
-            int t = 0;
-            while (!tile_live(t)) ++t;
-            fs_tile_load(J, ld, k, r0, tile_j0(t), fwd, pf);
+        };
+        const int ch_first = fwd ? J.first_row / kFS : nch - 1, step = fwd ? 1 : -1;
+        // the next chunk's first tile and right-hand sides are loaded while this chunk's triangle is
+        // solved (the loads overlap warp 0's substitution)
+        double accn[4];
+        load_rhs(ch_first * kFS, accn);
+        fs_tile_load(J, ld, k, ch_first * kFS, tile_j0(ch_first * kFS, first_tile(ch_first * kFS)), fwd, pf, dinv_b);
+        for (int ch = ch_first; fwd ? ch < nch : ch >= 0; ch += step) {
+            const int r0 = ch * kFS, chn = ch + step;
+            const bool has_next = fwd ? chn < nch : chn >= 0;
+            double acc[4] = {accn[0], accn[1], accn[2], accn[3]};
+            int t = first_tile(r0);
             fs_tile_store(Lt + (t & 1) * kFS * kFS, pf);
             __syncthreads();
             for (; t <= T; ++t) {
                 const double* L = Lt + (t & 1) * kFS * kFS;
                 if (t < T) {
-                    fs_tile_load(J, ld, k, r0, tile_j0(t + 1), fwd, pf);
-                    const int j0 = tile_j0(t);
+                    fs_tile_load(J, ld, k, r0, tile_j0(r0, t + 1), fwd, pf, dinv_b);
+                    const int j0 = tile_j0(r0, t);
                     const double* xr = Xr + slot(max(j0, 0)) * kFS + lane;
 #pragma unroll 8
                     for (int jj = 0; jj < kFS; ++jj) {
@@ -206,30 +227,60 @@ __global__ void __launch_bounds__(kFSThreads, 2)
                     double* xc = Xr + slot(r0) * kFS;
 #pragma unroll
                     for (int q = 0; q < 4; ++q) xc[(warp * 4 + q) * kFS + lane] = acc[q];
+                    if (has_next) {
+                        load_rhs(chn * kFS, accn);
+                        fs_tile_load(J, ld, k, chn * kFS, tile_j0(chn * kFS, first_tile(chn * kFS)), fwd, pf, dinv_b);
+                    }
                     __syncthreads();
-                    if (warp == 0) {
-                        double x[kFS];
+                    if (use_inv) {
+                        // x = T^{-1} acc: every warp, 4 rows each
+                        double y[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 8
+                        for (int jj = 0; jj < kFS; ++jj) {
+                            const double xv = xc[jj * kFS + lane];
+                            const double2 l01 = *reinterpret_cast<const double2*>(L + jj * kFS + warp * 4);
+                            const double2 l23 = *reinterpret_cast<const double2*>(L + jj * kFS + warp * 4 + 2);
+                            y[0] = fma(l01.x, xv, y[0]);
+                            y[1] = fma(l01.y, xv, y[1]);
+                            y[2] = fma(l23.x, xv, y[2]);
+                            y[3] = fma(l23.y, xv, y[3]);
+                        }
+                        __syncthreads();
 #pragma unroll
-                        for (int i = 0; i < kFS; ++i) x[i] = xc[i * kFS + lane];
-                        if (fwd) {
-#pragma unroll
-                            for (int j = 0; j < kFS - 1; ++j)
-#pragma unroll
-                                for (int i = j + 1; i < kFS; ++i) x[i] = fma(-L[j * kFS + i], x[j], x[i]);
-                        } else {
-#pragma unroll
-                            for (int j = kFS - 1; j >= 0; --j) {
-                                x[j] = r0 + j < m ? x[j] / L[j * kFS + j] : 0.0;
-#pragma unroll
-                                for (int i = 0; i < j; ++i) x[i] = fma(-L[j * kFS + i], x[j], x[i]);
+                        for (int q = 0; q < 4; ++q) {
+                            const int i = warp * 4 + q;
+                            xc[i * kFS + lane] = y[q];
+                            if (r0 + i < m && colok) {
+                                J.x[(long long)(r0 + i) * k + col] = y[q];
+                                if (!fwd && !isfinite(y[q])) bad = 1;
                             }
                         }
-#pragma unroll
+                    } else if (warp == 0) {
+                        // substitution in shared memory (lane = column): ill-conditioned triangles only
+                        if (fwd) {
+                            for (int j = 0; j < kFS - 1; ++j) {
+                                const double xj = xc[j * kFS + lane];
+                                for (int i = j + 1; i < kFS; ++i)
+                                    xc[i * kFS + lane] = fma(-L[j * kFS + i], xj, xc[i * kFS + lane]);
+                            }
+                        } else {
+                            // the 32 pivot reciprocals in parallel (lane i: row r0 + i), then
+                            // x / d = fma(fma(-q, d, x), 1/d, q), q = x / d rounded through 1/d
+                            const double rcl = r0 + lane < m ? 1.0 / L[lane * kFS + lane] : 0.0;
+                            for (int j = kFS - 1; j >= 0; --j) {
+                                const double rc = __shfl_sync(0xffffffffu, rcl, j), d = L[j * kFS + j];
+                                const double xv = xc[j * kFS + lane], q = xv * rc;
+                                const double xj = r0 + j < m ? fma(fma(-q, d, xv), rc, q) : 0.0;
+                                xc[j * kFS + lane] = xj;
+                                for (int i = 0; i < j; ++i)
+                                    xc[i * kFS + lane] = fma(-L[j * kFS + i], xj, xc[i * kFS + lane]);
+                            }
+                        }
                         for (int i = 0; i < kFS; ++i) {
-                            xc[i * kFS + lane] = x[i];
+                            const double xi = xc[i * kFS + lane];
                             if (r0 + i < m && colok) {
-                                J.x[(long long)(r0 + i) * k + col] = x[i];
-                                if (!fwd && !isfinite(x[i])) bad = 1;
+                                J.x[(long long)(r0 + i) * k + col] = xi;
+                                if (!fwd && !isfinite(xi)) bad = 1;
                             }
                         }
                     }
@@ -246,12 +297,14 @@ size_t full_spike_smem(int k) {
     return sizeof(double) * (2 * kFS * kFS + (size_t)(T + 1) * kFS * kFS);
 }
 
-void launch_full_spikes(const FullSpikeJob* d_jobs, int njobs, int k, int* nonfinite, cudaStream_t s) {
+void launch_full_spikes(const FullSpikeJob* d_jobs, int njobs, int k, int* nonfinite, const double* dinv, int nch_max,
+                        const unsigned long long* kappa, double kappa_max, cudaStream_t s) {
     if (njobs <= 0 || k == 0) return;
     const size_t bytes = full_spike_smem(k);
     if (bytes > 227 * 1024) throw InvalidArgument("third stage: half-bandwidth too large for the full-spike solve");
     SAP_CUDA(cudaFuncSetAttribute(k_full_spike_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    k_full_spike_solve<<<dim3(ceil_div(k, kFS), njobs), kFSThreads, bytes, s>>>(d_jobs, k, nonfinite);
+    k_full_spike_solve<<<dim3(ceil_div(k, kFS), njobs), kFSThreads, bytes, s>>>(d_jobs, k, nonfinite, dinv, nch_max,
+                                                                              kappa, kappa_max);
     SAP_LAUNCHED();
 }
 

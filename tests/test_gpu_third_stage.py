@@ -186,3 +186,15 @@ def test_third_stage_sparse_pipeline_matches_solve_sparse(sap, ref, kind):
     assert abs(st.iterations - so["iterations"]) <= 1.0, (st.iterations, so["iterations"])
     assert rel2(x, xr) <= 1e-8
     s.close()
+
+
+def test_third_stage_full_spikes_by_substitution(sap, ref, monkeypatch):
+    """The full-spike solve's substitution path (taken for ill-conditioned chunk triangles, forced here)
+    against the reference, like the chunk-inverse path above."""
+    monkeypatch.setenv("SAP_FULL_SPIKE_SUBST", "1")
+    n, k, p = 3000, 70, 4
+    band, _ = ref.random_banded(n, k, 1.0, 22)
+    kb = np.array([70, 44, 70, 33], np.int32)
+    hp = np.zeros(p, np.int32)
+    pm = np.tile(np.arange(n // p, dtype=np.int32), p)
+    _check_setup(sap, ref, n, k, band, p, kb, hp, pm).close()
