@@ -171,6 +171,14 @@ sap_status sap_setup_banded(sap_handle* h, int n, int k, const double* band, int
  * (pipeline.hpp:286-330); the Krylov operator stays the banded one until sap_set_operator_csr. */
 sap_status sap_setup_banded_from_csr(sap_handle* h, int n, int k, int nnz, const int* row_ptr, const int* col_idx,
                                      const double* values, int csr_on_device);
+/* drop_off (pipeline.hpp:59-99) + assemble_banded + setup, on the device (solve_sparse's
+ * pipeline.hpp:265-330 after the host reorderings): k_after = the smallest half-bandwidth whose
+ * dropped outside-band mass satisfies ||dropped||_F <= drop_tol ||A||_F (drop_tol = 0: half_bandwidth(A),
+ * nothing dropped), entries beyond it dropped, the band assembled at k_after and set up. The squared
+ * masses are summed in the reference's order, so k_after is the reference's. drop_tol outside [0, 1]
+ * -> SAP_ERR_INVALID_ARGUMENT ("drop_off: tolerance must lie in [0, 1]"). k_after may be NULL. */
+sap_status sap_setup_from_csr_drop(sap_handle* h, int n, int nnz, const int* row_ptr, const int* col_idx,
+                                   const double* values, double drop_tol, int csr_on_device, int* k_after);
 sap_status sap_set_operator_csr(sap_handle* h, int n, int nnz, const int* row_ptr, const int* col_idx,
                                 const double* values, int on_device);
 

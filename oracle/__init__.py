@@ -393,3 +393,13 @@ def scrambled_banded(n, kn, window, k, d, seed):
         assert abs(pi - pj) <= k
         band[pj * (2 * k + 1) + (pi - pj + k)] = v
     return band
+
+
+def ref_drop_off(n, row_ptr, col_idx, vals, tol):
+    """sap::drop_off (pipeline.hpp:59-99) through the compiled reference: (k_after, nnz kept)."""
+    R = ref()
+    R.sapref_drop_off.argtypes = [C.c_int, _ip, _ip, _dp, C.c_double, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    ka, nk = C.c_int(), C.c_int()
+    _ref_check(R.sapref_drop_off(n, np.ascontiguousarray(row_ptr, np.int32), np.ascontiguousarray(col_idx, np.int32),
+                                 np.ascontiguousarray(vals, np.float64), tol, C.byref(ka), C.byref(nk)))
+    return ka.value, nk.value

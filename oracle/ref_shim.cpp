@@ -296,6 +296,21 @@ int sapref_solve_sparse(int n, const int* row_ptr, const int* col_idx, const dou
     SAPREF_CATCH
 }
 
+// sap::drop_off (pipeline.hpp:59-99): the kept half-bandwidth and the kept entry count.
+int sapref_drop_off(int n, const int* row_ptr, const int* col_idx, const double* vals, double tol, int* k_after,
+                    int* nnz_after) {
+    SAPREF_TRY
+    sap::SparseMatrix m;
+    m.n = n;
+    m.row_ptr.assign(row_ptr, row_ptr + n + 1);
+    m.col_idx.assign(col_idx, col_idx + row_ptr[n]);
+    m.values.assign(vals, vals + row_ptr[n]);
+    const sap::DropResult r = sap::drop_off(m, tol);
+    *k_after = r.k_after;
+    *nnz_after = static_cast<int>(r.matrix.values.size());
+    SAPREF_CATCH
+}
+
 // sap::third_stage: block_k[p], has_perm[p], perm[n] (perm[offset(b) + r] = new position of block row r).
 int sapref_third_stage(int n, int k, const double* band, int p, unsigned seed, int* block_k, int* has_perm,
                        int* perm) {

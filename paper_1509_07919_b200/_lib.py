@@ -68,6 +68,7 @@ SIGNATURES = {
     "sap_get_report": (C.c_int, [_vp, C.POINTER(sap_report)]),
     "sap_get_factor": (C.c_int, [_vp, C.c_int, C.c_int, _vp, _ip, _dp]),
     "sap_get_spike": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, _vp, _vp, _ip]),
+    "sap_setup_from_csr_drop": (C.c_int, [_vp, C.c_int, C.c_int, _vp, _vp, _vp, C.c_double, C.c_int, _ip]),
     "sap_set_third_stage": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp, C.c_int]),
     "sap_get_full_spike": (C.c_int, [_vp, C.c_int, _vp, _vp]),
     "sap_rank_rows": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _ip, _ip]),

@@ -1188,6 +1188,44 @@ sap_status sap_setup_banded_dist(sap_handle* h, int n, int k, int row_lo, int ro
     });
 }
 
+namespace {
+// CSR (host or device) -> device pointers held by the handle
+void csr_to_device(sap_handle* h, int n, int nnz, const int*& rp, const int*& ci, const double*& v, int on_device) {
+    if (on_device) return;
+    const cudaStream_t s = h->stream;
+    h->asm_rp.alloc(n + 1);
+    h->asm_ci.alloc(std::max(nnz, 1));
+    h->asm_v.alloc(std::max(nnz, 1));
+    SAP_CUDA(cudaMemcpyAsync(h->asm_rp.get(), rp, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, s));
+    if (nnz > 0) {
+        SAP_CUDA(cudaMemcpyAsync(h->asm_ci.get(), ci, sizeof(int) * nnz, cudaMemcpyHostToDevice, s));
+        SAP_CUDA(cudaMemcpyAsync(h->asm_v.get(), v, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
+    }
+    rp = h->asm_rp.get();
+    ci = h->asm_ci.get();
+    v = h->asm_v.get();
+}
+
+// assemble_banded on the device; drop = true filters |i - j| > k (drop_off) instead of failing
+void assemble_and_setup(sap_handle* h, int n, int k, const int* rp, const int* ci, const double* v, bool drop) {
+    const cudaStream_t s = h->stream;
+    const size_t total = (size_t)n * (2 * (size_t)k + 1);
+    h->asm_band.alloc(std::max<size_t>(total, 1));
+    SAP_CUDA(cudaMemsetAsync(h->asm_band.get(), 0, sizeof(double) * total, s));
+    h->asm_bad.alloc(1);
+    SAP_CUDA(cudaMemsetAsync(h->asm_bad.get(), 0xff, sizeof(unsigned long long), s));
+    launch_assemble_band(rp, ci, v, n, k, h->asm_band.get(), drop ? nullptr : h->asm_bad.get(), s);
+    unsigned long long bad = 0;
+    SAP_CUDA(cudaMemcpyAsync(&bad, h->asm_bad.get(), sizeof(bad), cudaMemcpyDeviceToHost, s));
+    SAP_CUDA(cudaStreamSynchronize(s));
+    if (bad != ~0ULL)
+        throw InvalidArgument("assemble_banded: entry (" + std::to_string(bad / (unsigned long long)n) + ", " +
+                              std::to_string(bad % (unsigned long long)n) + ") outside half-bandwidth " +
+                              std::to_string(k));
+    setup_banded(h, n, k, h->asm_band.get(), 2);
+}
+}  // namespace
+
 sap_status sap_setup_banded_from_csr(sap_handle* h, int n, int k, int nnz, const int* row_ptr, const int* col_idx,
                                      const double* values, int csr_on_device) {
     return guard([&] {
@@ -1195,37 +1233,29 @@ sap_status sap_setup_banded_from_csr(sap_handle* h, int n, int k, int nnz, const
         require(!h->dist, "sap_setup_banded_from_csr: not available on a distributed handle");
         require(n >= 0 && k >= 0 && nnz >= 0, "BandedMatrix: negative dimension");
         SAP_CUDA(cudaSetDevice(h->opt.device));
-        const cudaStream_t s = h->stream;
         const int* rp = row_ptr;
         const int* ci = col_idx;
         const double* v = values;
-        if (!csr_on_device) {
-            h->asm_rp.alloc(n + 1);
-            h->asm_ci.alloc(std::max(nnz, 1));
-            h->asm_v.alloc(std::max(nnz, 1));
-            SAP_CUDA(cudaMemcpyAsync(h->asm_rp.get(), row_ptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, s));
-            if (nnz > 0) {
-                SAP_CUDA(cudaMemcpyAsync(h->asm_ci.get(), col_idx, sizeof(int) * nnz, cudaMemcpyHostToDevice, s));
-                SAP_CUDA(cudaMemcpyAsync(h->asm_v.get(), values, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
-            }
-            rp = h->asm_rp.get();
-            ci = h->asm_ci.get();
-            v = h->asm_v.get();
-        }
-        const size_t total = (size_t)n * (2 * (size_t)k + 1);
-        h->asm_band.alloc(std::max<size_t>(total, 1));
-        SAP_CUDA(cudaMemsetAsync(h->asm_band.get(), 0, sizeof(double) * total, s));
-        h->asm_bad.alloc(1);
-        SAP_CUDA(cudaMemsetAsync(h->asm_bad.get(), 0xff, sizeof(unsigned long long), s));
-        launch_assemble_band(rp, ci, v, n, k, h->asm_band.get(), h->asm_bad.get(), s);
-        unsigned long long bad = 0;
-        SAP_CUDA(cudaMemcpyAsync(&bad, h->asm_bad.get(), sizeof(bad), cudaMemcpyDeviceToHost, s));
-        SAP_CUDA(cudaStreamSynchronize(s));
-        if (bad != ~0ULL)
-            throw InvalidArgument("assemble_banded: entry (" + std::to_string(bad / (unsigned long long)n) + ", " +
-                                  std::to_string(bad % (unsigned long long)n) + ") outside half-bandwidth " +
-                                  std::to_string(k));
-        setup_banded(h, n, k, h->asm_band.get(), 2);
+        csr_to_device(h, n, nnz, rp, ci, v, csr_on_device);
+        assemble_and_setup(h, n, k, rp, ci, v, false);
+    });
+}
+
+sap_status sap_setup_from_csr_drop(sap_handle* h, int n, int nnz, const int* row_ptr, const int* col_idx,
+                                   const double* values, double drop_tol, int csr_on_device, int* k_after) {
+    return guard([&] {
+        require(h != nullptr, "null handle");
+        require(!h->dist, "sap_setup_from_csr_drop: not available on a distributed handle");
+        require(n >= 0 && nnz >= 0, "sap_setup_from_csr_drop: negative size");
+        if (!(drop_tol >= 0.0 && drop_tol <= 1.0)) throw InvalidArgument("drop_off: tolerance must lie in [0, 1]");
+        SAP_CUDA(cudaSetDevice(h->opt.device));
+        const int* rp = row_ptr;
+        const int* ci = col_idx;
+        const double* v = values;
+        csr_to_device(h, n, nnz, rp, ci, v, csr_on_device);
+        const int k = drop_off_k(rp, ci, v, n, nnz, drop_tol, h->stream);
+        if (k_after) *k_after = k;
+        assemble_and_setup(h, n, k, rp, ci, v, drop_tol > 0.0);
     });
 }
 

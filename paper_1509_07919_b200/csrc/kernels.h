@@ -128,8 +128,11 @@ void launch_band_spmv(const double* band, int n, int k, const double* x, double*
 void launch_band_spmv_rows(const double* band, int n, int k, int r0, int r1, const double* x, double* y, cudaStream_t s);
 // w x w row-major GEMV: mode 0: y = u - A v;  mode 1: y -= A v.
 void launch_gemv_w(const double* A, int w, const double* v, const double* u, double* y, int mode, cudaStream_t s);
+// bad == nullptr: entries outside k are dropped (drop_off's filter) instead of flagged
 void launch_assemble_band(const int* rp, const int* ci, const double* v, int n, int k, double* band,
                           unsigned long long* bad, cudaStream_t s);
+// drop_off's half-bandwidth (pipeline.hpp:59-99) of a CSR matrix on the device (synchronizes s).
+int drop_off_k(const int* rp, const int* ci, const double* v, int n, int nnz, double tol, cudaStream_t s);
 void launch_csr_spmv(const int* rp, const int* ci, const double* v, int n, const double* x, double* y,
                      const double* b, cudaStream_t s);
 

@@ -112,9 +112,9 @@ __global__ void k_assemble_band(const int* __restrict__ rp, const int* __restric
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
         for (int s = rp[i]; s < rp[i + 1]; ++s) {
             const int j = ci[s];
-            if (i - j > k || j - i > k)
-                atomicMin(bad, (unsigned long long)i * (unsigned long long)n + (unsigned long long)j);
-            else
+            if (i - j > k || j - i > k) {
+                if (bad) atomicMin(bad, (unsigned long long)i * (unsigned long long)n + (unsigned long long)j);
+            } else
                 band[(long long)j * w + (i - j + k)] = v[s];
         }
 }

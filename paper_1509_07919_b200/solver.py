@@ -210,6 +210,23 @@ class Solver:
         if self.options.precond in (PrecondKind.coupled, PrecondKind.decoupled):
             self.layout = make_partition_layout(n, self.p, k)
 
+    def setup_from_csr_drop(self, row_ptr, col_idx, values, drop_tol: float) -> int:
+        """drop_off (pipeline.hpp:59-99) + assemble_banded + setup on the device; returns k_after."""
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int32)
+        ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        n = len(rp) - 1
+        ka = C.c_int()
+        if getattr(self, "_ts", None):
+            raise ValueError("setup_from_csr_drop: arm the third stage after the bandwidth is known "
+                             "(use setup_from_csr with k_after)")
+        _check(L.load().sap_setup_from_csr_drop(self._h, n, len(ci), rp.ctypes.data, ci.ctypes.data, v.ctypes.data,
+                                                float(drop_tol), 0, C.byref(ka)))
+        self.n, self.k = n, ka.value
+        if self.options.precond in (PrecondKind.coupled, PrecondKind.decoupled):
+            self.layout = make_partition_layout(n, self.p, self.k)
+        return ka.value
+
     def set_third_stage(self, block_k, block_perms=None) -> None:
         """Arm the third stage (PipelineConfig::third_stage, pipeline.hpp:312-319) with
         sap::third_stage's result (ThirdStageResult, reorder_cm.hpp:227-231): block_k[p] per-partition
