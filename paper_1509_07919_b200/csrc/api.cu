@@ -129,6 +129,11 @@ struct sap_handle {
     DevBuf<double> vfull, wfull, norms_op, scratch_p;
     DevBuf<float> scratch_pf;
     DevBuf<FullSpikeJob> fsjobs;
+    // streamed band upload (host band): LU overlapped with the host->device copy
+    DevBuf<unsigned> d_ready;
+    DevBuf<double> d_minpiv;
+    DevBuf<int> d_sbad;
+    cudaEvent_t sev_norm = nullptr;
     // multi-GPU (sap_create_distributed): this rank owns global rows [row_lo, row_hi) = partitions
     // [pb, pe); the band slice holds global columns [c_lo, c_hi). Interface slots are ordered
     // [left cross?, local 0..p_loc-2, right cross?]; cross interfaces are solved on both ranks.
@@ -349,6 +354,26 @@ void apply_a(sap_handle* h, const double* in, double* out) {
 
 int op_n(const sap_handle* h) { return h->csr ? h->csr_n : h->n; }
 
+// cuStreamWriteValue32 (stream memory operation: the copy engine's stream writes the round counter
+// without an SM, so the factorization kernel polling it can never starve it)
+typedef CUresult (*WriteValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WriteValue32Fn write_value_fn() {
+    static WriteValue32Fn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<WriteValue32Fn>(p);
+        cudaGetLastError();
+    }
+    return fn;
+}
+
+constexpr int kUploadRounds = 24;
+
 void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device) {
     h->op_finite = false;
     require(n >= 0 && k >= 0, "BandedMatrix: negative dimension");
@@ -389,18 +414,23 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
     h->rep.partitions = p;
 
     const size_t total = (size_t)n * (2 * (size_t)k + 1);
+    // host band + block preconditioner on the default LU kernel: the upload streams in rounds while the
+    // LU / UL jobs factor the columns that have arrived (k_band_lu_res wait_cols)
+    const bool streamed = on_device == 0 && blocks && !h->ts && n > 0 && k >= 1 && L.p >= 1 &&
+                          band_lu_reads_source(k) && write_value_fn() != nullptr &&
+                          getenv("SAP_NO_STREAM_UPLOAD") == nullptr;
     SAP_CUDA(cudaEventRecord(h->ev[0], s));
     if (on_device == 2) {
         h->band.release();
         h->band_ptr = band;
     } else {
         h->band.alloc(total);
-        if (n > 0)
+        if (n > 0 && !streamed)
             SAP_CUDA(cudaMemcpyAsync(h->band.get(), band, sizeof(double) * total,
                                      on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
         h->band_ptr = h->band.get();
     }
-    SAP_CUDA(cudaEventRecord(h->ev[1], s));
+    if (!streamed) SAP_CUDA(cudaEventRecord(h->ev[1], s));
     h->scratch_in.alloc(std::max(n, 1));
     h->scratch_out.alloc(std::max(n, 1));
     h->dscal.alloc(4);
@@ -488,7 +518,7 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
                                h->d_kb.get(), h->fst, h->lu.get(), h->d_bad.get(), s);
         launch_block_norms(h->lu.get(), m_max, k, h->d_offsets.get(), p, &h->fst, h->norms.get(), s);
         h->scratch_p.alloc(n);
-    } else {
+    } else if (!streamed) {
         launch_block_norms(h->band_ptr, m_max, k, h->d_offsets.get(), p, nullptr, h->norms.get(), s,
                            h->op_nonfinite.get());
         if (from_src)
@@ -497,9 +527,93 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
             launch_copy_blocks(h->band_ptr, k, h->d_offsets.get(), p, h->fst, h->lu.get(),
                                want_ul ? h->ul.get() : nullptr, s);
     }
-    SAP_CUDA(cudaEventRecord(h->ev[8], s));
-    launch_band_lu(h->jobs.get(), njobs, k, h->opt.boost_eps, s);
-    SAP_CUDA(cudaEventRecord(h->ev[9], s));
+    if (streamed) {
+        // 1. every upload round and its counter write, enqueued on the side stream BEFORE the kernel that
+        //    polls the counter is launched (nothing the host does afterwards can hold the copies back);
+        //    round r brings `piece` more columns of every block from its top (LU) and, for SaP-C, its
+        //    bottom (UL)
+        const cudaStream_t cs = h->side;
+        const int ends = want_ul ? 2 : 1;
+        h->d_ready.alloc(1);
+        h->d_minpiv.alloc(njobs);
+        h->d_sbad.alloc(1);
+        if (!h->sev_norm) SAP_CUDA(cudaEventCreateWithFlags(&h->sev_norm, cudaEventDisableTiming));
+        SAP_CUDA(cudaEventRecord(h->sev[0], s));  // earlier work on s may still read the old band
+        SAP_CUDA(cudaStreamWaitEvent(cs, h->sev[0], 0));
+        SAP_CUDA(cudaMemsetAsync(h->d_ready.get(), 0, sizeof(unsigned), cs));
+        SAP_CUDA(cudaMemsetAsync(h->op_nonfinite.get(), 0, sizeof(int), cs));
+        std::vector<int> piece(p);
+        for (int b = 0; b < p; ++b) piece[b] = (L.sizes[b] + ends * kUploadRounds - 1) / (ends * kUploadRounds);
+        const size_t cb = w * sizeof(double);
+        bool uniform = true;  // equal blocks: one 2-D copy per round and end (block pitch), not one per block
+        for (int b = 1; b < p; ++b) uniform = uniform && L.sizes[b] == L.sizes[0];
+        for (int r = 0; r < kUploadRounds && uniform; ++r) {
+            const int m = L.sizes[0], pc = piece[0];
+            const size_t pitch = (size_t)m * cb;
+            const int t0 = std::min(m, r * pc), t1 = std::min(m, (r + 1) * pc);
+            if (t1 > t0)
+                SAP_CUDA(cudaMemcpy2DAsync(h->band.get() + (size_t)t0 * w, pitch, band + (size_t)t0 * w, pitch,
+                                           cb * (t1 - t0), p, cudaMemcpyHostToDevice, cs));
+            if (ends == 2) {
+                const int b1 = std::max(0, m - r * pc), b0 = std::max(0, m - (r + 1) * pc);
+                if (b1 > b0)
+                    SAP_CUDA(cudaMemcpy2DAsync(h->band.get() + (size_t)b0 * w, pitch, band + (size_t)b0 * w, pitch,
+                                               cb * (b1 - b0), p, cudaMemcpyHostToDevice, cs));
+            }
+            const CUresult wr = write_value_fn()(cs, (CUdeviceptr)h->d_ready.get(), (cuuint32_t)(r + 1), 0);
+            if (wr != CUDA_SUCCESS) throw CudaFailure("cuStreamWriteValue32 failed");
+        }
+        for (int r = 0; r < kUploadRounds && !uniform; ++r) {
+            for (int b = 0; b < p; ++b) {
+                const int m = L.sizes[b], off = L.offsets[b], pc = piece[b];
+                const int t0 = std::min(m, r * pc), t1 = std::min(m, (r + 1) * pc);
+                if (t1 > t0)
+                    SAP_CUDA(cudaMemcpyAsync(h->band.get() + (size_t)(off + t0) * w, band + (size_t)(off + t0) * w,
+                                             cb * (t1 - t0), cudaMemcpyHostToDevice, cs));
+                if (ends == 2) {
+                    const int b1 = std::max(0, m - r * pc), b0 = std::max(0, m - (r + 1) * pc);
+                    if (b1 > b0)
+                        SAP_CUDA(cudaMemcpyAsync(h->band.get() + (size_t)(off + b0) * w,
+                                                 band + (size_t)(off + b0) * w, cb * (b1 - b0),
+                                                 cudaMemcpyHostToDevice, cs));
+                }
+            }
+            const CUresult wr = write_value_fn()(cs, (CUdeviceptr)h->d_ready.get(), (cuuint32_t)(r + 1), 0);
+            if (wr != CUDA_SUCCESS) throw CudaFailure("cuStreamWriteValue32 failed");
+        }
+        SAP_CUDA(cudaEventRecord(h->ev[1], cs));
+        launch_block_norms(h->band_ptr, m_max, k, h->d_offsets.get(), p, nullptr, h->norms.get(), cs,
+                           h->op_nonfinite.get());
+        SAP_CUDA(cudaEventRecord(h->sev_norm, cs));
+        // 2. the LU / UL kernel in streamed mode (no boosting; min |pivot| per job)
+        std::vector<FactorJob> sj = jobs;
+        for (int j = 0; j < njobs; ++j) {
+            sj[j].ready = h->d_ready.get();
+            sj[j].piece = piece[j % p];
+            sj[j].ends = ends;
+            sj[j].minpiv = h->d_minpiv.get() + j;
+        }
+        DevBuf<FactorJob> sjobs;
+        sjobs.alloc(njobs);
+        SAP_CUDA(cudaMemcpyAsync(sjobs.get(), sj.data(), sizeof(FactorJob) * njobs, cudaMemcpyHostToDevice, s));
+        launch_zero_pad(k, h->d_offsets.get(), p, h->fst, h->lu.get(), want_ul ? h->ul.get() : nullptr, s);
+        SAP_CUDA(cudaEventRecord(h->ev[8], s));
+        launch_band_lu(sjobs.get(), njobs, k, h->opt.boost_eps, s, true);
+        SAP_CUDA(cudaEventRecord(h->ev[9], s));
+        // 3. once the norms exist: any pivot below the boost threshold means the reference would have
+        //    boosted -> refactor with boosting (rare; exact either way)
+        SAP_CUDA(cudaStreamWaitEvent(s, h->sev_norm, 0));
+        launch_stream_check(h->d_minpiv.get(), h->norms.get(), njobs, p, h->opt.boost_eps, h->d_sbad.get(), s);
+        int bad = 0;
+        SAP_CUDA(cudaMemcpyAsync(&bad, h->d_sbad.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+        SAP_CUDA(cudaStreamSynchronize(s));
+        if (bad & 2) throw CudaFailure("streamed band upload stalled");
+        if (bad & 1) launch_band_lu(h->jobs.get(), njobs, k, h->opt.boost_eps, s);
+    } else {
+        SAP_CUDA(cudaEventRecord(h->ev[8], s));
+        launch_band_lu(h->jobs.get(), njobs, k, h->opt.boost_eps, s);
+        SAP_CUDA(cudaEventRecord(h->ev[9], s));
+    }
     {
         SweepPlan<double>& lp = h->lplan;
         lp = SweepPlan<double>{};

@@ -55,6 +55,14 @@ struct FactorJob {
     const double* scale;  // boost scale (block infinity norm), device pointer
     int* boosts;      // device counter (written, not accumulated)
     const double* src = nullptr;  // unfactored block in the same strided view (nullptr: in place, base)
+    // streamed upload (k_band_lu_res only): the band arrives while the kernel runs. *ready counts the
+    // finished upload rounds; each brings `piece` more columns of this job's view from its own end
+    // (`ends` = 2: the other end too, for the UL job of the same block). No boosting in this mode:
+    // the kernel records min |pivot| in *minpiv and the caller checks it against the final scale.
+    const unsigned* ready = nullptr;
+    int piece = 0;
+    int ends = 1;
+    double* minpiv = nullptr;
 };
 
 // Per-block strided band store used for every factor buffer (LU, UL, reduced

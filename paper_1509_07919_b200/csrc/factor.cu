@@ -317,10 +317,11 @@ static void launch_lu_b(const FactorJob* jobs, int njobs, int max_k, double eps,
     SAP_LAUNCHED();
 }
 
-void launch_band_lu(const FactorJob* d_jobs, int njobs, int max_k, double boost_eps, cudaStream_t s) {
+void launch_band_lu(const FactorJob* d_jobs, int njobs, int max_k, double boost_eps, cudaStream_t s, bool streamed) {
     if (njobs <= 0) return;
     static const bool simple = getenv("SAP_LU_SIMPLE") != nullptr;
-    if (!simple && launch_band_lu_ws(d_jobs, njobs, max_k, boost_eps, s)) return;
+    if (!simple && launch_band_lu_ws(d_jobs, njobs, max_k, boost_eps, s, streamed)) return;
+    if (streamed) throw CudaFailure("streamed factorization needs k_band_lu_res");
     if (max_k >= 48 && max_k <= 360)
         launch_lu_b<32>(d_jobs, njobs, max_k, boost_eps, s);
     else if (max_k > 360 && max_k <= 820)
@@ -329,6 +330,37 @@ void launch_band_lu(const FactorJob* d_jobs, int njobs, int max_k, double boost_
         launch_lu_b<8>(d_jobs, njobs, max_k, boost_eps, s);
     else
         launch_lu_b<16>(d_jobs, njobs, max_k, boost_eps, s);
+}
+
+// ---------------------------------------------------------------------------
+// Streamed-upload check: job j (block j mod p) factored without boosting; the reference would have
+// boosted iff some |pivot| < boost_eps * ||A_b|| (block_factors.hpp:29). bad |= 1 then, |= 2 on a stalled
+// upload (minpiv < 0).
+__global__ void k_stream_check(const double* __restrict__ minpiv, const double* __restrict__ norms, int njobs, int p,
+                               double eps, int* __restrict__ bad) {
+    int f = 0;
+    for (int j = threadIdx.x; j < njobs; j += blockDim.x) {
+        const double sc = norms[j % p];
+        const double bv = eps * (sc > 0 ? sc : 1.0);
+        const double mp = minpiv[j];
+        if (mp < 0.0) f |= 2;
+        else if (mp < bv) f |= 1;
+    }
+    f = __reduce_or_sync(0xffffffffu, f);
+    __shared__ int sf[32];
+    if ((threadIdx.x & 31) == 0) sf[threadIdx.x >> 5] = f;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int g = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) g |= sf[w];
+        *bad = g;
+    }
+}
+
+void launch_stream_check(const double* minpiv, const double* norms, int njobs, int p, double eps, int* bad,
+                         cudaStream_t s) {
+    k_stream_check<<<1, 256, 0, s>>>(minpiv, norms, njobs, p, eps, bad);
+    SAP_LAUNCHED();
 }
 
 // ---------------------------------------------------------------------------

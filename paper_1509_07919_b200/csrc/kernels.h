@@ -22,11 +22,17 @@ void launch_block_norms(const double* band, int max_m, int k, const int* d_offse
 void launch_copy_blocks(const double* band, int k, const int* d_offsets, int p, const BandStore& st, double* lu,
                         double* ul, cudaStream_t s);
 // Blocked no-pivot LU with pivot boosting of every job (one CTA per job).
-void launch_band_lu(const FactorJob* d_jobs, int njobs, int max_k, double boost_eps, cudaStream_t s);
+// streamed: the jobs carry FactorJob::ready (k_band_lu_res<B, true>; only where band_lu_reads_source(max_k))
+void launch_band_lu(const FactorJob* d_jobs, int njobs, int max_k, double boost_eps, cudaStream_t s,
+                    bool streamed = false);
 // The warp-specialized look-ahead variant (lu.cu); false if the smem budget does not fit.
 bool band_lu_reads_source(int max_k);
 void launch_zero_pad(int k, const int* d_offsets, int p, const BandStore& st, double* lu, double* ul, cudaStream_t s);
-bool launch_band_lu_ws(const FactorJob* d_jobs, int njobs, int max_k, double boost_eps, cudaStream_t s);
+// streamed upload: *bad = 1 if some job's min |pivot| < boost_eps * ||A_b|| (refactor with boosting), 2 on a stall
+void launch_stream_check(const double* minpiv, const double* norms, int njobs, int p, double eps, int* bad,
+                         cudaStream_t s);
+bool launch_band_lu_ws(const FactorJob* d_jobs, int njobs, int max_k, double boost_eps, cudaStream_t s,
+                       bool streamed = false);
 // Row-sum infinity norms of ni dense row-major w x w blocks and a non-finite flag per block.
 void launch_dense_norms(const double* a, int w, int ni, double* norms, int* nonfinite, cudaStream_t s);
 

@@ -1265,21 +1265,51 @@ __device__ __noinline__ void res_bulk(const Lu& L, const double* __restrict__ P,
     }
 }
 
-template <int B>
+template <int B, bool STREAM>
 __global__ void __launch_bounds__(kLuThreads, 1)
     k_band_lu_res(const FactorJob* __restrict__ jobs, double eps, int pld, int uld) {
     extern __shared__ __align__(16) double smem[];
     __shared__ int s_boosts;
     __shared__ double s_rcp[2 * B];  // [0, B): 1/p, [B, 2B): p
     const FactorJob J = jobs[blockIdx.x];
-    const double scale = *J.scale;
-    Lu L{J.base, J.rs, J.cs, J.m, J.k, B, pld, uld, eps * (scale > 0 ? scale : 1.0), J.src ? J.src : J.base};
+    constexpr bool streamed = STREAM;  // J.ready != nullptr
+    const double scale = streamed ? 0.0 : *J.scale;  // streamed: the block norm is not known yet
+    Lu L{J.base, J.rs, J.cs, J.m, J.k, B, pld, uld, streamed ? 0.0 : eps * (scale > 0 ? scale : 1.0),
+         J.src ? J.src : J.base};
     const int psz = B * pld, usz = B * uld;
     const int tid = threadIdx.x, warp = tid >> 5;
     const int m = L.m, K = L.K;
+    __shared__ double s_minp;
+    __shared__ int s_timeout;
     for (int i = tid; i < 2 * (psz + usz); i += kLuThreads) smem[i] = 0.0;
-    if (tid == 0) s_boosts = 0;
+    if (tid == 0) {
+        s_boosts = 0;
+        s_minp = INFINITY;
+        s_timeout = 0;
+    }
+    // streamed upload: before a step reads the band, its columns [0, need) plus one margin column (no L1
+    // line of a read column reaches unarrived bytes) must have arrived
+    auto wait_cols = [&](int need) {
+        if constexpr (!STREAM) return;
+        if (tid == 0 && !s_timeout) {
+            const long long want = min(m, need + 1);
+            const long long t0 = clock64();
+            for (;;) {
+                unsigned r;
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(J.ready) : "memory");
+                const long long got = (long long)r * J.piece;
+                if (got >= want || got * J.ends >= m) break;
+                if (clock64() - t0 > (1LL << 36)) {  // ~35 s: the upload stalled; give up (reported)
+                    s_timeout = 1;
+                    break;
+                }
+                __nanosleep(256);
+            }
+        }
+        __syncthreads();
+    };
     __syncthreads();
+    wait_cols(3 * B + K);
     {
         const int nb = min(B, m), ph = min(nb + K, m), R = min(K, m - nb);
         res_fetch(L, smem, smem + 2 * psz, 0, nb, 0, ph, R, 0, kLuThreads);
@@ -1300,6 +1330,7 @@ __global__ void __launch_bounds__(kLuThreads, 1)
         double* A = smem + 2 * psz + cur * usz;
         double* Pn = smem + (cur ^ 1) * psz;
         double* An = smem + 2 * psz + (cur ^ 1) * usz;
+        wait_cols(jb + 3 * B + K);
         LU_TRACE(step, 0, tid == 0);
         // 1-2. blocked panel + U12: per 8-column sub-panel, the diagonal block (one thread) then the L rows,
         //      U rows and rank-8 updates (all threads); warps 8-15 prefetch step s+1's new band entries meanwhile
@@ -1323,6 +1354,13 @@ __global__ void __launch_bounds__(kLuThreads, 1)
             }
         }
         LU_TRACE(step, 3, tid == 0);
+        if (STREAM && warp == 0) {  // min |pivot| of this step (s_rcp[32 + c] holds pivot c)
+            const int lane = tid & 31;
+            double v = lane < nb ? fabs(s_rcp[32 + lane]) : INFINITY;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+            if (lane == 0) s_minp = fmin(s_minp, v);
+        }
         if (ja < m) prefetch_fresh(L, ja, R, nb);
         // 3. panel (L11\U11, L21) and U12 to global: a warp per column, lanes down the rows
         {
@@ -1352,6 +1390,7 @@ __global__ void __launch_bounds__(kLuThreads, 1)
         cur ^= 1;
     }
     if (tid == 0) *J.boosts = s_boosts;
+    if (STREAM && tid == 0) *J.minpiv = s_timeout ? -1.0 : s_minp;
 }
 
 // ---------------------------------------------------------------------------
@@ -1728,7 +1767,7 @@ void read_lu_trace(long long* out) {
     SAP_CUDA(cudaMemcpyFromSymbol(out, g_lu_trace, sizeof(long long) * kTraceSteps * kTraceSlots));
 }
 
-bool launch_band_lu_ws(const FactorJob* d_jobs, int njobs, int max_k, double eps, cudaStream_t s) {
+bool launch_band_lu_ws(const FactorJob* d_jobs, int njobs, int max_k, double eps, cudaStream_t s, bool streamed) {
     constexpr int B = 32;
     // panel rows (<= B + K) must fit one per panel-group thread
     if (max_k < 1 || B + max_k > kPgThreads) return false;
@@ -1795,8 +1834,15 @@ bool launch_band_lu_ws(const FactorJob* d_jobs, int njobs, int max_k, double eps
         const int uldr = pad_ld(max_k);
         const size_t rbytes = sizeof(double) * (size_t)(2 * B * pldr + 2 * B * uldr);
         if (rbytes <= 226 * 1024) {
-            SAP_CUDA(cudaFuncSetAttribute(k_band_lu_res<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rbytes));
-            k_band_lu_res<B><<<njobs, kLuThreads, rbytes, s>>>(d_jobs, eps, pldr, uldr);
+            if (streamed) {
+                SAP_CUDA(cudaFuncSetAttribute(k_band_lu_res<B, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)rbytes));
+                k_band_lu_res<B, true><<<njobs, kLuThreads, rbytes, s>>>(d_jobs, eps, pldr, uldr);
+            } else {
+                SAP_CUDA(cudaFuncSetAttribute(k_band_lu_res<B, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)rbytes));
+                k_band_lu_res<B, false><<<njobs, kLuThreads, rbytes, s>>>(d_jobs, eps, pldr, uldr);
+            }
             SAP_LAUNCHED();
             return true;
         }

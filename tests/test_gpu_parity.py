@@ -451,3 +451,48 @@ def test_sparse_pipeline_device_assembly_matches_solve_sparse(sap, oracle, kind)
     with pytest.raises(ValueError, match="outside half-bandwidth"):
         s.setup_from_csr(rp, ci, v, k - 1)
     s.close()
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_streamed_upload_matches_resident_band(sap, oracle, kind, monkeypatch):
+    """A host band streams in rounds while the LU / UL jobs factor the arrived columns (no boosting,
+    min |pivot| checked against the final norms): bitwise the factors of the resident-band setup."""
+    torch = pytest.importorskip("torch")
+    n, k, p = 12000, 120, 6
+    band, rhs = oracle.random_banded(n, k, 1.0, 31)
+    host = sap.Solver(p=p, precond=kind)
+    host.setup(band, n, k)
+    dev = sap.Solver(p=p, precond=kind)
+    dev.setup(torch.from_numpy(band).cuda(), n, k)
+    for b in range(p):
+        for which in ((0, 1) if kind == 0 else (0,)):
+            f1, b1, n1 = host.factor(b, which)
+            f2, b2, n2 = dev.factor(b, which)
+            assert np.array_equal(f1, f2) and b1 == b2 and n1 == n2
+    x1, s1 = host.solve(rhs)
+    x2, s2 = dev.solve(rhs)
+    assert np.array_equal(x1, x2.cpu().numpy() if hasattr(x2, "cpu") else x2) and s1.iterations == s2.iterations
+    host.close()
+    dev.close()
+
+
+def test_streamed_upload_refactors_when_the_reference_boosts(sap, oracle):
+    """Zero pivots (all-zero rows at the first / last row of blocks, the LU's and UL's first pivots): the
+    streamed factorization sees a pivot below boost_eps * ||A_b|| and the setup refactors with boosting,
+    giving the reference's boosted factors and counts."""
+    n, k, p = 4000, 40, 4
+    band, _ = oracle.random_banded(n, k, 1.0, 5)
+    w = 2 * k + 1
+    sizes, offs = oracle.partition_layout(n, p, k)
+    for i in (offs[1], offs[3], offs[1] - 1):  # all-zero rows at block edges: exact zero first / last pivots
+        for j in range(max(0, i - k), min(n, i + k + 1)):
+            band[j * w + (i - j + k)] = 0.0
+    want = oracle.factor_blocks(n, k, band, p, True)
+    s = sap.Solver(p=p, precond=sap.PrecondKind.coupled)
+    s.setup(band, n, k)
+    lu, boosts, norms = s.factors(0)
+    ul, bul, _ = s.factors(1)
+    assert np.array_equal(boosts, want["boosts"]) and np.array_equal(bul, want["boosts_ul"])
+    assert boosts.sum() > 0
+    assert nrel(lu, want["lu"]) <= 1e-13 and nrel(ul, want["ul"]) <= 1e-13
+    s.close()
