@@ -133,6 +133,7 @@ struct sap_handle {
     DevBuf<unsigned> d_ready;
     DevBuf<double> d_minpiv;
     DevBuf<int> d_sbad;
+    DevBuf<FactorJob> sjobs, gjobs;  // streamed jobs, gated refactor jobs
     cudaEvent_t sev_norm = nullptr;
     // multi-GPU (sap_create_distributed): this rank owns global rows [row_lo, row_hi) = partitions
     // [pb, pe); the band slice holds global columns [c_lo, c_hi). Interface slots are ordered
@@ -593,22 +594,22 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
             sj[j].ends = ends;
             sj[j].minpiv = h->d_minpiv.get() + j;
         }
-        DevBuf<FactorJob> sjobs;
-        sjobs.alloc(njobs);
-        SAP_CUDA(cudaMemcpyAsync(sjobs.get(), sj.data(), sizeof(FactorJob) * njobs, cudaMemcpyHostToDevice, s));
+        std::vector<FactorJob> gj = jobs;
+        for (int j = 0; j < njobs; ++j) gj[j].gate = h->d_sbad.get();
+        h->sjobs.alloc(njobs);
+        h->gjobs.alloc(njobs);
+        SAP_CUDA(cudaMemcpyAsync(h->sjobs.get(), sj.data(), sizeof(FactorJob) * njobs, cudaMemcpyHostToDevice, s));
+        SAP_CUDA(cudaMemcpyAsync(h->gjobs.get(), gj.data(), sizeof(FactorJob) * njobs, cudaMemcpyHostToDevice, s));
         launch_zero_pad(k, h->d_offsets.get(), p, h->fst, h->lu.get(), want_ul ? h->ul.get() : nullptr, s);
         SAP_CUDA(cudaEventRecord(h->ev[8], s));
-        launch_band_lu(sjobs.get(), njobs, k, h->opt.boost_eps, s, true);
+        launch_band_lu(h->sjobs.get(), njobs, k, h->opt.boost_eps, s, true);
         SAP_CUDA(cudaEventRecord(h->ev[9], s));
         // 3. once the norms exist: any pivot below the boost threshold means the reference would have
         //    boosted -> refactor with boosting (rare; exact either way)
         SAP_CUDA(cudaStreamWaitEvent(s, h->sev_norm, 0));
         launch_stream_check(h->d_minpiv.get(), h->norms.get(), njobs, p, h->opt.boost_eps, h->d_sbad.get(), s);
-        int bad = 0;
-        SAP_CUDA(cudaMemcpyAsync(&bad, h->d_sbad.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
-        SAP_CUDA(cudaStreamSynchronize(s));
-        if (bad & 2) throw CudaFailure("streamed band upload stalled");
-        if (bad & 1) launch_band_lu(h->jobs.get(), njobs, k, h->opt.boost_eps, s);
+        // the refactor with boosting is always launched; its CTAs exit at once unless the check asked for it
+        launch_band_lu(h->gjobs.get(), njobs, k, h->opt.boost_eps, s);
     } else {
         SAP_CUDA(cudaEventRecord(h->ev[8], s));
         launch_band_lu(h->jobs.get(), njobs, k, h->opt.boost_eps, s);
@@ -757,6 +758,11 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
         if (h->ts) h->scratch_pf.alloc(n);
     }
     SAP_CUDA(cudaStreamSynchronize(s));
+    if (streamed) {
+        int bad = 0;
+        SAP_CUDA(cudaMemcpy(&bad, h->d_sbad.get(), sizeof(int), cudaMemcpyDeviceToHost));
+        if (bad & 2) throw CudaFailure("streamed band upload stalled");
+    }
     if (h->ts) {
         int bad = 0;
         SAP_CUDA(cudaMemcpy(&bad, h->d_bad.get(), sizeof(int), cudaMemcpyDeviceToHost));

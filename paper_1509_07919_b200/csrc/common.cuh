@@ -63,6 +63,7 @@ struct FactorJob {
     int piece = 0;
     int ends = 1;
     double* minpiv = nullptr;
+    const int* gate = nullptr;  // k_band_lu_res<B, false>: run only if (*gate & 1) (the streamed refactor)
 };
 
 // Per-block strided band store used for every factor buffer (LU, UL, reduced

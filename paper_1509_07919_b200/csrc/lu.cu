@@ -1272,6 +1272,7 @@ __global__ void __launch_bounds__(kLuThreads, 1)
     __shared__ int s_boosts;
     __shared__ double s_rcp[2 * B];  // [0, B): 1/p, [B, 2B): p
     const FactorJob J = jobs[blockIdx.x];
+    if (!STREAM && J.gate && !(*J.gate & 1)) return;  // streamed setup: no pivot fell below the threshold
     constexpr bool streamed = STREAM;  // J.ready != nullptr
     const double scale = streamed ? 0.0 : *J.scale;  // streamed: the block norm is not known yet
     Lu L{J.base, J.rs, J.cs, J.m, J.k, B, pld, uld, streamed ? 0.0 : eps * (scale > 0 ? scale : 1.0),
