@@ -396,6 +396,9 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
     h->ts = h->ts_armed && blocks && n > 0;
     if (h->ts) {
         require((int)h->ts_k.size() == p, "third stage: block count does not match the partition layout");
+        bool any_perm = false;
+        for (int b = 0; b < p; ++b) any_perm = any_perm || h->ts_has[b];
+        require(!any_perm || (int)h->ts_perm.size() == n, "third stage: permutation length does not match n");
         for (int b = 0; b < p; ++b) {
             require(h->ts_k[b] >= 0 && h->ts_k[b] <= k,
                     "third stage: per-partition half-bandwidth outside [0, k]");
