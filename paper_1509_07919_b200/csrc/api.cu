@@ -435,6 +435,10 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
         h->band_ptr = h->band.get();
     }
     if (!streamed) SAP_CUDA(cudaEventRecord(h->ev[1], s));
+    // resident band on the same kernel: the LU starts at once in the no-boost mode while the block norms
+    // run beside it on the side stream (the check and gated refactor below keep it exact)
+    const bool early = !streamed && on_device != 0 && blocks && !h->ts && n > 0 && k >= 1 && L.p >= 1 &&
+                       band_lu_reads_source(k) && getenv("SAP_NO_EARLY_LU") == nullptr;
     h->scratch_in.alloc(std::max(n, 1));
     h->scratch_out.alloc(std::max(n, 1));
     h->dscal.alloc(4);
@@ -522,7 +526,7 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
                                h->d_kb.get(), h->fst, h->lu.get(), h->d_bad.get(), s);
         launch_block_norms(h->lu.get(), m_max, k, h->d_offsets.get(), p, &h->fst, h->norms.get(), s);
         h->scratch_p.alloc(n);
-    } else if (!streamed) {
+    } else if (!streamed && !early) {
         launch_block_norms(h->band_ptr, m_max, k, h->d_offsets.get(), p, nullptr, h->norms.get(), s,
                            h->op_nonfinite.get());
         if (from_src)
@@ -531,25 +535,27 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
             launch_copy_blocks(h->band_ptr, k, h->d_offsets.get(), p, h->fst, h->lu.get(),
                                want_ul ? h->ul.get() : nullptr, s);
     }
-    if (streamed) {
-        // 1. every upload round and its counter write, enqueued on the side stream BEFORE the kernel that
-        //    polls the counter is launched (nothing the host does afterwards can hold the copies back);
-        //    round r brings `piece` more columns of every block from its top (LU) and, for SaP-C, its
-        //    bottom (UL)
+    if (streamed || early) {
+        // 1. (streamed) every upload round and its counter write, enqueued on the side stream BEFORE the
+        //    kernel that polls the counter is launched (nothing the host does afterwards can hold the
+        //    copies back); round r brings `piece` more columns of every block from its top (LU) and, for
+        //    SaP-C, its bottom (UL). The counter is reset on s, ahead of the kernel in stream order (a
+        //    previous setup left it at its final value). (early) the counter says "all arrived".
         const cudaStream_t cs = h->side;
         const int ends = want_ul ? 2 : 1;
         h->d_ready.alloc(1);
         h->d_minpiv.alloc(njobs);
         h->d_sbad.alloc(1);
         if (!h->sev_norm) SAP_CUDA(cudaEventCreateWithFlags(&h->sev_norm, cudaEventDisableTiming));
+        SAP_CUDA(cudaMemsetAsync(h->d_ready.get(), early ? 0x7f : 0, sizeof(unsigned), s));
         SAP_CUDA(cudaEventRecord(h->sev[0], s));  // earlier work on s may still read the old band
         SAP_CUDA(cudaStreamWaitEvent(cs, h->sev[0], 0));
-        SAP_CUDA(cudaMemsetAsync(h->d_ready.get(), 0, sizeof(unsigned), cs));
         SAP_CUDA(cudaMemsetAsync(h->op_nonfinite.get(), 0, sizeof(int), cs));
         std::vector<int> piece(p);
-        for (int b = 0; b < p; ++b) piece[b] = (L.sizes[b] + ends * kUploadRounds - 1) / (ends * kUploadRounds);
+        for (int b = 0; b < p; ++b)
+            piece[b] = early ? 1 : (L.sizes[b] + ends * kUploadRounds - 1) / (ends * kUploadRounds);
         const size_t cb = w * sizeof(double);
-        bool uniform = true;  // equal blocks: one 2-D copy per round and end (block pitch), not one per block
+        bool uniform = streamed;  // equal blocks: one 2-D copy per round and end (block pitch), not one per block
         for (int b = 1; b < p; ++b) uniform = uniform && L.sizes[b] == L.sizes[0];
         for (int r = 0; r < kUploadRounds && uniform; ++r) {
             const int m = L.sizes[0], pc = piece[0];
@@ -567,7 +573,7 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
             const CUresult wr = write_value_fn()(cs, (CUdeviceptr)h->d_ready.get(), (cuuint32_t)(r + 1), 0);
             if (wr != CUDA_SUCCESS) throw CudaFailure("cuStreamWriteValue32 failed");
         }
-        for (int r = 0; r < kUploadRounds && !uniform; ++r) {
+        for (int r = 0; r < kUploadRounds && streamed && !uniform; ++r) {
             for (int b = 0; b < p; ++b) {
                 const int m = L.sizes[b], off = L.offsets[b], pc = piece[b];
                 const int t0 = std::min(m, r * pc), t1 = std::min(m, (r + 1) * pc);
@@ -585,7 +591,7 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
             const CUresult wr = write_value_fn()(cs, (CUdeviceptr)h->d_ready.get(), (cuuint32_t)(r + 1), 0);
             if (wr != CUDA_SUCCESS) throw CudaFailure("cuStreamWriteValue32 failed");
         }
-        SAP_CUDA(cudaEventRecord(h->ev[1], cs));
+        if (streamed) SAP_CUDA(cudaEventRecord(h->ev[1], cs));
         launch_block_norms(h->band_ptr, m_max, k, h->d_offsets.get(), p, nullptr, h->norms.get(), cs,
                            h->op_nonfinite.get());
         SAP_CUDA(cudaEventRecord(h->sev_norm, cs));
@@ -604,13 +610,15 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
         SAP_CUDA(cudaMemcpyAsync(h->sjobs.get(), sj.data(), sizeof(FactorJob) * njobs, cudaMemcpyHostToDevice, s));
         SAP_CUDA(cudaMemcpyAsync(h->gjobs.get(), gj.data(), sizeof(FactorJob) * njobs, cudaMemcpyHostToDevice, s));
         launch_zero_pad(k, h->d_offsets.get(), p, h->fst, h->lu.get(), want_ul ? h->ul.get() : nullptr, s);
+        SAP_CUDA(cudaMemsetAsync(h->d_minpiv.get(), 0, sizeof(double) * njobs, s));  // -1 = stalled upload
         SAP_CUDA(cudaEventRecord(h->ev[8], s));
         launch_band_lu(h->sjobs.get(), njobs, k, h->opt.boost_eps, s, true);
         SAP_CUDA(cudaEventRecord(h->ev[9], s));
         // 3. once the norms exist: any pivot below the boost threshold means the reference would have
         //    boosted -> refactor with boosting (rare; exact either way)
         SAP_CUDA(cudaStreamWaitEvent(s, h->sev_norm, 0));
-        launch_stream_check(h->d_minpiv.get(), h->norms.get(), njobs, p, h->opt.boost_eps, h->d_sbad.get(), s);
+        launch_stream_check(h->sjobs.get(), h->d_minpiv.get(), h->norms.get(), njobs, p, h->opt.boost_eps,
+                            h->d_sbad.get(), s);
         // the refactor with boosting is always launched; its CTAs exit at once unless the check asked for it
         launch_band_lu(h->gjobs.get(), njobs, k, h->opt.boost_eps, s);
     } else {
@@ -761,7 +769,7 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
         if (h->ts) h->scratch_pf.alloc(n);
     }
     SAP_CUDA(cudaStreamSynchronize(s));
-    if (streamed) {
+    if (streamed || early) {
         int bad = 0;
         SAP_CUDA(cudaMemcpy(&bad, h->d_sbad.get(), sizeof(int), cudaMemcpyDeviceToHost));
         if (bad & 2) throw CudaFailure("streamed band upload stalled");

@@ -333,33 +333,27 @@ void launch_band_lu(const FactorJob* d_jobs, int njobs, int max_k, double boost_
 }
 
 // ---------------------------------------------------------------------------
-// Streamed-upload check: job j (block j mod p) factored without boosting; the reference would have
-// boosted iff some |pivot| < boost_eps * ||A_b|| (block_factors.hpp:29). bad |= 1 then, |= 2 on a stalled
-// upload (minpiv < 0).
-__global__ void k_stream_check(const double* __restrict__ minpiv, const double* __restrict__ norms, int njobs, int p,
-                               double eps, int* __restrict__ bad) {
+// Streamed-upload check: job j (block j mod p) was factored without boosting; the reference would have
+// boosted iff some |pivot| < boost_eps * ||A_b|| (block_factors.hpp:29). One CTA per job reads the
+// pivots off U's diagonal; bad |= 1 then, |= 2 on a stalled upload (the kernel left minpiv[j] = -1).
+__global__ void k_stream_check(const FactorJob* __restrict__ jobs, const double* __restrict__ minpiv,
+                               const double* __restrict__ norms, int p, double eps, int* __restrict__ bad) {
+    const int j = blockIdx.x;
+    const FactorJob J = jobs[j];
+    const double sc = norms[j % p];
+    const double bv = eps * (sc > 0 ? sc : 1.0);
     int f = 0;
-    for (int j = threadIdx.x; j < njobs; j += blockDim.x) {
-        const double sc = norms[j % p];
-        const double bv = eps * (sc > 0 ? sc : 1.0);
-        const double mp = minpiv[j];
-        if (mp < 0.0) f |= 2;
-        else if (mp < bv) f |= 1;
-    }
-    f = __reduce_or_sync(0xffffffffu, f);
-    __shared__ int sf[32];
-    if ((threadIdx.x & 31) == 0) sf[threadIdx.x >> 5] = f;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int g = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) g |= sf[w];
-        *bad = g;
-    }
+    for (int i = threadIdx.x; i < J.m; i += blockDim.x)
+        if (fabs(J.base[(long long)i * (J.rs + J.cs)]) < bv) f = 1;
+    if (threadIdx.x == 0 && minpiv[j] < 0.0) f |= 2;
+    f = __syncthreads_or(f & 1) | (threadIdx.x == 0 ? (f & 2) : 0);
+    if (threadIdx.x == 0 && f) atomicOr(bad, f);
 }
 
-void launch_stream_check(const double* minpiv, const double* norms, int njobs, int p, double eps, int* bad,
-                         cudaStream_t s) {
-    k_stream_check<<<1, 256, 0, s>>>(minpiv, norms, njobs, p, eps, bad);
+void launch_stream_check(const FactorJob* d_jobs, const double* minpiv, const double* norms, int njobs, int p,
+                         double eps, int* bad, cudaStream_t s) {
+    SAP_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
+    k_stream_check<<<njobs, 256, 0, s>>>(d_jobs, minpiv, norms, p, eps, bad);
     SAP_LAUNCHED();
 }
 

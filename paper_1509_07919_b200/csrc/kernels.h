@@ -29,8 +29,8 @@ void launch_band_lu(const FactorJob* d_jobs, int njobs, int max_k, double boost_
 bool band_lu_reads_source(int max_k);
 void launch_zero_pad(int k, const int* d_offsets, int p, const BandStore& st, double* lu, double* ul, cudaStream_t s);
 // streamed upload: *bad = 1 if some job's min |pivot| < boost_eps * ||A_b|| (refactor with boosting), 2 on a stall
-void launch_stream_check(const double* minpiv, const double* norms, int njobs, int p, double eps, int* bad,
-                         cudaStream_t s);
+void launch_stream_check(const FactorJob* d_jobs, const double* minpiv, const double* norms, int njobs, int p,
+                         double eps, int* bad, cudaStream_t s);
 bool launch_band_lu_ws(const FactorJob* d_jobs, int njobs, int max_k, double boost_eps, cudaStream_t s,
                        bool streamed = false);
 // Row-sum infinity norms of ni dense row-major w x w blocks and a non-finite flag per block.

@@ -1290,16 +1290,25 @@ __global__ void __launch_bounds__(kLuThreads, 1)
     }
     // streamed upload: before a step reads the band, its columns [0, need) plus one margin column (no L1
     // line of a read column reaches unarrived bytes) must have arrived
+    // s_got: the last counter value seen (shared, changed only inside the polling branch, which ends in a
+    // barrier), so every thread takes the same branch and a satisfied step costs no load and no barrier
+    __shared__ unsigned s_got;
+    if (tid == 0) s_got = 0;
     auto wait_cols = [&](int need) {
         if constexpr (!STREAM) return;
-        if (tid == 0 && !s_timeout) {
-            const long long want = min(m, need + 1);
+        const long long want = min(m, need + 1);
+        const long long have = (long long)s_got * J.piece;
+        if (have >= want || have * J.ends >= m || s_timeout) return;
+        if (tid == 0) {
             const long long t0 = clock64();
             for (;;) {
                 unsigned r;
                 asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(J.ready) : "memory");
                 const long long got = (long long)r * J.piece;
-                if (got >= want || got * J.ends >= m) break;
+                if (got >= want || got * J.ends >= m) {
+                    s_got = r;
+                    break;
+                }
                 if (clock64() - t0 > (1LL << 36)) {  // ~35 s: the upload stalled; give up (reported)
                     s_timeout = 1;
                     break;
@@ -1355,13 +1364,6 @@ __global__ void __launch_bounds__(kLuThreads, 1)
             }
         }
         LU_TRACE(step, 3, tid == 0);
-        if (STREAM && warp == 0) {  // min |pivot| of this step (s_rcp[32 + c] holds pivot c)
-            const int lane = tid & 31;
-            double v = lane < nb ? fabs(s_rcp[32 + lane]) : INFINITY;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
-            if (lane == 0) s_minp = fmin(s_minp, v);
-        }
         if (ja < m) prefetch_fresh(L, ja, R, nb);
         // 3. panel (L11\U11, L21) and U12 to global: a warp per column, lanes down the rows
         {
@@ -1391,7 +1393,7 @@ __global__ void __launch_bounds__(kLuThreads, 1)
         cur ^= 1;
     }
     if (tid == 0) *J.boosts = s_boosts;
-    if (STREAM && tid == 0) *J.minpiv = s_timeout ? -1.0 : s_minp;
+    if (STREAM && tid == 0 && s_timeout) *J.minpiv = -1.0;  // min |pivot| is read off U's diagonal afterwards
 }
 
 // ---------------------------------------------------------------------------

@@ -496,3 +496,20 @@ def test_streamed_upload_refactors_when_the_reference_boosts(sap, oracle):
     assert boosts.sum() > 0
     assert nrel(lu, want["lu"]) <= 1e-13 and nrel(ul, want["ul"]) <= 1e-13
     s.close()
+
+
+@pytest.mark.parametrize("on_device", [False, True])
+def test_resetup_with_a_new_matrix_on_the_same_handle(sap, oracle, on_device):
+    """A second setup on the same handle (streamed upload for a host band, early-started LU for a device
+    band) must factor the NEW matrix: the upload counter and the norms are per setup."""
+    torch = pytest.importorskip("torch")
+    n, k, p = 8000, 64, 4
+    s = sap.Solver(p=p, precond=sap.PrecondKind.coupled)
+    for seed in (41, 42):
+        band, _ = oracle.random_banded(n, k, 1.0, seed)
+        s.setup(torch.from_numpy(band).cuda() if on_device else band, n, k)
+        want = oracle.factor_blocks(n, k, band, p, True)
+        lu, boosts, norms = s.factors(0)
+        assert np.array_equal(norms, want["norms"]) and np.array_equal(boosts, want["boosts"])
+        assert nrel(lu, want["lu"]) <= 1e-13
+    s.close()
