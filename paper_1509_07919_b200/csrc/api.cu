@@ -592,6 +592,9 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
             if (wr != CUDA_SUCCESS) throw CudaFailure("cuStreamWriteValue32 failed");
         }
         if (streamed) SAP_CUDA(cudaEventRecord(h->ev[1], cs));
+        // the stores' out-of-matrix slots (disjoint from everything the LU writes), beside the LU; the
+        // sweeps and chunk inverses that read them come after sev_norm / the side stream's later work
+        launch_zero_pad(k, h->d_offsets.get(), p, h->fst, h->lu.get(), want_ul ? h->ul.get() : nullptr, cs);
         launch_block_norms(h->band_ptr, m_max, k, h->d_offsets.get(), p, nullptr, h->norms.get(), cs,
                            h->op_nonfinite.get());
         SAP_CUDA(cudaEventRecord(h->sev_norm, cs));
@@ -609,7 +612,6 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
         h->gjobs.alloc(njobs);
         SAP_CUDA(cudaMemcpyAsync(h->sjobs.get(), sj.data(), sizeof(FactorJob) * njobs, cudaMemcpyHostToDevice, s));
         SAP_CUDA(cudaMemcpyAsync(h->gjobs.get(), gj.data(), sizeof(FactorJob) * njobs, cudaMemcpyHostToDevice, s));
-        launch_zero_pad(k, h->d_offsets.get(), p, h->fst, h->lu.get(), want_ul ? h->ul.get() : nullptr, s);
         SAP_CUDA(cudaMemsetAsync(h->d_minpiv.get(), 0, sizeof(double) * njobs, s));  // -1 = stalled upload
         SAP_CUDA(cudaEventRecord(h->ev[8], s));
         launch_band_lu(h->sjobs.get(), njobs, k, h->opt.boost_eps, s, true);

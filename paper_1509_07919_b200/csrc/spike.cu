@@ -387,11 +387,66 @@ __global__ void k_rbar(const double* __restrict__ wt, const double* __restrict__
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite + t, 1);
 }
 
+// The same product on DMMA (m8n8k4): 32 x 32 output tile per CTA, W and V staged 32 columns / rows at a
+// time, each warp two 8 x 8 tiles. The k-sum runs in groups of 4 inside the MMA (within the SURVEY §8c
+// tolerance of finish_reduced_blocks' ascending FMA order).
+constexpr int kRbLd = 36;
+__global__ void __launch_bounds__(256) k_rbar_mma(const double* __restrict__ wt, const double* __restrict__ vb, int w,
+                                                  double* __restrict__ rbar, long long rpstride, int rpad,
+                                                  int* __restrict__ nonfinite) {
+    __shared__ double As[32 * kRbLd];  // As[i][l] = W(i0 + i, l0 + l)
+    __shared__ double Bs[32 * kRbLd];  // Bs[l][j] = V(l0 + l, j0 + j)
+    const int t = blockIdx.z, i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
+    const int tm = warp >> 1, tn0 = (warp & 1) * 2;
+    const double* A = wt + (long long)t * w * w;
+    const double* Bm = vb + (long long)t * w * w;
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    for (int l0 = 0; l0 < w; l0 += 32) {
+        for (int idx = threadIdx.x; idx < 32 * 32; idx += 256) {
+            const int r = idx >> 5, c = idx & 31;
+            As[r * kRbLd + c] = (i0 + r < w && l0 + c < w) ? A[(long long)(i0 + r) * w + l0 + c] : 0.0;
+            Bs[r * kRbLd + c] = (l0 + r < w && j0 + c < w) ? Bm[(long long)(l0 + r) * w + j0 + c] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+            const int kk = ks * 4 + lc;
+            const double a = As[(tm * 8 + lr) * kRbLd + kk];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const double b = Bs[kk * kRbLd + (tn0 + q) * 8 + lr];
+                dmma_m8n8k4(acc[q][0], acc[q][1], a, b, acc[q][0], acc[q][1]);
+            }
+        }
+        __syncthreads();
+    }
+    int bad = 0;
+    const long long bw = 2LL * w - 1;
+    const int i = i0 + tm * 8 + lr;
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int j = j0 + (tn0 + q) * 8 + 2 * lc + e;
+            if (i < w && j < w) {
+                const double v = (i == j ? 1.0 : 0.0) - acc[q][e];
+                if (!isfinite(v)) bad = 1;
+                rbar[(long long)t * rpstride + rpad + (long long)j * bw + (i - j + w - 1)] = v;
+            }
+        }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite + t, 1);
+}
+
 void launch_rbar(const double* wt, const double* vb, int w, int ni, double* rbar, const BandStore& rst,
                  int* nonfinite, cudaStream_t s) {
     if (ni <= 0 || w == 0) return;
     dim3 grid(ceil_div(w, 32), ceil_div(w, 32), ni);
-    k_rbar<<<grid, 256, 0, s>>>(wt, vb, w, rbar, rst.pstride, rst.pad, nonfinite);
+    static const bool fma_path = getenv("SAP_RBAR_FMA") != nullptr;
+    if (fma_path)
+        k_rbar<<<grid, 256, 0, s>>>(wt, vb, w, rbar, rst.pstride, rst.pad, nonfinite);
+    else
+        k_rbar_mma<<<grid, 256, 0, s>>>(wt, vb, w, rbar, rst.pstride, rst.pad, nonfinite);
     SAP_LAUNCHED();
 }
 
