@@ -87,6 +87,10 @@ struct sap_handle {
     // SaP-C setup: the sweep chunk inverses run on `side` while extract/tips/rbar continue on `stream`
     cudaStream_t side = nullptr;
     cudaEvent_t sev[2] = {};
+    // setup runs on `prio` (highest priority, joined to the caller's stream at entry) so that the side
+    // stream's work (lowest priority: chunk inverses, norms, upload) fills the SMs the main chain leaves idle
+    cudaStream_t prio = nullptr;
+    cudaEvent_t pev = nullptr;
     // problem
     bool ready = false;
     int n = 0, k = 0;
@@ -375,7 +379,27 @@ WriteValue32Fn write_value_fn() {
 
 constexpr int kUploadRounds = 24;
 
+// Setup on the high-priority stream: it waits for the caller's stream at entry; setup_banded ends with a
+// synchronize, so nothing needs joining back.
+struct PrioScope {
+    sap_handle* h;
+    cudaStream_t user;
+    explicit PrioScope(sap_handle* hh) : h(hh), user(hh->stream) {
+        SAP_CUDA(cudaEventRecord(h->pev, user));
+        SAP_CUDA(cudaStreamWaitEvent(h->prio, h->pev, 0));
+        h->stream = h->prio;
+    }
+    ~PrioScope() {
+        if (h->stream == h->prio) {  // on an exception: the caller's stream must still see the setup's work
+            cudaEventRecord(h->pev, h->prio);
+            cudaStreamWaitEvent(user, h->pev, 0);
+        }
+        h->stream = user;
+    }
+};
+
 void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device) {
+    PrioScope prio_scope(h);
     h->op_finite = false;
     require(n >= 0 && k >= 0, "BandedMatrix: negative dimension");
     require(band != nullptr || n == 0, "sap_setup_banded: null band");
@@ -1239,7 +1263,11 @@ sap_status sap_create(const sap_options* opts, sap_handle** out) {
             SAP_CUDA(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
             h->stream = h->own_stream;
             for (auto& e : h->ev) SAP_CUDA(cudaEventCreate(&e));
-            SAP_CUDA(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+            int least = 0, greatest = 0;
+            SAP_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+            SAP_CUDA(cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, least));
+            SAP_CUDA(cudaStreamCreateWithPriority(&h->prio, cudaStreamNonBlocking, greatest));
+            SAP_CUDA(cudaEventCreateWithFlags(&h->pev, cudaEventDisableTiming));
             for (auto& e : h->sev) SAP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         } catch (...) {
             delete h;
@@ -1258,6 +1286,8 @@ void sap_destroy(sap_handle* h) {
     for (auto& e : h->sev)
         if (e) cudaEventDestroy(e);
     if (h->side) cudaStreamDestroy(h->side);
+    if (h->prio) cudaStreamDestroy(h->prio);
+    if (h->pev) cudaEventDestroy(h->pev);
     if (h->own_stream) cudaStreamDestroy(h->own_stream);
     delete h;
 }
