@@ -155,7 +155,8 @@ sap_status sap_synchronize(sap_handle* h);
 
 /* ---- setup ≙ build_precond_op<double|float> over make_partition_layout(n, opts.p, k).
  * Installs the band as the Krylov A operator too (the dense wiring of
- * proj/tests/acceptance.cpp:114-132). band_on_device: 0 = host pointer, copied;
+ * proj/tests/acceptance.cpp:114-132). band_on_device: 0 = host pointer, copied (for the block
+ * preconditioners the copy is streamed in rounds under the factorization; pinned memory overlaps best);
  * 1 = device pointer, copied; 2 = device pointer BORROWED for the A operator
  * (no copy; it must stay valid while the handle applies A, like the
  * reference's LinearOp capturing the BandedMatrix by reference). */
