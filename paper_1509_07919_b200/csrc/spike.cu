@@ -195,6 +195,13 @@ __device__ __forceinline__ void tip_phase(const TipCorner& F, double* __restrict
             acc[t][1] = ri < w ? X[ri * kTXld + c + 1] : 0.0;
         }
         // acc layout: D[m = lr][n = 2 lc + e] = X(r0 + tm*8 + lr, (tn0+t)*8 + 2lc + e)
+        // the diagonal block's loads are issued first: their latency hides behind the off-diagonal work
+        double dpre[kTB * kTB / 256];
+#pragma unroll
+        for (int u = 0; u < kTB * kTB / 256; ++u) {
+            const int idx = threadIdx.x + 256 * u, j = idx >> 5, i = idx & 31;
+            dpre[u] = (i < nr && j < nr) ? F.col(r0 + j)[r0 + i] : 0.0;
+        }
         // off-diagonal blocks: the next factor block loads into registers while this one multiplies
         double pre[kTB * kTB / 256];
         auto fetch = [&](int bj) {
@@ -238,7 +245,11 @@ __device__ __forceinline__ void tip_phase(const TipCorner& F, double* __restrict
                 X[ri * kTXld + c + 1] = acc[t][1];
             }
         }
-        tip_stage(F, S, r0, nr, r0, nr);
+#pragma unroll
+        for (int u = 0; u < kTB * kTB / 256; ++u) {  // tip_stage(F, S, r0, nr, r0, nr) from the registers
+            const int idx = threadIdx.x + 256 * u, j = idx >> 5, i = idx & 31;
+            S[i * kTSld + j] = dpre[u];
+        }
         __syncthreads();
         if (warp == 0) {
             // lane = column: substitution inside the diagonal block. 1/diag comes from one IEEE division per
