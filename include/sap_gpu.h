@@ -91,6 +91,11 @@ typedef struct sap_options {
     int mixed_precision;     /* FP32 preconditioner (build_precond_op<float>), default 0 */
     int caller_asserts_spd;  /* lets AUTOMATIC pick CG, default 0 */
     int device;              /* CUDA device ordinal, default 0 */
+    /* 32-row chunk triangles of the block solves (sweeps, third-stage full spikes): 0 = automatic (explicit
+     * chunk inverses unless their condition estimate exceeds 1e4, then substitution),
+     * 1 = always the inverse products, 2 = always substitution (the reference's band_lu_solve order).
+     * Not a reference option: it selects between two implementations of block_solve. Default 0. */
+    int triangle_solve;
 } sap_options;
 
 /* PipelineReport T_* stage timings (pipeline.hpp:37-52), in seconds,
@@ -162,8 +167,6 @@ sap_status sap_synchronize(sap_handle* h);
  * reference's LinearOp capturing the BandedMatrix by reference). */
 sap_status sap_setup_banded(sap_handle* h, int n, int k, const double* band, int band_on_device);
 
-/* ---- A operator override: CSR matrix (solve_sparse's apply_a, pipeline.hpp:336-338).
- * row_ptr[n+1], col_idx[nnz], values[nnz]; copied. */
 /* setup from a sparse matrix (pipeline.hpp:103-115 assemble_banded + build_precond_op): the CSR matrix
  * (already reordered / dropped by the host stage, every entry within half-bandwidth k) is assembled into
  * band storage ON THE DEVICE and set up like sap_setup_banded; entries outside the band are the
@@ -180,6 +183,11 @@ sap_status sap_setup_banded_from_csr(sap_handle* h, int n, int k, int nnz, const
  * -> SAP_ERR_INVALID_ARGUMENT ("drop_off: tolerance must lie in [0, 1]"). k_after may be NULL. */
 sap_status sap_setup_from_csr_drop(sap_handle* h, int n, int nnz, const int* row_ptr, const int* col_idx,
                                    const double* values, double drop_tol, int csr_on_device, int* k_after);
+/* ---- A operator override: CSR matrix (solve_sparse's apply_a, pipeline.hpp:336-338).
+ * row_ptr[n+1], col_idx[nnz], values[nnz]; copied. Which call wins: every setup (sap_setup_banded,
+ * sap_setup_banded_from_csr, sap_setup_from_csr_drop) resets the operator to the band it set up; a
+ * sap_set_operator_csr AFTER the setup makes the CSR matrix the operator until the next setup
+ * (solve_sparse's order: setup, then the solve over the unreduced CSR matrix). */
 sap_status sap_set_operator_csr(sap_handle* h, int n, int nnz, const int* row_ptr, const int* col_idx,
                                 const double* values, int on_device);
 

@@ -117,6 +117,7 @@ struct sap_handle {
     SweepPlan<float> lplan_f, rplan_f;
     // CSR operator
     bool csr = false;
+    bool diag_f32 = false;  // diagonal preconditioner built and applied in float (mixed_precision)
     int csr_n = 0;
     DevBuf<int> rp, ci;
     DevBuf<double> vals;
@@ -197,7 +198,7 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
 // handle's device factors. in/out are device pointers; they may alias.
 // Sweeps on ill-conditioned chunk triangles (max ||T|| ||T^-1|| over chunks above kSubstKappa: element
 // growth at low diagonal dominance) solve them by substitution (k_sweep_tma<SUBST>); well conditioned
-// factors keep the chunk-inverse product. SAP_SWEEP_TRI=subst/inverse forces the choice.
+// factors keep the chunk-inverse product. sap_options::triangle_solve (1 inverse, 2 substitution) forces it.
 constexpr double kSubstKappa = 1e4;
 void choose_triangle_solve(sap_handle* h) {
     int nf = 1;
@@ -208,16 +209,13 @@ void choose_triangle_solve(sap_handle* h) {
     if (h->kappa.get()) SAP_CUDA(cudaMemcpy(kb, h->kappa.get(), sizeof(kb), cudaMemcpyDeviceToHost));
     double kap[2];
     std::memcpy(kap, kb, sizeof(kap));
-    const char* force = getenv("SAP_SWEEP_TRI");
-    h->lplan.subst = force ? force[0] == 's' : kap[0] > kSubstKappa;
-    h->rplan.subst = force ? force[0] == 's' : kap[1] > kSubstKappa;
+    const int force = h->opt.triangle_solve;
+    h->lplan.subst = force ? force == 2 : kap[0] > kSubstKappa;
+    h->rplan.subst = force ? force == 2 : kap[1] > kSubstKappa;
     h->rep.chunk_condition = kap[0];
     h->rep.sweep_substitution = h->lplan.subst ? 1 : 0;
     h->lplan_f.subst = h->lplan.subst;
     h->rplan_f.subst = h->rplan.subst;
-    if (getenv("SAP_DEBUG_KAPPA"))
-        fprintf(stderr, "sap: chunk-triangle condition estimates LU %.3e reduced %.3e -> substitution %d %d\n", kap[0],
-                kap[1], (int)h->lplan.subst, (int)h->rplan.subst);
 }
 
 void apply_m_dist(sap_handle* h, const double* in, double* out);
@@ -311,7 +309,7 @@ void apply_m(sap_handle* h, const double* in, double* out) {
             if (out != in) SAP_CUDA(cudaMemcpyAsync(out, in, bytes, cudaMemcpyDeviceToDevice, s));
             return;
         case SAP_PRECOND_DIAGONAL:
-            launch_diag_apply(in, h->diag.get(), out, n, s);
+            launch_diag_apply(in, h->diag.get(), out, n, s, h->diag_f32);
             return;
         default:
             break;
@@ -445,8 +443,7 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
     // host band + block preconditioner on the default LU kernel: the upload streams in rounds while the
     // LU / UL jobs factor the columns that have arrived (k_band_lu_res wait_cols)
     const bool streamed = on_device == 0 && blocks && !h->ts && n > 0 && k >= 1 && L.p >= 1 &&
-                          band_lu_reads_source(k) && write_value_fn() != nullptr &&
-                          getenv("SAP_NO_STREAM_UPLOAD") == nullptr;
+                          band_lu_reads_source(k) && write_value_fn() != nullptr;
     SAP_CUDA(cudaEventRecord(h->ev[0], s));
     if (on_device == 2) {
         h->band.release();
@@ -462,7 +459,7 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
     // resident band on the same kernel: the LU starts at once in the no-boost mode while the block norms
     // run beside it on the side stream (the check and gated refactor below keep it exact)
     const bool early = !streamed && on_device != 0 && blocks && !h->ts && n > 0 && k >= 1 && L.p >= 1 &&
-                       band_lu_reads_source(k) && getenv("SAP_NO_EARLY_LU") == nullptr;
+                       band_lu_reads_source(k);
     h->scratch_in.alloc(std::max(n, 1));
     h->scratch_out.alloc(std::max(n, 1));
     h->dscal.alloc(4);
@@ -480,8 +477,10 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
         const int ho[2] = {0, n};
         SAP_CUDA(cudaMemcpyAsync(offs1.get(), ho, sizeof(ho), cudaMemcpyHostToDevice, s));
         h->diag.alloc(n);
-        launch_block_norms(h->band_ptr, n, k, offs1.get(), 1, nullptr, h->dscal.get(), s);
-        launch_boosted_diag(h->band_ptr, n, k, h->dscal.get(), h->opt.boost_eps, h->diag.get(), s);
+        h->diag_f32 = h->opt.mixed_precision != 0;  // build_precond_op<float> (pipeline.hpp:325-327)
+        launch_block_norms(h->band_ptr, n, k, offs1.get(), 1, nullptr, h->dscal.get(), s, nullptr, nullptr,
+                           h->diag_f32);
+        launch_boosted_diag(h->band_ptr, n, k, h->dscal.get(), h->opt.boost_eps, h->diag.get(), s, h->diag_f32);
         SAP_CUDA(cudaEventRecord(h->ev[2], s));
         SAP_CUDA(cudaStreamSynchronize(s));
         h->rep.t_dtransf = ev_ms(h->ev[0], h->ev[1]) * 1e-3;
@@ -742,9 +741,10 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
             h->fsjobs.alloc(fj.size());
             SAP_CUDA(cudaMemcpyAsync(h->fsjobs.get(), fj.data(), sizeof(FullSpikeJob) * fj.size(),
                                      cudaMemcpyHostToDevice, s));
-            const bool inv = h->lplan.tma && h->lplan.tr == 32 && !getenv("SAP_FULL_SPIKE_SUBST");
+            const bool inv = h->lplan.tma && h->lplan.tr == 32 && h->opt.triangle_solve != 2;
             launch_full_spikes(h->fsjobs.get(), (int)fj.size(), k, h->nonfinite.get(), inv ? h->lplan.dinv : nullptr,
-                               h->lplan.nch_max, h->kappa.get(), kSubstKappa, s);
+                               h->lplan.nch_max, h->kappa.get(), h->opt.triangle_solve == 1 ? HUGE_VAL : kSubstKappa,
+                               s);
             launch_full_tips(h->vfull.get(), h->wfull.get(), k, h->d_offsets.get(), ni, h->d_gperm.get(),
                              h->d_wid.get(), h->vb.get(), h->wt.get(), s);
         } else {
@@ -1191,6 +1191,7 @@ void sap_options_default(sap_options* o) {
     o->mixed_precision = 0;
     o->caller_asserts_spd = 0;
     o->device = 0;
+    o->triangle_solve = 0;
 }
 
 int sap_max_feasible_partitions(int n, int k) {
@@ -1311,6 +1312,7 @@ sap_status sap_setup_banded(sap_handle* h, int n, int k, const double* band, int
         require(h != nullptr, "null handle");
         require(!h->dist, "sap_setup_banded: use sap_setup_banded_dist on a distributed handle");
         SAP_CUDA(cudaSetDevice(h->opt.device));
+        h->csr = false;  // a dense setup's Krylov operator is its band (acceptance.cpp:114-132)
         setup_banded(h, n, k, band, band_on_device);
     });
 }
@@ -1399,6 +1401,7 @@ sap_status sap_setup_banded_from_csr(sap_handle* h, int n, int k, int nnz, const
         const int* rp = row_ptr;
         const int* ci = col_idx;
         const double* v = values;
+        h->csr = false;  // cleared by every setup; sap_set_operator_csr after it re-arms the CSR operator
         csr_to_device(h, n, nnz, rp, ci, v, csr_on_device);
         assemble_and_setup(h, n, k, rp, ci, v, false);
     });
@@ -1415,6 +1418,7 @@ sap_status sap_setup_from_csr_drop(sap_handle* h, int n, int nnz, const int* row
         const int* rp = row_ptr;
         const int* ci = col_idx;
         const double* v = values;
+        h->csr = false;
         csr_to_device(h, n, nnz, rp, ci, v, csr_on_device);
         const int k = drop_off_k(rp, ci, v, n, nnz, drop_tol, h->stream);
         if (k_after) *k_after = k;
@@ -1558,7 +1562,8 @@ sap_status sap_get_factor(sap_handle* h, int part, int which, double* out, int* 
         }
         require(part >= 0 && part < h->layout.p, "sap_get_factor: partition out of range");
         require(which == 0 || which == 1, "sap_get_factor: which must be 0 (LU) or 1 (UL)");
-        if (which == 1 && !h->coupled) throw InvalidArgument("block_solve: UL factors not available");
+        if (which == 1 && (!h->coupled || h->ul.get() == nullptr))
+            throw InvalidArgument("block_solve: UL factors not available");
         SAP_CUDA(cudaSetDevice(h->opt.device));
         const size_t w = 2 * (size_t)h->k + 1;
         const double* src = (which == 0 ? h->lu.get() : h->ul.get()) + h->fst.block(part);

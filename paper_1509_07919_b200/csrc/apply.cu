@@ -511,175 +511,6 @@ __global__ void __launch_bounds__(kSwThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
-// Register-streamed sweep (k_sweep_ldg, TR = 32, k <= 272). Same chunk
-// schedule as k_sweep_tma, but the slab never touches shared memory: each
-// warp loads its columns' 32-row segments (one coalesced 256-byte run per
-// column) straight from L2 into registers, one chunk ahead, while TMA only
-// prefetches future slabs into L2. A TMA->smem->register slab crosses the
-// SM's 128 B/clk L1/smem datapath twice; this crosses it once (measured: the
-// smem version is L1/smem-bandwidth bound at ~2K cycles per chunk).
-constexpr int kLdgQ = 16;  // max partA columns per warp (k <= 32 + 15*16)
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem));
-}
-
-template <class T>
-__global__ void __launch_bounds__(kSwThreads, 1)
-    k_sweep_ldg(const __grid_constant__ CUtensorMap map, const T* __restrict__ f0, long long pstride, int pad,
-                const T* __restrict__ dinv, int nch_max, const int* __restrict__ offs, int k, T* __restrict__ xbase,
-                int xw, int box_c, int nbox) {
-    constexpr int TR = 32, SD = 3, PF = 8;
-    extern __shared__ __align__(128) unsigned char smraw[];
-    T* dv = reinterpret_cast<T*>(smraw);  // SD x TR*TR
-    T* xs = dv + SD * TR * TR;            // xw
-    T* part = xs + xw;                    // kSwWarps x TR
-    const int b = blockIdx.x;
-    const int off = offs[b], m = offs[b + 1] - off;
-    T* x = xbase + off;
-    const T* f = f0 + (long long)b * pstride + pad;
-    const long long ld = 2LL * k;
-    const int xm = xw - 1;
-    const int nch = (m + TR - 1) / TR;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const T* dvb = dinv + (long long)b * nch_max * 2 * TR * TR;
-
-    for (int dir = 0; dir < 2; ++dir) {
-        const bool fwd = dir == 0;
-        for (int i = tid; i < xw; i += kSwThreads) xs[i] = T(0);
-        auto chunk_of = [&](int t) { return fwd ? t : nch - 1 - t; };
-        auto cbase_of = [&](int ch) { return fwd ? ch * TR - k : ch * TR + TR; };
-        // partA columns of this warp: fwd [0, k-TR), bwd [TR, k); partB: fwd [k-TR, k), bwd [0, min(TR,k))
-        const int a_lo = fwd ? 0 : TR, a_hi = fwd ? k - TR : k;
-        const int b_lo = fwd ? max(k - TR, 0) : 0, b_hi = fwd ? k : min(TR, k);
-        auto load_chunk = [&](int t, T (&va)[kLdgQ], T (&vb)[2]) {
-            const int ch = chunk_of(t);
-            const int i0 = ch * TR, cbase = cbase_of(ch);
-            const T* rowp = f + i0 + lane + k;
-#pragma unroll
-            for (int q = 0; q < kLdgQ; ++q) {
-                const int cc = a_lo + (warp - 1) + (kSwWarps - 1) * q;
-                const int c = cbase + cc;
-                va[q] = (warp > 0 && cc < a_hi && c >= 0 && c < m) ? __ldcg(rowp + (long long)c * ld) : T(0);
-            }
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                const int cc = b_lo + warp + kSwWarps * q;
-                const int c = cbase + cc;
-                vb[q] = (cc < b_hi && c >= 0 && c < m) ? __ldcg(rowp + (long long)c * ld) : T(0);
-            }
-        };
-        auto issue_dinv = [&](int t) {
-            if (t >= nch) return;
-            const T* src = dvb + ((long long)chunk_of(t) * 2 + (fwd ? 0 : 1)) * TR * TR;
-            T* dst = dv + (t % SD) * TR * TR;
-            for (int i = tid; i < TR * TR * (int)sizeof(T) / 16; i += kSwThreads) cp_async16(dst + i * (16 / sizeof(T)), src + i * (16 / sizeof(T)));
-        };
-        if (tid == 32)
-            for (int t = 0; t < PF && t < nch; ++t) {
-                const int ch = chunk_of(t);
-                for (int q = 0; q < nbox; ++q) tma_prefetch_3d(&map, ch * TR, cbase_of(ch) + q * box_c, b);
-            }
-        issue_dinv(0);
-        cp_async_commit();
-        T na[kLdgQ], nb2[2];
-        load_chunk(0, na, nb2);
-        T yprev = T(0);
-        int prev_rows = 0;
-        __syncthreads();
-        for (int t = 0; t <= nch; ++t) {
-            const int ch = chunk_of(t);
-            const int pch = fwd ? t - 1 : nch - t;
-            cp_async_wait<0>();
-            __syncthreads();  // A: dinv(t-1) landed, parts(t-1) and x(t-2) visible
-            issue_dinv(t + 1);
-            cp_async_commit();
-            if (tid == 32 && t + PF < nch) {
-                const int chp = chunk_of(t + PF);
-                for (int q = 0; q < nbox; ++q) tma_prefetch_3d(&map, chp * TR, cbase_of(chp) + q * box_c, b);
-            }
-            T ca[kLdgQ], cb2[2];
-#pragma unroll
-            for (int q = 0; q < kLdgQ; ++q) ca[q] = na[q];
-            cb2[0] = nb2[0];
-            cb2[1] = nb2[1];
-            if (t + 1 < nch) load_chunk(t + 1, na, nb2);
-            const int i0 = ch * TR, cbase = cbase_of(ch);
-            T sA = T(0);
-            if (warp == 0) {
-                if (t >= 1) {
-                    const int p0 = pch * TR;
-                    T tot = T(0);
-#pragma unroll
-                    for (int q = 0; q < kSwWarps; ++q) tot += part[q * TR + lane];
-                    const T z = yprev - tot;
-                    const T* D = dv + ((t - 1) % SD) * TR * TR;
-                    T a0 = T(0), a1 = T(0), a2 = T(0), a3 = T(0);
-#pragma unroll
-                    for (int jj = 0; jj < TR; jj += 4) {
-                        a0 = fma(D[jj * TR + lane], __shfl_sync(0xffffffffu, z, jj), a0);
-                        a1 = fma(D[(jj + 1) * TR + lane], __shfl_sync(0xffffffffu, z, jj + 1), a1);
-                        a2 = fma(D[(jj + 2) * TR + lane], __shfl_sync(0xffffffffu, z, jj + 2), a2);
-                        a3 = fma(D[(jj + 3) * TR + lane], __shfl_sync(0xffffffffu, z, jj + 3), a3);
-                    }
-                    const T xv = (a0 + a1) + (a2 + a3);
-                    if (lane < prev_rows) {
-                        xs[(p0 + lane) & xm] = xv;
-                        x[p0 + lane] = xv;
-                    }
-                }
-                if (t < nch) {
-                    const int in = i0 + lane;
-                    yprev = in < m ? x[in] : T(0);
-                    prev_rows = min(TR, m - i0);
-                }
-            } else if (t < nch) {
-                T s0 = T(0), s1 = T(0), s2 = T(0), s3 = T(0);
-#pragma unroll
-                for (int q = 0; q < kLdgQ; q += 4) {
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int cc = a_lo + (warp - 1) + (kSwWarps - 1) * (q + u);
-                        T l = ca[q + u];
-                        if (fwd ? (cc < TR && lane > cc) : (TR + cc - lane > k)) l = T(0);
-                        const T xv = xs[(cbase + cc) & xm];
-                        if (u == 0) s0 = fma(l, xv, s0);
-                        if (u == 1) s1 = fma(l, xv, s1);
-                        if (u == 2) s2 = fma(l, xv, s2);
-                        if (u == 3) s3 = fma(l, xv, s3);
-                    }
-                }
-                sA = (s0 + s1) + (s2 + s3);
-            }
-            __syncthreads();  // B: x(t-1) in xs
-            if (t < nch) {
-                T sB = T(0);
-#pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    const int cc = b_lo + warp + kSwWarps * q;
-                    T l = cb2[q];
-                    if (fwd ? (cc < TR && lane > cc) : (TR + cc - lane > k)) l = T(0);
-                    sB = fma(l, xs[(cbase + cc) & xm], sB);
-                }
-                part[warp * TR + lane] = sA + sB;
-            }
-        }
-        __syncthreads();
-    }
-}
-
-template <class T>
-static bool try_ldg(const SweepPlan<T>& pl, T* x, cudaStream_t s) {
-    if (!pl.tma || pl.tr != 32 || pl.k > 32 + (kSwWarps - 1) * kLdgQ || pl.k < 1) return false;
-    const size_t bytes = sizeof(T) * ((size_t)3 * 32 * 32 + pl.xw + kSwWarps * 32) + 128;
-    SAP_CUDA(cudaFuncSetAttribute(k_sweep_ldg<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    k_sweep_ldg<T><<<pl.p, kSwThreads, bytes, s>>>(pl.map, pl.f, pl.st.pstride, pl.st.pad, pl.dinv, pl.nch_max, pl.offs,
-                                                  pl.k, x, pl.xw, pl.box_c, pl.nbox);
-    SAP_LAUNCHED();
-    return true;
-}
-
-// ---------------------------------------------------------------------------
 // Fallback sweep (k == 0, or bands too wide for the TMA ring): cp.async slabs,
 // shuffle triangle solves. TR = 32.
 template <class T, int S>
@@ -904,13 +735,7 @@ static bool try_ldgsts(const SweepPlan<T>& pl, T* x, cudaStream_t s) {
 template <class T>
 void launch_block_solve(const SweepPlan<T>& pl, T* x, cudaStream_t s) {
     if (pl.p <= 0) return;
-    // register-streamed variant: opt-in (SAP_SWEEP_LDG=1); measured 2x slower than the TMA ring at K = 200
-    static const bool ldg = getenv("SAP_SWEEP_LDG") != nullptr;
-    if (ldg && try_ldg<T>(pl, x, s)) return;
-    // SAP_SWEEP_SUBST=1: the cp.async chunk ring with a substitution (shuffle) triangle solve instead of the
-    // precomputed chunk inverses (numerics study: substitution is backward stable under element growth)
-    static const bool subst = getenv("SAP_SWEEP_SUBST") != nullptr;
-    if (pl.tma && !subst) {
+    if (pl.tma) {
         if (pl.tr == 32)
             pl.stages == 3 ? run_tma<T, 32, 3>(pl, x, s) : run_tma<T, 32, 2>(pl, x, s);
         else
@@ -1007,30 +832,36 @@ template void launch_interfaces<float>(const float*, const int*, const SweepPlan
 
 // ---------------------------------------------------------------------------
 // Diagonal preconditioner (build_precond_op's `diagonal` branch, pipeline.hpp:151-161).
+// T = float: the band entries and the boost value rounded to float (banded_cast, pipeline.hpp:150-152); the
+// float diagonal is stored exactly in double.
+template <class T>
 __global__ void k_boosted_diag(const double* __restrict__ a, int n, int k, const double* __restrict__ scale,
                                double eps, double* __restrict__ diag) {
     const double sc = *scale;
-    const double bv = eps * (sc > 0 ? sc : 1.0);
+    const T bv = static_cast<T>(eps * (sc > 0 ? sc : 1.0));
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        double d = a[(long long)i * (2 * k + 1) + k];
-        if (fabs(d) < bv) d = d < 0.0 ? -bv : bv;
-        diag[i] = d;
+        T d = static_cast<T>(a[(long long)i * (2 * k + 1) + k]);
+        if (fabs(d) < bv) d = d < T(0) ? -bv : bv;
+        diag[i] = static_cast<double>(d);
     }
 }
 
 void launch_boosted_diag(const double* band, int n, int k, const double* scale, double boost_eps, double* diag,
-                         cudaStream_t s) {
-    k_boosted_diag<<<ceil_div(n, 256), 256, 0, s>>>(band, n, k, scale, boost_eps, diag);
+                         cudaStream_t s, bool f32) {
+    (f32 ? k_boosted_diag<float> : k_boosted_diag<double>)<<<ceil_div(n, 256), 256, 0, s>>>(band, n, k, scale,
+                                                                                            boost_eps, diag);
     SAP_LAUNCHED();
 }
 
+template <class T>
 __global__ void k_diag_apply(const double* __restrict__ in, const double* __restrict__ diag,
                              double* __restrict__ out, int n) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = in[i] / diag[i];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        out[i] = static_cast<double>(static_cast<T>(in[i]) / static_cast<T>(diag[i]));
 }
 
-void launch_diag_apply(const double* in, const double* diag, double* out, int n, cudaStream_t s) {
-    k_diag_apply<<<ceil_div(n, 256), 256, 0, s>>>(in, diag, out, n);
+void launch_diag_apply(const double* in, const double* diag, double* out, int n, cudaStream_t s, bool f32) {
+    (f32 ? k_diag_apply<float> : k_diag_apply<double>)<<<ceil_div(n, 256), 256, 0, s>>>(in, diag, out, n);
     SAP_LAUNCHED();
 }
 

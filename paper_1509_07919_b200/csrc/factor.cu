@@ -41,6 +41,9 @@ long long g_launch_count = 0;
 // order-independent: non-negative doubles compare like their bit patterns,
 // so atomicMax on the bits is exact; NaN rows are skipped like the
 // reference's `row > norm` test.
+// F32: the norm of the band cast to float (build_precond_op<float>'s banded_cast, pipeline.hpp:150; the
+// row sums stay double, banded_matrix.hpp:90).
+template <bool F32>
 __global__ void __launch_bounds__(256)
     k_block_norms(const double* __restrict__ a, int k, const int* __restrict__ offs, long long pstride, int pad,
                   unsigned long long* __restrict__ norms_bits, int* __restrict__ nonfinite, int p,
@@ -58,7 +61,7 @@ __global__ void __launch_bounds__(256)
     const double* col = base + (long long)clo * ld + r + k;
 #pragma unroll 8
     for (int c = clo; c <= chi; ++c, col += ld)
-        if (r < m && r - c <= k && c - r <= k) row += fabs(*col);
+        if (r < m && r - c <= k && c - r <= k) row += fabs(F32 ? (double)(float)*col : *col);
     if (nonfinite && r < m) {
         // finiteness of every stored entry of global row off + r (the Krylov solver may then take
         // b - A*0 = b exactly for the zero initial guess): the in-block entries through the row sum
@@ -76,10 +79,10 @@ __global__ void __launch_bounds__(256)
 }
 
 void launch_block_norms(const double* band, int max_m, int k, const int* d_offsets, int p, const BandStore* store,
-                        double* norms, cudaStream_t s, int* nonfinite, const int* d_nrows) {
+                        double* norms, cudaStream_t s, int* nonfinite, const int* d_nrows, bool f32) {
     SAP_CUDA(cudaMemsetAsync(norms, 0, sizeof(double) * p, s));
     dim3 grid(ceil_div(ceil_div(max_m, 32), 8), p);
-    k_block_norms<<<grid, 256, 0, s>>>(band, k, d_offsets, store ? store->pstride : 0, store ? store->pad : 0,
+    (f32 ? k_block_norms<true> : k_block_norms<false>)<<<grid, 256, 0, s>>>(band, k, d_offsets, store ? store->pstride : 0, store ? store->pad : 0,
                                         reinterpret_cast<unsigned long long*>(norms), store ? nullptr : nonfinite, p,
                                         d_nrows);
     SAP_LAUNCHED();
@@ -319,8 +322,7 @@ static void launch_lu_b(const FactorJob* jobs, int njobs, int max_k, double eps,
 
 void launch_band_lu(const FactorJob* d_jobs, int njobs, int max_k, double boost_eps, cudaStream_t s, bool streamed) {
     if (njobs <= 0) return;
-    static const bool simple = getenv("SAP_LU_SIMPLE") != nullptr;
-    if (!simple && launch_band_lu_ws(d_jobs, njobs, max_k, boost_eps, s, streamed)) return;
+    if (launch_band_lu_ws(d_jobs, njobs, max_k, boost_eps, s, streamed)) return;
     if (streamed) throw CudaFailure("streamed factorization needs k_band_lu_res");
     if (max_k >= 48 && max_k <= 360)
         launch_lu_b<32>(d_jobs, njobs, max_k, boost_eps, s);

@@ -17,7 +17,7 @@ namespace sapgpu {
 // d_nrows (optional): only rows r < d_nrows[b] of block b count (third-stage reduced blocks diag(R_t, I)).
 void launch_block_norms(const double* band, int max_m, int k, const int* d_offsets, int p, const BandStore* store,
                         double* norms, cudaStream_t s,
-                        int* nonfinite = nullptr, const int* d_nrows = nullptr);
+                        int* nonfinite = nullptr, const int* d_nrows = nullptr, bool f32 = false);
 // LU (and UL) BandStores = each diagonal block's band, entries outside the block zeroed.
 void launch_copy_blocks(const double* band, int k, const int* d_offsets, int p, const BandStore& st, double* lu,
                         double* ul, cudaStream_t s);
@@ -123,9 +123,11 @@ template <class T>
 void launch_interfaces(const T* g, const int* d_ioffs, const SweepPlan<T>& rplan, int ni, int k, const T* wt,
                        const T* vb, const T* bblk, const T* cblk, T* xt, T* xb, T* b2, bool skip_first_b,
                        bool skip_last_c, cudaStream_t s);
-void launch_diag_apply(const double* in, const double* diag, double* out, int n, cudaStream_t s);
+// f32: build_precond_op<float>'s diagonal (pipeline.hpp:151-161 at T = float): the diagonal and the boost
+// value rounded to float, the apply b / diag in float between casts (spike.hpp:304-351).
+void launch_diag_apply(const double* in, const double* diag, double* out, int n, cudaStream_t s, bool f32 = false);
 void launch_boosted_diag(const double* band, int n, int k, const double* scale, double boost_eps, double* diag,
-                         cudaStream_t s);
+                         cudaStream_t s, bool f32 = false);
 
 // ---- operators (spmv.cu) ----
 // y = A x on the band; if b != nullptr also y = b - A x.

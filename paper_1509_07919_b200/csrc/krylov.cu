@@ -17,8 +17,10 @@ constexpr int kMaxEll = 8;
 
 struct VecSet {
     double* p[2 * kMaxEll + 2];
-    double c[2 * kMaxEll + 2];
+    // k_final_update packs 3 coefficients per j = 1..ell-1 after c[0..2]: highest index 3 ell - 1
+    double c[3 * kMaxEll];
 };
+static_assert(3 * (kMaxEll - 1) + 2 < 3 * kMaxEll, "VecSet::c holds every polynomial-update coefficient");
 
 inline int vgrid(int n) { return std::max(1, std::min(ceil_div(n, 256), 148 * 8)); }
 

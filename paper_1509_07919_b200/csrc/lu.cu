@@ -1,31 +1,21 @@
-// Warp-specialized, look-ahead blocked band LU (the hot loop of factor_blocks).
+// Blocked band LU (the hot loop of factor_blocks) on FP64 tensor cores.
 //
 // Reference: band_lu_inplace / band_ul_inplace, proj/include/sap/block_factors.hpp:22-71;
 // dense_lu_nopivot_boosted, proj/include/sap/spike.hpp:20-45 (same strided job
 // views as factor.cu: LU, UL on the flipped system, and the reduced blocks).
 //
-// Panel width B (<= 32, from the smem budget). Step s owns panel columns
-// [jb, jb+nb); A22 = the R x R trailing window at (jb+nb, jb+nb), R = min(K, m-jb-nb).
-// The CTA's 16 warps split into
-//   PG, warps 0-3  : factor panel s+1 (one named barrier per column) and form
-//                    U12(s+1) = L11^{-1} A12 (right-looking, reference order);
-//   UG, warps 4-15 : the bulk of step s's trailing update A22 -= L21 U12 on
-//                    FP64 tensor cores (mma.sync m8n8k4 -> DMMA.8x8x4), A22
-//                    streamed through L2, the top rows (U12(s+1)'s) first.
-// Look-ahead: before the split, all 16 warps apply step s's update to the
-// next panel's columns straight into the next panel's smem buffer, so panel
-// s+1's factorization overlaps step s's bulk update. Panel and U12 buffers are
-// double-buffered. Every element still receives its rank-1 updates in the
-// reference's column order (DMMA / DFMA contract mul+sub).
+// One CTA per factorization job, panel width B = 32. k_band_lu_res (K <= 224): panel and U12 resident
+// in shared memory, trailing update A22 -= L21 U12 on DMMA.8x8x4 (mma.sync m8n8k4) with A22 streamed
+// through L2. k_band_lu_seq: the same steps with the panel staged per step (K up to
+// the shared-memory budget). Every element receives its rank-1 updates in the reference's column order
+// (DMMA / DFMA contract mul+sub). Measured-slower variants (warp-specialized look-ahead,
+// extended-row update) are in the git history (commit 4e449e9), not in the product library.
 #include <cstdint>
 #include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
 
-#ifndef SAP_LA2_PG
-#define SAP_LA2_PG 128  // k_band_lu_la2 panel-group threads (tools: -DSAP_LA2_PG=256 for the 8+8 split)
-#endif
 
 namespace sapgpu {
 
@@ -33,10 +23,8 @@ namespace {
 
 constexpr int kLuThreads = 512;
 constexpr int kPgWarps = 8;
-constexpr int kUgWarps = 8;
 constexpr int kPgThreads = kPgWarps * 32;
 constexpr int kBarPg = 1;   // named barrier: panel group (256 threads)
-constexpr int kBarTop = 2;  // named barrier: UG top rows done -> PG (512 threads)
 
 __device__ __forceinline__ void named_sync(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -401,86 +389,6 @@ __device__ __noinline__ void pg_u12(const Lu& L, const double* __restrict__ Pn, 
     }
 }
 
-// ---------------------------------------------------------------------------
-// Look-ahead kernel pieces (k_band_lu_la). The trailing update of step s is
-// C <- C - Pext * A12 over the extended rows [panel rows ; A22 rows] with
-// Pext = [I - L11^{-1} ; L21 L11^{-1}] and A12 the raw (unsolved) block row:
-// the top rows come out as U12 = L11^{-1} A12, the rest as
-// A22 - L21 U12 -- the U12 triangular solve folds into the tensor-core pass.
-
-// Panel group: factor the staged panel (register rows), store it, then build
-// Pext in place. Xs/L11s: 32 x 33 smem scratch.
-template <int B>
-__device__ __noinline__ void pg_panel_pext(const Lu& L, double* __restrict__ Pn, double* __restrict__ prow,
-                                           double* __restrict__ Xs, double* __restrict__ L11s, int* boost_ctr,
-                                           int jp, int np, int ph, int ptid) {
-    const int pld = L.pld;
-    double row[B];
-#pragma unroll
-    for (int c = 0; c < B; ++c) row[c] = ptid < ph ? Pn[c * pld + ptid] : 0.0;
-    if (ptid == 0 && np > 0) pg_pub<B, 0>(row, pg_recip<B, 0>(L, row, boost_ctr), prow);
-    pg_col<B, 0>(L, row, prow, boost_ctr, np, ph, ptid);
-    // the factored row: global store (L and U entries), and L11 to smem
-    if (ptid < ph) {
-#pragma unroll
-        for (int c = 0; c < B; ++c)
-            if (c < np && L.inband(ptid, c)) __stcg(L.at(jp + ptid, jp + c), row[c]);
-    }
-    if (ptid < 32) {
-#pragma unroll
-        for (int c = 0; c < B; ++c) L11s[ptid * 33 + c] = (c < ptid && ptid < np) ? row[c] : 0.0;
-        for (int c = B; c < 32; ++c) L11s[ptid * 33 + c] = 0.0;
-    }
-    for (int idx = ptid; idx < 32 * 33; idx += kPgThreads) Xs[idx] = (idx / 33 == idx % 33) ? 1.0 : 0.0;
-    named_sync(kBarPg, kPgThreads);
-    // X = L11^{-1}: X[i][c] -= L(i,j) X[j][c] for i > j >= c, j ascending (forward substitution order)
-    for (int j = 0; j + 1 < np; ++j) {
-        const int ni = np - 1 - j, nc = j + 1;
-        for (int idx = ptid; idx < ni * nc; idx += kPgThreads) {
-            const int i = j + 1 + idx / nc, c = idx % nc;
-            Xs[i * 33 + c] = fma(-L11s[i * 33 + j], Xs[j * 33 + c], Xs[i * 33 + c]);
-        }
-        named_sync(kBarPg, kPgThreads);
-    }
-    // Pext row ptid
-    for (int r = ptid; r < pld; r += kPgThreads) {
-        if (r < np) {
-#pragma unroll
-            for (int c = 0; c < B; ++c) Pn[c * pld + r] = (c < r && c < np) ? -Xs[r * 33 + c] : 0.0;
-        } else if (r < ph) {
-            // M(r, c) = sum_{j = c}^{np-1} L21(r, j) X(j, c)   (r == ptid: row[] holds L21(r, .))
-#pragma unroll
-            for (int c = 0; c < B; ++c) {
-                double acc = 0.0;
-#pragma unroll
-                for (int j = c; j < B; ++j)
-                    if (j < np) acc = fma(row[j], Xs[j * 33 + c], acc);
-                Pn[c * pld + r] = c < np ? acc : 0.0;
-            }
-        } else {
-#pragma unroll
-            for (int c = 0; c < B; ++c) Pn[c * pld + r] = 0.0;
-        }
-    }
-    named_sync(kBarPg, kPgThreads);
-}
-
-// Panel group: raw A12 of panel (jp, np): rows [0, np) x cols [0, Rn) at (jp, jp+np).
-template <int B>
-__device__ __forceinline__ void pg_stage_a12(const Lu& L, double* __restrict__ An, int jp, int np, int Rn, int ptid) {
-    const int uld = L.uld;
-    for (int idx = ptid; idx < 32 * uld; idx += kPgThreads) {
-        const int r = idx & 31, c = idx >> 5;
-        if (r >= B) continue;
-        if (r < np && c < Rn && np + c - r <= L.K)
-            cp_async8(An + r * uld + c, L.at(jp + r, jp + np + c));
-        else
-            An[r * uld + c] = 0.0;
-    }
-    cp_async_wait_all();
-    named_sync(kBarPg, kPgThreads);
-}
-
 }  // namespace
 
 // Optional phase trace (build with -DSAP_LU_TRACE): CTA 0 records clock64 at
@@ -498,91 +406,6 @@ __device__ long long g_lu_wtrace[64];  // per-warp timestamps of one step (SAP_L
 #define LU_TRACE(step, slot, cond) do { } while (0)
 #endif
 
-template <int B>
-__global__ void __launch_bounds__(kLuThreads, 1)
-    k_band_lu_ws(const FactorJob* __restrict__ jobs, double eps, int pld, int uld) {
-    extern __shared__ __align__(16) double smem[];
-    __shared__ int s_boosts;
-    __shared__ __align__(16) double s_prow[2 * (B + 2)];
-    const FactorJob J = jobs[blockIdx.x];
-    const double scale = *J.scale;
-    Lu L{J.base, J.rs, J.cs, J.m, J.k, B, pld, uld, eps * (scale > 0 ? scale : 1.0), J.src ? J.src : J.base};
-    const int psz = B * pld, usz = B * uld;
-    const int tid = threadIdx.x, warp = tid >> 5;
-    const bool pg = warp < kPgWarps;
-    const int ptid = tid;  // valid for PG threads (0..127)
-    const int m = L.m, K = L.K;
-    if (tid == 0) s_boosts = 0;
-    __syncthreads();
-
-    // ---- prologue: panel 0 and U12(0) ----
-    {
-        const int nb = min(B, m), ph = min(nb + K, m), R = min(K, m - nb);
-        if (pg) {
-            pg_stage_panel(L, smem, 0, nb, ph, 0, 0, ptid);
-            named_sync(kBarPg, kPgThreads);
-            pg_factor_panel<B>(L, smem, s_prow, &s_boosts, nb, ph, ptid);
-            pg_store_panel(L, smem, 0, nb, ph, ptid);
-            pg_u12<B>(L, smem, smem + 2 * psz, 0, nb, R, ptid);
-        }
-    }
-    int cur = 0;
-    int step = 0;
-    for (int jb = 0; jb < m; jb += B, ++step) {
-        __syncthreads();  // S0: panel s and U12(s) complete (smem and global)
-        LU_TRACE(step, 0, tid == 0);
-        const int nb = min(B, m - jb);
-        const int ja = jb + nb;               // A22 origin
-        const int R = min(K, m - ja);         // A22 order
-        const bool has_next = ja < m;
-        const int nbn = has_next ? min(B, m - ja) : 0;
-        const int phn = has_next ? min(nbn + K, m - ja) : 0;
-        const int Rn = has_next ? min(K, m - ja - nbn) : 0;
-        const int ca = min(nbn, R);           // next-panel columns inside A22
-        const double* P = smem + cur * psz;
-        const double* U = smem + 2 * psz + cur * usz;
-        double* Pn = smem + (cur ^ 1) * psz;
-        double* Un = smem + 2 * psz + (cur ^ 1) * usz;
-        // ---- phase (a): all warps update the next panel's columns into Pn ----
-        if (has_next) dmma_region(L, P, U, nb, ja, 0, R, 0, ca, warp, kLuThreads / 32, Pn);
-        __syncthreads();  // S1
-        LU_TRACE(step, 1, tid == 0);
-        if (pg) {
-            if (has_next) {
-                pg_stage_panel(L, Pn, ja, nbn, phn, R, ca, ptid);
-                named_sync(kBarPg, kPgThreads);
-                LU_TRACE(step, 2, tid == 0);
-                pg_factor_panel<B>(L, Pn, s_prow, &s_boosts, nbn, phn, ptid);
-                LU_TRACE(step, 3, tid == 0);
-                pg_store_panel(L, Pn, ja, nbn, phn, ptid);
-                LU_TRACE(step, 4, tid == 0);
-                named_sync(kBarTop, kLuThreads);  // UG has written A22's top rows (U12(s+1) sources)
-                LU_TRACE(step, 5, tid == 0);
-                pg_u12<B>(L, Pn, Un, ja, nbn, Rn, ptid);
-                LU_TRACE(step, 6, tid == 0);
-            }
-        } else {
-            const int uw = warp - kPgWarps;
-            const int top = has_next ? min(R, ((nbn + 15) >> 4) << 4) : 0;
-            dmma_region(L, P, U, nb, ja, 0, top, ca, R, uw, kUgWarps, nullptr);
-            LU_TRACE(step, 7, tid == kPgThreads);
-            if (has_next) {
-                __threadfence_block();
-                named_arrive(kBarTop, kLuThreads);
-            }
-            dmma_region(L, P, U, nb, ja, top, R, ca, R, uw, kUgWarps, nullptr);
-            LU_TRACE(step, 8, tid == kPgThreads);
-            LU_TRACE(step, 9, tid == kLuThreads - 32);
-        }
-        cur ^= 1;
-    }
-    __syncthreads();
-    if (tid == 0) *J.boosts = s_boosts;
-}
-
-// All warps in every phase (no specialization): stage -> factor panel ->
-// U12 -> DMMA trailing update, one panel at a time. Panel rows are owned by
-// threads 0..kPgThreads-1; the DMMA update uses all 16 warps.
 template <int B>
 __global__ void __launch_bounds__(kLuThreads, 1)
     k_band_lu_seq(const FactorJob* __restrict__ jobs, double eps, int pld, int uld) {
@@ -620,136 +443,6 @@ __global__ void __launch_bounds__(kLuThreads, 1)
         __syncthreads();
         LU_TRACE(step, 1, tid == 0);
         dmma_region(L, P, U, nb, ja, 0, R, 0, R, warp, kLuThreads / 32, nullptr);
-        LU_TRACE(step, 8, tid == 0);
-        LU_TRACE(step, 9, tid == kLuThreads - 32);
-        __syncthreads();
-    }
-    if (tid == 0) *J.boosts = s_boosts;
-}
-
-template <int B>
-__global__ void __launch_bounds__(kLuThreads, 1)
-    k_band_lu_la(const FactorJob* __restrict__ jobs, double eps, int pld, int uld) {
-    extern __shared__ __align__(16) double smem[];
-    __shared__ int s_boosts;
-    __shared__ __align__(16) double s_prow[2 * (B + 2)];
-    __shared__ double s_X[32 * 33];
-    __shared__ double s_L11[32 * 33];
-    const FactorJob J = jobs[blockIdx.x];
-    const double scale = *J.scale;
-    Lu L{J.base, J.rs, J.cs, J.m, J.k, B, pld, uld, eps * (scale > 0 ? scale : 1.0), J.src ? J.src : J.base};
-    const int psz = B * pld, usz = B * uld;
-    const int tid = threadIdx.x, warp = tid >> 5;
-    const bool pg = warp < kPgWarps;
-    const int m = L.m, K = L.K;
-    if (tid == 0) s_boosts = 0;
-    __syncthreads();
-    {
-        const int nb = min(B, m), ph = min(nb + K, m), R = min(K, m - nb);
-        if (pg) {
-            pg_stage_panel(L, smem, 0, nb, ph, 0, 0, tid);
-            named_sync(kBarPg, kPgThreads);
-            pg_panel_pext<B>(L, smem, s_prow, s_X, s_L11, &s_boosts, 0, nb, ph, tid);
-            pg_stage_a12<B>(L, smem + 2 * psz, 0, nb, R, tid);
-        }
-    }
-    int cur = 0;
-    int step = 0;
-    for (int jb = 0; jb < m; jb += B, ++step) {
-        __syncthreads();  // S0: Pext(s), A12(s) ready
-        LU_TRACE(step, 0, tid == 0);
-        const int nb = min(B, m - jb);
-        const int ja = jb + nb;
-        const int R = min(K, m - ja);
-        const bool has_next = ja < m;
-        const int nbn = has_next ? min(B, m - ja) : 0;
-        const int phn = has_next ? min(nbn + K, m - ja) : 0;
-        const int Rn = has_next ? min(K, m - ja - nbn) : 0;
-        const int ca = min(nbn, R);
-        const double* P = smem + cur * psz;
-        const double* A = smem + 2 * psz + cur * usz;
-        double* Pn = smem + (cur ^ 1) * psz;
-        double* An = smem + 2 * psz + (cur ^ 1) * usz;
-        // ---- phase (a): the next panel's columns (U12 part -> global, A22 part -> Pn) ----
-        if (has_next && ca > 0) {
-            dmma_tiles(L, make_tiles(0, nb, 0, ca, jb, ja, 0, nb, nb, 0), P, A, nb, warp, kLuThreads / 32, nullptr);
-            dmma_tiles(L, make_tiles(nb, nb + R, 0, ca, jb, ja, 0, 0, 0, nb), P, A, nb,
-                       (warp + kLuThreads / 32 - 2) % (kLuThreads / 32), kLuThreads / 32, Pn);
-        }
-        __syncthreads();  // S1
-        LU_TRACE(step, 1, tid == 0);
-        if (pg) {
-            if (has_next) {
-                pg_stage_panel(L, Pn, ja, nbn, phn, R, ca, tid);
-                named_sync(kBarPg, kPgThreads);
-                LU_TRACE(step, 2, tid == 0);
-                pg_panel_pext<B>(L, Pn, s_prow, s_X, s_L11, &s_boosts, ja, nbn, phn, tid);
-                LU_TRACE(step, 3, tid == 0);
-                named_sync(kBarTop, kLuThreads);  // UG has written A12(s+1)'s rows
-                LU_TRACE(step, 5, tid == 0);
-                pg_stage_a12<B>(L, An, ja, nbn, Rn, tid);
-                LU_TRACE(step, 6, tid == 0);
-            }
-        } else {
-            const int uw = warp - kPgWarps;
-            const int top = has_next ? nb + min(R, ((nbn + 15) >> 4) << 4) : nb;
-            dmma_tiles(L, make_tiles(nb, top, ca, R, jb, ja, 0, 0, 0, 0), P, A, nb, uw, kUgWarps, nullptr);
-            LU_TRACE(step, 7, tid == kPgThreads);
-            if (has_next) {
-                __threadfence_block();
-                named_arrive(kBarTop, kLuThreads);
-            }
-            dmma_tiles(L, make_tiles(0, nb, ca, R, jb, ja, 0, nb, nb, 0), P, A, nb, uw, kUgWarps, nullptr);
-            dmma_tiles(L, make_tiles(top, nb + R, ca, R, jb, ja, 0, 0, 0, 0), P, A, nb, uw, kUgWarps, nullptr);
-            LU_TRACE(step, 8, tid == kPgThreads);
-            LU_TRACE(step, 9, tid == kLuThreads - 32);
-        }
-        cur ^= 1;
-    }
-    __syncthreads();
-    if (tid == 0) *J.boosts = s_boosts;
-}
-
-// Sequential schedule with the extended-row update (no U12 triangular solve):
-// stage panel -> factor + build Pext (threads 0..255) -> stage raw A12 ->
-// C <- C - Pext * A12 over [panel rows ; A22 rows] with all 16 warps.
-template <int B>
-__global__ void __launch_bounds__(kLuThreads, 1)
-    k_band_lu_ext(const FactorJob* __restrict__ jobs, double eps, int pld, int uld) {
-    extern __shared__ __align__(16) double smem[];
-    __shared__ int s_boosts;
-    __shared__ __align__(16) double s_prow[2 * (B + 2)];
-    __shared__ double s_X[32 * 33];
-    __shared__ double s_L11[32 * 33];
-    const FactorJob J = jobs[blockIdx.x];
-    const double scale = *J.scale;
-    Lu L{J.base, J.rs, J.cs, J.m, J.k, B, pld, uld, eps * (scale > 0 ? scale : 1.0), J.src ? J.src : J.base};
-    double* P = smem;
-    double* A = smem + B * pld;
-    const int tid = threadIdx.x, warp = tid >> 5;
-    const bool pg = tid < kPgThreads;
-    const int m = L.m, K = L.K;
-    if (tid == 0) s_boosts = 0;
-    __syncthreads();
-    int step = 0;
-    for (int jb = 0; jb < m; jb += B, ++step) {
-        const int nb = min(B, m - jb);
-        const int ph = min(nb + K, m - jb);
-        const int ja = jb + nb;
-        const int R = min(K, m - ja);
-        LU_TRACE(step, 0, tid == 0);
-        if (pg) {
-            pg_stage_panel(L, P, jb, nb, ph, 0, 0, tid);
-            named_sync(kBarPg, kPgThreads);
-            LU_TRACE(step, 2, tid == 0);
-            pg_panel_pext<B>(L, P, s_prow, s_X, s_L11, &s_boosts, jb, nb, ph, tid);
-            LU_TRACE(step, 3, tid == 0);
-            pg_stage_a12<B>(L, A, jb, nb, R, tid);
-            LU_TRACE(step, 6, tid == 0);
-        }
-        __syncthreads();
-        LU_TRACE(step, 1, tid == 0);
-        dmma_tiles(L, make_tiles(0, nb + R, 0, R, jb, ja, 0, nb, nb, 0), P, A, nb, warp, kLuThreads / 32, nullptr);
         LU_TRACE(step, 8, tid == 0);
         LU_TRACE(step, 9, tid == kLuThreads - 32);
         __syncthreads();
@@ -1396,369 +1089,6 @@ __global__ void __launch_bounds__(kLuThreads, 1)
     if (STREAM && tid == 0 && s_timeout) *J.minpiv = -1.0;  // min |pivot| is read off U's diagonal afterwards
 }
 
-// ---------------------------------------------------------------------------
-// k_band_lu_la2: k_band_lu_res with look-ahead. Warps 0-7 (PG) factor panel s+1 and its U12 while warps
-// 8-15 (UG) finish step s's trailing update. UG first computes the tiles that form panel s+1 (A22's first
-// column tile) and A12(s+1) (its first two row tiles) into smem plus step s+1's new band entries, then
-// releases PG through a named barrier and streams the remaining tiles through L2.
-
-// Sub-panel [q0, q0+8) after its diagonal block, by a group of nthr threads (ptid = index in the group):
-// each thread takes one L row and one U column, then the rank-8 updates (DMMA when FULL).
-template <bool FULL>
-__device__ __noinline__ void grp_sub(double* __restrict__ P, double* __restrict__ A, int pld, int uld, int q0, int nq_rt,
-                                     int nb, int ph, int R, const double* __restrict__ s_rcp, int ptid, int nthr,
-                                     int bar) {
-    // rows [q1, ph) and columns (panel [q1, nb), then A12 [0, R)) are dealt round-robin over the group's nthr
-    // threads (one each when nthr covers them)
-    const int nq = FULL ? 8 : nq_rt;
-    const int q1 = q0 + 8;
-    const int npc = max(nb - q1, 0);
-    for (int r = q1 + ptid; r < ph; r += nthr) {
-        double xr[8];
-#pragma unroll
-        for (int cc = 0; cc < 8; ++cc) xr[cc] = P[(q0 + cc) * pld + r];
-#pragma unroll
-        for (int cc = 0; cc < 8; ++cc) {
-            if (cc < nq) {
-                const double l = div_rcp(xr[cc], s_rcp[32 + q0 + cc], s_rcp[q0 + cc]);
-                xr[cc] = l;
-#pragma unroll
-                for (int c2 = cc + 1; c2 < 8; ++c2) xr[c2] = fma(-l, P[(q0 + c2) * pld + q0 + cc], xr[c2]);
-            }
-        }
-#pragma unroll
-        for (int cc = 0; cc < 8; ++cc) P[(q0 + cc) * pld + r] = xr[cc];
-    }
-    for (int ct = ptid; ct < npc + R; ct += nthr) {
-        const bool is_p = ct < npc;
-        const int c = is_p ? q1 + ct : ct - npc;
-        double xc[8];
-        double* col = is_p ? P + c * pld + q0 : A + q0 * uld + c;
-        const int st = is_p ? 1 : uld;
-#pragma unroll
-        for (int rr = 0; rr < 8; ++rr) xc[rr] = col[rr * st];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            if (j < nq) {
-#pragma unroll
-                for (int rr = j + 1; rr < 8; ++rr) xc[rr] = fma(-P[(q0 + j) * pld + q0 + rr], xc[j], xc[rr]);
-            }
-        }
-#pragma unroll
-        for (int rr = 0; rr < 8; ++rr) col[rr * st] = xc[rr];
-    }
-    named_sync(bar, nthr);
-    if constexpr (FULL) {
-        const int lane = ptid & 31, w = ptid >> 5, nw = nthr >> 5, lr = lane >> 2, lc = lane & 3;
-        const int pct = (nb - q1 + 7) >> 3, np_t = ((ph - q1 + 7) >> 3) * pct;
-        const int act8 = (R + 7) >> 3, na_t = ((nb - q1 + 7) >> 3) * act8;
-        for (int t = w; t < np_t + na_t; t += nw) {
-            const bool pan = t < np_t;
-            const int t2 = pan ? t : t - np_t, tc = pan ? pct : act8;
-            const int i0 = q1 + (t2 / tc) * 8, j0 = (pan ? q1 : 0) + (t2 % tc) * 8;
-            const int rmax = pan ? ph : nb, cmax = pan ? nb : R;
-            const int j = j0 + lr;
-            double* cp = pan ? P + j * pld : A + j;
-            const int cs = pan ? 1 : uld;
-            const double* up = pan ? P + j * pld + q0 : A + q0 * uld + j;
-            const int us = pan ? 1 : uld;
-            const int ib = i0 + 2 * lc;
-            double c0 = (ib < rmax && j < cmax) ? cp[ib * cs] : 0.0;
-            double c1 = (ib + 1 < rmax && j < cmax) ? cp[(ib + 1) * cs] : 0.0;
-            const int il = i0 + lr;
-#pragma unroll
-            for (int ks = 0; ks < 2; ++ks) {
-                const int k = ks * 4 + lc;
-                const double av = j < cmax ? up[k * us] : 0.0;
-                const double bv = il < rmax ? -P[(q0 + k) * pld + il] : 0.0;
-                dmma_m8n8k4(c0, c1, av, bv, c0, c1);
-            }
-            if (j < cmax) {
-                if (ib < rmax) cp[ib * cs] = c0;
-                if (ib + 1 < rmax) cp[(ib + 1) * cs] = c1;
-            }
-        }
-    } else {
-        for (int r = q1 + ptid; r < ph; r += nthr)
-            for (int cc = q1; cc < nb; ++cc) {
-                double acc = P[cc * pld + r];
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    if (j < nq) acc = fma(-P[(q0 + j) * pld + r], P[cc * pld + q0 + j], acc);
-                P[cc * pld + r] = acc;
-            }
-        for (int c = ptid; c < R; c += nthr)
-            for (int rr = q1; rr < nb; ++rr) {
-                double acc = A[rr * uld + c];
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    if (j < nq) acc = fma(-P[(q0 + j) * pld + rr], A[(q0 + j) * uld + c], acc);
-                A[rr * uld + c] = acc;
-            }
-    }
-    named_sync(bar, nthr);
-}
-
-// Factor panel (jp, np) and its U12 (rows [0, np) x cols [0, R)) in smem with a thread group, then store
-// both to global.
-__device__ __noinline__ void grp_panel(const Lu& L, double* __restrict__ P, double* __restrict__ A, int jp, int np,
-                                       int ph, int R, double* __restrict__ s_rcp, int* boost_ctr, int ptid, int nthr,
-                                       int bar) {
-    const int pld = L.pld, uld = L.uld, K = L.K;
-    const bool full = np == 32;
-    for (int q0 = 0; q0 < np; q0 += 8) {
-        const int nq = min(8, np - q0);
-        if (ptid == 0) {
-            if (full)
-                res_diag8<true>(P, pld, L.bv, q0, nq, s_rcp, boost_ctr);
-            else
-                res_diag8<false>(P, pld, L.bv, q0, nq, s_rcp, boost_ctr);
-        }
-        named_sync(bar, nthr);
-        if (full)
-            grp_sub<true>(P, A, pld, uld, q0, nq, np, ph, R, s_rcp, ptid, nthr, bar);
-        else
-            grp_sub<false>(P, A, pld, uld, q0, nq, np, ph, R, s_rcp, ptid, nthr, bar);
-    }
-    // panel (L11\U11, L21) and U12 to global: a warp per column, lanes down the rows
-    const int lane = ptid & 31, w = ptid >> 5, nw = nthr >> 5;
-    const long long rs = L.rs;
-    for (int c = w; c < np; c += nw) {
-        double* g = L.at(jp, jp + c);
-        const int r0 = max(c - K, 0), r1 = min(ph, c + K + 1);
-        for (int r = r0 + lane; r < r1; r += 32) __stcg(g + r * rs, P[c * pld + r]);
-    }
-    for (int c = w; c < R; c += nw)
-        if (lane < np && np + c - lane <= K) __stcg(L.at(jp + lane, jp + np + c), A[lane * uld + c]);
-}
-
-// Trailing update tiles [t0, t1) of step (nb, ja, R) in priority order: the first column tile (panel s+1's
-// columns -> Pn), the first two row tiles (A12(s+1) -> An), then the rest (-> global).
-__device__ __noinline__ void ug_tiles(const Lu& L, const double* __restrict__ P, const double* __restrict__ U, int nb,
-                                      int ja, int R, int nbn, double* __restrict__ Pn, double* __restrict__ An, int t0,
-                                      int t1, int uw, int nuw) {
-    const int lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
-    const int pld = L.pld, uld = L.uld;
-    const TileCtx T = make_tiles(0, R, 0, R, ja, ja, nb, 0, 0, 0);
-    const int nrt = (R + kTileR - 1) / kTileR, tcols = T.tcols;
-    const int pr = min(2, nrt);  // priority row tiles (rows < 32)
-    const int ksteps = (nb + 3) >> 2;
-    double acc[2][kTQ][2];
-    for (int t = t0 + uw; t < t1; t += nuw) {
-        int ri, ci;
-        if (t < nrt) {
-            ri = t;
-            ci = 0;
-        } else if (t < nrt + pr * (tcols - 1)) {
-            const int u = t - nrt;
-            ri = u % pr;
-            ci = 1 + u / pr;
-        } else {
-            const int u = t - nrt - pr * (tcols - 1);
-            ri = pr + u / (tcols - 1);
-            ci = 1 + u % (tcols - 1);
-        }
-        const int tt = ri * tcols + ci;  // tile index in make_tiles order
-        const int row0 = ri * kTileR, col0 = ci * kTileC;
-        tile_load(L, T, tt, acc);
-        const bool a1 = row0 + 8 < R;
-        bool qv[kTQ];
-#pragma unroll
-        for (int q = 0; q < kTQ; ++q) qv[q] = col0 + q * 8 < R;
-        const double* pk = P + nb + row0 + lr;
-        const double* uk = U + col0 + lr;
-        if (ksteps == 8 && a1 && qv[kTQ - 1]) {
-            double b0 = -pk[lc * pld], b1 = -pk[lc * pld + 8], aq[kTQ];
-#pragma unroll
-            for (int q = 0; q < kTQ; ++q) aq[q] = uk[lc * uld + q * 8];
-#pragma unroll
-            for (int ks = 0; ks < 8; ++ks) {
-                double nb0 = 0.0, nb1 = 0.0, naq[kTQ];
-                if (ks + 1 < 8) {
-                    const int kn = (ks + 1) * 4 + lc;
-                    nb0 = -pk[kn * pld];
-                    nb1 = -pk[kn * pld + 8];
-#pragma unroll
-                    for (int q = 0; q < kTQ; ++q) naq[q] = uk[kn * uld + q * 8];
-                }
-#pragma unroll
-                for (int q = 0; q < kTQ; ++q) {
-                    dmma_m8n8k4(acc[0][q][0], acc[0][q][1], aq[q], b0, acc[0][q][0], acc[0][q][1]);
-                    dmma_m8n8k4(acc[1][q][0], acc[1][q][1], aq[q], b1, acc[1][q][0], acc[1][q][1]);
-                }
-                if (ks + 1 < 8) {
-                    b0 = nb0;
-                    b1 = nb1;
-#pragma unroll
-                    for (int q = 0; q < kTQ; ++q) aq[q] = naq[q];
-                }
-            }
-        } else {
-            for (int ks = 0; ks < ksteps; ++ks) {
-                const int kk = ks * 4 + lc;
-                const double b0 = -pk[kk * pld];
-                const double b1 = -pk[kk * pld + 8];
-#pragma unroll
-                for (int q = 0; q < kTQ; ++q) {
-                    if (qv[q]) {
-                        const double aq = uk[kk * uld + q * 8];
-                        dmma_m8n8k4(acc[0][q][0], acc[0][q][1], aq, b0, acc[0][q][0], acc[0][q][1]);
-                        if (a1) dmma_m8n8k4(acc[1][q][0], acc[1][q][1], aq, b1, acc[1][q][0], acc[1][q][1]);
-                    }
-                }
-            }
-        }
-        const int ib = row0 + 2 * lc, cb = col0 + lr;
-        const bool to_p = col0 < nbn, to_a = !to_p && row0 < nbn;
-        if (!to_p && !to_a) {
-            const long long rs = L.rs, ra8 = 8 * rs, cq8 = 8 * L.cs;
-            double* p00 = L.at(ja + ib, ja + cb);
-            double* lo00 = rs > 0 ? p00 : p00 - 1;
-            const bool fullt = row0 + kTileR <= R && col0 + kTileC <= R;
-            if (fullt && ((reinterpret_cast<uintptr_t>(lo00) & 15) == 0)) {
-#pragma unroll
-                for (int a = 0; a < 2; ++a)
-#pragma unroll
-                    for (int q = 0; q < kTQ; ++q) {
-                        double2 v;
-                        v.x = rs > 0 ? acc[a][q][0] : acc[a][q][1];
-                        v.y = rs > 0 ? acc[a][q][1] : acc[a][q][0];
-                        __stcg(reinterpret_cast<double2*>(lo00 + a * ra8 + q * cq8), v);
-                    }
-            } else {
-#pragma unroll
-                for (int a = 0; a < 2; ++a)
-#pragma unroll
-                    for (int q = 0; q < kTQ; ++q)
-#pragma unroll
-                        for (int e = 0; e < 2; ++e) {
-                            const int i = ib + a * 8 + e, c = cb + q * 8;
-                            if (i < R && c < R) __stcg(p00 + a * ra8 + e * rs + q * cq8, acc[a][q][e]);
-                        }
-            }
-        } else {
-#pragma unroll
-            for (int a = 0; a < 2; ++a)
-#pragma unroll
-                for (int q = 0; q < kTQ; ++q)
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        const int i = ib + a * 8 + e, c = cb + q * 8;
-                        if (i >= R || c >= R) continue;
-                        if (c < nbn)
-                            Pn[c * pld + i] = acc[a][q][e];
-                        else if (i < nbn)
-                            An[i * uld + (c - nbn)] = acc[a][q][e];
-                        else
-                            __stcg(L.at(ja + i, ja + c), acc[a][q][e]);
-                    }
-        }
-    }
-}
-
-// Step s+1's new band entries (panel rows [R, phn), A12 columns [R-nbn, Rn)) into smem, by a thread group.
-__device__ __noinline__ void ug_new_entries(const Lu& L, double* __restrict__ Pn, double* __restrict__ An, int ja, int R,
-                                            int nbn, int phn, int Rn, int uw, int nuw) {
-    const int lane = threadIdx.x & 31, pld = L.pld, uld = L.uld;
-    if (R < nbn) {  // tail: the generic fetch (rare)
-        res_fetch(L, Pn, An, ja, nbn, R, phn, Rn, threadIdx.x - lane - uw * 32, nuw * 32);
-        cp_async_wait_all();
-        return;
-    }
-    double v[8];
-    int n = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int f = uw + nuw * i;
-        v[i] = 0.0;
-        if (f < 32) {
-            const int r = R + lane;
-            if (f < nbn && r < phn && r - f <= L.K) v[i] = __ldcg(L.at(ja + r, ja + f));
-        } else if (f < 64) {
-            const int c = R - nbn + (f - 32);
-            if (c < Rn && lane < nbn && nbn + c - lane <= L.K) v[i] = __ldcg(L.at(ja + lane, ja + nbn + c));
-        }
-        n = i + 1;
-        if (uw + nuw * (i + 1) >= 64) break;
-    }
-    for (int i = 0; i < n; ++i) {
-        const int f = uw + nuw * i;
-        if (f < 32) {
-            const int r = R + lane;
-            if (f < nbn && r < phn) Pn[f * pld + r] = v[i];
-        } else if (f < 64) {
-            const int c = R - nbn + (f - 32);
-            if (c < Rn && lane < nbn) An[lane * uld + c] = v[i];
-        }
-    }
-}
-
-template <int B>
-__global__ void __launch_bounds__(kLuThreads, 1)
-    k_band_lu_la2(const FactorJob* __restrict__ jobs, double eps, int pld, int uld) {
-    extern __shared__ __align__(16) double smem[];
-    __shared__ int s_boosts;
-    __shared__ double s_rcp[2 * B];  // [0, B): 1/p, [B, 2B): p
-    constexpr int kPg = SAP_LA2_PG;   // PG: threads [0, kPg); UG: the rest
-    constexpr int kBarPgL = 3;        // PG internal
-    constexpr int kBarNext = 4;       // UG -> PG: panel s+1 / A12(s+1) complete in smem
-    const FactorJob J = jobs[blockIdx.x];
-    const double scale = *J.scale;
-    Lu L{J.base, J.rs, J.cs, J.m, J.k, B, pld, uld, eps * (scale > 0 ? scale : 1.0), J.src ? J.src : J.base};
-    const int psz = B * pld, usz = B * uld;
-    const int tid = threadIdx.x, warp = tid >> 5;
-    const bool pg = tid < kPg;
-    const int m = L.m, K = L.K;
-    for (int i = tid; i < 2 * (psz + usz); i += kLuThreads) smem[i] = 0.0;
-    if (tid == 0) s_boosts = 0;
-    __syncthreads();
-    {
-        const int nb = min(B, m), ph = min(nb + K, m), R = min(K, m - nb);
-        res_fetch(L, smem, smem + 2 * psz, 0, nb, 0, ph, R, 0, kLuThreads);
-        cp_async_wait_all();
-        __syncthreads();
-        if (pg) grp_panel(L, smem, smem + 2 * psz, 0, nb, ph, R, s_rcp, &s_boosts, tid, kPg, kBarPgL);
-    }
-    __syncthreads();
-    int cur = 0, step = 0;
-    for (int jb = 0; jb < m; jb += B, ++step) {
-        const int nb = min(B, m - jb);
-        const int ja = jb + nb;
-        const int R = min(K, m - ja);
-        const bool has_next = ja < m;
-        const int nbn = has_next ? min(B, m - ja) : 0;
-        const int phn = has_next ? min(nbn + K, m - ja) : 0;
-        const int Rn = has_next ? min(K, m - ja - nbn) : 0;
-        double* P = smem + cur * psz;
-        double* A = smem + 2 * psz + cur * usz;
-        double* Pn = smem + (cur ^ 1) * psz;
-        double* An = smem + 2 * psz + (cur ^ 1) * usz;
-        LU_TRACE(step, 0, tid == 0);
-        const int nrt = R > 0 ? (R + kTileR - 1) / kTileR : 0;
-        const int tcols = R > 0 ? (R + kTileC - 1) / kTileC : 0;
-        const int ntiles = nrt * tcols;
-        const int nprio = (has_next && nbn == B && tcols > 1) ? nrt + min(2, nrt) * (tcols - 1) : ntiles;
-        if (!pg) {
-            const int uw = warp - kPg / 32, nuw = (kLuThreads - kPg) / 32;
-            ug_tiles(L, P, A, nb, ja, R, nbn, Pn, An, 0, nprio, uw, nuw);
-            if (has_next) ug_new_entries(L, Pn, An, ja, R, nbn, phn, Rn, uw, nuw);
-            __threadfence_block();
-            named_arrive(kBarNext, kLuThreads);
-            LU_TRACE(step, 7, tid == kPg);
-            ug_tiles(L, P, A, nb, ja, R, nbn, Pn, An, nprio, ntiles, uw, nuw);
-            LU_TRACE(step, 8, tid == kPg);
-        } else {
-            named_sync(kBarNext, kLuThreads);
-            LU_TRACE(step, 2, tid == 0);
-            if (has_next) grp_panel(L, Pn, An, ja, nbn, phn, Rn, s_rcp, &s_boosts, tid, kPg, kBarPgL);
-            LU_TRACE(step, 3, tid == 0);
-        }
-        __syncthreads();
-        cur ^= 1;
-    }
-    if (tid == 0) *J.boosts = s_boosts;
-}
-
 static int pad_ld(int x) {
     // leading dimensions == 4 or 12 (mod 16) keep the DMMA fragment loads conflict-free
     while ((x % 16) != 4 && (x % 16) != 12) ++x;
@@ -1774,64 +1104,7 @@ bool launch_band_lu_ws(const FactorJob* d_jobs, int njobs, int max_k, double eps
     constexpr int B = 32;
     // panel rows (<= B + K) must fit one per panel-group thread
     if (max_k < 1 || B + max_k > kPgThreads) return false;
-    const int k8 = ((max_k + 7) / 8) * 8;
-    const int pld = pad_ld(B + 16 * ((max_k + 15) / 16) + 8);
-    const int uld = pad_ld(k8 + 32);
-    // variants kept for study, all measured slower than k_band_lu_seq on B200:
-    //   SAP_LU_EXT=1  extended-row update (U12 folded into DMMA through L11^{-1}; also less accurate at d < 0.5)
-    //   SAP_LU_LA=1   warp-specialized look-ahead + extended rows
-    //   SAP_LU_WS=1   warp-specialized look-ahead
-    static const bool ext = getenv("SAP_LU_EXT") != nullptr;
-    if (ext && B + max_k <= kPgThreads) {
-        const int plde = pad_ld(B + 16 * ((max_k + 15) / 16) + 8);
-        const int ulde = pad_ld(((max_k + 7) / 8) * 8 + 8);
-        const size_t bytes = sizeof(double) * (size_t)(B * plde + B * ulde);
-        if (bytes <= 200 * 1024) {
-            SAP_CUDA(cudaFuncSetAttribute(k_band_lu_ext<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-            k_band_lu_ext<B><<<njobs, kLuThreads, bytes, s>>>(d_jobs, eps, plde, ulde);
-            SAP_LAUNCHED();
-            return true;
-        }
-    }
-    static const bool la = getenv("SAP_LU_LA") != nullptr;
-    if (la) {
-        constexpr int BL = 28;
-        const int pldl = pad_ld(BL + 16 * ((max_k + 15) / 16) + 8);
-        const int uldl = pad_ld(((max_k + 7) / 8) * 8 + 8);
-        const size_t bytes = sizeof(double) * (size_t)(2 * BL * pldl + 2 * BL * uldl);
-        if (bytes <= 206 * 1024 && BL + max_k <= kPgThreads) {
-            SAP_CUDA(cudaFuncSetAttribute(k_band_lu_la<BL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-            k_band_lu_la<BL><<<njobs, kLuThreads, bytes, s>>>(d_jobs, eps, pldl, uldl);
-            SAP_LAUNCHED();
-            return true;
-        }
-    }
-    static const bool ws = getenv("SAP_LU_WS") != nullptr;
-    if (ws) {
-        constexpr int BW = 24;
-        const int pldw = pad_ld(BW + 16 * ((max_k + 15) / 16) + 8);
-        const int uldw = pad_ld(k8 + 8);
-        const size_t bytes = sizeof(double) * (size_t)(2 * BW * pldw + 2 * BW * uldw);
-        if (bytes > 222 * 1024) return false;
-        SAP_CUDA(cudaFuncSetAttribute(k_band_lu_ws<BW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-        k_band_lu_ws<BW><<<njobs, kLuThreads, bytes, s>>>(d_jobs, eps, pldw, uldw);
-        SAP_LAUNCHED();
-        return true;
-    }
-    static const bool seq = getenv("SAP_LU_SEQ") != nullptr;
-    static const bool la2 = getenv("SAP_LU_LA2") != nullptr;
-    if (!seq && la2 && max_k <= 256 - B) {
-        const int pldr = pad_ld(B + max_k);
-        const int uldr = pad_ld(max_k);
-        const size_t rbytes = sizeof(double) * (size_t)(2 * B * pldr + 2 * B * uldr);
-        if (rbytes <= 226 * 1024) {
-            SAP_CUDA(cudaFuncSetAttribute(k_band_lu_la2<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rbytes));
-            k_band_lu_la2<B><<<njobs, kLuThreads, rbytes, s>>>(d_jobs, eps, pldr, uldr);
-            SAP_LAUNCHED();
-            return true;
-        }
-    }
-    if (!seq && max_k <= 256 - B) {
+    if (max_k <= 256 - B) {
         // panel rows: L21 by threads 0-255, U12 columns by threads 256-511
         const int pldr = pad_ld(B + max_k);
         const int uldr = pad_ld(max_k);
@@ -1850,6 +1123,9 @@ bool launch_band_lu_ws(const FactorJob* d_jobs, int njobs, int max_k, double eps
             return true;
         }
     }
+    const int k8 = ((max_k + 7) / 8) * 8;
+    const int pld = pad_ld(B + 16 * ((max_k + 15) / 16) + 8);
+    const int uld = pad_ld(k8 + 32);
     const size_t bytes = sizeof(double) * (size_t)(B * pld + B * uld);
     if (bytes > 222 * 1024) return false;
     SAP_CUDA(cudaFuncSetAttribute(k_band_lu_seq<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
@@ -1862,9 +1138,6 @@ bool launch_band_lu_ws(const FactorJob* d_jobs, int njobs, int max_k, double eps
 // never-updated entry from FactorJob::src, so the factor stores need no initial copy of the band
 // (only their out-of-matrix slots zeroed, launch_zero_pad).
 bool band_lu_reads_source(int max_k) {
-    if (getenv("SAP_LU_SIMPLE") || getenv("SAP_LU_EXT") || getenv("SAP_LU_LA") || getenv("SAP_LU_WS") ||
-        getenv("SAP_LU_SEQ") || getenv("SAP_LU_LA2"))
-        return false;
     constexpr int B = 32;
     if (max_k < 1 || max_k > 256 - B) return false;
     const int pldr = pad_ld(B + max_k), uldr = pad_ld(max_k);

@@ -318,8 +318,7 @@ __global__ void __launch_bounds__(256, 3)
 
 void launch_spike_tips(const TipJob* d_jobs, int njobs, int k, int* nonfinite, cudaStream_t s) {
     if (njobs <= 0 || k == 0) return;
-    static const bool old = getenv("SAP_TIPS_OLD") != nullptr;
-    if (!old) {
+    {
         const size_t bytes = sizeof(double) * ((size_t)k * kTXld + kTB * kTSld);
         if (bytes <= 200 * 1024) {
             SAP_CUDA(cudaFuncSetAttribute(k_spike_tips_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
@@ -358,47 +357,8 @@ void launch_extract_one(const double* band, int n, int k, int e, int which, doub
 }
 
 // ---------------------------------------------------------------------------
-// rbar[t] = I - wt[t] vb[t]; each element accumulates l ascending (FMA) as
-// finish_reduced_blocks does (spike.hpp:154-160). 32x32 output tile per CTA.
-__global__ void k_rbar(const double* __restrict__ wt, const double* __restrict__ vb, int w,
-                       double* __restrict__ rbar, long long rpstride, int rpad, int* __restrict__ nonfinite) {
-    __shared__ double As[32][33];
-    __shared__ double Bs[32][33];
-    const int t = blockIdx.z;
-    const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads, 4 rows each
-    const double* A = wt + (long long)t * w * w;
-    const double* Bm = vb + (long long)t * w * w;
-    double acc[4] = {0, 0, 0, 0};
-    for (int l0 = 0; l0 < w; l0 += 32) {
-        for (int q = 0; q < 4; ++q) {
-            const int r = ty + 8 * q;
-            As[r][tx] = (i0 + r < w && l0 + tx < w) ? A[(long long)(i0 + r) * w + l0 + tx] : 0.0;
-            Bs[r][tx] = (l0 + r < w && j0 + tx < w) ? Bm[(long long)(l0 + r) * w + j0 + tx] : 0.0;
-        }
-        __syncthreads();
-        const int lmax = min(32, w - l0);
-        for (int l = 0; l < lmax; ++l) {
-            const double b = Bs[l][tx];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) acc[q] = fma(As[ty + 8 * q][l], b, acc[q]);
-        }
-        __syncthreads();
-    }
-    int bad = 0;
-    const long long bw = 2LL * w - 1;  // band width of the k = w-1 layout
-    for (int q = 0; q < 4; ++q) {
-        const int i = i0 + ty + 8 * q, j = j0 + tx;
-        if (i < w && j < w) {
-            const double v = (i == j ? 1.0 : 0.0) - acc[q];
-            if (!isfinite(v)) bad = 1;
-            rbar[(long long)t * rpstride + rpad + (long long)j * bw + (i - j + w - 1)] = v;
-        }
-    }
-    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite + t, 1);
-}
-
-// The same product on DMMA (m8n8k4): 32 x 32 output tile per CTA, W and V staged 32 columns / rows at a
+// rbar[t] = I - wt[t] vb[t] (finish_reduced_blocks, spike.hpp:154-160).
+// On DMMA (m8n8k4): 32 x 32 output tile per CTA, W and V staged 32 columns / rows at a
 // time, each warp two 8 x 8 tiles. The k-sum runs in groups of 4 inside the MMA (within the SURVEY §8c
 // tolerance of finish_reduced_blocks' ascending FMA order).
 constexpr int kRbLd = 36;
@@ -453,11 +413,7 @@ void launch_rbar(const double* wt, const double* vb, int w, int ni, double* rbar
                  int* nonfinite, cudaStream_t s) {
     if (ni <= 0 || w == 0) return;
     dim3 grid(ceil_div(w, 32), ceil_div(w, 32), ni);
-    static const bool fma_path = getenv("SAP_RBAR_FMA") != nullptr;
-    if (fma_path)
-        k_rbar<<<grid, 256, 0, s>>>(wt, vb, w, rbar, rst.pstride, rst.pad, nonfinite);
-    else
-        k_rbar_mma<<<grid, 256, 0, s>>>(wt, vb, w, rbar, rst.pstride, rst.pad, nonfinite);
+    k_rbar_mma<<<grid, 256, 0, s>>>(wt, vb, w, rbar, rst.pstride, rst.pad, nonfinite);
     SAP_LAUNCHED();
 }
 

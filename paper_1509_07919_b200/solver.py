@@ -131,7 +131,7 @@ class Solver:
     """SaP setup()/solve() over libsap_gpu (one handle, one CUDA stream)."""
 
     def __init__(self, p: int = 1, precond: PrecondKind = PrecondKind.coupled, boost_eps: float = 1e-10,
-                 krylov: KrylovOptions | None = None, device: int = 0):
+                 krylov: KrylovOptions | None = None, device: int = 0, triangle_solve: int = 0):
         kr = krylov or KrylovOptions()
         o = L.sap_options()
         L.load().sap_options_default(C.byref(o))
@@ -139,6 +139,7 @@ class Solver:
         o.method, o.ell, o.rel_tol, o.abs_tol = int(kr.method), int(kr.ell), float(kr.rel_tol), float(kr.abs_tol)
         o.max_iterations, o.mixed_precision = int(kr.max_iterations), int(kr.mixed_precision)
         o.caller_asserts_spd, o.device = int(kr.caller_asserts_spd), int(device)
+        o.triangle_solve = int(triangle_solve)  # 0 automatic, 1 chunk inverses, 2 substitution
         self.options = o
         self._h = C.c_void_p()
         self._create()
@@ -278,14 +279,37 @@ class Solver:
                                              v.ctypes.data, 0))
 
     # -- the two LinearOps ----------------------------------------------
+    @staticmethod
+    def _check_out(name, buf, like):
+        """The library writes len(like) float64 values through buf's raw pointer: a caller-supplied
+        output must be exactly that (the reference's std::span length check, spike.hpp:311-318)."""
+        if _is_cuda_tensor(like):
+            import torch
+            ok = (_is_cuda_tensor(buf) and buf.dtype == torch.float64 and buf.is_contiguous()
+                  and buf.numel() == like.numel() and buf.device == like.device)
+        else:
+            ok = (isinstance(buf, np.ndarray) and buf.dtype == np.float64 and buf.flags.c_contiguous
+                  and buf.flags.writeable and buf.size == like.size)
+        if not ok:
+            raise ValueError(f"{name}: output must be a writable C-contiguous float64 buffer of length "
+                             f"{like.numel() if _is_cuda_tensor(like) else like.size} on the input's device")
+
     def _op(self, fn, x, out):
         if _is_cuda_tensor(x):
             import torch
-            out = torch.empty_like(x) if out is None else out
+            if x.dtype != torch.float64 or not x.is_contiguous():
+                raise ValueError("input must be a contiguous float64 tensor")
+            if out is None:
+                out = torch.empty_like(x)
+            else:
+                self._check_out("apply", out, x)
             _check(fn(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(out.data_ptr()), 1))
             return out
         x = np.ascontiguousarray(x, dtype=np.float64)
-        out = np.empty_like(x) if out is None else out
+        if out is None:
+            out = np.empty_like(x)
+        else:
+            self._check_out("apply", out, x)
         _check(fn(self._h, x.ctypes.data, out.ctypes.data, 0))
         return out
 
@@ -306,11 +330,19 @@ class Solver:
         st.history_capacity = cap
         if _is_cuda_tensor(b):
             import torch
-            x = torch.empty_like(b) if x is None else x
+            if b.dtype != torch.float64 or not b.is_contiguous():
+                raise ValueError("solve: b must be a contiguous float64 tensor")
+            if x is None:
+                x = torch.empty_like(b)
+            else:
+                self._check_out("solve", x, b)
             _check(L.load().sap_solve(self._h, C.c_void_p(b.data_ptr()), C.c_void_p(x.data_ptr()), 1, C.byref(st)))
         else:
             b = np.ascontiguousarray(b, dtype=np.float64)
-            x = np.zeros_like(b) if x is None else x
+            if x is None:
+                x = np.zeros_like(b)
+            else:
+                self._check_out("solve", x, b)
             _check(L.load().sap_solve(self._h, b.ctypes.data, x.ctypes.data, 0, C.byref(st)))
         stats = SolveStats(iterations=st.iterations, residual_history=list(hist[:min(st.history_len, cap)]),
                            converged=bool(st.converged), final_relative_residual=st.final_relative_residual,

@@ -36,9 +36,9 @@ def _perms(n, k, p, kb, hp, pm, oracle):
     return [pm[offsets[b]:offsets[b] + sizes[b]] if hp[b] else None for b in range(p)]
 
 
-def _check_setup(sap, ref, n, k, band, p, kb, hp, pm):
+def _check_setup(sap, ref, n, k, band, p, kb, hp, pm, triangle_solve=0):
     want = ref.ref_third_setup(n, k, band, p, kb, hp, pm)
-    s = sap.Solver(p=p, precond=sap.PrecondKind.coupled)
+    s = sap.Solver(p=p, precond=sap.PrecondKind.coupled, triangle_solve=triangle_solve)
     s.set_third_stage(kb, _perms(n, k, p, kb, hp, pm, ref))
     s.setup(band, n, k)
     for b in range(p):
@@ -188,13 +188,12 @@ def test_third_stage_sparse_pipeline_matches_solve_sparse(sap, ref, kind):
     s.close()
 
 
-def test_third_stage_full_spikes_by_substitution(sap, ref, monkeypatch):
+def test_third_stage_full_spikes_by_substitution(sap, ref):
     """The full-spike solve's substitution path (taken for ill-conditioned chunk triangles, forced here)
     against the reference, like the chunk-inverse path above."""
-    monkeypatch.setenv("SAP_FULL_SPIKE_SUBST", "1")
     n, k, p = 3000, 70, 4
     band, _ = ref.random_banded(n, k, 1.0, 22)
     kb = np.array([70, 44, 70, 33], np.int32)
     hp = np.zeros(p, np.int32)
     pm = np.tile(np.arange(n // p, dtype=np.int32), p)
-    _check_setup(sap, ref, n, k, band, p, kb, hp, pm).close()
+    _check_setup(sap, ref, n, k, band, p, kb, hp, pm, triangle_solve=2).close()
