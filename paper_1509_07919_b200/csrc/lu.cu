@@ -29,9 +29,6 @@ constexpr int kBarPg = 1;   // named barrier: panel group (256 threads)
 __device__ __forceinline__ void named_sync(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
-__device__ __forceinline__ void named_arrive(int id, int n) {
-    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
 
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
     const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -72,6 +69,32 @@ struct TileCtx {
 constexpr int kTileR = 16, kTileC = 32;  // warp tile: 2 x 4 DMMA tiles
 constexpr int kTQ = kTileC / 8;
 
+// L2 residency of the trailing-update window: the A22 tiles go out and come back every step, so their
+// loads / stores carry an evict_last policy; the final factor columns (written once) stream out with .cs.
+__device__ __forceinline__ unsigned long long l2_keep_policy() {
+    unsigned long long p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double2 ld_keep2(const double* a) {
+    double2 v;
+    asm volatile("ld.global.cg.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(v.x), "=d"(v.y) : "l"(a), "l"(l2_keep_policy()));
+    return v;
+}
+__device__ __forceinline__ double ld_keep(const double* a) {
+    double v;
+    asm volatile("ld.global.cg.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(l2_keep_policy()));
+    return v;
+}
+__device__ __forceinline__ void st_keep2(double* a, double2 v) {
+    asm volatile("st.global.cg.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(a), "d"(v.x), "d"(v.y),
+                 "l"(l2_keep_policy()) : "memory");
+}
+__device__ __forceinline__ void st_keep(double* a, double v) {
+    asm volatile("st.global.cg.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(l2_keep_policy()) : "memory");
+}
+
 __device__ __forceinline__ bool tile_ok(const Lu& L, const TileCtx& T, int i, int c) {
     return i < T.r_hi && c < T.c_hi && (i >= T.band_top || T.nbk + c - i <= L.K);
 }
@@ -89,7 +112,7 @@ __device__ __forceinline__ void tile_load(const Lu& L, const TileCtx& T, int t, 
         for (int a = 0; a < 2; ++a)
 #pragma unroll
             for (int q = 0; q < kTQ; ++q) {
-                const double2 v = __ldcg(reinterpret_cast<const double2*>(lo00 + a * ra8 + q * cq8));
+                const double2 v = ld_keep2(lo00 + a * ra8 + q * cq8);
                 acc[a][q][0] = rs > 0 ? v.x : v.y;
                 acc[a][q][1] = rs > 0 ? v.y : v.x;
             }
@@ -101,7 +124,7 @@ __device__ __forceinline__ void tile_load(const Lu& L, const TileCtx& T, int t, 
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
                     const int i = ib + a * 8 + e, c = cb + q * 8;
-                    acc[a][q][e] = tile_ok(L, T, i, c) ? __ldcg(p00 + a * ra8 + e * rs + q * cq8) : 0.0;
+                    acc[a][q][e] = tile_ok(L, T, i, c) ? ld_keep(p00 + a * ra8 + e * rs + q * cq8) : 0.0;
                 }
     }
 }
@@ -454,249 +477,178 @@ __global__ void __launch_bounds__(kLuThreads, 1)
 // k_band_lu_res: panel and A12 resident in shared memory.
 //
 // Per step s (panel columns [jb, jb+nb), A22 = the R x R window at (ja, ja), ja = jb+nb):
-//   1. warp 0 factors the nb x nb diagonal block in registers (lane = row; the pivot
-//      row's entries and 1/p travel by shuffle: no CTA barrier on the pivot chain);
-//      warps 8-15 meanwhile prefetch the band's NEW rows of panel s+1 and NEW columns
-//      of A12(s+1) (never touched by an update, so they can load this early);
-//   2. threads 0-255 finish L21 row by row (x_c = (a_c - sum_{j<c} x_j u_jc) * (1/p_c)),
-//      threads 256-511 solve U12 = L11^{-1} A12 column by column;
-//   3. the panel and U12 go to global (fire and forget);
-//   4. all 16 warps run A22 -= L21 U12 on DMMA; the tiles that form panel s+1 (A22's
-//      first nb columns) and A12(s+1) (its first rows) are written straight into the
-//      other smem buffers instead of global, so the next step starts without staging.
-// Every element receives its updates in the reference's column order with the same
-// operations as k_band_lu_seq (bitwise identical factors).
-// 8 x 8 diagonal block at (q0, q0) of the panel, factored by ONE thread in registers: the pivot chain
-// (boost -> 1/p -> multiplier -> next pivot) involves no communication at all. Left-looking by column
-// (only the multipliers stay live), with per element the same FMAs in the same ascending-column order
-// as the right-looking loop of block_factors.hpp:22-44.
-template <bool FULL>
-__device__ __noinline__ void res_diag8(double* __restrict__ P, int pld, double bv, int q0, int nq_rt,
-                                       double* __restrict__ s_rcp, int* boost_ctr) {
-    const int nq = FULL ? 8 : nq_rt;  // compile-time in the common case: no branches on the pivot chain
-    double l[8][8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-        if (c < nq) {
-            double a[8];
-#pragma unroll
-            for (int r = 0; r < 8; ++r) a[r] = P[(q0 + c) * pld + q0 + r];
-#pragma unroll
-            for (int r = 1; r < 8; ++r)
-#pragma unroll
-                for (int j = 0; j < (r < c ? r : c); ++j) a[r] = fma(-l[r][j], a[j], a[r]);
-            double p = a[c];
-            if (fabs(p) < bv) {
-                p = p < 0.0 ? -bv : bv;
-                a[c] = p;
-                atomicAdd(boost_ctr, 1);
-            }
-            const double rc = fast_rcp(p);
-            s_rcp[q0 + c] = rc;
-            s_rcp[32 + q0 + c] = p;  // the (boosted) pivot, for the quotient correction of the L rows
-#pragma unroll
-            for (int r = c + 1; r < 8; ++r) {
-                l[r][c] = div_rcp(a[r], p, rc);
-                a[r] = l[r][c];
-            }
-#pragma unroll
-            for (int r = 0; r < 8; ++r) P[(q0 + c) * pld + q0 + r] = a[r];
-        }
-    }
+//   1. the nb x nb diagonal block was factored by warp 0 at the end of step s-1 (panel_diag: lane = row,
+//      the pivot chain inside one warp); all threads finish L21 rows / U12 columns (panel_rows_cols);
+//   2. all 16 warps run A22 -= L21 U12 on DMMA (res_bulk); the tiles that form panel s+1 (A22's first nb
+//      columns) and A12(s+1) (its first rows) go straight into the other smem buffers instead of global,
+//      with step s+1's new band entries, so the next step starts without staging;
+//   3. warp 0 factors panel s+1's diagonal block while warps 1-15 store this step's panel and U12 to
+//      global (evict-first) and L2-prefetch the band entries step s+1 meets first.
+// Every element receives its updates in the reference's column order (FMA-contracted; the DMMA k-sum in
+// groups of 4: the SURVEY §8c tolerances). The A22 tiles round-trip through L2 with an evict_last policy.
+// Shared-memory pair load kept in program order (volatile): stops the compiler from hoisting a whole
+// unrolled panel's operand loads to the top (register spills).
+__device__ __forceinline__ double2 lds2(const double* p) {
+    double2 v;
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
 }
 
-// The rest of sub-panel [q0, q0+8) once its diagonal block is factored (all 512 threads):
-//   rows:    threads 0-255 own panel rows r >= q0+8: x_c = (a_c - sum x_j u_jc) * (1/p_c) over the
-//            sub-panel's columns, then (after the barrier) the rank-8 update of their panel columns >= q0+8;
-//   columns: threads 256-511 own the sub-panel's U rows in panel columns >= q0+8 and in A12: the unit-lower
-//            solve, then (A12 columns) the rank-8 update of A12 rows [q0+8, nb).
-// Per element the updates arrive in ascending column order with the same FMAs as pg_col / pg_u12.
-template <bool FULL>
-__device__ __noinline__ void res_sub(double* __restrict__ P, double* __restrict__ A, int pld, int uld, int q0, int nq_rt,
-                                     int nb, int ph, int R, double* __restrict__ s_rcp, int step, double bv,
-                                     int* boost_ctr) {
-    const int nq = FULL ? 8 : nq_rt;
-    const int tid = threadIdx.x;
-    const int q1 = q0 + 8;
-    double x[8];
-    const bool rowt = tid < 256;
-    const int r = q1 + tid;  // row threads
-    const int t = tid - 256, npc = max(nb - q1, 0);
-    const bool is_p = t < npc;
-    const int c = is_p ? q1 + t : t - npc;  // column threads: panel column or A12 column
-    const bool act = rowt ? r < ph : (is_p || c < R);
-    if (act) {
-        if (rowt) {
+// Packed U11 rows: row c keeps entries j in [(c + 1) & ~1, B) (its U part plus at most one L entry),
+// 16-byte aligned, 528 doubles in all for B = 32.
+__host__ __device__ constexpr int ut_lo(int c) { return (c + 1) & ~1; }
+__host__ __device__ constexpr int ut_off(int c) { return 32 * c - 2 * (c / 2) * ((c + 1) / 2); }
+static_assert(ut_off(1) == 32 && ut_off(2) == 62 && ut_off(3) == 92 && ut_off(4) == 120, "packed U11 offsets");
+constexpr int kUtSize = ut_off(32);
+
+// 1/p from the MUFU.RCP64H seed and two Newton steps (2^-23 -> 2^-46 -> below one ulp); only ever used
+// through div_rcp's residual correction and the multipliers' FMA updates.
+__device__ __forceinline__ double rcp2(double p) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(p));
+    double e = fma(-p, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-p, r, 1.0);
+    return fma(r, e, r);
+}
+
+template <int B, bool FULL>
+__device__ __noinline__ void panel_diag(double* __restrict__ P, int pld, double* __restrict__ Ut,
+                                        double* __restrict__ s_piv, int nb_rt, double bv, int* boost_ctr) {
+    const int nb = FULL ? B : nb_rt;
+    const int r = threadIdx.x & 31;
+    const bool own = r < nb;
+    double a[B];
 #pragma unroll
-            for (int cc = 0; cc < 8; ++cc) x[cc] = P[(q0 + cc) * pld + r];
+    for (int j = 0; j < B; ++j) a[j] = (own && j < nb) ? P[j * pld + r] : 0.0;
+    // row 0 is final from the start: its owner publishes it (U part) before the first pivot
+    if (r == 0) {
 #pragma unroll
-            for (int cc = 0; cc < 8; ++cc) {
-                if (cc < nq) {
-                    const double l = div_rcp(x[cc], s_rcp[32 + q0 + cc], s_rcp[q0 + cc]);
-                    x[cc] = l;
-#pragma unroll
-                    for (int c2 = cc + 1; c2 < 8; ++c2) x[c2] = fma(-l, P[(q0 + c2) * pld + q0 + cc], x[c2]);
-                }
-            }
-#pragma unroll
-            for (int cc = 0; cc < 8; ++cc) P[(q0 + cc) * pld + r] = x[cc];
-        } else {
-            double* col = is_p ? P + c * pld + q0 : A + q0 * uld + c;
-            const int st = is_p ? 1 : uld;
-#pragma unroll
-            for (int rr = 0; rr < 8; ++rr) x[rr] = col[rr * st];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                if (j < nq) {
-#pragma unroll
-                    for (int rr = j + 1; rr < 8; ++rr) x[rr] = fma(-P[(q0 + j) * pld + q0 + rr], x[j], x[rr]);
-                }
-            }
-#pragma unroll
-            for (int rr = 0; rr < 8; ++rr) col[rr * st] = x[rr];
-        }
+        for (int j = ut_lo(0); j < B; j += 2)
+            *reinterpret_cast<double2*>(Ut + ut_off(0) + j - ut_lo(0)) = make_double2(a[j], a[j + 1]);
     }
-    if (q0 == 0) LU_TRACE(step, 9, threadIdx.x == 0);
-#ifdef SAP_LU_TRACE
-    if (q0 == 0 && step == 8 && blockIdx.x == 0 && (threadIdx.x & 31) == 0) g_lu_wtrace[threadIdx.x >> 5] = clock64();
-#endif
-    __syncthreads();
-    if (q0 == 0) LU_TRACE(step, 7, threadIdx.x == 0);
-    if constexpr (FULL) {
-        // rank-8 updates on DMMA (8 x 8 tiles, two k4 steps): the panel's rows [q1, ph) x columns [q1, nb)
-        // and A12's rows [q1, nb) x columns [0, R). Transposed product as in tile_compute_store:
-        // D^T = C^T - U^T L^T, so each thread's accumulator pair is two adjacent rows of one column.
-        // Work unit = a strip of up to three independent 8 x 8 tiles sharing one operand per k4 step:
-        // a panel row tile across the sub-panel's remaining columns (shared L fragment), or an A12
-        // column tile down its remaining rows (shared U fragment). Warp 0 takes only strip 0 (rows
-        // [q1, q1+8): it holds the next sub-panel's diagonal block) and then factors that block
-        // (res_diag8 by its lane 0) while warps 1..15 finish the other strips.
-        const int lane = tid & 31, warp = tid >> 5, lr = lane >> 2, lc = lane & 3;
-        const int nq8 = (nb - q1) >> 3;  // remaining sub-panel columns / U rows, in tiles (nb == B: exact)
-        const int prt = (ph - q1 + 7) >> 3, act8 = (R + 7) >> 3;
-        const int nw = blockDim.x >> 5;
-        for (int sidx = warp == 0 ? 0 : warp; sidx < prt + act8; sidx += warp == 0 ? prt + act8 : nw - 1) {
-            double c[3][2];
-            if (sidx < prt) {
-                const int i0 = q1 + sidx * 8, il = i0 + lr, ib = i0 + 2 * lc;
+    int boosts = 0;
+    // every lane boosts / inverts its own entry of the next pivot column (branch-free); only the owner's
+    // (lane c) is used (boost rule block_factors.hpp:26-34)
+    auto prep = [&](int c, double& p, double& rcl) {
+        p = a[c];
+        const bool boost = fabs(p) < bv;
+        p = boost ? (p < 0.0 ? -bv : bv) : p;
+        boosts += (boost && r == c) ? 1 : 0;
+        if (r == c) a[c] = p;
+        rcl = rcp2(p);
+    };
+    double pl, rl;
+    prep(0, pl, rl);
+    __syncwarp();
 #pragma unroll
-                for (int jt = 0; jt < 3; ++jt)
-                    if (jt < nq8) {
-                        const double* cp = P + (q1 + jt * 8 + lr) * pld;
-                        c[jt][0] = ib < ph ? cp[ib] : 0.0;
-                        c[jt][1] = ib + 1 < ph ? cp[ib + 1] : 0.0;
-                    }
-#pragma unroll
-                for (int ks = 0; ks < 2; ++ks) {
-                    const int k = ks * 4 + lc;
-                    const double bv8 = il < ph ? -P[(q0 + k) * pld + il] : 0.0;
-#pragma unroll
-                    for (int jt = 0; jt < 3; ++jt)
-                        if (jt < nq8) {
-                            const double av = P[(q1 + jt * 8 + lr) * pld + q0 + k];
-                            dmma_m8n8k4(c[jt][0], c[jt][1], av, bv8, c[jt][0], c[jt][1]);
-                        }
-                }
-#pragma unroll
-                for (int jt = 0; jt < 3; ++jt)
-                    if (jt < nq8) {
-                        double* cp = P + (q1 + jt * 8 + lr) * pld;
-                        if (ib < ph) cp[ib] = c[jt][0];
-                        if (ib + 1 < ph) cp[ib + 1] = c[jt][1];
-                    }
-            } else {
-                const int j = (sidx - prt) * 8 + lr;
-                const bool jok = j < R;
-#pragma unroll
-                for (int it = 0; it < 3; ++it)
-                    if (it < nq8) {
-                        const int ib = q1 + it * 8 + 2 * lc;
-                        c[it][0] = jok ? A[ib * uld + j] : 0.0;
-                        c[it][1] = jok ? A[(ib + 1) * uld + j] : 0.0;
-                    }
-#pragma unroll
-                for (int ks = 0; ks < 2; ++ks) {
-                    const int k = ks * 4 + lc;
-                    const double av = jok ? A[(q0 + k) * uld + j] : 0.0;
-#pragma unroll
-                    for (int it = 0; it < 3; ++it)
-                        if (it < nq8) {
-                            const double bv8 = -P[(q0 + k) * pld + q1 + it * 8 + lr];
-                            dmma_m8n8k4(c[it][0], c[it][1], av, bv8, c[it][0], c[it][1]);
-                        }
-                }
-                if (jok) {
-#pragma unroll
-                    for (int it = 0; it < 3; ++it)
-                        if (it < nq8) {
-                            const int ib = q1 + it * 8 + 2 * lc;
-                            A[ib * uld + j] = c[it][0];
-                            A[(ib + 1) * uld + j] = c[it][1];
-                        }
-                }
+    for (int c = 0; c < B; ++c) {
+        if (FULL || c < nb) {
+            // pivot row c, published by its owner at the end of the previous round: the pair holding entry
+            // c + 1 (the next pivot column) first
+            const double* __restrict__ urow = Ut + ut_off(c) - ut_lo(c);  // urow[j] = U(c, j), j >= ut_lo(c)
+            const double2 un2 = c + 1 < B ? lds2(urow + ((c + 1) & ~1)) : make_double2(0.0, 0.0);
+            const double pc = __shfl_sync(0xffffffffu, pl, c);
+            const double rc = __shfl_sync(0xffffffffu, rl, c);
+            if (r == c) {
+                s_piv[c] = pc;
+                s_piv[B + c] = rc;
             }
-        }
-        if (warp == 0 && nq8 > 0) {
+            // rows below: multiplier (block_factors.hpp:36) and rank-1 update; other lanes apply l = 0 (rows
+            // above stay as they are for finite pivot rows, the only kind a finite band produces)
+            const bool below = own && r > c;
+            const double lq = div_rcp(a[c], pc, rc);
+            const double l = below ? lq : 0.0;
+            a[c] = below ? lq : a[c];
+            if (own) P[c * pld + r] = a[c];  // column c of L11\U11 is final
+            if (c + 1 < B) {
+                // the next pivot column first, so its reciprocal overlaps the rest of the row update
+                if (c & 1) {  // pair (c + 1, c + 2)
+                    a[c + 1] = fma(-l, un2.x, a[c + 1]);
+                    if (c + 2 < B) a[c + 2] = fma(-l, un2.y, a[c + 2]);
+                } else {  // pair (c, c + 1)
+                    a[c + 1] = fma(-l, un2.y, a[c + 1]);
+                }
+                if (FULL || c + 1 < nb) prep(c + 1, pl, rl);
+            }
+            // the remaining pairs, four at a time (bounded register footprint)
+            constexpr int kChunk = 8;
+#pragma unroll
+            for (int j0 = (c & 1) ? c + 3 : c + 2; j0 < B; j0 += kChunk) {
+                double2 uu[kChunk / 2];
+#pragma unroll
+                for (int q = 0; q < kChunk / 2; ++q)
+                    if (j0 + 2 * q < B) uu[q] = lds2(urow + j0 + 2 * q);
+#pragma unroll
+                for (int q = 0; q < kChunk / 2; ++q)
+                    if (j0 + 2 * q < B) {
+                        a[j0 + 2 * q] = fma(-l, uu[q].x, a[j0 + 2 * q]);
+                        a[j0 + 2 * q + 1] = fma(-l, uu[q].y, a[j0 + 2 * q + 1]);
+                    }
+            }
+            // row c + 1 is final now: its owner publishes it for the next round
+            if (c + 1 < B && r == c + 1) {
+#pragma unroll
+                for (int j = ut_lo(c + 1); j < B; j += 2)
+                    *reinterpret_cast<double2*>(Ut + ut_off(c + 1) + j - ut_lo(c + 1)) = make_double2(a[j], a[j + 1]);
+            }
             __syncwarp();
-            if (lane == 0) res_diag8<true>(P, pld, bv, q1, 8, s_rcp, boost_ctr);
         }
-        return;
     }
-    if (!act) return;
-    if (rowt) {
-        // panel row r, columns [q1, nb) (nb - q1 is a multiple of 8 whenever nb == B): four independent
-        // accumulators per pass, the sub-panel's U rows read as 16-byte pairs
-        for (int cc0 = q1; cc0 < nb; cc0 += 4) {
-            double acc[4];
-            double u[4][8];
+    if (boosts) atomicAdd(boost_ctr, boosts);
+}
+
+template <int B, bool FULL>
+__device__ __noinline__ void panel_rows_cols(double* __restrict__ P, double* __restrict__ A, int pld, int uld,
+                                             const double* __restrict__ Ut, const double* __restrict__ s_piv,
+                                             int nb_rt, int ph, int R) {
+    const int nb = FULL ? B : nb_rt;
+    const int tid = threadIdx.x;
+    if (tid < 256) {
+        const int r = nb + tid;
+        if (r >= ph) return;
+        double x[B];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int cc = min(cc0 + k, nb - 1);
-                acc[k] = P[cc * pld + r];
-                const double2* up = reinterpret_cast<const double2*>(P + cc * pld + q0);
+        for (int c = 0; c < B; ++c) x[c] = c < nb ? P[c * pld + r] : 0.0;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const double2 v = up[j];
-                    u[k][2 * j] = v.x;
-                    u[k][2 * j + 1] = v.y;
+        for (int c = 0; c < B; ++c) {
+            if (c < nb) {
+                const double l = div_rcp(x[c], s_piv[c], s_piv[B + c]);
+                x[c] = l;
+                const double2* __restrict__ u2 = reinterpret_cast<const double2*>(Ut + ut_off(c) - ut_lo(c));
+#pragma unroll
+                for (int j = (c + 1) & ~1; j < B; j += 2) {
+                    const double2 u = lds2(reinterpret_cast<const double*>(u2 + (j >> 1)));
+                    if (j > c) x[j] = fma(-l, u.x, x[j]);
+                    x[j + 1] = fma(-l, u.y, x[j + 1]);
                 }
             }
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-                if (j < nq) {
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) acc[k] = fma(-x[j], u[k][j], acc[k]);
-                }
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if (cc0 + k < nb) P[(cc0 + k) * pld + r] = acc[k];
         }
-    } else if (!is_p) {
-        // A12 column c, rows [q1, nb): the L21 entries of four rows as 16-byte pairs
-        for (int rr0 = q1; rr0 < nb; rr0 += 4) {
-            double acc[4];
-            double lv[8][4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) acc[k] = A[min(rr0 + k, nb - 1) * uld + c];
+        for (int c = 0; c < B; ++c)
+            if (c < nb) P[c * pld + r] = x[c];
+    } else {
+        const int col = tid - 256;
+        if (col >= R) return;
+        double y[B];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const double2* lp = reinterpret_cast<const double2*>(P + (q0 + j) * pld + rr0);
-                const double2 v0 = lp[0], v1 = lp[1];
-                lv[j][0] = v0.x;
-                lv[j][1] = v0.y;
-                lv[j][2] = v1.x;
-                lv[j][3] = v1.y;
+        for (int q = 0; q < B; ++q) y[q] = q < nb ? A[q * uld + col] : 0.0;
+#pragma unroll
+        for (int c = 0; c < B; ++c) {
+            if (c < nb) {
+                const double2* __restrict__ l2 = reinterpret_cast<const double2*>(P + c * pld);
+#pragma unroll
+                for (int q = (c + 1) & ~1; q < B; q += 2) {
+                    const double2 l = lds2(reinterpret_cast<const double*>(l2 + (q >> 1)));
+                    if (q > c) y[q] = fma(-l.x, y[c], y[q]);
+                    y[q + 1] = fma(-l.y, y[c], y[q + 1]);
+                }
             }
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-                if (j < nq) {
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) acc[k] = fma(-lv[j][k], x[j], acc[k]);
-                }
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if (rr0 + k < nb) A[(rr0 + k) * uld + c] = acc[k];
         }
+#pragma unroll
+        for (int q = 0; q < B; ++q)
+            if (q < nb) A[q * uld + col] = y[q];
     }
 }
 
@@ -731,15 +683,6 @@ __device__ __forceinline__ void prefetch_run(const Lu& L, int c, int r0, int r1)
     uintptr_t hi = (reinterpret_cast<uintptr_t>(a) + 8 * (r1 - r0) + 15) & ~uintptr_t(15);
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"((unsigned)(hi - lo)) : "memory");
 }
-__device__ __forceinline__ void prefetch_fresh(const Lu& L, int ja, int R, int nb) {
-    const int e = ja + R;  // first row/column the next step sees fresh
-    if (e >= L.m) return;
-    const int t = threadIdx.x;
-    const int ncol = min(e + nb, L.m) - ja;  // columns [ja, e+nb): their rows [e, e+nb)
-    if (t < ncol) prefetch_run(L, ja + t, e, e + nb);
-    const int t2 = t - ncol;                 // columns [e, e+nb): rows [ja+nb, e)
-    if (t2 >= 0 && t2 < min(nb, L.m - e)) prefetch_run(L, e + t2, ja + nb, e);
-}
 
 // tile_load for k_band_lu_res: A22 entries at window coordinates (i, c) with i >= fr or c >= fr have never
 // been updated (they entered the window this step) and come from the unfactored source view; the rest
@@ -767,7 +710,7 @@ __device__ __forceinline__ void tile_load_fr(const Lu& L, const TileCtx& T, int 
 #pragma unroll
             for (int q = 0; q < kTQ; ++q) {
                 const bool fresh = ib + a * 8 >= fr || cb + q * 8 >= fr;
-                const double2 v = __ldcg(reinterpret_cast<const double2*>((fresh ? slo : dlo) + a * ra8 + q * cq8));
+                const double2 v = ld_keep2((fresh ? slo : dlo) + a * ra8 + q * cq8);
                 acc[a][q][0] = rs > 0 ? v.x : v.y;
                 acc[a][q][1] = rs > 0 ? v.y : v.x;
             }
@@ -781,7 +724,7 @@ __device__ __forceinline__ void tile_load_fr(const Lu& L, const TileCtx& T, int 
             for (int e = 0; e < 2; ++e) {
                 const int i = ib + a * 8 + e, c = cb + q * 8;
                 const long long o = a * ra8 + e * rs + q * cq8;
-                acc[a][q][e] = tile_ok(L, T, i, c) ? __ldcg((i >= fr || c >= fr ? s00 : d00) + o) : 0.0;
+                acc[a][q][e] = tile_ok(L, T, i, c) ? ld_keep((i >= fr || c >= fr ? s00 : d00) + o) : 0.0;
             }
 }
 
@@ -809,10 +752,10 @@ __device__ __noinline__ void res_bulk(const Lu& L, const double* __restrict__ P,
             pf[i] = 0.0;
             if (f < 32) {  // panel column f, row R + lane
                 const int r = R + lane;
-                if (f < nbn && r < phn && r - f <= L.K) pf[i] = __ldcg(L.src_at(ja + r, ja + f));
+                if (f < nbn && r < phn && r - f <= L.K) pf[i] = __ldcs(L.src_at(ja + r, ja + f));
             } else if (f < 64) {  // A12 column R - nbn + (f - 32), row lane
                 const int c = R - nbn + (f - 32);
-                if (c < Rn && lane < nbn && nbn + c - lane <= L.K) pf[i] = __ldcg(L.src_at(ja + lane, ja + nbn + c));
+                if (c < Rn && lane < nbn && nbn + c - lane <= L.K) pf[i] = __ldcs(L.src_at(ja + lane, ja + nbn + c));
             }
         }
     }
@@ -888,7 +831,7 @@ __device__ __noinline__ void res_bulk(const Lu& L, const double* __restrict__ P,
                             double2 v;
                             v.x = rs > 0 ? acc[a][q][0] : acc[a][q][1];
                             v.y = rs > 0 ? acc[a][q][1] : acc[a][q][0];
-                            __stcg(reinterpret_cast<double2*>(lo00 + a * ra8 + q * cq8), v);
+                            st_keep2(lo00 + a * ra8 + q * cq8, v);
                         }
                 } else {
 #pragma unroll
@@ -898,7 +841,7 @@ __device__ __noinline__ void res_bulk(const Lu& L, const double* __restrict__ P,
 #pragma unroll
                             for (int e = 0; e < 2; ++e) {
                                 const int i = ib + a * 8 + e, c = cb + q * 8;
-                                if (i < R && c < R) __stcg(p00 + a * ra8 + e * rs + q * cq8, acc[a][q][e]);
+                                if (i < R && c < R) st_keep(p00 + a * ra8 + e * rs + q * cq8, acc[a][q][e]);
                             }
                 }
             } else if (nbn == kTileC && row0 + kTileR <= R && col0 + kTileC <= R &&
@@ -935,7 +878,7 @@ __device__ __noinline__ void res_bulk(const Lu& L, const double* __restrict__ P,
                             else if (i < nbn)
                                 An[i * uld + (c - nbn)] = acc[a][q][e];
                             else
-                                __stcg(L.at(ja + i, ja + c), acc[a][q][e]);
+                                st_keep(L.at(ja + i, ja + c), acc[a][q][e]);
                         }
             }
         }
@@ -963,6 +906,8 @@ __global__ void __launch_bounds__(kLuThreads, 1)
     k_band_lu_res(const FactorJob* __restrict__ jobs, double eps, int pld, int uld) {
     extern __shared__ __align__(16) double smem[];
     __shared__ int s_boosts;
+    static_assert(B == 32, "packed U11 rows (kUtSize) assume B = 32");
+    __shared__ __align__(16) double s_ut[kUtSize];  // packed U11 rows of the current panel
     __shared__ double s_rcp[2 * B];  // [0, B): 1/p, [B, 2B): p
     const FactorJob J = jobs[blockIdx.x];
     if (!STREAM && J.gate && !(*J.gate & 1)) return;  // streamed setup: no pivot fell below the threshold
@@ -1017,6 +962,13 @@ __global__ void __launch_bounds__(kLuThreads, 1)
         const int nb = min(B, m), ph = min(nb + K, m), R = min(K, m - nb);
         res_fetch(L, smem, smem + 2 * psz, 0, nb, 0, ph, R, 0, kLuThreads);
         cp_async_wait_all();
+        __syncthreads();
+        if (warp == 0) {
+            if (nb == B)
+                panel_diag<B, true>(smem, pld, s_ut, s_rcp, nb, L.bv, &s_boosts);
+            else
+                panel_diag<B, false>(smem, pld, s_ut, s_rcp, nb, L.bv, &s_boosts);
+        }
     }
     __syncthreads();
     int cur = 0, step = 0;
@@ -1035,59 +987,71 @@ __global__ void __launch_bounds__(kLuThreads, 1)
         double* An = smem + 2 * psz + (cur ^ 1) * usz;
         wait_cols(jb + 3 * B + K);
         LU_TRACE(step, 0, tid == 0);
-        // 1-2. blocked panel + U12: per 8-column sub-panel, the diagonal block (one thread) then the L rows,
-        //      U rows and rank-8 updates (all threads); warps 8-15 prefetch step s+1's new band entries meanwhile
-        if (nb == B) {
-            // full panel: diagonal block 0 here, every later one inside the previous res_sub (overlapped)
-            if (tid == 0) res_diag8<true>(P, pld, L.bv, 0, 8, s_rcp, &s_boosts);
-            __syncthreads();
-            LU_TRACE(step, 5, tid == 0);
-            for (int q0 = 0; q0 < nb; q0 += 8) {
-                res_sub<true>(P, A, pld, uld, q0, 8, nb, ph, R, s_rcp, step, L.bv, &s_boosts);
-                __syncthreads();
-                if (q0 == 0) LU_TRACE(step, 6, tid == 0);
+        // 1-2. panel + U12: the diagonal block was factored by warp 0 during the previous step's update (or
+        //      the prologue); here all threads finish L21 rows / U12 columns
+        if (nb == B)
+            panel_rows_cols<B, true>(P, A, pld, uld, s_ut, s_rcp, nb, ph, R);
+        else
+            panel_rows_cols<B, false>(P, A, pld, uld, s_ut, s_rcp, nb, ph, R);
+        __syncthreads();
+        LU_TRACE(step, 3, tid == 0);
+        // 3. trailing update (next panel / A12 land in smem) + step s+1's new band entries; window entries at
+        //    or beyond the previous step's window edge (jb + min(K, m - jb)) are fresh
+        const int fr = jb == 0 ? 0 : min(K, m - jb) - nb;
+        res_bulk(L, P, A, nb, ja, R, nbn, phn, Rn, Pn, An, fr, step);
+        cp_async_wait_all();
+        __syncthreads();
+        LU_TRACE(step, 7, tid == 0);
+        // 4. warp 0: the next panel's diagonal block (one warp's pivot chain); warps 1-15 meanwhile store this
+        //    step's panel (L11\U11, L21) and U12 (warp per column, lanes down the rows; P, A are intact) and
+        //    L2-prefetch the next step's new band entries
+        if (warp == 0) {
+            if (has_next) {
+                if (nbn == B)
+                    panel_diag<B, true>(Pn, pld, s_ut, s_rcp, nbn, L.bv, &s_boosts);
+                else
+                    panel_diag<B, false>(Pn, pld, s_ut, s_rcp, nbn, L.bv, &s_boosts);
             }
         } else {
-            for (int q0 = 0; q0 < nb; q0 += 8) {
-                const int nq = min(8, nb - q0);
-                if (tid == 0) res_diag8<false>(P, pld, L.bv, q0, nq, s_rcp, &s_boosts);
-                __syncthreads();
-                res_sub<false>(P, A, pld, uld, q0, nq, nb, ph, R, s_rcp, step, L.bv, &s_boosts);
-                __syncthreads();
-            }
-        }
-        LU_TRACE(step, 3, tid == 0);
-        if (ja < m) prefetch_fresh(L, ja, R, nb);
-        // 3. panel (L11\U11, L21) and U12 to global: a warp per column, lanes down the rows
-        {
-            const int lane = tid & 31;
+            const int lane = tid & 31, w1 = warp - 1, nw1 = kLuThreads / 32 - 1;
             const long long rs = L.rs;
-            for (int c = warp; c < nb; c += kLuThreads / 32) {
+            for (int c = w1; c < nb; c += nw1) {
                 double* g = L.at(jb, jb + c);
                 const int r1 = min(ph, c + K + 1);
 #pragma unroll 4
-                for (int r = max(c - K, 0) + lane; r < r1; r += 32) __stcg(g + r * rs, P[c * pld + r]);
+                for (int r = max(c - K, 0) + lane; r < r1; r += 32) __stcs(g + r * rs, P[c * pld + r]);
             }
             if (lane < nb) {
                 double* g = L.at(jb + lane, ja);
                 const long long cs = L.cs;
 #pragma unroll 4
-                for (int c = warp; c < R; c += kLuThreads / 32)
-                    if (nb + c - lane <= K) __stcg(g + c * cs, A[lane * uld + c]);
+                for (int c = w1; c < R; c += nw1)
+                    if (nb + c - lane <= K) __stcs(g + c * cs, A[lane * uld + c]);
+            }
+            if (ja < m && ja + R < m) {
+                // prefetch_fresh's runs over warps 1-15
+                const int e = ja + R, t1 = tid - 32;
+                const int ncol = min(e + nbn, m) - ja;
+                for (int t = t1; t < ncol + min(nbn, m - e); t += kLuThreads - 32) {
+                    if (t < ncol)
+                        prefetch_run(L, ja + t, e, e + nbn);
+                    else
+                        prefetch_run(L, e + t - ncol, ja + nbn, e);
+                }
             }
         }
-        LU_TRACE(step, 4, tid == 0);
-        // 4. trailing update (next panel / A12 land in smem) + step s+1's new band entries
-        // window entries at or beyond the previous step's window edge (jb + min(K, m - jb)) are fresh
-        res_bulk(L, P, A, nb, ja, R, nbn, phn, Rn, Pn, An, jb == 0 ? 0 : min(K, m - jb) - nb, step);
         cp_async_wait_all();
-        LU_TRACE(step, 8, tid == 0);
+        LU_TRACE(step, 8, tid == 32);
         __syncthreads();
         cur ^= 1;
     }
     if (tid == 0) *J.boosts = s_boosts;
     if (STREAM && tid == 0 && s_timeout) *J.minpiv = -1.0;  // min |pivot| is read off U's diagonal afterwards
 }
+
+// dynamic shared memory of k_band_lu_res: 227 KB per block minus its static arrays (packed U11 rows,
+// pivots, counters)
+constexpr size_t kResSmemMax = 227 * 1024 - sizeof(double) * (kUtSize + 64) - 64;
 
 static int pad_ld(int x) {
     // leading dimensions == 4 or 12 (mod 16) keep the DMMA fragment loads conflict-free
@@ -1109,7 +1073,7 @@ bool launch_band_lu_ws(const FactorJob* d_jobs, int njobs, int max_k, double eps
         const int pldr = pad_ld(B + max_k);
         const int uldr = pad_ld(max_k);
         const size_t rbytes = sizeof(double) * (size_t)(2 * B * pldr + 2 * B * uldr);
-        if (rbytes <= 226 * 1024) {
+        if (rbytes <= kResSmemMax) {
             if (streamed) {
                 SAP_CUDA(cudaFuncSetAttribute(k_band_lu_res<B, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               (int)rbytes));
@@ -1141,7 +1105,7 @@ bool band_lu_reads_source(int max_k) {
     constexpr int B = 32;
     if (max_k < 1 || max_k > 256 - B) return false;
     const int pldr = pad_ld(B + max_k), uldr = pad_ld(max_k);
-    return sizeof(double) * (size_t)(2 * B * pldr + 2 * B * uldr) <= 226 * 1024;
+    return sizeof(double) * (size_t)(2 * B * pldr + 2 * B * uldr) <= kResSmemMax;
 }
 
 }  // namespace sapgpu

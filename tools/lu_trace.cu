@@ -15,7 +15,7 @@ int main(int argc, char** argv) {
     printf("t_factor_kernel %.3f ms\n", r.t_factor_kernel * 1e3);
     long long t[16 * 12];
     sapgpu::read_lu_trace(t);
-    const char* names[] = {"S0", "S1", "staged", "factored", "stored", "q0diag", "q0sub", "q0A2bar", "UGbulk", "q0A2"};
+    const char* names[] = {"S0", "S1", "prefetched", "rowscols", "stored", "diag_next", "q0sub", "phase1", "phase2", "q0A2"};
     for (int s = 0; s < 15; ++s) {
         long long b = t[s * 12];
         printf("step %2d:", s);
