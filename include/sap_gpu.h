@@ -252,6 +252,17 @@ typedef struct sap_comm {
                     double* recv_left, int n_rl, double* recv_right, int n_rr);
 } sap_comm;
 
+/* Native NCCL data plane (one process per GPU): the library opens libnccl.so.2 itself and runs every
+ * neighbour exchange (spike tips at setup, interface rows per preconditioner apply, the k-row operator
+ * halo) as grouped ncclSend / ncclRecv on the handle's stream and every Krylov dot as an ncclAllReduce on
+ * the device scalar -- no callbacks, no host staging, no stream synchronisation per exchange.
+ * Rank 0 calls sap_nccl_get_unique_id; the 128 id bytes reach every rank out of band (torch.distributed,
+ * MPI, a file); then every rank calls sap_create_distributed_nccl (collective) with its CUDA device in
+ * opts->device. Setup / apply / solve are the same calls as for sap_create_distributed. */
+sap_status sap_nccl_get_unique_id(unsigned char id[128]);
+sap_status sap_create_distributed_nccl(const sap_options* opts, const unsigned char id[128], int rank, int world,
+                                       sap_handle** out);
+
 /* Rank r's row range under the SURVEY §8e assignment: partitions
  * [r*p/world, (r+1)*p/world) of make_partition_layout(n, p, k). */
 sap_status sap_rank_rows(int n, int p, int k, int rank, int world, int* row_lo, int* row_hi);

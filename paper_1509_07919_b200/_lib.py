@@ -74,6 +74,8 @@ SIGNATURES = {
     "sap_get_full_spike": (C.c_int, [_vp, C.c_int, _vp, _vp]),
     "sap_rank_rows": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _ip, _ip]),
     "sap_create_distributed": (C.c_int, [C.POINTER(sap_options), C.POINTER(sap_comm), C.POINTER(_vp)]),
+    "sap_nccl_get_unique_id": (C.c_int, [_vp]),
+    "sap_create_distributed_nccl": (C.c_int, [C.POINTER(sap_options), _vp, C.c_int, C.c_int, C.POINTER(_vp)]),
     "sap_setup_banded_dist": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp, C.c_int]),
 }
 

@@ -16,6 +16,7 @@
 #include "../../include/sap_gpu.h"
 #include "common.cuh"
 #include "kernels.h"
+#include "comm_nccl.h"
 #include "krylov.h"
 
 using namespace sapgpu;
@@ -145,6 +146,8 @@ struct sap_handle {
     // [left cross?, local 0..p_loc-2, right cross?]; cross interfaces are solved on both ranks.
     bool dist = false;
     sap_comm comm{};
+    NcclComm* nccl = nullptr;  // native data plane (sap_create_distributed_nccl); else the comm callbacks
+    DevBuf<double> dred;       // device staging of host-side reductions over NCCL
     Layout glayout;
     int n_glob = 0, row_lo = 0, row_hi = 0, c_lo = 0, c_hi = 0, pb = 0, pe = 0, ni_tot = 0;
     bool has_left = false, has_right = false;
@@ -848,18 +851,36 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
 // g = D^{-1} in each way and no second round. The operator exchanges a k-row halo each way;
 // Krylov dots are summed over ranks.
 
-void comm_exchange(sap_handle* h, const double* sl, const double* sr, double* rl, double* rr, int count) {
-    if (count == 0 || h->comm.world <= 1) return;
+// Neighbour exchange of device buffers (counts may be 0). NCCL: grouped send / recv on the handle's stream,
+// stream-ordered with the kernels around it (no host synchronisation). Callbacks: the stream is synchronised
+// first and the callback completes the transfer before returning.
+void comm_exchange_raw(sap_handle* h, const double* sl, int n_sl, const double* sr, int n_sr, double* rl, int n_rl,
+                       double* rr, int n_rr) {
+    if (h->comm.world <= 1) return;
+    if (h->nccl) return nccl_exchange(h->nccl, sl, n_sl, sr, n_sr, rl, n_rl, rr, n_rr, h->stream);
     SAP_CUDA(cudaStreamSynchronize(h->stream));
-    const int rc = h->comm.exchange(h->comm.ctx, h->has_left ? sl : nullptr, h->has_left ? count : 0,
-                                    h->has_right ? sr : nullptr, h->has_right ? count : 0,
-                                    h->has_left ? rl : nullptr, h->has_left ? count : 0,
-                                    h->has_right ? rr : nullptr, h->has_right ? count : 0);
+    const int rc = h->comm.exchange(h->comm.ctx, sl, n_sl, sr, n_sr, rl, n_rl, rr, n_rr);
     if (rc != 0) throw CommFailure("sap: neighbour exchange failed (" + std::to_string(rc) + ")");
 }
 
+void comm_exchange(sap_handle* h, const double* sl, const double* sr, double* rl, double* rr, int count) {
+    if (count == 0) return;
+    comm_exchange_raw(h, h->has_left ? sl : nullptr, h->has_left ? count : 0, h->has_right ? sr : nullptr,
+                      h->has_right ? count : 0, h->has_left ? rl : nullptr, h->has_left ? count : 0,
+                      h->has_right ? rr : nullptr, h->has_right ? count : 0);
+}
+
+// In-place sum over ranks of `count` HOST doubles (setup flags, Krylov failure flags).
 void comm_allreduce(sap_handle* h, double* v, int count) {
     if (h->comm.world <= 1 || count == 0) return;
+    if (h->nccl) {
+        h->dred.alloc(std::max(count, 16));
+        SAP_CUDA(cudaMemcpyAsync(h->dred.get(), v, sizeof(double) * count, cudaMemcpyHostToDevice, h->stream));
+        nccl_allreduce(h->nccl, h->dred.get(), count, h->stream);
+        SAP_CUDA(cudaMemcpyAsync(v, h->dred.get(), sizeof(double) * count, cudaMemcpyDeviceToHost, h->stream));
+        SAP_CUDA(cudaStreamSynchronize(h->stream));
+        return;
+    }
     const int rc = h->comm.allreduce_sum(h->comm.ctx, v, count);
     if (rc != 0) throw CommFailure("sap: allreduce failed (" + std::to_string(rc) + ")");
 }
@@ -1095,13 +1116,10 @@ void setup_banded_dist(sap_handle* h, int n, int k, int row_lo, int row_hi, cons
         SAP_CUDA(cudaMemcpyAsync(h->tipjobs.get(), tj.data(), sizeof(TipJob) * tj.size(), cudaMemcpyHostToDevice, s));
         launch_spike_tips(h->tipjobs.get(), (int)tj.size(), k, h->nonfinite.get(), s);
         if (h->comm.world > 1) {
-            const size_t cnt = ww;
-            SAP_CUDA(cudaStreamSynchronize(s));
-            const int rcode = h->comm.exchange(
-                h->comm.ctx, lc ? h->wt.get() : nullptr, lc ? (int)cnt : 0,
-                rc ? h->vb.get() + (ni - 1) * ww : nullptr, rc ? (int)cnt : 0, lc ? h->vb.get() : nullptr,
-                lc ? (int)cnt : 0, rc ? h->wt.get() + (ni - 1) * ww : nullptr, rc ? (int)cnt : 0);
-            if (rcode != 0) throw CommFailure("sap: spike tip exchange failed (" + std::to_string(rcode) + ")");
+            const int cnt = (int)ww;
+            comm_exchange_raw(h, lc ? h->wt.get() : nullptr, lc ? cnt : 0, rc ? h->vb.get() + (ni - 1) * ww : nullptr,
+                              rc ? cnt : 0, lc ? h->vb.get() : nullptr, lc ? cnt : 0,
+                              rc ? h->wt.get() + (ni - 1) * ww : nullptr, rc ? cnt : 0);
         }
         SAP_CUDA(cudaEventRecord(h->ev[4], s));
         // T_LUrdcd: every slot's R̄ (cross ones on both ranks)
@@ -1290,6 +1308,7 @@ void sap_destroy(sap_handle* h) {
     if (h->prio) cudaStreamDestroy(h->prio);
     if (h->pev) cudaEventDestroy(h->pev);
     if (h->own_stream) cudaStreamDestroy(h->own_stream);
+    nccl_destroy(h->nccl);
     delete h;
 }
 
@@ -1339,6 +1358,36 @@ sap_status sap_create_distributed(const sap_options* opts, const sap_comm* comm,
         if (st != SAP_OK) throw InvalidArgument(g_last_error);
         (*out)->dist = true;
         (*out)->comm = *comm;
+    });
+}
+
+sap_status sap_nccl_get_unique_id(unsigned char* id) {
+    return guard([&] {
+        require(id != nullptr, "sap_nccl_get_unique_id: null argument");
+        nccl_unique_id(id);
+    });
+}
+
+sap_status sap_create_distributed_nccl(const sap_options* opts, const unsigned char* id, int rank, int world,
+                                       sap_handle** out) {
+    return guard([&] {
+        require(id != nullptr && out != nullptr, "sap_create_distributed_nccl: null argument");
+        require(world >= 1 && rank >= 0 && rank < world, "sap_create_distributed_nccl: rank out of range");
+        const sap_status st = sap_create(opts, out);
+        if (st != SAP_OK) throw InvalidArgument(g_last_error);
+        sap_handle* h = *out;
+        h->dist = true;
+        h->comm = sap_comm{};
+        h->comm.rank = rank;
+        h->comm.world = world;
+        try {
+            SAP_CUDA(cudaSetDevice(h->opt.device));
+            h->nccl = nccl_create(id, rank, world);
+        } catch (...) {
+            sap_destroy(h);
+            *out = nullptr;
+            throw;
+        }
     });
 }
 
@@ -1512,6 +1561,8 @@ sap_status sap_solve(sap_handle* h, const double* b, double* x, int on_device, s
         kc.zero_guess_exact = h->op_finite && !h->csr && !h->dist;
         if (h->dist && h->comm.world > 1) {
             kc.reduce = [h](double* v, int c) { comm_allreduce(h, v, c); };
+            if (h->nccl)  // dot products reduced on the device before their one copy to the host
+                kc.dreduce = [h](double* d, int c, cudaStream_t st) { nccl_allreduce(h->nccl, d, c, st); };
             kc.row_offset = h->row_lo;
         }
         DeviceOp A = [h](const double* in, double* out) { apply_a(h, in, out); };

@@ -129,9 +129,10 @@ void KrylovSolver::ensure(int n, int ell) {
 
 double KrylovSolver::dot(const double* a, const double* b) {
     launch_dot(a, b, n_, partials_, counter_, dscal_, s_);
+    if (dreduce_) dreduce_(dscal_, 1, s_);
     SAP_CUDA(cudaMemcpyAsync(hpinned_, dscal_, sizeof(double), cudaMemcpyDeviceToHost, s_));
     SAP_CUDA(cudaStreamSynchronize(s_));
-    if (reduce_) reduce_(hpinned_, 1);
+    if (reduce_ && !dreduce_) reduce_(hpinned_, 1);
     return hpinned_[0];
 }
 
@@ -154,6 +155,7 @@ KrylovResult KrylovSolver::run(const DeviceOp& A, const DeviceOp& M, const doubl
                                const KrylovConfig& cfg, cudaStream_t s) {
     s_ = s;
     reduce_ = cfg.reduce;
+    dreduce_ = cfg.dreduce;
     int method = cfg.method;
     if (method == 2) method = cfg.caller_asserts_spd ? 1 : 0;  // run_krylov dispatch (krylov.hpp:437-441)
     if (method == 0) {

@@ -32,6 +32,9 @@ struct KrylovConfig {
     // multi-GPU: in-place sum over ranks of host doubles (null = single rank), and the
     // global index of this rank's first row (for the restart perturbation stream)
     std::function<void(double*, int)> reduce;
+    // multi-GPU over NCCL: in-place sum over ranks of device doubles on the solver's stream; when set, dot
+    // products are reduced on the device before their single device->host copy
+    std::function<void(double*, int, cudaStream_t)> dreduce;
     long long row_offset = 0;
     // the operator has only finite entries (checked at setup): with the zero initial guess the first
     // residual b - A*0 is b exactly (every row sum of a*(+0) terms is +0), so the first A apply is skipped
@@ -59,6 +62,7 @@ private:
 
     int n_ = 0, ell_ = 0;
     std::function<void(double*, int)> reduce_;
+    std::function<void(double*, int, cudaStream_t)> dreduce_;
     cudaStream_t s_ = nullptr;
     double* buf_ = nullptr;       // all vectors
     double* partials_ = nullptr;  // reduction partials

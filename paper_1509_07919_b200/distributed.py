@@ -10,7 +10,12 @@ every operator apply one k-row halo exchange, and every Krylov reduction a
 scalar allreduce (the reference's single-process spike.hpp:304-351 /
 krylov.hpp:110-442 data flow, cut at partition boundaries).
 
-``TorchComm`` supplies the ``sap_comm`` callbacks of include/sap_gpu.h:
+``NcclComm`` selects the library's native data plane (``sap_create_distributed_nccl``): grouped
+ncclSend / ncclRecv on the handle's stream for every exchange and device-side ncclAllReduce for the Krylov
+dots, no Python on the data path; the torch.distributed group only carries the 128-byte NCCL id once.
+
+``TorchComm`` supplies the ``sap_comm`` callbacks of include/sap_gpu.h instead (the CPU tests and the
+several-ranks-on-one-GPU GPU tests, where NCCL cannot run):
 
 * backend ``nccl``: device buffers are sent as-is (``batch_isend_irecv``),
 * backend ``gloo``: device buffers are staged through host tensors — the way
@@ -132,6 +137,28 @@ class TorchComm:
             return 1
 
 
+class NcclComm:
+    """The library's own NCCL communicator (one process per GPU). Collective: every rank of `group`
+    constructs it; rank 0's ``sap_nccl_get_unique_id`` reaches the others through torch.distributed."""
+
+    def __init__(self, group=None):
+        import torch
+        import torch.distributed as dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.error: BaseException | None = None
+        uid = np.zeros(128, np.uint8)
+        if self.rank == 0:
+            _check(L.load().sap_nccl_get_unique_id(uid.ctypes.data))
+        t = torch.from_numpy(uid)
+        if str(dist.get_backend(group)) == "nccl":
+            t = t.to(f"cuda:{torch.cuda.current_device()}")
+        src = 0 if group is None else dist.get_global_rank(group, 0)
+        dist.broadcast(t, src=src, group=group)
+        self.uid = np.ascontiguousarray(t.cpu().numpy(), np.uint8)
+
+
 class DistributedSolver(Solver):
     """Solver whose partitions are sharded over the ranks of a TorchComm.
 
@@ -140,14 +167,19 @@ class DistributedSolver(Solver):
     partition / interface indices owned by (or crossing into) this rank.
     """
 
-    def __init__(self, comm: TorchComm, p: int, precond: PrecondKind = PrecondKind.coupled,
+    def __init__(self, comm: "TorchComm | NcclComm", p: int, precond: PrecondKind = PrecondKind.coupled,
                  boost_eps: float = 1e-10, krylov: KrylovOptions | None = None, device: int = 0):
         self.comm = comm
         super().__init__(p=p, precond=precond, boost_eps=boost_eps, krylov=krylov, device=device)
         self.row_lo = self.row_hi = 0
 
     def _create(self) -> None:
-        _check(L.load().sap_create_distributed(C.byref(self.options), C.byref(self.comm.struct), C.byref(self._h)))
+        if isinstance(self.comm, NcclComm):
+            _check(L.load().sap_create_distributed_nccl(C.byref(self.options), self.comm.uid.ctypes.data,
+                                                        self.comm.rank, self.comm.world, C.byref(self._h)))
+        else:
+            _check(L.load().sap_create_distributed(C.byref(self.options), C.byref(self.comm.struct),
+                                                   C.byref(self._h)))
 
     def rows(self, n: int, k: int) -> tuple[int, int]:
         return rank_rows(n, self.p, k, self.comm.rank, self.comm.world)
@@ -203,4 +235,4 @@ class DistributedSolver(Solver):
             self._raise_comm()
 
 
-__all__ = ["TorchComm", "DistributedSolver", "rank_rows", "band_slice_columns", "PartitionLayout"]
+__all__ = ["TorchComm", "NcclComm", "DistributedSolver", "rank_rows", "band_slice_columns", "PartitionLayout"]

@@ -153,3 +153,32 @@ def gpu_dist_solve(rank, world, port, n, k, p, d, seed, precond):
     dist.barrier()
     dist.destroy_process_group()
     return res
+
+
+def gpu_nccl_solve(rank, world, port, n, k, p, d, seed, precond):
+    """The native NCCL data plane (sap_create_distributed_nccl; torch.distributed only bootstraps the id):
+    one rank per GPU. On a one-GPU box world = 1 (NCCL refuses two ranks on one device)."""
+    dist = _init(rank, world, port)
+    import torch
+    import oracle as O
+    from paper_1509_07919_b200 import KrylovOptions, PrecondKind
+    from paper_1509_07919_b200.distributed import DistributedSolver, NcclComm
+    torch.cuda.set_device(rank)
+    comm = NcclComm()
+    band, rhs = O.random_banded(n, k, d, seed)
+    s = DistributedSolver(comm, p=p, precond=PrecondKind(precond), krylov=KrylovOptions(), device=rank)
+    s.setup_from_global(band, n, k)
+    lo, hi = s.row_lo, s.row_hi
+    res = {"rows": (lo, hi)}
+    res["apply"] = s.apply_preconditioner(rhs[lo:hi].copy()).tolist()
+    xg = np.sin(np.arange(n) * 0.37)
+    res["matvec"] = s.matvec(xg[lo:hi].copy()).tolist()
+    x, st = s.solve(rhs[lo:hi].copy())
+    res["x"] = x.tolist()
+    res["iterations"] = st.iterations
+    res["converged"] = st.converged
+    res["history"] = list(st.residual_history)
+    s.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    return res

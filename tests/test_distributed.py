@@ -123,3 +123,22 @@ def test_gpu_distributed_matches_single(sap, oracle, n, k, p, d, world, precond)
     rep = res[0]["report"]
     assert rep["partitions"] == p and rep["n"] == n
     assert all(r["calls"]["exchange"] > 0 for r in res)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precond", [0, 1])
+def test_gpu_native_nccl_world1_matches_single(sap, oracle, precond):
+    """The library's own NCCL communicator (ncclCommInitRank from an id broadcast over torch.distributed,
+    exchanges as ncclSend/ncclRecv on the handle's stream, Krylov dots as device ncclAllReduce) at the world
+    size one GPU allows: bitwise the single-GPU setup, apply, operator and solve."""
+    n, k, p, d = 20000, 20, 8, 1.0
+    res = _spawn(W.gpu_nccl_solve, 1, n, k, p, d, 11, precond, timeout=600)[0]
+    band, rhs = oracle.random_banded(n, k, d, 11)
+    single = sap.Solver(p=p, precond=sap.PrecondKind(precond))
+    single.setup(band, n, k)
+    assert tuple(res["rows"]) == (0, n)
+    np.testing.assert_array_equal(np.array(res["apply"]), single.apply_preconditioner(rhs))
+    np.testing.assert_array_equal(np.array(res["matvec"]), single.matvec(np.sin(np.arange(n) * 0.37)))
+    x1, st1 = single.solve(rhs)
+    assert res["converged"] and res["iterations"] == st1.iterations
+    assert np.linalg.norm(np.array(res["x"]) - x1) <= 1e-12 * np.linalg.norm(x1)
