@@ -118,6 +118,10 @@ typedef struct sap_report {
      * the block solves use substitution instead of the inverse products (1 = substitution) */
     double chunk_condition;
     int sweep_substitution;
+    /* CSR setups (sap_setup_banded_from_csr, sap_setup_from_csr_drop): drop_off on the device (T_Drop) and
+     * the band assembly (T_Asmbl), CUDA events; 0 for the other setups */
+    double t_drop;
+    double t_asmbl;
 } sap_report;
 
 /* SolveStats (krylov.hpp:35-41). history: caller-owned buffer of

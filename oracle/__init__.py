@@ -113,6 +113,8 @@ def ref():
                                           C.c_double, C.c_int, C.c_double, C.c_uint, C.c_int, C.c_double, C.c_int,
                                           C.c_int, _dp, _dp, C.POINTER(C.c_double), C.POINTER(C.c_int),
                                           C.POINTER(C.c_double), C.POINTER(C.c_int)]
+        R.sapref_host_stage.argtypes = [C.c_int, _ip, _ip, _dp, _dp, C.c_int, C.c_int, C.c_int, C.c_uint, _ip, _ip,
+                                        _dp, _dp, _ip, _dp, _dp]
         _ref = R
     return _ref
 
@@ -259,6 +261,49 @@ def ref_solve_banded(n, k, band, rhs, p, kind, boost_eps=1e-10, ell=2, rel_tol=1
     return x, dict(iterations=it.value, converged=bool(conv.value), final_relative_residual=res.value,
                    failure=fail.value, residual_history=hist[:min(hl.value, cap)].copy(),
                    t_lu=tim[0], t_bc=tim[1], t_spk=tim[2], t_lurdcd=tim[3], t_kry=tim[4])
+
+
+def ref_host_stage(n, row_ptr, col_idx, vals, rhs, use_db=True, db_scaling=True, use_cm=True, seed=0):
+    """solve_sparse's host stage (pipeline.hpp:228-266) run by the compiled reference: db_reorder + scaling,
+    cm_reorder. Returns the reordered CSR (rp, ci, v), rhs, the CM permutation and column scaling that map
+    the solution back (x[i] = z[cm_perm[i]] * col_scale[i]), and (t_db, t_cm) in seconds."""
+    nnz = int(row_ptr[n])
+    rp, ci, v = np.zeros(n + 1, np.int32), np.zeros(nnz, np.int32), np.zeros(nnz)
+    r, perm, cs, tim = np.zeros(n), np.zeros(n, np.int32), np.zeros(n), np.zeros(2)
+    _ref_check(ref().sapref_host_stage(n, np.ascontiguousarray(row_ptr, np.int32),
+                                       np.ascontiguousarray(col_idx, np.int32), np.ascontiguousarray(vals, np.float64),
+                                       np.ascontiguousarray(rhs, np.float64), int(use_db), int(db_scaling),
+                                       int(use_cm), seed, rp, ci, v, r, perm, cs, tim))
+    return dict(rp=rp, ci=ci, v=v, rhs=r, cm_perm=perm, col_scale=cs, t_db=tim[0], t_cm=tim[1])
+
+
+def convection_diffusion_3d(s):
+    """3-D 7-point upwind convection-diffusion on an s^3 grid (natural order), diagonal
+    6.3, -1.3 on the x-1 / y-1 / z-1 neighbours, -0.7 on +1 (a builder-defined 3-D analog of
+    proj/tests/acceptance.cpp:442-454). Returns n, row_ptr, col_idx, values (CSR, ascending columns)."""
+    n = s ** 3
+    idx = np.arange(n, dtype=np.int64)
+    z, y, x = idx // (s * s), (idx // s) % s, idx % s
+    cols, vals = [], []
+    for off, cond, val in ((-s * s, z > 0, -1.3), (-s, y > 0, -1.3), (-1, x > 0, -1.3), (0, None, 6.3),
+                           (1, x < s - 1, -0.7), (s, y < s - 1, -0.7), (s * s, z < s - 1, -0.7)):
+        m = np.ones(n, bool) if cond is None else cond
+        c = np.where(m, idx + off, -1)
+        cols.append(c)
+        vals.append(np.where(m, val, 0.0))
+    C_ = np.stack(cols, 1)
+    V_ = np.stack(vals, 1)
+    keep = C_ >= 0
+    rp = np.concatenate([[0], np.cumsum(keep.sum(1))]).astype(np.int32)
+    return n, rp, C_[keep].astype(np.int32), V_[keep].astype(np.float64)
+
+
+def manufactured_solution(n):
+    """benchmark.hpp:23-34: x_j = 1 + 399 (1 - t^2), t = 2 j / (n - 1) - 1."""
+    if n == 1:
+        return np.array([400.0])
+    t = 2.0 * np.arange(n) / (n - 1) - 1.0
+    return 1.0 + 399.0 * (1.0 - t * t)
 
 
 def ref_solve_sparse(n, row_ptr, col_idx, vals, rhs, p, kind, use_db=False, db_scaling=True, use_cm=False,

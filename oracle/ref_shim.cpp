@@ -296,6 +296,58 @@ int sapref_solve_sparse(int n, const int* row_ptr, const int* col_idx, const dou
     SAPREF_CATCH
 }
 
+// solve_sparse's host stage (pipeline.hpp:228-266): db_reorder (+ row/column scaling) and cm_reorder with the
+// matching right-hand-side permutations, exactly as solve_sparse runs them. Outputs the reordered matrix
+// (same nnz: row_ptr[n+1], col_idx, values), the reordered rhs, the CM permutation (identity when off) and
+// the column scaling (ones when off) that map the solution back, and the stage times.
+// timings[0] = t_db, [1] = t_cm (seconds).
+int sapref_host_stage(int n, const int* row_ptr, const int* col_idx, const double* vals, const double* rhs,
+                      int use_db, int db_scaling, int use_cm, unsigned seed, int* out_rp, int* out_ci,
+                      double* out_v, double* out_rhs, int* cm_perm, double* col_scale, double* timings) {
+    SAPREF_TRY
+    sap::SparseMatrix work;
+    work.n = n;
+    work.row_ptr.assign(row_ptr, row_ptr + n + 1);
+    work.col_idx.assign(col_idx, col_idx + row_ptr[n]);
+    work.values.assign(vals, vals + row_ptr[n]);
+    std::vector<double> r(rhs, rhs + n);
+    for (int i = 0; i < n; ++i) {
+        cm_perm[i] = i;
+        col_scale[i] = 1.0;
+    }
+    timings[0] = timings[1] = 0.0;
+    if (use_db) {
+        const auto t0 = std::chrono::steady_clock::now();
+        sap::DbResult db = sap::db_reorder(work, db_scaling != 0);
+        if (db.scaled) {
+            work = sap::scale_rows_cols(work, db.row_scale, db.col_scale);
+            for (int i = 0; i < n; ++i) r[static_cast<std::size_t>(i)] *= db.row_scale[static_cast<std::size_t>(i)];
+            for (int i = 0; i < n; ++i) col_scale[i] = db.col_scale[static_cast<std::size_t>(i)];
+        }
+        work = sap::permute_rows(work, db.perm);
+        std::vector<double> pr(static_cast<std::size_t>(n));
+        for (int i = 0; i < n; ++i) pr[static_cast<std::size_t>(db.perm[static_cast<std::size_t>(i)])] = r[static_cast<std::size_t>(i)];
+        r = std::move(pr);
+        timings[0] = seconds_since(t0);
+    }
+    if (use_cm) {
+        const auto t0 = std::chrono::steady_clock::now();
+        const sap::AdjGraph g = sap::build_graph(work);
+        sap::CmResult cm = sap::cm_reorder(g, seed);
+        work = sap::permute_symmetric(work, cm.perm);
+        std::vector<double> pr(static_cast<std::size_t>(n));
+        for (int i = 0; i < n; ++i) pr[static_cast<std::size_t>(cm.perm[static_cast<std::size_t>(i)])] = r[static_cast<std::size_t>(i)];
+        r = std::move(pr);
+        for (int i = 0; i < n; ++i) cm_perm[i] = cm.perm[static_cast<std::size_t>(i)];
+        timings[1] = seconds_since(t0);
+    }
+    std::memcpy(out_rp, work.row_ptr.data(), sizeof(int) * (n + 1));
+    std::memcpy(out_ci, work.col_idx.data(), sizeof(int) * work.col_idx.size());
+    std::memcpy(out_v, work.values.data(), sizeof(double) * work.values.size());
+    std::memcpy(out_rhs, r.data(), sizeof(double) * n);
+    SAPREF_CATCH
+}
+
 // sap::drop_off (pipeline.hpp:59-99): the kept half-bandwidth and the kept entry count.
 int sapref_drop_off(int n, const int* row_ptr, const int* col_idx, const double* vals, double tol, int* k_after,
                     int* nnz_after) {

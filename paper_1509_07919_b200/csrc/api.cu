@@ -126,6 +126,7 @@ struct sap_handle {
     DevBuf<int> asm_rp, asm_ci;
     DevBuf<double> asm_v;
     DevBuf<unsigned long long> asm_bad;
+    cudaEvent_t cev[3] = {};  // CSR setups: drop_off and assembly timers (T_Drop, T_Asmbl)
     DevBuf<TipJob> tipjobs;
     // third stage (sap_set_third_stage): ThirdStageResult (reorder_cm.hpp:227-231) applied at setup
     bool ts_armed = false;  // set by the caller; consumed by every following block setup
@@ -1308,6 +1309,8 @@ void sap_destroy(sap_handle* h) {
     if (h->prio) cudaStreamDestroy(h->prio);
     if (h->pev) cudaEventDestroy(h->pev);
     if (h->own_stream) cudaStreamDestroy(h->own_stream);
+    for (auto& e : h->cev)
+        if (e) cudaEventDestroy(e);
     nccl_destroy(h->nccl);
     delete h;
 }
@@ -1420,9 +1423,21 @@ void csr_to_device(sap_handle* h, int n, int nnz, const int*& rp, const int*& ci
     v = h->asm_v.get();
 }
 
-// assemble_banded on the device; drop = true filters |i - j| > k (drop_off) instead of failing
-void assemble_and_setup(sap_handle* h, int n, int k, const int* rp, const int* ci, const double* v, bool drop) {
+void csr_event(sap_handle* h, int i) {
+    if (!h->cev[i]) SAP_CUDA(cudaEventCreate(&h->cev[i]));
+    SAP_CUDA(cudaEventRecord(h->cev[i], h->stream));
+}
+
+// assemble_banded on the device; drop = true filters |i - j| > k (drop_off) instead of failing. The report's
+// t_drop (cev[0] -> cev[1], recorded by the caller around drop_off) and t_asmbl (cev[1] -> cev[2]) are
+// filled in after the setup (which resets the report).
+void assemble_and_setup(sap_handle* h, int n, int k, const int* rp, const int* ci, const double* v, bool drop,
+                        bool timed_drop) {
     const cudaStream_t s = h->stream;
+    if (!timed_drop) {
+        csr_event(h, 0);
+        csr_event(h, 1);
+    }
     const size_t total = (size_t)n * (2 * (size_t)k + 1);
     h->asm_band.alloc(std::max<size_t>(total, 1));
     SAP_CUDA(cudaMemsetAsync(h->asm_band.get(), 0, sizeof(double) * total, s));
@@ -1436,7 +1451,21 @@ void assemble_and_setup(sap_handle* h, int n, int k, const int* rp, const int* c
         throw InvalidArgument("assemble_banded: entry (" + std::to_string(bad / (unsigned long long)n) + ", " +
                               std::to_string(bad % (unsigned long long)n) + ") outside half-bandwidth " +
                               std::to_string(k));
-    setup_banded(h, n, k, h->asm_band.get(), 2);
+    csr_event(h, 2);
+    // solve_sparse's partition count (pipeline.hpp:291-301): reduced to max_feasible_partitions(n, k) when
+    // the requested p would leave a block below 2k rows
+    const int p_req = h->opt.p;
+    const int p_max = sap_max_feasible_partitions(n, k);
+    if (p_max >= 1 && p_req > p_max) h->opt.p = p_max;
+    try {
+        setup_banded(h, n, k, h->asm_band.get(), 2);
+    } catch (...) {
+        h->opt.p = p_req;
+        throw;
+    }
+    h->opt.p = p_req;
+    h->rep.t_drop = timed_drop ? ev_ms(h->cev[0], h->cev[1]) * 1e-3 : 0.0;
+    h->rep.t_asmbl = ev_ms(h->cev[1], h->cev[2]) * 1e-3;
 }
 }  // namespace
 
@@ -1452,7 +1481,7 @@ sap_status sap_setup_banded_from_csr(sap_handle* h, int n, int k, int nnz, const
         const double* v = values;
         h->csr = false;  // cleared by every setup; sap_set_operator_csr after it re-arms the CSR operator
         csr_to_device(h, n, nnz, rp, ci, v, csr_on_device);
-        assemble_and_setup(h, n, k, rp, ci, v, false);
+        assemble_and_setup(h, n, k, rp, ci, v, false, false);
     });
 }
 
@@ -1469,9 +1498,11 @@ sap_status sap_setup_from_csr_drop(sap_handle* h, int n, int nnz, const int* row
         const double* v = values;
         h->csr = false;
         csr_to_device(h, n, nnz, rp, ci, v, csr_on_device);
+        csr_event(h, 0);
         const int k = drop_off_k(rp, ci, v, n, nnz, drop_tol, h->stream);
+        csr_event(h, 1);
         if (k_after) *k_after = k;
-        assemble_and_setup(h, n, k, rp, ci, v, drop_tol > 0.0);
+        assemble_and_setup(h, n, k, rp, ci, v, drop_tol > 0.0, true);
     });
 }
 

@@ -513,3 +513,28 @@ def test_resetup_with_a_new_matrix_on_the_same_handle(sap, oracle, on_device):
         assert np.array_equal(norms, want["norms"]) and np.array_equal(boosts, want["boosts"])
         assert nrel(lu, want["lu"]) <= 1e-13
     s.close()
+
+
+@pytest.mark.parametrize("kind,drop_tol", [(0, 0.365), (1, 0.365), (0, 0.37)])
+def test_config4_pipeline_with_host_reorderings_matches_solve_sparse(sap, oracle, kind, drop_tol):
+    """BASELINE config 4's full path at s = 30 (N = 27000): the reference's host stage (db_reorder with
+    scaling, cm_reorder; oracle.ref_host_stage) feeding the device drop_off + assembly + SaP setup + CSR
+    BiCGStab(2) (paper_1509_07919_b200.sparse.solve_reordered), against the reference's own solve_sparse
+    with use_db = use_cm = true and the same drop_tol: k_after equal, iterations within +-1, x within 1e-8,
+    and the benchmark's 1% error gate against the manufactured solution (benchmark.hpp:47)."""
+    if not oracle.has_ref():
+        pytest.skip("compiled reference absent")
+    from paper_1509_07919_b200.sparse import solve_reordered
+    n, rp, ci, v = oracle.convection_diffusion_3d(30)
+    xs = oracle.manufactured_solution(n)
+    b = oracle.csr_matvec(n, rp, ci, v, xs)
+    xr, so = oracle.ref_solve_sparse(n, rp, ci, v, b, 8, kind, use_db=True, use_cm=True, drop_tol=drop_tol)
+    hs = oracle.ref_host_stage(n, rp, ci, v, b)
+    x, st, rep = solve_reordered(hs["rp"], hs["ci"], hs["v"], hs["rhs"], hs["cm_perm"], hs["col_scale"], 8,
+                                 drop_tol, precond=sap.PrecondKind(kind))
+    assert rep["k_after"] == so["k_after"]
+    assert so["converged"] and st.converged and st.final_relative_residual <= 1e-10
+    assert abs(st.iterations - so["iterations"]) <= 1.0, (st.iterations, so["iterations"])
+    assert rel2(x, xr) <= 1e-8
+    assert rel2(x, xs) <= 0.01
+    assert rep["t_drop"] > 0 and rep["t_asmbl"] > 0
