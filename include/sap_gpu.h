@@ -122,6 +122,9 @@ typedef struct sap_report {
      * the band assembly (T_Asmbl), CUDA events; 0 for the other setups */
     double t_drop;
     double t_asmbl;
+    /* host synchronisations of the last sap_solve (each scalar the host recurrences need costs one; the dot
+     * products a step needs next ride with its true residual, MGS runs on device scalars) */
+    long long krylov_host_syncs;
 } sap_report;
 
 /* SolveStats (krylov.hpp:35-41). history: caller-owned buffer of

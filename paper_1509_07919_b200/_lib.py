@@ -25,7 +25,8 @@ class sap_report(C.Structure):
                 ("partitions", C.c_int), ("total_boosts", C.c_int), ("total_boosts_ul", C.c_int),
                 ("total_rbar_boosts", C.c_int), ("kernel_launches", C.c_longlong),
                 ("t_factor_kernel", C.c_double), ("factor_flops", C.c_double), ("chunk_condition", C.c_double),
-                ("sweep_substitution", C.c_int), ("t_drop", C.c_double), ("t_asmbl", C.c_double)]
+                ("sweep_substitution", C.c_int), ("t_drop", C.c_double), ("t_asmbl", C.c_double),
+                ("krylov_host_syncs", C.c_longlong)]
 
 
 class sap_solve_stats(C.Structure):

@@ -1610,6 +1610,7 @@ sap_status sap_solve(sap_handle* h, const double* b, double* x, int on_device, s
         if (!on_device && n) SAP_CUDA(cudaMemcpyAsync(x, dx, bytes, cudaMemcpyDeviceToHost, s));
         SAP_CUDA(cudaStreamSynchronize(s));
         h->rep.t_kry = ev_ms(h->ev[6], h->ev[7]) * 1e-3;
+        h->rep.krylov_host_syncs = h->krylov.host_syncs();
         if (stats) {
             stats->iterations = r.iterations;
             stats->converged = r.converged ? 1 : 0;

@@ -147,6 +147,15 @@ void launch_csr_spmv(const int* rp, const int* ci, const double* v, int n, const
 // ---- vector kernels (vec.cu) ----
 // Deterministic reductions: fixed partition of [0, n) into blocks, fixed tree.
 int reduce_blocks(int n);
+constexpr int kMaxDots = 4;
+struct DotBatch {  // up to kMaxDots dot products in one pass (kind 1: squared norm of a - b)
+    const double* a[kMaxDots];
+    const double* b[kMaxDots];
+    int kind[kMaxDots];
+    int m;
+};
+void launch_dots(const DotBatch& d, int n, double* partials, unsigned* counter, double* out, cudaStream_t s);
+void launch_axpy_quot(double* y, const double* num, const double* den, const double* x, int n, cudaStream_t s);
 // *counter must be 0 on entry (the kernel leaves it 0).
 void launch_dot(const double* a, const double* b, int n, double* partials, unsigned* counter, double* out,
                 cudaStream_t s);

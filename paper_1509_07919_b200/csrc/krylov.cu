@@ -14,6 +14,9 @@ namespace sapgpu {
 namespace {
 
 constexpr int kMaxEll = 8;
+// device scalar slots: [0, kMaxDots) batch outputs; [16, 16 + kMaxEll * kMaxEll) MGS dot numerators
+// (tau_ij at 16 + i * kMaxEll + j, sigma_j at 16 + j * kMaxEll + j, gamma'_j at 16 + j)
+constexpr int kScal = 16 + kMaxEll * kMaxEll + 16;
 
 struct VecSet {
     double* p[2 * kMaxEll + 2];
@@ -103,14 +106,14 @@ void KrylovSolver::ensure(int n, int ell) {
     const int nvec = 2 * (ell + 1) + 5;
     SAP_CUDA(cudaMalloc(&buf_, sizeof(double) * N * nvec));
     SAP_CUDA(cudaMemset(buf_, 0, sizeof(double) * N * nvec));
-    SAP_CUDA(cudaMalloc(&partials_, sizeof(double) * (size_t)reduce_blocks(n)));
-    if (!dscal_) SAP_CUDA(cudaMalloc(&dscal_, sizeof(double) * 16));
+    SAP_CUDA(cudaMalloc(&partials_, sizeof(double) * (size_t)reduce_blocks(n) * kMaxDots));
+    if (!dscal_) SAP_CUDA(cudaMalloc(&dscal_, sizeof(double) * kScal));
     if (!counter_) {
         SAP_CUDA(cudaMalloc(&counter_, sizeof(unsigned)));
         SAP_CUDA(cudaMemset(counter_, 0, sizeof(unsigned)));
     }
     if (!dflag_) SAP_CUDA(cudaMalloc(&dflag_, sizeof(int)));
-    if (!hpinned_) SAP_CUDA(cudaMallocHost(&hpinned_, sizeof(double) * 16));
+    if (!hpinned_) SAP_CUDA(cudaMallocHost(&hpinned_, sizeof(double) * kScal));
     if (!hflag_) SAP_CUDA(cudaMallocHost(&hflag_, sizeof(int)));
     r_.assign(ell + 1, nullptr);
     u_.assign(ell + 1, nullptr);
@@ -127,13 +130,41 @@ void KrylovSolver::ensure(int n, int ell) {
     ell_ = ell;
 }
 
+void KrylovSolver::sync_host() {
+    SAP_CUDA(cudaStreamSynchronize(s_));
+    ++syncs_;
+}
+
 double KrylovSolver::dot(const double* a, const double* b) {
     launch_dot(a, b, n_, partials_, counter_, dscal_, s_);
     if (dreduce_) dreduce_(dscal_, 1, s_);
     SAP_CUDA(cudaMemcpyAsync(hpinned_, dscal_, sizeof(double), cudaMemcpyDeviceToHost, s_));
-    SAP_CUDA(cudaStreamSynchronize(s_));
+    sync_host();
     if (reduce_ && !dreduce_) reduce_(hpinned_, 1);
     return hpinned_[0];
+}
+
+// Several dot products (kind 1: squared norm of a - b) in one kernel, one device->host copy and one
+// synchronisation; each value bitwise the dot() of the same operands. The x-update's non-finite flag rides
+// along when flag_too is set.
+std::vector<double> KrylovSolver::dots(const std::vector<DotReq>& rq, bool flag_too) {
+    const int m = (int)rq.size();
+    for (int q0 = 0; q0 < m; q0 += kMaxDots) {
+        DotBatch d{};
+        d.m = std::min(kMaxDots, m - q0);
+        for (int q = 0; q < d.m; ++q) {
+            d.a[q] = rq[q0 + q].a;
+            d.b[q] = rq[q0 + q].b;
+            d.kind[q] = rq[q0 + q].kind;
+        }
+        launch_dots(d, n_, partials_, counter_, dscal_ + q0, s_);
+    }
+    if (dreduce_) dreduce_(dscal_, m, s_);
+    SAP_CUDA(cudaMemcpyAsync(hpinned_, dscal_, sizeof(double) * m, cudaMemcpyDeviceToHost, s_));
+    if (flag_too) SAP_CUDA(cudaMemcpyAsync(hflag_, dflag_, sizeof(int), cudaMemcpyDeviceToHost, s_));
+    sync_host();
+    if (reduce_ && !dreduce_) reduce_(hpinned_, m);
+    return std::vector<double>(hpinned_, hpinned_ + m);
 }
 
 bool KrylovSolver::any_flag(int local) {
@@ -147,13 +178,14 @@ bool KrylovSolver::nonfinite(const double* v) {
     SAP_CUDA(cudaMemsetAsync(dflag_, 0, sizeof(int), s_));
     launch_nonfinite(v, n_, dflag_, s_);
     SAP_CUDA(cudaMemcpyAsync(hflag_, dflag_, sizeof(int), cudaMemcpyDeviceToHost, s_));
-    SAP_CUDA(cudaStreamSynchronize(s_));
+    sync_host();
     return *hflag_ != 0;
 }
 
 KrylovResult KrylovSolver::run(const DeviceOp& A, const DeviceOp& M, const double* b, double* x, int n,
                                const KrylovConfig& cfg, cudaStream_t s) {
     s_ = s;
+    syncs_ = 0;
     reduce_ = cfg.reduce;
     dreduce_ = cfg.dreduce;
     int method = cfg.method;
@@ -203,15 +235,22 @@ KrylovResult KrylovSolver::bicgstab(const DeviceOp& A, const DeviceOp& M, const 
         A(in, tmp_);
         M(tmp_, out);
     };
-    // true_residual (krylov.hpp:62-72): ||b - A x||
-    auto tres = [&](const double* xv) -> double {
+    // true_residual (krylov.hpp:62-72): ||b - A x|| -- A x into scratch, then the residual's squared norm in
+    // the same one-sync reduction as the dot products the next step needs (each value bitwise the separate
+    // k_xpay + k_dot of round 1)
+    auto tres = [&](const double* xv, std::vector<DotReq> more, bool flag, std::vector<double>& extra) -> double {
         A(xv, scratch_);
-        k_xpay<<<G, 256, 0, s_>>>(scratch_, -1.0, b, n);  // scratch = b - A x
-        SAP_LAUNCHED();
-        return std::sqrt(dot(scratch_, scratch_));
+        more.insert(more.begin(), DotReq{b, scratch_, 1});
+        std::vector<double> v = dots(more, flag);
+        extra.assign(v.begin() + 1, v.end());
+        return std::sqrt(v[0]);
     };
     bool x_is_zero = true;  // x was just zeroed (krylov.hpp:117); false once any update is applied
+    // dot products computed ahead of their use in the same synchronisation as the previous true residual
+    bool have_rho = false, have_gram = false;
+    double rho_next = 0.0, g11 = 0.0, g10 = 0.0;
     auto reset_iteration_state = [&](bool perturb) {
+        have_rho = have_gram = false;
         if (x_is_zero && cfg.zero_guess_exact) {
             SAP_CUDA(cudaMemcpyAsync(tmp_, b, sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, s_));
         } else {
@@ -232,7 +271,7 @@ KrylovResult KrylovSolver::bicgstab(const DeviceOp& A, const DeviceOp& M, const 
             SAP_CUDA(cudaMemcpyAsync(noise_, h.data(), sizeof(double) * (size_t)n, cudaMemcpyHostToDevice, s_));
             k_axpy_check<<<G, 256, 0, s_>>>(rtilde_, scale, noise_, n, nullptr);
             SAP_LAUNCHED();
-            SAP_CUDA(cudaStreamSynchronize(s_));
+            sync_host();
         }
         SAP_CUDA(cudaMemsetAsync(u_[0], 0, sizeof(double) * (size_t)n, s_));
     };
@@ -243,12 +282,17 @@ KrylovResult KrylovSolver::bicgstab(const DeviceOp& A, const DeviceOp& M, const 
     bool restarted = false, breakdown = false;
     std::vector<double> gamma(ell + 1), gamma_p(ell + 1), gamma_pp(ell + 1), sigma(ell + 1);
     std::vector<double> tau((size_t)(ell + 1) * (ell + 1));
+    std::vector<double> extra;
+    // MGS on the device (no host round trip per tau) needs a device-side reduction; the host-callback
+    // transport (gloo tests) keeps the per-dot path
+    const bool device_mgs = !(reduce_ && !dreduce_);
 
     for (int sweep = 0; sweep < cfg.max_iterations; ++sweep) {
         breakdown = false;
         rho0 = -omega * rho0;
         for (int j = 0; j < ell && !breakdown; ++j) {
-            const double rho1 = dot(r_[j], rtilde_);
+            const double rho1 = have_rho ? rho_next : dot(r_[j], rtilde_);
+            have_rho = false;
             if (!std::isfinite(rho1)) { st.failure = 3; return st; }
             if (rho0 == 0.0 || rho1 == 0.0) { breakdown = true; break; }
             const double beta = alpha * rho1 / rho0;
@@ -266,8 +310,24 @@ KrylovResult KrylovSolver::bicgstab(const DeviceOp& A, const DeviceOp& M, const 
             SAP_CUDA(cudaMemsetAsync(dflag_, 0, sizeof(int), s_));
             k_axpy_check<<<G, 256, 0, s_>>>(x, alpha, u_[0], n, dflag_);
             SAP_LAUNCHED();
-            SAP_CUDA(cudaMemcpyAsync(hflag_, dflag_, sizeof(int), cudaMemcpyDeviceToHost, s_));
-            tr = tres(x);  // synchronizes (dot), so hflag_ is valid below
+            // with the residual: the next step's rho1 = (r_{j+1}, r~), or after the last step the first Gram
+            // entries (r_1, r_1), (r_1, r_0) of the MGS trial / first MGS column (r_0..r_l are final here)
+            std::vector<DotReq> ahead;
+            if (j + 1 < ell)
+                ahead.push_back(DotReq{r_[j + 1], rtilde_, 0});
+            else if (ell >= 2) {
+                ahead.push_back(DotReq{r_[1], r_[1], 0});
+                ahead.push_back(DotReq{r_[1], r_[0], 0});
+            }
+            tr = tres(x, ahead, true, extra);
+            if (j + 1 < ell) {
+                rho_next = extra[0];
+                have_rho = true;
+            } else if (ell >= 2) {
+                g11 = extra[0];
+                g10 = extra[1];
+                have_gram = true;
+            }
             if (any_flag(*hflag_)) { st.failure = 3; return st; }
             if (!std::isfinite(tr)) { st.failure = 3; return st; }
             record(sweep, j + 1, tr);
@@ -276,9 +336,20 @@ KrylovResult KrylovSolver::bicgstab(const DeviceOp& A, const DeviceOp& M, const 
         if (!breakdown) {
             for (int d = 1; d < ell; ++d) {
                 std::vector<double> gram((size_t)d * d), rhs(d);
-                for (int a = 1; a <= d; ++a) {
-                    for (int c = 1; c <= d; ++c) gram[(size_t)(a - 1) * d + (c - 1)] = dot(r_[a], r_[c]);
-                    rhs[a - 1] = dot(r_[a], r_[0]);
+                if (d == 1 && have_gram) {
+                    gram[0] = g11;
+                    rhs[0] = g10;
+                } else {
+                    std::vector<DotReq> rq;
+                    for (int a = 1; a <= d; ++a) {
+                        for (int c = 1; c <= d; ++c) rq.push_back(DotReq{r_[a], r_[c], 0});
+                        rq.push_back(DotReq{r_[a], r_[0], 0});
+                    }
+                    const std::vector<double> v = dots(rq);
+                    for (int a = 1; a <= d; ++a) {
+                        for (int c = 1; c <= d; ++c) gram[(size_t)(a - 1) * d + (c - 1)] = v[(size_t)(a - 1) * (d + 1) + (c - 1)];
+                        rhs[a - 1] = v[(size_t)(a - 1) * (d + 1) + d];
+                    }
                 }
                 // tiny_solve with partial pivoting (krylov.hpp:76-99)
                 bool solvable = true;
@@ -315,7 +386,7 @@ KrylovResult KrylovSolver::bicgstab(const DeviceOp& A, const DeviceOp& M, const 
                 for (int i = 1; i <= d; ++i) xs.c[i - 1] = rhs[i - 1];
                 k_xc<<<G, 256, 0, s_>>>(xc_, x, xs, d, n);
                 SAP_LAUNCHED();
-                tr = tres(xc_);
+                tr = tres(xc_, {}, false, extra);
                 if (!std::isfinite(tr)) continue;
                 record(sweep, ell + d, tr);
                 if (tr <= thr) {
@@ -324,18 +395,66 @@ KrylovResult KrylovSolver::bicgstab(const DeviceOp& A, const DeviceOp& M, const 
                     return st;
                 }
             }
-            for (int j = 1; j <= ell && !breakdown; ++j) {
-                for (int i = 1; i < j; ++i) {
-                    const double tij = dot(r_[j], r_[i]) / sigma[i];
-                    tau[(size_t)i * (ell + 1) + j] = tij;
-                    k_axpy_check<<<G, 256, 0, s_>>>(r_[j], -tij, r_[i], n, nullptr);
-                    SAP_LAUNCHED();
+            // modified Gram-Schmidt (krylov.hpp:323-334)
+            if (device_mgs) {
+                // every dot into its own device slot, each tau_ij = (r_j, r_i) / sigma_i formed and applied on
+                // the device; one copy back, then the reference's checks in its order on the same values
+                double* slot = dscal_ + 16;
+                auto sl = [&](int i, int jj) { return slot + i * kMaxEll + jj; };  // tau_ij (i < j), sigma_j (i == j)
+                if (have_gram) {  // sigma_1 for the device-side tau_1j quotients
+                    hpinned_[kScal - 1] = g11;
+                    SAP_CUDA(cudaMemcpyAsync(sl(1, 1), hpinned_ + kScal - 1, sizeof(double), cudaMemcpyHostToDevice,
+                                             s_));
                 }
-                sigma[j] = dot(r_[j], r_[j]);
-                if (!std::isfinite(sigma[j])) { st.failure = 3; return st; }
-                if (sigma[j] == 0.0) { breakdown = true; break; }
-                gamma_p[j] = dot(r_[0], r_[j]) / sigma[j];
+                for (int jj = 1; jj <= ell; ++jj) {
+                    for (int i = 1; i < jj; ++i) {
+                        DotBatch dq{};
+                        dq.m = 1;
+                        dq.a[0] = r_[jj];
+                        dq.b[0] = r_[i];
+                        launch_dots(dq, n_, partials_, counter_, sl(i, jj), s_);
+                        if (dreduce_) dreduce_(sl(i, jj), 1, s_);
+                        launch_axpy_quot(r_[jj], sl(i, jj), sl(i, i), r_[i], n, s_);
+                    }
+                    if (jj == 1 && have_gram) continue;  // sigma_1 = (r_1, r_1), gamma'_1 from (r_1, r_0)
+                    DotBatch dq{};
+                    dq.m = 2;
+                    dq.a[0] = r_[jj];
+                    dq.b[0] = r_[jj];
+                    dq.a[1] = r_[0];
+                    dq.b[1] = r_[jj];
+                    launch_dots(dq, n_, partials_, counter_, dscal_, s_);
+                    if (dreduce_) dreduce_(dscal_, 2, s_);
+                    SAP_CUDA(cudaMemcpyAsync(sl(jj, jj), dscal_, sizeof(double), cudaMemcpyDeviceToDevice, s_));
+                    SAP_CUDA(cudaMemcpyAsync(slot + kMaxEll * kMaxEll + jj, dscal_ + 1, sizeof(double),
+                                             cudaMemcpyDeviceToDevice, s_));
+                }
+                SAP_CUDA(cudaMemcpyAsync(hpinned_ + 16, slot, sizeof(double) * (kMaxEll * kMaxEll + kMaxEll + 1),
+                                         cudaMemcpyDeviceToHost, s_));
+                sync_host();
+                const double* hs = hpinned_ + 16;
+                for (int jj = 1; jj <= ell && !breakdown; ++jj) {
+                    for (int i = 1; i < jj; ++i) tau[(size_t)i * (ell + 1) + jj] = hs[i * kMaxEll + jj] / sigma[i];
+                    sigma[jj] = (jj == 1 && have_gram) ? g11 : hs[jj * kMaxEll + jj];
+                    if (!std::isfinite(sigma[jj])) { st.failure = 3; return st; }
+                    if (sigma[jj] == 0.0) { breakdown = true; break; }
+                    gamma_p[jj] = ((jj == 1 && have_gram) ? g10 : hs[kMaxEll * kMaxEll + jj]) / sigma[jj];
+                }
+            } else {
+                for (int j = 1; j <= ell && !breakdown; ++j) {
+                    for (int i = 1; i < j; ++i) {
+                        const double tij = dot(r_[j], r_[i]) / sigma[i];
+                        tau[(size_t)i * (ell + 1) + j] = tij;
+                        k_axpy_check<<<G, 256, 0, s_>>>(r_[j], -tij, r_[i], n, nullptr);
+                        SAP_LAUNCHED();
+                    }
+                    sigma[j] = dot(r_[j], r_[j]);
+                    if (!std::isfinite(sigma[j])) { st.failure = 3; return st; }
+                    if (sigma[j] == 0.0) { breakdown = true; break; }
+                    gamma_p[j] = dot(r_[0], r_[j]) / sigma[j];
+                }
             }
+            have_gram = false;
         }
         if (!breakdown) {
             gamma[ell] = gamma_p[ell];
@@ -362,8 +481,10 @@ KrylovResult KrylovSolver::bicgstab(const DeviceOp& A, const DeviceOp& M, const 
             SAP_CUDA(cudaMemsetAsync(dflag_, 0, sizeof(int), s_));
             k_final_update<<<G, 256, 0, s_>>>(x, fs, ell, n, dflag_);
             SAP_LAUNCHED();
-            SAP_CUDA(cudaMemcpyAsync(hflag_, dflag_, sizeof(int), cudaMemcpyDeviceToHost, s_));
-            tr = tres(x);
+            // with the residual: the next sweep's first rho1 = (r_0, r~)
+            tr = tres(x, {DotReq{r_[0], rtilde_, 0}}, true, extra);
+            rho_next = extra[0];
+            have_rho = true;
             if (any_flag(*hflag_)) { st.failure = 3; return st; }
             if (!std::isfinite(tr)) { st.failure = 3; return st; }
             record(sweep, 2 * ell, tr);

@@ -5,6 +5,7 @@
 #pragma once
 
 #include <functional>
+#include <initializer_list>
 #include <vector>
 
 #include "common.cuh"
@@ -51,16 +52,25 @@ public:
     // run_krylov: b, x device pointers; x is overwritten (x0 = 0).
     KrylovResult run(const DeviceOp& A, const DeviceOp& M, const double* b, double* x, int n,
                      const KrylovConfig& cfg, cudaStream_t s);
+    long long host_syncs() const { return syncs_; }  // stream synchronisations of the last run
 
 private:
+    struct DotReq {
+        const double* a;
+        const double* b;
+        int kind;  // 0: dot(a, b); 1: ||a - b||^2
+    };
     void ensure(int n, int ell);
+    void sync_host();
     double dot(const double* a, const double* b);
+    std::vector<double> dots(const std::vector<DotReq>& reqs, bool flag_too = false);
     bool any_flag(int local);
     bool nonfinite(const double* v);
     KrylovResult bicgstab(const DeviceOp& A, const DeviceOp& M, const double* b, double* x, const KrylovConfig& cfg);
     KrylovResult cg(const DeviceOp& A, const DeviceOp& M, const double* b, double* x, const KrylovConfig& cfg);
 
     int n_ = 0, ell_ = 0;
+    long long syncs_ = 0;
     std::function<void(double*, int)> reduce_;
     std::function<void(double*, int, cudaStream_t)> dreduce_;
     cudaStream_t s_ = nullptr;

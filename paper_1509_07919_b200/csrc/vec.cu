@@ -61,6 +61,74 @@ void launch_dot(const double* a, const double* b, int n, double* partials, unsig
     SAP_LAUNCHED();
 }
 
+// Several dot products in one pass over the same fixed partition and trees as k_dot: pair q is bitwise
+// k_dot(a[q], b[q]). kind[q] = 1: the squared norm of the residual a[q] - b[q] (each element fma(-1, b, a),
+// exactly k_xpay's scratch = b - A x, then fma(r, r, acc) as k_dot(scratch, scratch)) without storing it.
+__global__ void __launch_bounds__(kRedThreads)
+    k_dots(DotBatch d, int n, double* __restrict__ partials, unsigned* __restrict__ counter, double* __restrict__ out) {
+    __shared__ double sh[32];
+    __shared__ bool last;
+    const int base = blockIdx.x * kRedChunk;
+    const int end = min(base + kRedChunk, n);
+    double s[kMaxDots];
+#pragma unroll
+    for (int q = 0; q < kMaxDots; ++q) s[q] = 0.0;
+    for (int i = base + threadIdx.x; i < end; i += kRedThreads) {
+#pragma unroll
+        for (int q = 0; q < kMaxDots; ++q) {
+            if (q < d.m) {
+                if (d.kind[q]) {
+                    const double r = fma(-1.0, d.b[q][i], d.a[q][i]);
+                    s[q] = fma(r, r, s[q]);
+                } else {
+                    s[q] = fma(d.a[q][i], d.b[q][i], s[q]);
+                }
+            }
+        }
+    }
+    for (int q = 0; q < d.m; ++q) {
+        const double t = block_sum(s[q], sh);
+        if (threadIdx.x == 0) partials[q * gridDim.x + blockIdx.x] = t;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned prev = atomicAdd(counter, 1u);
+        last = (prev == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        if (threadIdx.x < d.m) {
+            const int q = threadIdx.x;
+            double tot = 0.0;
+            for (int b = 0; b < (int)gridDim.x; ++b) tot += __ldcg(partials + q * gridDim.x + b);
+            out[q] = tot;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) *counter = 0u;
+    }
+}
+
+void launch_dots(const DotBatch& d, int n, double* partials, unsigned* counter, double* out, cudaStream_t s) {
+    if (d.m <= 0) return;
+    k_dots<<<reduce_blocks(n), kRedThreads, 0, s>>>(d, n, partials, counter, out);
+    SAP_LAUNCHED();
+}
+
+// y -= (num / den) x with num, den device scalars (the quotient on the device, IEEE division like the host's
+// dot / sigma): the MGS step of krylov.hpp:323-329 without a host round trip.
+__global__ void k_axpy_quot(double* __restrict__ y, const double* __restrict__ num, const double* __restrict__ den,
+                            const double* __restrict__ x, int n) {
+    const double a = -(*num / *den);
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) y[t] = fma(a, x[t], y[t]);
+}
+
+void launch_axpy_quot(double* y, const double* num, const double* den, const double* x, int n, cudaStream_t s) {
+    k_axpy_quot<<<std::max(1, std::min(ceil_div(n, 256), 148 * 8)), 256, 0, s>>>(y, num, den, x, n);
+    SAP_LAUNCHED();
+}
+
 __global__ void k_nonfinite(const double* __restrict__ a, int n, int* flag) {
     int bad = 0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)

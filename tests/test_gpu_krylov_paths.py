@@ -110,3 +110,22 @@ def test_diagonal_preconditioner(sap, oracle, mixed):
         assert abs(st.iterations - so["iterations"]) <= 1.0, (st.iterations, so["iterations"])
         assert rel2(x, xr) <= 1e-8
     s.close()
+
+
+def test_bicgstab2_host_synchronisations_per_sweep(sap, oracle):
+    """Device-side Krylov bookkeeping: a BiCGStab(2) sweep synchronises with the host about 7 times (the two
+    rho / g scalars of each BiCG step, its true residual with the next step's dot products batched into it,
+    the MGS trial's residual, one read-back of the device-side MGS, the final residual with the next sweep's
+    rho) instead of once per dot product (15); iterations unchanged against the oracle."""
+    n, k, p = 6000, 24, 12
+    band, rhs = oracle.random_banded(n, k, 0.2, 101)
+    _, so = oracle.solve_banded(n, k, band, rhs, p, 1, ell=2, max_iterations=200)
+    s = sap.Solver(p=p, precond=1, krylov=sap.KrylovOptions(ell=2, max_iterations=200))
+    s.setup(band, n, k)
+    x, st = s.solve(rhs)
+    assert st.converged and abs(st.iterations - so["iterations"]) <= 1.0
+    sweeps = int(np.ceil(st.iterations))
+    assert sweeps >= 3
+    syncs = s.report()["krylov_host_syncs"]
+    assert syncs <= 7 * sweeps + 3, (syncs, sweeps)
+    s.close()
