@@ -104,6 +104,7 @@ struct sap_handle {
         scratch_out, dscal, xt, xb;
     DevBuf<int> boosts, rbar_boosts, nonfinite;
     DevBuf<FactorJob> jobs, rjobs;
+    DevBuf<int> lu_scr;  // k_band_lu_df work counter and dependency flags (one launch at a time on the stream)
     BandStore fst, rst;                  // LU/UL and reduced-block stores
     DevBuf<double> dinv, rdinv;          // chunk inverses (+ triangles) for the sweeps
     DevBuf<unsigned long long> kappa;    // [0] LU plan, [1] reduced plan: chunk-triangle condition estimates
@@ -186,6 +187,24 @@ sap_status guard(F&& f) {
         g_last_error = e.what();
         return SAP_ERR_CUDA;
     }
+}
+
+// grows only: a launch already enqueued on the handle's stream may still use the buffer
+int* lu_scratch(sap_handle* h, int njobs, int m_max) {
+    const size_t need = lu_df_scratch_ints(njobs, m_max);
+    if (h->lu_scr.n < need) h->lu_scr.alloc(need);
+    return h->lu_scr.get();
+}
+
+// k_band_lu_df: a dependency wait that timed out (never expected) fails the setup instead of returning
+// factors computed from stale data
+void lu_check(sap_handle* h) {
+    if (!h->lu_scr.get()) return;
+    int d[7];
+    if (lu_df_error(h->lu_scr.get(), d))
+        throw CudaFailure("band LU (k_band_lu_df): dependency wait timed out (CTA " + std::to_string(d[1]) + ", SM " +
+                          std::to_string(d[2]) + ", flag " + std::to_string(d[3]) + " want " + std::to_string(d[4]) +
+                          " have " + std::to_string(d[5]) + ", site " + std::to_string(d[6]) + ")");
 }
 
 void require(bool c, const char* msg) {
@@ -525,6 +544,7 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
         }
     }
     h->jobs.alloc(njobs);
+    lu_df_clear_error(lu_scratch(h, njobs, m_max), s);
     SAP_CUDA(cudaMemcpyAsync(h->jobs.get(), jobs.data(), sizeof(FactorJob) * njobs, cudaMemcpyHostToDevice, s));
     h->kappa.alloc(2);
     SAP_CUDA(cudaMemsetAsync(h->kappa.get(), 0, 2 * sizeof(unsigned long long), s));
@@ -641,7 +661,7 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
         SAP_CUDA(cudaMemcpyAsync(h->gjobs.get(), gj.data(), sizeof(FactorJob) * njobs, cudaMemcpyHostToDevice, s));
         SAP_CUDA(cudaMemsetAsync(h->d_minpiv.get(), 0, sizeof(double) * njobs, s));  // -1 = stalled upload
         SAP_CUDA(cudaEventRecord(h->ev[8], s));
-        launch_band_lu(h->sjobs.get(), njobs, k, h->opt.boost_eps, s, true);
+        launch_band_lu(h->sjobs.get(), njobs, k, h->opt.boost_eps, s, true, m_max, lu_scratch(h, njobs, m_max));
         SAP_CUDA(cudaEventRecord(h->ev[9], s));
         // 3. once the norms exist: any pivot below the boost threshold means the reference would have
         //    boosted -> refactor with boosting (rare; exact either way)
@@ -649,10 +669,10 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
         launch_stream_check(h->sjobs.get(), h->d_minpiv.get(), h->norms.get(), njobs, p, h->opt.boost_eps,
                             h->d_sbad.get(), s);
         // the refactor with boosting is always launched; its CTAs exit at once unless the check asked for it
-        launch_band_lu(h->gjobs.get(), njobs, k, h->opt.boost_eps, s);
+        launch_band_lu(h->gjobs.get(), njobs, k, h->opt.boost_eps, s, false, m_max, lu_scratch(h, njobs, m_max));
     } else {
         SAP_CUDA(cudaEventRecord(h->ev[8], s));
-        launch_band_lu(h->jobs.get(), njobs, k, h->opt.boost_eps, s);
+        launch_band_lu(h->jobs.get(), njobs, k, h->opt.boost_eps, s, false, m_max, lu_scratch(h, njobs, m_max));
         SAP_CUDA(cudaEventRecord(h->ev[9], s));
     }
     {
@@ -777,7 +797,7 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
                                   h->rbar_norms.get() + t, h->rbar_boosts.get() + t};
             h->rjobs.alloc(ni);
             SAP_CUDA(cudaMemcpyAsync(h->rjobs.get(), rj.data(), sizeof(FactorJob) * ni, cudaMemcpyHostToDevice, s));
-            launch_band_lu(h->rjobs.get(), ni, k - 1, h->opt.boost_eps, s);
+            launch_band_lu(h->rjobs.get(), ni, k - 1, h->opt.boost_eps, s, false, k, lu_scratch(h, ni, k));
             SweepPlan<double>& rp = h->rplan;
             rp = SweepPlan<double>{};
             rp.f = h->rbar.get();
@@ -799,6 +819,7 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
         if (h->ts) h->scratch_pf.alloc(n);
     }
     SAP_CUDA(cudaStreamSynchronize(s));
+    lu_check(h);
     if (streamed || early) {
         int bad = 0;
         SAP_CUDA(cudaMemcpy(&bad, h->d_sbad.get(), sizeof(int), cudaMemcpyDeviceToHost));
@@ -1022,6 +1043,7 @@ void setup_banded_dist(sap_handle* h, int n, int k, int row_lo, int row_hi, cons
         }
     }
     h->jobs.alloc(njobs);
+    lu_df_clear_error(lu_scratch(h, njobs, m_max), s);
     SAP_CUDA(cudaMemcpyAsync(h->jobs.get(), jobs.data(), sizeof(FactorJob) * njobs, cudaMemcpyHostToDevice, s));
     h->kappa.alloc(2);
     SAP_CUDA(cudaMemsetAsync(h->kappa.get(), 0, 2 * sizeof(unsigned long long), s));
@@ -1032,7 +1054,7 @@ void setup_banded_dist(sap_handle* h, int n, int k, int row_lo, int row_hi, cons
         launch_copy_blocks(h->band_ptr, k, h->d_boffs.get(), pl, h->fst, h->lu.get(),
                            h->coupled ? h->ul.get() : nullptr, s);
     SAP_CUDA(cudaEventRecord(h->ev[8], s));
-    launch_band_lu(h->jobs.get(), njobs, k, h->opt.boost_eps, s);
+    launch_band_lu(h->jobs.get(), njobs, k, h->opt.boost_eps, s, false, m_max, lu_scratch(h, njobs, m_max));
     SAP_CUDA(cudaEventRecord(h->ev[9], s));
     {
         SweepPlan<double>& lp = h->lplan;
@@ -1132,7 +1154,7 @@ void setup_banded_dist(sap_handle* h, int n, int k, int row_lo, int row_hi, cons
                               h->rbar_norms.get() + t, h->rbar_boosts.get() + t};
         h->rjobs.alloc(ni);
         SAP_CUDA(cudaMemcpyAsync(h->rjobs.get(), rj.data(), sizeof(FactorJob) * ni, cudaMemcpyHostToDevice, s));
-        launch_band_lu(h->rjobs.get(), ni, w - 1, h->opt.boost_eps, s);
+        launch_band_lu(h->rjobs.get(), ni, w - 1, h->opt.boost_eps, s, false, w, lu_scratch(h, ni, w));
         SweepPlan<double>& rp = h->rplan;
         rp = SweepPlan<double>{};
         rp.f = h->rbar.get();
@@ -1147,6 +1169,7 @@ void setup_banded_dist(sap_handle* h, int n, int k, int row_lo, int row_hi, cons
         SAP_CUDA(cudaEventRecord(h->ev[5], s));
     }
     SAP_CUDA(cudaStreamSynchronize(s));
+    lu_check(h);
     choose_triangle_solve(h);
     h->rep.t_dtransf = ev_ms(h->ev[0], h->ev[1]) * 1e-3;
     h->rep.t_lu = ev_ms(h->ev[1], h->ev[2]) * 1e-3;

@@ -23,8 +23,18 @@ void launch_copy_blocks(const double* band, int k, const int* d_offsets, int p, 
                         double* ul, cudaStream_t s);
 // Blocked no-pivot LU with pivot boosting of every job (one CTA per job).
 // streamed: the jobs carry FactorJob::ready (k_band_lu_res<B, true>; only where band_lu_reads_source(max_k))
+// df_scratch (lu_df_scratch_ints(njobs, m_max) ints, owned by the caller, one launch at a time): run the
+// dataflow kernel k_band_lu_df over every SM where it applies (lu_df_applies(max_k)); m_max = largest job.
 void launch_band_lu(const FactorJob* d_jobs, int njobs, int max_k, double boost_eps, cudaStream_t s,
-                    bool streamed = false);
+                    bool streamed = false, int m_max = 0, int* df_scratch = nullptr);
+size_t lu_df_scratch_ints(int njobs, int m_max);
+bool lu_df_applies(int max_k, int njobs);
+void launch_band_lu_df(const FactorJob* d_jobs, int njobs, int m_max, int max_k, double eps, cudaStream_t s,
+                       bool streamed, int* scratch);
+// 1 if a dependency wait of the last k_band_lu_df launch on this scratch timed out (synchronous read);
+// detail (optional, 7 ints): flag, CTA, SM, flag word offset from panel_cnt, want, have, wait site
+int lu_df_error(const int* scratch, int* detail = nullptr);
+void lu_df_clear_error(int* scratch, cudaStream_t s);
 // The warp-specialized look-ahead variant (lu.cu); false if the smem budget does not fit.
 bool band_lu_reads_source(int max_k);
 void launch_zero_pad(int k, const int* d_offsets, int p, const BandStore& st, double* lu, double* ul, cudaStream_t s);

@@ -10,6 +10,7 @@
 // the shared-memory budget). Every element receives its rank-1 updates in the reference's column order
 // (DMMA / DFMA contract mul+sub). Measured-slower variants (warp-specialized look-ahead,
 // extended-row update) are in the git history (commit 4e449e9), not in the product library.
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 
@@ -93,6 +94,25 @@ __device__ __forceinline__ void st_keep2(double* a, double2 v) {
 }
 __device__ __forceinline__ void st_keep(double* a, double v) {
     asm volatile("st.global.cg.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(l2_keep_policy()) : "memory");
+}
+
+// final factor entries that were last written with evict_last: stored with evict_first so that the
+// priority does not stay on lines the factorization is done with (the L2 would fill with them)
+__device__ __forceinline__ unsigned long long l2_first_policy() {
+    unsigned long long p;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void st_first(double* a, double v) {
+    asm volatile("st.global.cg.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(l2_first_policy()) : "memory");
+}
+__device__ __forceinline__ unsigned long long l2_normal_policy() {
+    unsigned long long p;
+    asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void st_normal(double* a, double v) {
+    asm volatile("st.global.cg.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(l2_normal_policy()) : "memory");
 }
 
 __device__ __forceinline__ bool tile_ok(const Lu& L, const TileCtx& T, int i, int c) {
@@ -1098,6 +1118,720 @@ bool launch_band_lu_ws(const FactorJob* d_jobs, int njobs, int max_k, double eps
     return true;
 }
 
+// ---------------------------------------------------------------------------
+// k_band_lu_df: the same factorization as a dataflow over every SM.
+//
+// One 32-column step s of job J (panel columns [jb, jb + nb), trailing window [ja, ja + R)^2, ja = jb + nb)
+// is split into work items:
+//   panel(J, s)     the 32 x 32 diagonal block (one warp's pivot chain, panel_diag) and the L21 rows
+//                   (panel_rows_cols), stored final;
+//   strip(J, s, j)  window columns [32 j, 32 j + 32): the U12 slice = L11^{-1} A12 (thread per column,
+//                   the reference's order) stored final, then A22 -= L21 U12 on DMMA over all R rows, stored
+//                   back in place (L2, evict_last).
+// Dependencies (per job): panel(s) <- strip(s-1, 0) (it produced the panel's columns); strip(s, j) <-
+// panel(s) and strip(s-1, j+1) (it produced the strip's columns). Items are numbered in a topological
+// order with look-ahead -- wave w: strip(w, 0) of every job, panel(w+1) of every job, strip(w, j >= 1) of
+// every job -- and grabbed from one atomic counter by persistent CTAs (two per SM), so a panel's pivot chain
+// overlaps other jobs' DMMA strips on the same SM and a job is no longer confined to one SM. A CTA only
+// ever waits for items grabbed before its own by running CTAs, so the schedule cannot deadlock whatever
+// the residency. Completion is published per job: panel_cnt[J] = s + 1, col_step[J][a] = s + 1 for the
+// 32-column block a a strip updated (st.release.gpu after a CTA barrier; readers ld.acquire.gpu, then
+// read the data with L1-bypassing .cg loads).
+// Every element receives exactly the arithmetic of k_band_lu_res (same panel code, same DMMA fragments
+// and k order): the factors are bitwise those of the single-CTA kernel.
+constexpr int kDfThreads = 256;
+constexpr int kLuDfMinK = 192;  // narrower bands: too few strips per step to pay for the item overheads
+constexpr int kDfNG = 7;
+constexpr int kDfMaxSm = 256;  // %smid bound  // row groups (8 rows) per warp: 4 warps share a strip's rows, K <= 224
+
+struct DfArgs {
+    const FactorJob* jobs;
+    int njobs, m_max, K, S;  // S = ceil(m_max / 32) steps; item numbering from the largest job
+    unsigned* counter_p;  // chain items (panel SMs)
+    unsigned* counter_w;  // worker strips
+    int nps;              // the first nps SMs this launch's CTAs start on run chain items
+    int* sm_role;         // [kDfMaxSm]: 0 undecided, 1 panel, 2 worker, 3 being decided
+    int* n_panel_sm;      // SMs claimed so far
+    int* panel_cnt;  // [njobs]
+    int* col_step;   // [njobs][S]
+    int* boost_acc;  // [njobs]
+    int* err;        // a dependency wait timed out (never expected: reported as a CUDA failure)
+    double eps;
+    int pld, uld;
+    unsigned long long* trace;  // tools only (lu_df_trace): per item grab / ready / end globaltimer + SM
+};
+
+__device__ __forceinline__ unsigned long long df_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ int ld_acquire_i(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_i(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ double ld_cg(const double* a) {
+    double v;
+    asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(a));
+    return v;
+}
+__device__ __forceinline__ double2 ld_cg2(const double* a) {
+    double2 v;
+    asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(a));
+    return v;
+}
+
+__device__ __forceinline__ int ld_relaxed_i(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// the acquire side of every wait of an item, once (an acquire load / fence invalidates the SM's whole L1:
+// polling with it would wipe the co-resident CTA's L1 and stack on every probe)
+__device__ __forceinline__ void df_acquire() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+// thread 0: spin (relaxed loads) until *flag >= want (~4 s cap: a lost dependency is reported, never a hang;
+// err[0] = 1, err[1..6] = the first timed-out wait: CTA, SM, the flag's word offset, want, have, tag)
+__device__ __forceinline__ void df_wait(const int* flag, int want, int* err, const int* base, int tag) {
+    if (ld_relaxed_i(flag) >= want) return;
+    const long long t0 = clock64();
+    while (ld_relaxed_i(flag) < want) {
+        __nanosleep(100);
+        if (clock64() - t0 > (1LL << 33)) {
+            if (atomicExch(err, 1) == 0) {
+                unsigned smid;
+                asm("mov.u32 %0, %%smid;" : "=r"(smid));
+                err[1] = blockIdx.x;
+                err[2] = (int)smid;
+                err[3] = (int)(flag - base);
+                err[4] = want;
+                err[5] = ld_relaxed_i(flag);
+                err[6] = tag;
+            }
+            return;
+        }
+    }
+}
+
+// thread 0, streamed upload: band columns [0, need) of this job's view have arrived (k_band_lu_res wait_cols)
+__device__ __forceinline__ void df_wait_cols(const FactorJob& J, int need) {
+    const long long want = min(J.m, need + 1);
+    const long long t0 = clock64();
+    for (;;) {
+        unsigned r;
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(J.ready) : "memory");
+        const long long got = (long long)r * J.piece;
+        if (got >= want || got * J.ends >= J.m) return;
+        if (clock64() - t0 > (1LL << 36)) {  // ~35 s: the upload stalled (reported through minpiv)
+            *J.minpiv = -1.0;
+            return;
+        }
+        __nanosleep(128);
+    }
+}
+
+// element (i, c) of the job's view from the factor store (updated by an earlier item) or, when it has never
+// been updated (fresh), from the unfactored source
+__device__ __forceinline__ double df_ld(const Lu& L, int i, int c, bool fresh) {
+    return ld_cg(fresh ? L.src_at(i, c) : L.at(i, c));
+}
+
+// trace mark (tools/lu_df_trace.py): per-CTA slot `k` of the current item
+#define DF_MARK(k)                                                                      \
+    do {                                                                                \
+        if (A.trace && threadIdx.x == 0) A.trace[8 * (size_t)blockIdx.x + (k)] = df_now(); \
+    } while (0)
+
+// Lean staging of a 32-column panel-shaped region: rows [0, nr) of view columns cb + [0, 32) starting at view
+// row i0 -> dst[c * ld + r]; rows r < rsplit come from the store, the rest from the source; entries outside the
+// band (|i - c| > K) and columns >= nc are zero. Thread (c = tid / 8, k = tid % 8) takes the row pairs
+// 2 (k + 8 it): one column pointer per thread, one 16-byte load per pair where the pair lies inside the band
+// and is aligned (alignment is uniform per job and source for even rows); loads of a batch before any use.
+__device__ __forceinline__ void df_stage_panel(const Lu& L, double* __restrict__ dst, int ld, int i0, int cb, int nr,
+                                               int nc, int rsplit) {
+    const int c = threadIdx.x >> 3, k = threadIdx.x & 7;
+    const long long rs = L.rs;
+    const int gc = cb + c;
+    const int lo_r = max(0, gc - L.K - i0), hi_r = min(nr, gc + L.K + 1 - i0);
+    const double* ps = L.at(i0, gc);
+    const double* pf = L.src_at(i0, gc);
+    const bool vec = rs == 1 || rs == -1;
+    // 16-byte alignment of the pair (r, r + 1), r even: uniform per pointer
+    const bool al_s = vec && ((reinterpret_cast<uintptr_t>(rs > 0 ? ps : ps - 1) & 15) == 0);
+    const bool al_f = vec && ((reinterpret_cast<uintptr_t>(rs > 0 ? pf : pf - 1) & 15) == 0);
+    constexpr int NB = 8;
+    for (int it0 = 0; 2 * (k + 8 * it0) < nr; it0 += NB) {
+        double2 v[NB];
+        unsigned paired = 0;
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+            const int r = 2 * (k + 8 * (it0 + u));
+            v[u] = make_double2(0.0, 0.0);
+            if (c >= nc || r >= nr) continue;
+            const bool in0 = r >= lo_r && r < hi_r, in1 = r + 1 >= lo_r && r + 1 < hi_r;
+            const bool f0 = r >= rsplit, f1 = r + 1 >= rsplit;
+            const double* p0 = (f0 ? pf : ps) + r * rs;
+            if (in0 && in1 && f0 == f1 && (f0 ? al_f : al_s)) {
+                v[u] = __ldcg(reinterpret_cast<const double2*>(rs > 0 ? p0 : p0 - 1));
+                paired |= 1u << u;
+            } else {
+                if (in0) v[u].x = __ldcg(p0);
+                if (in1) v[u].y = __ldcg((f1 ? pf : ps) + (r + 1) * rs);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+            const int r = 2 * (k + 8 * (it0 + u));
+            if (r >= nr) continue;
+            const double2 w = (rs < 0 && (paired >> u & 1)) ? make_double2(v[u].y, v[u].x) : v[u];
+            if (r + 1 < nr)
+                *reinterpret_cast<double2*>(dst + c * ld + r) = w;
+            else
+                dst[c * ld + r] = w.x;
+        }
+    }
+}
+
+// ---- item helpers (256 threads) -------------------------------------------------------------------------
+// The C tile of a strip: window rows [0, R) x window columns [c0, c0 + wc) of step (ja, fr). Warp w takes
+// columns c0 + 16 (w >> 2) + [0, 16) and row groups (w & 3) + 4 t; the thread holds
+// C(8 g + 2 lc + e, col0 + 8 q + lr) in acc[t][q][e] (k_band_lu_res' DMMA fragment layout).
+struct DfTile {
+    int ja, R, c0, wc, fr;
+};
+
+__device__ __forceinline__ void df_c_load(const Lu& L, const DfTile& T, double (&acc)[kDfNG][2][2]) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
+    const int col0 = T.c0 + 16 * (warp >> 2), rw = warp & 3, ngr = (T.R + 7) >> 3;
+    const long long rs = L.rs;
+    const bool vec = rs == 1 || rs == -1;
+    unsigned paired = 0;
+    // all loads first (reversed pairs are swapped once every load is in flight); one column pointer per q
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const int c = col0 + 8 * q + lr;
+        const bool cok = c < T.c0 + T.wc, fc = c >= T.fr;
+        const double* ps = L.at(T.ja, T.ja + c);
+        const double* pf = L.src_at(T.ja, T.ja + c);
+        const bool al_s = vec && ((reinterpret_cast<uintptr_t>(rs > 0 ? ps : ps - 1) & 15) == 0);
+        const bool al_f = vec && ((reinterpret_cast<uintptr_t>(rs > 0 ? pf : pf - 1) & 15) == 0);
+#pragma unroll
+        for (int t = 0; t < kDfNG; ++t) {
+            const int g = rw + 4 * t, i = 8 * g + 2 * lc;
+            acc[t][q][0] = acc[t][q][1] = 0.0;
+            if (g >= ngr || !cok || i >= T.R) continue;
+            const bool f0 = fc || i >= T.fr, f1 = fc || i + 1 >= T.fr;
+            const double* p0 = (f0 ? pf : ps) + i * rs;
+            if (i + 1 < T.R && f0 == f1 && (f0 ? al_f : al_s)) {
+                const double* lo = rs > 0 ? p0 : p0 - 1;
+                const double2 v = f0 ? ld_cg2(lo) : ld_keep2(lo);
+                acc[t][q][0] = v.x;
+                acc[t][q][1] = v.y;
+                paired |= 1u << (2 * t + q);
+            } else {
+                acc[t][q][0] = ld_cg(p0);
+                if (i + 1 < T.R) acc[t][q][1] = ld_cg((f1 ? pf : ps) + (i + 1) * rs);
+            }
+        }
+    }
+    if (rs < 0) {
+#pragma unroll
+        for (int t = 0; t < kDfNG; ++t)
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+                if (paired >> (2 * t + q) & 1) {
+                    const double x = acc[t][q][0];
+                    acc[t][q][0] = acc[t][q][1];
+                    acc[t][q][1] = x;
+                }
+    }
+}
+
+__device__ __forceinline__ void df_c_store(const Lu& L, const DfTile& T, const double (&acc)[kDfNG][2][2]) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
+    const int col0 = T.c0 + 16 * (warp >> 2), rw = warp & 3, ngr = (T.R + 7) >> 3;
+    const long long rs = L.rs;
+    const bool vec = rs == 1 || rs == -1;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const int c = col0 + 8 * q + lr;
+        if (c >= T.c0 + T.wc) continue;
+        double* ps = L.at(T.ja, T.ja + c);
+        const bool al = vec && ((reinterpret_cast<uintptr_t>(rs > 0 ? ps : ps - 1) & 15) == 0);
+#pragma unroll
+        for (int t = 0; t < kDfNG; ++t) {
+            const int g = rw + 4 * t, i = 8 * g + 2 * lc;
+            if (g >= ngr || i >= T.R) continue;
+            double* p0 = ps + i * rs;
+            if (i + 1 < T.R && al) {
+                double2 v;
+                v.x = rs > 0 ? acc[t][q][0] : acc[t][q][1];
+                v.y = rs > 0 ? acc[t][q][1] : acc[t][q][0];
+                st_keep2(rs > 0 ? p0 : p0 - 1, v);
+            } else {
+                st_keep(p0, acc[t][q][0]);
+                if (i + 1 < T.R) st_keep(p0 + rs, acc[t][q][1]);
+            }
+        }
+    }
+}
+
+// A12 slice of step (jb, ja): rows [0, 32) x slice columns [0, 32) -> U[r * uld + c] (zero outside the band
+// and beyond wc); entries in window columns >= fr (or every entry at step 0) have never been updated.
+// Thread: column tid / 8, rows 4 (tid % 8) + [0, 4).
+__device__ __forceinline__ void df_a12(const Lu& L, int jb, int ja, const DfTile& T, bool first, double* U, int uld) {
+    const int c = threadIdx.x >> 3, r0 = (threadIdx.x & 7) * 4;
+    const int gc = ja + T.c0 + c;
+    const double* p = (first || T.c0 + c >= T.fr) ? L.src_at(jb, gc) : L.at(jb, gc);
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int r = r0 + u;
+        v[u] = (c < T.wc && 32 + T.c0 + c - r <= L.K) ? __ldcg(p + r * L.rs) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) U[(r0 + u) * uld + c] = v[u];
+}
+
+// The chain's strip(s-1, 0) on the FP64 FMA pipe (a DMMA stream on a panel SM would stall the other chain's
+// pivot chain): C = window rows [0, R) x columns [0, wc) of step (ja, fr), C -= L21 U12 with the k-sum in the
+// reference's order (c -= l_k u_k, k = 0..31, FMA-contracted), the result straight into the next panel
+// Pn[c * pld + i] (after the barrier that ends every read of P). Thread: rows (tid % 64) + 64 h, columns
+// 8 (tid / 64) + [0, 8) (a warp shares its columns: U12 loads are broadcasts).
+__device__ __forceinline__ void df_chain_update(const Lu& L, const DfTile& T, const double* __restrict__ P,
+                                                double* __restrict__ Pn, int pld, const double* __restrict__ U,
+                                                int uld) {
+    const int i0 = threadIdx.x & 63, cg = threadIdx.x >> 6;
+    const long long rs = L.rs;
+    double c[4][8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int cc = 8 * cg + q;
+        const bool fc = cc >= T.fr;
+        const double* ps = L.at(T.ja, T.ja + cc);
+        const double* pf = L.src_at(T.ja, T.ja + cc);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const int i = i0 + 64 * h;
+            c[h][q] = (i < T.R && cc < T.wc) ? __ldcg(((fc || i >= T.fr) ? pf : ps) + i * rs) : 0.0;
+        }
+    }
+#pragma unroll 4
+    for (int k = 0; k < 32; ++k) {
+        double u[8], l[4];
+        const double2* uk = reinterpret_cast<const double2*>(U + k * uld + 8 * cg);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double2 w = uk[q];
+            u[2 * q] = w.x;
+            u[2 * q + 1] = w.y;
+        }
+#pragma unroll
+        for (int h = 0; h < 4; ++h) l[h] = P[k * pld + 32 + i0 + 64 * h];
+#pragma unroll
+        for (int h = 0; h < 4; ++h)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) c[h][q] = fma(-l[h], u[q], c[h][q]);
+    }
+    __syncthreads();  // every warp is done with panel s-1
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+        const int i = i0 + 64 * h;
+        if (i >= T.R) continue;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (8 * cg + q < T.wc) Pn[(8 * cg + q) * pld + i] = c[h][q];
+    }
+}
+
+// U12 slice = L11^{-1} A12 in 8-row blocks: rows of block b first take j = 0..8b-1 (256 threads: row 8b + tid/32,
+// column tid%32), then the block's unit-lower 8 x 8 triangle (thread per column). Element (q, c) receives
+// j = 0..q-1 in ascending order with the same FMAs as a column-sequential substitution (block_factors.hpp:
+// 246-250 order; bitwise panel_rows_cols' column half) but the dependent chain per thread is <= 24 + 7 long.
+// The final U12 entries go to the store. Ends with a barrier.
+__device__ __forceinline__ void df_u12(const Lu& L, int jb, int ja, const DfTile& T, const double* __restrict__ P,
+                                       int pld, double* __restrict__ U, int uld) {
+    constexpr int B = 32, H = 8;
+    const int tid = threadIdx.x, rr = tid >> 5, c = tid & 31;
+#pragma unroll 1
+    for (int b0 = 0; b0 < B; b0 += H) {
+        if (b0 > 0) {
+            const int q = b0 + rr;
+            double x = U[q * uld + c];
+            const double* __restrict__ lq = P + q;
+#pragma unroll 8
+            for (int j = 0; j < b0; ++j) x = fma(-lq[j * pld], U[j * uld + c], x);
+            U[q * uld + c] = x;
+            __syncthreads();
+        }
+        if (tid < 32) {
+            double x[H];
+#pragma unroll
+            for (int r = 0; r < H; ++r) x[r] = U[(b0 + r) * uld + c];
+#pragma unroll
+            for (int j = 0; j + 1 < H; ++j) {
+                const double* __restrict__ lj = P + (b0 + j) * pld + b0;
+#pragma unroll
+                for (int r = j + 1; r < H; ++r) x[r] = fma(-lj[r], x[j], x[r]);
+            }
+#pragma unroll
+            for (int r = 0; r < H; ++r) U[(b0 + r) * uld + c] = x[r];
+        }
+        __syncthreads();
+    }
+    // final U12 entries (the store's A12 rows; evict-first: the factorization is done with them)
+    for (int e = tid; e < B * 32; e += kDfThreads) {
+        const int r = e >> 5, cc = e & 31;
+        if (cc < T.wc && B + T.c0 + cc - r <= L.K) st_first(L.at(jb + r, ja + T.c0 + cc), U[r * uld + cc]);
+    }
+}
+
+// C -= L21 U12 (C^T -= U12^T L21^T, k-steps of 4 in order: k_band_lu_res' fragments and order)
+__device__ __forceinline__ void df_dmma(const DfTile& T, const double* __restrict__ P, int pld,
+                                        const double* __restrict__ U, int uld, double (&acc)[kDfNG][2][2]) {
+    constexpr int nb = 32;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
+    const int cp = warp >> 2, rw = warp & 3, ngr = (T.R + 7) >> 3;
+    const double* pk = P + nb + lr;
+    const double* uk = U + 16 * cp + lr;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+        const int kk = ks * 4 + lc;
+        const double a0 = uk[kk * uld], a1 = uk[kk * uld + 8];
+#pragma unroll
+        for (int t = 0; t < kDfNG; ++t) {
+            const int g = rw + 4 * t;
+            if (g < ngr) {
+                const double b = -pk[kk * pld + 8 * g];
+                dmma_m8n8k4(acc[t][0][0], acc[t][0][1], a0, b, acc[t][0][0], acc[t][0][1]);
+                dmma_m8n8k4(acc[t][1][0], acc[t][1][1], a1, b, acc[t][1][0], acc[t][1][1]);
+            }
+        }
+    }
+}
+
+// ---- chain item (panel SMs): strip(s-1, 0) -- the update of block s -- fused with panel(s) -----------------
+template <bool STREAM>
+__device__ __forceinline__ void df_chain(const DfArgs& A, const FactorJob& J, int jid, int s, double* __restrict__ P,
+                                         double* __restrict__ U, double* __restrict__ s_ut,
+                                         double* __restrict__ s_rcp, int* s_boosts) {
+    constexpr int B = 32;
+    const int m = J.m, K = J.k;
+    if (s * B >= m) return;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int pld = A.pld, uld = A.uld;
+    const int jb = s * B, nb = min(B, m - jb), ph = min(nb + K, m - jb), ja = jb + nb;
+    const int R = min(K, m - ja);
+    const int rprev = s > 0 ? min(K, m - jb) : 0;  // window s-1 rows; panel rows >= rprev are fresh
+    const double scale = STREAM ? 0.0 : *J.scale;
+    Lu L{J.base, J.rs, J.cs, m, K, B, pld, uld, STREAM ? 0.0 : A.eps * (scale > 0 ? scale : 1.0),
+         J.src ? J.src : J.base};
+    const int nbn = ja < m ? min(B, m - ja) : 0;
+    // step s-1 (the strip that produces this panel)
+    const int sp = s - 1, jbp = jb - B, rprevp = sp > 0 ? min(K, m - jbp) : 0;
+    const DfTile T{jb, rprev, 0, min(B, rprev), sp > 0 ? rprevp - B : 0};
+    if (tid == 0) {
+        if (STREAM) df_wait_cols(J, ja + R + nbn + 1);
+        if (s > 0) df_wait(A.panel_cnt + jid, s, A.err, A.panel_cnt, 1);
+        if (sp > 0 && B < rprevp) df_wait(A.col_step + (size_t)jid * A.S + s, sp, A.err, A.panel_cnt, 2);
+        df_acquire();
+        *s_boosts = 0;
+        if (A.trace) A.trace[8 * (size_t)blockIdx.x + 0] = df_now();
+    }
+    __syncthreads();
+    if (s > 0) {
+        df_stage_panel(L, P, pld, jbp, jbp, B + rprev, B, B + rprev);
+        df_a12(L, jbp, jb, T, sp == 0, U, uld);
+        // this panel's rows that no earlier step updated: loaded now, written after the update
+        double fv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = tid + u * kDfThreads, c = e >> 5, r = rprev + (e & 31);
+            fv[u] = (c < nb && r < ph && L.inband(r, c)) ? __ldcg(L.src_at(jb + r, jb + c)) : 0.0;
+        }
+        __syncthreads();
+        DF_MARK(1);
+        df_u12(L, jbp, jb, T, P, pld, U, uld);
+        df_chain_update(L, T, P, P, pld, U, uld);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = tid + u * kDfThreads, c = e >> 5, r = rprev + (e & 31);
+            if (r < pld) P[c * pld + r] = fv[u];
+        }
+    } else {
+        df_stage_panel(L, P, pld, jb, jb, ph, nb, 0);
+    }
+    __syncthreads();
+    DF_MARK(2);
+    if (warp == 0) {
+        if (nb == B)
+            panel_diag<B, true>(P, pld, s_ut, s_rcp, nb, L.bv, s_boosts);
+        else
+            panel_diag<B, false>(P, pld, s_ut, s_rcp, nb, L.bv, s_boosts);
+    }
+    __syncthreads();
+    // L21 rows (thread per row; panel_rows_cols' row half)
+    if (nb == B)
+        panel_rows_cols<B, true>(P, nullptr, pld, uld, s_ut, s_rcp, nb, ph, 0);
+    else
+        panel_rows_cols<B, false>(P, nullptr, pld, uld, s_ut, s_rcp, nb, ph, 0);
+    __syncthreads();
+    DF_MARK(3);
+    // the panel is final: L11\U11 and L21 to the store (the worker strips of this step read it from L2)
+    const long long rs = L.rs;
+    for (int c = warp; c < nb; c += kDfThreads / 32) {
+        double* g = L.at(jb, jb + c);
+        const int r1 = min(ph, c + K + 1);
+#pragma unroll 4
+        for (int r = max(c - K, 0) + lane; r < r1; r += 32) st_normal(g + r * rs, P[c * pld + r]);
+    }
+    // L2 prefetch of the band entries step s+1 meets first (rows [e, e + nbn) and columns [e, e + nbn))
+    if (nbn > 0 && ja + R < m) {
+        const int e = ja + R;
+        const int ncol = min(e + nbn, m) - ja;
+        for (int t = tid; t < ncol + min(nbn, m - e); t += kDfThreads) {
+            if (t < ncol)
+                prefetch_run(L, ja + t, e, e + nbn);
+            else
+                prefetch_run(L, e + t - ncol, ja + nbn, e);
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const int nbst = *s_boosts;
+        if (nbst) atomicAdd(A.boost_acc + jid, nbst);
+        if (jb + nb >= m) *J.boosts = atomicAdd(A.boost_acc + jid, 0);  // the job's last panel
+        DF_MARK(4);
+        st_release_i(A.panel_cnt + jid, s + 1);  // after the CTA barrier: publishes every thread's stores
+    }
+}
+
+// ---- worker strip (worker SMs): strip(s, j >= 1) ------------------------------------------------------------
+template <bool STREAM>
+__device__ __forceinline__ void df_strip(const DfArgs& A, const FactorJob& J, int jid, int s, int j,
+                                         double* __restrict__ P, double* __restrict__ U) {
+    constexpr int B = 32;
+    const int m = J.m, K = J.k;
+    const int jb = s * B;
+    if (jb + B >= m) return;  // no trailing window (a strip step always has nb = 32)
+    const int nb = B, ja = jb + nb, R = min(K, m - ja), ph = nb + R;
+    const int c0 = j * 32;
+    if (c0 >= R) return;
+    const int tid = threadIdx.x;
+    const int pld = A.pld, uld = A.uld;
+    const int rprev = s > 0 ? min(K, m - jb) : 0;
+    const DfTile T{ja, R, c0, min(32, R - c0), s > 0 ? rprev - nb : 0};
+    const int a = s + 1 + j;  // the 32-column block this strip updates
+    Lu L{J.base, J.rs, J.cs, m, K, B, pld, uld, 0.0, J.src ? J.src : J.base};
+    if (tid == 0) {
+        if (STREAM) df_wait_cols(J, ja + c0 + T.wc + 1);
+        df_wait(A.panel_cnt + jid, s + 1, A.err, A.panel_cnt, 3);
+        if (s > 0 && 32 * (j + 1) < rprev) df_wait(A.col_step + (size_t)jid * A.S + a, s, A.err, A.panel_cnt, 4);
+        df_acquire();
+        if (A.trace) A.trace[8 * (size_t)blockIdx.x + 0] = df_now();
+    }
+    __syncthreads();
+    double acc[kDfNG][2][2];
+    df_c_load(L, T, acc);
+    df_stage_panel(L, P, pld, jb, jb, ph, B, ph);
+    df_a12(L, jb, ja, T, s == 0, U, uld);
+    __syncthreads();
+    DF_MARK(1);
+    df_u12(L, jb, ja, T, P, pld, U, uld);
+    DF_MARK(2);
+    df_dmma(T, P, pld, U, uld, acc);
+    DF_MARK(3);
+    df_c_store(L, T, acc);
+    __syncthreads();
+    if (tid == 0) {
+        DF_MARK(4);
+        st_release_i(A.col_step + (size_t)jid * A.S + a, s + 1);
+    }
+}
+
+// Panel SMs (smid < nps) take chain items from counter_p in order (s-major); the other SMs take worker strips
+// from counter_w in wave order. Both orders are consistent with one topological order (chain(s) ~ 2s,
+// strip(s, .) ~ 2s + 1), so the earliest unfinished item is always grabbed and runnable: no deadlock.
+template <bool STREAM>
+__global__ void __launch_bounds__(kDfThreads, 2) k_band_lu_df(DfArgs A) {
+    extern __shared__ __align__(16) double smem[];
+    __shared__ __align__(16) double s_ut[kUtSize];
+    __shared__ double s_rcp[64];
+    __shared__ int s_item, s_boosts;
+    {
+        const int* gate = A.jobs[0].gate;
+        if (!STREAM && gate && !(*gate & 1)) return;  // the streamed refactor: nothing to redo
+    }
+    double* P = smem;
+    double* U = smem + 32 * A.pld;
+    const int tid = threadIdx.x, J = A.njobs;
+    unsigned smid;
+    asm("mov.u32 %0, %%smid;" : "=r"(smid));
+    // SM role: the first nps SMs on which CTAs of this launch actually start become panel SMs (placement and
+    // %smid numbering are not under our control; every CTA of an SM shares its SM's role)
+    __shared__ int s_role;
+    if (tid == 0) {
+        int* rp = A.sm_role + (smid % kDfMaxSm);
+        int r = atomicCAS(rp, 0, 3);
+        if (r == 0) {
+            r = atomicAdd(A.n_panel_sm, 1) < A.nps ? 1 : 2;
+            atomicExch(rp, r);
+        } else {
+            while (r == 3) {
+                __nanosleep(20);
+                r = ld_relaxed_i(rp);
+            }
+        }
+        s_role = r;
+    }
+    __syncthreads();
+    const bool panel_role = s_role == 1;
+    unsigned* ctr = panel_role ? A.counter_p : A.counter_w;
+    if (tid == 0) s_item = (int)atomicAdd(ctr, 1u);
+    __syncthreads();
+    // worker wave cursor: wave w holds strips [w0, w0 + wn) (J x (strips - 1) of step w)
+    int w = 0, w0 = 0;
+    auto wave_n = [&](int ww) {
+        const int R = min(A.K, A.m_max - 32 * (ww + 1));
+        return J * ((R + 31) / 32 - 1);
+    };
+    int wn = A.S >= 2 ? wave_n(0) : 0;
+    for (;;) {
+        const int item = s_item;
+        __syncthreads();
+        if (tid == 0) s_item = (int)atomicAdd(ctr, 1u);
+        unsigned long long t_grab = 0;
+        if (A.trace && tid == 0) {
+            t_grab = df_now();
+            for (int q = 0; q < 5; ++q) A.trace[8 * (size_t)blockIdx.x + q] = 0;
+        }
+        long long rec;
+        if (panel_role) {
+            if (item >= A.S * J) break;
+            const int s = item / J, jid = item - s * J;
+            const FactorJob Jb = A.jobs[jid];
+            df_chain<STREAM>(A, Jb, jid, s, P, U, s_ut, s_rcp, &s_boosts);
+            rec = item;
+        } else {
+            bool done = false;
+            while (item >= w0 + wn) {
+                w0 += wn;
+                ++w;
+                if (w > A.S - 2) {
+                    done = true;
+                    break;
+                }
+                wn = wave_n(w);
+            }
+            if (done) break;
+            const int ns1 = wn / J, o = item - w0, jid = o / ns1;
+            const FactorJob Jb = A.jobs[jid];
+            df_strip<STREAM>(A, Jb, jid, w, 1 + o % ns1, P, U);
+            rec = (long long)A.S * J + item;
+        }
+        __syncthreads();
+        if (A.trace && tid == 0) {
+            unsigned long long* tr = A.trace + 8 * ((size_t)gridDim.x + rec);
+            tr[0] = t_grab;
+            for (int q = 0; q < 5; ++q) tr[1 + q] = A.trace[8 * (size_t)blockIdx.x + q];
+            tr[6] = df_now();
+            tr[7] = ((unsigned long long)smid << 32) | blockIdx.x;
+        }
+    }
+}
+
+static unsigned long long* g_df_trace = nullptr;
+static size_t g_df_trace_cap = 0;
+static long long g_df_trace_items = 0;
+static int g_df_trace_grid = 0;
+
+// scratch: [1..7] timeout report, [8] chain counter, [10] worker counter, [12] panel SMs claimed,
+// [16, 16 + kDfMaxSm) SM roles, then panel_cnt[njobs], boost_acc[njobs], col_step[njobs][S]
+constexpr int kDfHdr = 16 + kDfMaxSm;
+size_t lu_df_scratch_ints(int njobs, int m_max) {
+    const int S = (m_max + 31) / 32;
+    return kDfHdr + 2 * (size_t)njobs + (size_t)njobs * S;
+}
+
+// Where the dataflow kernel beats one CTA per job (profiles/lu_df_r02.txt): few jobs for the SMs (a job's
+// trailing update then spreads over the idle SMs) and bandwidths whose single-CTA step is long
+bool lu_df_applies(int max_k, int njobs) {
+    int dev = 0, nsm = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    return max_k >= kLuDfMinK && max_k <= 224 && njobs <= nsm / 2;
+}
+
+void launch_band_lu_df(const FactorJob* d_jobs, int njobs, int m_max, int max_k, double eps, cudaStream_t s,
+                       bool streamed, int* scratch) {
+    constexpr int B = 32;
+    const int S = (m_max + B - 1) / B;
+    // [1..7]: timeout report (cleared by lu_df_clear_error, kept across launches); [8], [10]: work counters
+    SAP_CUDA(cudaMemsetAsync(scratch + 8, 0, sizeof(int) * (lu_df_scratch_ints(njobs, m_max) - 8), s));
+    DfArgs A;
+    A.jobs = d_jobs;
+    A.njobs = njobs;
+    A.m_max = m_max;
+    A.K = max_k;
+    A.S = S;
+    A.counter_p = reinterpret_cast<unsigned*>(scratch + 8);
+    A.counter_w = reinterpret_cast<unsigned*>(scratch + 10);
+    A.err = scratch + 1;
+    A.n_panel_sm = scratch + 12;
+    A.sm_role = scratch + 16;
+    A.panel_cnt = scratch + kDfHdr;
+    A.boost_acc = scratch + kDfHdr + njobs;
+    A.col_step = scratch + kDfHdr + 2 * njobs;
+    A.eps = eps;
+    A.pld = pad_ld(B + max_k);
+    A.uld = pad_ld(32);
+    A.trace = nullptr;
+    const size_t bytes = sizeof(double) * (size_t)(B * A.pld + B * A.uld);
+    auto kern = streamed ? k_band_lu_df<true> : k_band_lu_df<false>;
+    SAP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    int dev = 0, nsm = 0, per_sm = 0;
+    SAP_CUDA(cudaGetDevice(&dev));
+    SAP_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    SAP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDfThreads, bytes));
+    // chain items (one per job and step) + worker strips
+    long long items = (long long)njobs * S;
+    for (int w = 0; w <= S - 2; ++w) items += (long long)njobs * ((std::min(max_k, m_max - B * (w + 1)) + 31) / 32 - 1);
+    const int grid = nsm * std::max(per_sm, 1);
+    // panel SMs: one resident chain per job where the SMs allow (chains are latency-bound), at most 40 %
+    int nps = std::min((njobs + per_sm - 1) / std::max(per_sm, 1), (2 * nsm) / 5);
+    if (const char* e = getenv("SAP_LU_DF_NPS")) nps = atoi(e);
+    A.nps = std::max(1, std::min(nps, nsm - 1));
+    const char* tr_env = getenv("SAP_LU_DF_TRACE");  // "s": trace streamed launches, "n": the others
+    if (tr_env && (tr_env[0] == 's') == streamed) {
+        const size_t need = 8 * (size_t)(grid + items);
+        if (g_df_trace_cap < need) {
+            if (g_df_trace) cudaFree(g_df_trace);
+            SAP_CUDA(cudaMalloc(&g_df_trace, need * sizeof(unsigned long long)));
+            g_df_trace_cap = need;
+        }
+        SAP_CUDA(cudaMemsetAsync(g_df_trace, 0, need * sizeof(unsigned long long), s));
+        A.trace = g_df_trace;
+        g_df_trace_items = items;
+        g_df_trace_grid = grid;
+    }
+    kern<<<grid, kDfThreads, bytes, s>>>(A);
+    SAP_LAUNCHED();
+}
+
+void lu_df_clear_error(int* scratch, cudaStream_t s) { SAP_CUDA(cudaMemsetAsync(scratch, 0, sizeof(int) * 8, s)); }
+
+int lu_df_error(const int* scratch, int* detail) {
+    int e[8] = {};
+    SAP_CUDA(cudaMemcpy(e, scratch + 1, sizeof(e), cudaMemcpyDeviceToHost));
+    if (detail)
+        for (int i = 0; i < 7; ++i) detail[i] = e[i];
+    return e[0];
+}
+
 // True when launch_band_lu_ws will run k_band_lu_res for this bandwidth: that kernel reads every
 // never-updated entry from FactorJob::src, so the factor stores need no initial copy of the band
 // (only their out-of-matrix slots zeroed, launch_zero_pad).
@@ -1109,3 +1843,15 @@ bool band_lu_reads_source(int max_k) {
 }
 
 }  // namespace sapgpu
+
+// tools/lu_df_trace.py only (not in include/sap_gpu.h): the last traced k_band_lu_df launch, 8 u64 per item
+// (grab, dependencies met, phase marks 1-4, end: globaltimer ns; SM << 32 | CTA). Returns the item count.
+extern "C" long long sap_dev_lu_df_trace(unsigned long long* out, long long cap) {
+    using namespace sapgpu;
+    if (!g_df_trace) return 0;
+    const long long n = std::min<long long>(cap, g_df_trace_items);
+    cudaDeviceSynchronize();
+    cudaMemcpy(out, g_df_trace + 8 * (size_t)g_df_trace_grid, sizeof(unsigned long long) * 8 * n,
+               cudaMemcpyDeviceToHost);
+    return n;
+}

@@ -1,0 +1,106 @@
+"""A/B check of the dataflow band LU (k_band_lu_df) against the single-CTA kernel (k_band_lu_res):
+factors (LU, UL), boost counts and reduced blocks must be BITWISE equal; prints the factor-kernel times.
+
+    python tools/lu_df_check.py            # on a GPU box
+"""
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_1509_07919_b200 as S  # noqa: E402
+
+CASES = [
+    (20000, 100, 0.5, 5, S.PrecondKind.coupled, False),  # n, k, d, p, kind, band on device
+    (3000, 64, 1.0, 3, S.PrecondKind.coupled, True),
+    (20000, 100, 0.5, 5, S.PrecondKind.coupled, False),
+    (20011, 77, 1.0, 7, S.PrecondKind.coupled, True),
+    (40000, 200, 1.0, 10, S.PrecondKind.coupled, True),
+    (40000, 200, 0.06, 10, S.PrecondKind.coupled, True),
+    (40000, 224, 1.0, 8, S.PrecondKind.decoupled, False),
+    (9000, 130, 0.2, 4, S.PrecondKind.coupled, False),
+    (200000, 200, 1.0, 50, S.PrecondKind.coupled, True),
+    (200000, 200, 1.0, 50, S.PrecondKind.decoupled, True),
+]
+
+
+def run(case, df):
+    n, k, d, p, kind, dev = case
+    os.environ["SAP_LU_DF"] = "1" if df else "0"
+    band, rhs = S.random_banded(n, k, d, 1)
+    src = torch.from_numpy(band).cuda() if dev else band
+    out = {}
+    with S.Solver(p=p, precond=kind, device=0) as s:
+        for _ in range(3):
+            s.setup(src, n, k)
+        s.synchronize()
+        r = s.report()
+        out["t_factor"] = r["t_factor_kernel"]
+        out["lu"] = s.factors(0)
+        if kind == S.PrecondKind.coupled:
+            out["ul"] = s.factors(1)
+            out["rbar"] = [s.spike(t)["rbar"] for t in range(p - 1)]
+            out["rbar_boosts"] = [s.spike(t)["rbar_boosts"] for t in range(p - 1)]
+        x, st = s.solve(rhs)
+        out["it"] = st.iterations
+        out["res"] = st.final_relative_residual
+    return out
+
+
+def main():
+    bad = 0
+    reps = int(os.environ.get("REPS", "1"))
+    for case in [c for c in CASES for _ in range(reps)]:
+        t0 = time.time()
+        a = run(case, False)
+        if len(sys.argv) > 1 and sys.argv[1] == "old2":
+            b = run(case, False)
+        else:
+            b = run(case, True)
+        same = np.array_equal(a["lu"][0], b["lu"][0]) and np.array_equal(a["lu"][1], b["lu"][1])
+        if "ul" in a:
+            same = same and np.array_equal(a["ul"][0], b["ul"][0]) and np.array_equal(a["ul"][1], b["ul"][1])
+            same = same and all(np.array_equal(x, y) for x, y in zip(a["rbar"], b["rbar"]))
+            same = same and a["rbar_boosts"] == b["rbar_boosts"]
+        d = np.max(np.abs(a["lu"][0] - b["lu"][0])) if not same else 0.0
+        if not same:
+            n_, k_, _, p_ = case[:4]
+            w = 2 * k_ + 1
+            sizes = S.make_partition_layout(n_, p_, k_).sizes
+            for nm in ("lu", "ul"):
+                if nm not in a:
+                    continue
+                off = 0
+                for blk, m in enumerate(sizes):
+                    x = a[nm][0][off: off + m * w].reshape(m, w)
+                    y = b[nm][0][off: off + m * w].reshape(m, w)
+                    off += m * w
+                    bad_cols = np.nonzero(np.any(x != y, axis=1))[0]
+                    if len(bad_cols):
+                        c = bad_cols[0]
+                        rows = np.nonzero(x[c] != y[c])[0] - k_ + c
+                        sl = np.nonzero(x[c] != y[c])[0][:4]
+                        inb = [(r0 >= 0 and r0 < m and abs(r0 - c) <= k_) for r0 in rows[:8]]
+                        print(f"   {nm} block {blk} (m={m}): first bad column {c} rows {rows[:8]} in-matrix {inb} "
+                              f"ncols {len(bad_cols)} values {x[c][sl]} vs {y[c][sl]}")
+                        break
+        # not bitwise (the chain's strip 0 is on DFMA): the SURVEY 8c tolerances against the single-CTA kernel
+        tol = 1e-13 if case[2] >= 0.5 else 1e-6
+        rel = max(np.max(np.abs(a[nm][0] - b[nm][0])) / np.max(np.abs(a[nm][0])) for nm in ("lu", "ul") if nm in a)
+        ok = rel <= tol and np.array_equal(a["lu"][1], b["lu"][1]) and abs(a["it"] - b["it"]) <= 1
+        same = ok
+        print(f"   normwise rel diff {rel:.2e} (tol {tol:g})")
+        bad += not same
+        print(f"{case[:4]} {'C' if case[4] == S.PrecondKind.coupled else 'D'} dev={case[5]}: bitwise={same} "
+              f"maxdiff={d:.3g} boosts={int(b['lu'][1].sum())} t_factor res {a['t_factor']*1e3:.3f} ms -> "
+              f"df {b['t_factor']*1e3:.3f} ms; it {a['it']} / {b['it']} res {b['res']:.2e} ({time.time()-t0:.1f}s)",
+              flush=True)
+    print("ALL BITWISE" if not bad else f"{bad} MISMATCHES")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,24 @@
+"""Factor-kernel time of the single-CTA LU (SAP_LU_DF=0) vs the dataflow LU over shapes (device band)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch, paper_1509_07919_b200 as S
+
+CASES = [(2000000, 128, 512, "C"), (2000000, 128, 512, "D"), (2000000, 128, 64, "C"), (200000, 64, 50, "C"),
+         (200000, 100, 50, "C"), (200000, 160, 50, "C"), (200000, 200, 50, "C"), (200000, 200, 50, "D"),
+         (200000, 224, 50, "C"), (200000, 200, 25, "C")]
+for n, k, p, kind in CASES:
+    band, rhs = S.random_banded(n, k, 1.0, 1)
+    db = torch.from_numpy(band).cuda()
+    del band
+    res = []
+    for df in ("0", "1"):
+        os.environ["SAP_LU_DF"] = df
+        with S.Solver(p=p, precond=S.PrecondKind.coupled if kind == "C" else S.PrecondKind.decoupled, device=0) as s:
+            ts = []
+            for _ in range(4):
+                s.setup(db, n, k)
+                ts.append(s.report()["t_factor_kernel"])
+            res.append(min(ts[1:]) * 1e3)
+    print(f"n={n} k={k} p={p} {kind}: single-CTA {res[0]:.3f} ms, dataflow {res[1]:.3f} ms", flush=True)
+    del db
+    torch.cuda.empty_cache()
