@@ -1142,7 +1142,8 @@ bool launch_band_lu_ws(const FactorJob* d_jobs, int njobs, int max_k, double eps
 constexpr int kDfThreads = 256;
 constexpr int kLuDfMinK = 192;  // narrower bands: too few strips per step to pay for the item overheads
 constexpr int kDfNG = 7;
-constexpr int kDfMaxSm = 256;  // %smid bound  // row groups (8 rows) per warp: 4 warps share a strip's rows, K <= 224
+constexpr int kDfMaxSm = 256;  // %smid bound
+constexpr int kDfG = 3;        // strips per worker item (one panel load and one U12 solve for all of them)  // row groups (8 rows) per warp: 4 warps share a strip's rows, K <= 224
 
 struct DfArgs {
     const FactorJob* jobs;
@@ -1381,21 +1382,29 @@ __device__ __forceinline__ void df_c_store(const Lu& L, const DfTile& T, const d
     }
 }
 
-// A12 slice of step (jb, ja): rows [0, 32) x slice columns [0, 32) -> U[r * uld + c] (zero outside the band
-// and beyond wc); entries in window columns >= fr (or every entry at step 0) have never been updated.
-// Thread: column tid / 8, rows 4 (tid % 8) + [0, 4).
-__device__ __forceinline__ void df_a12(const Lu& L, int jb, int ja, const DfTile& T, bool first, double* U, int uld) {
-    const int c = threadIdx.x >> 3, r0 = (threadIdx.x & 7) * 4;
-    const int gc = ja + T.c0 + c;
-    const double* p = (first || T.c0 + c >= T.fr) ? L.src_at(jb, gc) : L.at(jb, gc);
-    double v[4];
+// A12 rows of step (jb, ja) for window columns [c0, c0 + nc) (nc <= 32 kDfG): -> U[r * uld + c] (zero outside
+// the band and for c >= wc); entries in window columns >= fr (or every entry at step 0) have never been
+// updated. Column-major over the threads (coalesced band columns), four loads in flight per thread.
+__device__ __forceinline__ void df_a12(const Lu& L, int jb, int ja, int c0, int nc, int wc, int fr, bool first,
+                                       double* __restrict__ U, int uld) {
+    const int total = 32 * nc;
+    for (int e0 = threadIdx.x; e0 < total; e0 += 4 * kDfThreads) {
+        double v[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const int r = r0 + u;
-        v[u] = (c < T.wc && 32 + T.c0 + c - r <= L.K) ? __ldcg(p + r * L.rs) : 0.0;
+        for (int u = 0; u < 4; ++u) {
+            const int e = e0 + u * kDfThreads, c = e >> 5, r = e & 31;
+            v[u] = 0.0;
+            if (e < total && c < wc && 32 + c0 + c - r <= L.K) {
+                const int gc = ja + c0 + c;
+                v[u] = __ldcg((first || c0 + c >= fr) ? L.src_at(jb + r, gc) : L.at(jb + r, gc));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = e0 + u * kDfThreads;
+            if (e < total) U[(e & 31) * uld + (e >> 5)] = v[u];
+        }
     }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) U[(r0 + u) * uld + c] = v[u];
 }
 
 // The chain's strip(s-1, 0) on the FP64 FMA pipe (a DMMA stream on a panel SM would stall the other chain's
@@ -1449,30 +1458,39 @@ __device__ __forceinline__ void df_chain_update(const Lu& L, const DfTile& T, co
     }
 }
 
-// U12 slice = L11^{-1} A12 in 8-row blocks: rows of block b first take j = 0..8b-1 (256 threads: row 8b + tid/32,
-// column tid%32), then the block's unit-lower 8 x 8 triangle (thread per column). Element (q, c) receives
-// j = 0..q-1 in ascending order with the same FMAs as a column-sequential substitution (block_factors.hpp:
-// 246-250 order; bitwise panel_rows_cols' column half) but the dependent chain per thread is <= 24 + 7 long.
-// The final U12 entries go to the store. Ends with a barrier.
-__device__ __forceinline__ void df_u12(const Lu& L, int jb, int ja, const DfTile& T, const double* __restrict__ P,
-                                       int pld, double* __restrict__ U, int uld) {
+// U12 = L11^{-1} A12 for nc (<= 32 kDfG) columns, in 8-row blocks: rows of block b first take j = 0..8b-1 (256
+// threads: row 8b + tid/32, columns tid%32 + 32 g), then the block's unit-lower 8 x 8 triangle (thread per
+// column). Element (q, c) receives j = 0..q-1 in ascending order with the same FMAs as a column-sequential
+// substitution (block_factors.hpp:246-250 order; bitwise panel_rows_cols' column half) with dependent chains
+// <= 24 + 7 long. The final U12 entries (window columns [c0, c0 + wc)) go to the store. Ends with a barrier.
+__device__ __forceinline__ void df_u12(const Lu& L, int jb, int ja, int c0, int nc, int wc,
+                                       const double* __restrict__ P, int pld, double* __restrict__ U, int uld) {
     constexpr int B = 32, H = 8;
     const int tid = threadIdx.x, rr = tid >> 5, c = tid & 31;
 #pragma unroll 1
     for (int b0 = 0; b0 < B; b0 += H) {
         if (b0 > 0) {
             const int q = b0 + rr;
-            double x = U[q * uld + c];
+            double x[kDfG];
+#pragma unroll
+            for (int g = 0; g < kDfG; ++g) x[g] = c + 32 * g < nc ? U[q * uld + c + 32 * g] : 0.0;
             const double* __restrict__ lq = P + q;
-#pragma unroll 8
-            for (int j = 0; j < b0; ++j) x = fma(-lq[j * pld], U[j * uld + c], x);
-            U[q * uld + c] = x;
+#pragma unroll 4
+            for (int j = 0; j < b0; ++j) {
+                const double l = lq[j * pld];
+#pragma unroll
+                for (int g = 0; g < kDfG; ++g)
+                    if (c + 32 * g < nc) x[g] = fma(-l, U[j * uld + c + 32 * g], x[g]);
+            }
+#pragma unroll
+            for (int g = 0; g < kDfG; ++g)
+                if (c + 32 * g < nc) U[q * uld + c + 32 * g] = x[g];
             __syncthreads();
         }
-        if (tid < 32) {
+        if (tid < nc) {
             double x[H];
 #pragma unroll
-            for (int r = 0; r < H; ++r) x[r] = U[(b0 + r) * uld + c];
+            for (int r = 0; r < H; ++r) x[r] = U[(b0 + r) * uld + tid];
 #pragma unroll
             for (int j = 0; j + 1 < H; ++j) {
                 const double* __restrict__ lj = P + (b0 + j) * pld + b0;
@@ -1480,14 +1498,14 @@ __device__ __forceinline__ void df_u12(const Lu& L, int jb, int ja, const DfTile
                 for (int r = j + 1; r < H; ++r) x[r] = fma(-lj[r], x[j], x[r]);
             }
 #pragma unroll
-            for (int r = 0; r < H; ++r) U[(b0 + r) * uld + c] = x[r];
+            for (int r = 0; r < H; ++r) U[(b0 + r) * uld + tid] = x[r];
         }
         __syncthreads();
     }
     // final U12 entries (the store's A12 rows; evict-first: the factorization is done with them)
-    for (int e = tid; e < B * 32; e += kDfThreads) {
-        const int r = e >> 5, cc = e & 31;
-        if (cc < T.wc && B + T.c0 + cc - r <= L.K) st_first(L.at(jb + r, ja + T.c0 + cc), U[r * uld + cc]);
+    for (int e = tid; e < B * nc; e += kDfThreads) {
+        const int cc = e >> 5, r = e & 31;
+        if (cc < wc && B + c0 + cc - r <= L.K) st_first(L.at(jb + r, ja + c0 + cc), U[r * uld + cc]);
     }
 }
 
@@ -1546,7 +1564,7 @@ __device__ __forceinline__ void df_chain(const DfArgs& A, const FactorJob& J, in
     __syncthreads();
     if (s > 0) {
         df_stage_panel(L, P, pld, jbp, jbp, B + rprev, B, B + rprev);
-        df_a12(L, jbp, jb, T, sp == 0, U, uld);
+        df_a12(L, jbp, jb, 0, 32, T.wc, T.fr, sp == 0, U, uld);
         // this panel's rows that no earlier step updated: loaded now, written after the update
         double fv[4];
 #pragma unroll
@@ -1556,7 +1574,7 @@ __device__ __forceinline__ void df_chain(const DfArgs& A, const FactorJob& J, in
         }
         __syncthreads();
         DF_MARK(1);
-        df_u12(L, jbp, jb, T, P, pld, U, uld);
+        df_u12(L, jbp, jb, 0, 32, T.wc, P, pld, U, uld);
         df_chain_update(L, T, P, P, pld, U, uld);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -1611,51 +1629,58 @@ __device__ __forceinline__ void df_chain(const DfArgs& A, const FactorJob& J, in
     }
 }
 
-// ---- worker strip (worker SMs): strip(s, j >= 1) ------------------------------------------------------------
+// ---- worker item (worker SMs): strips j = 1 + kDfG g .. of step s -------------------------------------------
+// One panel load, one A12 load and one U12 solve for the group; then per strip: C tile in, DMMA, C tile out and
+// its column block's flag released at once (the chain two steps on waits for strip 1 only).
 template <bool STREAM>
-__device__ __forceinline__ void df_strip(const DfArgs& A, const FactorJob& J, int jid, int s, int j,
-                                         double* __restrict__ P, double* __restrict__ U) {
+__device__ __forceinline__ void df_worker(const DfArgs& A, const FactorJob& J, int jid, int s, int g,
+                                          double* __restrict__ P, double* __restrict__ U) {
     constexpr int B = 32;
     const int m = J.m, K = J.k;
     const int jb = s * B;
     if (jb + B >= m) return;  // no trailing window (a strip step always has nb = 32)
     const int nb = B, ja = jb + nb, R = min(K, m - ja), ph = nb + R;
-    const int c0 = j * 32;
+    const int j0 = 1 + kDfG * g, c0 = 32 * j0;
     if (c0 >= R) return;
+    const int j1 = min(j0 + kDfG, (R + 31) / 32);  // strips [j0, j1)
     const int tid = threadIdx.x;
     const int pld = A.pld, uld = A.uld;
     const int rprev = s > 0 ? min(K, m - jb) : 0;
-    const DfTile T{ja, R, c0, min(32, R - c0), s > 0 ? rprev - nb : 0};
-    const int a = s + 1 + j;  // the 32-column block this strip updates
+    const int fr = s > 0 ? rprev - nb : 0;
     Lu L{J.base, J.rs, J.cs, m, K, B, pld, uld, 0.0, J.src ? J.src : J.base};
     if (tid == 0) {
-        if (STREAM) df_wait_cols(J, ja + c0 + T.wc + 1);
+        if (STREAM) df_wait_cols(J, ja + R + 1);
         df_wait(A.panel_cnt + jid, s + 1, A.err, A.panel_cnt, 3);
-        if (s > 0 && 32 * (j + 1) < rprev) df_wait(A.col_step + (size_t)jid * A.S + a, s, A.err, A.panel_cnt, 4);
+        for (int j = j0; j < j1; ++j)
+            if (s > 0 && 32 * (j + 1) < rprev)
+                df_wait(A.col_step + (size_t)jid * A.S + s + 1 + j, s, A.err, A.panel_cnt, 4);
         df_acquire();
         if (A.trace) A.trace[8 * (size_t)blockIdx.x + 0] = df_now();
     }
     __syncthreads();
-    double acc[kDfNG][2][2];
-    df_c_load(L, T, acc);
     df_stage_panel(L, P, pld, jb, jb, ph, B, ph);
-    df_a12(L, jb, ja, T, s == 0, U, uld);
+    df_a12(L, jb, ja, c0, 32 * (j1 - j0), R - c0, fr, s == 0, U, uld);
     __syncthreads();
     DF_MARK(1);
-    df_u12(L, jb, ja, T, P, pld, U, uld);
+    df_u12(L, jb, ja, c0, 32 * (j1 - j0), R - c0, P, pld, U, uld);
     DF_MARK(2);
-    df_dmma(T, P, pld, U, uld, acc);
-    DF_MARK(3);
-    df_c_store(L, T, acc);
-    __syncthreads();
+    for (int j = j0; j < j1; ++j) {
+        const DfTile T{ja, R, 32 * j, min(32, R - 32 * j), fr};
+        double acc[kDfNG][2][2];
+        df_c_load(L, T, acc);
+        df_dmma(T, P, pld, U + 32 * (j - j0), uld, acc);
+        df_c_store(L, T, acc);
+        __syncthreads();
+        if (tid == 0) st_release_i(A.col_step + (size_t)jid * A.S + s + 1 + j, s + 1);
+    }
     if (tid == 0) {
+        DF_MARK(3);
         DF_MARK(4);
-        st_release_i(A.col_step + (size_t)jid * A.S + a, s + 1);
     }
 }
 
-// Panel SMs (smid < nps) take chain items from counter_p in order (s-major); the other SMs take worker strips
-// from counter_w in wave order. Both orders are consistent with one topological order (chain(s) ~ 2s,
+// Panel SMs take chain items from counter_p in order (s-major); the other SMs take worker items from counter_w
+// in wave order. Both orders are consistent with one topological order (chain(s) ~ 2s,
 // strip(s, .) ~ 2s + 1), so the earliest unfinished item is always grabbed and runnable: no deadlock.
 template <bool STREAM>
 __global__ void __launch_bounds__(kDfThreads, 2) k_band_lu_df(DfArgs A) {
@@ -1696,9 +1721,9 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_band_lu_df(DfArgs A) {
     __syncthreads();
     // worker wave cursor: wave w holds strips [w0, w0 + wn) (J x (strips - 1) of step w)
     int w = 0, w0 = 0;
-    auto wave_n = [&](int ww) {
+    auto wave_n = [&](int ww) {  // worker items of step ww: J x ceil((strips - 1) / kDfG)
         const int R = min(A.K, A.m_max - 32 * (ww + 1));
-        return J * ((R + 31) / 32 - 1);
+        return J * (((R + 31) / 32 - 1 + kDfG - 1) / kDfG);
     };
     int wn = A.S >= 2 ? wave_n(0) : 0;
     for (;;) {
@@ -1729,9 +1754,9 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_band_lu_df(DfArgs A) {
                 wn = wave_n(w);
             }
             if (done) break;
-            const int ns1 = wn / J, o = item - w0, jid = o / ns1;
+            const int ng = wn / J, o = item - w0, jid = o / ng;
             const FactorJob Jb = A.jobs[jid];
-            df_strip<STREAM>(A, Jb, jid, w, 1 + o % ns1, P, U);
+            df_worker<STREAM>(A, Jb, jid, w, o % ng, P, U);
             rec = (long long)A.S * J + item;
         }
         __syncthreads();
@@ -1758,12 +1783,13 @@ size_t lu_df_scratch_ints(int njobs, int m_max) {
     return kDfHdr + 2 * (size_t)njobs + (size_t)njobs * S;
 }
 
-// Where the dataflow kernel beats one CTA per job (profiles/lu_df_r02.txt): few jobs for the SMs (a job's
-// trailing update then spreads over the idle SMs) and bandwidths whose single-CTA step is long
+// Where the dataflow kernel beats one CTA per job (profiles/lu_df_r02.txt): wide bands (enough strips per step
+// to spread) and no more jobs than ~0.7 x SMs (one chain CTA per job on the panel SMs, the rest for workers;
+// with more jobs the single-CTA kernel's per-flop efficiency wins)
 bool lu_df_applies(int max_k, int njobs) {
     int dev = 0, nsm = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    return max_k >= kLuDfMinK && max_k <= 224 && njobs <= nsm / 2;
+    return max_k >= kLuDfMinK && max_k <= 224 && 10 * njobs <= 7 * nsm;
 }
 
 void launch_band_lu_df(const FactorJob* d_jobs, int njobs, int m_max, int max_k, double eps, cudaStream_t s,
@@ -1788,7 +1814,7 @@ void launch_band_lu_df(const FactorJob* d_jobs, int njobs, int m_max, int max_k,
     A.col_step = scratch + kDfHdr + 2 * njobs;
     A.eps = eps;
     A.pld = pad_ld(B + max_k);
-    A.uld = pad_ld(32);
+    A.uld = pad_ld(32 * kDfG);
     A.trace = nullptr;
     const size_t bytes = sizeof(double) * (size_t)(B * A.pld + B * A.uld);
     auto kern = streamed ? k_band_lu_df<true> : k_band_lu_df<false>;
@@ -1799,7 +1825,8 @@ void launch_band_lu_df(const FactorJob* d_jobs, int njobs, int m_max, int max_k,
     SAP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDfThreads, bytes));
     // chain items (one per job and step) + worker strips
     long long items = (long long)njobs * S;
-    for (int w = 0; w <= S - 2; ++w) items += (long long)njobs * ((std::min(max_k, m_max - B * (w + 1)) + 31) / 32 - 1);
+    for (int w = 0; w <= S - 2; ++w)
+        items += (long long)njobs * (((std::min(max_k, m_max - B * (w + 1)) + 31) / 32 - 1 + kDfG - 1) / kDfG);
     const int grid = nsm * std::max(per_sm, 1);
     // panel SMs: one resident chain per job where the SMs allow (chains are latency-bound), at most 40 %
     int nps = std::min((njobs + per_sm - 1) / std::max(per_sm, 1), (2 * nsm) / 5);

@@ -23,10 +23,10 @@ def decode(item, J, K, m_max):
     w = 0
     while True:
         R = min(K, m_max - 32 * (w + 1))
-        ns1 = (R + 31) // 32 - 1
-        wn = J * ns1
+        ng = ((R + 31) // 32 - 1 + 2) // 3
+        wn = J * ng
         if o < wn:
-            return ("strip", o // ns1, w, 1 + o % ns1)
+            return ("strip", o // ng, w, 1 + 3 * (o % ng))
         o -= wn
         w += 1
 
