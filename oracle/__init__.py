@@ -100,6 +100,9 @@ def ref():
         R.sapref_factor_blocks.argtypes = [C.c_int, C.c_int, _dp, C.c_int, C.c_int, C.c_double, _dp, C.c_void_p,
                                            _ip, C.c_void_p, C.c_void_p]
         R.sapref_spikes.argtypes = [C.c_int, C.c_int, _dp, C.c_int, C.c_double, _dp, _dp, _dp, _dp, _dp, _ip]
+        R.sapref_factor_blocks_f32.argtypes = R.sapref_factor_blocks.argtypes
+        R.sapref_spikes_f32.argtypes = R.sapref_spikes.argtypes
+        R.sapref_apply_f32.argtypes = [C.c_int, C.c_int, _dp, C.c_int, C.c_int, C.c_double, _dp, _dp]
         R.sapref_apply.argtypes = [C.c_int, C.c_int, _dp, C.c_int, C.c_int, C.c_double, _dp, _dp]
         R.sapref_solve_banded.argtypes = [C.c_int, C.c_int, _dp, _dp, C.c_int, C.c_int, C.c_double, C.c_int,
                                           C.c_double, C.c_double, C.c_int, C.c_int, _dp,
@@ -245,6 +248,33 @@ def ref_spikes(n, k, band, p, boost_eps=1e-10):
 def ref_apply(n, k, band, p, kind, x, boost_eps=1e-10):
     out = np.zeros(n)
     _ref_check(ref().sapref_apply(n, k, band, p, kind, boost_eps, np.ascontiguousarray(x, np.float64), out))
+    return out
+
+
+def ref_factor_blocks_f32(n, k, band, p, lu_and_ul, boost_eps=1e-10):
+    """factor_blocks<float> on banded_cast<float>(band) (build_precond_op<float>), widened to double."""
+    lu = np.zeros(n * (2 * k + 1))
+    ul = np.zeros(n * (2 * k + 1))
+    boosts = np.zeros(p, np.int32)
+    bul = np.zeros(p, np.int32)
+    norms = np.zeros(p)
+    _ref_check(ref().sapref_factor_blocks_f32(n, k, band, p, int(lu_and_ul), boost_eps, lu, ul.ctypes.data, boosts,
+                                              bul.ctypes.data, norms.ctypes.data))
+    return dict(lu=lu, ul=ul if lu_and_ul else None, boosts=boosts, boosts_ul=bul, norms=norms)
+
+
+def ref_spikes_f32(n, k, band, p, boost_eps=1e-10):
+    ww = max(p - 1, 0) * k * k
+    B, Cb, vb, wt, rb = (np.zeros(max(ww, 1)) for _ in range(5))
+    rbo = np.zeros(max(p - 1, 1), np.int32)
+    _ref_check(ref().sapref_spikes_f32(n, k, band, p, boost_eps, B, Cb, vb, wt, rb, rbo))
+    cut = slice(0, ww)
+    return dict(B=B[cut], C=Cb[cut], vb=vb[cut], wt=wt[cut], rbar=rb[cut], rbar_boosts=rbo[:max(p - 1, 0)])
+
+
+def ref_apply_f32(n, k, band, p, kind, x, boost_eps=1e-10):
+    out = np.zeros(n)
+    _ref_check(ref().sapref_apply_f32(n, k, band, p, kind, boost_eps, np.ascontiguousarray(x, np.float64), out))
     return out
 
 

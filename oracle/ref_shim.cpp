@@ -19,6 +19,10 @@
 //                             proj/include/sap/krylov.hpp:434-442), the dense wiring of
 //                             proj/tests/acceptance.cpp:114-132.
 //   * sapref_solve_sparse   : sap::solve_sparse (proj/include/sap/pipeline.hpp:213-369).
+//   * sapref_*_f32          : the same factor_blocks / extract_coupling + compute_spike_tips /
+//                             apply_preconditioner at T = float on banded_cast<float> of the band:
+//                             build_precond_op<float>'s preconditioner (proj/include/sap/pipeline.hpp:140-202,
+//                             banded_matrix.hpp:129-136), outputs widened to double.
 //   * sapref_third_*        : the third stage - sap::third_stage (proj/include/sap/reorder_cm.hpp:233-274),
 //                             factor_blocks with block permutations and per-partition bandwidths,
 //                             compute_full_spikes (spike.hpp:258-296), apply_preconditioner and
@@ -169,6 +173,68 @@ int sapref_apply(int n, int k, const double* band, int p, int kind, double boost
     const auto r = sap::apply_preconditioner<double>(static_cast<sap::PrecondKind>(kind), f, s,
                                                      std::span<const double>(in, static_cast<std::size_t>(n)));
     std::memcpy(out, r.data(), sizeof(double) * r.size());
+    SAPREF_CATCH
+}
+
+// ---- T = float (mixed_precision): build_precond_op<float>'s pieces on banded_cast<float>(band) ----
+int sapref_factor_blocks_f32(int n, int k, const double* band, int p, int lu_and_ul, double boost_eps,
+                             double* lu_out, double* ul_out, int* boosts, int* boosts_ul, double* norms) {
+    SAPREF_TRY
+    const auto a = sap::banded_cast<float>(wrap_band(n, k, band));
+    const auto layout = sap::make_partition_layout(n, p, k);
+    const auto f = sap::factor_blocks<float>(
+        a, layout, lu_and_ul ? sap::FactorMode::lu_and_ul : sap::FactorMode::lu_only, boost_eps);
+    std::size_t off = 0;
+    for (int b = 0; b < p; ++b) {
+        const auto& lu = f.lu[static_cast<std::size_t>(b)];
+        for (std::size_t i = 0; i < lu.size(); ++i) lu_out[off + i] = lu[i];
+        if (lu_and_ul && ul_out)
+            for (std::size_t i = 0; i < lu.size(); ++i) ul_out[off + i] = f.ul[static_cast<std::size_t>(b)][i];
+        off += lu.size();
+        boosts[b] = f.boost_count[static_cast<std::size_t>(b)];
+        if (boosts_ul) boosts_ul[b] = f.boost_count_ul[static_cast<std::size_t>(b)];
+        if (norms) norms[b] = f.block_norm[static_cast<std::size_t>(b)];
+    }
+    SAPREF_CATCH
+}
+
+int sapref_spikes_f32(int n, int k, const double* band, int p, double boost_eps, double* b_out, double* c_out,
+                      double* vb_out, double* wt_out, double* rbar_out, int* rbar_boosts) {
+    SAPREF_TRY
+    const auto a = sap::banded_cast<float>(wrap_band(n, k, band));
+    const auto layout = sap::make_partition_layout(n, p, k);
+    const auto f = sap::factor_blocks<float>(a, layout, sap::FactorMode::lu_and_ul, boost_eps);
+    const auto cb = sap::extract_coupling<float>(a, layout);
+    const auto s = sap::compute_spike_tips<float>(f, cb);
+    std::size_t off = 0;
+    auto widen = [](double* dst, const std::vector<float>& v) {
+        for (std::size_t i = 0; i < v.size(); ++i) dst[i] = v[i];
+    };
+    for (int t = 0; t < s.interfaces(); ++t) {
+        const std::size_t ww = s.v_bottom[static_cast<std::size_t>(t)].size();
+        widen(b_out + off, cb.b_blocks[static_cast<std::size_t>(t)]);
+        widen(c_out + off, cb.c_blocks[static_cast<std::size_t>(t)]);
+        widen(vb_out + off, s.v_bottom[static_cast<std::size_t>(t)]);
+        widen(wt_out + off, s.w_top[static_cast<std::size_t>(t)]);
+        widen(rbar_out + off, s.rbar[static_cast<std::size_t>(t)]);
+        rbar_boosts[t] = s.rbar_boosts[static_cast<std::size_t>(t)];
+        off += ww;
+    }
+    SAPREF_CATCH
+}
+
+// M r through build_precond_op<float>'s closure: r cast to float, apply_preconditioner<float>, widened back
+int sapref_apply_f32(int n, int k, const double* band, int p, int kind, double boost_eps, const double* in,
+                     double* out) {
+    SAPREF_TRY
+    const auto a = wrap_band(n, k, band);
+    const auto layout = sap::make_partition_layout(n, p, k);
+    sap::PipelineConfig cfg;
+    cfg.precond = static_cast<sap::PrecondKind>(kind);
+    cfg.boost_eps = boost_eps;
+    sap::PipelineReport rep;
+    const sap::LinearOp op = sap::detail::build_precond_op<float>(a, layout, cfg, false, nullptr, rep);
+    op(std::span<const double>(in, static_cast<std::size_t>(n)), std::span<double>(out, static_cast<std::size_t>(n)));
     SAPREF_CATCH
 }
 

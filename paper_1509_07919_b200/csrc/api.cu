@@ -115,6 +115,12 @@ struct sap_handle {
     // applied in FP32 from FP32 copies of the factors, tips and reduced factors
     bool mixed = false;
     DevBuf<float> lu_f, rbar_f, vb_f, wt_f, bblk_f, cblk_f, dinv_f, rdinv_f, g_f, o_f, xt_f, xb_f;
+    // f32fac: the block preconditioner was FACTORED in FP32 (build_precond_op<float>; setup_mixed): the
+    // parity getters read the FP32 factors / tips / reduced blocks
+    bool f32fac = false;
+    DevBuf<float> ul_f;
+    DevBuf<FactorJobF> fjobs;
+    DevBuf<TipJobF> ftipjobs;
     DevBuf<unsigned long long> kappa_f;
     SweepPlan<float> lplan_f, rplan_f;
     // CSR operator
@@ -419,6 +425,180 @@ struct PrioScope {
     }
 };
 
+// build_precond_op<float> (pipeline.hpp:140-202) for the block preconditioners: banded_cast<float> of the
+// resident band into the LU / UL stores, block norms over the float entries (accumulated in double,
+// block_factors.hpp:187-195), FP32 LU / UL with boosting (mixed.cu), the coupling corners in float, FP32 spike
+// tips and reduced blocks, then the FP32 sweep plans the apply uses (apply_m_fp32). T_* timers as in the
+// FP64 setup; the FP64 factors are not built.
+void setup_mixed(sap_handle* h, const Layout& L, bool want_ul) {
+    const cudaStream_t s = h->stream;
+    const int n = h->n, k = h->k, p = L.p;
+    h->mixed = true;
+    h->f32fac = true;
+    SAP_CUDA(cudaEventRecord(h->ev[1], s));  // the band is resident
+    h->d_offsets.alloc(p + 1);
+    SAP_CUDA(cudaMemcpyAsync(h->d_offsets.get(), L.offsets.data(), sizeof(int) * (p + 1), cudaMemcpyHostToDevice, s));
+    h->norms.alloc(p);
+    h->boosts.alloc(2 * (size_t)p);
+    SAP_CUDA(cudaMemsetAsync(h->boosts.get(), 0, sizeof(int) * 2 * p, s));
+    SAP_CUDA(cudaMemsetAsync(h->norms.get(), 0, sizeof(double) * p, s));
+    h->op_nonfinite.alloc(1);
+    SAP_CUDA(cudaMemsetAsync(h->op_nonfinite.get(), 0, sizeof(int), s));
+    const int m_max = L.sizes[0];
+    h->fst = BandStore::make(m_max, k);
+    h->lu.release();
+    h->ul.release();
+    h->lu_f.alloc(h->fst.total(p));
+    if (want_ul)
+        h->ul_f.alloc(h->fst.total(p));
+    else
+        h->ul_f.release();
+    launch_block_norms(h->band_ptr, m_max, k, h->d_offsets.get(), p, nullptr, h->norms.get(), s,
+                       h->op_nonfinite.get(), nullptr, true);
+    launch_copy_blocks_f32(h->band_ptr, k, h->d_offsets.get(), p, h->fst, h->lu_f.get(), want_ul ? h->ul_f.get() : nullptr,
+                           s);
+    const int njobs = want_ul ? 2 * p : p;
+    std::vector<FactorJobF> jobs(njobs);
+    const size_t w = 2 * (size_t)k + 1;
+    for (int b = 0; b < p; ++b) {
+        const int m = L.sizes[b];
+        jobs[b] = FactorJobF{h->lu_f.get() + h->fst.block(b) + k, 1, 2LL * k, m, k, h->norms.get() + b,
+                             h->boosts.get() + b};
+        if (want_ul)
+            jobs[p + b] = FactorJobF{h->ul_f.get() + h->fst.block(b) + (size_t)(m - 1) * w + k, -1, -2LL * k, m, k,
+                                     h->norms.get() + b, h->boosts.get() + p + b};
+    }
+    h->fjobs.alloc(njobs);
+    SAP_CUDA(cudaMemcpyAsync(h->fjobs.get(), jobs.data(), sizeof(FactorJobF) * njobs, cudaMemcpyHostToDevice, s));
+    SAP_CUDA(cudaEventRecord(h->ev[8], s));
+    launch_band_lu_f32(h->fjobs.get(), njobs, k, h->opt.boost_eps, s);
+    SAP_CUDA(cudaEventRecord(h->ev[9], s));
+    h->kappa_f.alloc(2);
+    SAP_CUDA(cudaMemsetAsync(h->kappa_f.get(), 0, 2 * sizeof(unsigned long long), s));
+    {
+        SweepPlan<float>& lp = h->lplan_f;
+        lp = SweepPlan<float>{};
+        lp.f = h->lu_f.get();
+        lp.st = h->fst;
+        lp.offs = h->d_offsets.get();
+        lp.p = p;
+        lp.k = k;
+        h->dinv_f.alloc(std::max<size_t>(sweep_dinv_elems(lp), 1));
+        plan_sweeps(lp, h->dinv_f.get());
+        lp.kappa = h->kappa_f.get();
+        launch_chunk_inverses(lp, s);
+    }
+    SAP_CUDA(cudaEventRecord(h->ev[2], s));
+    for (int b = 0; b < p; ++b) {
+        const double m = L.sizes[b], kk = std::min<double>(k, m - 1 > 0 ? m - 1 : 0);
+        const double f = (m - kk) * (2 * kk * kk + kk) + (kk - 1) * kk * (4 * kk + 1) / 6.0;
+        h->rep.factor_flops += (want_ul ? 2.0 : 1.0) * f;
+    }
+    int ni = 0;
+    if (h->coupled) {
+        ni = p - 1;
+        const size_t ww = (size_t)k * k * ni;
+        h->rst = BandStore::make(k, k > 0 ? k - 1 : 0);
+        h->bblk.alloc(std::max<size_t>(ww, 1));
+        h->cblk.alloc(std::max<size_t>(ww, 1));
+        h->bblk_f.alloc(std::max<size_t>(ww, 1));
+        h->cblk_f.alloc(std::max<size_t>(ww, 1));
+        h->vb_f.alloc(std::max<size_t>(ww, 1));
+        h->wt_f.alloc(std::max<size_t>(ww, 1));
+        h->rbar_f.alloc(std::max<size_t>(h->rst.total(ni), 1));
+        SAP_CUDA(cudaMemsetAsync(h->rbar_f.get(), 0, sizeof(float) * h->rst.total(ni), s));
+        h->rbar_boosts.alloc(ni);
+        h->nonfinite.alloc(3 * (size_t)ni);
+        SAP_CUDA(cudaMemsetAsync(h->nonfinite.get(), 0, sizeof(int) * 3 * ni, s));
+        SAP_CUDA(cudaMemsetAsync(h->rbar_boosts.get(), 0, sizeof(int) * ni, s));
+        h->xt_f.alloc(std::max<size_t>((size_t)ni * k, 1));
+        h->xb_f.alloc(std::max<size_t>((size_t)ni * k, 1));
+        std::vector<int> roffs(ni + 1);
+        for (int t = 0; t <= ni; ++t) roffs[t] = t * k;
+        h->d_roffsets.alloc(ni + 1);
+        SAP_CUDA(cudaMemcpyAsync(h->d_roffsets.get(), roffs.data(), sizeof(int) * (ni + 1), cudaMemcpyHostToDevice, s));
+        // T_BC: extract_coupling<float> = the FP64 corners rounded to float (the band is cast entrywise)
+        launch_extract_coupling(h->band_ptr, n, k, h->d_offsets.get(), p, h->bblk.get(), h->cblk.get(), s);
+        launch_cast_band<float>(h->bblk.get(), h->bblk_f.get(), ww, s);
+        launch_cast_band<float>(h->cblk.get(), h->cblk_f.get(), ww, s);
+        SAP_CUDA(cudaEventRecord(h->ev[3], s));
+        // T_SPK: compute_spike_tips<float>
+        std::vector<TipJobF> tj;
+        for (int t = 0; t < ni; ++t) {
+            const size_t o = (size_t)t * k * k;
+            tj.push_back(TipJobF{h->lu_f.get() + h->fst.block(t), L.sizes[t] - k, 0, h->bblk_f.get() + o,
+                                 h->vb_f.get() + o, 2 * t});
+            tj.push_back(TipJobF{h->ul_f.get() + h->fst.block(t + 1), 0, 1, h->cblk_f.get() + o, h->wt_f.get() + o,
+                                 2 * t + 1});
+        }
+        h->ftipjobs.alloc(std::max<size_t>(tj.size(), 1));
+        SAP_CUDA(cudaMemcpyAsync(h->ftipjobs.get(), tj.data(), sizeof(TipJobF) * tj.size(), cudaMemcpyHostToDevice, s));
+        launch_spike_tips_f32(h->ftipjobs.get(), (int)tj.size(), k, h->nonfinite.get(), s);
+        SAP_CUDA(cudaEventRecord(h->ev[4], s));
+        // T_LUrdcd: finish_reduced_blocks<float>
+        if (k > 0) {
+            launch_rbar_f32(h->wt_f.get(), h->vb_f.get(), k, ni, h->opt.boost_eps, h->rbar_f.get(), h->rst,
+                            h->rbar_boosts.get(), h->nonfinite.get() + 2 * ni, s);
+            SweepPlan<float>& rp = h->rplan_f;
+            rp = SweepPlan<float>{};
+            rp.f = h->rbar_f.get();
+            rp.st = h->rst;
+            rp.offs = h->d_roffsets.get();
+            rp.p = ni;
+            rp.k = k - 1;
+            h->rdinv_f.alloc(std::max<size_t>(sweep_dinv_elems(rp), 1));
+            plan_sweeps(rp, h->rdinv_f.get());
+            rp.kappa = h->kappa_f.get() + 1;
+            launch_chunk_inverses(rp, s);
+        }
+        SAP_CUDA(cudaEventRecord(h->ev[5], s));
+    }
+    h->g_f.alloc(std::max(n, 1));
+    h->o_f.alloc(std::max(n, 1));
+    h->scratch_in.alloc(std::max(n, 1));
+    h->scratch_out.alloc(std::max(n, 1));
+    SAP_CUDA(cudaStreamSynchronize(s));
+    int opbad = 0;
+    SAP_CUDA(cudaMemcpy(&opbad, h->op_nonfinite.get(), sizeof(int), cudaMemcpyDeviceToHost));
+    h->op_finite = opbad == 0;
+    {  // chunk triangles of the FP32 factors: the same substitution rule as the FP64 sweeps
+        unsigned long long kb[2] = {0, 0};
+        SAP_CUDA(cudaMemcpy(kb, h->kappa_f.get(), sizeof(kb), cudaMemcpyDeviceToHost));
+        double kap[2];
+        std::memcpy(kap, kb, sizeof(kap));
+        const int force = h->opt.triangle_solve;
+        h->lplan_f.subst = force ? force == 2 : kap[0] > kSubstKappa;
+        h->rplan_f.subst = force ? force == 2 : kap[1] > kSubstKappa;
+        h->rep.chunk_condition = kap[0];
+        h->rep.sweep_substitution = h->lplan_f.subst ? 1 : 0;
+    }
+    h->rep.t_dtransf = ev_ms(h->ev[0], h->ev[1]) * 1e-3;
+    h->rep.t_lu = ev_ms(h->ev[1], h->ev[2]) * 1e-3;
+    h->rep.t_factor_kernel = ev_ms(h->ev[8], h->ev[9]) * 1e-3;
+    std::vector<int> hb(2 * p);
+    SAP_CUDA(cudaMemcpy(hb.data(), h->boosts.get(), sizeof(int) * 2 * p, cudaMemcpyDeviceToHost));
+    for (int b = 0; b < p; ++b) {
+        h->rep.total_boosts += hb[b];
+        h->rep.total_boosts_ul += hb[p + b];
+    }
+    if (h->coupled) {
+        h->rep.t_bc = ev_ms(h->ev[2], h->ev[3]) * 1e-3;
+        h->rep.t_spk = ev_ms(h->ev[3], h->ev[4]) * 1e-3;
+        h->rep.t_lurdcd = ev_ms(h->ev[4], h->ev[5]) * 1e-3;
+        std::vector<int> nf(3 * ni), rb(ni);
+        SAP_CUDA(cudaMemcpy(nf.data(), h->nonfinite.get(), sizeof(int) * 3 * ni, cudaMemcpyDeviceToHost));
+        SAP_CUDA(cudaMemcpy(rb.data(), h->rbar_boosts.get(), sizeof(int) * ni, cudaMemcpyDeviceToHost));
+        for (int t = 0; t < ni; ++t) h->rep.total_rbar_boosts += rb[t];
+        for (int t = 0; t < ni; ++t) {
+            if (nf[2 * t]) throw PreconditionerFailure("right spike tip at interface " + std::to_string(t) + " is not finite");
+            if (nf[2 * t + 1]) throw PreconditionerFailure("left spike tip at interface " + std::to_string(t) + " is not finite");
+        }
+        for (int t = 0; t < ni; ++t)
+            if (nf[2 * ni + t]) throw PreconditionerFailure("reduced interface block " + std::to_string(t) + " is not finite");
+    }
+    h->ready = true;
+}
+
 void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device) {
     PrioScope prio_scope(h);
     h->op_finite = false;
@@ -426,6 +606,7 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
     require(band != nullptr || n == 0, "sap_setup_banded: null band");
     const cudaStream_t s = h->stream;
     h->mixed = false;
+    h->f32fac = false;
     h->ready = false;
     h->kind = h->opt.precond;
     require(h->kind >= 0 && h->kind <= 3, "sap_setup_banded: unknown preconditioner kind");
@@ -465,7 +646,9 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
     const size_t total = (size_t)n * (2 * (size_t)k + 1);
     // host band + block preconditioner on the default LU kernel: the upload streams in rounds while the
     // LU / UL jobs factor the columns that have arrived (k_band_lu_res wait_cols)
-    const bool streamed = on_device == 0 && blocks && !h->ts && n > 0 && k >= 1 && L.p >= 1 &&
+    // FP32 factorization (mixed precision without the third stage): setup_mixed, after a plain upload
+    const bool f32fac = blocks && !h->ts && h->opt.mixed_precision && n > 0;
+    const bool streamed = on_device == 0 && blocks && !h->ts && !f32fac && n > 0 && k >= 1 && L.p >= 1 &&
                           band_lu_reads_source(k) && write_value_fn() != nullptr;
     SAP_CUDA(cudaEventRecord(h->ev[0], s));
     if (on_device == 2) {
@@ -481,7 +664,7 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
     if (!streamed) SAP_CUDA(cudaEventRecord(h->ev[1], s));
     // resident band on the same kernel: the LU starts at once in the no-boost mode while the block norms
     // run beside it on the side stream (the check and gated refactor below keep it exact)
-    const bool early = !streamed && on_device != 0 && blocks && !h->ts && n > 0 && k >= 1 && L.p >= 1 &&
+    const bool early = !streamed && on_device != 0 && blocks && !h->ts && !f32fac && n > 0 && k >= 1 && L.p >= 1 &&
                        band_lu_reads_source(k);
     h->scratch_in.alloc(std::max(n, 1));
     h->scratch_out.alloc(std::max(n, 1));
@@ -512,6 +695,7 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
         return;
     }
 
+    if (f32fac) return setup_mixed(h, L, want_ul);
     // ---- factor_blocks: norms, block band copies, LU (+ UL) ----
     h->d_offsets.alloc(p + 1);
     SAP_CUDA(cudaMemcpyAsync(h->d_offsets.get(), L.offsets.data(), sizeof(int) * (p + 1), cudaMemcpyHostToDevice, s));
@@ -808,8 +992,7 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
             h->rdinv.alloc(std::max<size_t>(sweep_dinv_elems(rp), 1));
             plan_sweeps(rp, h->rdinv.get());
             rp.kappa = h->kappa.get() + 1;
-            rp.kappa = h->kappa.get() + 1;
-        launch_chunk_inverses(rp, s);
+            launch_chunk_inverses(rp, s);
         }
         SAP_CUDA(cudaEventRecord(h->ev[5], s));
         if (want_ul) SAP_CUDA(cudaStreamWaitEvent(s, h->sev[1], 0));  // the LU chunk inverses (side stream)
@@ -1668,10 +1851,25 @@ sap_status sap_get_factor(sap_handle* h, int part, int which, double* out, int* 
         }
         require(part >= 0 && part < h->layout.p, "sap_get_factor: partition out of range");
         require(which == 0 || which == 1, "sap_get_factor: which must be 0 (LU) or 1 (UL)");
-        if (which == 1 && (!h->coupled || h->ul.get() == nullptr))
+        if (which == 1 && (!h->coupled || (h->f32fac ? h->ul_f.get() == nullptr : h->ul.get() == nullptr)))
             throw InvalidArgument("block_solve: UL factors not available");
         SAP_CUDA(cudaSetDevice(h->opt.device));
         const size_t w = 2 * (size_t)h->k + 1;
+        if (h->f32fac) {  // factor_blocks<float>'s factors, widened
+            const int m = h->layout.sizes[part];
+            if (out) {
+                std::vector<float> f((size_t)m * w);
+                SAP_CUDA(cudaMemcpy(f.data(), (which == 0 ? h->lu_f.get() : h->ul_f.get()) + h->fst.block(part),
+                                    sizeof(float) * f.size(), cudaMemcpyDeviceToHost));
+                for (size_t i = 0; i < f.size(); ++i) out[i] = f[i];
+            }
+            if (boosts)
+                SAP_CUDA(cudaMemcpy(boosts, h->boosts.get() + (which == 0 ? 0 : h->layout.p) + part, sizeof(int),
+                                    cudaMemcpyDeviceToHost));
+            if (block_norm)
+                SAP_CUDA(cudaMemcpy(block_norm, h->norms.get() + part, sizeof(double), cudaMemcpyDeviceToHost));
+            return;
+        }
         const double* src = (which == 0 ? h->lu.get() : h->ul.get()) + h->fst.block(part);
         const int m = h->layout.sizes[part];
         if (out && h->ts && h->ts_k[part] != h->k) {
@@ -1750,6 +1948,29 @@ sap_status sap_get_spike(sap_handle* h, int iface, double* b_block, double* c_bl
         }
         SAP_CUDA(cudaSetDevice(h->opt.device));
         const size_t ww = (size_t)h->k * h->k, off = ww * iface, bytes = sizeof(double) * ww;
+        if (h->f32fac) {  // compute_spike_tips<float> / finish_reduced_blocks<float>, widened
+            auto get = [&](double* dst, const float* src) {
+                if (!dst) return;
+                std::vector<float> f(ww);
+                SAP_CUDA(cudaMemcpy(f.data(), src + off, sizeof(float) * ww, cudaMemcpyDeviceToHost));
+                for (size_t i = 0; i < ww; ++i) dst[i] = f[i];
+            };
+            get(b_block, h->bblk_f.get());
+            get(c_block, h->cblk_f.get());
+            get(v_bottom, h->vb_f.get());
+            get(w_top, h->wt_f.get());
+            if (rbar && h->k > 0) {
+                const int w = h->k;
+                std::vector<float> band((size_t)w * (2 * (size_t)w - 1));
+                SAP_CUDA(cudaMemcpy(band.data(), h->rbar_f.get() + h->rst.block(iface), sizeof(float) * band.size(),
+                                    cudaMemcpyDeviceToHost));
+                for (int i = 0; i < w; ++i)
+                    for (int j = 0; j < w; ++j) rbar[(size_t)i * w + j] = band[(size_t)j * (2 * w - 1) + (i - j + w - 1)];
+            }
+            if (rbar_boosts)
+                SAP_CUDA(cudaMemcpy(rbar_boosts, h->rbar_boosts.get() + iface, sizeof(int), cudaMemcpyDeviceToHost));
+            return;
+        }
         if (h->ts) {
             // third stage: interface width w_t <= k, embedded in the k x k corners (third.cu header)
             const int k = h->k, w = h->widths[iface], o = k - w;

@@ -46,6 +46,30 @@ bool launch_band_lu_ws(const FactorJob* d_jobs, int njobs, int max_k, double boo
 // Row-sum infinity norms of ni dense row-major w x w blocks and a non-finite flag per block.
 void launch_dense_norms(const double* a, int w, int ni, double* norms, int* nonfinite, cudaStream_t s);
 
+// ---- FP32 preconditioner (mixed.cu): build_precond_op<float> (pipeline.hpp:140-202) ----
+struct FactorJobF {  // FactorJob at T = float (base = the float store's strided view)
+    float* base;
+    long long rs, cs;
+    int m, k;
+    const double* scale;  // block norm of the float band (k_block_norms<true>), device
+    int* boosts;
+};
+struct TipJobF {  // TipJob at T = float
+    const float* f;
+    int corner;
+    int which;
+    const float* rhs;
+    float* out;
+    int flag;
+};
+void launch_copy_blocks_f32(const double* band, int k, const int* d_offsets, int p, const BandStore& st, float* lu,
+                            float* ul, cudaStream_t s);
+void launch_band_lu_f32(const FactorJobF* d_jobs, int njobs, int max_k, double boost_eps, cudaStream_t s);
+void launch_spike_tips_f32(const TipJobF* d_jobs, int njobs, int k, int* nonfinite, cudaStream_t s);
+// R_t = I - W_t V_t and its boosted dense LU, written in the reduced BandStore layout (k' = w - 1)
+void launch_rbar_f32(const float* wt, const float* vb, int w, int ni, double boost_eps, float* rbar,
+                     const BandStore& rst, int* boosts, int* nonfinite, cudaStream_t s);
+
 // ---- spikes (spike.cu) ----
 // d_wid (optional, third stage): interface widths w_t <= k embedded in the k x k corners (third.cu).
 void launch_extract_coupling(const double* band, int n, int k, const int* d_offsets, int p, double* bblk,

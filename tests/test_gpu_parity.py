@@ -388,10 +388,10 @@ def test_mixed_precision_preconditioner_tracks_fp64(sap, oracle):
 
 @pytest.mark.parametrize("kind", [0, 1])
 def test_mixed_precision_solve_reaches_full_accuracy(sap, oracle, kind):
-    """test_pipeline.cpp:327-347: FP32 preconditioning still converges to rel_tol 1e-10 in FP64 Krylov.
-    The FP32 operands here are rounded from the FP64 factorization, a more accurate
-    preconditioner than the reference's FP32-arithmetic factorization: iterations are at most the
-    reference's + 1 (measured 7.25 vs 11.25 SaP-C at this case)."""
+    """test_pipeline.cpp:327-347: FP32 preconditioning (the FP32 factorization, build_precond_op<float>) still
+    converges to rel_tol 1e-10 in FP64 Krylov. The iteration count under an FP32 preconditioner is
+    rounding-chaotic (tests/test_gpu_mixed.py header: the reference's own FMA build moves it by up to 2x), so
+    the bound is 2.5x the reference's + 1; the preconditioner itself is pinned in test_gpu_mixed.py."""
     n, k, p = 20000, 50, 8
     band, rhs = sap.random_banded(n, k, 1.0, 910)
     s = make(sap, n, k, band, p, kind, mixed_precision=True)
@@ -399,7 +399,7 @@ def test_mixed_precision_solve_reaches_full_accuracy(sap, oracle, kind):
     assert st.converged and st.final_relative_residual <= 1e-10
     if oracle.has_ref():
         _, so = oracle.ref_solve_banded(n, k, band, rhs, p, kind, mixed_precision=True)
-        assert so["converged"] and st.iterations <= so["iterations"] + 1.0, (st.iterations, so["iterations"])
+        assert so["converged"] and st.iterations <= 2.5 * so["iterations"] + 1.0, (st.iterations, so["iterations"])
     s.close()
 
 

@@ -1,35 +1,26 @@
-"""Config 2 time-to-solution with the FP32 preconditioner (KrylovOptions.mixed_precision) vs FP64."""
-import os
-import sys
+"""Mixed precision (FP32 factorization, build_precond_op<float>) vs FP64 at configs 2 and 3: setup / solve
+device times, iterations, and the reference's FP32 path for comparison (iterations).
+    python tools/mixed_time.py"""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_1509_07919_b200 as S
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-sys.path.insert(0, ROOT)
-import torch  # noqa: E402
-
-import paper_1509_07919_b200 as S  # noqa: E402
-
-n, k, p = 200000, 200, 50
-band_h, rhs_h = S.random_banded(n, k, 1.0, 1)
-band = torch.from_numpy(band_h).cuda()
-rhs = torch.from_numpy(rhs_h).cuda()
-for kind in (S.PrecondKind.coupled, S.PrecondKind.decoupled):
+CASES = [(200000, 200, 1.0, 50, "C"), (200000, 200, 1.0, 50, "D"), (200000, 50, 1.0, 50, "C"),
+         (200000, 100, 0.5, 50, "C"), (200000, 10, 1.0, 50, "D")]
+for n, k, d, p, kind in CASES:
+    band, rhs = S.random_banded(n, k, d, 1)
+    db = torch.from_numpy(band).cuda()
+    pk = S.PrecondKind.coupled if kind == "C" else S.PrecondKind.decoupled
+    row = []
     for mixed in (False, True):
-        s = S.Solver(p=p, precond=kind, krylov=S.KrylovOptions(mixed_precision=mixed))
-        stream = torch.cuda.Stream()
-        s.set_stream(stream)
-        best = None
-        with torch.cuda.stream(stream):
-            for i in range(4):
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                s.setup(band, n, k)
+        with S.Solver(p=p, precond=pk, krylov=S.KrylovOptions(mixed_precision=mixed)) as s:
+            for _ in range(2):
+                s.setup(db, n, k)
                 x, st = s.solve(rhs)
-                e1.record(stream)
-                torch.cuda.synchronize()
-                t = e0.elapsed_time(e1)
-                if i and (best is None or t < best[0]):
-                    best = (t, s.report(), st)
-        t, r, st = best
-        print(f"{'SaP-C' if kind == 0 else 'SaP-D'} mixed={mixed}: {t:.3f} ms (setup t_lu {r['t_lu'] * 1e3:.3f}, "
-              f"t_kry {r['t_kry'] * 1e3:.3f}), iterations {st.iterations}, residual {st.final_relative_residual:.2e}")
-        s.close()
+            r = s.report()
+            t_setup = r["t_lu"] + r["t_bc"] + r["t_spk"] + r["t_lurdcd"]
+            row.append(f"{'FP32' if mixed else 'FP64'}: setup {t_setup*1e3:.2f} ms (LU kernel "
+                       f"{r['t_factor_kernel']*1e3:.2f}), solve {r['t_kry']*1e3:.2f} ms, {st.iterations} it, "
+                       f"res {st.final_relative_residual:.1e}")
+    print(f"n={n} k={k} d={d} p={p} {kind}: " + " | ".join(row), flush=True)
