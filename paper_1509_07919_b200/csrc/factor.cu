@@ -324,7 +324,7 @@ void launch_band_lu(const FactorJob* d_jobs, int njobs, int max_k, double boost_
                     int m_max, int* df_scratch) {
     if (njobs <= 0) return;
     const char* force = getenv("SAP_LU_DF");  // tools/lu_df_*.py A/B: "0" single-CTA, "1" dataflow where it runs
-    const bool df = force ? (atoi(force) != 0 && max_k >= 64 && max_k <= 224) : lu_df_applies(max_k, njobs);
+    const bool df = force ? (atoi(force) != 0 && max_k >= 64 && max_k <= 512) : lu_df_applies(max_k, njobs);
     if (df_scratch && m_max > 0 && df) {
         launch_band_lu_df(d_jobs, njobs, m_max, max_k, boost_eps, s, streamed, df_scratch);
         return;

@@ -1139,9 +1139,16 @@ bool launch_band_lu_ws(const FactorJob* d_jobs, int njobs, int max_k, double eps
 // read the data with L1-bypassing .cg loads).
 // Every element receives exactly the arithmetic of k_band_lu_res (same panel code, same DMMA fragments
 // and k order): the factors are bitwise those of the single-CTA kernel.
-constexpr int kDfThreads = 256;
+// CTA shapes: 256 threads, two CTAs per SM for K <= 224; 512 threads, one CTA per SM up to K = 512 (the panel
+// alone is (32 + K) x 32 doubles). RW row-warps x 2 column halves share a strip's C tile, NG row groups each.
+template <int NT>
+struct DfCfg {
+    static constexpr int RW = NT / 64;
+    static constexpr int NG = NT == 256 ? 7 : 8;
+    static constexpr int MAXK = NT == 256 ? 224 : 512;
+    static constexpr int MINB = NT == 256 ? 2 : 1;
+};
 constexpr int kLuDfMinK = 192;  // narrower bands: too few strips per step to pay for the item overheads
-constexpr int kDfNG = 7;
 constexpr int kDfMaxSm = 256;  // %smid bound
 constexpr int kDfG = 3;        // strips per worker item (one panel load and one U12 solve for all of them)  // row groups (8 rows) per warp: 4 warps share a strip's rows, K <= 224
 
@@ -1253,9 +1260,11 @@ __device__ __forceinline__ double df_ld(const Lu& L, int i, int c, bool fresh) {
 // band (|i - c| > K) and columns >= nc are zero. Thread (c = tid / 8, k = tid % 8) takes the row pairs
 // 2 (k + 8 it): one column pointer per thread, one 16-byte load per pair where the pair lies inside the band
 // and is aligned (alignment is uniform per job and source for even rows); loads of a batch before any use.
+template <int NT>
 __device__ __forceinline__ void df_stage_panel(const Lu& L, double* __restrict__ dst, int ld, int i0, int cb, int nr,
                                                int nc, int rsplit) {
-    const int c = threadIdx.x >> 3, k = threadIdx.x & 7;
+    constexpr int TPC = NT / 32;  // threads per column
+    const int c = threadIdx.x / TPC, k = threadIdx.x % TPC;
     const long long rs = L.rs;
     const int gc = cb + c;
     const int lo_r = max(0, gc - L.K - i0), hi_r = min(nr, gc + L.K + 1 - i0);
@@ -1266,12 +1275,12 @@ __device__ __forceinline__ void df_stage_panel(const Lu& L, double* __restrict__
     const bool al_s = vec && ((reinterpret_cast<uintptr_t>(rs > 0 ? ps : ps - 1) & 15) == 0);
     const bool al_f = vec && ((reinterpret_cast<uintptr_t>(rs > 0 ? pf : pf - 1) & 15) == 0);
     constexpr int NB = 8;
-    for (int it0 = 0; 2 * (k + 8 * it0) < nr; it0 += NB) {
+    for (int it0 = 0; 2 * (k + TPC * it0) < nr; it0 += NB) {
         double2 v[NB];
         unsigned paired = 0;
 #pragma unroll
         for (int u = 0; u < NB; ++u) {
-            const int r = 2 * (k + 8 * (it0 + u));
+            const int r = 2 * (k + TPC * (it0 + u));
             v[u] = make_double2(0.0, 0.0);
             if (c >= nc || r >= nr) continue;
             const bool in0 = r >= lo_r && r < hi_r, in1 = r + 1 >= lo_r && r + 1 < hi_r;
@@ -1287,7 +1296,7 @@ __device__ __forceinline__ void df_stage_panel(const Lu& L, double* __restrict__
         }
 #pragma unroll
         for (int u = 0; u < NB; ++u) {
-            const int r = 2 * (k + 8 * (it0 + u));
+            const int r = 2 * (k + TPC * (it0 + u));
             if (r >= nr) continue;
             const double2 w = (rs < 0 && (paired >> u & 1)) ? make_double2(v[u].y, v[u].x) : v[u];
             if (r + 1 < nr)
@@ -1306,9 +1315,10 @@ struct DfTile {
     int ja, R, c0, wc, fr;
 };
 
-__device__ __forceinline__ void df_c_load(const Lu& L, const DfTile& T, double (&acc)[kDfNG][2][2]) {
+template <int NT>
+__device__ __forceinline__ void df_c_load(const Lu& L, const DfTile& T, double (&acc)[DfCfg<NT>::NG][2][2]) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
-    const int col0 = T.c0 + 16 * (warp >> 2), rw = warp & 3, ngr = (T.R + 7) >> 3;
+    const int col0 = T.c0 + 16 * (warp / DfCfg<NT>::RW), rw = warp % DfCfg<NT>::RW, ngr = (T.R + 7) >> 3;
     const long long rs = L.rs;
     const bool vec = rs == 1 || rs == -1;
     unsigned paired = 0;
@@ -1322,8 +1332,8 @@ __device__ __forceinline__ void df_c_load(const Lu& L, const DfTile& T, double (
         const bool al_s = vec && ((reinterpret_cast<uintptr_t>(rs > 0 ? ps : ps - 1) & 15) == 0);
         const bool al_f = vec && ((reinterpret_cast<uintptr_t>(rs > 0 ? pf : pf - 1) & 15) == 0);
 #pragma unroll
-        for (int t = 0; t < kDfNG; ++t) {
-            const int g = rw + 4 * t, i = 8 * g + 2 * lc;
+        for (int t = 0; t < DfCfg<NT>::NG; ++t) {
+            const int g = rw + DfCfg<NT>::RW * t, i = 8 * g + 2 * lc;
             acc[t][q][0] = acc[t][q][1] = 0.0;
             if (g >= ngr || !cok || i >= T.R) continue;
             const bool f0 = fc || i >= T.fr, f1 = fc || i + 1 >= T.fr;
@@ -1342,7 +1352,7 @@ __device__ __forceinline__ void df_c_load(const Lu& L, const DfTile& T, double (
     }
     if (rs < 0) {
 #pragma unroll
-        for (int t = 0; t < kDfNG; ++t)
+        for (int t = 0; t < DfCfg<NT>::NG; ++t)
 #pragma unroll
             for (int q = 0; q < 2; ++q)
                 if (paired >> (2 * t + q) & 1) {
@@ -1353,9 +1363,10 @@ __device__ __forceinline__ void df_c_load(const Lu& L, const DfTile& T, double (
     }
 }
 
-__device__ __forceinline__ void df_c_store(const Lu& L, const DfTile& T, const double (&acc)[kDfNG][2][2]) {
+template <int NT>
+__device__ __forceinline__ void df_c_store(const Lu& L, const DfTile& T, const double (&acc)[DfCfg<NT>::NG][2][2]) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
-    const int col0 = T.c0 + 16 * (warp >> 2), rw = warp & 3, ngr = (T.R + 7) >> 3;
+    const int col0 = T.c0 + 16 * (warp / DfCfg<NT>::RW), rw = warp % DfCfg<NT>::RW, ngr = (T.R + 7) >> 3;
     const long long rs = L.rs;
     const bool vec = rs == 1 || rs == -1;
 #pragma unroll
@@ -1365,8 +1376,8 @@ __device__ __forceinline__ void df_c_store(const Lu& L, const DfTile& T, const d
         double* ps = L.at(T.ja, T.ja + c);
         const bool al = vec && ((reinterpret_cast<uintptr_t>(rs > 0 ? ps : ps - 1) & 15) == 0);
 #pragma unroll
-        for (int t = 0; t < kDfNG; ++t) {
-            const int g = rw + 4 * t, i = 8 * g + 2 * lc;
+        for (int t = 0; t < DfCfg<NT>::NG; ++t) {
+            const int g = rw + DfCfg<NT>::RW * t, i = 8 * g + 2 * lc;
             if (g >= ngr || i >= T.R) continue;
             double* p0 = ps + i * rs;
             if (i + 1 < T.R && al) {
@@ -1385,14 +1396,15 @@ __device__ __forceinline__ void df_c_store(const Lu& L, const DfTile& T, const d
 // A12 rows of step (jb, ja) for window columns [c0, c0 + nc) (nc <= 32 kDfG): -> U[r * uld + c] (zero outside
 // the band and for c >= wc); entries in window columns >= fr (or every entry at step 0) have never been
 // updated. Column-major over the threads (coalesced band columns), four loads in flight per thread.
+template <int NT>
 __device__ __forceinline__ void df_a12(const Lu& L, int jb, int ja, int c0, int nc, int wc, int fr, bool first,
                                        double* __restrict__ U, int uld) {
     const int total = 32 * nc;
-    for (int e0 = threadIdx.x; e0 < total; e0 += 4 * kDfThreads) {
+    for (int e0 = threadIdx.x; e0 < total; e0 += 4 * NT) {
         double v[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            const int e = e0 + u * kDfThreads, c = e >> 5, r = e & 31;
+            const int e = e0 + u * NT, c = e >> 5, r = e & 31;
             v[u] = 0.0;
             if (e < total && c < wc && 32 + c0 + c - r <= L.K) {
                 const int gc = ja + c0 + c;
@@ -1401,7 +1413,7 @@ __device__ __forceinline__ void df_a12(const Lu& L, int jb, int ja, int c0, int 
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            const int e = e0 + u * kDfThreads;
+            const int e = e0 + u * NT;
             if (e < total) U[(e & 31) * uld + (e >> 5)] = v[u];
         }
     }
@@ -1412,10 +1424,12 @@ __device__ __forceinline__ void df_a12(const Lu& L, int jb, int ja, int c0, int 
 // reference's order (c -= l_k u_k, k = 0..31, FMA-contracted), the result straight into the next panel
 // Pn[c * pld + i] (after the barrier that ends every read of P). Thread: rows (tid % 64) + 64 h, columns
 // 8 (tid / 64) + [0, 8) (a warp shares its columns: U12 loads are broadcasts).
+template <int NT>
 __device__ __forceinline__ void df_chain_update(const Lu& L, const DfTile& T, const double* __restrict__ P,
                                                 double* __restrict__ Pn, int pld, const double* __restrict__ U,
                                                 int uld) {
-    const int i0 = threadIdx.x & 63, cg = threadIdx.x >> 6;
+    constexpr int RS = NT / 4;  // rows per pass; 4 column groups of 8
+    const int i0 = threadIdx.x % RS, cg = threadIdx.x / RS;
     const long long rs = L.rs;
     double c[4][8];
 #pragma unroll
@@ -1426,7 +1440,7 @@ __device__ __forceinline__ void df_chain_update(const Lu& L, const DfTile& T, co
         const double* pf = L.src_at(T.ja, T.ja + cc);
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
-            const int i = i0 + 64 * h;
+            const int i = i0 + RS * h;
             c[h][q] = (i < T.R && cc < T.wc) ? __ldcg(((fc || i >= T.fr) ? pf : ps) + i * rs) : 0.0;
         }
     }
@@ -1441,7 +1455,7 @@ __device__ __forceinline__ void df_chain_update(const Lu& L, const DfTile& T, co
             u[2 * q + 1] = w.y;
         }
 #pragma unroll
-        for (int h = 0; h < 4; ++h) l[h] = P[k * pld + 32 + i0 + 64 * h];
+        for (int h = 0; h < 4; ++h) l[h] = P[k * pld + 32 + i0 + RS * h];
 #pragma unroll
         for (int h = 0; h < 4; ++h)
 #pragma unroll
@@ -1450,7 +1464,7 @@ __device__ __forceinline__ void df_chain_update(const Lu& L, const DfTile& T, co
     __syncthreads();  // every warp is done with panel s-1
 #pragma unroll
     for (int h = 0; h < 4; ++h) {
-        const int i = i0 + 64 * h;
+        const int i = i0 + RS * h;
         if (i >= T.R) continue;
 #pragma unroll
         for (int q = 0; q < 8; ++q)
@@ -1463,13 +1477,14 @@ __device__ __forceinline__ void df_chain_update(const Lu& L, const DfTile& T, co
 // column). Element (q, c) receives j = 0..q-1 in ascending order with the same FMAs as a column-sequential
 // substitution (block_factors.hpp:246-250 order; bitwise panel_rows_cols' column half) with dependent chains
 // <= 24 + 7 long. The final U12 entries (window columns [c0, c0 + wc)) go to the store. Ends with a barrier.
+template <int NT>
 __device__ __forceinline__ void df_u12(const Lu& L, int jb, int ja, int c0, int nc, int wc,
                                        const double* __restrict__ P, int pld, double* __restrict__ U, int uld) {
     constexpr int B = 32, H = 8;
     const int tid = threadIdx.x, rr = tid >> 5, c = tid & 31;
 #pragma unroll 1
     for (int b0 = 0; b0 < B; b0 += H) {
-        if (b0 > 0) {
+        if (b0 > 0 && rr < H) {
             const int q = b0 + rr;
             double x[kDfG];
 #pragma unroll
@@ -1485,8 +1500,8 @@ __device__ __forceinline__ void df_u12(const Lu& L, int jb, int ja, int c0, int 
 #pragma unroll
             for (int g = 0; g < kDfG; ++g)
                 if (c + 32 * g < nc) U[q * uld + c + 32 * g] = x[g];
-            __syncthreads();
         }
+        if (b0 > 0) __syncthreads();
         if (tid < nc) {
             double x[H];
 #pragma unroll
@@ -1503,18 +1518,19 @@ __device__ __forceinline__ void df_u12(const Lu& L, int jb, int ja, int c0, int 
         __syncthreads();
     }
     // final U12 entries (the store's A12 rows; evict-first: the factorization is done with them)
-    for (int e = tid; e < B * nc; e += kDfThreads) {
+    for (int e = tid; e < B * nc; e += NT) {
         const int cc = e >> 5, r = e & 31;
         if (cc < wc && B + c0 + cc - r <= L.K) st_first(L.at(jb + r, ja + c0 + cc), U[r * uld + cc]);
     }
 }
 
 // C -= L21 U12 (C^T -= U12^T L21^T, k-steps of 4 in order: k_band_lu_res' fragments and order)
+template <int NT>
 __device__ __forceinline__ void df_dmma(const DfTile& T, const double* __restrict__ P, int pld,
-                                        const double* __restrict__ U, int uld, double (&acc)[kDfNG][2][2]) {
+                                        const double* __restrict__ U, int uld, double (&acc)[DfCfg<NT>::NG][2][2]) {
     constexpr int nb = 32;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
-    const int cp = warp >> 2, rw = warp & 3, ngr = (T.R + 7) >> 3;
+    const int cp = warp / DfCfg<NT>::RW, rw = warp % DfCfg<NT>::RW, ngr = (T.R + 7) >> 3;
     const double* pk = P + nb + lr;
     const double* uk = U + 16 * cp + lr;
 #pragma unroll
@@ -1522,8 +1538,8 @@ __device__ __forceinline__ void df_dmma(const DfTile& T, const double* __restric
         const int kk = ks * 4 + lc;
         const double a0 = uk[kk * uld], a1 = uk[kk * uld + 8];
 #pragma unroll
-        for (int t = 0; t < kDfNG; ++t) {
-            const int g = rw + 4 * t;
+        for (int t = 0; t < DfCfg<NT>::NG; ++t) {
+            const int g = rw + DfCfg<NT>::RW * t;
             if (g < ngr) {
                 const double b = -pk[kk * pld + 8 * g];
                 dmma_m8n8k4(acc[t][0][0], acc[t][0][1], a0, b, acc[t][0][0], acc[t][0][1]);
@@ -1533,8 +1549,38 @@ __device__ __forceinline__ void df_dmma(const DfTile& T, const double* __restric
     }
 }
 
+// L21 rows of a factored diagonal block: panel_rows_cols' row half (thread per row, the same operations, hence
+// the same bits) for any number of rows over NT threads
+template <int B, bool FULL, int NT>
+__device__ __noinline__ void df_rows(double* __restrict__ P, int pld, const double* __restrict__ Ut,
+                                     const double* __restrict__ s_piv, int nb_rt, int ph) {
+    const int nb = FULL ? B : nb_rt;
+    for (int r = nb + (int)threadIdx.x; r < ph; r += NT) {
+        double x[B];
+#pragma unroll
+        for (int c = 0; c < B; ++c) x[c] = c < nb ? P[c * pld + r] : 0.0;
+#pragma unroll
+        for (int c = 0; c < B; ++c) {
+            if (c < nb) {
+                const double l = div_rcp(x[c], s_piv[c], s_piv[B + c]);
+                x[c] = l;
+                const double2* __restrict__ u2 = reinterpret_cast<const double2*>(Ut + ut_off(c) - ut_lo(c));
+#pragma unroll
+                for (int j = (c + 1) & ~1; j < B; j += 2) {
+                    const double2 u = lds2(reinterpret_cast<const double*>(u2 + (j >> 1)));
+                    if (j > c) x[j] = fma(-l, u.x, x[j]);
+                    x[j + 1] = fma(-l, u.y, x[j + 1]);
+                }
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < B; ++c)
+            if (c < nb) P[c * pld + r] = x[c];
+    }
+}
+
 // ---- chain item (panel SMs): strip(s-1, 0) -- the update of block s -- fused with panel(s) -----------------
-template <bool STREAM>
+template <int NT, bool STREAM>
 __device__ __forceinline__ void df_chain(const DfArgs& A, const FactorJob& J, int jid, int s, double* __restrict__ P,
                                          double* __restrict__ U, double* __restrict__ s_ut,
                                          double* __restrict__ s_rcp, int* s_boosts) {
@@ -1563,26 +1609,27 @@ __device__ __forceinline__ void df_chain(const DfArgs& A, const FactorJob& J, in
     }
     __syncthreads();
     if (s > 0) {
-        df_stage_panel(L, P, pld, jbp, jbp, B + rprev, B, B + rprev);
-        df_a12(L, jbp, jb, 0, 32, T.wc, T.fr, sp == 0, U, uld);
-        // this panel's rows that no earlier step updated: loaded now, written after the update
-        double fv[4];
+        df_stage_panel<NT>(L, P, pld, jbp, jbp, B + rprev, B, B + rprev);
+        df_a12<NT>(L, jbp, jb, 0, 32, T.wc, T.fr, sp == 0, U, uld);
+        // this panel's rows that no earlier step updated (<= 32 of them): loaded now, written after the update
+        constexpr int NF = 1024 / NT;
+        double fv[NF];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int e = tid + u * kDfThreads, c = e >> 5, r = rprev + (e & 31);
+        for (int u = 0; u < NF; ++u) {
+            const int e = tid + u * NT, c = e >> 5, r = rprev + (e & 31);
             fv[u] = (c < nb && r < ph && L.inband(r, c)) ? __ldcg(L.src_at(jb + r, jb + c)) : 0.0;
         }
         __syncthreads();
         DF_MARK(1);
-        df_u12(L, jbp, jb, 0, 32, T.wc, P, pld, U, uld);
-        df_chain_update(L, T, P, P, pld, U, uld);
+        df_u12<NT>(L, jbp, jb, 0, 32, T.wc, P, pld, U, uld);
+        df_chain_update<NT>(L, T, P, P, pld, U, uld);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int e = tid + u * kDfThreads, c = e >> 5, r = rprev + (e & 31);
+        for (int u = 0; u < NF; ++u) {
+            const int e = tid + u * NT, c = e >> 5, r = rprev + (e & 31);
             if (r < pld) P[c * pld + r] = fv[u];
         }
     } else {
-        df_stage_panel(L, P, pld, jb, jb, ph, nb, 0);
+        df_stage_panel<NT>(L, P, pld, jb, jb, ph, nb, 0);
     }
     __syncthreads();
     DF_MARK(2);
@@ -1595,14 +1642,14 @@ __device__ __forceinline__ void df_chain(const DfArgs& A, const FactorJob& J, in
     __syncthreads();
     // L21 rows (thread per row; panel_rows_cols' row half)
     if (nb == B)
-        panel_rows_cols<B, true>(P, nullptr, pld, uld, s_ut, s_rcp, nb, ph, 0);
+        df_rows<B, true, NT>(P, pld, s_ut, s_rcp, nb, ph);
     else
-        panel_rows_cols<B, false>(P, nullptr, pld, uld, s_ut, s_rcp, nb, ph, 0);
+        df_rows<B, false, NT>(P, pld, s_ut, s_rcp, nb, ph);
     __syncthreads();
     DF_MARK(3);
     // the panel is final: L11\U11 and L21 to the store (the worker strips of this step read it from L2)
     const long long rs = L.rs;
-    for (int c = warp; c < nb; c += kDfThreads / 32) {
+    for (int c = warp; c < nb; c += NT / 32) {
         double* g = L.at(jb, jb + c);
         const int r1 = min(ph, c + K + 1);
 #pragma unroll 4
@@ -1612,7 +1659,7 @@ __device__ __forceinline__ void df_chain(const DfArgs& A, const FactorJob& J, in
     if (nbn > 0 && ja + R < m) {
         const int e = ja + R;
         const int ncol = min(e + nbn, m) - ja;
-        for (int t = tid; t < ncol + min(nbn, m - e); t += kDfThreads) {
+        for (int t = tid; t < ncol + min(nbn, m - e); t += NT) {
             if (t < ncol)
                 prefetch_run(L, ja + t, e, e + nbn);
             else
@@ -1632,7 +1679,7 @@ __device__ __forceinline__ void df_chain(const DfArgs& A, const FactorJob& J, in
 // ---- worker item (worker SMs): strips j = 1 + kDfG g .. of step s -------------------------------------------
 // One panel load, one A12 load and one U12 solve for the group; then per strip: C tile in, DMMA, C tile out and
 // its column block's flag released at once (the chain two steps on waits for strip 1 only).
-template <bool STREAM>
+template <int NT, bool STREAM>
 __device__ __forceinline__ void df_worker(const DfArgs& A, const FactorJob& J, int jid, int s, int g,
                                           double* __restrict__ P, double* __restrict__ U) {
     constexpr int B = 32;
@@ -1658,18 +1705,18 @@ __device__ __forceinline__ void df_worker(const DfArgs& A, const FactorJob& J, i
         if (A.trace) A.trace[8 * (size_t)blockIdx.x + 0] = df_now();
     }
     __syncthreads();
-    df_stage_panel(L, P, pld, jb, jb, ph, B, ph);
-    df_a12(L, jb, ja, c0, 32 * (j1 - j0), R - c0, fr, s == 0, U, uld);
+    df_stage_panel<NT>(L, P, pld, jb, jb, ph, B, ph);
+    df_a12<NT>(L, jb, ja, c0, 32 * (j1 - j0), R - c0, fr, s == 0, U, uld);
     __syncthreads();
     DF_MARK(1);
-    df_u12(L, jb, ja, c0, 32 * (j1 - j0), R - c0, P, pld, U, uld);
+    df_u12<NT>(L, jb, ja, c0, 32 * (j1 - j0), R - c0, P, pld, U, uld);
     DF_MARK(2);
     for (int j = j0; j < j1; ++j) {
         const DfTile T{ja, R, 32 * j, min(32, R - 32 * j), fr};
-        double acc[kDfNG][2][2];
-        df_c_load(L, T, acc);
-        df_dmma(T, P, pld, U + 32 * (j - j0), uld, acc);
-        df_c_store(L, T, acc);
+        double acc[DfCfg<NT>::NG][2][2];
+        df_c_load<NT>(L, T, acc);
+        df_dmma<NT>(T, P, pld, U + 32 * (j - j0), uld, acc);
+        df_c_store<NT>(L, T, acc);
         __syncthreads();
         if (tid == 0) st_release_i(A.col_step + (size_t)jid * A.S + s + 1 + j, s + 1);
     }
@@ -1682,8 +1729,8 @@ __device__ __forceinline__ void df_worker(const DfArgs& A, const FactorJob& J, i
 // Panel SMs take chain items from counter_p in order (s-major); the other SMs take worker items from counter_w
 // in wave order. Both orders are consistent with one topological order (chain(s) ~ 2s,
 // strip(s, .) ~ 2s + 1), so the earliest unfinished item is always grabbed and runnable: no deadlock.
-template <bool STREAM>
-__global__ void __launch_bounds__(kDfThreads, 2) k_band_lu_df(DfArgs A) {
+template <int NT, bool STREAM>
+__global__ void __launch_bounds__(NT, DfCfg<NT>::MINB) k_band_lu_df(DfArgs A) {
     extern __shared__ __align__(16) double smem[];
     __shared__ __align__(16) double s_ut[kUtSize];
     __shared__ double s_rcp[64];
@@ -1740,7 +1787,7 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_band_lu_df(DfArgs A) {
             if (item >= A.S * J) break;
             const int s = item / J, jid = item - s * J;
             const FactorJob Jb = A.jobs[jid];
-            df_chain<STREAM>(A, Jb, jid, s, P, U, s_ut, s_rcp, &s_boosts);
+            df_chain<NT, STREAM>(A, Jb, jid, s, P, U, s_ut, s_rcp, &s_boosts);
             rec = item;
         } else {
             bool done = false;
@@ -1756,7 +1803,7 @@ __global__ void __launch_bounds__(kDfThreads, 2) k_band_lu_df(DfArgs A) {
             if (done) break;
             const int ng = wn / J, o = item - w0, jid = o / ng;
             const FactorJob Jb = A.jobs[jid];
-            df_worker<STREAM>(A, Jb, jid, w, o % ng, P, U);
+            df_worker<NT, STREAM>(A, Jb, jid, w, o % ng, P, U);
             rec = (long long)A.S * J + item;
         }
         __syncthreads();
@@ -1789,7 +1836,8 @@ size_t lu_df_scratch_ints(int njobs, int m_max) {
 bool lu_df_applies(int max_k, int njobs) {
     int dev = 0, nsm = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    return max_k >= kLuDfMinK && max_k <= 224 && 10 * njobs <= 7 * nsm;
+    if (max_k > 224) return max_k <= 512;  // no resident single-CTA kernel beyond K = 224
+    return max_k >= kLuDfMinK && 10 * njobs <= 7 * nsm;
 }
 
 void launch_band_lu_df(const FactorJob* d_jobs, int njobs, int m_max, int max_k, double eps, cudaStream_t s,
@@ -1817,12 +1865,16 @@ void launch_band_lu_df(const FactorJob* d_jobs, int njobs, int m_max, int max_k,
     A.uld = pad_ld(32 * kDfG);
     A.trace = nullptr;
     const size_t bytes = sizeof(double) * (size_t)(B * A.pld + B * A.uld);
-    auto kern = streamed ? k_band_lu_df<true> : k_band_lu_df<false>;
+    const bool wide = max_k > DfCfg<256>::MAXK;
+    if (max_k > DfCfg<512>::MAXK) throw InvalidArgument("band LU (dataflow): half-bandwidth above 512");
+    const int nt = wide ? 512 : 256;
+    void (*kern)(DfArgs) = wide ? (streamed ? k_band_lu_df<512, true> : k_band_lu_df<512, false>)
+                                : (streamed ? k_band_lu_df<256, true> : k_band_lu_df<256, false>);
     SAP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     int dev = 0, nsm = 0, per_sm = 0;
     SAP_CUDA(cudaGetDevice(&dev));
     SAP_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    SAP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDfThreads, bytes));
+    SAP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, bytes));
     // chain items (one per job and step) + worker strips
     long long items = (long long)njobs * S;
     for (int w = 0; w <= S - 2; ++w)
@@ -1845,7 +1897,7 @@ void launch_band_lu_df(const FactorJob* d_jobs, int njobs, int m_max, int max_k,
         g_df_trace_items = items;
         g_df_trace_grid = grid;
     }
-    kern<<<grid, kDfThreads, bytes, s>>>(A);
+    kern<<<grid, nt, bytes, s>>>(A);
     SAP_LAUNCHED();
 }
 

@@ -23,6 +23,9 @@ CASES = [
     (40000, 200, 0.06, 10, S.PrecondKind.coupled, True),
     (40000, 224, 1.0, 8, S.PrecondKind.decoupled, False),
     (9000, 130, 0.2, 4, S.PrecondKind.coupled, False),
+    (40000, 300, 1.0, 8, S.PrecondKind.coupled, True),
+    (60000, 500, 1.0, 10, S.PrecondKind.coupled, True),
+    (50000, 401, 0.5, 9, S.PrecondKind.decoupled, False),
     (200000, 200, 1.0, 50, S.PrecondKind.coupled, True),
     (200000, 200, 1.0, 50, S.PrecondKind.decoupled, True),
 ]

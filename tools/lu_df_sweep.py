@@ -3,7 +3,7 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, paper_1509_07919_b200 as S
 
-CASES = [(2000000, 128, 512, "C"), (2000000, 128, 512, "D"), (2000000, 128, 64, "C"), (200000, 64, 50, "C"),
+CASES = [(200000, 300, 50, "C"), (200000, 300, 50, "D"), (200000, 500, 50, "C"), (200000, 500, 50, "D"),(2000000, 128, 512, "C"), (2000000, 128, 512, "D"), (2000000, 128, 64, "C"), (200000, 64, 50, "C"),
          (200000, 100, 50, "C"), (200000, 160, 50, "C"), (200000, 200, 50, "C"), (200000, 200, 50, "D"),
          (200000, 224, 50, "C"), (200000, 200, 25, "C")]
 for n, k, p, kind in CASES:
