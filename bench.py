@@ -368,7 +368,10 @@ def run_ours(args) -> None:
     peak = FP64_PEAK_TFLOPS * world
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "kernel": "k_band_lu_res (block LU+UL, DMMA f64)",
+                "kernel": "k_band_lu_df (dataflow block LU+UL over every SM: pivot chains on claimed panel SMs, "
+                          "DMMA f64 strips on the others)" if pre == "C" else
+                          "k_band_lu_df (dataflow block LU over every SM: pivot chains on claimed panel SMs, "
+                          "DMMA f64 strips on the others)",
                 "peak_source": f"FP64 DMMA measured on this pool (profiles/fp64_peaks_r01.json) x {world} GPU; "
                                "MEASURED_PEAKS.json carries no FP64 figure",
                 "algorithmic_flops_per_launch": m2["flops"], "launch_ms": m2["t_fk"] * 1e3}

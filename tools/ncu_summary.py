@@ -76,7 +76,7 @@ def main(tag):
     if "lu" in traffic:
         with open(os.path.join(out_dir, "ncu_lu_traffic.json"), "w") as f:
             json.dump({"SaP-C": traffic["lu"], "source": f"profiles/ncu_{tag}.txt (dram__bytes_read.sum + "
-                       "dram__bytes_write.sum of one k_band_lu_res launch, LU+UL of config 2)",
+                       "dram__bytes_write.sum of one band LU launch (k_band_lu_df), LU+UL of config 2)",
                        "sweep": traffic.get("sweep"), "spmv": traffic.get("spmv")}, f, indent=1)
     print("\n".join(lines))
 
