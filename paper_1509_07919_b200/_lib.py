@@ -16,7 +16,7 @@ class sap_options(C.Structure):
     _fields_ = [("p", C.c_int), ("precond", C.c_int), ("boost_eps", C.c_double), ("method", C.c_int),
                 ("ell", C.c_int), ("rel_tol", C.c_double), ("abs_tol", C.c_double), ("max_iterations", C.c_int),
                 ("mixed_precision", C.c_int), ("caller_asserts_spd", C.c_int), ("device", C.c_int),
-                ("triangle_solve", C.c_int)]
+                ("triangle_solve", C.c_int), ("lu_kernel", C.c_int)]
 
 
 class sap_report(C.Structure):

@@ -845,7 +845,7 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
         SAP_CUDA(cudaMemcpyAsync(h->gjobs.get(), gj.data(), sizeof(FactorJob) * njobs, cudaMemcpyHostToDevice, s));
         SAP_CUDA(cudaMemsetAsync(h->d_minpiv.get(), 0, sizeof(double) * njobs, s));  // -1 = stalled upload
         SAP_CUDA(cudaEventRecord(h->ev[8], s));
-        launch_band_lu(h->sjobs.get(), njobs, k, h->opt.boost_eps, s, true, m_max, lu_scratch(h, njobs, m_max));
+        launch_band_lu(h->sjobs.get(), njobs, k, h->opt.boost_eps, s, true, m_max, lu_scratch(h, njobs, m_max), h->opt.lu_kernel);
         SAP_CUDA(cudaEventRecord(h->ev[9], s));
         // 3. once the norms exist: any pivot below the boost threshold means the reference would have
         //    boosted -> refactor with boosting (rare; exact either way)
@@ -853,10 +853,10 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
         launch_stream_check(h->sjobs.get(), h->d_minpiv.get(), h->norms.get(), njobs, p, h->opt.boost_eps,
                             h->d_sbad.get(), s);
         // the refactor with boosting is always launched; its CTAs exit at once unless the check asked for it
-        launch_band_lu(h->gjobs.get(), njobs, k, h->opt.boost_eps, s, false, m_max, lu_scratch(h, njobs, m_max));
+        launch_band_lu(h->gjobs.get(), njobs, k, h->opt.boost_eps, s, false, m_max, lu_scratch(h, njobs, m_max), h->opt.lu_kernel);
     } else {
         SAP_CUDA(cudaEventRecord(h->ev[8], s));
-        launch_band_lu(h->jobs.get(), njobs, k, h->opt.boost_eps, s, false, m_max, lu_scratch(h, njobs, m_max));
+        launch_band_lu(h->jobs.get(), njobs, k, h->opt.boost_eps, s, false, m_max, lu_scratch(h, njobs, m_max), h->opt.lu_kernel);
         SAP_CUDA(cudaEventRecord(h->ev[9], s));
     }
     {
@@ -981,7 +981,7 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
                                   h->rbar_norms.get() + t, h->rbar_boosts.get() + t};
             h->rjobs.alloc(ni);
             SAP_CUDA(cudaMemcpyAsync(h->rjobs.get(), rj.data(), sizeof(FactorJob) * ni, cudaMemcpyHostToDevice, s));
-            launch_band_lu(h->rjobs.get(), ni, k - 1, h->opt.boost_eps, s, false, k, lu_scratch(h, ni, k));
+            launch_band_lu(h->rjobs.get(), ni, k - 1, h->opt.boost_eps, s, false, k, lu_scratch(h, ni, k), h->opt.lu_kernel);
             SweepPlan<double>& rp = h->rplan;
             rp = SweepPlan<double>{};
             rp.f = h->rbar.get();
@@ -1237,7 +1237,7 @@ void setup_banded_dist(sap_handle* h, int n, int k, int row_lo, int row_hi, cons
         launch_copy_blocks(h->band_ptr, k, h->d_boffs.get(), pl, h->fst, h->lu.get(),
                            h->coupled ? h->ul.get() : nullptr, s);
     SAP_CUDA(cudaEventRecord(h->ev[8], s));
-    launch_band_lu(h->jobs.get(), njobs, k, h->opt.boost_eps, s, false, m_max, lu_scratch(h, njobs, m_max));
+    launch_band_lu(h->jobs.get(), njobs, k, h->opt.boost_eps, s, false, m_max, lu_scratch(h, njobs, m_max), h->opt.lu_kernel);
     SAP_CUDA(cudaEventRecord(h->ev[9], s));
     {
         SweepPlan<double>& lp = h->lplan;
@@ -1337,7 +1337,7 @@ void setup_banded_dist(sap_handle* h, int n, int k, int row_lo, int row_hi, cons
                               h->rbar_norms.get() + t, h->rbar_boosts.get() + t};
         h->rjobs.alloc(ni);
         SAP_CUDA(cudaMemcpyAsync(h->rjobs.get(), rj.data(), sizeof(FactorJob) * ni, cudaMemcpyHostToDevice, s));
-        launch_band_lu(h->rjobs.get(), ni, w - 1, h->opt.boost_eps, s, false, w, lu_scratch(h, ni, w));
+        launch_band_lu(h->rjobs.get(), ni, w - 1, h->opt.boost_eps, s, false, w, lu_scratch(h, ni, w), h->opt.lu_kernel);
         SweepPlan<double>& rp = h->rplan;
         rp = SweepPlan<double>{};
         rp.f = h->rbar.get();
@@ -1417,6 +1417,7 @@ void sap_options_default(sap_options* o) {
     o->caller_asserts_spd = 0;
     o->device = 0;
     o->triangle_solve = 0;
+    o->lu_kernel = 0;
 }
 
 int sap_max_feasible_partitions(int n, int k) {

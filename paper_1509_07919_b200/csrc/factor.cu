@@ -321,10 +321,11 @@ static void launch_lu_b(const FactorJob* jobs, int njobs, int max_k, double eps,
 }
 
 void launch_band_lu(const FactorJob* d_jobs, int njobs, int max_k, double boost_eps, cudaStream_t s, bool streamed,
-                    int m_max, int* df_scratch) {
+                    int m_max, int* df_scratch, int lu_kernel) {
     if (njobs <= 0) return;
-    const char* force = getenv("SAP_LU_DF");  // tools/lu_df_*.py A/B: "0" single-CTA, "1" dataflow where it runs
-    const bool df = force ? (atoi(force) != 0 && max_k >= 64 && max_k <= 512) : lu_df_applies(max_k, njobs);
+    const bool df = lu_kernel == 1   ? false
+                    : lu_kernel == 2 ? (max_k >= 64 && max_k <= 512)
+                                     : lu_df_applies(max_k, njobs);
     if (df_scratch && m_max > 0 && df) {
         launch_band_lu_df(d_jobs, njobs, m_max, max_k, boost_eps, s, streamed, df_scratch);
         return;

@@ -25,8 +25,9 @@ void launch_copy_blocks(const double* band, int k, const int* d_offsets, int p, 
 // streamed: the jobs carry FactorJob::ready (k_band_lu_res<B, true>; only where band_lu_reads_source(max_k))
 // df_scratch (lu_df_scratch_ints(njobs, m_max) ints, owned by the caller, one launch at a time): run the
 // dataflow kernel k_band_lu_df over every SM where it applies (lu_df_applies(max_k)); m_max = largest job.
+// lu_kernel: sap_options::lu_kernel (0 automatic, 1 one CTA per job, 2 dataflow where supported)
 void launch_band_lu(const FactorJob* d_jobs, int njobs, int max_k, double boost_eps, cudaStream_t s,
-                    bool streamed = false, int m_max = 0, int* df_scratch = nullptr);
+                    bool streamed = false, int m_max = 0, int* df_scratch = nullptr, int lu_kernel = 0);
 size_t lu_df_scratch_ints(int njobs, int m_max);
 bool lu_df_applies(int max_k, int njobs);
 void launch_band_lu_df(const FactorJob* d_jobs, int njobs, int m_max, int max_k, double eps, cudaStream_t s,

@@ -1158,6 +1158,7 @@ struct DfArgs {
     unsigned* counter_p;  // chain items (panel SMs)
     unsigned* counter_w;  // worker strips
     int nps;              // the first nps SMs this launch's CTAs start on run chain items
+    int excl;             // 1: one chain CTA per panel SM (its other CTAs exit); the chain's update on DMMA
     int* sm_role;         // [kDfMaxSm]: 0 undecided, 1 panel, 2 worker, 3 being decided
     int* n_panel_sm;      // SMs claimed so far
     int* panel_cnt;  // [njobs]
@@ -1393,6 +1394,27 @@ __device__ __forceinline__ void df_c_store(const Lu& L, const DfTile& T, const d
     }
 }
 
+// The C tile (DMMA fragment layout, window columns [0, wc)) into the next panel's buffer: (i, c) -> Pn[c * pld + i]
+template <int NT>
+__device__ __forceinline__ void df_c_to_smem(const DfTile& T, const double (&acc)[DfCfg<NT>::NG][2][2], double* Pn,
+                                             int pld) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
+    const int col0 = 16 * (warp / DfCfg<NT>::RW), rw = warp % DfCfg<NT>::RW, ngr = (T.R + 7) >> 3;
+#pragma unroll
+    for (int t = 0; t < DfCfg<NT>::NG; ++t) {
+        const int g = rw + DfCfg<NT>::RW * t;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int c = col0 + 8 * q + lr, i = 8 * g + 2 * lc;
+            if (g >= ngr || c >= T.wc || i >= T.R) continue;
+            if (i + 1 < T.R)
+                *reinterpret_cast<double2*>(Pn + c * pld + i) = make_double2(acc[t][q][0], acc[t][q][1]);
+            else
+                Pn[c * pld + i] = acc[t][q][0];
+        }
+    }
+}
+
 // A12 rows of step (jb, ja) for window columns [c0, c0 + nc) (nc <= 32 kDfG): -> U[r * uld + c] (zero outside
 // the band and for c >= wc); entries in window columns >= fr (or every entry at step 0) have never been
 // updated. Column-major over the threads (coalesced band columns), four loads in flight per thread.
@@ -1622,7 +1644,15 @@ __device__ __forceinline__ void df_chain(const DfArgs& A, const FactorJob& J, in
         __syncthreads();
         DF_MARK(1);
         df_u12<NT>(L, jbp, jb, 0, 32, T.wc, P, pld, U, uld);
-        df_chain_update<NT>(L, T, P, P, pld, U, uld);
+        if (A.excl) {  // alone on its SM: the strip on DMMA (bitwise the DFMA form)
+            double acc[DfCfg<NT>::NG][2][2];
+            df_c_load<NT>(L, T, acc);
+            df_dmma<NT>(T, P, pld, U, uld, acc);
+            __syncthreads();  // every warp is done with panel s-1
+            df_c_to_smem<NT>(T, acc, P, pld);
+        } else {
+            df_chain_update<NT>(L, T, P, P, pld, U, uld);
+        }
 #pragma unroll
         for (int u = 0; u < NF; ++u) {
             const int e = tid + u * NT, c = e >> 5, r = rprev + (e & 31);
@@ -1758,10 +1788,18 @@ __global__ void __launch_bounds__(NT, DfCfg<NT>::MINB) k_band_lu_df(DfArgs A) {
                 __nanosleep(20);
                 r = ld_relaxed_i(rp);
             }
+            if (r == 1 && A.excl) r = 0;  // exclusive panel SM: only its deciding CTA stays
         }
         s_role = r;
     }
     __syncthreads();
+    if (s_role == 0) {
+        // spare CTA of an exclusive panel SM: it holds the slot (so no other kernel's CTAs land beside the
+        // pivot chain) until every chain item has been taken
+        if (tid == 0)
+            while (ld_relaxed_i(reinterpret_cast<const int*>(A.counter_p)) < A.S * J) __nanosleep(4000);
+        return;
+    }
     const bool panel_role = s_role == 1;
     unsigned* ctr = panel_role ? A.counter_p : A.counter_w;
     if (tid == 0) s_item = (int)atomicAdd(ctr, 1u);
@@ -1817,6 +1855,7 @@ __global__ void __launch_bounds__(NT, DfCfg<NT>::MINB) k_band_lu_df(DfArgs A) {
     }
 }
 
+static int g_df_trace_mode = 0;  // sap_dev_lu_df_trace_mode: 1 trace streamed launches, 2 the others
 static unsigned long long* g_df_trace = nullptr;
 static size_t g_df_trace_cap = 0;
 static long long g_df_trace_items = 0;
@@ -1881,11 +1920,14 @@ void launch_band_lu_df(const FactorJob* d_jobs, int njobs, int m_max, int max_k,
         items += (long long)njobs * (((std::min(max_k, m_max - B * (w + 1)) + 31) / 32 - 1 + kDfG - 1) / kDfG);
     const int grid = nsm * std::max(per_sm, 1);
     // panel SMs: one resident chain per job where the SMs allow (chains are latency-bound), at most 40 %
-    int nps = std::min((njobs + per_sm - 1) / std::max(per_sm, 1), (2 * nsm) / 5);
-    if (const char* e = getenv("SAP_LU_DF_NPS")) nps = atoi(e);
+    // panel SMs: one resident chain per job (chains are latency-bound), at most 40 % of the SMs; when every
+    // job gets a panel SM to itself (few jobs), it is exclusive: the chain's strip update then runs on DMMA
+    // without stalling another chain's pivots
+    const int cap = (2 * nsm) / 5;
+    A.excl = (njobs <= cap || per_sm <= 1) ? 1 : 0;  // one CTA per SM (wide bands) is exclusive anyway
+    int nps = A.excl ? std::min(njobs, cap) : std::min((njobs + per_sm - 1) / std::max(per_sm, 1), cap);
     A.nps = std::max(1, std::min(nps, nsm - 1));
-    const char* tr_env = getenv("SAP_LU_DF_TRACE");  // "s": trace streamed launches, "n": the others
-    if (tr_env && (tr_env[0] == 's') == streamed) {
+    if (g_df_trace_mode && (g_df_trace_mode == 1) == streamed) {  // tools/lu_df_trace.py
         const size_t need = 8 * (size_t)(grid + items);
         if (g_df_trace_cap < need) {
             if (g_df_trace) cudaFree(g_df_trace);
@@ -1925,6 +1967,8 @@ bool band_lu_reads_source(int max_k) {
 
 // tools/lu_df_trace.py only (not in include/sap_gpu.h): the last traced k_band_lu_df launch, 8 u64 per item
 // (grab, dependencies met, phase marks 1-4, end: globaltimer ns; SM << 32 | CTA). Returns the item count.
+extern "C" void sap_dev_lu_df_trace_mode(int mode) { sapgpu::g_df_trace_mode = mode; }
+
 extern "C" long long sap_dev_lu_df_trace(unsigned long long* out, long long cap) {
     using namespace sapgpu;
     if (!g_df_trace) return 0;

@@ -131,7 +131,8 @@ class Solver:
     """SaP setup()/solve() over libsap_gpu (one handle, one CUDA stream)."""
 
     def __init__(self, p: int = 1, precond: PrecondKind = PrecondKind.coupled, boost_eps: float = 1e-10,
-                 krylov: KrylovOptions | None = None, device: int = 0, triangle_solve: int = 0):
+                 krylov: KrylovOptions | None = None, device: int = 0, triangle_solve: int = 0,
+                 lu_kernel: int = 0):
         kr = krylov or KrylovOptions()
         o = L.sap_options()
         L.load().sap_options_default(C.byref(o))
@@ -140,6 +141,7 @@ class Solver:
         o.max_iterations, o.mixed_precision = int(kr.max_iterations), int(kr.mixed_precision)
         o.caller_asserts_spd, o.device = int(kr.caller_asserts_spd), int(device)
         o.triangle_solve = int(triangle_solve)  # 0 automatic, 1 chunk inverses, 2 substitution
+        o.lu_kernel = int(lu_kernel)  # 0 automatic, 1 one CTA per job, 2 dataflow (bitwise-equal factors)
         self.options = o
         self._h = C.c_void_p()
         self._create()

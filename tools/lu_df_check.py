@@ -33,11 +33,10 @@ CASES = [
 
 def run(case, df):
     n, k, d, p, kind, dev = case
-    os.environ["SAP_LU_DF"] = "1" if df else "0"
     band, rhs = S.random_banded(n, k, d, 1)
     src = torch.from_numpy(band).cuda() if dev else band
     out = {}
-    with S.Solver(p=p, precond=kind, device=0) as s:
+    with S.Solver(p=p, precond=kind, device=0, lu_kernel=2 if df else 1) as s:
         for _ in range(3):
             s.setup(src, n, k)
         s.synchronize()

@@ -17,8 +17,7 @@ dev = len(sys.argv) > 6 and sys.argv[6] == "dev"
 band, rhs = S.random_banded(n, k, d, 1)
 out = {}
 for df in (0, 1):
-    os.environ["SAP_LU_DF"] = str(df)
-    with S.Solver(p=p, precond=kind, device=0) as s:
+    with S.Solver(p=p, precond=kind, device=0, lu_kernel=2 if df else 1) as s:
         s.setup(torch.from_numpy(band).cuda() if dev else band, n, k)
         s.synchronize()
         out[f"lu{df}"] = s.factors(0)[0]

@@ -1,4 +1,4 @@
-"""Factor-kernel time of the single-CTA LU (SAP_LU_DF=0) vs the dataflow LU over shapes (device band)."""
+"""Factor-kernel time of the single-CTA LU (lu_kernel=1) vs the dataflow LU (lu_kernel=2) over shapes (device band)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, paper_1509_07919_b200 as S
@@ -11,9 +11,9 @@ for n, k, p, kind in CASES:
     db = torch.from_numpy(band).cuda()
     del band
     res = []
-    for df in ("0", "1"):
-        os.environ["SAP_LU_DF"] = df
-        with S.Solver(p=p, precond=S.PrecondKind.coupled if kind == "C" else S.PrecondKind.decoupled, device=0) as s:
+    for lk in (1, 2):
+        with S.Solver(p=p, precond=S.PrecondKind.coupled if kind == "C" else S.PrecondKind.decoupled, device=0,
+                      lu_kernel=lk) as s:
             ts = []
             for _ in range(4):
                 s.setup(db, n, k)

@@ -1,6 +1,6 @@
 """Timeline of one k_band_lu_df launch (per work item: grab, dependencies met, end) for config 2.
 
-    SAP_LU_DF_TRACE=s python tools/lu_df_trace.py [C|D] [n k p]
+    python tools/lu_df_trace.py [C|D] [n k p]    (traces the dataflow kernel's streamed/early-start launch)
 """
 import ctypes as C
 import os
@@ -34,11 +34,11 @@ def decode(item, J, K, m_max):
 def main():
     kind = sys.argv[1] if len(sys.argv) > 1 else "C"
     n, k, p = (int(x) for x in sys.argv[2:5]) if len(sys.argv) > 4 else (200000, 200, 50)
-    os.environ.setdefault("SAP_LU_DF_TRACE", "s")
+    _lib.load().sap_dev_lu_df_trace_mode(1)
     band, rhs = S.random_banded(n, k, 1.0, 1)
     src = torch.from_numpy(band).cuda()
     pk = S.PrecondKind.coupled if kind == "C" else S.PrecondKind.decoupled
-    with S.Solver(p=p, precond=pk, device=0) as s:
+    with S.Solver(p=p, precond=pk, device=0, lu_kernel=2) as s:
         for _ in range(3):
             s.setup(src, n, k)
         s.synchronize()
