@@ -271,6 +271,7 @@ void build_fp32_preconditioner(sap_handle* h, cudaStream_t s) {
     h->dinv_f.alloc(std::max<size_t>(sweep_dinv_elems(lp), 1));
     plan_sweeps(lp, h->dinv_f.get());
     lp.kappa = h->kappa_f.get();
+    lp.kb = h->ts ? h->d_kb.get() : nullptr;
     launch_chunk_inverses(lp, s);
     if (h->coupled && k > 0) {
         const int ni = p - 1;
@@ -719,7 +720,10 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
         const int m = L.sizes[b];
         double* f = h->lu.get() + h->fst.block(b);
         const double* a = h->band_ptr + (size_t)L.offsets[b] * w;
-        jobs[b] = FactorJob{f + k, 1, 2LL * k, m, k, h->norms.get() + b, h->boosts.get() + b, from_src ? a + k : nullptr};
+        // third stage: block b is factored at its own K_b inside the k-wide store (block_factors.hpp:155-180;
+        // the entries beyond K_b are zero and stay zero), so its cost scales with K_b^2
+        const int kj = h->ts ? std::max(h->ts_k[b], 1) : k;
+        jobs[b] = FactorJob{f + k, 1, 2LL * k, m, kj, h->norms.get() + b, h->boosts.get() + b, from_src ? a + k : nullptr};
         if (want_ul) {
             double* g = h->ul.get() + h->fst.block(b);
             const size_t last = (size_t)(m - 1) * w + k;
@@ -870,6 +874,7 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
         h->dinv.alloc(std::max<size_t>(sweep_dinv_elems(lp), 1));
         plan_sweeps(lp, h->dinv.get());
         lp.kappa = h->kappa.get();
+        lp.kb = h->ts ? h->d_kb.get() : nullptr;  // third stage: sweeps read each block's K_b columns only
         if (want_ul) {  // only the solve needs them: overlap with coupling / tips / reduced blocks
             SAP_CUDA(cudaEventRecord(h->sev[0], s));
             SAP_CUDA(cudaStreamWaitEvent(h->side, h->sev[0], 0));

@@ -268,7 +268,7 @@ template <class T, int TR, int S, bool SUBST>
 __global__ void __launch_bounds__(kSwThreads, 1)
     k_sweep_tma(const __grid_constant__ CUtensorMap map, const T* __restrict__ dinv, int nch_max,
                 const int* __restrict__ offs, int k, T* __restrict__ xbase, int xw, int slab_cols, int box_c,
-                int nbox, const T* __restrict__ tri) {
+                int nbox, const T* __restrict__ tri, const int* __restrict__ kbs) {
     constexpr int SD = SweepSmem<T, TR, S>::SD;
     constexpr int CG = 32 / TR;  // column groups per warp
     constexpr int PF = 6;        // L2 prefetch distance (chunks)
@@ -283,6 +283,11 @@ __global__ void __launch_bounds__(kSwThreads, 1)
 
     const int b = blockIdx.x;
     const int off = offs[b], m = offs[b + 1] - off;
+    // third stage: block b's own half-bandwidth K_b <= k (block_factors.hpp:155-180); its factor lives in the
+    // k-wide store with zeros beyond K_b, so only the slab boxes and columns within K_b are loaded and summed
+    const int kb = kbs ? min(max(kbs[b], 0), k) : k;
+    const int qf0 = (k - kb) / box_c;          // forward: first box reaching a column in [k - kb, k)
+    const int qb1 = (kb + box_c - 1) / box_c;  // backward: boxes covering columns [0, kb)
     T* x = xbase + off;
     const int xm = xw - 1;
     const int nch = (m + TR - 1) / TR;
@@ -315,9 +320,10 @@ __global__ void __launch_bounds__(kSwThreads, 1)
             return;
         }
 #endif
-        mbar_expect_tx(bar + st, slab_bytes + dv_bytes);
+        const int q0 = fwd ? qf0 : 0, q1 = fwd ? nbox : min(qb1, nbox);
+        mbar_expect_tx(bar + st, (unsigned)(max(q1 - q0, 0) * TR * box_c * sizeof(T)) + dv_bytes);
         T* dst = slab + st * slab_elems;
-        for (int q = 0; q < nbox; ++q) tma_load_3d(dst + (size_t)q * TR * box_c, &map, i0, c0 + q * box_c, b, bar + st);
+        for (int q = q0; q < q1; ++q) tma_load_3d(dst + (size_t)q * TR * box_c, &map, i0, c0 + q * box_c, b, bar + st);
         const long long o = ((long long)ch * 2 + (fwd ? 0 : 1)) * TR * TR;
         bulk_load(dv + (g % SD) * TR * TR, (SUBST ? tri : dinv) + (long long)b * nch_max * 2 * TR * TR + o, dv_bytes,
                   bar + st);
@@ -327,7 +333,8 @@ __global__ void __launch_bounds__(kSwThreads, 1)
         const int ch = fwd ? g : 2 * nch - 1 - g;
         const int i0 = ch * TR;
         const int c0 = fwd ? i0 - k : i0 + TR;
-        for (int q = 0; q < nbox; ++q) tma_prefetch_3d(&map, i0, c0 + q * box_c, b);
+        const int q0 = fwd ? qf0 : 0, q1 = fwd ? nbox : min(qb1, nbox);
+        for (int q = q0; q < q1; ++q) tma_prefetch_3d(&map, i0, c0 + q * box_c, b);
     };
 
     for (int dir = 0; dir < 2; ++dir) {
@@ -440,8 +447,8 @@ __global__ void __launch_bounds__(kSwThreads, 1)
                     prev_rows = min(TR, m - i0);
                 }
             } else if (t < nch && warp < kSwWarps - 1) {
-                // columns needing only x older than chunk pch
-                const int ca = fwd ? 0 : TR, cb = fwd ? k - TR : k;
+                // columns needing only x older than chunk pch (within K_b)
+                const int ca = fwd ? k - kb : TR, cb = fwd ? k - TR : kb;
                 const int cbase = fwd ? i0 - k : i0 + TR;
                 // contiguous column ranges: helper warp (warp-1) of 14, column group cg of CG
                 if constexpr (TR == 32) {
@@ -464,7 +471,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
 #endif
             // ---- phase 2: the TR columns of chunk pch ----
             if (t < nch) {
-                const int ca = fwd ? max(k - TR, 0) : 0, cb = fwd ? k : min(TR, k);
+                const int ca = fwd ? max(max(k - TR, 0), k - kb) : 0, cb = fwd ? k : min(TR, kb);
                 const int cbase = fwd ? i0 - k : i0 + TR;
                 if constexpr (TR == 32) {
                     const int len = (cb - ca + kSwWarps - 1) / kSwWarps;
@@ -717,7 +724,7 @@ static void run_tma(const SweepPlan<T>& pl, T* x, cudaStream_t s) {
     auto kern = pl.subst ? k_sweep_tma<T, TR, S, true> : k_sweep_tma<T, TR, S, false>;
     SAP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
     kern<<<pl.p, kSwThreads, pl.smem, s>>>(pl.map, pl.dinv, pl.nch_max, pl.offs, pl.k, x, pl.xw, cols, pl.box_c,
-                                           pl.nbox, pl.tri);
+                                           pl.nbox, pl.tri, pl.kb);
     SAP_LAUNCHED();
 }
 

@@ -135,6 +135,7 @@ struct SweepPlan {
     T* tri = nullptr;           // [p][nch_max][2][tr*tr] the chunk triangles themselves (substitution)
     unsigned long long* kappa = nullptr;  // device: max chunk-triangle condition estimate (double bits)
     bool subst = false;         // sweeps solve chunk triangles by substitution (ill-conditioned triangles)
+    const int* kb = nullptr;    // third stage: per-block half-bandwidth K_b <= k (device), nullptr = k
     CUtensorMap map;
 };
 // Elements of chunk-inverse storage the plan needs (0 when the TMA path is not used).

@@ -1,13 +1,16 @@
-"""The two band LU implementations (sap_options::lu_kernel: 1 = one CTA per job, k_band_lu_res / the staged
-kernels; 2 = the dataflow kernel k_band_lu_df) give BITWISE equal factors, boost counts and
-reduced blocks (the dataflow kernel performs every element's operations in the same order), across the shapes
-the dispatch can route either way: odd K, unequal blocks, a host band (streamed upload), low dominance,
-K beyond the resident single-CTA kernel. The automatic choice (0) equals both."""
+"""The two band LU implementations (sap_options::lu_kernel: 1 = one CTA per job; 2 = the dataflow kernel
+k_band_lu_df) give BITWISE equal factors, boost counts and reduced blocks where the one-CTA
+kernel is k_band_lu_res (the dataflow kernel performs every element's operations in the same order), across the
+shapes the dispatch can route either way: odd K, unequal blocks, a host band (streamed upload), low dominance,
+and K = 300 beyond it. At K = 224 k_band_lu_res does not fit shared memory and the one-CTA kernel is the staged
+k_band_lu_seq, whose panel multiplies by a reciprocal (l = a (1/p)): there the two agree within the SURVEY 8c
+factor tolerance (1e-13 normwise), boost counts equal. The automatic choice (0) equals one of them."""
 import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
 
+BITWISE = {0, 1, 2, 3, 5}
 CASES = [  # n, k, d, p, coupled, host band
     (3000, 64, 1.0, 3, True, False),
     (20011, 77, 1.0, 7, True, False),
@@ -36,11 +39,19 @@ def _factors(sap, case, lu_kernel):
     return out
 
 
-@pytest.mark.parametrize("case", CASES)
-def test_dataflow_lu_is_bitwise_the_single_cta_lu(sap, case):
+@pytest.mark.parametrize("ci", range(len(CASES)))
+def test_dataflow_lu_is_bitwise_the_single_cta_lu(sap, ci):
+    case = CASES[ci]
     a, b, c = (_factors(sap, case, lk) for lk in (1, 2, 0))
+    if ci not in BITWISE:
+        for key in ("lu", "ul"):
+            if key in a:
+                den = np.max(np.abs(a[key][0]))
+                assert np.max(np.abs(a[key][0] - b[key][0])) <= 1e-13 * den and np.array_equal(a[key][1], b[key][1])
+        assert abs(a["it"] - b["it"]) <= 1.0
+        a = b  # the automatic choice is the dataflow kernel here
     for key in a:
-        for other in (b, c):
+        for other in ((b, c) if ci in BITWISE else (c,)):
             if key in ("lu", "ul"):
                 assert np.array_equal(a[key][0], other[key][0]) and np.array_equal(a[key][1], other[key][1]), key
             elif key == "rbar":
