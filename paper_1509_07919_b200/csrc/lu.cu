@@ -1677,13 +1677,29 @@ __device__ __forceinline__ void df_chain(const DfArgs& A, const FactorJob& J, in
         df_rows<B, false, NT>(P, pld, s_ut, s_rcp, nb, ph);
     __syncthreads();
     DF_MARK(3);
-    // the panel is final: L11\U11 and L21 to the store (the worker strips of this step read it from L2)
+    // the panel is final: L11\U11 and L21 to the store (the worker strips of this step read it from L2); row pairs
+    // (r, r + 1), r even, as one 16-byte store where both are in the band (alignment is uniform per column)
     const long long rs = L.rs;
+    const unsigned long long pol = l2_normal_policy();
     for (int c = warp; c < nb; c += NT / 32) {
         double* g = L.at(jb, jb + c);
-        const int r1 = min(ph, c + K + 1);
-#pragma unroll 4
-        for (int r = max(c - K, 0) + lane; r < r1; r += 32) st_normal(g + r * rs, P[c * pld + r]);
+        const int r0 = max(c - K, 0), r1 = min(ph, c + K + 1);
+        const bool al = (rs == 1 || rs == -1) && ((reinterpret_cast<uintptr_t>(rs > 0 ? g : g - 1) & 15) == 0);
+        const double* pc = P + c * pld;
+        for (int r = 2 * lane; r < r1; r += 64) {
+            const bool in0 = r >= r0, in1 = r + 1 >= r0 && r + 1 < r1;
+            const double2 v = *reinterpret_cast<const double2*>(pc + r);
+            if (in0 && in1 && al) {
+                const double2 w = rs > 0 ? v : make_double2(v.y, v.x);
+                asm volatile("st.global.cg.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(rs > 0 ? g + r : g - r - 1),
+                             "d"(w.x), "d"(w.y), "l"(pol) : "memory");
+            } else {
+                if (in0) asm volatile("st.global.cg.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(g + r * rs), "d"(v.x),
+                                      "l"(pol) : "memory");
+                if (in1) asm volatile("st.global.cg.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(g + (r + 1) * rs),
+                                      "d"(v.y), "l"(pol) : "memory");
+            }
+        }
     }
     // L2 prefetch of the band entries step s+1 meets first (rows [e, e + nbn) and columns [e, e + nbn))
     if (nbn > 0 && ja + R < m) {
