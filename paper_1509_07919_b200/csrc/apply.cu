@@ -168,8 +168,8 @@ __global__ void k_chunk_inverses(const T* __restrict__ f0, long long pstride, in
 
 // ---------------------------------------------------------------------------
 #ifdef SAP_SWEEP_TRACE
-__device__ long long g_sw_trace[16];
-void read_sweep_trace(long long* out) { SAP_CUDA(cudaMemcpyFromSymbol(out, g_sw_trace, sizeof(long long) * 16)); }
+__device__ long long g_sw_trace[24];
+void read_sweep_trace(long long* out) { SAP_CUDA(cudaMemcpyFromSymbol(out, g_sw_trace, sizeof(long long) * 18)); }
 #define SWT(var) long long var = clock64()
 #else
 #define SWT(var) do { } while (0)
@@ -501,8 +501,8 @@ __global__ void __launch_bounds__(kSwThreads, 1)
 #endif
         }
 #ifdef SAP_SWEEP_TRACE
-        if (blockIdx.x == 0 && fwd && (tid == 0 || tid == 32)) {
-            const int o = tid == 0 ? 0 : 6;
+        if (blockIdx.x == 0 && fwd && (tid == 0 || tid == 32 || tid == kSwThreads - 32)) {
+            const int o = tid == 0 ? 0 : tid == 32 ? 6 : 12;
             g_sw_trace[o + 0] = clock64() - t_loop0;
             g_sw_trace[o + 1] = acc_wait;
             g_sw_trace[o + 2] = acc_a;

@@ -14,13 +14,13 @@ int main() {
     sap_setup_banded(h, n, k, band.data(), 0);
     sap_apply_preconditioner(h, rhs.data(), out.data(), 0);
     sap_apply_preconditioner(h, rhs.data(), out.data(), 0);
-    long long t[16];
+    long long t[24];
     sapgpu::read_sweep_trace(t);
-    for (int w = 0; w < 2; ++w) {
+    for (int w = 0; w < 3; ++w) {
         const long long* r = t + 6 * w;
         const double c = (double)r[5];
-        printf("warp %d: %lld chunks, per chunk: total %.0f | mbar wait %.0f | barrier A %.0f | phase 1 %.0f | "
-               "phase 2 (+B) %.0f cycles\n", w, r[5], r[0] / c, r[1] / c, r[2] / c, r[3] / c, r[4] / c);
+        printf("%s: %lld chunks, per chunk: total %.0f | mbar wait %.0f | barrier A %.0f | phase 1 %.0f | "
+               "phase 2 (+B) %.0f cycles\n", w == 0 ? "warp 0 (finisher)" : w == 1 ? "warp 1 (helper)" : "warp 15 (producer)", r[5], r[0] / c, r[1] / c, r[2] / c, r[3] / c, r[4] / c);
     }
     sap_destroy(h);
 }
