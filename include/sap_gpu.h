@@ -98,7 +98,7 @@ typedef struct sap_options {
     int triangle_solve;
     /* Band LU kernel (not a reference option: two implementations of band_lu_inplace / band_ul_inplace with
      * bitwise-equal factors): 0 = automatic (the dataflow kernel for K in [192, 224] with at
-     * most 0.7 x SMs jobs and for K in (224, 512], else one CTA per job), 1 = one CTA per job,
+     * most 0.7 x SMs jobs of at least 512 rows and for K in (224, 512], else one CTA per job), 1 = one CTA per job,
      * 2 = the dataflow kernel wherever it supports the bandwidth (K in [64, 512]). Default 0. */
     int lu_kernel;
 } sap_options;

@@ -325,7 +325,7 @@ void launch_band_lu(const FactorJob* d_jobs, int njobs, int max_k, double boost_
     if (njobs <= 0) return;
     const bool df = lu_kernel == 1   ? false
                     : lu_kernel == 2 ? (max_k >= 64 && max_k <= 512)
-                                     : lu_df_applies(max_k, njobs);
+                                     : lu_df_applies(max_k, njobs, m_max);
     if (df_scratch && m_max > 0 && df) {
         launch_band_lu_df(d_jobs, njobs, m_max, max_k, boost_eps, s, streamed, df_scratch);
         return;

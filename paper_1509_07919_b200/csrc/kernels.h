@@ -29,7 +29,7 @@ void launch_copy_blocks(const double* band, int k, const int* d_offsets, int p, 
 void launch_band_lu(const FactorJob* d_jobs, int njobs, int max_k, double boost_eps, cudaStream_t s,
                     bool streamed = false, int m_max = 0, int* df_scratch = nullptr, int lu_kernel = 0);
 size_t lu_df_scratch_ints(int njobs, int m_max);
-bool lu_df_applies(int max_k, int njobs);
+bool lu_df_applies(int max_k, int njobs, int m_max);
 void launch_band_lu_df(const FactorJob* d_jobs, int njobs, int m_max, int max_k, double eps, cudaStream_t s,
                        bool streamed, int* scratch);
 // 1 if a dependency wait of the last k_band_lu_df launch on this scratch timed out (synchronous read);

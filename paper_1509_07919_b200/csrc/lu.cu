@@ -1886,13 +1886,14 @@ size_t lu_df_scratch_ints(int njobs, int m_max) {
 }
 
 // Where the dataflow kernel beats one CTA per job (profiles/lu_df_r02.txt): wide bands (enough strips per step
-// to spread) and no more jobs than ~0.7 x SMs (one chain CTA per job on the panel SMs, the rest for workers;
+// to spread), at least 16 steps per job, and no more jobs than ~0.7 x SMs (one chain CTA per job on the panel SMs, the rest for workers;
 // with more jobs the single-CTA kernel's per-flop efficiency wins)
-bool lu_df_applies(int max_k, int njobs) {
+bool lu_df_applies(int max_k, int njobs, int m_max) {
     int dev = 0, nsm = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (max_k > 224) return max_k <= 512;  // no resident single-CTA kernel beyond K = 224
-    return max_k >= kLuDfMinK && 10 * njobs <= 7 * nsm;
+    // short jobs (e.g. the reduced blocks, m = w: 7 steps) do not amortize the items' latency
+    return max_k >= kLuDfMinK && 10 * njobs <= 7 * nsm && m_max >= 16 * 32;
 }
 
 void launch_band_lu_df(const FactorJob* d_jobs, int njobs, int m_max, int max_k, double eps, cudaStream_t s,
