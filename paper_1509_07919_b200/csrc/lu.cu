@@ -1251,9 +1251,11 @@ __device__ __forceinline__ double df_ld(const Lu& L, int i, int c, bool fresh) {
 }
 
 // trace mark (tools/lu_df_trace.py): per-CTA slot `k` of the current item
-#define DF_MARK(k)                                                                      \
-    do {                                                                                \
-        if (A.trace && threadIdx.x == 0) A.trace[8 * (size_t)blockIdx.x + (k)] = df_now(); \
+// marks go to shared memory (one global record per item at its end: tracing must not perturb the item)
+__shared__ unsigned long long g_df_smark[8];
+#define DF_MARK(k)                                                   \
+    do {                                                             \
+        if (A.trace && threadIdx.x == 0) g_df_smark[k] = clock64(); \
     } while (0)
 
 // Lean staging of a 32-column panel-shaped region: rows [0, nr) of view columns cb + [0, 32) starting at view
@@ -1627,7 +1629,7 @@ __device__ __forceinline__ void df_chain(const DfArgs& A, const FactorJob& J, in
         if (sp > 0 && B < rprevp) df_wait(A.col_step + (size_t)jid * A.S + s, sp, A.err, A.panel_cnt, 2);
         df_acquire();
         *s_boosts = 0;
-        if (A.trace) A.trace[8 * (size_t)blockIdx.x + 0] = df_now();
+        if (A.trace) g_df_smark[0] = clock64();
     }
     __syncthreads();
     if (s > 0) {
@@ -1748,7 +1750,7 @@ __device__ __forceinline__ void df_worker(const DfArgs& A, const FactorJob& J, i
             if (s > 0 && 32 * (j + 1) < rprev)
                 df_wait(A.col_step + (size_t)jid * A.S + s + 1 + j, s, A.err, A.panel_cnt, 4);
         df_acquire();
-        if (A.trace) A.trace[8 * (size_t)blockIdx.x + 0] = df_now();
+        if (A.trace) g_df_smark[0] = clock64();
     }
     __syncthreads();
     df_stage_panel<NT>(L, P, pld, jb, jb, ph, B, ph);
@@ -1834,7 +1836,8 @@ __global__ void __launch_bounds__(NT, DfCfg<NT>::MINB) k_band_lu_df(DfArgs A) {
         unsigned long long t_grab = 0;
         if (A.trace && tid == 0) {
             t_grab = df_now();
-            for (int q = 0; q < 5; ++q) A.trace[8 * (size_t)blockIdx.x + q] = 0;
+            for (int q = 0; q < 5; ++q) g_df_smark[q] = 0;
+            g_df_smark[5] = clock64();
         }
         long long rec;
         if (panel_role) {
@@ -1862,11 +1865,15 @@ __global__ void __launch_bounds__(NT, DfCfg<NT>::MINB) k_band_lu_df(DfArgs A) {
         }
         __syncthreads();
         if (A.trace && tid == 0) {
-            unsigned long long* tr = A.trace + 8 * ((size_t)gridDim.x + rec);
+            // record (10 u64): grab / end (globaltimer ns), grab / ready / marks 1-4 / end (clock64), SM << 32 | CTA
+            const unsigned long long c_end = clock64();
+            unsigned long long* tr = A.trace + 10 * ((size_t)gridDim.x + rec);
             tr[0] = t_grab;
-            for (int q = 0; q < 5; ++q) tr[1 + q] = A.trace[8 * (size_t)blockIdx.x + q];
-            tr[6] = df_now();
-            tr[7] = ((unsigned long long)smid << 32) | blockIdx.x;
+            tr[1] = df_now();
+            tr[2] = g_df_smark[5];
+            for (int q = 0; q < 5; ++q) tr[3 + q] = g_df_smark[q];
+            tr[8] = c_end;
+            tr[9] = ((unsigned long long)smid << 32) | blockIdx.x;
         }
     }
 }
@@ -1945,7 +1952,7 @@ void launch_band_lu_df(const FactorJob* d_jobs, int njobs, int m_max, int max_k,
     int nps = A.excl ? std::min(njobs, cap) : std::min((njobs + per_sm - 1) / std::max(per_sm, 1), cap);
     A.nps = std::max(1, std::min(nps, nsm - 1));
     if (g_df_trace_mode && (g_df_trace_mode == 1) == streamed) {  // tools/lu_df_trace.py
-        const size_t need = 8 * (size_t)(grid + items);
+        const size_t need = 10 * (size_t)(grid + items);
         if (g_df_trace_cap < need) {
             if (g_df_trace) cudaFree(g_df_trace);
             SAP_CUDA(cudaMalloc(&g_df_trace, need * sizeof(unsigned long long)));
@@ -1982,8 +1989,8 @@ bool band_lu_reads_source(int max_k) {
 
 }  // namespace sapgpu
 
-// tools/lu_df_trace.py only (not in include/sap_gpu.h): the last traced k_band_lu_df launch, 8 u64 per item
-// (grab, dependencies met, phase marks 1-4, end: globaltimer ns; SM << 32 | CTA). Returns the item count.
+// tools/lu_df_trace.py only (not in include/sap_gpu.h): the last traced k_band_lu_df launch, 10 u64 per item
+// (grab, end: globaltimer ns; grab, dependencies met, phase marks 1-4, end: clock64; SM << 32 | CTA).
 extern "C" void sap_dev_lu_df_trace_mode(int mode) { sapgpu::g_df_trace_mode = mode; }
 
 extern "C" long long sap_dev_lu_df_trace(unsigned long long* out, long long cap) {
@@ -1991,7 +1998,7 @@ extern "C" long long sap_dev_lu_df_trace(unsigned long long* out, long long cap)
     if (!g_df_trace) return 0;
     const long long n = std::min<long long>(cap, g_df_trace_items);
     cudaDeviceSynchronize();
-    cudaMemcpy(out, g_df_trace + 8 * (size_t)g_df_trace_grid, sizeof(unsigned long long) * 8 * n,
+    cudaMemcpy(out, g_df_trace + 10 * (size_t)g_df_trace_grid, sizeof(unsigned long long) * 10 * n,
                cudaMemcpyDeviceToHost);
     return n;
 }

@@ -11,12 +11,12 @@ timeout 600 python bench.py > $O/${TAG}_bench_C.json 2> $O/${TAG}_bench_C.err
 timeout 600 python bench.py --precond D --no-cpu-baseline > $O/${TAG}_bench_D.json 2> $O/${TAG}_bench_D.err
 if [ "${SKIP_NCU:-0}" != "1" ]; then
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/${TAG}_launches_C.csv \
-   python bench.py --steps 1 --warmup 1 --no-cpu-baseline > $O/${TAG}_ncu_launch.log 2>&1
+   python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-config5 > $O/${TAG}_ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_band_lu_(res|df)' -s 0 -c 1 \
-   -o $O/${TAG}_lu python bench.py --steps 1 --warmup 1 --no-cpu-baseline > $O/${TAG}_ncu_lu.log 2>&1
+   -o $O/${TAG}_lu python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-config5 > $O/${TAG}_ncu_lu.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_sweep' -s 0 -c 1 \
-   -o $O/${TAG}_sweep python bench.py --steps 1 --warmup 1 --no-cpu-baseline > $O/${TAG}_ncu_sweep.log 2>&1
+   -o $O/${TAG}_sweep python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-config5 > $O/${TAG}_ncu_sweep.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_band_spmv' -s 2 -c 1 \
-   -o $O/${TAG}_spmv python bench.py --steps 1 --warmup 1 --no-cpu-baseline > $O/${TAG}_ncu_spmv.log 2>&1
+   -o $O/${TAG}_spmv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-config5 > $O/${TAG}_ncu_spmv.log 2>&1
 fi
 echo done

@@ -46,23 +46,25 @@ def main():
     lib = _lib.load()
     lib.sap_dev_lu_df_trace.restype = C.c_longlong
     cap = 2_000_000
-    buf = np.zeros(8 * cap, np.uint64)
+    buf = np.zeros(10 * cap, np.uint64)
     cnt = lib.sap_dev_lu_df_trace(buf.ctypes.data_as(C.POINTER(C.c_ulonglong)), cap)
-    t = buf[: 8 * cnt].reshape(cnt, 8).astype(np.int64)
+    t = buf[: 10 * cnt].reshape(cnt, 10).astype(np.int64)
     os.makedirs("gpurun_out", exist_ok=True)
     np.save(f"gpurun_out/dftrace_{kind}.npy", t)
     J = 2 * p if kind == "C" else p
     m_max = -(-n // p)
-    valid = t[:, 6] > 0
+    valid = t[:, 1] > 0
+    GHZ = 1.965  # clock64 -> ns
     t0 = t[valid, 0].min()
-    grab, ready, end = t[:, 0] - t0, t[:, 1] - t0, t[:, 6] - t0
+    grab, end = t[:, 0] - t0, t[:, 1] - t0
+    ready = grab + (t[:, 3] - t[:, 2]) / GHZ  # dependencies met, from the SM clock
     print(f"items {cnt}, traced {valid.sum()}, span {(end[valid].max())/1e3:.1f} us")
     types = {}
     for i in range(cnt):
         if not valid[i]:
             continue
         ty, job, st, j = decode(i, J, k, m_max)
-        skipped = t[i, 1] == 0
+        skipped = t[i, 3] == 0
         d = types.setdefault(ty, [0, 0.0, 0.0, 0, np.zeros(5)])
         d[0] += 1
         if skipped:
@@ -70,17 +72,17 @@ def main():
             continue
         d[1] += (ready[i] - grab[i]) / 1e3
         d[2] += (end[i] - ready[i]) / 1e3
-        marks = [t[i, 1]] + [t[i, 2 + q] if t[i, 2 + q] > 0 else t[i, 1] for q in range(4)] + [t[i, 6]]
-        d[4] += np.diff(marks) / 1e3
+        marks = [t[i, 3]] + [t[i, 4 + q] if t[i, 4 + q] > 0 else t[i, 3] for q in range(4)] + [t[i, 8]]
+        d[4] += np.diff(marks) / GHZ / 1e3
     for ty, (c, wsum, ksum, sk, ph) in types.items():
         c2 = max(c - sk, 1)
         print(f"{ty:7s} n={c:6d} skipped={sk:5d} wait avg {wsum / c2:7.2f} us  work avg {ksum / c2:7.2f} us  "
               f"total work {ksum/1e3:.2f} ms; phases (us) " + " ".join(f"{x / c2:.2f}" for x in ph))
     # per CTA: busy (work) vs waiting vs idle
-    ncta = int((t[valid, 7] & 0xffffffff).max()) + 1
+    ncta = int((t[valid, 9] & 0xffffffff).max()) + 1
     span = end[valid].max()
-    work = sum((end[i] - ready[i]) for i in range(cnt) if valid[i] and t[i, 1] > 0)
-    wait = sum((ready[i] - grab[i]) for i in range(cnt) if valid[i] and t[i, 1] > 0)
+    work = sum((end[i] - ready[i]) for i in range(cnt) if valid[i] and t[i, 3] > 0)
+    wait = sum((ready[i] - grab[i]) for i in range(cnt) if valid[i] and t[i, 3] > 0)
     print(f"CTAs {ncta}: work {work / (ncta * span):.2%}, dependency wait {wait / (ncta * span):.2%} of CTA-time")
     # critical path sample: job 0's panels
     ps = sorted((decode(i, J, k, m_max)[2], ready[i], end[i]) for i in range(cnt)
