@@ -1161,6 +1161,10 @@ struct DfArgs {
     int excl;             // 1: one chain CTA per panel SM (its other CTAs exit); the chain's update on DMMA
     int* sm_role;         // [kDfMaxSm]: 0 undecided, 1 panel, 2 worker, 3 being decided
     int* n_panel_sm;      // SMs claimed so far
+    int* n_chain;         // chain CTAs so far (a chain CTA's rank)
+    int* started;         // CTAs past their role claim
+    int* mode;            // chain schedule: 0 undecided, 1 job owners, 2 shared s-major queue
+    int owners_ok;        // 0: always the queue (tools/lu_df_check.py A/B)
     int* panel_cnt;  // [njobs]
     int* col_step;   // [njobs][S]
     int* boost_acc;  // [njobs]
@@ -1607,7 +1611,7 @@ __device__ __noinline__ void df_rows(double* __restrict__ P, int pld, const doub
 template <int NT, bool STREAM>
 __device__ __forceinline__ void df_chain(const DfArgs& A, const FactorJob& J, int jid, int s, double* __restrict__ P,
                                          double* __restrict__ U, double* __restrict__ s_ut,
-                                         double* __restrict__ s_rcp, int* s_boosts) {
+                                         double* __restrict__ s_rcp, int* s_boosts, bool have_panel) {
     constexpr int B = 32;
     const int m = J.m, K = J.k;
     if (s * B >= m) return;
@@ -1633,7 +1637,8 @@ __device__ __forceinline__ void df_chain(const DfArgs& A, const FactorJob& J, in
     }
     __syncthreads();
     if (s > 0) {
-        df_stage_panel<NT>(L, P, pld, jbp, jbp, B + rprev, B, B + rprev);
+        // panel s-1: still in shared memory when this CTA factored it (job owner), else from L2
+        if (!have_panel) df_stage_panel<NT>(L, P, pld, jbp, jbp, B + rprev, B, B + rprev);
         df_a12<NT>(L, jbp, jb, 0, 32, T.wc, T.fr, sp == 0, U, uld);
         // this panel's rows that no earlier step updated (<= 32 of them): loaded now, written after the update
         constexpr int NF = 1024 / NT;
@@ -1794,7 +1799,7 @@ __global__ void __launch_bounds__(NT, DfCfg<NT>::MINB) k_band_lu_df(DfArgs A) {
     asm("mov.u32 %0, %%smid;" : "=r"(smid));
     // SM role: the first nps SMs on which CTAs of this launch actually start become panel SMs (placement and
     // %smid numbering are not under our control; every CTA of an SM shares its SM's role)
-    __shared__ int s_role;
+    __shared__ int s_role, s_rank, s_mode;
     if (tid == 0) {
         int* rp = A.sm_role + (smid % kDfMaxSm);
         int r = atomicCAS(rp, 0, 3);
@@ -1809,6 +1814,9 @@ __global__ void __launch_bounds__(NT, DfCfg<NT>::MINB) k_band_lu_df(DfArgs A) {
             if (r == 1 && A.excl) r = 0;  // exclusive panel SM: only its deciding CTA stays
         }
         s_role = r;
+        s_rank = r == 1 ? atomicAdd(A.n_chain, 1) : -1;
+        __threadfence();
+        atomicAdd(A.started, 1);
     }
     __syncthreads();
     if (s_role == 0) {
@@ -1819,6 +1827,54 @@ __global__ void __launch_bounds__(NT, DfCfg<NT>::MINB) k_band_lu_df(DfArgs A) {
         return;
     }
     const bool panel_role = s_role == 1;
+    if (panel_role) {
+        // Job owners when every CTA of the launch is resident and there is a chain CTA per job: chain CTA r runs
+        // chain(r, 0), chain(r, 1), ... and keeps each panel in shared memory for the next step. Deadlock-free like
+        // the queue (each job's items run in order on a resident CTA; the workers' queue is unchanged). Otherwise
+        // (a CTA still waiting for a slot after 20 us, or fewer chain CTAs than jobs) the shared queue.
+        if (tid == 0) {
+            int md = ld_relaxed_i(A.mode);
+            if (md == 0) {
+                const unsigned long long t0 = df_now();
+                while (ld_relaxed_i(A.started) < (int)gridDim.x && df_now() - t0 < 20000) __nanosleep(64);
+                const int want = A.owners_ok && ld_relaxed_i(A.started) == (int)gridDim.x &&
+                                         ld_relaxed_i(A.n_chain) >= J
+                                     ? 1
+                                     : 2;
+                md = atomicCAS(A.mode, 0, want);
+                if (md == 0) md = want;
+            }
+            s_mode = md;
+        }
+        __syncthreads();
+        if (s_mode == 1) {
+            const int jid = s_rank;
+            if (jid >= J) return;
+            const FactorJob Jb = A.jobs[jid];
+            for (int s = 0; s < A.S && s * 32 < Jb.m; ++s) {
+                unsigned long long t_grab = 0;
+                if (A.trace && tid == 0) {
+                    t_grab = df_now();
+                    for (int q = 0; q < 5; ++q) g_df_smark[q] = 0;
+                    g_df_smark[5] = clock64();
+                }
+                df_chain<NT, STREAM>(A, Jb, jid, s, P, U, s_ut, s_rcp, &s_boosts, s > 0);
+                __syncthreads();
+                if (A.trace && tid == 0) {
+                    const unsigned long long c_end = clock64();
+                    unsigned long long* tr = A.trace + 10 * ((size_t)gridDim.x + (size_t)s * J + jid);
+                    tr[0] = t_grab;
+                    tr[1] = df_now();
+                    tr[2] = g_df_smark[5];
+                    for (int q = 0; q < 5; ++q) tr[3 + q] = g_df_smark[q];
+                    tr[8] = c_end;
+                    tr[9] = ((unsigned long long)smid << 32) | blockIdx.x;
+                }
+            }
+            if (tid == 0) atomicAdd(A.counter_p, (unsigned)A.S);  // releases the exclusive SMs' spare CTAs
+            return;
+        }
+    }
     unsigned* ctr = panel_role ? A.counter_p : A.counter_w;
     if (tid == 0) s_item = (int)atomicAdd(ctr, 1u);
     __syncthreads();
@@ -1844,7 +1900,7 @@ __global__ void __launch_bounds__(NT, DfCfg<NT>::MINB) k_band_lu_df(DfArgs A) {
             if (item >= A.S * J) break;
             const int s = item / J, jid = item - s * J;
             const FactorJob Jb = A.jobs[jid];
-            df_chain<NT, STREAM>(A, Jb, jid, s, P, U, s_ut, s_rcp, &s_boosts);
+            df_chain<NT, STREAM>(A, Jb, jid, s, P, U, s_ut, s_rcp, &s_boosts, false);
             rec = item;
         } else {
             bool done = false;
@@ -1878,13 +1934,15 @@ __global__ void __launch_bounds__(NT, DfCfg<NT>::MINB) k_band_lu_df(DfArgs A) {
     }
 }
 
+static int g_df_owners = 1;      // sap_dev_lu_df_owners
 static int g_df_trace_mode = 0;  // sap_dev_lu_df_trace_mode: 1 trace streamed launches, 2 the others
 static unsigned long long* g_df_trace = nullptr;
 static size_t g_df_trace_cap = 0;
 static long long g_df_trace_items = 0;
 static int g_df_trace_grid = 0;
 
-// scratch: [1..7] timeout report, [8] chain counter, [10] worker counter, [12] panel SMs claimed,
+// scratch: [1..7] timeout report, [8] chain counter, [10] worker counter, [12] panel SMs claimed, [13] chain CTAs,
+// [14] CTAs started, [15] chain schedule,
 // [16, 16 + kDfMaxSm) SM roles, then panel_cnt[njobs], boost_acc[njobs], col_step[njobs][S]
 constexpr int kDfHdr = 16 + kDfMaxSm;
 size_t lu_df_scratch_ints(int njobs, int m_max) {
@@ -1919,6 +1977,10 @@ void launch_band_lu_df(const FactorJob* d_jobs, int njobs, int m_max, int max_k,
     A.counter_w = reinterpret_cast<unsigned*>(scratch + 10);
     A.err = scratch + 1;
     A.n_panel_sm = scratch + 12;
+    A.n_chain = scratch + 13;
+    A.started = scratch + 14;
+    A.mode = scratch + 15;
+    A.owners_ok = g_df_owners;
     A.sm_role = scratch + 16;
     A.panel_cnt = scratch + kDfHdr;
     A.boost_acc = scratch + kDfHdr + njobs;
@@ -1992,6 +2054,8 @@ bool band_lu_reads_source(int max_k) {
 // tools/lu_df_trace.py only (not in include/sap_gpu.h): the last traced k_band_lu_df launch, 10 u64 per item
 // (grab, end: globaltimer ns; grab, dependencies met, phase marks 1-4, end: clock64; SM << 32 | CTA).
 extern "C" void sap_dev_lu_df_trace_mode(int mode) { sapgpu::g_df_trace_mode = mode; }
+// tools only: 0 keeps the dataflow LU's chain items on the shared queue (no job owners), 1 the default
+extern "C" void sap_dev_lu_df_owners(int on) { sapgpu::g_df_owners = on; }
 
 extern "C" long long sap_dev_lu_df_trace(unsigned long long* out, long long cap) {
     using namespace sapgpu;

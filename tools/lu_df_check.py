@@ -2,6 +2,7 @@
 factors (LU, UL), boost counts and reduced blocks must be BITWISE equal; prints the factor-kernel times.
 
     python tools/lu_df_check.py            # on a GPU box
+    python tools/lu_df_check.py owners     # the dataflow kernel without / with job-owner chains
 """
 import os
 import sys
@@ -31,8 +32,9 @@ CASES = [
 ]
 
 
-def run(case, df):
+def run(case, df, owners=1):
     n, k, d, p, kind, dev = case
+    S._lib.load().sap_dev_lu_df_owners(owners)
     band, rhs = S.random_banded(n, k, d, 1)
     src = torch.from_numpy(band).cuda() if dev else band
     out = {}
@@ -61,6 +63,9 @@ def main():
         a = run(case, False)
         if len(sys.argv) > 1 and sys.argv[1] == "old2":
             b = run(case, False)
+        elif len(sys.argv) > 1 and sys.argv[1] == "owners":  # dataflow: shared chain queue vs job owners (bitwise)
+            a = run(case, True, 0)
+            b = run(case, True, 1)
         else:
             b = run(case, True)
         same = np.array_equal(a["lu"][0], b["lu"][0]) and np.array_equal(a["lu"][1], b["lu"][1])
@@ -91,7 +96,7 @@ def main():
                               f"ncols {len(bad_cols)} values {x[c][sl]} vs {y[c][sl]}")
                         break
         # not bitwise (the chain's strip 0 is on DFMA): the SURVEY 8c tolerances against the single-CTA kernel
-        tol = 1e-13 if case[2] >= 0.5 else 1e-6
+        tol = 0.0 if len(sys.argv) > 1 and sys.argv[1] == "owners" else 1e-13 if case[2] >= 0.5 else 1e-6
         rel = max(np.max(np.abs(a[nm][0] - b[nm][0])) / np.max(np.abs(a[nm][0])) for nm in ("lu", "ul") if nm in a)
         ok = rel <= tol and np.array_equal(a["lu"][1], b["lu"][1]) and abs(a["it"] - b["it"]) <= 1
         same = ok
