@@ -508,6 +508,10 @@ __global__ void __launch_bounds__(kLuThreads, 1)
 // groups of 4: the SURVEY §8c tolerances). The A22 tiles round-trip through L2 with an evict_last policy.
 // Shared-memory pair load kept in program order (volatile): stops the compiler from hoisting a whole
 // unrolled panel's operand loads to the top (register spills).
+__device__ __forceinline__ void sts1(double* p, double v) {
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
 __device__ __forceinline__ double2 lds2(const double* p) {
     double2 v;
     const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -533,9 +537,88 @@ __device__ __forceinline__ double rcp2(double p) {
     return fma(r, e, r);
 }
 
+// Pivot c of panel_diag (lane = row r, a[j] = the row's entry in column j; every index a compile-time
+// constant). Stores go through explicit st.shared / ld.shared (a generic store to P here cost ~11%).
+template <int c>
+__device__ __forceinline__ void pd_pivot(double (&a)[32], int nb, bool full, int r, bool own, double bv, double& pl,
+                                         double& rl, int& boosts, double* __restrict__ P, int pld,
+                                         double* __restrict__ Ut, double* __restrict__ s_piv) {
+    constexpr int B = 32;
+    // pivot row c, published by its owner at the end of the previous round: the pair holding entry c + 1 (the
+    // next pivot column) first
+    const double* __restrict__ urow = Ut + ut_off(c) - ut_lo(c);  // urow[j] = U(c, j), j >= ut_lo(c)
+    double2 un2 = make_double2(0.0, 0.0);
+    if constexpr (c + 1 < B) un2 = lds2(urow + ((c + 1) & ~1));
+    const double pc = __shfl_sync(0xffffffffu, pl, c);
+    const double rc = __shfl_sync(0xffffffffu, rl, c);
+    if (r == c) {
+        s_piv[c] = pc;
+        s_piv[B + c] = rc;
+    }
+    // rows below: multiplier (block_factors.hpp:36) and rank-1 update; other lanes apply l = 0 (rows above
+    // stay as they are for finite pivot rows, the only kind a finite band produces)
+    const bool below = own && r > c;
+    const double lq = div_rcp(a[c], pc, rc);
+    const double l = below ? lq : 0.0;
+    a[c] = below ? lq : a[c];
+    if (own) sts1(P + c * pld + r, a[c]);  // column c of L11\U11 is final
+    if constexpr (c + 1 < B) {
+        // the next pivot column first, so its reciprocal overlaps the rest of the row update
+        if constexpr (c & 1) {  // pair (c + 1, c + 2)
+            a[c + 1] = fma(-l, un2.x, a[c + 1]);
+            if constexpr (c + 2 < B) a[c + 2] = fma(-l, un2.y, a[c + 2]);
+        } else {  // pair (c, c + 1)
+            a[c + 1] = fma(-l, un2.y, a[c + 1]);
+        }
+        if (full || c + 1 < nb) {  // boost rule block_factors.hpp:26-34; every lane inverts its own entry
+            double p = a[c + 1];
+            const bool boost = fabs(p) < bv;
+            p = boost ? (p < 0.0 ? -bv : bv) : p;
+            boosts += (boost && r == c + 1) ? 1 : 0;
+            if (r == c + 1) a[c + 1] = p;
+            pl = p;
+            rl = rcp2(p);
+        }
+    }
+    // the remaining pairs (aligned)
+#pragma unroll
+    for (int j = (c & 1) ? c + 3 : c + 2; j < B; j += 2) {
+        const double2 u = lds2(urow + j);
+        a[j] = fma(-l, u.x, a[j]);
+        a[j + 1] = fma(-l, u.y, a[j + 1]);
+    }
+    // row c + 1 is final now: its owner publishes it for the next round
+    if constexpr (c + 1 < B) {
+        if (r == c + 1) {
+#pragma unroll
+            for (int j = ut_lo(c + 1); j < B; j += 2)
+                *reinterpret_cast<double2*>(Ut + ut_off(c + 1) + j - ut_lo(c + 1)) = make_double2(a[j], a[j + 1]);
+        }
+    }
+    __syncwarp();
+}
+
+template <int c, bool FULL>
+__device__ __forceinline__ void pd_all(double (&a)[32], int nb, int r, bool own, double bv, double& pl, double& rl,
+                                       int& boosts, double* __restrict__ P, int pld, double* __restrict__ Ut,
+                                       double* __restrict__ s_piv, unsigned long long* marks) {
+    if constexpr (c % 4 == 0) {
+        if (marks && r == 0) marks[c >> 2] = clock64();  // tools/lu_df_trace.py: 4-pivot groups
+    }
+    if (FULL || c < nb) pd_pivot<c>(a, nb, FULL, r, own, bv, pl, rl, boosts, P, pld, Ut, s_piv);
+    if constexpr (c + 1 < 32) pd_all<c + 1, FULL>(a, nb, r, own, bv, pl, rl, boosts, P, pld, Ut, s_piv, marks);
+}
+
+// The nb x nb diagonal block's pivot chain in one warp (lane = row), fully unrolled (rolled 2- / 4-pivot loops
+// with a register shift measured 1.9x / 1.8x slower, tools/probe/diag_throttle.cu). Every element gets the
+// same FMAs in the same order as a column-by-column right-looking elimination; the published U rows (Ut,
+// packed) and the pivots / reciprocals (s_piv) feed the L21 rows. The calling warp must be converged (see
+// df_wait).
 template <int B, bool FULL>
 __device__ __noinline__ void panel_diag(double* __restrict__ P, int pld, double* __restrict__ Ut,
-                                        double* __restrict__ s_piv, int nb_rt, double bv, int* boost_ctr) {
+                                        double* __restrict__ s_piv, int nb_rt, double bv, int* boost_ctr,
+                                        unsigned long long* marks = nullptr) {
+    static_assert(B == 32, "panel_diag: 32-column panels");
     const int nb = FULL ? B : nb_rt;
     const int r = threadIdx.x & 31;
     const bool own = r < nb;
@@ -549,73 +632,19 @@ __device__ __noinline__ void panel_diag(double* __restrict__ P, int pld, double*
             *reinterpret_cast<double2*>(Ut + ut_off(0) + j - ut_lo(0)) = make_double2(a[j], a[j + 1]);
     }
     int boosts = 0;
-    // every lane boosts / inverts its own entry of the next pivot column (branch-free); only the owner's
-    // (lane c) is used (boost rule block_factors.hpp:26-34)
-    auto prep = [&](int c, double& p, double& rcl) {
-        p = a[c];
+    double pl, rl;
+    {
+        double p = a[0];
         const bool boost = fabs(p) < bv;
         p = boost ? (p < 0.0 ? -bv : bv) : p;
-        boosts += (boost && r == c) ? 1 : 0;
-        if (r == c) a[c] = p;
-        rcl = rcp2(p);
-    };
-    double pl, rl;
-    prep(0, pl, rl);
-    __syncwarp();
-#pragma unroll
-    for (int c = 0; c < B; ++c) {
-        if (FULL || c < nb) {
-            // pivot row c, published by its owner at the end of the previous round: the pair holding entry
-            // c + 1 (the next pivot column) first
-            const double* __restrict__ urow = Ut + ut_off(c) - ut_lo(c);  // urow[j] = U(c, j), j >= ut_lo(c)
-            const double2 un2 = c + 1 < B ? lds2(urow + ((c + 1) & ~1)) : make_double2(0.0, 0.0);
-            const double pc = __shfl_sync(0xffffffffu, pl, c);
-            const double rc = __shfl_sync(0xffffffffu, rl, c);
-            if (r == c) {
-                s_piv[c] = pc;
-                s_piv[B + c] = rc;
-            }
-            // rows below: multiplier (block_factors.hpp:36) and rank-1 update; other lanes apply l = 0 (rows
-            // above stay as they are for finite pivot rows, the only kind a finite band produces)
-            const bool below = own && r > c;
-            const double lq = div_rcp(a[c], pc, rc);
-            const double l = below ? lq : 0.0;
-            a[c] = below ? lq : a[c];
-            if (own) P[c * pld + r] = a[c];  // column c of L11\U11 is final
-            if (c + 1 < B) {
-                // the next pivot column first, so its reciprocal overlaps the rest of the row update
-                if (c & 1) {  // pair (c + 1, c + 2)
-                    a[c + 1] = fma(-l, un2.x, a[c + 1]);
-                    if (c + 2 < B) a[c + 2] = fma(-l, un2.y, a[c + 2]);
-                } else {  // pair (c, c + 1)
-                    a[c + 1] = fma(-l, un2.y, a[c + 1]);
-                }
-                if (FULL || c + 1 < nb) prep(c + 1, pl, rl);
-            }
-            // the remaining pairs, four at a time (bounded register footprint)
-            constexpr int kChunk = 8;
-#pragma unroll
-            for (int j0 = (c & 1) ? c + 3 : c + 2; j0 < B; j0 += kChunk) {
-                double2 uu[kChunk / 2];
-#pragma unroll
-                for (int q = 0; q < kChunk / 2; ++q)
-                    if (j0 + 2 * q < B) uu[q] = lds2(urow + j0 + 2 * q);
-#pragma unroll
-                for (int q = 0; q < kChunk / 2; ++q)
-                    if (j0 + 2 * q < B) {
-                        a[j0 + 2 * q] = fma(-l, uu[q].x, a[j0 + 2 * q]);
-                        a[j0 + 2 * q + 1] = fma(-l, uu[q].y, a[j0 + 2 * q + 1]);
-                    }
-            }
-            // row c + 1 is final now: its owner publishes it for the next round
-            if (c + 1 < B && r == c + 1) {
-#pragma unroll
-                for (int j = ut_lo(c + 1); j < B; j += 2)
-                    *reinterpret_cast<double2*>(Ut + ut_off(c + 1) + j - ut_lo(c + 1)) = make_double2(a[j], a[j + 1]);
-            }
-            __syncwarp();
-        }
+        boosts += (boost && r == 0) ? 1 : 0;
+        if (r == 0) a[0] = p;
+        pl = p;
+        rl = rcp2(p);
     }
+    __syncwarp();
+    pd_all<0, FULL>(a, nb, r, own, bv, pl, rl, boosts, P, pld, Ut, s_piv, marks);
+    if (marks && r == 0) marks[8] = clock64();
     if (boosts) atomicAdd(boost_ctr, boosts);
 }
 
@@ -957,22 +986,24 @@ __global__ void __launch_bounds__(kLuThreads, 1)
         const long long want = min(m, need + 1);
         const long long have = (long long)s_got * J.piece;
         if (have >= want || have * J.ends >= m || s_timeout) return;
-        if (tid == 0) {
-            const long long t0 = clock64();
+        if (tid < 32) {  // warp-uniform spin (df_wait: a lane-0 spin leaves the pivot warp diverged)
+            const long long t0 = __shfl_sync(0xffffffffu, clock64(), 0);
             for (;;) {
                 unsigned r;
                 asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(J.ready) : "memory");
+                r = __shfl_sync(0xffffffffu, r, 0);
                 const long long got = (long long)r * J.piece;
                 if (got >= want || got * J.ends >= m) {
-                    s_got = r;
+                    if (tid == 0) s_got = r;
                     break;
                 }
-                if (clock64() - t0 > (1LL << 36)) {  // ~35 s: the upload stalled; give up (reported)
-                    s_timeout = 1;
+                if (__shfl_sync(0xffffffffu, clock64(), 0) - t0 > (1LL << 36)) {  // ~35 s: the upload stalled
+                    if (tid == 0) s_timeout = 1;
                     break;
                 }
                 __nanosleep(256);
             }
+            __syncwarp();
         }
         __syncthreads();
     };
@@ -1210,13 +1241,18 @@ __device__ __forceinline__ void df_acquire() { asm volatile("fence.acq_rel.gpu;"
 
 // thread 0: spin (relaxed loads) until *flag >= want (~4 s cap: a lost dependency is reported, never a hang;
 // err[0] = 1, err[1..6] = the first timed-out wait: CTA, SM, the flag's word offset, want, have, tag)
+// Called by all 32 lanes of one warp: the spin is warp-uniform (lane 0's value decides). A lane-0-only spin
+// with __nanosleep left the warp diverged: the pivot chain it ran next took ~3.3x as long (every chain item that
+// had waited, profiles/lu_df_r02.txt).
+__device__ __forceinline__ int ld_relaxed_w(const int* p) { return __shfl_sync(0xffffffffu, ld_relaxed_i(p), 0); }
+
 __device__ __forceinline__ void df_wait(const int* flag, int want, int* err, const int* base, int tag) {
-    if (ld_relaxed_i(flag) >= want) return;
-    const long long t0 = clock64();
-    while (ld_relaxed_i(flag) < want) {
+    if (ld_relaxed_w(flag) >= want) return;
+    const long long t0 = __shfl_sync(0xffffffffu, clock64(), 0);
+    while (ld_relaxed_w(flag) < want) {
         __nanosleep(100);
-        if (clock64() - t0 > (1LL << 33)) {
-            if (atomicExch(err, 1) == 0) {
+        if (__shfl_sync(0xffffffffu, clock64(), 0) - t0 > (1LL << 33)) {
+            if ((threadIdx.x & 31) == 0 && atomicExch(err, 1) == 0) {
                 unsigned smid;
                 asm("mov.u32 %0, %%smid;" : "=r"(smid));
                 err[1] = blockIdx.x;
@@ -1226,22 +1262,26 @@ __device__ __forceinline__ void df_wait(const int* flag, int want, int* err, con
                 err[5] = ld_relaxed_i(flag);
                 err[6] = tag;
             }
+            __syncwarp();
             return;
         }
     }
 }
 
-// thread 0, streamed upload: band columns [0, need) of this job's view have arrived (k_band_lu_res wait_cols)
+// one warp (all lanes, warp-uniform like df_wait), streamed upload: band columns [0, need) of this job's view have
+// arrived (k_band_lu_res wait_cols)
 __device__ __forceinline__ void df_wait_cols(const FactorJob& J, int need) {
     const long long want = min(J.m, need + 1);
-    const long long t0 = clock64();
+    const long long t0 = __shfl_sync(0xffffffffu, clock64(), 0);
     for (;;) {
         unsigned r;
         asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(J.ready) : "memory");
+        r = __shfl_sync(0xffffffffu, r, 0);
         const long long got = (long long)r * J.piece;
         if (got >= want || got * J.ends >= J.m) return;
-        if (clock64() - t0 > (1LL << 36)) {  // ~35 s: the upload stalled (reported through minpiv)
-            *J.minpiv = -1.0;
+        if (__shfl_sync(0xffffffffu, clock64(), 0) - t0 > (1LL << 36)) {  // ~35 s: the upload stalled (minpiv)
+            if ((threadIdx.x & 31) == 0) *J.minpiv = -1.0;
+            __syncwarp();
             return;
         }
         __nanosleep(128);
@@ -1257,6 +1297,8 @@ __device__ __forceinline__ double df_ld(const Lu& L, int i, int c, bool fresh) {
 // trace mark (tools/lu_df_trace.py): per-CTA slot `k` of the current item
 // marks go to shared memory (one global record per item at its end: tracing must not perturb the item)
 __shared__ unsigned long long g_df_smark[8];
+__shared__ unsigned long long g_df_pmark[10];  // trace: panel_diag's 4-pivot groups [0, 9), the update rows' end
+constexpr int kDfRec = 20;                     // trace record (u64)
 #define DF_MARK(k)                                                   \
     do {                                                             \
         if (A.trace && threadIdx.x == 0) g_df_smark[k] = clock64(); \
@@ -1500,6 +1542,105 @@ __device__ __forceinline__ void df_chain_update(const Lu& L, const DfTile& T, co
     }
 }
 
+// The chain's update split so that the pivot chain overlaps most of it (same per-element FMAs, k ascending, as
+// df_chain_update). Top: rows [0, 32) of the new panel -- all the pivot chain needs -- by every thread (row
+// tid % 32, a warp shares its columns), written in place (they overwrite only panel s-1's L11\U11, which nobody
+// reads any more); rows [R, 32) below a short last block become zeros. Ends with a barrier.
+template <int NT>
+__device__ __forceinline__ void df_upd_top(const Lu& L, const DfTile& T, double* __restrict__ P, int pld,
+                                           const double* __restrict__ U, int uld) {
+    constexpr int CPW = 32 / (NT / 32);  // columns per warp
+    const int i = threadIdx.x & 31, c0 = CPW * (threadIdx.x >> 5);
+    const long long rs = L.rs;
+    double c[CPW];
+#pragma unroll
+    for (int q = 0; q < CPW; ++q) {
+        const int cc = c0 + q;
+        const double* p = (cc >= T.fr || i >= T.fr) ? L.src_at(T.ja, T.ja + cc) : L.at(T.ja, T.ja + cc);
+        c[q] = (i < T.R && cc < T.wc) ? __ldcg(p + i * rs) : 0.0;
+    }
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) {
+        const double l = P[k * pld + 32 + i];
+#pragma unroll
+        for (int q = 0; q < CPW; ++q) c[q] = fma(-l, U[k * uld + c0 + q], c[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < CPW; ++q)
+        if (c0 + q < T.wc) P[(c0 + q) * pld + i] = i < T.R ? c[q] : 0.0;
+    __syncthreads();
+}
+
+// Rows [32, R) of the new panel by warps 1.. (NT - 32 threads: rows 32 + (t % RS) + RS h, columns 8 (t / RS) +
+// [0, 8)) while warp 0 runs the pivot chain; results are written after the group's named barrier ends every
+// read of panel s-1's L21 rows (they are overwritten in place).
+template <int NT>
+__device__ __forceinline__ void df_upd_rest(const Lu& L, const DfTile& T, double* __restrict__ P, int pld,
+                                            const double* __restrict__ U, int uld) {
+    constexpr int NW = NT - 32, RS = NW / 4;  // 4 column groups of 8; RS * 4 >= MAXK - 32 rows
+    const int t = threadIdx.x - 32, i0 = 32 + t % RS, cg = t / RS;
+    const long long rs = L.rs;
+    double c[4][8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int cc = 8 * cg + q;
+        const bool fc = cc >= T.fr;
+        const double* ps = L.at(T.ja, T.ja + cc);
+        const double* pf = L.src_at(T.ja, T.ja + cc);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const int i = i0 + RS * h;
+            c[h][q] = (i < T.R && cc < T.wc) ? __ldcg(((fc || i >= T.fr) ? pf : ps) + i * rs) : 0.0;
+        }
+    }
+    if (32 + RS * 3 >= T.R) {  // three row passes cover it (K <= 32 + 3 RS)
+#pragma unroll 4
+        for (int k = 0; k < 32; ++k) {
+            double u[8], l[3];
+            const double2* uk = reinterpret_cast<const double2*>(U + k * uld + 8 * cg);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const double2 w = uk[q];
+                u[2 * q] = w.x;
+                u[2 * q + 1] = w.y;
+            }
+#pragma unroll
+            for (int h = 0; h < 3; ++h) l[h] = P[k * pld + 32 + i0 + RS * h];
+#pragma unroll
+            for (int h = 0; h < 3; ++h)
+#pragma unroll
+                for (int q = 0; q < 8; ++q) c[h][q] = fma(-l[h], u[q], c[h][q]);
+        }
+    } else {
+#pragma unroll 4
+        for (int k = 0; k < 32; ++k) {
+            double u[8], l[4];
+            const double2* uk = reinterpret_cast<const double2*>(U + k * uld + 8 * cg);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const double2 w = uk[q];
+                u[2 * q] = w.x;
+                u[2 * q + 1] = w.y;
+            }
+#pragma unroll
+            for (int h = 0; h < 4; ++h) l[h] = P[k * pld + 32 + i0 + RS * h];
+#pragma unroll
+            for (int h = 0; h < 4; ++h)
+#pragma unroll
+                for (int q = 0; q < 8; ++q) c[h][q] = fma(-l[h], u[q], c[h][q]);
+        }
+    }
+    named_sync(kBarPg, NW);  // every reader of panel s-1's L21 in this group is done
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+        const int i = i0 + RS * h;
+        if (i >= T.R) continue;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (8 * cg + q < T.wc) P[(8 * cg + q) * pld + i] = c[h][q];
+    }
+}
+
 // U12 = L11^{-1} A12 for nc (<= 32 kDfG) columns, in 8-row blocks: rows of block b first take j = 0..8b-1 (256
 // threads: row 8b + tid/32, columns tid%32 + 32 g), then the block's unit-lower 8 x 8 triangle (thread per
 // column). Element (q, c) receives j = 0..q-1 in ascending order with the same FMAs as a column-sequential
@@ -1627,54 +1768,62 @@ __device__ __forceinline__ void df_chain(const DfArgs& A, const FactorJob& J, in
     // step s-1 (the strip that produces this panel)
     const int sp = s - 1, jbp = jb - B, rprevp = sp > 0 ? min(K, m - jbp) : 0;
     const DfTile T{jb, rprev, 0, min(B, rprev), sp > 0 ? rprevp - B : 0};
-    if (tid == 0) {
+    if (warp == 0) {
         if (STREAM) df_wait_cols(J, ja + R + nbn + 1);
         if (s > 0) df_wait(A.panel_cnt + jid, s, A.err, A.panel_cnt, 1);
         if (sp > 0 && B < rprevp) df_wait(A.col_step + (size_t)jid * A.S + s, sp, A.err, A.panel_cnt, 2);
-        df_acquire();
-        *s_boosts = 0;
-        if (A.trace) g_df_smark[0] = clock64();
+        if (lane == 0) {
+            df_acquire();
+            *s_boosts = 0;
+            if (A.trace) g_df_smark[0] = clock64();
+        }
     }
     __syncthreads();
     if (s > 0) {
         // panel s-1: still in shared memory when this CTA factored it (job owner), else from L2
         if (!have_panel) df_stage_panel<NT>(L, P, pld, jbp, jbp, B + rprev, B, B + rprev);
         df_a12<NT>(L, jbp, jb, 0, 32, T.wc, T.fr, sp == 0, U, uld);
-        // this panel's rows that no earlier step updated (<= 32 of them): loaded now, written after the update
-        constexpr int NF = 1024 / NT;
+        // this panel's rows that no earlier step updated (<= 32 of them), loaded now by warps 1.. and written
+        // once the update has finished reading panel s-1
+        constexpr int NW = NT - 32, NF = (1024 + NW - 1) / NW;
         double fv[NF];
 #pragma unroll
         for (int u = 0; u < NF; ++u) {
-            const int e = tid + u * NT, c = e >> 5, r = rprev + (e & 31);
-            fv[u] = (c < nb && r < ph && L.inband(r, c)) ? __ldcg(L.src_at(jb + r, jb + c)) : 0.0;
+            const int e = tid - 32 + u * NW, c = e >> 5, r = rprev + (e & 31);
+            fv[u] = (warp > 0 && e < 1024 && c < nb && r < ph && L.inband(r, c)) ? __ldcg(L.src_at(jb + r, jb + c))
+                                                                                  : 0.0;
         }
         __syncthreads();
         DF_MARK(1);
         df_u12<NT>(L, jbp, jb, 0, 32, T.wc, P, pld, U, uld);
-        if (A.excl) {  // alone on its SM: the strip on DMMA (bitwise the DFMA form)
-            double acc[DfCfg<NT>::NG][2][2];
-            df_c_load<NT>(L, T, acc);
-            df_dmma<NT>(T, P, pld, U, uld, acc);
-            __syncthreads();  // every warp is done with panel s-1
-            df_c_to_smem<NT>(T, acc, P, pld);
+        df_upd_top<NT>(L, T, P, pld, U, uld);
+        DF_MARK(2);
+        if (warp == 0) {
+            if (nb == B)
+                panel_diag<B, true>(P, pld, s_ut, s_rcp, nb, L.bv, s_boosts, A.trace ? g_df_pmark : nullptr);
+            else
+                panel_diag<B, false>(P, pld, s_ut, s_rcp, nb, L.bv, s_boosts, A.trace ? g_df_pmark : nullptr);
+            DF_MARK(3);
         } else {
-            df_chain_update<NT>(L, T, P, P, pld, U, uld);
-        }
+            df_upd_rest<NT>(L, T, P, pld, U, uld);
 #pragma unroll
-        for (int u = 0; u < NF; ++u) {
-            const int e = tid + u * NT, c = e >> 5, r = rprev + (e & 31);
-            if (r < pld) P[c * pld + r] = fv[u];
+            for (int u = 0; u < NF; ++u) {
+                const int e = tid - 32 + u * NW, c = e >> 5, r = rprev + (e & 31);
+                if (e < 1024 && r < pld) P[c * pld + r] = fv[u];
+            }
+            if (A.trace && tid == 32) g_df_pmark[9] = clock64();
         }
     } else {
         df_stage_panel<NT>(L, P, pld, jb, jb, ph, nb, 0);
-    }
-    __syncthreads();
-    DF_MARK(2);
-    if (warp == 0) {
-        if (nb == B)
-            panel_diag<B, true>(P, pld, s_ut, s_rcp, nb, L.bv, s_boosts);
-        else
-            panel_diag<B, false>(P, pld, s_ut, s_rcp, nb, L.bv, s_boosts);
+        __syncthreads();
+        DF_MARK(2);
+        if (warp == 0) {
+            if (nb == B)
+                panel_diag<B, true>(P, pld, s_ut, s_rcp, nb, L.bv, s_boosts, A.trace ? g_df_pmark : nullptr);
+            else
+                panel_diag<B, false>(P, pld, s_ut, s_rcp, nb, L.bv, s_boosts, A.trace ? g_df_pmark : nullptr);
+            DF_MARK(3);
+        }
     }
     __syncthreads();
     // L21 rows (thread per row; panel_rows_cols' row half)
@@ -1683,7 +1832,7 @@ __device__ __forceinline__ void df_chain(const DfArgs& A, const FactorJob& J, in
     else
         df_rows<B, false, NT>(P, pld, s_ut, s_rcp, nb, ph);
     __syncthreads();
-    DF_MARK(3);
+    DF_MARK(4);
     // the panel is final: L11\U11 and L21 to the store (the worker strips of this step read it from L2); row pairs
     // (r, r + 1), r even, as one 16-byte store where both are in the band (alignment is uniform per column)
     const long long rs = L.rs;
@@ -1724,7 +1873,6 @@ __device__ __forceinline__ void df_chain(const DfArgs& A, const FactorJob& J, in
         const int nbst = *s_boosts;
         if (nbst) atomicAdd(A.boost_acc + jid, nbst);
         if (jb + nb >= m) *J.boosts = atomicAdd(A.boost_acc + jid, 0);  // the job's last panel
-        DF_MARK(4);
         st_release_i(A.panel_cnt + jid, s + 1);  // after the CTA barrier: publishes every thread's stores
     }
 }
@@ -1748,14 +1896,16 @@ __device__ __forceinline__ void df_worker(const DfArgs& A, const FactorJob& J, i
     const int rprev = s > 0 ? min(K, m - jb) : 0;
     const int fr = s > 0 ? rprev - nb : 0;
     Lu L{J.base, J.rs, J.cs, m, K, B, pld, uld, 0.0, J.src ? J.src : J.base};
-    if (tid == 0) {
+    if (tid < 32) {
         if (STREAM) df_wait_cols(J, ja + R + 1);
         df_wait(A.panel_cnt + jid, s + 1, A.err, A.panel_cnt, 3);
         for (int j = j0; j < j1; ++j)
             if (s > 0 && 32 * (j + 1) < rprev)
                 df_wait(A.col_step + (size_t)jid * A.S + s + 1 + j, s, A.err, A.panel_cnt, 4);
-        df_acquire();
-        if (A.trace) g_df_smark[0] = clock64();
+        if (tid == 0) {
+            df_acquire();
+            if (A.trace) g_df_smark[0] = clock64();
+        }
     }
     __syncthreads();
     df_stage_panel<NT>(L, P, pld, jb, jb, ph, B, ph);
@@ -1800,23 +1950,26 @@ __global__ void __launch_bounds__(NT, DfCfg<NT>::MINB) k_band_lu_df(DfArgs A) {
     // SM role: the first nps SMs on which CTAs of this launch actually start become panel SMs (placement and
     // %smid numbering are not under our control; every CTA of an SM shares its SM's role)
     __shared__ int s_role, s_rank, s_mode;
-    if (tid == 0) {
+    if (tid < 32) {  // warp 0 together (lane 0 does the atomics): no divergent spin (df_wait)
+        const bool l0 = tid == 0;
         int* rp = A.sm_role + (smid % kDfMaxSm);
-        int r = atomicCAS(rp, 0, 3);
+        int r = __shfl_sync(0xffffffffu, l0 ? atomicCAS(rp, 0, 3) : 0, 0);
         if (r == 0) {
-            r = atomicAdd(A.n_panel_sm, 1) < A.nps ? 1 : 2;
-            atomicExch(rp, r);
+            r = __shfl_sync(0xffffffffu, l0 ? (atomicAdd(A.n_panel_sm, 1) < A.nps ? 1 : 2) : 0, 0);
+            if (l0) atomicExch(rp, r);
         } else {
             while (r == 3) {
                 __nanosleep(20);
-                r = ld_relaxed_i(rp);
+                r = ld_relaxed_w(rp);
             }
             if (r == 1 && A.excl) r = 0;  // exclusive panel SM: only its deciding CTA stays
         }
-        s_role = r;
-        s_rank = r == 1 ? atomicAdd(A.n_chain, 1) : -1;
-        __threadfence();
-        atomicAdd(A.started, 1);
+        if (l0) {
+            s_role = r;
+            s_rank = r == 1 ? atomicAdd(A.n_chain, 1) : -1;
+            __threadfence();
+            atomicAdd(A.started, 1);
+        }
     }
     __syncthreads();
     if (s_role == 0) {
@@ -1832,19 +1985,19 @@ __global__ void __launch_bounds__(NT, DfCfg<NT>::MINB) k_band_lu_df(DfArgs A) {
         // chain(r, 0), chain(r, 1), ... and keeps each panel in shared memory for the next step. Deadlock-free like
         // the queue (each job's items run in order on a resident CTA; the workers' queue is unchanged). Otherwise
         // (a CTA still waiting for a slot after 20 us, or fewer chain CTAs than jobs) the shared queue.
-        if (tid == 0) {
-            int md = ld_relaxed_i(A.mode);
+        if (tid < 32) {
+            int md = ld_relaxed_w(A.mode);
             if (md == 0) {
-                const unsigned long long t0 = df_now();
-                while (ld_relaxed_i(A.started) < (int)gridDim.x && df_now() - t0 < 20000) __nanosleep(64);
-                const int want = A.owners_ok && ld_relaxed_i(A.started) == (int)gridDim.x &&
-                                         ld_relaxed_i(A.n_chain) >= J
-                                     ? 1
-                                     : 2;
-                md = atomicCAS(A.mode, 0, want);
+                const unsigned long long t0 = __shfl_sync(0xffffffffu, df_now(), 0);
+                while (ld_relaxed_w(A.started) < (int)gridDim.x &&
+                       __shfl_sync(0xffffffffu, df_now(), 0) - t0 < 20000)
+                    __nanosleep(64);
+                const int want =
+                    A.owners_ok && ld_relaxed_w(A.started) == (int)gridDim.x && ld_relaxed_w(A.n_chain) >= J ? 1 : 2;
+                md = __shfl_sync(0xffffffffu, tid == 0 ? atomicCAS(A.mode, 0, want) : 0, 0);
                 if (md == 0) md = want;
             }
-            s_mode = md;
+            if (tid == 0) s_mode = md;
         }
         __syncthreads();
         if (s_mode == 1) {
@@ -1856,19 +2009,22 @@ __global__ void __launch_bounds__(NT, DfCfg<NT>::MINB) k_band_lu_df(DfArgs A) {
                 if (A.trace && tid == 0) {
                     t_grab = df_now();
                     for (int q = 0; q < 5; ++q) g_df_smark[q] = 0;
+                    for (int q = 0; q < 10; ++q) g_df_pmark[q] = 0;
                     g_df_smark[5] = clock64();
                 }
                 df_chain<NT, STREAM>(A, Jb, jid, s, P, U, s_ut, s_rcp, &s_boosts, s > 0);
                 __syncthreads();
                 if (A.trace && tid == 0) {
                     const unsigned long long c_end = clock64();
-                    unsigned long long* tr = A.trace + 10 * ((size_t)gridDim.x + (size_t)s * J + jid);
+                    unsigned long long* tr = A.trace + kDfRec * ((size_t)gridDim.x + (size_t)s * J + jid);
                     tr[0] = t_grab;
                     tr[1] = df_now();
                     tr[2] = g_df_smark[5];
                     for (int q = 0; q < 5; ++q) tr[3 + q] = g_df_smark[q];
                     tr[8] = c_end;
                     tr[9] = ((unsigned long long)smid << 32) | blockIdx.x;
+            for (int q = 0; q < 10; ++q) tr[10 + q] = g_df_pmark[q];
+                    for (int q = 0; q < 10; ++q) tr[10 + q] = g_df_pmark[q];
                 }
             }
             if (tid == 0) atomicAdd(A.counter_p, (unsigned)A.S);  // releases the exclusive SMs' spare CTAs
@@ -1893,6 +2049,7 @@ __global__ void __launch_bounds__(NT, DfCfg<NT>::MINB) k_band_lu_df(DfArgs A) {
         if (A.trace && tid == 0) {
             t_grab = df_now();
             for (int q = 0; q < 5; ++q) g_df_smark[q] = 0;
+            for (int q = 0; q < 10; ++q) g_df_pmark[q] = 0;
             g_df_smark[5] = clock64();
         }
         long long rec;
@@ -1923,13 +2080,14 @@ __global__ void __launch_bounds__(NT, DfCfg<NT>::MINB) k_band_lu_df(DfArgs A) {
         if (A.trace && tid == 0) {
             // record (10 u64): grab / end (globaltimer ns), grab / ready / marks 1-4 / end (clock64), SM << 32 | CTA
             const unsigned long long c_end = clock64();
-            unsigned long long* tr = A.trace + 10 * ((size_t)gridDim.x + rec);
+            unsigned long long* tr = A.trace + kDfRec * ((size_t)gridDim.x + rec);
             tr[0] = t_grab;
             tr[1] = df_now();
             tr[2] = g_df_smark[5];
             for (int q = 0; q < 5; ++q) tr[3 + q] = g_df_smark[q];
             tr[8] = c_end;
             tr[9] = ((unsigned long long)smid << 32) | blockIdx.x;
+            for (int q = 0; q < 10; ++q) tr[10 + q] = g_df_pmark[q];
         }
     }
 }
@@ -2014,7 +2172,7 @@ void launch_band_lu_df(const FactorJob* d_jobs, int njobs, int m_max, int max_k,
     int nps = A.excl ? std::min(njobs, cap) : std::min((njobs + per_sm - 1) / std::max(per_sm, 1), cap);
     A.nps = std::max(1, std::min(nps, nsm - 1));
     if (g_df_trace_mode && (g_df_trace_mode == 1) == streamed) {  // tools/lu_df_trace.py
-        const size_t need = 10 * (size_t)(grid + items);
+        const size_t need = kDfRec * (size_t)(grid + items);
         if (g_df_trace_cap < need) {
             if (g_df_trace) cudaFree(g_df_trace);
             SAP_CUDA(cudaMalloc(&g_df_trace, need * sizeof(unsigned long long)));
@@ -2062,7 +2220,7 @@ extern "C" long long sap_dev_lu_df_trace(unsigned long long* out, long long cap)
     if (!g_df_trace) return 0;
     const long long n = std::min<long long>(cap, g_df_trace_items);
     cudaDeviceSynchronize();
-    cudaMemcpy(out, g_df_trace + 10 * (size_t)g_df_trace_grid, sizeof(unsigned long long) * 10 * n,
+    cudaMemcpy(out, g_df_trace + kDfRec * (size_t)g_df_trace_grid, sizeof(unsigned long long) * kDfRec * n,
                cudaMemcpyDeviceToHost);
     return n;
 }

@@ -45,12 +45,14 @@ def main():
         print("t_factor_kernel ms", s.report()["t_factor_kernel"] * 1e3)
     lib = _lib.load()
     lib.sap_dev_lu_df_trace.restype = C.c_longlong
-    cap = 2_000_000
-    buf = np.zeros(10 * cap, np.uint64)
+    cap = 1_000_000
+    REC = 20  # lu.cu kDfRec: grab/end ns, grab/ready/marks 1-4/end clock, SM|CTA, panel_diag groups 0-8, rows end
+    buf = np.zeros(REC * cap, np.uint64)
     cnt = lib.sap_dev_lu_df_trace(buf.ctypes.data_as(C.POINTER(C.c_ulonglong)), cap)
-    t = buf[: 10 * cnt].reshape(cnt, 10).astype(np.int64)
-    os.makedirs("gpurun_out", exist_ok=True)
-    np.save(f"gpurun_out/dftrace_{kind}.npy", t)
+    t = buf[: REC * cnt].reshape(cnt, REC).astype(np.int64)
+    out = os.path.join(ROOT, "gpurun_out")
+    os.makedirs(out, exist_ok=True)
+    np.save(os.path.join(out, f"dftrace_{kind}.npy"), t)
     J = 2 * p if kind == "C" else p
     m_max = -(-n // p)
     valid = t[:, 1] > 0
