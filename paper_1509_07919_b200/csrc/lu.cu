@@ -1181,7 +1181,7 @@ struct DfCfg {
 };
 constexpr int kLuDfMinK = 192;  // narrower bands: too few strips per step to pay for the item overheads
 constexpr int kDfMaxSm = 256;  // %smid bound
-constexpr int kDfG = 3;        // strips per worker item (one panel load and one U12 solve for all of them)  // row groups (8 rows) per warp: 4 warps share a strip's rows, K <= 224
+constexpr int kDfG = 3;        // max strips per worker item (one panel load and one U12 solve for all of them)  // row groups (8 rows) per warp: 4 warps share a strip's rows, K <= 224
 
 struct DfArgs {
     const FactorJob* jobs;
@@ -1196,6 +1196,7 @@ struct DfArgs {
     int* started;         // CTAs past their role claim
     int* mode;            // chain schedule: 0 undecided, 1 job owners, 2 shared s-major queue
     int owners_ok;        // 0: always the queue (tools/lu_df_check.py A/B)
+    int grp;              // strips per worker item (1..kDfG)
     int* panel_cnt;  // [njobs]
     int* col_step;   // [njobs][S]
     int* boost_acc;  // [njobs]
@@ -1641,13 +1642,53 @@ __device__ __forceinline__ void df_upd_rest(const Lu& L, const DfTile& T, double
     }
 }
 
-// U12 = L11^{-1} A12 for nc (<= 32 kDfG) columns, in 8-row blocks: rows of block b first take j = 0..8b-1 (256
+// U12 = L11^{-1} A12 for nc (<= 32 kDfG) columns: a thread per column, right-looking substitution with every
+// index compile-time (x in registers, L11 pairs as 16-byte broadcasts). Element (q, c) receives j = 0..q-1 in
+// ascending order with the same FMAs as a column-sequential substitution (block_factors.hpp:246-250 order;
+// bitwise panel_rows_cols' column half). Latency ~31 dependent FMAs (the 8-row blocked form with its barriers
+// took ~4 us for 96 columns). The final U12 entries (window columns [c0, c0 + wc)) go to the store.
+template <int j>
+__device__ __forceinline__ void u12_col(double (&x)[32], const double* __restrict__ P, int pld) {
+    const double* __restrict__ lj = P + j * pld;  // lj[q] = L11(q, j)
+    constexpr int q0 = j + 1;
+    if constexpr (q0 < 32 && (q0 & 1)) x[q0] = fma(-lj[q0], x[j], x[q0]);
+#pragma unroll
+    for (int q = (q0 + 1) & ~1; q < 32; q += 2) {
+        const double2 l2 = *reinterpret_cast<const double2*>(lj + q);  // free to hoist (not lds2)
+        x[q] = fma(-l2.x, x[j], x[q]);
+        x[q + 1] = fma(-l2.y, x[j], x[q + 1]);
+    }
+    if constexpr (j + 1 < 31) u12_col<j + 1>(x, P, pld);
+}
+
+template <int NT>
+__device__ __forceinline__ void df_u12(const Lu& L, int jb, int ja, int c0, int nc, int wc,
+                                       const double* __restrict__ P, int pld, double* __restrict__ U, int uld) {
+    constexpr int B = 32;
+    const int tid = threadIdx.x;
+    if (tid < nc) {
+        double x[B];
+#pragma unroll
+        for (int q = 0; q < B; ++q) x[q] = U[q * uld + tid];
+        u12_col<0>(x, P, pld);
+#pragma unroll
+        for (int q = 1; q < B; ++q) U[q * uld + tid] = x[q];
+    }
+    __syncthreads();
+    // final U12 entries (the store's A12 rows; evict-first: the factorization is done with them)
+    for (int e = tid; e < B * nc; e += NT) {
+        const int cc = e >> 5, r = e & 31;
+        if (cc < wc && B + c0 + cc - r <= L.K) st_first(L.at(jb + r, ja + c0 + cc), U[r * uld + cc]);
+    }
+}
+
+// U12 = L11^{-1} A12 (the chain's 32 columns), in 8-row blocks: rows of block b first take j = 0..8b-1 (256
 // threads: row 8b + tid/32, columns tid%32 + 32 g), then the block's unit-lower 8 x 8 triangle (thread per
 // column). Element (q, c) receives j = 0..q-1 in ascending order with the same FMAs as a column-sequential
 // substitution (block_factors.hpp:246-250 order; bitwise panel_rows_cols' column half) with dependent chains
 // <= 24 + 7 long. The final U12 entries (window columns [c0, c0 + wc)) go to the store. Ends with a barrier.
 template <int NT>
-__device__ __forceinline__ void df_u12(const Lu& L, int jb, int ja, int c0, int nc, int wc,
+__device__ __forceinline__ void df_u12_blk(const Lu& L, int jb, int ja, int c0, int nc, int wc,
                                        const double* __restrict__ P, int pld, double* __restrict__ U, int uld) {
     constexpr int B = 32, H = 8;
     const int tid = threadIdx.x, rr = tid >> 5, c = tid & 31;
@@ -1795,7 +1836,7 @@ __device__ __forceinline__ void df_chain(const DfArgs& A, const FactorJob& J, in
         }
         __syncthreads();
         DF_MARK(1);
-        df_u12<NT>(L, jbp, jb, 0, 32, T.wc, P, pld, U, uld);
+        df_u12_blk<NT>(L, jbp, jb, 0, 32, T.wc, P, pld, U, uld);  // all warps (the 1-warp form ran slower here)
         df_upd_top<NT>(L, T, P, pld, U, uld);
         DF_MARK(2);
         if (warp == 0) {
@@ -1888,9 +1929,9 @@ __device__ __forceinline__ void df_worker(const DfArgs& A, const FactorJob& J, i
     const int jb = s * B;
     if (jb + B >= m) return;  // no trailing window (a strip step always has nb = 32)
     const int nb = B, ja = jb + nb, R = min(K, m - ja), ph = nb + R;
-    const int j0 = 1 + kDfG * g, c0 = 32 * j0;
+    const int j0 = 1 + A.grp * g, c0 = 32 * j0;
     if (c0 >= R) return;
-    const int j1 = min(j0 + kDfG, (R + 31) / 32);  // strips [j0, j1)
+    const int j1 = min(j0 + A.grp, (R + 31) / 32);  // strips [j0, j1)
     const int tid = threadIdx.x;
     const int pld = A.pld, uld = A.uld;
     const int rprev = s > 0 ? min(K, m - jb) : 0;
@@ -2036,9 +2077,9 @@ __global__ void __launch_bounds__(NT, DfCfg<NT>::MINB) k_band_lu_df(DfArgs A) {
     __syncthreads();
     // worker wave cursor: wave w holds strips [w0, w0 + wn) (J x (strips - 1) of step w)
     int w = 0, w0 = 0;
-    auto wave_n = [&](int ww) {  // worker items of step ww: J x ceil((strips - 1) / kDfG)
+    auto wave_n = [&](int ww) {  // worker items of step ww: J x ceil((strips - 1) / grp)
         const int R = min(A.K, A.m_max - 32 * (ww + 1));
-        return J * (((R + 31) / 32 - 1 + kDfG - 1) / kDfG);
+        return J * (((R + 31) / 32 - 1 + A.grp - 1) / A.grp);
     };
     int wn = A.S >= 2 ? wave_n(0) : 0;
     for (;;) {
@@ -2093,6 +2134,7 @@ __global__ void __launch_bounds__(NT, DfCfg<NT>::MINB) k_band_lu_df(DfArgs A) {
 }
 
 static int g_df_owners = 1;      // sap_dev_lu_df_owners
+static int g_df_group = 0;       // sap_dev_lu_df_group (0: auto)
 static int g_df_trace_mode = 0;  // sap_dev_lu_df_trace_mode: 1 trace streamed launches, 2 the others
 static unsigned long long* g_df_trace = nullptr;
 static size_t g_df_trace_cap = 0;
@@ -2158,19 +2200,20 @@ void launch_band_lu_df(const FactorJob* d_jobs, int njobs, int m_max, int max_k,
     SAP_CUDA(cudaGetDevice(&dev));
     SAP_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     SAP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, bytes));
-    // chain items (one per job and step) + worker strips
-    long long items = (long long)njobs * S;
-    for (int w = 0; w <= S - 2; ++w)
-        items += (long long)njobs * (((std::min(max_k, m_max - B * (w + 1)) + 31) / 32 - 1 + kDfG - 1) / kDfG);
     const int grid = nsm * std::max(per_sm, 1);
-    // panel SMs: one resident chain per job where the SMs allow (chains are latency-bound), at most 40 %
     // panel SMs: one resident chain per job (chains are latency-bound), at most 40 % of the SMs; when every
-    // job gets a panel SM to itself (few jobs), it is exclusive: the chain's strip update then runs on DMMA
-    // without stalling another chain's pivots
+    // job gets a panel SM to itself (few jobs), it is exclusive: no other chain CTA on its SM
     const int cap = (2 * nsm) / 5;
     A.excl = (njobs <= cap || per_sm <= 1) ? 1 : 0;  // one CTA per SM (wide bands) is exclusive anyway
     int nps = A.excl ? std::min(njobs, cap) : std::min((njobs + per_sm - 1) / std::max(per_sm, 1), cap);
     A.nps = std::max(1, std::min(nps, nsm - 1));
+    // strips per worker item: a group waits for the previous step's group to finish (its strips shifted by one),
+    // so the group's duration bounds the step period; few jobs leave worker SMs idle enough for shorter groups
+    A.grp = g_df_group > 0 ? std::min(g_df_group, kDfG) : (A.excl ? 2 : kDfG);
+    // chain items (one per job and step) + worker strips
+    long long items = (long long)njobs * S;
+    for (int w = 0; w <= S - 2; ++w)
+        items += (long long)njobs * (((std::min(max_k, m_max - B * (w + 1)) + 31) / 32 - 1 + A.grp - 1) / A.grp);
     if (g_df_trace_mode && (g_df_trace_mode == 1) == streamed) {  // tools/lu_df_trace.py
         const size_t need = kDfRec * (size_t)(grid + items);
         if (g_df_trace_cap < need) {
@@ -2214,6 +2257,8 @@ bool band_lu_reads_source(int max_k) {
 extern "C" void sap_dev_lu_df_trace_mode(int mode) { sapgpu::g_df_trace_mode = mode; }
 // tools only: 0 keeps the dataflow LU's chain items on the shared queue (no job owners), 1 the default
 extern "C" void sap_dev_lu_df_owners(int on) { sapgpu::g_df_owners = on; }
+// tools only: strips per worker item (1..3; 0 = auto)
+extern "C" void sap_dev_lu_df_group(int g) { sapgpu::g_df_group = g; }
 
 extern "C" long long sap_dev_lu_df_trace(unsigned long long* out, long long cap) {
     using namespace sapgpu;

@@ -15,7 +15,7 @@ import paper_1509_07919_b200 as S  # noqa: E402
 from paper_1509_07919_b200 import _lib  # noqa: E402
 
 
-def decode(item, J, K, m_max):
+def decode(item, J, K, m_max, G=3):
     S = -(-m_max // 32)
     if item < S * J:
         return ("chain", item % J, item // J, 0)
@@ -23,10 +23,10 @@ def decode(item, J, K, m_max):
     w = 0
     while True:
         R = min(K, m_max - 32 * (w + 1))
-        ng = ((R + 31) // 32 - 1 + 2) // 3
+        ng = ((R + 31) // 32 - 1 + G - 1) // G
         wn = J * ng
         if o < wn:
-            return ("strip", o // ng, w, 1 + 3 * (o % ng))
+            return ("strip", o // ng, w, 1 + G * (o % ng))
         o -= wn
         w += 1
 
@@ -35,6 +35,10 @@ def main():
     kind = sys.argv[1] if len(sys.argv) > 1 else "C"
     n, k, p = (int(x) for x in sys.argv[2:5]) if len(sys.argv) > 4 else (200000, 200, 50)
     _lib.load().sap_dev_lu_df_trace_mode(1)
+    G = int(os.environ.get("DF_GROUP", "0"))  # strips per worker item (lu.cu A.grp); 0: the launcher's choice
+    _lib.load().sap_dev_lu_df_group(G)
+    if G == 0:
+        G = 2 if (kind == "D" and p <= 59) else 3  # launch_band_lu_df: exclusive panel SMs -> 2
     band, rhs = S.random_banded(n, k, 1.0, 1)
     src = torch.from_numpy(band).cuda()
     pk = S.PrecondKind.coupled if kind == "C" else S.PrecondKind.decoupled
@@ -65,7 +69,7 @@ def main():
     for i in range(cnt):
         if not valid[i]:
             continue
-        ty, job, st, j = decode(i, J, k, m_max)
+        ty, job, st, j = decode(i, J, k, m_max, G)
         skipped = t[i, 3] == 0
         d = types.setdefault(ty, [0, 0.0, 0.0, 0, np.zeros(5)])
         d[0] += 1
@@ -87,19 +91,19 @@ def main():
     wait = sum((ready[i] - grab[i]) for i in range(cnt) if valid[i] and t[i, 3] > 0)
     print(f"CTAs {ncta}: work {work / (ncta * span):.2%}, dependency wait {wait / (ncta * span):.2%} of CTA-time")
     # critical path sample: job 0's panels
-    ps = sorted((decode(i, J, k, m_max)[2], ready[i], end[i]) for i in range(cnt)
-                if valid[i] and decode(i, J, k, m_max)[:2] == ("chain", 0))
+    ps = sorted((decode(i, J, k, m_max, G)[2], ready[i], end[i]) for i in range(cnt)
+                if valid[i] and decode(i, J, k, m_max, G)[:2] == ("chain", 0))
     if len(ps) > 4:
         steps = np.diff([x[2] for x in ps])
         print(f"job 0 panel-to-panel: median {np.median(steps)/1e3:.2f} us, panel work median "
               f"{np.median([x[2]-x[1] for x in ps])/1e3:.2f} us")
-    s0 = [(decode(i, J, k, m_max)[2], grab[i], ready[i], end[i]) for i in range(cnt)
-          if valid[i] and decode(i, J, k, m_max)[:2] == ("strip", 0) and decode(i, J, k, m_max)[3] == 1]
+    s0 = [(decode(i, J, k, m_max, G)[2], grab[i], ready[i], end[i]) for i in range(cnt)
+          if valid[i] and decode(i, J, k, m_max, G)[:2] == ("strip", 0) and decode(i, J, k, m_max, G)[3] == 1]
     if s0:
         print("job 0 strip1 work median %.2f us, wait median %.2f us" % (
             np.median([x[3] - x[2] for x in s0]) / 1e3, np.median([x[2] - x[1] for x in s0]) / 1e3))
     for w in (5, 50, 100):
-        sel = [i for i in range(cnt) if valid[i] and decode(i, J, k, m_max)[2] == w]
+        sel = [i for i in range(cnt) if valid[i] and decode(i, J, k, m_max, G)[2] == w]
         if sel:
             print(f"step {w}: items {len(sel)} grab [{grab[sel].min()/1e3:.1f}, {grab[sel].max()/1e3:.1f}] "
                   f"end [{end[sel].min()/1e3:.1f}, {end[sel].max()/1e3:.1f}] us")
