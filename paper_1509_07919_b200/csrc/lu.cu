@@ -1299,7 +1299,7 @@ __device__ __forceinline__ double df_ld(const Lu& L, int i, int c, bool fresh) {
 // marks go to shared memory (one global record per item at its end: tracing must not perturb the item)
 __shared__ unsigned long long g_df_smark[8];
 __shared__ unsigned long long g_df_pmark[10];  // trace: panel_diag's 4-pivot groups [0, 9), the update rows' end
-constexpr int kDfRec = 20;                     // trace record (u64)
+constexpr int kDfRec = 22;                     // trace record (u64)
 #define DF_MARK(k)                                                   \
     do {                                                             \
         if (A.trace && threadIdx.x == 0) g_df_smark[k] = clock64(); \
@@ -1776,10 +1776,19 @@ __device__ __noinline__ void df_rows(double* __restrict__ P, int pld, const doub
                 x[c] = l;
                 const double2* __restrict__ u2 = reinterpret_cast<const double2*>(Ut + ut_off(c) - ut_lo(c));
 #pragma unroll
-                for (int j = (c + 1) & ~1; j < B; j += 2) {
-                    const double2 u = lds2(reinterpret_cast<const double*>(u2 + (j >> 1)));
-                    if (j > c) x[j] = fma(-l, u.x, x[j]);
-                    x[j + 1] = fma(-l, u.y, x[j + 1]);
+                for (int j0 = (c + 1) & ~1; j0 < B; j0 += 8) {  // 4 pairs per batch: one load latency each
+                    double2 u[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (j0 + 2 * q < B) u[q] = lds2(reinterpret_cast<const double*>(u2 + ((j0 >> 1) + q)));
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int j = j0 + 2 * q;
+                        if (j < B) {
+                            if (j > c) x[j] = fma(-l, u[q].x, x[j]);
+                            x[j + 1] = fma(-l, u[q].y, x[j + 1]);
+                        }
+                    }
                 }
             }
         }
@@ -1898,23 +1907,16 @@ __device__ __forceinline__ void df_chain(const DfArgs& A, const FactorJob& J, in
             }
         }
     }
-    // L2 prefetch of the band entries step s+1 meets first (rows [e, e + nbn) and columns [e, e + nbn))
-    if (nbn > 0 && ja + R < m) {
-        const int e = ja + R;
-        const int ncol = min(e + nbn, m) - ja;
-        for (int t = tid; t < ncol + min(nbn, m - e); t += NT) {
-            if (t < ncol)
-                prefetch_run(L, ja + t, e, e + nbn);
-            else
-                prefetch_run(L, e + t - ncol, ja + nbn, e);
-        }
-    }
+    // (no L2 prefetch of step s+1's first band entries here: 64 bulk prefetches cost the chain ~1.4 us, more than
+    // the worker loads they would speed up)
     __syncthreads();
     if (tid == 0) {
+        if (A.trace) g_df_smark[6] = clock64();
         const int nbst = *s_boosts;
         if (nbst) atomicAdd(A.boost_acc + jid, nbst);
         if (jb + nb >= m) *J.boosts = atomicAdd(A.boost_acc + jid, 0);  // the job's last panel
         st_release_i(A.panel_cnt + jid, s + 1);  // after the CTA barrier: publishes every thread's stores
+        if (A.trace) g_df_smark[7] = clock64();
     }
 }
 
@@ -2049,7 +2051,7 @@ __global__ void __launch_bounds__(NT, DfCfg<NT>::MINB) k_band_lu_df(DfArgs A) {
                 unsigned long long t_grab = 0;
                 if (A.trace && tid == 0) {
                     t_grab = df_now();
-                    for (int q = 0; q < 5; ++q) g_df_smark[q] = 0;
+                    for (int q = 0; q < 8; ++q) if (q != 5) g_df_smark[q] = 0;
                     for (int q = 0; q < 10; ++q) g_df_pmark[q] = 0;
                     g_df_smark[5] = clock64();
                 }
@@ -2064,8 +2066,9 @@ __global__ void __launch_bounds__(NT, DfCfg<NT>::MINB) k_band_lu_df(DfArgs A) {
                     for (int q = 0; q < 5; ++q) tr[3 + q] = g_df_smark[q];
                     tr[8] = c_end;
                     tr[9] = ((unsigned long long)smid << 32) | blockIdx.x;
-            for (int q = 0; q < 10; ++q) tr[10 + q] = g_df_pmark[q];
                     for (int q = 0; q < 10; ++q) tr[10 + q] = g_df_pmark[q];
+                    tr[20] = g_df_smark[6];
+                    tr[21] = g_df_smark[7];
                 }
             }
             if (tid == 0) atomicAdd(A.counter_p, (unsigned)A.S);  // releases the exclusive SMs' spare CTAs
@@ -2089,7 +2092,7 @@ __global__ void __launch_bounds__(NT, DfCfg<NT>::MINB) k_band_lu_df(DfArgs A) {
         unsigned long long t_grab = 0;
         if (A.trace && tid == 0) {
             t_grab = df_now();
-            for (int q = 0; q < 5; ++q) g_df_smark[q] = 0;
+            for (int q = 0; q < 8; ++q) if (q != 5) g_df_smark[q] = 0;
             for (int q = 0; q < 10; ++q) g_df_pmark[q] = 0;
             g_df_smark[5] = clock64();
         }
@@ -2129,6 +2132,8 @@ __global__ void __launch_bounds__(NT, DfCfg<NT>::MINB) k_band_lu_df(DfArgs A) {
             tr[8] = c_end;
             tr[9] = ((unsigned long long)smid << 32) | blockIdx.x;
             for (int q = 0; q < 10; ++q) tr[10 + q] = g_df_pmark[q];
+            tr[20] = g_df_smark[6];
+            tr[21] = g_df_smark[7];
         }
     }
 }

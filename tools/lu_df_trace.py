@@ -50,7 +50,7 @@ def main():
     lib = _lib.load()
     lib.sap_dev_lu_df_trace.restype = C.c_longlong
     cap = 1_000_000
-    REC = 20  # lu.cu kDfRec: grab/end ns, grab/ready/marks 1-4/end clock, SM|CTA, panel_diag groups 0-8, rows end
+    REC = 22  # lu.cu kDfRec: grab/end ns, grab/ready/marks 1-4/end clock, SM|CTA, panel_diag groups 0-8, rows end, chain stores done, release done
     buf = np.zeros(REC * cap, np.uint64)
     cnt = lib.sap_dev_lu_df_trace(buf.ctypes.data_as(C.POINTER(C.c_ulonglong)), cap)
     t = buf[: REC * cnt].reshape(cnt, REC).astype(np.int64)

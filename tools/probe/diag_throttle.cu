@@ -74,6 +74,14 @@ __global__ void __launch_bounds__(256, 1) k_probe(int mode, int nchain, int burs
         __syncthreads();
         if (mode == 2 && threadIdx.x >= 32) burst(burst_n);
         if (mode == 2) __syncthreads();
+        if (mode == 3) {  // ~72 KB of other code through the instruction caches first (panel_diag<32, false>)
+            if (threadIdx.x >= 32 && threadIdx.x < 64)
+                panel_diag<32, false>(smem + 32 * pld, pld, s_ut, s_rcp, 31, 1e-10, &s_b);
+            __syncthreads();
+            for (int i = threadIdx.x; i < 32 * pld; i += 256)
+                smem[i] = (i % pld == i / pld) ? 40.0 + call : 0.01 * ((i * 7 + call) % 13 - 6);
+            __syncthreads();
+        }
         if (threadIdx.x < 32) {
             const long long t0 = clock64();
             panel_diag<32, true>(smem, pld, s_ut, s_rcp, 32, 1e-10, &s_b);
@@ -119,6 +127,7 @@ int main() {
     run("1 CTA, alone", 0, 1, 1, bn);
     run("1 CTA, beside DFMA burst", 1, 1, 1, bn);
     run("1 CTA, after DFMA burst", 2, 1, 1, bn);
+    run("1 CTA, after 72 KB of other code", 3, 1, 1, bn);
     run("50 CTAs, beside DFMA burst", 1, 50, 50, bn);
     run("50 CTAs, beside burst, 98 SMs DMMA", 1, 50, nsm, bn);
     run("50 CTAs, alone, 98 SMs DMMA", 0, 50, nsm, bn);
