@@ -87,8 +87,12 @@ __global__ void __launch_bounds__(256, 1) k_probe(int mode, int nchain, int burs
             panel_diag<32, true>(smem, pld, s_ut, s_rcp, 32, 1e-10, &s_b);
             __syncwarp();
             if (threadIdx.x == 0) out[(size_t)slot * kCalls + call] = clock64() - t0;
-        } else if (mode == 1) {
-            burst(burst_n);
+        } else if (mode == 1 || (mode == 4 && (threadIdx.x >> 5) % 4 != 0)) {
+            burst(burst_n);  // mode 4: not on warp 0's SM sub-partition (warps 4, 8, ...)
+        } else if (mode == 5 || (mode == 6 && (threadIdx.x >> 5) % 4 != 0)) {
+            double a = threadIdx.x, b = 1.0, c0 = 0, c1 = 0;  // DMMA (mode 6: off warp 0's sub-partition)
+            for (int r = 0; r < burst_n; ++r) dmma_m8n8k4(c0, c1, a, b, c0, c1);
+            if (c0 == 12345.0) g_sink = c1;
         }
         __syncthreads();
     }
@@ -128,6 +132,9 @@ int main() {
     run("1 CTA, beside DFMA burst", 1, 1, 1, bn);
     run("1 CTA, after DFMA burst", 2, 1, 1, bn);
     run("1 CTA, after 72 KB of other code", 3, 1, 1, bn);
+    run("1 CTA, beside DFMA burst, warp 4 idle", 4, 1, 1, bn);
+    run("1 CTA, beside DMMA burst", 5, 1, 1, bn);
+    run("1 CTA, beside DMMA burst, warp 4 idle", 6, 1, 1, bn);
     run("50 CTAs, beside DFMA burst", 1, 50, 50, bn);
     run("50 CTAs, beside burst, 98 SMs DMMA", 1, 50, nsm, bn);
     run("50 CTAs, alone, 98 SMs DMMA", 0, 50, nsm, bn);
