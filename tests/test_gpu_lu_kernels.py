@@ -58,3 +58,37 @@ def test_dataflow_lu_is_bitwise_the_single_cta_lu(sap, ci):
                 assert np.array_equal(a[key], other[key])
             else:
                 assert a[key] == other[key], key
+
+
+SCHEDULES = [  # (job owners, strips per worker item): the dataflow kernel's schedule knobs (lu.cu DfArgs)
+    (0, 3), (1, 1), (1, 2), (1, 3), (0, 1),
+]
+
+
+@pytest.mark.parametrize("case", [(40000, 200, 1.0, 10, True, False), (40000, 224, 0.5, 8, False, True),
+                                  (30000, 300, 1.0, 5, True, False)])
+def test_dataflow_schedules_are_bitwise_equal(sap, case):
+    """The dataflow kernel's work split (chain items on job-owner CTAs or the shared queue; 1-3 strips per worker
+    item) changes only who computes what and when, never an element's operations: factors, boosts and reduced
+    blocks are bitwise the same for every schedule."""
+    from paper_1509_07919_b200 import _lib
+    lib = _lib.load()
+    ref = None
+    try:
+        for owners, grp in SCHEDULES:
+            lib.sap_dev_lu_df_owners(owners)
+            lib.sap_dev_lu_df_group(grp)
+            out = _factors(sap, case, 2)
+            if ref is None:
+                ref = out
+                continue
+            for key in ref:
+                if key in ("lu", "ul"):
+                    assert np.array_equal(ref[key][0], out[key][0]) and np.array_equal(ref[key][1], out[key][1]), key
+                elif key == "rbar":
+                    assert np.array_equal(ref[key], out[key])
+                else:
+                    assert ref[key] == out[key], key
+    finally:
+        lib.sap_dev_lu_df_owners(1)
+        lib.sap_dev_lu_df_group(0)

@@ -56,6 +56,18 @@ __global__ void __launch_bounds__(256, 1) k_probe(int mode, int nchain, int burs
             slot = s_slot;
         }
     }
+    if (dmma && mode == 7) {  // other SMs stream a large code footprint (panel_diag<32, false>, ~72 KB) until done
+        unsigned long long t0, t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        for (int i = threadIdx.x; i < 32 * pld; i += 256) smem[i] = (i % pld == i / pld) ? 40.0 : 0.001;
+        __syncthreads();
+        do {
+            if (threadIdx.x < 32) panel_diag<32, false>(smem, pld, s_ut, s_rcp, 31, 1e-10, &s_b);
+            __syncthreads();
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        } while (*(volatile int*)flag < nchain && t1 - t0 < 3000000000ull);
+        return;
+    }
     if (dmma) {  // worker SM: DMMA until the chains are done
         double a = threadIdx.x, b = 1.0, c0 = 0, c1 = 0;
         unsigned long long t0, t1;
@@ -135,6 +147,7 @@ int main() {
     run("1 CTA, beside DFMA burst, warp 4 idle", 4, 1, 1, bn);
     run("1 CTA, beside DMMA burst", 5, 1, 1, bn);
     run("1 CTA, beside DMMA burst, warp 4 idle", 6, 1, 1, bn);
+    run("50 CTAs alone, 98 SMs big code", 7, 50, nsm, bn);
     run("50 CTAs, beside DFMA burst", 1, 50, 50, bn);
     run("50 CTAs, beside burst, 98 SMs DMMA", 1, 50, nsm, bn);
     run("50 CTAs, alone, 98 SMs DMMA", 0, 50, nsm, bn);

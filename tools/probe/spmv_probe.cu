@@ -78,6 +78,33 @@ __global__ void __launch_bounds__(256) v2(const double* __restrict__ a, int n, i
     }
 }
 
+// V3: the CTA's 8 warps (rows rb .. rb + 255) walk one common column range in lock-step (a barrier every SYNC
+// columns), each warp active on its own window, so at any time the CTA reads ~2 KB contiguous of one column
+// block instead of 8 scattered 256-byte pieces (same per-row order)
+template <int SYNC>
+__global__ void __launch_bounds__(256) v3(const double* __restrict__ a, int n, int k, const double* __restrict__ x,
+                                          double* __restrict__ y) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long ld = 2LL * k;
+    for (int rb = blockIdx.x * 256; rb < n; rb += gridDim.x * 256) {
+        const int r0 = rb + 32 * warp, i = r0 + lane;
+        const int clo = max(r0 - k, 0), chi = min(r0 + 31 + k, n - 1);
+        const int blo = max(rb - k, 0), bhi = min(rb + 255 + k, n - 1);
+        double acc = 0.0;
+        for (int j0 = blo; j0 <= bhi; j0 += SYNC) {
+            const int ja = max(j0, clo), jb = min(j0 + SYNC - 1, chi);
+            const double* col = a + (long long)ja * ld + i + k;
+#pragma unroll 8
+            for (int j = ja; j <= jb; ++j, col += ld) {
+                const double xv = __ldg(x + j);
+                if (i < n && i - j <= k && j - i <= k) acc = fma(*col, xv, acc);
+            }
+            __syncthreads();
+        }
+        if (i < n) y[i] = acc;
+    }
+}
+
 int main() {
     const int n = 200000, k = 200;
     const size_t w = 2 * k + 1, total = (size_t)n * w;
@@ -123,6 +150,9 @@ int main() {
     timeit("v1 batch 32", [&] { v1<32><<<g(warps, 8), 256>>>(a, n, k, x, y1); });
     timeit("v2 two row groups", [&] { v2<<<g((n + 63) / 64, 8), 256>>>(a, n, k, x, y1); });
     timeit("v0 128-thread blocks", [&] { v0<<<g(warps, 4), 128>>>(a, n, k, x, y1); });
+    timeit("v3 lock-step, sync 16", [&] { v3<16><<<g(warps, 8), 256>>>(a, n, k, x, y1); });
+    timeit("v3 lock-step, sync 32", [&] { v3<32><<<g(warps, 8), 256>>>(a, n, k, x, y1); });
+    timeit("v3 lock-step, sync 64", [&] { v3<64><<<g(warps, 8), 256>>>(a, n, k, x, y1); });
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
