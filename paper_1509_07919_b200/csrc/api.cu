@@ -1816,8 +1816,13 @@ sap_status sap_solve(sap_handle* h, const double* b, double* x, int on_device, s
                 SAP_CUDA(cudaMemcpyAsync(out, in, sizeof(double) * (size_t)op_n(h), cudaMemcpyDeviceToDevice,
                                          h->stream));
         };
+        DeviceOp2 A2;  // banded operator on one GPU: A r_j and the true residual's A x in one band read
+        if (!h->dist && !h->csr)
+            A2 = [h](const double* i0, double* o0, const double* i1, double* o1) {
+                launch_band_spmv2(h->band_ptr, h->n, h->k, i0, o0, i1, o1, h->stream);
+            };
         SAP_CUDA(cudaEventRecord(h->ev[6], s));
-        const KrylovResult r = h->krylov.run(A, M, db, dx, n, kc, s);
+        const KrylovResult r = h->krylov.run(A, M, db, dx, n, kc, s, A2);
         SAP_CUDA(cudaEventRecord(h->ev[7], s));
         if (!on_device && n) SAP_CUDA(cudaMemcpyAsync(x, dx, bytes, cudaMemcpyDeviceToHost, s));
         SAP_CUDA(cudaStreamSynchronize(s));

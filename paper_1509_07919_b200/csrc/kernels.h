@@ -168,6 +168,9 @@ void launch_boosted_diag(const double* band, int n, int k, const double* scale, 
 // ---- operators (spmv.cu) ----
 // y = A x on the band; if b != nullptr also y = b - A x.
 void launch_band_spmv(const double* band, int n, int k, const double* x, double* y, const double* b, cudaStream_t s);
+// y0 = A x0 and y1 = A x1 in one read of the band (each bitwise launch_band_spmv's)
+void launch_band_spmv2(const double* band, int n, int k, const double* x0, double* y0, const double* x1, double* y1,
+                       cudaStream_t s);
 // y[i - r0] = sum_j A(i, j) x[j], rows [r0, r1) of a band with n columns (x indexed like the band's columns).
 void launch_band_spmv_rows(const double* band, int n, int k, int r0, int r1, const double* x, double* y, cudaStream_t s);
 // w x w row-major GEMV: mode 0: y = u - A v;  mode 1: y -= A v.

@@ -183,7 +183,7 @@ bool KrylovSolver::nonfinite(const double* v) {
 }
 
 KrylovResult KrylovSolver::run(const DeviceOp& A, const DeviceOp& M, const double* b, double* x, int n,
-                               const KrylovConfig& cfg, cudaStream_t s) {
+                               const KrylovConfig& cfg, cudaStream_t s, const DeviceOp2& A2) {
     s_ = s;
     syncs_ = 0;
     reduce_ = cfg.reduce;
@@ -195,11 +195,11 @@ KrylovResult KrylovSolver::run(const DeviceOp& A, const DeviceOp& M, const doubl
         if (cfg.ell > kMaxEll) throw InvalidArgument("solve_krylov: ell above the supported maximum of 8");
     }
     ensure(n, method == 0 ? cfg.ell : 1);
-    return method == 0 ? bicgstab(A, M, b, x, cfg) : cg(A, M, b, x, cfg);
+    return method == 0 ? bicgstab(A, M, b, x, cfg, A2) : cg(A, M, b, x, cfg);
 }
 
 KrylovResult KrylovSolver::bicgstab(const DeviceOp& A, const DeviceOp& M, const double* b, double* x,
-                                    const KrylovConfig& cfg) {
+                                    const KrylovConfig& cfg, const DeviceOp2& A2) {
     const int n = n_, ell = cfg.ell;
     const int G = vgrid(n);
     KrylovResult st;
@@ -238,8 +238,10 @@ KrylovResult KrylovSolver::bicgstab(const DeviceOp& A, const DeviceOp& M, const 
     // true_residual (krylov.hpp:62-72): ||b - A x|| -- A x into scratch, then the residual's squared norm in
     // the same one-sync reduction as the dot products the next step needs (each value bitwise the separate
     // k_xpay + k_dot of round 1)
-    auto tres = [&](const double* xv, std::vector<DotReq> more, bool flag, std::vector<double>& extra) -> double {
-        A(xv, scratch_);
+    // (with A x already in scratch_ when have_ax: the fused A2 pass below)
+    auto tres = [&](const double* xv, std::vector<DotReq> more, bool flag, std::vector<double>& extra,
+                    bool have_ax = false) -> double {
+        if (!have_ax) A(xv, scratch_);
         more.insert(more.begin(), DotReq{b, scratch_, 1});
         std::vector<double> v = dots(more, flag);
         extra.assign(v.begin() + 1, v.end());
@@ -306,10 +308,20 @@ KrylovResult KrylovSolver::bicgstab(const DeviceOp& A, const DeviceOp& M, const 
             alpha = rho0 / g;
             k_r_update<<<G, 256, 0, s_>>>(vs, j, alpha, n);
             SAP_LAUNCHED();
-            apply_hat(r_[j], r_[j + 1]);
-            SAP_CUDA(cudaMemsetAsync(dflag_, 0, sizeof(int), s_));
-            k_axpy_check<<<G, 256, 0, s_>>>(x, alpha, u_[0], n, dflag_);
-            SAP_LAUNCHED();
+            if (A2) {
+                // x += alpha u_0 does not read r_j or r_{j+1}: update x first, then A r_j and the true
+                // residual's A x in one pass over the operator (each product bitwise its own A call)
+                SAP_CUDA(cudaMemsetAsync(dflag_, 0, sizeof(int), s_));
+                k_axpy_check<<<G, 256, 0, s_>>>(x, alpha, u_[0], n, dflag_);
+                SAP_LAUNCHED();
+                A2(r_[j], tmp_, x, scratch_);
+                M(tmp_, r_[j + 1]);
+            } else {
+                apply_hat(r_[j], r_[j + 1]);
+                SAP_CUDA(cudaMemsetAsync(dflag_, 0, sizeof(int), s_));
+                k_axpy_check<<<G, 256, 0, s_>>>(x, alpha, u_[0], n, dflag_);
+                SAP_LAUNCHED();
+            }
             // with the residual: the next step's rho1 = (r_{j+1}, r~), or after the last step the first Gram
             // entries (r_1, r_1), (r_1, r_0) of the MGS trial / first MGS column (r_0..r_l are final here)
             std::vector<DotReq> ahead;
@@ -319,7 +331,7 @@ KrylovResult KrylovSolver::bicgstab(const DeviceOp& A, const DeviceOp& M, const 
                 ahead.push_back(DotReq{r_[1], r_[1], 0});
                 ahead.push_back(DotReq{r_[1], r_[0], 0});
             }
-            tr = tres(x, ahead, true, extra);
+            tr = tres(x, ahead, true, extra, (bool)A2);
             if (j + 1 < ell) {
                 rho_next = extra[0];
                 have_rho = true;

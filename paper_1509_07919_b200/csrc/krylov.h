@@ -14,6 +14,8 @@ namespace sapgpu {
 
 // Device LinearOp: out = Op(in), both device pointers of length n.
 using DeviceOp = std::function<void(const double* in, double* out)>;
+// Optional fused pair: out0 = Op(in0), out1 = Op(in1) in one pass over the operator (empty = two Op calls).
+using DeviceOp2 = std::function<void(const double* in0, double* out0, const double* in1, double* out1)>;
 
 struct KrylovResult {
     double iterations = 0.0;
@@ -51,7 +53,7 @@ public:
 
     // run_krylov: b, x device pointers; x is overwritten (x0 = 0).
     KrylovResult run(const DeviceOp& A, const DeviceOp& M, const double* b, double* x, int n,
-                     const KrylovConfig& cfg, cudaStream_t s);
+                     const KrylovConfig& cfg, cudaStream_t s, const DeviceOp2& A2 = nullptr);
     long long host_syncs() const { return syncs_; }  // stream synchronisations of the last run
 
 private:
@@ -66,7 +68,8 @@ private:
     std::vector<double> dots(const std::vector<DotReq>& reqs, bool flag_too = false);
     bool any_flag(int local);
     bool nonfinite(const double* v);
-    KrylovResult bicgstab(const DeviceOp& A, const DeviceOp& M, const double* b, double* x, const KrylovConfig& cfg);
+    KrylovResult bicgstab(const DeviceOp& A, const DeviceOp& M, const double* b, double* x, const KrylovConfig& cfg,
+                          const DeviceOp2& A2);
     KrylovResult cg(const DeviceOp& A, const DeviceOp& M, const double* b, double* x, const KrylovConfig& cfg);
 
     int n_ = 0, ell_ = 0;

@@ -42,6 +42,45 @@ void launch_band_spmv(const double* band, int n, int k, const double* x, double*
     SAP_LAUNCHED();
 }
 
+// Two products over one read of the band: y0 = A x0, y1 = A x1. BiCGStab's step applies A to the updated
+// residual and (for the true residual, krylov.hpp:62-72) to the updated iterate back to back; each row's
+// sum is formed exactly as in k_band_spmv (ascending columns, FMA from zero), so both are bitwise its.
+__global__ void __launch_bounds__(256)
+    k_band_spmv2(const double* __restrict__ a, int n, int k, const double* __restrict__ x0, double* __restrict__ y0,
+                 const double* __restrict__ x1, double* __restrict__ y1) {
+    const int lane = threadIdx.x & 31;
+    const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const long long ld = 2LL * k;
+    for (int r0 = warp_global * 32; r0 < n; r0 += nwarps * 32) {
+        const int i = r0 + lane;
+        const int clo = max(r0 - k, 0), chi = min(r0 + 31 + k, n - 1);
+        double acc0 = 0.0, acc1 = 0.0;
+        const double* col = a + (long long)clo * ld + i + k;
+#pragma unroll 8
+        for (int j = clo; j <= chi; ++j, col += ld) {
+            const double xv0 = __ldg(x0 + j), xv1 = __ldg(x1 + j);
+            if (i < n && i - j <= k && j - i <= k) {
+                const double av = *col;
+                acc0 = fma(av, xv0, acc0);
+                acc1 = fma(av, xv1, acc1);
+            }
+        }
+        if (i < n) {
+            y0[i] = acc0;
+            y1[i] = acc1;
+        }
+    }
+}
+
+void launch_band_spmv2(const double* band, int n, int k, const double* x0, double* y0, const double* x1, double* y1,
+                       cudaStream_t s) {
+    const int warps = ceil_div(n, 32);
+    const int grid = std::min(ceil_div(warps, 8), 148 * 64);
+    k_band_spmv2<<<grid, 256, 0, s>>>(band, n, k, x0, y0, x1, y1);
+    SAP_LAUNCHED();
+}
+
 __global__ void __launch_bounds__(256)
     k_band_spmv_rows(const double* __restrict__ a, int n, int k, int rbeg, int rend, const double* __restrict__ x,
                      double* __restrict__ y) {
