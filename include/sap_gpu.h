@@ -101,6 +101,13 @@ typedef struct sap_options {
      * most 0.7 x SMs jobs of at least 512 rows and for K in (224, 512], else one CTA per job), 1 = one CTA per job,
      * 2 = the dataflow kernel wherever it supports the bandwidth (K in [64, 512]). Default 0. */
     int lu_kernel;
+    /* SaP-C apply, first block solve g = D^{-1} r (not a reference option: the interfaces read only g's first
+     * and last w rows of every block): 0 = automatic (the last rows from the LU sweeps with the backward sweep
+     * stopped there, the first rows from UL sweeps over the UL factors with the top-down sweep stopped there,
+     * both at once -- when no LU or UL pivot was boosted and both stores' chunk triangles are well
+     * conditioned; equal to the LU solve's rows up to rounding), 1 = the full LU block solve
+     * (spike.hpp:323-329). Default 0. */
+    int tip_solve;
 } sap_options;
 
 /* PipelineReport T_* stage timings (pipeline.hpp:37-52), in seconds,
@@ -130,6 +137,8 @@ typedef struct sap_report {
     /* host synchronisations of the last sap_solve (each scalar the host recurrences need costs one; the dot
      * products a step needs next ride with its true residual, MGS runs on device scalars) */
     long long krylov_host_syncs;
+    /* 1 if the last setup's SaP-C applies form g's interface rows from LU + UL tip sweeps (tip_solve) */
+    int ul_tip_sweeps;
 } sap_report;
 
 /* SolveStats (krylov.hpp:35-41). history: caller-owned buffer of

@@ -16,7 +16,7 @@ class sap_options(C.Structure):
     _fields_ = [("p", C.c_int), ("precond", C.c_int), ("boost_eps", C.c_double), ("method", C.c_int),
                 ("ell", C.c_int), ("rel_tol", C.c_double), ("abs_tol", C.c_double), ("max_iterations", C.c_int),
                 ("mixed_precision", C.c_int), ("caller_asserts_spd", C.c_int), ("device", C.c_int),
-                ("triangle_solve", C.c_int), ("lu_kernel", C.c_int)]
+                ("triangle_solve", C.c_int), ("lu_kernel", C.c_int), ("tip_solve", C.c_int)]
 
 
 class sap_report(C.Structure):
@@ -26,7 +26,7 @@ class sap_report(C.Structure):
                 ("total_rbar_boosts", C.c_int), ("kernel_launches", C.c_longlong),
                 ("t_factor_kernel", C.c_double), ("factor_flops", C.c_double), ("chunk_condition", C.c_double),
                 ("sweep_substitution", C.c_int), ("t_drop", C.c_double), ("t_asmbl", C.c_double),
-                ("krylov_host_syncs", C.c_longlong)]
+                ("krylov_host_syncs", C.c_longlong), ("ul_tip_sweeps", C.c_int)]
 
 
 class sap_solve_stats(C.Structure):

@@ -111,6 +111,15 @@ struct sap_handle {
     DevBuf<int> op_nonfinite;            // any non-finite entry in the banded operator (single-GPU setup)
     bool op_finite = false;              // checked: the zero-guess shortcut of the Krylov solver applies
     SweepPlan<double> lplan, rplan;      // block sweeps over LU and over the reduced blocks
+    // SaP-C apply, first block solve: only the rows the interfaces read are needed -- each block's last w rows
+    // from an LU sweep pair whose second sweep stops there, its first w rows from a UL sweep pair (uplan over the
+    // UL store) on tside, both at once (sap_options::tip_solve; used when no pivot was boosted and the chunk
+    // triangles of both stores are well conditioned)
+    bool ul_tips = false;
+    SweepPlan<double> uplan;
+    DevBuf<double> udinv, scratch_gu;
+    cudaStream_t tside = nullptr;
+    cudaEvent_t tev[2] = {};
     // mixed precision (KrylovOptions::mixed_precision, build_precond_op<float>): the preconditioner is
     // applied in FP32 from FP32 copies of the factors, tips and reduced factors
     bool mixed = false;
@@ -229,6 +238,15 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
 // growth at low diagonal dominance) solve them by substitution (k_sweep_tma<SUBST>); well conditioned
 // factors keep the chunk-inverse product. sap_options::triangle_solve (1 inverse, 2 substitution) forces it.
 constexpr double kSubstKappa = 1e4;
+// The LU and UL tip sweeps of a SaP-C apply run side by side, one CTA per block each: they pay only while both
+// launches fit on the SMs at once (with more blocks the sweeps run in waves and the pair costs about a full
+// solve; config 5, P = 512, keeps the LU solve).
+bool tip_sweeps_fit(int blocks) {
+    int dev = 0, nsm = 0;
+    SAP_CUDA(cudaGetDevice(&dev));
+    SAP_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    return 2 * blocks <= nsm;
+}
 void choose_triangle_solve(sap_handle* h) {
     int nf = 1;
     if (!h->dist && h->op_nonfinite.get())
@@ -369,6 +387,23 @@ void apply_m(sap_handle* h, const double* in, double* out) {
     }
     double* g = h->scratch_g.get();
     SAP_CUDA(cudaMemcpyAsync(g, in, bytes, cudaMemcpyDeviceToDevice, s));
+    if (h->ul_tips) {
+        // the interfaces read g's last w rows of every block (LU sweeps, the backward one stopped there) and
+        // its first w rows (UL sweeps on tside, the top-down one stopped there), computed side by side
+        double* gu = h->scratch_gu.get();
+        SAP_CUDA(cudaMemcpyAsync(gu, in, bytes, cudaMemcpyDeviceToDevice, s));
+        SAP_CUDA(cudaEventRecord(h->tev[0], s));
+        SAP_CUDA(cudaStreamWaitEvent(h->tside, h->tev[0], 0));
+        launch_block_solve<double>(h->uplan, gu, h->tside, k);
+        SAP_CUDA(cudaEventRecord(h->tev[1], h->tside));
+        if (out != in) SAP_CUDA(cudaMemcpyAsync(out, in, bytes, cudaMemcpyDeviceToDevice, s));
+        launch_block_solve<double>(h->lplan, g, s, k);
+        SAP_CUDA(cudaStreamWaitEvent(s, h->tev[1], 0));
+        launch_interfaces<double>(g, h->d_offsets.get(), h->rplan, p - 1, k, h->wt.get(), h->vb.get(),
+                                  h->bblk.get(), h->cblk.get(), h->xt.get(), h->xb.get(), out, false, false, s, gu);
+        launch_block_solve<double>(h->lplan, out, s);
+        return;
+    }
     if (out != in) SAP_CUDA(cudaMemcpyAsync(out, in, bytes, cudaMemcpyDeviceToDevice, s));
     launch_block_solve<double>(h->lplan, g, s);
     launch_interfaces<double>(g, h->d_offsets.get(), h->rplan, p - 1, k, h->wt.get(), h->vb.get(), h->bblk.get(),
@@ -609,6 +644,7 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
     h->mixed = false;
     h->f32fac = false;
     h->ready = false;
+    h->ul_tips = false;
     h->kind = h->opt.precond;
     require(h->kind >= 0 && h->kind <= 3, "sap_setup_banded: unknown preconditioner kind");
     const bool blocks = h->kind == SAP_PRECOND_COUPLED || h->kind == SAP_PRECOND_DECOUPLED;
@@ -734,8 +770,8 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
     h->jobs.alloc(njobs);
     lu_df_clear_error(lu_scratch(h, njobs, m_max), s);
     SAP_CUDA(cudaMemcpyAsync(h->jobs.get(), jobs.data(), sizeof(FactorJob) * njobs, cudaMemcpyHostToDevice, s));
-    h->kappa.alloc(2);
-    SAP_CUDA(cudaMemsetAsync(h->kappa.get(), 0, 2 * sizeof(unsigned long long), s));
+    h->kappa.alloc(3);
+    SAP_CUDA(cudaMemsetAsync(h->kappa.get(), 0, 3 * sizeof(unsigned long long), s));
     h->op_nonfinite.alloc(1);
     SAP_CUDA(cudaMemsetAsync(h->op_nonfinite.get(), 0, sizeof(int), s));
     if (h->ts) {
@@ -879,6 +915,21 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
             SAP_CUDA(cudaEventRecord(h->sev[0], s));
             SAP_CUDA(cudaStreamWaitEvent(h->side, h->sev[0], 0));
             launch_chunk_inverses(lp, h->side);
+            SweepPlan<double>& up = h->uplan;
+            up = SweepPlan<double>{};
+            if (!h->ts && !h->opt.mixed_precision && h->opt.tip_solve != 1 && lp.tma && lp.tr == 32 &&
+                tip_sweeps_fit(p)) {
+                up.f = h->ul.get();
+                up.st = h->fst;
+                up.offs = h->d_offsets.get();
+                up.p = p;
+                up.k = k;
+                up.ul = true;
+                h->udinv.alloc(std::max<size_t>(sweep_dinv_elems(up), 1));
+                plan_sweeps(up, h->udinv.get());
+                up.kappa = h->kappa.get() + 2;
+                if (up.tma && up.tr == 32) launch_chunk_inverses(up, h->side);
+            }
             SAP_CUDA(cudaEventRecord(h->sev[1], h->side));
         } else {
             launch_chunk_inverses(lp, s);
@@ -1048,7 +1099,21 @@ void setup_banded(sap_handle* h, int n, int k, const double* band, int on_device
         }
         for (int t = 0; t < ni; ++t)
             if (nf[2 * ni + t]) throw PreconditionerFailure("reduced interface block " + std::to_string(t) + " is not finite");
+        // first block solve of the apply from the LU (last rows) and UL (first rows) sweeps: equal to the LU
+        // solve's rows up to rounding when neither factorization boosted a pivot (a boosted LU and UL are
+        // different perturbations of A_b) and both stores' chunk triangles are well conditioned
+        const SweepPlan<double>& up = h->uplan;
+        if (up.ul && up.tma && up.tr == 32 && !h->lplan.subst && !h->ts && !h->mixed && h->rep.total_boosts == 0 &&
+            h->rep.total_boosts_ul == 0 && h->opt.tip_solve != 1 && h->opt.triangle_solve != 2) {
+            unsigned long long kb = 0;
+            SAP_CUDA(cudaMemcpy(&kb, h->kappa.get() + 2, sizeof(kb), cudaMemcpyDeviceToHost));
+            double kap;
+            std::memcpy(&kap, &kb, sizeof(kap));
+            h->ul_tips = kap <= kSubstKappa;
+            if (h->ul_tips) h->scratch_gu.alloc(n);
+        }
     }
+    h->rep.ul_tip_sweeps = h->ul_tips ? 1 : 0;
     h->ready = true;
 }
 
@@ -1110,6 +1175,26 @@ void apply_m_dist(sap_handle* h, const double* in, double* out) {
     }
     double* g = h->scratch_g.get() + k;  // [left halo w | own n | right halo w]
     SAP_CUDA(cudaMemcpyAsync(g, in, bytes, cudaMemcpyDeviceToDevice, s));
+    if (h->ul_tips) {
+        // g's last rows of every block from the LU tip sweeps, the first rows from the UL ones (gu, same
+        // halo layout); this rank's first w rows go left from gu, its last w rows right from g, and the halos
+        // land where the interfaces read them (left: bottom rows in g, right: top rows in gu)
+        double* gu = h->scratch_gu.get() + k;
+        SAP_CUDA(cudaMemcpyAsync(gu, in, bytes, cudaMemcpyDeviceToDevice, s));
+        SAP_CUDA(cudaEventRecord(h->tev[0], s));
+        SAP_CUDA(cudaStreamWaitEvent(h->tside, h->tev[0], 0));
+        launch_block_solve<double>(h->uplan, gu, h->tside, k);
+        SAP_CUDA(cudaEventRecord(h->tev[1], h->tside));
+        if (out != in) SAP_CUDA(cudaMemcpyAsync(out, in, bytes, cudaMemcpyDeviceToDevice, s));
+        launch_block_solve<double>(h->lplan, g, s, k);
+        SAP_CUDA(cudaStreamWaitEvent(s, h->tev[1], 0));
+        comm_exchange(h, gu, g + n - k, g - k, gu + n, k);
+        launch_interfaces<double>(g, h->d_ioffs.get(), h->rplan, h->ni_tot, k, h->wt.get(), h->vb.get(),
+                                  h->bblk.get(), h->cblk.get(), h->xt.get(), h->xb.get(), out, h->has_left,
+                                  h->has_right, s, gu);
+        launch_block_solve<double>(h->lplan, out, s);
+        return;
+    }
     if (out != in) SAP_CUDA(cudaMemcpyAsync(out, in, bytes, cudaMemcpyDeviceToDevice, s));
     launch_block_solve<double>(h->lplan, g, s);
     comm_exchange(h, g, g + n - k, g - k, g + n, k);
@@ -1135,6 +1220,7 @@ void setup_banded_dist(sap_handle* h, int n, int k, int row_lo, int row_hi, cons
         throw InvalidArgument("sap_setup_banded_dist: mixed_precision is not supported by this build");
     const cudaStream_t s = h->stream;
     h->ready = false;
+    h->ul_tips = false;
     h->kind = h->opt.precond;
     require(h->kind == SAP_PRECOND_COUPLED || h->kind == SAP_PRECOND_DECOUPLED || h->kind == SAP_PRECOND_NONE,
             "sap_setup_banded_dist: only the coupled, decoupled and none preconditioners are distributed");
@@ -1233,8 +1319,8 @@ void setup_banded_dist(sap_handle* h, int n, int k, int row_lo, int row_hi, cons
     h->jobs.alloc(njobs);
     lu_df_clear_error(lu_scratch(h, njobs, m_max), s);
     SAP_CUDA(cudaMemcpyAsync(h->jobs.get(), jobs.data(), sizeof(FactorJob) * njobs, cudaMemcpyHostToDevice, s));
-    h->kappa.alloc(2);
-    SAP_CUDA(cudaMemsetAsync(h->kappa.get(), 0, 2 * sizeof(unsigned long long), s));
+    h->kappa.alloc(3);
+    SAP_CUDA(cudaMemsetAsync(h->kappa.get(), 0, 3 * sizeof(unsigned long long), s));
     launch_block_norms(h->band_ptr, m_max, k, h->d_boffs.get(), pl, nullptr, h->norms.get(), s);
     if (from_src)
         launch_zero_pad(k, h->d_boffs.get(), pl, h->fst, h->lu.get(), h->coupled ? h->ul.get() : nullptr, s);
@@ -1256,6 +1342,21 @@ void setup_banded_dist(sap_handle* h, int n, int k, int row_lo, int row_hi, cons
         plan_sweeps(lp, h->dinv.get());
         lp.kappa = h->kappa.get();
         launch_chunk_inverses(lp, s);
+        // UL tip sweeps (sap_options::tip_solve), as in setup_banded; the choice is made over all ranks below
+        SweepPlan<double>& up = h->uplan;
+        up = SweepPlan<double>{};
+        if (h->coupled && h->opt.tip_solve != 1 && lp.tma && lp.tr == 32 && tip_sweeps_fit(G.p)) {
+            up.f = h->ul.get();
+            up.st = h->fst;
+            up.offs = h->d_offsets.get();
+            up.p = pl;
+            up.k = k;
+            up.ul = true;
+            h->udinv.alloc(std::max<size_t>(sweep_dinv_elems(up), 1));
+            plan_sweeps(up, h->udinv.get());
+            up.kappa = h->kappa.get() + 2;
+            if (up.tma && up.tr == 32) launch_chunk_inverses(up, s);
+        }
     }
     SAP_CUDA(cudaEventRecord(h->ev[2], s));
     for (int b = 0; b < pl; ++b) {
@@ -1369,7 +1470,20 @@ void setup_banded_dist(sap_handle* h, int n, int k, int row_lo, int row_hi, cons
     }
     // global failure flags and boost counts, summed over ranks so every rank raises the same error
     const int nig = P - 1;
-    std::vector<double> gl(3 * (size_t)nig + 3, 0.0);
+    std::vector<double> gl(3 * (size_t)nig + 4, 0.0);
+    {  // UL tip sweeps: vetoed on every rank if any rank cannot use them (the single-GPU choice, made globally)
+        bool ok = h->uplan.ul && h->uplan.tma && h->uplan.tr == 32 && !h->lplan.subst &&
+                  h->opt.triangle_solve != 2;
+        if (ok) {
+            unsigned long long kb = 0;
+            SAP_CUDA(cudaStreamSynchronize(s));
+            SAP_CUDA(cudaMemcpy(&kb, h->kappa.get() + 2, sizeof(kb), cudaMemcpyDeviceToHost));
+            double kap;
+            std::memcpy(&kap, &kb, sizeof(kap));
+            ok = kap <= kSubstKappa;
+        }
+        gl[3 * (size_t)nig + 3] = (h->coupled && !ok) ? 1.0 : 0.0;
+    }
     std::vector<int> hb(2 * pl);
     SAP_CUDA(cudaMemcpy(hb.data(), h->boosts.get(), sizeof(int) * 2 * pl, cudaMemcpyDeviceToHost));
     for (int b = 0; b < pl; ++b) {
@@ -1394,6 +1508,12 @@ void setup_banded_dist(sap_handle* h, int n, int k, int row_lo, int row_hi, cons
     h->rep.total_boosts = (int)gl[3 * nig];
     h->rep.total_boosts_ul = (int)gl[3 * nig + 1];
     h->rep.total_rbar_boosts = (int)gl[3 * nig + 2];
+    h->ul_tips = h->coupled && gl[3 * (size_t)nig + 3] == 0.0 && h->rep.total_boosts == 0 && h->rep.total_boosts_ul == 0;
+    if (h->ul_tips) {
+        h->scratch_gu.alloc((size_t)h->n + 2 * k);
+        SAP_CUDA(cudaMemsetAsync(h->scratch_gu.get(), 0, sizeof(double) * ((size_t)h->n + 2 * k), s));
+    }
+    h->rep.ul_tip_sweeps = h->ul_tips ? 1 : 0;
     for (int t = 0; t < nig; ++t) {
         if (gl[2 * t] != 0.0) throw PreconditionerFailure("right spike tip at interface " + std::to_string(t) + " is not finite");
         if (gl[2 * t + 1] != 0.0) throw PreconditionerFailure("left spike tip at interface " + std::to_string(t) + " is not finite");
@@ -1423,6 +1543,7 @@ void sap_options_default(sap_options* o) {
     o->device = 0;
     o->triangle_solve = 0;
     o->lu_kernel = 0;
+    o->tip_solve = 0;
 }
 
 int sap_max_feasible_partitions(int n, int k) {
@@ -1501,6 +1622,8 @@ sap_status sap_create(const sap_options* opts, sap_handle** out) {
             SAP_CUDA(cudaStreamCreateWithPriority(&h->prio, cudaStreamNonBlocking, greatest));
             SAP_CUDA(cudaEventCreateWithFlags(&h->pev, cudaEventDisableTiming));
             for (auto& e : h->sev) SAP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            SAP_CUDA(cudaStreamCreateWithFlags(&h->tside, cudaStreamNonBlocking));
+            for (auto& e : h->tev) SAP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         } catch (...) {
             delete h;
             throw;
@@ -1519,6 +1642,9 @@ void sap_destroy(sap_handle* h) {
         if (e) cudaEventDestroy(e);
     if (h->side) cudaStreamDestroy(h->side);
     if (h->prio) cudaStreamDestroy(h->prio);
+    for (auto& e : h->tev)
+        if (e) cudaEventDestroy(e);
+    if (h->tside) cudaStreamDestroy(h->tside);
     if (h->pev) cudaEventDestroy(h->pev);
     if (h->own_stream) cudaStreamDestroy(h->own_stream);
     for (auto& e : h->cev)

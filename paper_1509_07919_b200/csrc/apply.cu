@@ -89,7 +89,10 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // (L_qq^{-1})(i, j) for dir 0 (unit lower), (U_qq^{-1})(i, j) for dir 1.
 // Rows beyond the block are padded with the identity. One warp per inverse,
 // lane j builds column j by substitution on e_j.
-template <class T, int TR>
+// UL: the chunk triangles of a UL store (A = U'L', U' unit upper, L' lower with the diagonal; the UL
+// job's factors at their original positions): dir 0 (top-down) inverts the lower triangle with its
+// diagonal, dir 1 (bottom-up) the unit upper one; no substitution triangles (UL sweeps use inverses only).
+template <class T, int TR, bool UL = false>
 __global__ void k_chunk_inverses(const T* __restrict__ f0, long long pstride, int pad, const int* __restrict__ offs,
                                  int k, T* __restrict__ dinv, int nch_max, T* __restrict__ tri,
                                  unsigned long long* __restrict__ kappa_bits) {
@@ -113,7 +116,24 @@ __global__ void k_chunk_inverses(const T* __restrict__ f0, long long pstride, in
     }
     __syncthreads();
     const int dir = threadIdx.x >> 5, j = threadIdx.x & 31;
-    if (j < TR) {
+    if (UL && j < TR) {
+        if (dir == 0) {  // lower with diagonal
+            for (int i = 0; i < TR; ++i) X[0][j][i] = T(0);
+            X[0][j][j] = T(1) / blk[j][j];
+            for (int i = j + 1; i < TR; ++i) {
+                T acc = T(0);
+                for (int l = j; l < i; ++l) acc = fma(blk[l][i], X[0][j][l], acc);
+                X[0][j][i] = -acc / blk[i][i];
+            }
+        } else {  // unit upper
+            for (int i = 0; i < TR; ++i) X[1][j][i] = (i == j) ? T(1) : T(0);
+            for (int i = j - 1; i >= 0; --i) {
+                T acc = T(0);
+                for (int l = i + 1; l <= j; ++l) acc = fma(blk[l][i], X[1][j][l], acc);
+                X[1][j][i] = -acc;
+            }
+        }
+    } else if (j < TR) {
         if (dir == 0) {  // unit lower
             for (int i = 0; i < TR; ++i) X[0][j][i] = (i == j) ? T(1) : T(0);
             for (int i = j + 1; i < TR; ++i) {
@@ -137,6 +157,7 @@ __global__ void k_chunk_inverses(const T* __restrict__ f0, long long pstride, in
     for (int idx = threadIdx.x; idx < 2 * TR * TR; idx += blockDim.x) {
         const int d = idx / (TR * TR), r = idx % (TR * TR), jj = r / TR, ii = r % TR;
         out[idx] = X[d][jj][ii];
+        if (UL) continue;
         // the triangle itself (unit lower / upper with diagonal), for the substitution sweeps; the upper
         // triangle's unused strictly-lower slots carry 1/d_ii (tri_rcp_slot) for the quotient
         T v = d == 0 ? (jj < ii ? blk[jj][ii] : (jj == ii ? T(1) : T(0))) : (jj >= ii ? blk[jj][ii] : T(0));
@@ -153,7 +174,8 @@ __global__ void k_chunk_inverses(const T* __restrict__ f0, long long pstride, in
         double rt = 0.0, ri = 0.0;
         if (i < TR)
             for (int jj = 0; jj < TR; ++jj) {
-                const T tv = d == 0 ? (jj < i ? blk[jj][i] : (jj == i ? T(1) : T(0))) : (jj >= i ? blk[jj][i] : T(0));
+                const T tv = UL ? (d == 0 ? (jj <= i ? blk[jj][i] : T(0)) : (jj > i ? blk[jj][i] : (jj == i ? T(1) : T(0))))
+                                : (d == 0 ? (jj < i ? blk[jj][i] : (jj == i ? T(1) : T(0))) : (jj >= i ? blk[jj][i] : T(0)));
                 rt += fabs((double)tv);
                 ri += fabs((double)X[d][jj][i]);
             }
@@ -264,11 +286,16 @@ struct SweepSmem {
 // dominance, max ||T|| ||T^-1|| > 1e4): a product with an explicit inverse is not backward stable there
 // and moves the Krylov iteration counts (measured: config 3 at d = 0.06, 20.25 vs the reference's 1.5);
 // well-conditioned factors keep the 32x32 inverse mat-vec (one dependent step instead of 32).
-template <class T, int TR, int S, bool SUBST>
+// UL: a UL store (A = U'L'): the bottom-up sweep (unit upper U') runs first, then the top-down one (L' with
+// its diagonal); the slabs are the LU sweeps' (strictly upper / strictly lower entries beyond the chunk),
+// only the chunk inverses differ (k_chunk_inverses<UL>).
+// tip_rows > 0: the second sweep stops once the tip_rows rows it reaches first are final (LU: the block's
+// last rows, UL: its first rows) -- the SaP-C apply needs only those rows of its first block solve.
+template <class T, int TR, int S, bool SUBST, bool UL>
 __global__ void __launch_bounds__(kSwThreads, 1)
     k_sweep_tma(const __grid_constant__ CUtensorMap map, const T* __restrict__ dinv, int nch_max,
                 const int* __restrict__ offs, int k, T* __restrict__ xbase, int xw, int slab_cols, int box_c,
-                int nbox, const T* __restrict__ tri, const int* __restrict__ kbs) {
+                int nbox, const T* __restrict__ tri, const int* __restrict__ kbs, int tip_rows) {
     constexpr int SD = SweepSmem<T, TR, S>::SD;
     constexpr int CG = 32 / TR;  // column groups per warp
     constexpr int PF = 6;        // L2 prefetch distance (chunks)
@@ -307,10 +334,16 @@ __global__ void __launch_bounds__(kSwThreads, 1)
     for (int i = tid; i < xw; i += kSwThreads) xs[i] = T(0);
     __syncthreads();
 
-    // g = global chunk sequence number (forward 0..nch-1, backward nch..2nch-1)
+    // g = global chunk sequence number (first sweep 0..nch-1, second nch..; LU: forward first, UL: backward)
+    auto chunk_of = [&](int g, bool& fwd) {
+        const bool first = g < nch;
+        fwd = first != UL;
+        const int q = first ? g : g - nch;
+        return fwd ? q : nch - 1 - q;
+    };
     auto issue = [&](int g) {
-        const bool fwd = g < nch;
-        const int ch = fwd ? g : 2 * nch - 1 - g;
+        bool fwd;
+        const int ch = chunk_of(g, fwd);
         const int i0 = ch * TR;
         const int c0 = fwd ? i0 - k : i0 + TR;
         const int st = g % S;
@@ -329,8 +362,8 @@ __global__ void __launch_bounds__(kSwThreads, 1)
                   bar + st);
     };
     auto prefetch = [&](int g) {
-        const bool fwd = g < nch;
-        const int ch = fwd ? g : 2 * nch - 1 - g;
+        bool fwd;
+        const int ch = chunk_of(g, fwd);
         const int i0 = ch * TR;
         const int c0 = fwd ? i0 - k : i0 + TR;
         const int q0 = fwd ? qf0 : 0, q1 = fwd ? nbox : min(qb1, nbox);
@@ -338,11 +371,15 @@ __global__ void __launch_bounds__(kSwThreads, 1)
     };
 
     for (int dir = 0; dir < 2; ++dir) {
-        const bool fwd = dir == 0;
-        const int gbase = fwd ? 0 : nch;
+        const bool fwd = (dir == 0) != UL;
+        const int gbase = dir == 0 ? 0 : nch;
+        // chunks this sweep finishes (all, or the second sweep's first tip_rows rows)
+        const int nl = (dir == 1 && tip_rows > 0)
+                           ? (fwd ? min(nch, (tip_rows + TR - 1) / TR) : nch - max(m - tip_rows, 0) / TR)
+                           : nch;
         if (producer) {
-            for (int q = 0; q < S - 1 && q < nch; ++q) issue(gbase + q);
-            for (int q = S - 1; q < S - 1 + PF && q < nch; ++q) prefetch(gbase + q);
+            for (int q = 0; q < S - 1 && q < nl; ++q) issue(gbase + q);
+            for (int q = S - 1; q < S - 1 + PF && q < nl; ++q) prefetch(gbase + q);
         }
         T yprev = T(0);  // y of the chunk warp 0 finishes next (warp 0 only)
         if (warp == 0) {
@@ -354,12 +391,12 @@ __global__ void __launch_bounds__(kSwThreads, 1)
 #ifdef SAP_SWEEP_TRACE
         long long acc_wait = 0, acc_p1 = 0, acc_p2 = 0, acc_a = 0, t_loop0 = clock64();
 #endif
-        for (int t = 0; t <= nch; ++t) {
+        for (int t = 0; t <= nl; ++t) {
             const int g = gbase + t;
             const int ch = fwd ? t : nch - 1 - t;   // chunk whose row sums are formed now
             const int pch = fwd ? t - 1 : nch - t;  // chunk finished now by warp 0
             SWT(tw0);
-            if (t < nch) mbar_wait(bar + g % S, (unsigned)((g / S) & 1));
+            if (t < nl) mbar_wait(bar + g % S, (unsigned)((g / S) & 1));
             SWT(tw1);
             __syncthreads();  // A
             SWT(tw2);
@@ -367,9 +404,9 @@ __global__ void __launch_bounds__(kSwThreads, 1)
             acc_wait += tw1 - tw0;
             acc_a += tw2 - tw1;
 #endif
-            if (producer && t + S - 1 < nch) {
+            if (producer && t + S - 1 < nl) {
                 issue(g + S - 1);
-                if (t + S - 1 + PF < nch) prefetch(g + S - 1 + PF);
+                if (t + S - 1 + PF < nl) prefetch(g + S - 1 + PF);
             }
             const T* L = slab + (g % S) * slab_elems;
             const int i0 = ch * TR;
@@ -441,12 +478,12 @@ __global__ void __launch_bounds__(kSwThreads, 1)
                         x[p0 + lane] = xv;
                     }
                 }
-                if (t < nch) {  // y of chunk ch, finished in the next iteration
+                if (t < nl) {  // y of chunk ch, finished in the next iteration
                     const int in = i0 + lane;
                     yprev = (lane < TR && in < m) ? x[in] : T(0);
                     prev_rows = min(TR, m - i0);
                 }
-            } else if (t < nch && warp < kSwWarps - 1) {
+            } else if (t < nl && warp < kSwWarps - 1) {
                 // columns needing only x older than chunk pch (within K_b)
                 const int ca = fwd ? k - kb : TR, cb = fwd ? k - TR : kb;
                 const int cbase = fwd ? i0 - k : i0 + TR;
@@ -470,7 +507,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
             acc_p1 += tw3 - tw2;
 #endif
             // ---- phase 2: the TR columns of chunk pch ----
-            if (t < nch) {
+            if (t < nl) {
                 const int ca = fwd ? max(max(k - TR, 0), k - kb) : 0, cb = fwd ? k : min(TR, kb);
                 const int cbase = fwd ? i0 - k : i0 + TR;
                 if constexpr (TR == 32) {
@@ -707,7 +744,11 @@ template <class T>
 void launch_chunk_inverses(const SweepPlan<T>& pl, cudaStream_t s) {
     if (!pl.tma) return;
     dim3 grid(pl.nch_max, pl.p);
-    if (pl.tr == 32)
+    if (pl.ul && pl.tr != 32) throw InvalidArgument("UL sweeps need 32-row chunks");
+    if (pl.ul)
+        k_chunk_inverses<T, 32, true><<<grid, 64, 0, s>>>(pl.f, pl.st.pstride, pl.st.pad, pl.offs, pl.k, pl.dinv,
+                                                          pl.nch_max, pl.tri, pl.kappa);
+    else if (pl.tr == 32)
         k_chunk_inverses<T, 32><<<grid, 64, 0, s>>>(pl.f, pl.st.pstride, pl.st.pad, pl.offs, pl.k, pl.dinv, pl.nch_max,
                                                     pl.tri, pl.kappa);
     else
@@ -719,12 +760,13 @@ template void launch_chunk_inverses<double>(const SweepPlan<double>&, cudaStream
 template void launch_chunk_inverses<float>(const SweepPlan<float>&, cudaStream_t);
 
 template <class T, int TR, int S>
-static void run_tma(const SweepPlan<T>& pl, T* x, cudaStream_t s) {
+static void run_tma(const SweepPlan<T>& pl, T* x, int tip_rows, cudaStream_t s) {
     const int cols = pl.box_c * pl.nbox;
-    auto kern = pl.subst ? k_sweep_tma<T, TR, S, true> : k_sweep_tma<T, TR, S, false>;
+    auto kern = pl.ul ? k_sweep_tma<T, TR, S, false, true>
+                      : (pl.subst ? k_sweep_tma<T, TR, S, true, false> : k_sweep_tma<T, TR, S, false, false>);
     SAP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
     kern<<<pl.p, kSwThreads, pl.smem, s>>>(pl.map, pl.dinv, pl.nch_max, pl.offs, pl.k, x, pl.xw, cols, pl.box_c,
-                                           pl.nbox, pl.tri, pl.kb);
+                                           pl.nbox, pl.tri, pl.kb, tip_rows);
     SAP_LAUNCHED();
 }
 
@@ -740,13 +782,15 @@ static bool try_ldgsts(const SweepPlan<T>& pl, T* x, cudaStream_t s) {
 }
 
 template <class T>
-void launch_block_solve(const SweepPlan<T>& pl, T* x, cudaStream_t s) {
+void launch_block_solve(const SweepPlan<T>& pl, T* x, cudaStream_t s, int tip_rows) {
     if (pl.p <= 0) return;
+    if ((pl.ul || tip_rows > 0) && !(pl.tma && pl.tr == 32 && !pl.subst && !pl.kb))
+        throw InvalidArgument("tip sweeps need the 32-row inverse-product TMA path");
     if (pl.tma) {
         if (pl.tr == 32)
-            pl.stages == 3 ? run_tma<T, 32, 3>(pl, x, s) : run_tma<T, 32, 2>(pl, x, s);
+            pl.stages == 3 ? run_tma<T, 32, 3>(pl, x, tip_rows, s) : run_tma<T, 32, 2>(pl, x, tip_rows, s);
         else
-            pl.stages == 3 ? run_tma<T, 16, 3>(pl, x, s) : run_tma<T, 16, 2>(pl, x, s);
+            pl.stages == 3 ? run_tma<T, 16, 3>(pl, x, tip_rows, s) : run_tma<T, 16, 2>(pl, x, tip_rows, s);
         return;
     }
     if (try_ldgsts<T, 4>(pl, x, s)) return;
@@ -754,8 +798,8 @@ void launch_block_solve(const SweepPlan<T>& pl, T* x, cudaStream_t s) {
     if (try_ldgsts<T, 2>(pl, x, s)) return;
     throw InvalidArgument("band solve: half-bandwidth too large for the shared-memory chunk ring");
 }
-template void launch_block_solve<double>(const SweepPlan<double>&, double*, cudaStream_t);
-template void launch_block_solve<float>(const SweepPlan<float>&, float*, cudaStream_t);
+template void launch_block_solve<double>(const SweepPlan<double>&, double*, cudaStream_t, int);
+template void launch_block_solve<float>(const SweepPlan<float>&, float*, cudaStream_t, int);
 
 // ---------------------------------------------------------------------------
 // SaP-C interface step (spike.hpp:323-347), split into wide GEMV kernels:
@@ -773,15 +817,16 @@ __device__ __forceinline__ T row_dot(const T* __restrict__ a, const T* __restric
     return acc;
 }
 
+// g: the first block solve's bottom rows of block t (g[e-w, e)); gt: its top rows of block t+1 (gt[e, e+w))
 template <class T>
-__global__ void k_iface_pre(const T* __restrict__ g, const int* __restrict__ offs, int w, const T* __restrict__ wt,
-                            T* __restrict__ xt) {
+__global__ void k_iface_pre(const T* __restrict__ g, const T* __restrict__ gt, const int* __restrict__ offs, int w,
+                            const T* __restrict__ wt, T* __restrict__ xt) {
     const int t = blockIdx.y, lane = threadIdx.x & 31;
     const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (i >= w) return;
     const int e = offs[t + 1];
     const T acc = row_dot(wt + ((size_t)t * w + i) * w, g + e - w, w, lane);
-    if (lane == 0) xt[(size_t)t * w + i] = g[e + i] - acc;
+    if (lane == 0) xt[(size_t)t * w + i] = gt[e + i] - acc;
 }
 
 template <class T>
@@ -818,11 +863,11 @@ __global__ void k_iface_post2(const int* __restrict__ offs, int w, const T* __re
 template <class T>
 void launch_interfaces(const T* g, const int* d_ioffs, const SweepPlan<T>& rplan, int ni, int k, const T* wt,
                        const T* vb, const T* bblk, const T* cblk, T* xt, T* xb, T* b2, bool skip_first_b,
-                       bool skip_last_c, cudaStream_t s) {
+                       bool skip_last_c, cudaStream_t s, const T* gtop) {
     if (ni < 1 || k == 0) return;
     const int w = k;
     dim3 grid(ceil_div(w, 8), ni);
-    k_iface_pre<T><<<grid, 256, 0, s>>>(g, d_ioffs, w, wt, xt);
+    k_iface_pre<T><<<grid, 256, 0, s>>>(g, gtop ? gtop : g, d_ioffs, w, wt, xt);
     SAP_LAUNCHED();
     launch_block_solve<T>(rplan, xt, s);
     k_iface_post1<T><<<dim3(grid.x, ni, 2), 256, 0, s>>>(g, d_ioffs, w, vb, bblk, xt, xb, b2, skip_first_b);
@@ -832,10 +877,10 @@ void launch_interfaces(const T* g, const int* d_ioffs, const SweepPlan<T>& rplan
 }
 template void launch_interfaces<double>(const double*, const int*, const SweepPlan<double>&, int, int, const double*,
                                         const double*, const double*, const double*, double*, double*, double*, bool,
-                                        bool, cudaStream_t);
+                                        bool, cudaStream_t, const double*);
 template void launch_interfaces<float>(const float*, const int*, const SweepPlan<float>&, int, int, const float*,
                                        const float*, const float*, const float*, float*, float*, float*, bool, bool,
-                                       cudaStream_t);
+                                       cudaStream_t, const float*);
 
 // ---------------------------------------------------------------------------
 // Diagonal preconditioner (build_precond_op's `diagonal` branch, pipeline.hpp:151-161).

@@ -136,6 +136,7 @@ struct SweepPlan {
     unsigned long long* kappa = nullptr;  // device: max chunk-triangle condition estimate (double bits)
     bool subst = false;         // sweeps solve chunk triangles by substitution (ill-conditioned triangles)
     const int* kb = nullptr;    // third stage: per-block half-bandwidth K_b <= k (device), nullptr = k
+    bool ul = false;            // f is a UL store (A = U'L'): bottom-up sweep first (k_sweep_tma<UL>)
     CUtensorMap map;
 };
 // Elements of chunk-inverse storage the plan needs (0 when the TMA path is not used).
@@ -147,8 +148,10 @@ void plan_sweeps(SweepPlan<T>& pl, T* dinv_storage);
 template <class T>
 void launch_chunk_inverses(const SweepPlan<T>& pl, cudaStream_t s);
 // x <- D^{-1} x per block with the LU factors (band_lu_solve, block_factors.hpp:74-90).
+// tip_rows > 0: the second sweep stops once the tip_rows rows it reaches first are final (LU: the last rows
+// of every block, UL: the first); the other rows of x are then intermediate values.
 template <class T>
-void launch_block_solve(const SweepPlan<T>& pl, T* x, cudaStream_t s);
+void launch_block_solve(const SweepPlan<T>& pl, T* x, cudaStream_t s, int tip_rows = 0);
 // SaP-C interface step (apply_preconditioner, spike.hpp:323-347): from g (= D^{-1} b) form
 // x^t (xt), x^b (xb) per interface and subtract the coupling terms from b2 (which holds b).
 // rbar_band: the reduced blocks' LU in band layout (k = w-1), blocks at d_roffsets (t*w).
@@ -158,7 +161,7 @@ template <class T>
 // neighbour owns (g then carries the neighbour's w rows as a halo on that side).
 void launch_interfaces(const T* g, const int* d_ioffs, const SweepPlan<T>& rplan, int ni, int k, const T* wt,
                        const T* vb, const T* bblk, const T* cblk, T* xt, T* xb, T* b2, bool skip_first_b,
-                       bool skip_last_c, cudaStream_t s);
+                       bool skip_last_c, cudaStream_t s, const T* gtop = nullptr);
 // f32: build_precond_op<float>'s diagonal (pipeline.hpp:151-161 at T = float): the diagonal and the boost
 // value rounded to float, the apply b / diag in float between casts (spike.hpp:304-351).
 void launch_diag_apply(const double* in, const double* diag, double* out, int n, cudaStream_t s, bool f32 = false);

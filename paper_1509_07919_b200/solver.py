@@ -132,7 +132,7 @@ class Solver:
 
     def __init__(self, p: int = 1, precond: PrecondKind = PrecondKind.coupled, boost_eps: float = 1e-10,
                  krylov: KrylovOptions | None = None, device: int = 0, triangle_solve: int = 0,
-                 lu_kernel: int = 0):
+                 lu_kernel: int = 0, tip_solve: int = 0):
         kr = krylov or KrylovOptions()
         o = L.sap_options()
         L.load().sap_options_default(C.byref(o))
@@ -142,6 +142,7 @@ class Solver:
         o.caller_asserts_spd, o.device = int(kr.caller_asserts_spd), int(device)
         o.triangle_solve = int(triangle_solve)  # 0 automatic, 1 chunk inverses, 2 substitution
         o.lu_kernel = int(lu_kernel)  # 0 automatic, 1 one CTA per job, 2 dataflow (bitwise-equal factors)
+        o.tip_solve = int(tip_solve)  # SaP-C first block solve: 0 automatic (LU + UL tip sweeps), 1 full LU solve
         self.options = o
         self._h = C.c_void_p()
         self._create()

@@ -48,7 +48,7 @@ def test_options_defaults_match_reference(sap):
     sap.load().sap_options_default(C.byref(o))
     assert (o.p, o.precond, o.boost_eps, o.method, o.ell) == (1, 0, 1e-10, 0, 2)
     assert (o.rel_tol, o.abs_tol, o.max_iterations, o.mixed_precision, o.caller_asserts_spd) == (1e-10, 0.0, 500, 0, 0)
-    assert (o.triangle_solve, o.lu_kernel) == (0, 0)  # implementation choices, automatic by default
+    assert (o.triangle_solve, o.lu_kernel, o.tip_solve) == (0, 0, 0)  # implementation choices, automatic by default
 
 
 def test_partition_layout_matches_reference(sap, oracle):

@@ -18,5 +18,9 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_s
    -o $O/${TAG}_sweep python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-config5 > $O/${TAG}_ncu_sweep.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_band_spmv' -s 2 -c 1 \
    -o $O/${TAG}_spmv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-config5 > $O/${TAG}_ncu_spmv.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_band_spmv2' -s 0 -c 1 \
+   -o $O/${TAG}_spmv2 python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-config5 > $O/${TAG}_ncu_spmv2.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $O/${TAG}_launches_D.csv \
+   python bench.py --precond D --steps 1 --warmup 1 --no-cpu-baseline --no-config5 > $O/${TAG}_ncu_launch_D.log 2>&1
 fi
 echo done

@@ -51,7 +51,7 @@ def main(tag):
     out_dir = os.path.join(ROOT, "profiles")
     lines = [f"# ncu summaries ({tag}): one launch each, --set full --clock-control none (cold caches, serialised)", ""]
     traffic = {}
-    for part in ("lu", "sweep", "spmv"):
+    for part in ("lu", "sweep", "spmv", "spmv2"):
         rep = os.path.join(ROOT, "gpurun_out", f"{tag}_{part}.ncu-rep")
         if not os.path.exists(rep):
             continue
@@ -71,6 +71,11 @@ def main(tag):
     if os.path.exists(lc):
         lines.append("## launch list (bench.py --steps 1 --warmup 1, SaP-C; gpu__time_duration per kernel)")
         lines.append(launches.summarise(lc))
+    ld = os.path.join(ROOT, "gpurun_out", f"{tag}_launches_D.csv")
+    if os.path.exists(ld):
+        lines.append("")
+        lines.append("## launch list (bench.py --precond D --steps 1 --warmup 1, SaP-D)")
+        lines.append(launches.summarise(ld))
     with open(os.path.join(out_dir, f"ncu_{tag}.txt"), "w") as f:
         f.write("\n".join(lines) + "\n")
     if "lu" in traffic:
