@@ -14,6 +14,13 @@
 
 namespace sapgpu {
 
+// Row sums over the union window [clo, chi] of a warp's 32 rows: the band slots of kSpB columns are loaded
+// (predicated on the band) before their FMAs, so a thread keeps several 8-byte loads in flight instead of one
+// (the conditional load-then-use loop compiled to one outstanding load; tools/probe/spmv2_probe.cu measured
+// 132 -> 118 us for one product at config 2, 195 -> 143 us for two). The FMAs still run in ascending column
+// order and skip the out-of-band slots, so every row's sum is bitwise the reference order's.
+constexpr int kSpB = 8;
+
 __global__ void __launch_bounds__(256)
     k_band_spmv(const double* __restrict__ a, int n, int k, const double* __restrict__ x, double* __restrict__ y,
                 const double* __restrict__ b) {
@@ -26,11 +33,22 @@ __global__ void __launch_bounds__(256)
         const int clo = max(r0 - k, 0), chi = min(r0 + 31 + k, n - 1);
         double acc = 0.0;
         const double* col = a + (long long)clo * ld + i + k;
-#pragma unroll 8
-        for (int j = clo; j <= chi; ++j, col += ld) {
-            const double xv = __ldg(x + j);
-            if (i < n && i - j <= k && j - i <= k) acc = fma(*col, xv, acc);
+        int j = clo;
+        for (; j + kSpB - 1 <= chi; j += kSpB, col += kSpB * ld) {
+            double av[kSpB];
+#pragma unroll
+            for (int u = 0; u < kSpB; ++u) {
+                const int jj = j + u;
+                av[u] = (i < n && i - jj <= k && jj - i <= k) ? __ldg(col + u * ld) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < kSpB; ++u) {
+                const int jj = j + u;
+                if (i < n && i - jj <= k && jj - i <= k) acc = fma(av[u], __ldg(x + jj), acc);
+            }
         }
+        for (; j <= chi; ++j, col += ld)
+            if (i < n && i - j <= k && j - i <= k) acc = fma(__ldg(col), __ldg(x + j), acc);
         if (i < n) y[i] = b ? b[i] - acc : acc;
     }
 }
@@ -57,15 +75,29 @@ __global__ void __launch_bounds__(256)
         const int clo = max(r0 - k, 0), chi = min(r0 + 31 + k, n - 1);
         double acc0 = 0.0, acc1 = 0.0;
         const double* col = a + (long long)clo * ld + i + k;
-#pragma unroll 8
-        for (int j = clo; j <= chi; ++j, col += ld) {
-            const double xv0 = __ldg(x0 + j), xv1 = __ldg(x1 + j);
-            if (i < n && i - j <= k && j - i <= k) {
-                const double av = *col;
-                acc0 = fma(av, xv0, acc0);
-                acc1 = fma(av, xv1, acc1);
+        int j = clo;
+        for (; j + kSpB - 1 <= chi; j += kSpB, col += kSpB * ld) {
+            double av[kSpB];
+#pragma unroll
+            for (int u = 0; u < kSpB; ++u) {
+                const int jj = j + u;
+                av[u] = (i < n && i - jj <= k && jj - i <= k) ? __ldg(col + u * ld) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < kSpB; ++u) {
+                const int jj = j + u;
+                if (i < n && i - jj <= k && jj - i <= k) {
+                    acc0 = fma(av[u], __ldg(x0 + jj), acc0);
+                    acc1 = fma(av[u], __ldg(x1 + jj), acc1);
+                }
             }
         }
+        for (; j <= chi; ++j, col += ld)
+            if (i < n && i - j <= k && j - i <= k) {
+                const double av = __ldg(col);
+                acc0 = fma(av, __ldg(x0 + j), acc0);
+                acc1 = fma(av, __ldg(x1 + j), acc1);
+            }
         if (i < n) {
             y0[i] = acc0;
             y1[i] = acc1;
@@ -93,11 +125,22 @@ __global__ void __launch_bounds__(256)
         const int clo = max(r0 - k, 0), chi = min(r0 + 31 + k, n - 1);
         double acc = 0.0;
         const double* col = a + (long long)clo * ld + i + k;
-#pragma unroll 8
-        for (int j = clo; j <= chi; ++j, col += ld) {
-            const double xv = __ldg(x + j);
-            if (i < rend && i - j <= k && j - i <= k) acc = fma(*col, xv, acc);
+        int j = clo;
+        for (; j + kSpB - 1 <= chi; j += kSpB, col += kSpB * ld) {
+            double av[kSpB];
+#pragma unroll
+            for (int u = 0; u < kSpB; ++u) {
+                const int jj = j + u;
+                av[u] = (i < rend && i - jj <= k && jj - i <= k) ? __ldg(col + u * ld) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < kSpB; ++u) {
+                const int jj = j + u;
+                if (i < rend && i - jj <= k && jj - i <= k) acc = fma(av[u], __ldg(x + jj), acc);
+            }
         }
+        for (; j <= chi; ++j, col += ld)
+            if (i < rend && i - j <= k && j - i <= k) acc = fma(__ldg(col), __ldg(x + j), acc);
         if (i < rend) y[i - rbeg] = acc;
     }
 }
