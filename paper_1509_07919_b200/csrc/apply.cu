@@ -116,7 +116,10 @@ __global__ void k_chunk_inverses(const T* __restrict__ f0, long long pstride, in
     }
     __syncthreads();
     const int dir = threadIdx.x >> 5, j = threadIdx.x & 31;
-    if (UL && j < TR) {
+    // UL: the top-down (lower) inverses are read only by the tip sweeps' stopped second sweep, i.e. for the
+    // chunks covering the first k rows; the others are not formed (half the kernel's work on the side stream)
+    const bool skip = UL && dir == 0 && q >= (k + TR - 1) / TR;
+    if (UL && j < TR && !skip) {
         if (dir == 0) {  // lower with diagonal
             for (int i = 0; i < TR; ++i) X[0][j][i] = T(0);
             X[0][j][j] = T(1) / blk[j][j];
@@ -133,7 +136,7 @@ __global__ void k_chunk_inverses(const T* __restrict__ f0, long long pstride, in
                 X[1][j][i] = -acc;
             }
         }
-    } else if (j < TR) {
+    } else if (!UL && j < TR) {
         if (dir == 0) {  // unit lower
             for (int i = 0; i < TR; ++i) X[0][j][i] = (i == j) ? T(1) : T(0);
             for (int i = j + 1; i < TR; ++i) {
@@ -172,7 +175,7 @@ __global__ void k_chunk_inverses(const T* __restrict__ f0, long long pstride, in
     {
         const int d = threadIdx.x >> 5, i = threadIdx.x & 31;
         double rt = 0.0, ri = 0.0;
-        if (i < TR)
+        if (i < TR && !skip)
             for (int jj = 0; jj < TR; ++jj) {
                 const T tv = UL ? (d == 0 ? (jj <= i ? blk[jj][i] : T(0)) : (jj > i ? blk[jj][i] : (jj == i ? T(1) : T(0))))
                                 : (d == 0 ? (jj < i ? blk[jj][i] : (jj == i ? T(1) : T(0))) : (jj >= i ? blk[jj][i] : T(0)));
