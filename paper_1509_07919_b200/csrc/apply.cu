@@ -105,14 +105,22 @@ __global__ void k_chunk_inverses(const T* __restrict__ f0, long long pstride, in
     const int rows = min(TR, m - i0);
     const T* f = f0 + (long long)b * pstride + pad;
     const long long ld = 2LL * k;
-    for (int idx = threadIdx.x; idx < TR * TR; idx += blockDim.x) {
+    // every thread's TR*TR/64 chunk entries are loaded before any is stored (the conditional load-then-store
+    // loop kept one global load in flight per thread: ~16 serial L2/HBM round trips per CTA)
+    constexpr int kPer = TR * TR / 64;
+    T v[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+        const int idx = threadIdx.x + u * 64;
         const int j = idx / TR, i = idx % TR;
-        T v;
-        if (i < rows && j < rows)
-            v = (i - j <= k && j - i <= k) ? f[(long long)(i0 + j) * ld + i0 + i + k] : T(0);
-        else
-            v = (i == j) ? T(1) : T(0);
-        blk[j][i] = v;
+        const bool in = i < rows && j < rows && i - j <= k && j - i <= k;
+        v[u] = in ? f[(long long)(i0 + j) * ld + i0 + i + k] : T(0);
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+        const int idx = threadIdx.x + u * 64;
+        const int j = idx / TR, i = idx % TR;
+        blk[j][i] = (i < rows && j < rows) ? v[u] : ((i == j) ? T(1) : T(0));
     }
     __syncthreads();
     const int dir = threadIdx.x >> 5, j = threadIdx.x & 31;
