@@ -17,30 +17,47 @@
 
 namespace sapgpu {
 
-__global__ void k_extract_coupling(const double* __restrict__ a, int n, int k, const int* __restrict__ offs,
-                                   double* __restrict__ bblk, double* __restrict__ cblk,
-                                   const int* __restrict__ wid) {
-    const int t = blockIdx.y;
+// One 32 x 32 tile of B_t and C_t per CTA, through shared memory: the band is read down its columns (for a fixed
+// corner column the corner rows are consecutive band slots) and the row-major corners are written along rows, so
+// both sides are coalesced (element-per-thread in corner order read the band at a 2K-double stride).
+__global__ void __launch_bounds__(256)
+    k_extract_coupling(const double* __restrict__ a, int n, int k, const int* __restrict__ offs,
+                       double* __restrict__ bblk, double* __restrict__ cblk, const int* __restrict__ wid) {
+    __shared__ double tb[32][33], tc[32][33];  // [corner column j][corner row r]
+    const int t = blockIdx.z;
     const int w = k;
     const int wt = wid ? wid[t] : k;  // third stage: the reference's width, embedded (third.cu)
     const int e = offs[t + 1];
     const long long ld = 2LL * k;
-    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < w * w; idx += gridDim.x * blockDim.x) {
-        const int r = idx / w, j = idx - r * w;
+    const int r0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int j = j0 + ty + 8 * q, r = r0 + tx;
         // B_t[r][j] = A(e-w+r, e+j); C_t[r][j] = A(e+r, e-w+j)  (zero outside the band)
         const int bi = e - w + r, bj = e + j, ci = e + r, cj = e - w + j;
-        const bool bin = bi >= 0 && bi < n && bj >= 0 && bj < n && bi - bj <= k && bj - bi <= k;
-        const bool cin = ci >= 0 && ci < n && cj >= 0 && cj < n && ci - cj <= k && cj - ci <= k;
+        const bool ok = r < w && j < w;
+        const bool bin = ok && bi >= 0 && bi < n && bj >= 0 && bj < n && bi - bj <= k && bj - bi <= k;
+        const bool cin = ok && ci >= 0 && ci < n && cj >= 0 && cj < n && ci - cj <= k && cj - ci <= k;
         const bool bw = r >= w - wt && j < wt, cw = r < wt && j >= w - wt;
-        bblk[(long long)t * w * w + idx] = bin && bw ? a[(long long)bj * ld + bi + k] : 0.0;
-        cblk[(long long)t * w * w + idx] = cin && cw ? a[(long long)cj * ld + ci + k] : 0.0;
+        tb[ty + 8 * q][tx] = bin && bw ? a[(long long)bj * ld + bi + k] : 0.0;
+        tc[ty + 8 * q][tx] = cin && cw ? a[(long long)cj * ld + ci + k] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int r = r0 + ty + 8 * q, j = j0 + tx;
+        if (r < w && j < w) {
+            bblk[(long long)t * w * w + (long long)r * w + j] = tb[tx][ty + 8 * q];
+            cblk[(long long)t * w * w + (long long)r * w + j] = tc[tx][ty + 8 * q];
+        }
     }
 }
 
 void launch_extract_coupling(const double* band, int n, int k, const int* d_offsets, int p, double* bblk,
                              double* cblk, cudaStream_t s, const int* d_wid) {
     if (p < 2 || k == 0) return;
-    dim3 grid(ceil_div((long long)k * k, 256), p - 1);
+    dim3 grid(ceil_div(k, 32), ceil_div(k, 32), p - 1);
     k_extract_coupling<<<grid, 256, 0, s>>>(band, n, k, d_offsets, bblk, cblk, d_wid);
     SAP_LAUNCHED();
 }
@@ -292,9 +309,22 @@ __global__ void __launch_bounds__(256, 3)
     double* X = sm;                  // [w][kTXld]
     double* S = sm + (size_t)w * kTXld;  // [32][kTSld]
     const TipCorner F{J.f, J.corner, 2LL * k, k};
-    for (int idx = threadIdx.x; idx < w * kTC; idx += blockDim.x) {
-        const int r = idx / kTC, c = idx - r * kTC;
-        X[r * kTXld + c] = c < nc ? J.rhs[(long long)r * w + c0 + c] : 0.0;
+    // the right-hand sides in batches of 8 loads per thread issued before their stores (a load-then-store
+    // loop keeps one global load in flight: ~25 serial round trips per CTA at w = 200)
+    for (int base = 0; base < w * kTC; base += 8 * 256) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int idx = base + threadIdx.x + 256 * u;
+            const int r = idx / kTC, c = idx - r * kTC;
+            v[u] = (idx < w * kTC && c < nc) ? J.rhs[(long long)r * w + c0 + c] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int idx = base + threadIdx.x + 256 * u;
+            const int r = idx / kTC, c = idx - r * kTC;
+            if (idx < w * kTC) X[r * kTXld + c] = v[u];
+        }
     }
     __syncthreads();
     if (J.which == 0) {
@@ -374,10 +404,19 @@ __global__ void __launch_bounds__(256) k_rbar_mma(const double* __restrict__ wt,
     const double* Bm = vb + (long long)t * w * w;
     double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
     for (int l0 = 0; l0 < w; l0 += 32) {
-        for (int idx = threadIdx.x; idx < 32 * 32; idx += 256) {
-            const int r = idx >> 5, c = idx & 31;
-            As[r * kRbLd + c] = (i0 + r < w && l0 + c < w) ? A[(long long)(i0 + r) * w + l0 + c] : 0.0;
-            Bs[r * kRbLd + c] = (l0 + r < w && j0 + c < w) ? Bm[(long long)(l0 + r) * w + j0 + c] : 0.0;
+        // all 8 of this thread's W / V entries in flight before the stores (one at a time before)
+        double av[4], bv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int idx = threadIdx.x + 256 * u, r = idx >> 5, c = idx & 31;
+            av[u] = (i0 + r < w && l0 + c < w) ? A[(long long)(i0 + r) * w + l0 + c] : 0.0;
+            bv[u] = (l0 + r < w && j0 + c < w) ? Bm[(long long)(l0 + r) * w + j0 + c] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int idx = threadIdx.x + 256 * u, r = idx >> 5, c = idx & 31;
+            As[r * kRbLd + c] = av[u];
+            Bs[r * kRbLd + c] = bv[u];
         }
         __syncthreads();
 #pragma unroll
