@@ -822,7 +822,30 @@ template void launch_block_solve<float>(const SweepPlan<float>&, float*, cudaStr
 template <class T>
 __device__ __forceinline__ T row_dot(const T* __restrict__ a, const T* __restrict__ v, int w, int lane) {
     T acc = T(0);
-    for (int j = lane; j < w; j += 32) acc = fma(a[j], v[j], acc);
+    int j0 = 0;
+    // a lane's terms 8 at a time, all loads in flight before the (same-order) FMA chain
+    for (; j0 + 8 * 32 <= w; j0 += 8 * 32) {
+        T av[8], vv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            av[u] = a[j0 + lane + 32 * u];
+            vv[u] = v[j0 + lane + 32 * u];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = fma(av[u], vv[u], acc);
+    }
+    {
+        T av[8], vv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int j = j0 + lane + 32 * u;
+            av[u] = j < w ? a[j] : T(0);
+            vv[u] = j < w ? v[j] : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (j0 + lane + 32 * u < w) acc = fma(av[u], vv[u], acc);
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     return acc;

@@ -14,8 +14,10 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
    python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-config5 > $O/${TAG}_ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_band_lu_(res|df)' -s 0 -c 1 \
    -o $O/${TAG}_lu python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-config5 > $O/${TAG}_ncu_lu.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_band_lu_(res|df)' -s 0 -c 1 \
+   -o $O/${TAG}_luD python bench.py --precond D --steps 1 --warmup 1 --no-cpu-baseline --no-config5 > $O/${TAG}_ncu_luD.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_sweep' -s 0 -c 1 \
-   -o $O/${TAG}_sweep python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-config5 > $O/${TAG}_ncu_sweep.log 2>&1
+   -o $O/${TAG}_sweep python bench.py --precond D --steps 1 --warmup 1 --no-cpu-baseline --no-config5 > $O/${TAG}_ncu_sweep.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_band_spmv' -s 2 -c 1 \
    -o $O/${TAG}_spmv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-config5 > $O/${TAG}_ncu_spmv.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_band_spmv2' -s 0 -c 1 \

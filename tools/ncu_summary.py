@@ -51,7 +51,7 @@ def main(tag):
     out_dir = os.path.join(ROOT, "profiles")
     lines = [f"# ncu summaries ({tag}): one launch each, --set full --clock-control none (cold caches, serialised)", ""]
     traffic = {}
-    for part in ("lu", "sweep", "spmv", "spmv2"):
+    for part in ("lu", "luD", "sweep", "spmv", "spmv2"):
         rep = os.path.join(ROOT, "gpurun_out", f"{tag}_{part}.ncu-rep")
         if not os.path.exists(rep):
             continue
@@ -80,8 +80,9 @@ def main(tag):
         f.write("\n".join(lines) + "\n")
     if "lu" in traffic:
         with open(os.path.join(out_dir, "ncu_lu_traffic.json"), "w") as f:
-            json.dump({"SaP-C": traffic["lu"], "source": f"profiles/ncu_{tag}.txt (dram__bytes_read.sum + "
-                       "dram__bytes_write.sum of one band LU launch (k_band_lu_df), LU+UL of config 2)",
+            json.dump({"SaP-C": traffic["lu"], "SaP-D": traffic.get("luD"),
+                       "source": f"profiles/ncu_{tag}.txt (dram__bytes_read.sum + dram__bytes_write.sum of one "
+                       "band LU launch (k_band_lu_df) of config 2: LU+UL for SaP-C (lu), LU for SaP-D (luD))",
                        "sweep": traffic.get("sweep"), "spmv": traffic.get("spmv")}, f, indent=1)
     print("\n".join(lines))
 
