@@ -195,6 +195,11 @@ struct DotBatch {  // up to kMaxDots dot products in one pass (kind 1: squared n
     const double* b[kMaxDots];
     int kind[kMaxDots];
     int m;
+    // optional: the results also written to host-mapped memory, and *flag_dst = *flag_src, by the kernel itself
+    // (the host reads them after its stream synchronisation with no device->host copy on the stream)
+    double* hout;
+    const int* flag_src;
+    int* flag_dst;
 };
 void launch_dots(const DotBatch& d, int n, double* partials, unsigned* counter, double* out, cudaStream_t s);
 void launch_axpy_quot(double* y, const double* num, const double* den, const double* x, int n, cudaStream_t s);

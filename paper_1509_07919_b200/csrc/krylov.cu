@@ -113,8 +113,14 @@ void KrylovSolver::ensure(int n, int ell) {
         SAP_CUDA(cudaMemset(counter_, 0, sizeof(unsigned)));
     }
     if (!dflag_) SAP_CUDA(cudaMalloc(&dflag_, sizeof(int)));
-    if (!hpinned_) SAP_CUDA(cudaMallocHost(&hpinned_, sizeof(double) * kScal));
-    if (!hflag_) SAP_CUDA(cudaMallocHost(&hflag_, sizeof(int)));
+    if (!hpinned_) {
+        SAP_CUDA(cudaHostAlloc(&hpinned_, sizeof(double) * kScal, cudaHostAllocMapped));
+        SAP_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dhpinned_), hpinned_, 0));
+    }
+    if (!hflag_) {
+        SAP_CUDA(cudaHostAlloc(&hflag_, sizeof(int), cudaHostAllocMapped));
+        SAP_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dhflag_), hflag_, 0));
+    }
     r_.assign(ell + 1, nullptr);
     u_.assign(ell + 1, nullptr);
     for (int i = 0; i <= ell; ++i) {
@@ -136,6 +142,7 @@ void KrylovSolver::sync_host() {
 }
 
 double KrylovSolver::dot(const double* a, const double* b) {
+    if (!dreduce_) return dots({DotReq{a, b, 0}})[0];  // k_dots with one pair is bitwise k_dot
     launch_dot(a, b, n_, partials_, counter_, dscal_, s_);
     if (dreduce_) dreduce_(dscal_, 1, s_);
     SAP_CUDA(cudaMemcpyAsync(hpinned_, dscal_, sizeof(double), cudaMemcpyDeviceToHost, s_));
@@ -149,6 +156,9 @@ double KrylovSolver::dot(const double* a, const double* b) {
 // along when flag_too is set.
 std::vector<double> KrylovSolver::dots(const std::vector<DotReq>& rq, bool flag_too) {
     const int m = (int)rq.size();
+    // single batch, no device-side reduction over ranks: the kernel writes the values (and the x-update flag)
+    // straight into the mapped host buffers -- no device->host copies between it and the synchronisation
+    const bool direct = !dreduce_ && m <= kMaxDots;
     for (int q0 = 0; q0 < m; q0 += kMaxDots) {
         DotBatch d{};
         d.m = std::min(kMaxDots, m - q0);
@@ -157,11 +167,20 @@ std::vector<double> KrylovSolver::dots(const std::vector<DotReq>& rq, bool flag_
             d.b[q] = rq[q0 + q].b;
             d.kind[q] = rq[q0 + q].kind;
         }
+        if (direct) {
+            d.hout = dhpinned_;
+            if (flag_too) {
+                d.flag_src = dflag_;
+                d.flag_dst = dhflag_;
+            }
+        }
         launch_dots(d, n_, partials_, counter_, dscal_ + q0, s_);
     }
-    if (dreduce_) dreduce_(dscal_, m, s_);
-    SAP_CUDA(cudaMemcpyAsync(hpinned_, dscal_, sizeof(double) * m, cudaMemcpyDeviceToHost, s_));
-    if (flag_too) SAP_CUDA(cudaMemcpyAsync(hflag_, dflag_, sizeof(int), cudaMemcpyDeviceToHost, s_));
+    if (!direct) {
+        if (dreduce_) dreduce_(dscal_, m, s_);
+        SAP_CUDA(cudaMemcpyAsync(hpinned_, dscal_, sizeof(double) * m, cudaMemcpyDeviceToHost, s_));
+        if (flag_too) SAP_CUDA(cudaMemcpyAsync(hflag_, dflag_, sizeof(int), cudaMemcpyDeviceToHost, s_));
+    }
     sync_host();
     if (reduce_ && !dreduce_) reduce_(hpinned_, m);
     return std::vector<double>(hpinned_, hpinned_ + m);

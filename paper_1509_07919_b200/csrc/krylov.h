@@ -82,8 +82,10 @@ private:
     double* dscal_ = nullptr;     // device scalar outputs
     unsigned* counter_ = nullptr;
     int* dflag_ = nullptr;
-    double* hpinned_ = nullptr;   // pinned host scalar
+    double* hpinned_ = nullptr;   // pinned host scalars (mapped: k_dots writes its results here directly)
     int* hflag_ = nullptr;
+    double* dhpinned_ = nullptr;  // their device aliases
+    int* dhflag_ = nullptr;
     std::vector<double*> r_, u_;
     double *tmp_ = nullptr, *rtilde_ = nullptr, *scratch_ = nullptr, *xc_ = nullptr, *noise_ = nullptr;
 };

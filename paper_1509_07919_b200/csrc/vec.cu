@@ -143,7 +143,11 @@ __global__ void __launch_bounds__(kRedThreads)
     if (last) {
         __threadfence();
         const double tot = sum_partials(partials, gridDim.x, d.m, threadIdx.x);
-        if (threadIdx.x < d.m) out[threadIdx.x] = tot;
+        if (threadIdx.x < d.m) {
+            out[threadIdx.x] = tot;
+            if (d.hout) d.hout[threadIdx.x] = tot;
+        }
+        if (threadIdx.x == 0 && d.flag_dst) *d.flag_dst = __ldcg(d.flag_src);
         __syncthreads();
         if (threadIdx.x == 0) *counter = 0u;
     }
