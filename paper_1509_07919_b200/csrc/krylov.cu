@@ -223,20 +223,7 @@ KrylovResult KrylovSolver::bicgstab(const DeviceOp& A, const DeviceOp& M, const 
     const int G = vgrid(n);
     KrylovResult st;
     SAP_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * (size_t)n, s_));
-    const double bnorm = std::sqrt(dot(b, b));
-    if (bnorm == 0.0) {
-        st.converged = true;
-        st.residual_history.push_back(0.0);
-        return st;
-    }
-    const double thr = cfg.rel_tol * bnorm + cfg.abs_tol;
-    double tr = bnorm;
-    st.residual_history.push_back(tr / bnorm);
-    st.final_relative_residual = tr / bnorm;
-    if (tr <= thr) {
-        st.converged = true;
-        return st;
-    }
+    double bnorm = 0.0, thr = 0.0, tr = 0.0;  // ||b||, the stopping threshold, the true residual norm
     auto record = [&](int sweep, int step, double res) {
         const long steps = (long)sweep * 2 * ell + step;
         const long quarters = (4 * steps + 2 * ell - 1) / (2 * ell);
@@ -297,7 +284,35 @@ KrylovResult KrylovSolver::bicgstab(const DeviceOp& A, const DeviceOp& M, const 
         SAP_CUDA(cudaMemsetAsync(u_[0], 0, sizeof(double) * (size_t)n, s_));
     };
 
-    reset_iteration_state(false);
+    // ||b|| and the early exits (krylov.hpp:118-133). With the exact zero-guess shortcut the first
+    // preconditioned residual r0 = M b does not depend on ||b||: it is enqueued first and rho1 = (r0, r~) (r~ = r0)
+    // rides with (b, b) in the same synchronisation (both values bitwise the separate dots'); if the solve
+    // ends at ||b|| the speculative M b is simply not used.
+    const bool spec = x_is_zero && cfg.zero_guess_exact;
+    if (spec) reset_iteration_state(false);
+    {
+        const std::vector<double> v =
+            spec ? dots({DotReq{b, b, 0}, DotReq{r_[0], rtilde_, 0}}) : std::vector<double>{dot(b, b)};
+        bnorm = std::sqrt(v[0]);
+        if (bnorm == 0.0) {
+            st.converged = true;
+            st.residual_history.push_back(0.0);
+            return st;
+        }
+        thr = cfg.rel_tol * bnorm + cfg.abs_tol;
+        tr = bnorm;
+        st.residual_history.push_back(tr / bnorm);
+        st.final_relative_residual = tr / bnorm;
+        if (tr <= thr) {
+            st.converged = true;
+            return st;
+        }
+        if (spec) {
+            rho_next = v[1];
+            have_rho = true;
+        }
+    }
+    if (!spec) reset_iteration_state(false);
     x_is_zero = false;  // the restart (reset_iteration_state(true)) always applies A to the current x
     double rho0 = 1.0, alpha = 0.0, omega = 1.0;
     bool restarted = false, breakdown = false;
