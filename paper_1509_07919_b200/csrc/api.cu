@@ -1938,7 +1938,7 @@ sap_status sap_solve(sap_handle* h, const double* b, double* x, int on_device, s
         DeviceOp M = [h](const double* in, double* out) {
             if (h->ready)
                 apply_m(h, in, out);
-            else
+            else if (out != in)
                 SAP_CUDA(cudaMemcpyAsync(out, in, sizeof(double) * (size_t)op_n(h), cudaMemcpyDeviceToDevice,
                                          h->stream));
         };

@@ -237,9 +237,10 @@ KrylovResult KrylovSolver::bicgstab(const DeviceOp& A, const DeviceOp& M, const 
         vs.p[i] = r_[i];
         vs.p[kMaxEll + 1 + i] = u_[i];
     }
+    // A then M in place on the output (M's apply may alias: no copy of A's result into M's output first)
     auto apply_hat = [&](const double* in, double* out) {
-        A(in, tmp_);
-        M(tmp_, out);
+        A(in, out);
+        M(out, out);
     };
     // true_residual (krylov.hpp:62-72): ||b - A x|| -- A x into scratch, then the residual's squared norm in
     // the same one-sync reduction as the dot products the next step needs (each value bitwise the separate
@@ -348,8 +349,8 @@ KrylovResult KrylovSolver::bicgstab(const DeviceOp& A, const DeviceOp& M, const 
                 SAP_CUDA(cudaMemsetAsync(dflag_, 0, sizeof(int), s_));
                 k_axpy_check<<<G, 256, 0, s_>>>(x, alpha, u_[0], n, dflag_);
                 SAP_LAUNCHED();
-                A2(r_[j], tmp_, x, scratch_);
-                M(tmp_, r_[j + 1]);
+                A2(r_[j], r_[j + 1], x, scratch_);
+                M(r_[j + 1], r_[j + 1]);
             } else {
                 apply_hat(r_[j], r_[j + 1]);
                 SAP_CUDA(cudaMemsetAsync(dflag_, 0, sizeof(int), s_));
