@@ -386,24 +386,24 @@ void apply_m(sap_handle* h, const double* in, double* out) {
         return;
     }
     double* g = h->scratch_g.get();
-    SAP_CUDA(cudaMemcpyAsync(g, in, bytes, cudaMemcpyDeviceToDevice, s));
     if (h->ul_tips) {
         // the interfaces read g's last w rows of every block (LU sweeps, the backward one stopped there) and
-        // its first w rows (UL sweeps on tside, the top-down one stopped there), computed side by side
+        // its first w rows (UL sweeps on tside, the top-down one stopped there), computed side by side; both
+        // read `in` and write their own copies
         double* gu = h->scratch_gu.get();
-        SAP_CUDA(cudaMemcpyAsync(gu, in, bytes, cudaMemcpyDeviceToDevice, s));
         SAP_CUDA(cudaEventRecord(h->tev[0], s));
         SAP_CUDA(cudaStreamWaitEvent(h->tside, h->tev[0], 0));
-        launch_block_solve<double>(h->uplan, gu, h->tside, k);
-        SAP_CUDA(cudaEventRecord(h->tev[1], h->tside));
+        launch_block_solve<double>(h->uplan, gu, h->tside, k, in);
         if (out != in) SAP_CUDA(cudaMemcpyAsync(out, in, bytes, cudaMemcpyDeviceToDevice, s));
-        launch_block_solve<double>(h->lplan, g, s, k);
+        launch_block_solve<double>(h->lplan, g, s, k, in);
+        SAP_CUDA(cudaEventRecord(h->tev[1], h->tside));
         SAP_CUDA(cudaStreamWaitEvent(s, h->tev[1], 0));
         launch_interfaces<double>(g, h->d_offsets.get(), h->rplan, p - 1, k, h->wt.get(), h->vb.get(),
                                   h->bblk.get(), h->cblk.get(), h->xt.get(), h->xb.get(), out, false, false, s, gu);
         launch_block_solve<double>(h->lplan, out, s);
         return;
     }
+    SAP_CUDA(cudaMemcpyAsync(g, in, bytes, cudaMemcpyDeviceToDevice, s));
     if (out != in) SAP_CUDA(cudaMemcpyAsync(out, in, bytes, cudaMemcpyDeviceToDevice, s));
     launch_block_solve<double>(h->lplan, g, s);
     launch_interfaces<double>(g, h->d_offsets.get(), h->rplan, p - 1, k, h->wt.get(), h->vb.get(), h->bblk.get(),

@@ -306,7 +306,8 @@ template <class T, int TR, int S, bool SUBST, bool UL>
 __global__ void __launch_bounds__(kSwThreads, 1)
     k_sweep_tma(const __grid_constant__ CUtensorMap map, const T* __restrict__ dinv, int nch_max,
                 const int* __restrict__ offs, int k, T* __restrict__ xbase, int xw, int slab_cols, int box_c,
-                int nbox, const T* __restrict__ tri, const int* __restrict__ kbs, int tip_rows) {
+                int nbox, const T* __restrict__ tri, const int* __restrict__ kbs, int tip_rows,
+                const T* __restrict__ xsrc) {
     constexpr int SD = SweepSmem<T, TR, S>::SD;
     constexpr int CG = 32 / TR;  // column groups per warp
     constexpr int PF = 6;        // L2 prefetch distance (chunks)
@@ -327,6 +328,8 @@ __global__ void __launch_bounds__(kSwThreads, 1)
     const int qf0 = (k - kb) / box_c;          // forward: first box reaching a column in [k - kb, k)
     const int qb1 = (kb + box_c - 1) / box_c;  // backward: boxes covering columns [0, kb)
     T* x = xbase + off;
+    // xsrc: the right-hand side when it is not x itself (the first sweep reads it, every sweep writes x)
+    const T* x1 = xsrc ? xsrc + off : x;
     const int xm = xw - 1;
     const int nch = (m + TR - 1) / TR;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -396,7 +399,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
         if (warp == 0) {
             const int ch0 = fwd ? 0 : nch - 1;
             const int in = ch0 * TR + lane;
-            yprev = (lane < TR && in < m) ? x[in] : T(0);
+            yprev = (lane < TR && in < m) ? (dir == 0 ? x1 : x)[in] : T(0);
         }
         int prev_rows = 0;
 #ifdef SAP_SWEEP_TRACE
@@ -491,7 +494,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
                 }
                 if (t < nl) {  // y of chunk ch, finished in the next iteration
                     const int in = i0 + lane;
-                    yprev = (lane < TR && in < m) ? x[in] : T(0);
+                    yprev = (lane < TR && in < m) ? (dir == 0 ? x1 : x)[in] : T(0);
                     prev_rows = min(TR, m - i0);
                 }
             } else if (t < nl && warp < kSwWarps - 1) {
@@ -771,13 +774,13 @@ template void launch_chunk_inverses<double>(const SweepPlan<double>&, cudaStream
 template void launch_chunk_inverses<float>(const SweepPlan<float>&, cudaStream_t);
 
 template <class T, int TR, int S>
-static void run_tma(const SweepPlan<T>& pl, T* x, int tip_rows, cudaStream_t s) {
+static void run_tma(const SweepPlan<T>& pl, T* x, int tip_rows, const T* xsrc, cudaStream_t s) {
     const int cols = pl.box_c * pl.nbox;
     auto kern = pl.ul ? k_sweep_tma<T, TR, S, false, true>
                       : (pl.subst ? k_sweep_tma<T, TR, S, true, false> : k_sweep_tma<T, TR, S, false, false>);
     SAP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
     kern<<<pl.p, kSwThreads, pl.smem, s>>>(pl.map, pl.dinv, pl.nch_max, pl.offs, pl.k, x, pl.xw, cols, pl.box_c,
-                                           pl.nbox, pl.tri, pl.kb, tip_rows);
+                                           pl.nbox, pl.tri, pl.kb, tip_rows, xsrc);
     SAP_LAUNCHED();
 }
 
@@ -793,15 +796,16 @@ static bool try_ldgsts(const SweepPlan<T>& pl, T* x, cudaStream_t s) {
 }
 
 template <class T>
-void launch_block_solve(const SweepPlan<T>& pl, T* x, cudaStream_t s, int tip_rows) {
+void launch_block_solve(const SweepPlan<T>& pl, T* x, cudaStream_t s, int tip_rows, const T* xsrc) {
     if (pl.p <= 0) return;
+    if (xsrc && !pl.tma) throw InvalidArgument("out-of-place band solve needs the TMA sweep");  // fallback: in place
     if ((pl.ul || tip_rows > 0) && !(pl.tma && pl.tr == 32 && !pl.subst && !pl.kb))
         throw InvalidArgument("tip sweeps need the 32-row inverse-product TMA path");
     if (pl.tma) {
         if (pl.tr == 32)
-            pl.stages == 3 ? run_tma<T, 32, 3>(pl, x, tip_rows, s) : run_tma<T, 32, 2>(pl, x, tip_rows, s);
+            pl.stages == 3 ? run_tma<T, 32, 3>(pl, x, tip_rows, xsrc, s) : run_tma<T, 32, 2>(pl, x, tip_rows, xsrc, s);
         else
-            pl.stages == 3 ? run_tma<T, 16, 3>(pl, x, tip_rows, s) : run_tma<T, 16, 2>(pl, x, tip_rows, s);
+            pl.stages == 3 ? run_tma<T, 16, 3>(pl, x, tip_rows, xsrc, s) : run_tma<T, 16, 2>(pl, x, tip_rows, xsrc, s);
         return;
     }
     if (try_ldgsts<T, 4>(pl, x, s)) return;
@@ -809,8 +813,8 @@ void launch_block_solve(const SweepPlan<T>& pl, T* x, cudaStream_t s, int tip_ro
     if (try_ldgsts<T, 2>(pl, x, s)) return;
     throw InvalidArgument("band solve: half-bandwidth too large for the shared-memory chunk ring");
 }
-template void launch_block_solve<double>(const SweepPlan<double>&, double*, cudaStream_t, int);
-template void launch_block_solve<float>(const SweepPlan<float>&, float*, cudaStream_t, int);
+template void launch_block_solve<double>(const SweepPlan<double>&, double*, cudaStream_t, int, const double*);
+template void launch_block_solve<float>(const SweepPlan<float>&, float*, cudaStream_t, int, const float*);
 
 // ---------------------------------------------------------------------------
 // SaP-C interface step (spike.hpp:323-347), split into wide GEMV kernels:

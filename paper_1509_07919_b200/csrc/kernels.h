@@ -150,8 +150,9 @@ void launch_chunk_inverses(const SweepPlan<T>& pl, cudaStream_t s);
 // x <- D^{-1} x per block with the LU factors (band_lu_solve, block_factors.hpp:74-90).
 // tip_rows > 0: the second sweep stops once the tip_rows rows it reaches first are final (LU: the last rows
 // of every block, UL: the first); the other rows of x are then intermediate values.
+// xsrc != nullptr: the right-hand side is read from xsrc (not modified) and the solution written to x.
 template <class T>
-void launch_block_solve(const SweepPlan<T>& pl, T* x, cudaStream_t s, int tip_rows = 0);
+void launch_block_solve(const SweepPlan<T>& pl, T* x, cudaStream_t s, int tip_rows = 0, const T* xsrc = nullptr);
 // SaP-C interface step (apply_preconditioner, spike.hpp:323-347): from g (= D^{-1} b) form
 // x^t (xt), x^b (xb) per interface and subtract the coupling terms from b2 (which holds b).
 // rbar_band: the reduced blocks' LU in band layout (k = w-1), blocks at d_roffsets (t*w).
