@@ -37,6 +37,18 @@ __global__ void k_r_update(VecSet v, int j, double alpha, int n) {
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
         for (int i = 0; i <= j; ++i) v.p[i][t] = fma(-alpha, v.p[kMaxEll + 2 + i][t], v.p[i][t]);
 }
+// k_r_update and then x += alpha * u[0] (flag if x becomes non-finite) in one pass: the x update reads neither
+// r[0..j] nor r[j+1], so BiCGStab's step runs both before A r_j (each element's operations unchanged)
+__global__ void k_r_update_x(VecSet v, int j, double alpha, double* __restrict__ x, int n, int* flag) {
+    int bad = 0;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        for (int i = 0; i <= j; ++i) v.p[i][t] = fma(-alpha, v.p[kMaxEll + 2 + i][t], v.p[i][t]);
+        const double xv = fma(alpha, v.p[kMaxEll + 1][t], x[t]);
+        x[t] = xv;
+        if (!isfinite(xv)) bad = 1;
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
 // y += a * x, flag if y becomes non-finite
 __global__ void k_axpy_check(double* __restrict__ y, double a, const double* __restrict__ x, int n, int* flag) {
     int bad = 0;
@@ -341,17 +353,17 @@ KrylovResult KrylovSolver::bicgstab(const DeviceOp& A, const DeviceOp& M, const 
             if (!std::isfinite(g)) { st.failure = 3; return st; }
             if (g == 0.0) { breakdown = true; break; }
             alpha = rho0 / g;
-            k_r_update<<<G, 256, 0, s_>>>(vs, j, alpha, n);
-            SAP_LAUNCHED();
             if (A2) {
-                // x += alpha u_0 does not read r_j or r_{j+1}: update x first, then A r_j and the true
+                // x += alpha u_0 does not read r_j or r_{j+1}: update x with r, then A r_j and the true
                 // residual's A x in one pass over the operator (each product bitwise its own A call)
                 SAP_CUDA(cudaMemsetAsync(dflag_, 0, sizeof(int), s_));
-                k_axpy_check<<<G, 256, 0, s_>>>(x, alpha, u_[0], n, dflag_);
+                k_r_update_x<<<G, 256, 0, s_>>>(vs, j, alpha, x, n, dflag_);
                 SAP_LAUNCHED();
                 A2(r_[j], r_[j + 1], x, scratch_);
                 M(r_[j + 1], r_[j + 1]);
             } else {
+                k_r_update<<<G, 256, 0, s_>>>(vs, j, alpha, n);
+                SAP_LAUNCHED();
                 apply_hat(r_[j], r_[j + 1]);
                 SAP_CUDA(cudaMemsetAsync(dflag_, 0, sizeof(int), s_));
                 k_axpy_check<<<G, 256, 0, s_>>>(x, alpha, u_[0], n, dflag_);
