@@ -2027,13 +2027,16 @@ __global__ void __launch_bounds__(NT, DfCfg<NT>::MINB) k_band_lu_df(DfArgs A) {
         // Job owners when every CTA of the launch is resident and there is a chain CTA per job: chain CTA r runs
         // chain(r, 0), chain(r, 1), ... and keeps each panel in shared memory for the next step. Deadlock-free like
         // the queue (each job's items run in order on a resident CTA; the workers' queue is unchanged). Otherwise
-        // (a CTA still waiting for a slot after 20 us, or fewer chain CTAs than jobs) the shared queue.
+        // (a CTA still waiting for a slot after 200 us, or fewer chain CTAs than jobs) the shared queue. The wait
+        // covers the side stream's block norms / zero padding, launched just ahead of a resident-band LU: their
+        // short CTAs hold some SMs for a few tens of us, and a 20 us limit sent ~1 launch in 20 to the queue
+        // (LU+UL 4.1 -> 6.9 ms in that step); the loop exits as soon as every CTA has started.
         if (tid < 32) {
             int md = ld_relaxed_w(A.mode);
             if (md == 0) {
                 const unsigned long long t0 = __shfl_sync(0xffffffffu, df_now(), 0);
                 while (ld_relaxed_w(A.started) < (int)gridDim.x &&
-                       __shfl_sync(0xffffffffu, df_now(), 0) - t0 < 20000)
+                       __shfl_sync(0xffffffffu, df_now(), 0) - t0 < 200000)
                     __nanosleep(64);
                 const int want =
                     A.owners_ok && ld_relaxed_w(A.started) == (int)gridDim.x && ld_relaxed_w(A.n_chain) >= J ? 1 : 2;
